@@ -1,0 +1,46 @@
+# Builds the product library in-tree (travels to the GPU box with the snapshot) and
+# the test-only oracle libraries (oracle/Makefile).
+#   paper_2508_08438_b200/libsafekv_b200.so   C ABI of include/safekv_b200.h (sm_100a)
+NVCC     ?= /usr/local/cuda/bin/nvcc
+JSON_INC ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2508_08438_b200
+SRC      := $(PKG)/csrc
+LIB      := $(PKG)/libsafekv_b200.so
+BUILD    := build
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -I/usr/local/cuda/include -I$(JSON_INC)
+
+OBJS := $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o
+
+all: $(LIB) oracle
+
+$(BUILD):
+	mkdir -p $(BUILD)
+
+$(BUILD)/kernels.o: $(SRC)/kernels.cu $(SRC)/ctx.hpp include/safekv_b200.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; exit 1)
+
+$(BUILD)/capi.o: $(SRC)/capi.cpp $(SRC)/ctx.hpp $(SRC)/rules.hpp include/safekv_b200.h | $(BUILD)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/rules.o: $(SRC)/rules.cpp $(SRC)/rules.hpp | $(BUILD)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/workload.o: $(SRC)/workload.cpp include/safekv_b200.h | $(BUILD)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lpthread -ldl -lrt
+
+oracle:
+	$(MAKE) -C oracle oracle
+	@if [ -d /root/reference/proj/include ]; then $(MAKE) -C oracle ref; fi
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(BUILD)/libsafekv_b200.sass
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+
+.PHONY: all oracle sass clean

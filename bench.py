@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""SafeKV admission hot-path benchmark (BASELINE.json metric: KV blocks admitted/s through
+hash + scan + lookup + monitor, and % of HBM roofline).
+
+Default workload = BASELINE.json configs[1] ("config 2"): 65,536 prompts x 2,048 tokens,
+16-token blocks, 64 users, every prompt = one of 256 shared 640-token pool prefixes
+(pre-inserted, ~31% inter-user reuse) + a unique filler body with ~1 PII phrase per KiB;
+window W = 32 right-context tokens.  One step = one fresh batch through admit (hash,
+rule-DFA scan, chained keys, index probe, monitor record) + commit + monitor epoch.
+Every step uses a distinct pre-generated batch (512 MiB of tokens > 126 MB L2, so no
+L2 flush is needed between steps).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  For N > 1 (torchrun) every rank admits its own shard
+of the prompt stream against its own index replica (weak scaling; see DESIGN.md
+"Multi-GPU" -- the replica merge is not part of this round's timed step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG2 = dict(n_prompts=65536, prompt_tokens=2048, block_tokens=16, window_tokens=32, n_users=64,
+            pool_size=256, pool_tokens=640, pii_per_kib=1.0, seed=1)
+METRIC = "KV blocks admitted/sec (hash+scan+lookup+monitor) and % HBM roofline, 1/2/4/8 B200"
+UNIT = "blocks/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int, verbose=False):
+    """Reference CPU implementation of the path (oracle/_ref: the unmodified reference
+    headers driven by the Appendix-A contract): std::regex Tier-1 scan on a thread pool,
+    RadixCacheIndex / EntropyMonitor single-threaded behind their mutex."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from refh import RefEngine, RefRules, load_ref
+    from paper_2508_08438_b200 import GenSpec, generate, generate_pool
+    L = load_ref()
+    if L is None:
+        return None
+    c = CFG2
+    spec = GenSpec(n_prompts=sample_prompts, prompt_tokens=c["prompt_tokens"], n_users=c["n_users"],
+                   pool_size=c["pool_size"], pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"],
+                   seed=c["seed"])
+    eng = RefEngine(L, RefRules(L), B=c["block_tokens"], W=c["window_tokens"], threads=threads)
+    pool = generate_pool(spec)
+    eng.admit(*pool)
+    eng.commit()
+    eng.epoch()
+    times, blocks = [], 0
+    for k in range(warmup + steps):
+        spec.prompt_id_base = (k + 1) * 10_000_000
+        batch = generate(spec)
+        t0 = time.perf_counter()
+        o = eng.admit(*batch)
+        eng.commit()
+        eng.epoch()
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            blocks += len(o["block_h"])
+    eng.close()
+    tot = sum(times)
+    return {"value": blocks / tot, "seconds": tot, "blocks": blocks, "steps": steps}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample
+    r = cpu_reference_run(args.steps, args.warmup, sample, threads)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsafekv_ref.so not built"}))
+        return
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/u64 integer; f64 entropy",
+        "data": "synthetic (deterministic generator, SURVEY 8(d) config 2 shape)",
+        "config": {"workload": f"config 2 sample: {sample} prompts/step x 2048 tokens, B=16, W=32, 64 users, "
+                               "256x640-token shared pool pre-inserted", "sample_prompts_per_step": sample},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} steps x {sample} prompts of config 2"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import ctypes as C
+    from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, GenSpec, generate, generate_pool
+    from paper_2508_08438_b200 import native as N
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = dict(CFG2)
+    if args.prompts:
+        c["n_prompts"] = args.prompts
+    n_local = c["n_prompts"]  # weak scaling: every rank admits a full config-2 batch per step
+    L, B = c["prompt_tokens"], c["block_tokens"]
+    steps, warm = args.steps, args.warmup
+    n_batches = steps + warm
+    blocks_per_batch = n_local * (L // B)
+    cap = 1 << max(20, int(np.ceil(np.log2((n_batches + 1) * blocks_per_batch * 1.7))))
+    ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
+                        max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 21,
+                        device=local)
+
+    # ---- inputs: distinct batches, generated into pinned host memory, copied to HBM
+    spec = GenSpec(n_prompts=n_local, prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
+                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"])
+    host, devb = [], []
+    for k in range(n_batches):
+        spec.prompt_id_base = (k + 1) * 100_000_000 + rank * n_local
+        tok_pin = torch.empty(n_local * L, dtype=torch.int32, pin_memory=True)
+        tok_np = tok_pin.numpy().view(np.uint32)
+        _, off, users, owners = generate(spec, tokens_out=tok_np)
+        host.append((tok_pin, tok_np, off, users, owners))
+    for (tok_pin, _, off, users, owners) in host:
+        devb.append((tok_pin.to(dev, non_blocking=True), torch.from_numpy(off.view(np.int64)).to(dev),
+                     torch.from_numpy(users.view(np.int64)).to(dev), torch.from_numpy(owners).to(dev)))
+    torch.cuda.synchronize()
+    pool = generate_pool(spec)
+
+    def fresh_engine():
+        eng = AdmissionEngine(ecfg)
+        eng.admit(*pool)
+        eng.commit()
+        eng.epoch_pass()
+        return eng
+
+    def step_device(eng, k):
+        t, o, u, w = devb[k]
+        b = N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, n_local * L, 1)
+        eng.admit_raw(b)
+        eng.commit()
+        eng.epoch_pass()
+
+    # outputs returned to the host in the e2e arm: labels per block + match length per prompt
+    out_label = np.empty(blocks_per_batch, np.uint8)
+    out_match = np.empty(n_local, np.uint32)
+
+    def step_host(eng, k):
+        _, tok, off, users, owners = host[k]
+        b = N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
+                    n_local * L, 0)
+        o = N.AdmitOut(None, None, out_label.ctypes.data, None, None, out_match.ctypes.data, None, None, 0, 0, 0)
+        eng.admit_raw(b, o)
+        eng.commit()
+        eng.epoch_pass()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(step_fn):
+        eng = fresh_engine()
+        ext = torch.cuda.ExternalStream(eng.stream, device=dev)
+        for k in range(warm):
+            step_fn(eng, k)
+        hs, launches = [], 0
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for k in range(warm, warm + steps):
+            step_fn(eng, k)
+            t = eng.times()
+            hs.append(t["hash_scan_ms"])
+            launches += t["kernels_launched"] + 2 + 6  # admit + commit (claim, commit) + epoch kernels
+        e1.record(ext)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            import torch.distributed as dist
+            x = torch.tensor([ms], device=dev)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            ms = float(x.item())
+        last = eng.times()
+        eng.close()
+        return ms, hs, launches, last
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_dev, hs, launches, last = timed(step_device)
+    clk = clocks.stop()
+    ms_e2e, _, _, _ = timed(step_host)
+
+    total_blocks = blocks_per_batch * steps * world
+    value = total_blocks / (ms_dev / 1e3)
+    e2e_value = total_blocks / (ms_e2e / 1e3)
+    # roofline of the dominant kernel (k_hash_scan): algorithmic bytes per launch =
+    # 4 B/token read once + 8 B digest + 4 B rule mask written per block
+    hs_avg = float(np.mean(hs))
+    alg_bytes = 4 * n_local * L + 12 * blocks_per_batch
+    achieved = alg_bytes / (hs_avg / 1e3) / 1e9
+    peak, kind = peaks()
+    traffic = None
+    tp = ROOT / "profiles" / "hash_scan_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        r = cpu_reference_run(steps=1, warmup=0, sample_prompts=args.cpu_sample, threads=os.cpu_count() or 1)
+        if r is not None:
+            cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
+                   "sample": f"{args.cpu_sample} prompts of config 2 (pool pre-inserted), 1 batch: "
+                             f"{r['seconds']:.1f} s"}
+    h2d = n_local * L * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
+    d2h = blocks_per_batch + n_local * 4
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": ms_dev / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 tokens / u64 keys (integer), f64 entropy", "data": "synthetic (deterministic generator)",
+        "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
+                               f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
+                   "global_batch_prompts": n_local * world, "l2": "inputs 512 MiB/step > L2, distinct batch per step",
+                   "step": "admit + commit + epoch", "parallelism": f"replicas x{world}"},
+        "stage_ms_last": {k: round(float(last[k]), 4) for k in ("hash_scan_ms", "chain_probe_ms", "record_ms",
+                                                                  "admit_total_ms", "commit_ms", "epoch_ms")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_hash_scan", "peak_kind": kind,
+                     "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": hs_avg},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/* safekv_b200.h -- C ABI of the B200-native SafeKV admission hot path.
+ *
+ * This is the drop-in boundary for the per-batch admission path of the SafeKV
+ * reference (arxiv 2508.08438, /root/reference/proj/include/safekv).  The reference is
+ * header-only C++ with no FFI of its own; each entry point below names the reference
+ * interface it replaces (file:line under proj/include/safekv/).  The C++ facade in
+ * include/safekv_b200/safekv.hpp re-exposes these under the reference's class and
+ * method names; INTEGRATION.md shows how ServingSimulator::submit would call them.
+ *
+ * Conventions
+ *  - Every call returns an int status (SKV_OK == 0).  The facade rethrows the
+ *    matching safekv::Error subclass (core.hpp:19-59).
+ *  - The caller owns all buffers it passes; the context owns device memory.
+ *  - One CUDA stream per context; calls on one context are serialised, mirroring the
+ *    reference's single-writer contract (cache_index.hpp:122-127).
+ *  - There is no CPU fallback: without a CUDA device skv_create fails with
+ *    SKV_ERR_CUDA.  Rule compilation (skv_rules_*) is host-only, like the
+ *    reference's std::regex construction (detection.hpp:120-144).
+ */
+#ifndef SAFEKV_B200_H_
+#define SAFEKV_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKV_ABI_VERSION 1
+
+enum {
+  SKV_OK = 0,
+  SKV_ERR_ARG = 1,       /* bad argument (null pointer, size mismatch)            */
+  SKV_ERR_PARSE = 2,     /* safekv::ParseError      (detection.hpp:224-279)      */
+  SKV_ERR_COMPILE = 3,   /* safekv::CompileError    (detection.hpp:126-137)      */
+  SKV_ERR_CONFIG = 4,    /* safekv::ConfigError                                   */
+  SKV_ERR_CAPACITY = 5,  /* safekv::CapacityExhausted (cache_index.hpp:801-806)   */
+  SKV_ERR_STATE = 6,     /* call-order violation (e.g. commit with no admitted batch) */
+  SKV_ERR_CUDA = 7,      /* no sm_100 device, or a CUDA runtime failure           */
+  SKV_ERR_INTERNAL = 8
+};
+
+/* SensitivityLabel values (core.hpp:167) */
+enum { SKV_LABEL_PRIVATE = 0, SKV_LABEL_PUBLIC = 1, SKV_LABEL_PENDING = 2, SKV_LABEL_RESTRICTED = 3 };
+/* MemTier values (core.hpp:145) */
+enum { SKV_TIER_HBM = 0, SKV_TIER_DRAM = 1, SKV_TIER_SSD = 2 };
+/* per-block lookup decision */
+enum { SKV_MISS = 0, SKV_PUBLIC_HIT = 1, SKV_OWNER_HIT = 2 };
+/* AnomalyAction (monitor.hpp:17) */
+enum { SKV_ACTION_NONE = 0, SKV_ACTION_DOWNGRADE = 1, SKV_ACTION_RESTRICT = 2 };
+
+/* ------------------------------------------------------------------------------
+ * Rule sets (host).  Replaces CompiledRuleSet::compile (detection.hpp:120-144),
+ * RuleEngine::load_rules_json (detection.hpp:222-242) and default_pattern_rules
+ * (detection.hpp:185-204).  A skv_rules is an immutable snapshot (the reference's
+ * shared_ptr<const CompiledRuleSet>); the rule list is compiled into one search DFA.
+ * ------------------------------------------------------------------------------ */
+typedef struct skv_rules skv_rules;
+
+int skv_rules_default(skv_rules** out);
+/* err receives the reference-style message ("rule 'b': bad regex: ..."). */
+int skv_rules_from_json(const char* json, size_t len, skv_rules** out, char* err, size_t errcap);
+void skv_rules_free(skv_rules* r);
+uint64_t skv_rules_version(const skv_rules* r);
+uint32_t skv_rules_count(const skv_rules* r);
+/* rule i: id, category, kind (0 regex, 1 blacklist), enabled */
+int skv_rules_info(const skv_rules* r, uint32_t i, const char** rule_id, const char** category, int* kind,
+                   int* enabled);
+size_t skv_rules_warning_count(const skv_rules* r);
+const char* skv_rules_warning(const skv_rules* r, size_t i);
+/* Device rule masks use bit j = j-th ENABLED rule; this maps j -> rule list index. */
+uint32_t skv_rules_enabled_count(const skv_rules* r);
+uint32_t skv_rules_enabled_rule(const skv_rules* r, uint32_t j);
+
+/* Read-only view of the compiled automaton (tests / tooling). */
+typedef struct {
+  uint32_t n_states, n_classes, start;
+  const uint8_t* class_map; /* [256] byte -> class                     */
+  const uint16_t* next;     /* [n_states * n_classes]                   */
+  const uint32_t* acc;      /* [n_states * (n_classes + 1)], last = EOS */
+  uint32_t nfa_states, dfa_states_unminimized;
+} skv_dfa_view;
+int skv_rules_dfa(const skv_rules* r, skv_dfa_view* out);
+
+/* ------------------------------------------------------------------------------
+ * Context.  Holds the device-resident index (flattened, hash-addressed replacement
+ * of RadixCacheIndex, cache_index.hpp:127-836), the monitor state (EntropyMonitor,
+ * monitor.hpp:44-113) and the active rule DFA.
+ * ------------------------------------------------------------------------------ */
+typedef struct skv_ctx skv_ctx;
+
+typedef struct {
+  int device;                  /* CUDA device ordinal                                 */
+  uint32_t block_tokens;       /* B: tokens per KV block (multiple of 4, 4..4096)     */
+  uint32_t window_tokens;      /* W: right-context tokens of a block's scan window    */
+  uint64_t index_capacity;     /* entry slots (rounded up to a power of two)          */
+  uint64_t max_prompts;        /* per batch                                           */
+  uint64_t max_tokens;         /* per batch                                           */
+  uint64_t max_window_entries; /* distinct entries touched per monitor window         */
+  double entropy_jump;         /* MonitorConfig::entropy_jump (monitor.hpp:12)        */
+  uint64_t u_pre_max;          /* MonitorConfig::u_pre_max    (monitor.hpp:13)        */
+} skv_config;
+
+void skv_config_default(skv_config* c);
+int skv_create(const skv_config* c, skv_ctx** out);
+int skv_destroy(skv_ctx* ctx);
+const char* skv_last_error(const skv_ctx* ctx);
+/* Atomic snapshot swap; takes effect at the next skv_admit (RuleEngine::load_rules
+ * swap semantics, detection.hpp:238-241).  The context keeps its own copy. */
+int skv_set_rules(skv_ctx* ctx, const skv_rules* r);
+/* cudaStream_t of the context (as void*). */
+void* skv_stream(skv_ctx* ctx);
+
+/* ------------------------------------------------------------------------------
+ * Batch admission: phase L = skv_admit, phase C = skv_commit,
+ * phase E = skv_epoch.  Replaces the per-request sequence of ServingSimulator::submit
+ * (serving_sim.hpp:184-218): token_seq_digest (core.hpp:68-73),
+ * RuleEngine::tier1_scan (detection.hpp:217), RadixCacheIndex::match_prefix
+ * (cache_index.hpp:213-237), EntropyMonitor::record_access (monitor.hpp:50),
+ * RadixCacheIndex::insert + resolve_block (cache_index.hpp:152-205, 321-343) and
+ * EntropyMonitor::epoch_pass (monitor.hpp:85-99).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  const uint32_t* tokens;  /* concatenated prompts, TokenId = uint32 (core.hpp:65) */
+  const uint64_t* offsets; /* n_prompts + 1 token offsets                          */
+  const uint64_t* users;   /* UserId::value per prompt (core.hpp:129-135)          */
+  const uint8_t* owners;   /* OwnerClass per prompt (0 Customer, 1 Business); NULL = Customer */
+  uint32_t n_prompts;
+  uint64_t n_tokens;
+  int on_device;           /* 1: all pointers are device pointers (inputs resident in HBM) */
+} skv_batch;
+
+typedef struct {
+  /* per block, prompt-major, n_blocks = sum floor(L_p / B).  Any pointer may be NULL. */
+  uint64_t* block_h;     /* chained prefix key h_b                          */
+  uint64_t* block_d;     /* token_seq_digest of the block d_b               */
+  uint8_t* label;        /* SKV_LABEL_PRIVATE / SKV_LABEL_PUBLIC (A.4)      */
+  uint32_t* rule_mask;   /* window verdict, bit j = j-th enabled rule (A.3) */
+  uint8_t* decision;     /* SKV_MISS / SKV_PUBLIC_HIT / SKV_OWNER_HIT (A.5) */
+  /* per prompt */
+  uint32_t* matched_blocks; /* longest visible prefix, in blocks            */
+  uint8_t* lowest_tier;     /* MatchResult::lowest_tier (cache_index.hpp:234) */
+  uint64_t* block_offsets;  /* n_prompts + 1                                 */
+  int on_device;            /* 1: the pointers above are device pointers     */
+  /* summary, always filled (host) */
+  uint64_t n_blocks;
+  uint64_t matched_total;
+} skv_admit_out;
+
+int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
+/* Insert the new blocks of the last admitted batch (first creator wins; intra-batch
+ * duplicates are won by the lowest prompt index).  new_entries may be NULL. */
+int skv_commit(skv_ctx* ctx, uint64_t* new_entries);
+
+typedef struct {
+  uint64_t h, d;          /* entry key                           */
+  uint8_t action;         /* SKV_ACTION_*                        */
+  uint8_t owner;          /* OwnerClass                          */
+  double entropy_now, entropy_prev;
+  uint64_t u_pre;
+  uint64_t epoch;
+} skv_event;
+
+/* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d). */
+int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
+
+/* Tier tags of existing entries (demote, cache_index.hpp:362-381). */
+int skv_set_tiers(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, size_t n);
+
+typedef struct {
+  uint64_t h, d, creator;
+  uint8_t label, owner, tier;
+  uint64_t hit_cur, u_cnt, hit_pre, u_pre; /* AccessStats (access_stats.hpp:18-21) */
+} skv_entry;
+/* Export all live entries (parity dump; order unspecified). */
+int skv_export(skv_ctx* ctx, skv_entry* out, size_t cap, size_t* n);
+uint64_t skv_entry_count(skv_ctx* ctx);
+
+/* Per-stage device times of the last skv_admit / skv_commit (CUDA events, ms). */
+typedef struct {
+  float hash_scan_ms, chain_probe_ms, record_ms, admit_total_ms, commit_ms, epoch_ms;
+  uint64_t matched_total, accesses, new_blocks, touched_entries;
+  uint32_t kernels_launched;
+} skv_stage_times;
+int skv_last_times(skv_ctx* ctx, skv_stage_times* out);
+
+/* Per-call wrappers (batch of one, still on the device) for the facade:
+ * RuleEngine::tier1_scan (detection.hpp:217) and token_seq_digest (core.hpp:68). */
+int skv_tier1_scan(skv_ctx* ctx, const char* text, size_t len, uint32_t* rule_mask);
+int skv_token_seq_digest(skv_ctx* ctx, const uint32_t* tokens, size_t n, uint64_t* digest);
+
+/* ------------------------------------------------------------------------------
+ * Synthetic workload generator (host), deterministic, built from the reference's
+ * generator primitives (workload.hpp:155-266; util.hpp:14-55).  See DESIGN.md.
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t n_prompts, prompt_tokens;  /* prompt length (all prompts equal) */
+  uint64_t n_users;                   /* user = first_user + p % n_users   */
+  uint64_t first_user;
+  uint64_t pool_size, pool_tokens;    /* shared-prefix pool                */
+  double shared_fraction;             /* fraction of prompts that start with a pool prefix */
+  double pii_per_kib;                 /* PII phrases per KiB of unique body */
+  uint32_t pii_mix;                   /* 1: config-3 mix (60% none, 30% one per 2 KiB, 10% one per 256 B) */
+  uint64_t seed;
+  uint64_t prompt_id_base;            /* global id of prompt 0 (sharding)  */
+} skv_gen_spec;
+/* Writes n_prompts*prompt_tokens tokens and n_prompts+1 offsets; users/owners may be NULL. */
+int skv_generate(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
+                 uint8_t* owners, int nthreads);
+/* The pool prefixes themselves (pool_size prompts of pool_tokens). */
+int skv_generate_pool(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
+                      uint8_t* owners);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAFEKV_B200_H_ */

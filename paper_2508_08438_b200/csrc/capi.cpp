@@ -1,0 +1,744 @@
+// capi.cpp -- C ABI (include/safekv_b200.h): rule snapshots, context lifetime, and the
+// host orchestration of the device stages of one admission batch.  Host code only
+// sequences kernels and moves buffers; every per-token / per-block / per-entry
+// computation runs on the device (kernels.cu).  There is no CPU fallback path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/safekv_b200.h"
+#include "ctx.hpp"
+#include "rules.hpp"
+
+struct skv_rules {
+  skv::RuleSetSpec spec;
+  skv::DfaTables dfa;
+};
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CapacityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int log2u(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+uint64_t fnv_u32_host(uint64_t h, uint32_t v) {
+  for (int i = 0; i < 4; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * 0x100000001b3ULL;
+  return h;
+}
+
+}  // namespace
+
+struct skv_ctx {
+  skv_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::vector<void*> owned;
+
+  // rules
+  skv_rules rules_host;
+  skv::DevRules rules_dev;
+  void* rules_buf = nullptr;
+  bool rules_loaded = false;
+
+  // index
+  skv::Index ix;
+  uint64_t entries = 0;
+
+  // monitor window state
+  unsigned long long* sets = nullptr;
+  uint32_t* set_size = nullptr;
+  uint32_t pool_cap = 0;
+  uint32_t* touched[2] = {nullptr, nullptr};
+  uint32_t* counters = nullptr;  // [0]=pool_count [1..2]=n_touched[2] [3]=n_cands [4]=n_events [5]=err_flag [6]=n_runs
+  unsigned long long* n_new = nullptr;
+  int cur = 0;
+  uint32_t* cands = nullptr;
+  uint32_t* fired = nullptr;
+  void* events = nullptr;
+  uint64_t epoch = 0;
+
+  // batch buffers
+  uint64_t max_prompts = 0, max_tokens = 0, max_blocks = 0;
+  uint32_t* d_tokens = nullptr;
+  uint64_t* d_off = nullptr;
+  uint64_t* d_users = nullptr;
+  uint8_t* d_owners = nullptr;
+  uint32_t* counts = nullptr;
+  uint32_t* blk_off = nullptr;
+  uint32_t* first_sens = nullptr;
+  uint32_t* matched = nullptr;
+  uint32_t* exist = nullptr;
+  uint8_t* tier = nullptr;
+  uint32_t* acc_off = nullptr;
+  uint64_t* bh = nullptr;
+  uint64_t* bd = nullptr;
+  uint32_t* bmask = nullptr;
+  uint8_t* blabel = nullptr;
+  uint8_t* bdecision = nullptr;
+  uint32_t* bslot = nullptr;
+  uint32_t *key_a = nullptr, *key_b = nullptr, *val_a = nullptr, *val_b = nullptr;
+  uint32_t *uniq = nullptr, *runs = nullptr, *starts = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
+  int hs_grid = 0;
+  uint32_t hs_smem = 0;
+  uint32_t rec_grid = 0;
+
+  // pending batch (between admit and commit)
+  bool pending = false;
+  uint32_t p_n = 0;
+  uint64_t p_blocks = 0;
+  const uint64_t* p_users = nullptr;
+  const uint8_t* p_owners = nullptr;
+  uint32_t batch_id = 0;
+
+  cudaEvent_t ev[8] = {};
+  skv_stage_times times{};
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int fail(skv_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+template <typename F>
+int guard(skv_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const skv::ParseError& e) {
+    return fail(c, SKV_ERR_PARSE, e.what());
+  } catch (const skv::CompileError& e) {
+    return fail(c, SKV_ERR_COMPILE, e.what());
+  } catch (const skv::ConfigError& e) {
+    return fail(c, SKV_ERR_CONFIG, e.what());
+  } catch (const CudaError& e) {
+    return fail(c, SKV_ERR_CUDA, e.what());
+  } catch (const StateError& e) {
+    return fail(c, SKV_ERR_STATE, e.what());
+  } catch (const CapacityError& e) {
+    return fail(c, SKV_ERR_CAPACITY, e.what());
+  } catch (const ArgError& e) {
+    return fail(c, SKV_ERR_ARG, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, SKV_ERR_INTERNAL, e.what());
+  }
+}
+
+// Device form of the DFA (see ctx.hpp DevRules).  The 16-bit row offsets and the
+// 16-bit in-entry rule mask bound the device automaton; larger rule sets are rejected
+// here with CompileError (documented in DESIGN.md).
+void upload_rules(skv_ctx* c, const skv_rules& r) {
+  const auto& d = r.dfa;
+  const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 4;
+  if (static_cast<uint64_t>(S) * row > 65535)
+    throw skv::CompileError("device DFA: " + std::to_string(S) + " states x " + std::to_string(C + 1) +
+                            " columns exceed the 16-bit row offset");
+  if (d.rule_index.size() > 16) throw skv::CompileError("device DFA: more than 16 enabled rules");
+  std::vector<uint32_t> tab(static_cast<size_t>(S) * (C + 1) + 4, 0);
+  for (uint32_t s = 0; s < S; ++s) {
+    for (uint32_t k = 0; k <= C; ++k) {
+      uint32_t next_row = k < C ? static_cast<uint32_t>(d.next[s * C + k]) * row : 0;
+      tab[s * (C + 1) + k] = next_row | (d.acc[s * (C + 1) + k] << 16);
+    }
+  }
+  uint8_t class4[256];
+  for (int b = 0; b < 256; ++b) class4[b] = static_cast<uint8_t>(d.class_map[b] * 4);
+  size_t tab_bytes = ((S * (C + 1) * 4) + 15) & ~size_t(15);
+  void* buf = nullptr;
+  CK(cudaMalloc(&buf, tab_bytes + 256 + 64));
+  CK(cudaMemcpyAsync(buf, tab.data(), tab_bytes, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(static_cast<uint8_t*>(buf) + tab_bytes, class4, 256, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->rules_buf) CK(cudaFree(c->rules_buf));
+  c->rules_buf = buf;
+  c->rules_dev.table = static_cast<uint32_t*>(buf);
+  c->rules_dev.class4 = static_cast<uint8_t*>(buf) + tab_bytes;
+  c->rules_dev.table_bytes = S * (C + 1) * 4;
+  c->rules_dev.start_row = d.start * row;
+  c->rules_dev.eos4 = C * 4;
+  c->rules_dev.n_enabled = static_cast<uint32_t>(d.rule_index.size());
+  c->rules_host = r;
+  c->rules_loaded = true;
+  c->hs_smem = skv::hash_scan_smem(c->rules_dev, c->cfg.block_tokens, c->cfg.window_tokens);
+  if (c->hs_smem > 227 * 1024) throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB");
+  c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------------ rules
+int skv_rules_default(skv_rules** out) {
+  if (!out) return SKV_ERR_ARG;
+  return guard(nullptr, [&] {
+    auto r = std::make_unique<skv_rules>();
+    r->spec.version = 1;  // RuleEngine() default snapshot version (detection.hpp:210)
+    r->spec.rules = skv::default_pattern_rules();
+    r->dfa = skv::compile_rules(r->spec.rules);
+    *out = r.release();
+    return SKV_OK;
+  });
+}
+
+int skv_rules_from_json(const char* json, size_t len, skv_rules** out, char* err, size_t errcap) {
+  if (!json || !out) return SKV_ERR_ARG;
+  skv_ctx scratch;  // carries the error message
+  int rc = guard(&scratch, [&] {
+    auto r = std::make_unique<skv_rules>();
+    r->spec = skv::parse_rules_json(std::string(json, len));
+    r->dfa = skv::compile_rules(r->spec.rules);
+    *out = r.release();
+    return SKV_OK;
+  });
+  if (rc != SKV_OK && err && errcap) {
+    size_t n = std::min(errcap - 1, scratch.err.size());
+    std::memcpy(err, scratch.err.data(), n);
+    err[n] = 0;
+  }
+  return rc;
+}
+
+void skv_rules_free(skv_rules* r) { delete r; }
+uint64_t skv_rules_version(const skv_rules* r) { return r ? r->spec.version : 0; }
+uint32_t skv_rules_count(const skv_rules* r) { return r ? static_cast<uint32_t>(r->spec.rules.size()) : 0; }
+
+int skv_rules_info(const skv_rules* r, uint32_t i, const char** rule_id, const char** category, int* kind,
+                   int* enabled) {
+  if (!r || i >= r->spec.rules.size()) return SKV_ERR_ARG;
+  const auto& x = r->spec.rules[i];
+  if (rule_id) *rule_id = x.rule_id.c_str();
+  if (category) *category = x.category.c_str();
+  if (kind) *kind = x.blacklist ? 1 : 0;
+  if (enabled) *enabled = x.enabled ? 1 : 0;
+  return SKV_OK;
+}
+
+size_t skv_rules_warning_count(const skv_rules* r) { return r ? r->spec.warnings.size() : 0; }
+const char* skv_rules_warning(const skv_rules* r, size_t i) {
+  return (r && i < r->spec.warnings.size()) ? r->spec.warnings[i].c_str() : nullptr;
+}
+uint32_t skv_rules_enabled_count(const skv_rules* r) {
+  return r ? static_cast<uint32_t>(r->dfa.rule_index.size()) : 0;
+}
+uint32_t skv_rules_enabled_rule(const skv_rules* r, uint32_t j) {
+  return (r && j < r->dfa.rule_index.size()) ? r->dfa.rule_index[j] : UINT32_MAX;
+}
+
+int skv_rules_dfa(const skv_rules* r, skv_dfa_view* v) {
+  if (!r || !v) return SKV_ERR_ARG;
+  v->n_states = r->dfa.n_states;
+  v->n_classes = r->dfa.n_classes;
+  v->start = r->dfa.start;
+  v->class_map = r->dfa.class_map;
+  v->next = r->dfa.next.data();
+  v->acc = r->dfa.acc.data();
+  v->nfa_states = r->dfa.nfa_states;
+  v->dfa_states_unminimized = r->dfa.dfa_states_unminimized;
+  return SKV_OK;
+}
+
+// ------------------------------------------------------------------ context
+void skv_config_default(skv_config* c) {
+  if (!c) return;
+  c->device = 0;
+  c->block_tokens = 16;
+  c->window_tokens = 32;
+  c->index_capacity = 1ull << 20;
+  c->max_prompts = 1ull << 16;
+  c->max_tokens = 1ull << 24;
+  c->max_window_entries = 1ull << 18;
+  c->entropy_jump = 0.3;  // MonitorConfig defaults (monitor.hpp:12-15)
+  c->u_pre_max = 1;
+}
+
+int skv_create(const skv_config* cfg, skv_ctx** out) {
+  if (!cfg || !out) return SKV_ERR_ARG;
+  auto c = std::make_unique<skv_ctx>();
+  int rc = guard(c.get(), [&] {
+    c->cfg = *cfg;
+    const uint32_t B = cfg->block_tokens;
+    if (B < 4 || B > 4096 || B % 4) throw skv::ConfigError("block_tokens must be a multiple of 4 in [4, 4096]");
+    if (cfg->window_tokens > 4096) throw skv::ConfigError("window_tokens must be <= 4096");
+    if (cfg->max_prompts == 0 || cfg->max_prompts >= (1ull << 31)) throw skv::ConfigError("bad max_prompts");
+    if (cfg->max_tokens / B >= (1ull << 31)) throw skv::ConfigError("max_tokens / block_tokens must be < 2^31");
+    if (cfg->max_window_entries == 0 || cfg->max_window_entries >= (1ull << 31))
+      throw skv::ConfigError("bad max_window_entries");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      throw CudaError("no CUDA device available (this library has no CPU fallback)");
+    if (cfg->device < 0 || cfg->device >= ndev) throw skv::ConfigError("device ordinal out of range");
+    c->device = cfg->device;
+    CK(cudaSetDevice(c->device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major != 10)
+      throw CudaError("device " + std::string(prop.name) + " is not sm_100 (built for sm_100a only)");
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& ev : c->ev) CK(cudaEventCreate(&ev));
+    // index
+    uint64_t cap = next_pow2(std::max<uint64_t>(cfg->index_capacity, 1024));
+    if (cap > (1ull << 31)) throw skv::ConfigError("index_capacity must be <= 2^31");
+    c->cfg.index_capacity = cap;
+    c->ix.cap = cap;
+    c->ix.mask = cap - 1;
+    c->ix.rec = dalloc<skv::Rec>(cap, c->owned);
+    c->ix.stats = dalloc<skv::Stats>(cap, c->owned);
+    c->ix.aux = dalloc<skv::Aux>(cap, c->owned);
+    c->ix.claim = dalloc<unsigned long long>(cap, c->owned);
+    CK(cudaMemsetAsync(c->ix.rec, 0, cap * sizeof(skv::Rec), c->stream));
+    CK(cudaMemsetAsync(c->ix.stats, 0, cap * sizeof(skv::Stats), c->stream));
+    CK(cudaMemsetAsync(c->ix.aux, 0xff, cap * sizeof(skv::Aux), c->stream));
+    CK(cudaMemsetAsync(c->ix.claim, 0, cap * sizeof(unsigned long long), c->stream));
+    // monitor window
+    c->pool_cap = static_cast<uint32_t>(cfg->max_window_entries);
+    c->sets = dalloc<unsigned long long>(static_cast<size_t>(c->pool_cap) * skv::kMaxSetUsers, c->owned);
+    c->set_size = dalloc<uint32_t>(c->pool_cap, c->owned);
+    c->touched[0] = dalloc<uint32_t>(c->pool_cap, c->owned);
+    c->touched[1] = dalloc<uint32_t>(c->pool_cap, c->owned);
+    c->counters = dalloc<uint32_t>(16, c->owned);
+    c->n_new = dalloc<unsigned long long>(1, c->owned);
+    CK(cudaMemsetAsync(c->counters, 0, 16 * sizeof(uint32_t), c->stream));
+    c->cands = dalloc<uint32_t>(2ull * c->pool_cap, c->owned);
+    c->fired = dalloc<uint32_t>(2ull * c->pool_cap, c->owned);
+    c->events = dalloc<skv_event>(2ull * c->pool_cap, c->owned);
+    // batch buffers
+    c->max_prompts = cfg->max_prompts;
+    c->max_tokens = cfg->max_tokens;
+    c->max_blocks = cfg->max_tokens / B;
+    const uint64_t N = c->max_prompts, NB = std::max<uint64_t>(c->max_blocks, 1);
+    c->d_tokens = dalloc<uint32_t>(c->max_tokens + 4, c->owned);
+    c->d_off = dalloc<uint64_t>(N + 1, c->owned);
+    c->d_users = dalloc<uint64_t>(N, c->owned);
+    c->d_owners = dalloc<uint8_t>(N, c->owned);
+    c->counts = dalloc<uint32_t>(N + 1, c->owned);
+    c->blk_off = dalloc<uint32_t>(N + 1, c->owned);
+    c->first_sens = dalloc<uint32_t>(N, c->owned);
+    c->matched = dalloc<uint32_t>(N + 1, c->owned);
+    c->exist = dalloc<uint32_t>(N, c->owned);
+    c->tier = dalloc<uint8_t>(N, c->owned);
+    c->acc_off = dalloc<uint32_t>(N + 1, c->owned);
+    c->bh = dalloc<uint64_t>(NB, c->owned);
+    c->bd = dalloc<uint64_t>(NB, c->owned);
+    c->bmask = dalloc<uint32_t>(NB, c->owned);
+    c->blabel = dalloc<uint8_t>(NB, c->owned);
+    c->bdecision = dalloc<uint8_t>(NB, c->owned);
+    c->bslot = dalloc<uint32_t>(NB, c->owned);
+    c->key_a = dalloc<uint32_t>(NB, c->owned);
+    c->key_b = dalloc<uint32_t>(NB, c->owned);
+    c->val_a = dalloc<uint32_t>(NB, c->owned);
+    c->val_b = dalloc<uint32_t>(NB, c->owned);
+    c->uniq = dalloc<uint32_t>(NB, c->owned);
+    c->runs = dalloc<uint32_t>(NB, c->owned);
+    c->starts = dalloc<uint32_t>(NB, c->owned);
+    size_t tb = std::max({skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
+                          skv::sort_temp_bytes(static_cast<uint32_t>(NB), log2u(cap)),
+                          skv::rle_temp_bytes(static_cast<uint32_t>(NB))});
+    c->temp_bytes = tb;
+    c->temp = dalloc<uint8_t>(tb, c->owned);
+    CK(cudaMallocHost(&c->host_small, 64 * sizeof(uint32_t)));
+    c->rec_grid = skv::record_grid(c->device);
+    // default rules
+    skv_rules* r = nullptr;
+    int rr = skv_rules_default(&r);
+    if (rr != SKV_OK) throw skv::CompileError("default rules failed to compile");
+    std::unique_ptr<skv_rules> hold(r);
+    upload_rules(c.get(), *r);
+    CK(cudaStreamSynchronize(c->stream));
+    return SKV_OK;
+  });
+  if (rc != SKV_OK) {
+    // the ctx is destroyed: keep the message for skv_last_error(NULL)
+    g_create_err = c->err;
+    for (void* p : c->owned) cudaFree(p);
+    c->owned.clear();
+    *out = nullptr;
+    return rc;
+  }
+  *out = c.release();
+  return SKV_OK;
+}
+
+int skv_destroy(skv_ctx* c) {
+  if (!c) return SKV_ERR_ARG;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->owned) cudaFree(p);
+  if (c->rules_buf) cudaFree(c->rules_buf);
+  if (c->host_small) cudaFreeHost(c->host_small);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return SKV_OK;
+}
+
+const char* skv_last_error(const skv_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int skv_set_rules(skv_ctx* c, const skv_rules* r) {
+  if (!c || !r) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    upload_rules(c, *r);
+    return SKV_OK;
+  });
+}
+
+void* skv_stream(skv_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+// ------------------------------------------------------------------ admission
+int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
+  if (!c || !b) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    const uint32_t N = b->n_prompts;
+    const uint32_t B = c->cfg.block_tokens;
+    if (N > c->max_prompts) throw ArgError("n_prompts exceeds max_prompts");
+    if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
+    if (N == 0) {
+      if (out) out->n_blocks = 0, out->matched_total = 0;
+      c->pending = true;
+      c->p_n = 0;
+      c->p_blocks = 0;
+      return SKV_OK;
+    }
+    if (!b->tokens || !b->offsets || !b->users) throw ArgError("null batch pointer");
+    cudaStream_t s = c->stream;
+    const uint32_t* tokens;
+    const uint64_t* off;
+    const uint64_t* users;
+    const uint8_t* owners;
+    uint64_t n_blocks = 0;
+    CK(cudaEventRecord(c->ev[0], s));
+    if (!b->on_device) {
+      if (b->offsets[0] != 0 || b->offsets[N] != b->n_tokens) throw ArgError("offsets must span [0, n_tokens]");
+      for (uint32_t p = 0; p < N; ++p) {
+        if (b->offsets[p + 1] < b->offsets[p]) throw ArgError("offsets must be non-decreasing");
+        n_blocks += (b->offsets[p + 1] - b->offsets[p]) / B;
+      }
+      CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(c->d_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(c->d_users, b->users, N * 8ull, cudaMemcpyHostToDevice, s));
+      if (b->owners) CK(cudaMemcpyAsync(c->d_owners, b->owners, N, cudaMemcpyHostToDevice, s));
+      tokens = c->d_tokens;
+      off = c->d_off;
+      users = c->d_users;
+      owners = b->owners ? c->d_owners : nullptr;
+    } else {
+      tokens = b->tokens;
+      if (reinterpret_cast<uintptr_t>(tokens) % 16) {
+        CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyDeviceToDevice, s));
+        tokens = c->d_tokens;
+      }
+      off = b->offsets;
+      users = b->users;
+      owners = b->owners;
+    }
+    skv::launch_block_counts(off, N, B, c->counts, s);
+    skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
+    if (b->on_device) {
+      CK(cudaMemcpyAsync(c->host_small, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      n_blocks = c->host_small[0];
+    }
+    if (n_blocks > c->max_blocks) throw ArgError("batch has more blocks than max_tokens / block_tokens");
+    CK(cudaMemsetAsync(c->first_sens, 0xff, N * 4ull, s));
+    CK(cudaMemsetAsync(c->bdecision, 0, std::max<uint64_t>(n_blocks, 1), s));
+    CK(cudaMemsetAsync(c->matched + N, 0, 4, s));
+    CK(cudaEventRecord(c->ev[1], s));
+    // stages 1+2: digest + rule-tier window scan
+    skv::HashScanArgs a;
+    a.tokens = tokens;
+    a.tok_off = off;
+    a.blk_off = c->blk_off;
+    a.n_prompts = N;
+    a.n_tokens = b->n_tokens;
+    a.n_blocks = static_cast<uint32_t>(n_blocks);
+    a.B = B;
+    a.W = c->cfg.window_tokens;
+    a.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, B);
+    a.rules = c->rules_dev;
+    a.d_out = c->bd;
+    a.mask_out = c->bmask;
+    a.first_sens = c->first_sens;
+    skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, s);
+    CK(cudaEventRecord(c->ev[2], s));
+    // chained keys + labels, then the index probe (stage 3)
+    skv::launch_chain(c->bd, c->blk_off, c->first_sens, N, c->bh, c->blabel, s);
+    skv::launch_probe(c->ix, c->bh, c->bd, c->blk_off, users, N, c->bdecision, c->bslot, c->matched, c->exist, c->tier,
+                      s);
+    CK(cudaEventRecord(c->ev[3], s));
+    // stage 4: monitor record
+    skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->matched, c->acc_off, N + 1, s);
+    CK(cudaMemcpyAsync(c->host_small, c->acc_off + N, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t M = c->host_small[0];
+    uint32_t launched = 5;
+    if (M > 0) {
+      const int bits = log2u(c->ix.cap);
+      skv::launch_emit_accesses(c->bslot, c->blk_off, c->matched, c->acc_off, N, c->key_a, c->val_a, s);
+      skv::launch_sort_pairs(c->temp, c->temp_bytes, c->key_a, c->key_b, c->val_a, c->val_b, M, bits, s);
+      skv::launch_rle(c->temp, c->temp_bytes, c->key_b, c->uniq, c->runs, c->counters + 6, M, s);
+      skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->runs, c->starts, M, s);
+      skv::launch_record(c->ix, c->uniq, c->runs, c->starts, c->counters + 6, c->val_b, users, c->sets, c->set_size,
+                         c->pool_cap, c->counters + 0, c->touched[c->cur], c->counters + 1 + c->cur,
+                         c->counters + 5, static_cast<int>(c->rec_grid), s);
+      launched += 5;
+    }
+    CK(cudaEventRecord(c->ev[4], s));
+    // outputs
+    if (out) {
+      cudaMemcpyKind k = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      if (out->block_h) CK(cudaMemcpyAsync(out->block_h, c->bh, n_blocks * 8, k, s));
+      if (out->block_d) CK(cudaMemcpyAsync(out->block_d, c->bd, n_blocks * 8, k, s));
+      if (out->label) CK(cudaMemcpyAsync(out->label, c->blabel, n_blocks, k, s));
+      if (out->rule_mask) CK(cudaMemcpyAsync(out->rule_mask, c->bmask, n_blocks * 4, k, s));
+      if (out->decision) CK(cudaMemcpyAsync(out->decision, c->bdecision, n_blocks, k, s));
+      if (out->matched_blocks) CK(cudaMemcpyAsync(out->matched_blocks, c->matched, N * 4ull, k, s));
+      if (out->lowest_tier) CK(cudaMemcpyAsync(out->lowest_tier, c->tier, N, k, s));
+      if (out->block_offsets) CK(cudaMemcpyAsync(out->block_offsets, c->blk_off, (N + 1) * 4ull, k, s));
+      out->n_blocks = n_blocks;
+      out->matched_total = M;
+    }
+    CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (c->host_small[8 + 5] & 1u)
+      throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
+    c->times.hash_scan_ms = elapsed(c->ev[1], c->ev[2]);
+    c->times.chain_probe_ms = elapsed(c->ev[2], c->ev[3]);
+    c->times.record_ms = elapsed(c->ev[3], c->ev[4]);
+    c->times.admit_total_ms = elapsed(c->ev[0], c->ev[4]);
+    c->times.matched_total = M;
+    c->times.accesses = M;
+    c->times.touched_entries = c->host_small[8 + 1 + c->cur];
+    c->times.kernels_launched = launched;
+    c->pending = true;
+    c->p_n = N;
+    c->p_blocks = n_blocks;
+    c->p_users = users;
+    c->p_owners = owners;
+    return SKV_OK;
+  });
+}
+
+int skv_commit(skv_ctx* c, uint64_t* new_entries) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->pending) throw StateError("skv_commit without a preceding skv_admit");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    if (c->p_n == 0) {
+      c->pending = false;
+      if (new_entries) *new_entries = 0;
+      return SKV_OK;
+    }
+    if (c->entries + c->p_blocks > c->ix.cap - c->ix.cap / 8)
+      throw CapacityError("index capacity exhausted (eviction is not part of this path)");
+    CK(cudaEventRecord(c->ev[5], s));
+    CK(cudaMemsetAsync(c->n_new, 0, 8, s));
+    ++c->batch_id;
+    skv::launch_claim(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->p_n, c->batch_id, c->bslot, c->counters + 5, s);
+    skv::launch_commit(c->ix, c->blk_off, c->exist, c->blabel, c->p_users, c->p_owners, c->p_n, c->batch_id, c->bslot,
+                       c->n_new, s);
+    CK(cudaEventRecord(c->ev[6], s));
+    unsigned long long nn = 0;
+    CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(&nn, c->host_small, 8);
+    if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
+    c->entries += nn;
+    c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
+    c->times.new_blocks = nn;
+    c->pending = false;
+    if (new_entries) *new_entries = nn;
+    return SKV_OK;
+  });
+}
+
+int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch_out) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(c->ev[5], s));
+    const uint64_t epoch = ++c->epoch;  // advance_epoch (cache_index.hpp:296-299)
+    const uint32_t stamp = static_cast<uint32_t>(epoch);
+    CK(cudaMemcpyAsync(c->host_small, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int cur = c->cur, prev = 1 - c->cur;
+    const uint32_t n_cur = c->host_small[1 + cur], n_prev = c->host_small[1 + prev];
+    const uint32_t bound = n_cur + n_prev;
+    CK(cudaMemsetAsync(c->counters + 3, 0, 8, s));  // n_cands, n_events
+    skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, n_cur, 0, stamp, c->cfg.entropy_jump,
+                                 c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+    skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, n_prev, 1, stamp,
+                                 c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+    skv::launch_epoch_fire(c->ix, c->cands, c->counters + 3, bound, stamp, epoch, c->events, c->counters + 4, c->fired,
+                           s);
+    skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
+    skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, n_prev, 1, s);
+    skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, n_cur, 0, s);
+    CK(cudaMemcpyAsync(c->host_small, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t ne = c->host_small[0];
+    std::vector<skv_event> ev(ne);
+    if (ne) CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
+    // swap windows: the current list becomes the previous one
+    uint32_t reset[3] = {0, 0, 0};
+    reset[1 + prev] = 0;
+    reset[1 + cur] = n_cur;
+    // counters[0] pool_count = 0; counters[1+prev] (new cur) = 0; counters[1+cur] (new prev) = n_cur
+    CK(cudaMemcpyAsync(c->counters, reset, 12, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    c->cur = prev;
+    CK(cudaEventRecord(c->ev[6], s));
+    CK(cudaEventSynchronize(c->ev[6]));
+    c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
+    std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
+      return x.h != y.h ? x.h < y.h : x.d < y.d;
+    });
+    if (events)
+      for (size_t i = 0; i < ev.size() && i < cap; ++i) events[i] = ev[i];
+    if (n_events) *n_events = ev.size();
+    if (epoch_out) *epoch_out = epoch;
+    return SKV_OK;
+  });
+}
+
+int skv_set_tiers(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, size_t n) {
+  if (!c || (n && (!h || !d || !tiers))) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return SKV_OK;
+    std::vector<void*> tmp;
+    uint64_t* dh = dalloc<uint64_t>(n, tmp);
+    uint64_t* dd = dalloc<uint64_t>(n, tmp);
+    uint8_t* dt = dalloc<uint8_t>(n, tmp);
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(dh, h, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dt, tiers, n, cudaMemcpyHostToDevice, s));
+    skv::launch_set_tiers(c->ix, dh, dd, dt, static_cast<uint32_t>(n), s);
+    CK(cudaStreamSynchronize(s));
+    for (void* p : tmp) cudaFree(p);
+    return SKV_OK;
+  });
+}
+
+int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    std::vector<void*> tmp;
+    skv_entry* dout = dalloc<skv_entry>(std::max<uint64_t>(c->entries, 1), tmp);
+    uint32_t* dn = dalloc<uint32_t>(1, tmp);
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(dn, 0, 4, s));
+    skv::launch_export(c->ix, dout, dn, s);
+    uint32_t cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (out && cnt) CK(cudaMemcpy(out, dout, std::min<size_t>(cnt, cap) * sizeof(skv_entry), cudaMemcpyDeviceToHost));
+    for (void* p : tmp) cudaFree(p);
+    if (n) *n = cnt;
+    return SKV_OK;
+  });
+}
+
+uint64_t skv_entry_count(skv_ctx* c) { return c ? c->entries : 0; }
+
+int skv_last_times(skv_ctx* c, skv_stage_times* out) {
+  if (!c || !out) return SKV_ERR_ARG;
+  *out = c->times;
+  return SKV_OK;
+}
+
+int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {
+  if (!c || (!text && len) || !mask) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    std::vector<void*> tmp;
+    uint8_t* dt = dalloc<uint8_t>(len + 1, tmp);
+    uint32_t* dm = dalloc<uint32_t>(1, tmp);
+    cudaStream_t s = c->stream;
+    if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
+    skv::launch_scan_text(dt, static_cast<uint32_t>(len), c->rules_dev, dm, s);
+    CK(cudaMemcpyAsync(c->host_small, dm, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *mask = c->host_small[0];
+    for (void* p : tmp) cudaFree(p);
+    return SKV_OK;
+  });
+}
+
+int skv_token_seq_digest(skv_ctx* c, const uint32_t* tokens, size_t n, uint64_t* digest) {
+  if (!c || (!tokens && n) || !digest) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    std::vector<void*> tmp;
+    uint32_t* dt = dalloc<uint32_t>(n + 1, tmp);
+    uint64_t* dd = dalloc<uint64_t>(1, tmp);
+    cudaStream_t s = c->stream;
+    if (n) CK(cudaMemcpyAsync(dt, tokens, n * 4, cudaMemcpyHostToDevice, s));
+    skv::launch_digest(dt, static_cast<uint32_t>(n), dd, s);
+    CK(cudaMemcpyAsync(c->host_small, dd, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(digest, c->host_small, 8);
+    for (void* p : tmp) cudaFree(p);
+    return SKV_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// ctx.hpp -- internal device-side layout shared by capi.cpp and kernels.cu.
+//
+// HBM layout of the flattened privacy-aware index (replaces the pointer radix tree of
+// reference cache_index.hpp:65-98,127-836):
+//   rec[cap]    32 B  key (h,d) + creator + parent slot + label/owner/tier/state
+//   stats[cap]  16 B  AccessStats window (hit_cur, u_cnt, hit_pre, u_pre)
+//   aux[cap]    16 B  child list links, user-set handle, candidate stamp
+//   claim[cap]   8 B  intra-batch first-creator arbitration (batch<<32 | ~prompt)
+// Open addressing with linear probing; a slot is empty iff its key is (0,0).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace skv {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr uint32_t kMaxSetUsers = 64;  // AccessStats::kMaxTrackedUsers (access_stats.hpp:15)
+
+struct __align__(32) Rec {
+  uint64_t h, d;      // chained prefix key, block digest
+  uint64_t creator;   // UserId of the first inserter
+  uint32_t parent;    // slot of the previous block's entry, kNone for block 0
+  uint8_t label;      // SensitivityLabel
+  uint8_t owner;      // OwnerClass
+  uint8_t tier;       // MemTier
+  uint8_t state;      // 0 empty/claimed-unwritten, 1 live
+};
+static_assert(sizeof(Rec) == 32, "record must be one 32-B sector");
+
+struct __align__(16) Stats {
+  uint32_t hit_cur, u_cnt, hit_pre, u_pre;
+};
+
+struct __align__(16) Aux {
+  uint32_t first_child, next_sibling;  // subtree walk for label propagation
+  uint32_t set_idx;                    // user-set pool slot for the current window, kNone if untouched
+  uint32_t cand;                       // epoch stamp when this entry was an anomaly candidate
+};
+
+// Device form of the compiled rule DFA.  Entry (s, c) at byte offset s*row_bytes + 4c:
+// bits 0..15 = byte offset of the next state's row, bits 16..31 = enabled-rule mask.
+struct DevRules {
+  uint32_t* table = nullptr;  // n_states * (n_classes + 1) entries
+  uint8_t* class4 = nullptr;  // [256] byte -> 4 * class
+  uint32_t table_bytes = 0;
+  uint32_t start_row = 0;
+  uint32_t eos4 = 0;          // 4 * n_classes
+  uint32_t n_enabled = 0;
+};
+
+struct HashScanArgs {
+  const uint32_t* tokens;
+  const uint64_t* tok_off;
+  const uint32_t* blk_off;
+  uint32_t n_prompts;
+  uint64_t n_tokens;
+  uint32_t n_blocks;
+  uint32_t B, W;
+  uint64_t digest_init;  // FNV state after update_u32(B)
+  DevRules rules;
+  uint64_t* d_out;
+  uint32_t* mask_out;
+  uint32_t* first_sens;
+};
+
+struct Index {
+  Rec* rec = nullptr;
+  Stats* stats = nullptr;
+  Aux* aux = nullptr;
+  unsigned long long* claim = nullptr;
+  uint64_t cap = 0, mask = 0;
+};
+
+// kernel launchers (kernels.cu)
+void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, cudaStream_t s);
+size_t scan_temp_bytes(uint32_t n);
+void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint32_t n,
+                           cudaStream_t s);
+int hash_scan_grid(int device, uint32_t smem_bytes);
+uint32_t hash_scan_smem(const DevRules& r, uint32_t B, uint32_t W);
+void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s);
+void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n_prompts,
+                  uint64_t* h, uint8_t* label, cudaStream_t s);
+void launch_probe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                  const uint64_t* users, uint32_t n_prompts, uint8_t* decision, uint32_t* slot,
+                  uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s);
+void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
+                          const uint32_t* acc_off, uint32_t n_prompts, uint32_t* key, uint32_t* val,
+                          cudaStream_t s);
+size_t sort_temp_bytes(uint32_t n, int bits);
+void launch_sort_pairs(void* temp, size_t temp_bytes, uint32_t* key_in, uint32_t* key_out, uint32_t* val_in,
+                       uint32_t* val_out, uint32_t n, int bits, cudaStream_t s);
+size_t rle_temp_bytes(uint32_t n);
+void launch_rle(void* temp, size_t temp_bytes, const uint32_t* keys, uint32_t* unique, uint32_t* counts,
+                uint32_t* n_runs, uint32_t n, cudaStream_t s);
+void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* counts, const uint32_t* starts,
+                   const uint32_t* n_runs, const uint32_t* vals, const uint64_t* users,
+                   unsigned long long* sets, uint32_t* set_size, uint32_t pool_cap, uint32_t* pool_count,
+                   uint32_t* touched, uint32_t* n_touched, uint32_t* err_flag, int grid, cudaStream_t s);
+void launch_claim(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                  const uint32_t* exist, uint32_t n_prompts, uint32_t batch, uint32_t* slot, uint32_t* err_flag,
+                  cudaStream_t s);
+void launch_commit(const Index& ix, const uint32_t* blk_off, const uint32_t* exist, const uint8_t* label,
+                   const uint64_t* users, const uint8_t* owners, uint32_t n_prompts, uint32_t batch,
+                   const uint32_t* slot, unsigned long long* n_new, cudaStream_t s);
+void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
+                             int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
+                             uint32_t* n_cands, cudaStream_t s);
+void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n_cands, uint32_t grid_n,
+                       uint32_t stamp, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
+                       cudaStream_t s);
+void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
+                            cudaStream_t s);
+void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
+                       cudaStream_t s);
+void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n,
+                      cudaStream_t s);
+void launch_export(const Index& ix, void* out, uint32_t* n_out, cudaStream_t s);
+void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
+void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
+uint32_t record_grid(int device);
+
+}  // namespace skv

@@ -1,0 +1,840 @@
+// kernels.cu -- sm_100a kernels of the SafeKV admission hot path.
+//
+// Stage map (reference symbols they replace, proj/include/safekv/...):
+//   k_hash_scan   token_seq_digest (core.hpp:68-73) + CompiledRuleSet::scan
+//                 (detection.hpp:148-170) on every block window
+//   k_chain       Fnv1a64 chained prefix key (util.hpp:58-81, A.2) + inherited label (A.4)
+//   k_probe       RadixCacheIndex::match_prefix / visible / lowest_tier
+//                 (cache_index.hpp:213-237, 483-485) over the flat index (A.5)
+//   k_record      AccessStats::record (access_stats.hpp:27-37) -- exact, order-preserving
+//   k_claim/k_commit  RadixCacheIndex::insert first-creator-wins + resolve_block (A.7)
+//   k_epoch_*     EntropyMonitor::epoch_pass / check_anomaly (monitor.hpp:56-99),
+//                 set_label propagation (cache_index.hpp:654-685), AccessStats::roll
+// No tensor cores: nothing here is a contraction.  Everything is integer/byte work
+// bounded by HBM, shared-memory lookups or memory latency.
+#include <cub/cub.cuh>
+
+#include "../../include/safekv_b200.h"
+#include "ctx.hpp"
+
+namespace skv {
+namespace {
+
+constexpr uint64_t kFnvOff = 0xcbf29ce484222325ULL;
+constexpr uint64_t kFnvP = 0x100000001b3ULL;
+constexpr uint64_t kFnvP4 = kFnvP * kFnvP * kFnvP * kFnvP;  // (h^t)*P^4 == update_u32(t) for t < 256
+
+__device__ __forceinline__ uint64_t fnv_byte(uint64_t h, uint32_t b) { return (h ^ b) * kFnvP; }
+__device__ __forceinline__ uint64_t fnv_u32(uint64_t h, uint32_t v) {
+  h = fnv_byte(h, v & 0xff);
+  h = fnv_byte(h, (v >> 8) & 0xff);
+  h = fnv_byte(h, (v >> 16) & 0xff);
+  return fnv_byte(h, v >> 24);
+}
+__device__ __forceinline__ uint64_t fnv_u64(uint64_t h, uint64_t v) {
+  h = fnv_u32(h, static_cast<uint32_t>(v));
+  return fnv_u32(h, static_cast<uint32_t>(v >> 32));
+}
+// A.2: h_b = FNV(u64 h_{b-1} || u64 d_b), h_{-1} = 0
+__device__ __forceinline__ uint64_t chain_key(uint64_t prev, uint64_t d) {
+  return fnv_u64(fnv_u64(kFnvOff, prev), d);
+}
+
+__device__ __forceinline__ uint64_t slot_hash(uint64_t h, uint64_t d) {
+  uint64_t x = h ^ (d * 0x9e3779b97f4a7c15ULL);
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint4 ldg_stream(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------------------------
+// K0: blocks per prompt
+// ---------------------------------------------------------------------------------
+__global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uint32_t B, uint32_t* counts) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) counts[p] = static_cast<uint32_t>((off[p + 1] - off[p]) / B);
+  if (p == n) counts[p] = 0;
+}
+
+// ---------------------------------------------------------------------------------
+// K12: fused block digest + rule-DFA window scan.
+//
+// Persistent CTAs; CTA i owns global blocks [i*nb/G, (i+1)*nb/G).  Each iteration takes
+// a chunk of up to kHSThreads consecutive blocks (may span prompts), stages the chunk's
+// token span [first window start, last window end) HBM -> SMEM once with coalesced
+// 128-bit streaming loads (each token read from HBM exactly once), converting every
+// token to its pre-scaled DFA byte class and its raw byte.  Thread t then hashes
+// block t from the SMEM raw bytes and runs the SMEM-resident DFA over its window
+// (block + W right-context tokens, clipped at the prompt end) -- the window overlap
+// is served from SMEM, not HBM.
+// ---------------------------------------------------------------------------------
+constexpr int kHSThreads = 256;
+constexpr int kSoEntries = kHSThreads + 1;
+
+__host__ __device__ inline uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+__host__ __device__ inline uint32_t stage_bytes(uint32_t B, uint32_t W) {
+  return round16(kHSThreads * B + W + 16);
+}
+
+__device__ __forceinline__ uint32_t lds_u32(const uint8_t* base, uint32_t byte_off) {
+  return *reinterpret_cast<const uint32_t*>(base + byte_off);
+}
+
+__device__ __forceinline__ uint32_t dfa_window(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
+                                               uint32_t o, uint32_t end, uint32_t row, uint32_t eos4) {
+  uint32_t acc = 0;
+  while (o < end && (o & 3)) {
+    uint32_t e = lds_u32(tab, row + cls[o]);
+    acc |= e;
+    row = e & 0xffffu;
+    ++o;
+  }
+  for (; o + 4 <= end; o += 4) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t e = lds_u32(tab, row + ((w >> (8 * k)) & 0xffu));
+      acc |= e;
+      row = e & 0xffffu;
+    }
+  }
+  for (; o < end; ++o) {
+    uint32_t e = lds_u32(tab, row + cls[o]);
+    acc |= e;
+    row = e & 0xffffu;
+  }
+  acc |= lds_u32(tab, row + eos4);
+  return acc >> 16;
+}
+
+__device__ __forceinline__ uint64_t digest_bytes(const uint8_t* __restrict__ raw, uint32_t o, uint32_t n,
+                                                 uint64_t h) {
+  uint32_t end = o + n;
+  while (o < end && (o & 3)) h = (h ^ raw[o++]) * kFnvP4;
+  for (; o + 4 <= end; o += 4) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(raw + o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h = (h ^ ((w >> (8 * k)) & 0xffu)) * kFnvP4;
+  }
+  for (; o < end; ++o) h = (h ^ raw[o]) * kFnvP4;
+  return h;
+}
+
+// index of the last element <= x in so[0..n) (so[0] <= x guaranteed)
+__device__ __forceinline__ uint32_t so_search(const uint32_t* so, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;  // invariant so[lo] <= x, so[hi] > x (virtual)
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (so[mid] <= x)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t tb = round16(a.rules.table_bytes);
+  uint8_t* tab = sm;
+  uint8_t* cmap = sm + tb;
+  uint32_t* so = reinterpret_cast<uint32_t*>(cmap + 256);
+  uint8_t* cls = reinterpret_cast<uint8_t*>(so) + round16(kSoEntries * 4);
+  const uint32_t stage = stage_bytes(a.B, a.W);
+  uint8_t* raw = cls + stage;
+  __shared__ uint32_t s_pp;
+
+  const uint32_t tid = threadIdx.x;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.rules.table);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (uint32_t i = tid; i < tb / 16; i += blockDim.x) dst[i] = src[i];
+    if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class4)[tid];
+  }
+  const uint32_t nb = a.n_blocks;
+  const uint32_t G0 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * nb) / gridDim.x);
+  const uint32_t G1 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x + 1) * nb) / gridDim.x);
+  if (tid == 0 && G0 < G1) {
+    // prompt containing G0: last p with blk_off[p] <= G0 and blk_off[p+1] > G0
+    uint32_t lo = 0, hi = a.n_prompts;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (a.blk_off[mid] <= G0)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    while (a.blk_off[lo + 1] <= G0) ++lo;  // skip empty prompts
+    s_pp = lo;
+  }
+  __syncthreads();
+  if (G0 >= G1) return;
+  uint32_t pp = s_pp;
+  uint32_t g = G0;
+  const uint32_t B = a.B, W = a.W;
+  while (g < G1) {
+    for (uint32_t t = tid; t < kSoEntries; t += blockDim.x)
+      so[t] = a.blk_off[min(pp + t, a.n_prompts)];
+    __syncthreads();
+    uint32_t nw = min(static_cast<uint32_t>(kHSThreads), G1 - g);
+    uint32_t n_so = kSoEntries;
+    if (pp + kHSThreads <= a.n_prompts) {
+      nw = min(nw, so[kHSThreads] - g);
+    } else {
+      n_so = a.n_prompts - pp + 1;
+    }
+    uint32_t lastg = g + nw - 1;
+    uint32_t il = so_search(so, n_so, lastg);
+    uint64_t s_tok = a.tok_off[pp] + static_cast<uint64_t>(g - so[0]) * B;
+    uint64_t e_tok = min(a.tok_off[pp + il + 1],
+                         a.tok_off[pp + il] + static_cast<uint64_t>(lastg - so[il] + 1) * B + W);
+    uint64_t as = s_tok & ~3ull;
+    if (e_tok - as > stage - 8) {  // too many prompt tails in the span: single-prompt chunk
+      nw = min(nw, so[1] - g);
+      lastg = g + nw - 1;
+      il = 0;
+      e_tok = min(a.tok_off[pp + 1], a.tok_off[pp] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
+    }
+    // ---- stage tokens -> (class*4, raw byte), 4 tokens per 128-bit load
+    const uint32_t span = static_cast<uint32_t>(e_tok - as);
+    const uint32_t nq = (span + 3) >> 2;
+    uint32_t wide = 0;
+    for (uint32_t q = tid; q < nq; q += blockDim.x) {
+      uint64_t gi = as + 4ull * q;
+      uint32_t t0, t1, t2, t3;
+      if (gi + 4 <= a.n_tokens) {
+        uint4 v = ldg_stream(a.tokens + gi);
+        t0 = v.x, t1 = v.y, t2 = v.z, t3 = v.w;
+      } else {
+        t0 = gi < a.n_tokens ? a.tokens[gi] : 0;
+        t1 = gi + 1 < a.n_tokens ? a.tokens[gi + 1] : 0;
+        t2 = gi + 2 < a.n_tokens ? a.tokens[gi + 2] : 0;
+        t3 = 0;
+      }
+      wide |= (t0 | t1 | t2 | t3) >> 8;
+      uint32_t c = cmap[t0 & 0xff] | (cmap[t1 & 0xff] << 8) | (cmap[t2 & 0xff] << 16) | (cmap[t3 & 0xff] << 24);
+      uint32_t r = (t0 & 0xff) | ((t1 & 0xff) << 8) | ((t2 & 0xff) << 16) | ((t3 & 0xff) << 24);
+      reinterpret_cast<uint32_t*>(cls)[q] = c;
+      reinterpret_cast<uint32_t*>(raw)[q] = r;
+    }
+    wide = __syncthreads_or(wide != 0);
+    if (tid < nw) {
+      uint32_t gb = g + tid;
+      uint32_t i = so_search(so, il + 1, gb);
+      uint32_t p = pp + i;
+      uint32_t b = gb - so[i];
+      uint64_t base = a.tok_off[p];
+      uint64_t L = a.tok_off[p + 1] - base;
+      uint32_t ws = static_cast<uint32_t>(base + static_cast<uint64_t>(b) * B - as);
+      uint64_t wend = min(L, static_cast<uint64_t>(b) * B + B + W);
+      uint32_t we = static_cast<uint32_t>(base + wend - as);
+      uint64_t dg;
+      if (!wide) {
+        dg = digest_bytes(raw, ws, B, a.digest_init);
+      } else {  // some token >= 256 in this chunk: full update_u32 per token
+        dg = a.digest_init;
+        const uint32_t* tp = a.tokens + base + static_cast<uint64_t>(b) * B;
+        for (uint32_t k = 0; k < B; ++k) dg = fnv_u32(dg, tp[k]);
+      }
+      uint32_t mask = dfa_window(tab, cls, ws, we, a.rules.start_row, a.rules.eos4);
+      a.d_out[gb] = dg;
+      a.mask_out[gb] = mask;
+      if (mask) atomicMin(&a.first_sens[p], b);
+    }
+    g += nw;
+    if (tid == 0) {
+      uint32_t np = pp + il;
+      while (np < a.n_prompts && a.blk_off[np + 1] <= g) ++np;
+      s_pp = np;
+    }
+    __syncthreads();
+    pp = s_pp;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K3a: chained prefix keys + inherited labels, one lane per prompt (the FNV chain is
+// serial along a prompt, so SIMD runs across prompts).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_chain(const uint64_t* __restrict__ d, const uint32_t* __restrict__ blk_off,
+                                               const uint32_t* __restrict__ first_sens, uint32_t n_prompts,
+                                               uint64_t* __restrict__ h_out, uint8_t* __restrict__ label) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_prompts) return;
+  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, fs = first_sens[p];
+  uint64_t h = 0;
+#pragma unroll 4
+  for (uint32_t b = 0; b < n; ++b) {
+    h = chain_key(h, d[bo + b]);
+    h_out[bo + b] = h;
+    label[bo + b] = b >= fs ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K3b: warp-cooperative index probe, one warp per prompt; 32 lanes probe 32
+// consecutive block keys; ballots give the first invisible (match length m) and the
+// first missing block (k, where the commit starts).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, Rec* out) {
+  uint64_t s = slot_hash(h, d) & ix.mask;
+  for (uint64_t i = 0; i <= ix.mask; ++i) {
+    const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(ix.rec + s);
+    ulonglong2 k = rp[0];
+    if (k.x == h && k.y == d) {
+      ulonglong2 m = rp[1];
+      out->h = h;
+      out->d = d;
+      out->creator = m.x;
+      out->parent = static_cast<uint32_t>(m.y);
+      out->label = static_cast<uint8_t>(m.y >> 32);
+      out->owner = static_cast<uint8_t>(m.y >> 40);
+      out->tier = static_cast<uint8_t>(m.y >> 48);
+      out->state = static_cast<uint8_t>(m.y >> 56);
+      return static_cast<uint32_t>(s);
+    }
+    if (k.x == 0 && k.y == 0) return kNone;
+    s = (s + 1) & ix.mask;
+  }
+  return kNone;
+}
+
+__global__ void __launch_bounds__(256) k_probe(Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
+                                               const uint32_t* __restrict__ blk_off, const uint64_t* __restrict__ users,
+                                               uint32_t n_prompts, uint8_t* __restrict__ decision,
+                                               uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched,
+                                               uint32_t* __restrict__ exist, uint8_t* __restrict__ tier) {
+  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t lane = lane_id();
+  if (p >= n_prompts) return;
+  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  uint64_t user = users[p];
+  uint32_t m = n, k = n, tmax = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    uint32_t b = base + lane;
+    bool act = b < n, found = false, vis = false;
+    uint32_t slot = kNone;
+    Rec r{};
+    if (act) {
+      slot = find_slot(ix, hk[bo + b], dk[bo + b], &r);
+      found = slot != kNone;
+      vis = found && (r.label == SKV_LABEL_PUBLIC || r.creator == user);
+    }
+    uint32_t nf = __ballot_sync(0xffffffffu, act && !found);
+    uint32_t nv = __ballot_sync(0xffffffffu, act && !vis);
+    if (m == n && nv) m = base + __ffs(nv) - 1;
+    if (k == n && nf) k = base + __ffs(nf) - 1;
+    if (act) {
+      if (b < m) {
+        decision[bo + b] = r.label == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
+        tmax = max(tmax, static_cast<uint32_t>(r.tier));
+      }
+      if (b < k) slot_out[bo + b] = slot;
+    }
+    if (k != n) break;
+  }
+  tmax = __reduce_max_sync(0xffffffffu, tmax);
+  if (lane == 0) {
+    matched[p] = m;
+    exist[p] = k;
+    tier[p] = static_cast<uint8_t>(tmax);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K4: monitor record.  Accesses (slot, prompt) are emitted in prompt order, stably
+// radix-sorted by slot, run-length encoded; one warp replays each entry's accesses in
+// global order with the tracked user set (<= 64) in registers, reproducing the
+// order-dependent saturating count of AccessStats::record exactly.
+// ---------------------------------------------------------------------------------
+__global__ void k_emit_accesses(const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                                const uint32_t* __restrict__ matched, const uint32_t* __restrict__ acc_off,
+                                uint32_t n_prompts, uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  uint32_t bo = blk_off[p], m = matched[p], ao = acc_off[p];
+  for (uint32_t b = lane_id(); b < m; b += 32) {
+    key[ao + b] = slot[bo + b];
+    val[ao + b] = p;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_record(Index ix, const uint32_t* __restrict__ unique,
+                                                const uint32_t* __restrict__ counts,
+                                                const uint32_t* __restrict__ starts,
+                                                const uint32_t* __restrict__ n_runs_p,
+                                                const uint32_t* __restrict__ vals, const uint64_t* __restrict__ users,
+                                                unsigned long long* __restrict__ sets, uint32_t* __restrict__ set_size,
+                                                uint32_t pool_cap, uint32_t* pool_count, uint32_t* touched,
+                                                uint32_t* n_touched, uint32_t* err_flag) {
+  const uint32_t lane = lane_id();
+  const uint32_t n_runs = *n_runs_p;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_runs; r += nwarps) {
+    const uint32_t slot = unique[r], cnt = counts[r], start = starts[r];
+    uint32_t si = 0;
+    if (lane == 0) {
+      si = ix.aux[slot].set_idx;
+      if (si == kNone) {
+        si = atomicAdd(pool_count, 1u);
+        if (si >= pool_cap) {
+          atomicOr(err_flag, 1u);
+        } else {
+          ix.aux[slot].set_idx = si;
+          set_size[si] = 0;
+          touched[atomicAdd(n_touched, 1u)] = slot;
+        }
+      }
+    }
+    si = __shfl_sync(0xffffffffu, si, 0);
+    if (si >= pool_cap) continue;
+    unsigned long long* set = sets + static_cast<uint64_t>(si) * kMaxSetUsers;
+    uint32_t size = set_size[si];
+    unsigned long long m0 = lane < size ? set[lane] : 0ull;
+    unsigned long long m1 = lane + 32 < size ? set[lane + 32] : 0ull;
+    const uint32_t size0 = size;
+    uint32_t add_total = 0;
+    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+      uint32_t i = c0 + lane;
+      bool valid = i < cnt;
+      unsigned long long u = valid ? users[vals[start + i]] : 0ull;
+      bool member = false;
+      for (uint32_t j = 0; j < size; ++j) {
+        unsigned long long mj = __shfl_sync(0xffffffffu, j < 32 ? m0 : m1, j & 31);
+        member |= (mj == u);
+      }
+      bool nonmem = valid && !member;
+      uint32_t nm_mask = __ballot_sync(0xffffffffu, nonmem);
+      uint32_t peers = __match_any_sync(0xffffffffu, u) & nm_mask;
+      uint32_t leader = nonmem ? static_cast<uint32_t>(__ffs(peers) - 1) : 0u;
+      bool is_leader = nonmem && leader == lane;
+      uint32_t leaders = __ballot_sync(0xffffffffu, is_leader);
+      uint32_t room = kMaxSetUsers - size;
+      uint32_t lrank = __popc(leaders & ((1u << leader) - 1u));
+      bool admitted = nonmem && lrank < room;
+      add_total += nonmem ? (admitted ? (is_leader ? 1u : 0u) : 1u) : 0u;
+      uint32_t adm = __ballot_sync(0xffffffffu, is_leader && admitted);
+      uint32_t pos = size;
+      while (adm) {
+        uint32_t ll = __ffs(adm) - 1;
+        adm &= adm - 1;
+        unsigned long long v = __shfl_sync(0xffffffffu, u, ll);
+        if (lane == (pos & 31)) {
+          if (pos < 32)
+            m0 = v;
+          else
+            m1 = v;
+        }
+        ++pos;
+      }
+      size = pos;
+    }
+    add_total = __reduce_add_sync(0xffffffffu, add_total);
+    if (lane >= size0 && lane < size) set[lane] = m0;
+    if (lane + 32 >= size0 && lane + 32 < size) set[lane + 32] = m1;
+    if (lane == 0) {
+      set_size[si] = size;
+      ix.stats[slot].hit_cur += cnt;
+      ix.stats[slot].u_cnt += add_total;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K6: commit.  k_claim inserts the keys of new blocks (128-bit CAS on the key) and
+// arbitrates intra-batch duplicates with atomicMax(batch<<32 | ~prompt) -> lowest
+// prompt wins; k_commit lets each winner write its record and link it under its parent.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long long cmp_lo, unsigned long long cmp_hi,
+                                       unsigned long long new_lo, unsigned long long new_hi,
+                                       unsigned long long* old_lo, unsigned long long* old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(*old_lo), "=l"(*old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+  return *old_lo == cmp_lo && *old_hi == cmp_hi;
+}
+
+__global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
+                                               const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist,
+                                               uint32_t n_prompts, uint32_t batch, uint32_t* __restrict__ slot_out,
+                                               uint32_t* err_flag) {
+  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  const unsigned long long tag = (static_cast<unsigned long long>(batch) << 32) | (0xffffffffu - p);
+  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
+    uint64_t h = hk[bo + b], d = dk[bo + b];
+    uint64_t s = slot_hash(h, d) & ix.mask;
+    uint64_t i = 0;
+    for (; i <= ix.mask; ++i) {
+      unsigned long long ol, oh;
+      unsigned long long* kp = reinterpret_cast<unsigned long long*>(ix.rec + s);
+      if (cas128(kp, 0ull, 0ull, h, d, &ol, &oh) || (ol == h && oh == d)) break;
+      s = (s + 1) & ix.mask;
+    }
+    if (i > ix.mask) {
+      atomicOr(err_flag, 2u);
+      return;
+    }
+    atomicMax(&ix.claim[s], tag);
+    slot_out[bo + b] = static_cast<uint32_t>(s);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_commit(Index ix, const uint32_t* __restrict__ blk_off,
+                                                const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
+                                                const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
+                                                uint32_t n_prompts, uint32_t batch, const uint32_t* __restrict__ slot,
+                                                unsigned long long* n_new) {
+  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  const unsigned long long tag = (static_cast<unsigned long long>(batch) << 32) | (0xffffffffu - p);
+  uint32_t mine = 0;
+  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
+    uint32_t s = slot[bo + b];
+    if (ix.claim[s] != tag || ix.rec[s].state != 0) continue;
+    uint32_t parent = b > 0 ? slot[bo + b - 1] : kNone;
+    Rec& r = ix.rec[s];
+    r.creator = users[p];
+    r.parent = parent;
+    r.label = label[bo + b];
+    r.owner = owners ? owners[p] : 0;
+    r.tier = SKV_TIER_HBM;
+    r.state = 1;
+    if (parent != kNone) ix.aux[s].next_sibling = atomicExch(&ix.aux[parent].first_child, s);
+    ++mine;
+  }
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  if (lane_id() == 0 && mine) atomicAdd(n_new, static_cast<unsigned long long>(mine));
+}
+
+// ---------------------------------------------------------------------------------
+// K5: monitor epoch (A.6).  Candidates = Public entries whose FP64 predicate holds
+// (monitor.hpp:68-70); a candidate fires iff no ancestor is a candidate (the
+// reference's pre-order pass relabels a fired node's subtree before visiting it);
+// fired nodes relabel their subtree; then every touched window rolls.
+// ---------------------------------------------------------------------------------
+struct DevEvent {
+  uint64_t h, d;
+  uint8_t action, owner, pad[6];
+  double now, prev;
+  uint64_t u_pre, epoch;
+};
+static_assert(sizeof(DevEvent) == sizeof(skv_event), "event layout");
+
+__global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
+                                   int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max,
+                                   uint32_t* __restrict__ cands, uint32_t* __restrict__ n_cands) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_list) return;
+  uint32_t s = list[i];
+  if (only_untouched && ix.aux[s].set_idx != kNone) return;
+  if (ix.rec[s].label != SKV_LABEL_PUBLIC) return;
+  Stats st = ix.stats[s];
+  if (st.hit_pre == 0) return;
+  double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
+  double prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
+  if ((now - prev) >= jump && static_cast<uint64_t>(st.u_pre) <= u_pre_max) {
+    ix.aux[s].cand = stamp;
+    cands[atomicAdd(n_cands, 1u)] = s;
+  }
+}
+
+__global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const uint32_t* __restrict__ n_cands,
+                             uint32_t stamp, uint64_t epoch, DevEvent* __restrict__ events,
+                             uint32_t* __restrict__ n_events, uint32_t* __restrict__ fired) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_cands) return;
+  uint32_t s = cands[i];
+  for (uint32_t a = ix.rec[s].parent; a != kNone; a = ix.rec[a].parent)
+    if (ix.aux[a].cand == stamp) return;
+  Stats st = ix.stats[s];
+  const Rec& r = ix.rec[s];
+  uint32_t e = atomicAdd(n_events, 1u);
+  DevEvent ev;
+  ev.h = r.h;
+  ev.d = r.d;
+  ev.owner = r.owner;
+  ev.action = r.owner == 0 ? SKV_ACTION_DOWNGRADE : SKV_ACTION_RESTRICT;
+  for (int k = 0; k < 6; ++k) ev.pad[k] = 0;
+  ev.now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
+  ev.prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
+  ev.u_pre = st.u_pre;
+  ev.epoch = epoch;
+  events[e] = ev;
+  fired[e] = s;
+}
+
+__global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, const uint32_t* __restrict__ n_fired) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_fired) return;
+  uint32_t root = fired[i];
+  uint8_t lab = ix.rec[root].owner == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+  ix.rec[root].label = lab;
+  uint32_t cur = ix.aux[root].first_child;
+  while (cur != kNone) {
+    ix.rec[cur].label = lab;
+    uint32_t c = ix.aux[cur].first_child;
+    if (c != kNone) {
+      cur = c;
+      continue;
+    }
+    while (cur != root && ix.aux[cur].next_sibling == kNone) cur = ix.rec[cur].parent;
+    if (cur == root) break;
+    cur = ix.aux[cur].next_sibling;
+  }
+}
+
+__global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
+                             int prev_list) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_list) return;
+  uint32_t s = list[i];
+  if (prev_list) {
+    if (ix.aux[s].set_idx != kNone) return;  // rolled by the current-window list
+    Stats z{0, 0, 0, 0};
+    ix.stats[s] = z;
+  } else {
+    Stats st = ix.stats[s];
+    Stats r{0, 0, st.hit_cur, st.u_cnt};
+    ix.stats[s] = r;
+    ix.aux[s].set_idx = kNone;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// misc: tiers, export, per-call wrappers
+// ---------------------------------------------------------------------------------
+__global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Rec r;
+  uint32_t s = find_slot(ix, h[i], d[i], &r);
+  if (s != kNone) ix.rec[s].tier = tiers[i];
+}
+
+__global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
+  uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.rec[s];
+  if (r.h == 0 && r.d == 0) return;
+  Stats st = ix.stats[s];
+  skv_entry e;
+  e.h = r.h;
+  e.d = r.d;
+  e.creator = r.creator;
+  e.label = r.label;
+  e.owner = r.owner;
+  e.tier = r.tier;
+  e.hit_cur = st.hit_cur;
+  e.u_cnt = st.u_cnt;
+  e.hit_pre = st.hit_pre;
+  e.u_pre = st.u_pre;
+  out[atomicAdd(n_out, 1u)] = e;
+}
+
+__global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint8_t* tab = reinterpret_cast<const uint8_t*>(r.table);
+  uint32_t row = r.start_row, acc = 0;
+  for (uint32_t i = 0; i < len; ++i) {
+    uint32_t e = *reinterpret_cast<const uint32_t*>(tab + row + r.class4[text[i]]);
+    acc |= e;
+    row = e & 0xffffu;
+  }
+  acc |= *reinterpret_cast<const uint32_t*>(tab + row + r.eos4);
+  *mask = acc >> 16;
+}
+
+__global__ void k_digest(const uint32_t* t, uint32_t n, uint64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint64_t h = fnv_u32(kFnvOff, n);
+  for (uint32_t i = 0; i < n; ++i) h = fnv_u32(h, t[i]);
+  *out = h;
+}
+
+inline uint32_t cdiv(uint64_t a, uint64_t b) { return static_cast<uint32_t>((a + b - 1) / b); }
+
+}  // namespace
+
+// =================================================================================
+// launchers
+// =================================================================================
+void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, cudaStream_t s) {
+  k_block_counts<<<cdiv(n + 1, 256), 256, 0, s>>>(tok_off, n, B, counts);
+}
+
+size_t scan_temp_bytes(uint32_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), n);
+  return bytes;
+}
+
+void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint32_t n,
+                           cudaStream_t s) {
+  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, n, s);
+}
+
+uint32_t hash_scan_smem(const DevRules& r, uint32_t B, uint32_t W) {
+  return round16(r.table_bytes) + 256 + round16(kSoEntries * 4) + 2 * stage_bytes(B, W);
+}
+
+int hash_scan_grid(int device, uint32_t smem) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_hash_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, kHSThreads, smem);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * sms;
+}
+
+void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s) {
+  if (a.n_blocks == 0) return;
+  uint32_t g = std::min<uint32_t>(grid, a.n_blocks);
+  k_hash_scan<<<g, kHSThreads, smem, s>>>(a);
+}
+
+void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n, uint64_t* h,
+                  uint8_t* label, cudaStream_t s) {
+  if (n) k_chain<<<cdiv(n, 128), 128, 0, s>>>(d, blk_off, first_sens, n, h, label);
+}
+
+void launch_probe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                  const uint64_t* users, uint32_t n, uint8_t* decision, uint32_t* slot, uint32_t* matched,
+                  uint32_t* exist, uint8_t* tier, cudaStream_t s) {
+  if (n) k_probe<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, users, n, decision, slot,
+                                                                          matched, exist, tier);
+}
+
+void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
+                          const uint32_t* acc_off, uint32_t n, uint32_t* key, uint32_t* val, cudaStream_t s) {
+  if (n)
+    k_emit_accesses<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(slot, blk_off, matched, acc_off, n, key,
+                                                                            val);
+}
+
+size_t sort_temp_bytes(uint32_t n, int bits) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), n, 0, bits);
+  return bytes;
+}
+
+void launch_sort_pairs(void* temp, size_t temp_bytes, uint32_t* key_in, uint32_t* key_out, uint32_t* val_in,
+                       uint32_t* val_out, uint32_t n, int bits, cudaStream_t s) {
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_in, key_out, val_in, val_out, n, 0, bits, s);
+}
+
+size_t rle_temp_bytes(uint32_t n) {
+  size_t bytes = 0;
+  cub::DeviceRunLengthEncode::Encode(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                     static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                     static_cast<uint32_t*>(nullptr), n);
+  return bytes;
+}
+
+void launch_rle(void* temp, size_t temp_bytes, const uint32_t* keys, uint32_t* unique, uint32_t* counts,
+                uint32_t* n_runs, uint32_t n, cudaStream_t s) {
+  cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, keys, unique, counts, n_runs, n, s);
+}
+
+uint32_t record_grid(int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return static_cast<uint32_t>(sms) * 8;
+}
+
+void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* counts, const uint32_t* starts,
+                   const uint32_t* n_runs, const uint32_t* vals, const uint64_t* users, unsigned long long* sets,
+                   uint32_t* set_size, uint32_t pool_cap, uint32_t* pool_count, uint32_t* touched,
+                   uint32_t* n_touched, uint32_t* err_flag, int grid, cudaStream_t s) {
+  k_record<<<grid, 256, 0, s>>>(ix, unique, counts, starts, n_runs, vals, users, sets, set_size, pool_cap, pool_count,
+                                touched, n_touched, err_flag);
+}
+
+void launch_claim(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                  const uint32_t* exist, uint32_t n, uint32_t batch, uint32_t* slot, uint32_t* err_flag,
+                  cudaStream_t s) {
+  if (n) k_claim<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, n, batch, slot,
+                                                                         err_flag);
+}
+
+void launch_commit(const Index& ix, const uint32_t* blk_off, const uint32_t* exist, const uint8_t* label,
+                   const uint64_t* users, const uint8_t* owners, uint32_t n, uint32_t batch, const uint32_t* slot,
+                   unsigned long long* n_new, cudaStream_t s) {
+  if (n)
+    k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, blk_off, exist, label, users, owners, n,
+                                                                      batch, slot, n_new);
+}
+
+void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
+                             int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
+                             uint32_t* n_cands, cudaStream_t s) {
+  if (grid_n)
+    k_epoch_candidates<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, only_untouched, stamp, jump, u_pre_max,
+                                                          cands, n_cands);
+}
+
+void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n_cands, uint32_t grid_n,
+                       uint32_t stamp, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
+                       cudaStream_t s) {
+  if (grid_n)
+    k_epoch_fire<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, cands, n_cands, stamp, epoch, static_cast<DevEvent*>(events),
+                                                    n_events, fired);
+}
+
+void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
+                            cudaStream_t s) {
+  if (grid_n) k_epoch_propagate<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, fired, n_events);
+}
+
+void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
+                       cudaStream_t s) {
+  if (grid_n) k_epoch_roll<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, prev_list);
+}
+
+void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n,
+                      cudaStream_t s) {
+  if (n) k_set_tiers<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, tiers, n);
+}
+
+void launch_export(const Index& ix, void* out, uint32_t* n_out, cudaStream_t s) {
+  k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, static_cast<skv_entry*>(out), n_out);
+}
+
+void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s) {
+  k_scan_text<<<1, 32, 0, s>>>(text, len, r, mask);
+}
+
+void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s) {
+  k_digest<<<1, 32, 0, s>>>(tokens, n, out);
+}
+
+}  // namespace skv

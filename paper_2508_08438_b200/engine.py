@@ -1,0 +1,344 @@
+"""Host-side mirror of the reference interface for the admission path.
+
+Python names follow the reference C++ API (``safekv::RuleEngine::tier1_scan``,
+``RadixCacheIndex::match_prefix``, ``EntropyMonitor::epoch_pass`` ...), but every call
+goes through the C ABI into the CUDA library; nothing is computed here beyond argument
+marshalling.  The batch entry points implement the parity contract of SURVEY.md
+Appendix A (phases L / C / E).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import native as N
+
+
+def _ptr(a: Optional[np.ndarray]) -> Optional[int]:
+    return None if a is None else a.ctypes.data
+
+
+class RuleSet:
+    """Immutable compiled rule snapshot (reference ``CompiledRuleSet``, detection.hpp:118-181)."""
+
+    def __init__(self, handle: int):
+        self._lib = N.load_library()
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def default(cls) -> "RuleSet":
+        lib = N.load_library()
+        h = C.c_void_p()
+        N.raise_for(lib.skv_rules_default(C.byref(h)), "default rules")
+        return cls(h.value)
+
+    @classmethod
+    def from_json(cls, text: str | bytes) -> "RuleSet":
+        """``RuleEngine::load_rules_json`` (detection.hpp:222-242): ParseError / CompileError."""
+        lib = N.load_library()
+        raw = text.encode() if isinstance(text, str) else text
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = lib.skv_rules_from_json(raw, len(raw), C.byref(h), err, len(err))
+        N.raise_for(rc, err.value.decode(errors="replace"))
+        return cls(h.value)
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._lib.skv_rules_free(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def version(self) -> int:
+        return int(self._lib.skv_rules_version(self._h))
+
+    def size(self) -> int:
+        return int(self._lib.skv_rules_count(self._h))
+
+    def rules(self) -> list[dict]:
+        out = []
+        for i in range(self.size()):
+            rid, cat = C.c_char_p(), C.c_char_p()
+            kind, en = C.c_int(), C.c_int()
+            N.raise_for(self._lib.skv_rules_info(self._h, i, C.byref(rid), C.byref(cat), C.byref(kind),
+                                                 C.byref(en)), "rules_info")
+            out.append({"rule_id": rid.value.decode(), "category": cat.value.decode(),
+                        "kind": "blacklist" if kind.value else "regex", "enabled": bool(en.value)})
+        return out
+
+    def warnings(self) -> list[str]:
+        n = self._lib.skv_rules_warning_count(self._h)
+        return [self._lib.skv_rules_warning(self._h, i).decode() for i in range(n)]
+
+    def enabled_rules(self) -> list[int]:
+        n = self._lib.skv_rules_enabled_count(self._h)
+        return [int(self._lib.skv_rules_enabled_rule(self._h, j)) for j in range(n)]
+
+    def to_rule_mask(self, device_mask: int) -> int:
+        """Device mask (bit j = j-th enabled rule) -> mask over rule-list positions."""
+        m = 0
+        for j, r in enumerate(self.enabled_rules()):
+            if device_mask >> j & 1:
+                m |= 1 << r
+        return m
+
+    def categories(self, device_mask: int) -> list[str]:
+        """Ordered, de-duplicated categories exactly as ``CompiledRuleSet::scan`` lists them
+        (rule order of the hit rules, detection.hpp:160-166)."""
+        rules = self.rules()
+        rm = self.to_rule_mask(device_mask)
+        cats: list[str] = []
+        for i, r in enumerate(rules):
+            if rm >> i & 1 and r["category"] not in cats:
+                cats.append(r["category"])
+        return cats
+
+    def dfa(self) -> dict:
+        v = N.DfaView()
+        N.raise_for(self._lib.skv_rules_dfa(self._h, C.byref(v)), "dfa")
+        S, Cn = v.n_states, v.n_classes
+        return {
+            "n_states": S, "n_classes": Cn, "start": v.start,
+            "class_map": np.ctypeslib.as_array(v.class_map, shape=(256,)).copy(),
+            "next": np.ctypeslib.as_array(v.next, shape=(S * Cn,)).reshape(S, Cn).copy(),
+            "acc": np.ctypeslib.as_array(v.acc, shape=(S * (Cn + 1),)).reshape(S, Cn + 1).copy(),
+            "nfa_states": v.nfa_states, "dfa_states_unminimized": v.dfa_states_unminimized,
+        }
+
+
+@dataclass
+class AdmitResult:
+    block_offsets: np.ndarray   # n_prompts + 1 (uint32)
+    block_h: np.ndarray         # uint64 per block
+    block_d: np.ndarray
+    label: np.ndarray           # uint8 per block (0 Private, 1 Public)
+    rule_mask: np.ndarray       # uint32 per block (bit j = j-th enabled rule)
+    decision: np.ndarray        # uint8 per block (0 miss, 1 public hit, 2 owner hit)
+    matched_blocks: np.ndarray  # uint32 per prompt
+    lowest_tier: np.ndarray     # uint8 per prompt
+    n_blocks: int = 0
+    matched_total: int = 0
+
+
+@dataclass
+class AnomalyEvent:
+    h: int
+    d: int
+    action: int
+    owner: int
+    entropy_now: float
+    entropy_prev: float
+    u_pre: int
+    epoch: int
+
+
+@dataclass
+class EngineConfig:
+    block_tokens: int = 16
+    window_tokens: int = 32
+    index_capacity: int = 1 << 20
+    max_prompts: int = 1 << 16
+    max_tokens: int = 1 << 24
+    max_window_entries: int = 1 << 18
+    entropy_jump: float = 0.3
+    u_pre_max: int = 1
+    device: int = 0
+
+
+class AdmissionEngine:
+    """Device-resident SafeKV admission context (index + monitor + rule DFA)."""
+
+    def __init__(self, cfg: EngineConfig | None = None, **kw):
+        self.cfg = cfg or EngineConfig(**kw)
+        self._lib = N.load_library()
+        c = N.Config()
+        self._lib.skv_config_default(C.byref(c))
+        for f, _ in N.Config._fields_:
+            setattr(c, f, getattr(self.cfg, f))
+        h = C.c_void_p()
+        rc = self._lib.skv_create(C.byref(c), C.byref(h))
+        if rc != N.SKV_OK:
+            N.raise_for(rc, self._lib.skv_last_error(None).decode())
+        self._h = h
+        self.rules = RuleSet.default()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.skv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _err(self) -> str:
+        return self._lib.skv_last_error(self._h).decode(errors="replace")
+
+    def _check(self, rc: int):
+        N.raise_for(rc, self._err())
+
+    @property
+    def stream(self) -> int:
+        return int(self._lib.skv_stream(self._h) or 0)
+
+    def set_rules(self, rs: RuleSet):
+        self._check(self._lib.skv_set_rules(self._h, rs.handle))
+        self.rules = rs
+
+    # --------------------------------------------------------------- phase L
+    def admit(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,
+              owners: Optional[np.ndarray] = None) -> AdmitResult:
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        users = np.ascontiguousarray(users, dtype=np.uint64)
+        if owners is not None:
+            owners = np.ascontiguousarray(owners, dtype=np.uint8)
+        n = len(offsets) - 1
+        B = self.cfg.block_tokens
+        nb = int(((offsets[1:] - offsets[:-1]) // B).sum()) if n > 0 else 0
+        res = AdmitResult(
+            block_offsets=np.zeros(n + 1, np.uint32), block_h=np.zeros(nb, np.uint64),
+            block_d=np.zeros(nb, np.uint64), label=np.zeros(nb, np.uint8), rule_mask=np.zeros(nb, np.uint32),
+            decision=np.zeros(nb, np.uint8), matched_blocks=np.zeros(n, np.uint32),
+            lowest_tier=np.zeros(n, np.uint8))
+        b = N.Batch(_ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), n, len(tokens), 0)
+        o = N.AdmitOut(_ptr(res.block_h), _ptr(res.block_d), _ptr(res.label), _ptr(res.rule_mask),
+                       _ptr(res.decision), _ptr(res.matched_blocks), _ptr(res.lowest_tier),
+                       _ptr(res.block_offsets), 0, 0, 0)
+        self._check(self._lib.skv_admit(self._h, C.byref(b), C.byref(o)))
+        res.n_blocks, res.matched_total = int(o.n_blocks), int(o.matched_total)
+        return res
+
+    def admit_raw(self, batch: N.Batch, out: Optional[N.AdmitOut] = None) -> None:
+        """Zero-copy entry point: device (or host) pointers supplied by the caller."""
+        self._check(self._lib.skv_admit(self._h, C.byref(batch), C.byref(out) if out is not None else None))
+
+    # --------------------------------------------------------------- phase C
+    def commit(self) -> int:
+        n = C.c_uint64()
+        self._check(self._lib.skv_commit(self._h, C.byref(n)))
+        return int(n.value)
+
+    # --------------------------------------------------------------- phase E
+    def epoch_pass(self, cap: int = 1 << 16) -> tuple[int, list[AnomalyEvent]]:
+        """advance_epoch + ``EntropyMonitor::epoch_pass`` (monitor.hpp:85-99): returns the
+        epoch number and the fired events sorted by entry key."""
+        buf = (N.Event * cap)()
+        n = C.c_size_t()
+        ep = C.c_uint64()
+        self._check(self._lib.skv_epoch(self._h, buf, cap, C.byref(n), C.byref(ep)))
+        evs = [AnomalyEvent(e.h, e.d, e.action, e.owner, e.entropy_now, e.entropy_prev, e.u_pre, e.epoch)
+               for e in buf[:min(cap, n.value)]]
+        if n.value > cap:
+            raise N.CapacityExhausted(f"{n.value} events > buffer {cap}")
+        return int(ep.value), evs
+
+    # --------------------------------------------------------------- misc
+    def set_tiers(self, h: np.ndarray, d: np.ndarray, tiers: np.ndarray):
+        h = np.ascontiguousarray(h, np.uint64)
+        d = np.ascontiguousarray(d, np.uint64)
+        tiers = np.ascontiguousarray(tiers, np.uint8)
+        self._check(self._lib.skv_set_tiers(self._h, _ptr(h), _ptr(d), _ptr(tiers), len(h)))
+
+    def export(self) -> np.ndarray:
+        cnt = int(self._lib.skv_entry_count(self._h))
+        cap = max(cnt, 1)
+        buf = (N.Entry * cap)()
+        n = C.c_size_t()
+        self._check(self._lib.skv_export(self._h, buf, cap, C.byref(n)))
+        dt = np.dtype([("h", "<u8"), ("d", "<u8"), ("creator", "<u8"), ("label", "u1"), ("owner", "u1"),
+                       ("tier", "u1"), ("hit_cur", "<u8"), ("u_cnt", "<u8"), ("hit_pre", "<u8"),
+                       ("u_pre", "<u8")], align=True)
+        assert dt.itemsize == C.sizeof(N.Entry)
+        arr = np.frombuffer(bytes(buf), dtype=dt, count=min(n.value, cap)).copy()
+        arr.sort(order=["h", "d"])
+        return arr
+
+    def entry_count(self) -> int:
+        return int(self._lib.skv_entry_count(self._h))
+
+    def times(self) -> dict:
+        t = N.StageTimes()
+        self._check(self._lib.skv_last_times(self._h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in N.StageTimes._fields_}
+
+    def tier1_scan(self, text: str | bytes) -> int:
+        """``RuleEngine::tier1_scan`` (detection.hpp:217) as a batch of one on the device.
+        Returns the device rule mask; ``self.rules.categories(mask)`` gives the verdict's
+        category list and ``mask != 0`` its ``sensitive`` flag."""
+        raw = text.encode("latin-1") if isinstance(text, str) else bytes(text)
+        m = C.c_uint32()
+        self._check(self._lib.skv_tier1_scan(self._h, raw, len(raw), C.byref(m)))
+        return int(m.value)
+
+    def token_seq_digest(self, tokens: Sequence[int]) -> int:
+        """``safekv::token_seq_digest`` (core.hpp:68-73) on the device."""
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+        d = C.c_uint64()
+        self._check(self._lib.skv_token_seq_digest(self._h, _ptr(t), len(t), C.byref(d)))
+        return int(d.value)
+
+
+@dataclass
+class GenSpec:
+    n_prompts: int
+    prompt_tokens: int
+    n_users: int = 64
+    first_user: int = 1
+    pool_size: int = 256
+    pool_tokens: int = 640
+    shared_fraction: float = 1.0
+    pii_per_kib: float = 1.0
+    pii_mix: int = 0
+    seed: int = 1
+    prompt_id_base: int = 0
+
+    def native(self) -> N.GenSpec:
+        return N.GenSpec(self.n_prompts, self.prompt_tokens, self.n_users, self.first_user, self.pool_size,
+                         self.pool_tokens, self.shared_fraction, self.pii_per_kib, self.pii_mix, self.seed,
+                         self.prompt_id_base)
+
+
+def generate(spec: GenSpec, nthreads: int = 0, tokens_out: Optional[np.ndarray] = None):
+    """Deterministic synthetic batch (host).  Returns tokens, offsets, users, owners."""
+    lib = N.load_library()
+    n, L = spec.n_prompts, spec.prompt_tokens
+    tokens = tokens_out if tokens_out is not None else np.empty(n * L, np.uint32)
+    offsets = np.empty(n + 1, np.uint64)
+    users = np.empty(n, np.uint64)
+    owners = np.empty(n, np.uint8)
+    s = spec.native()
+    N.raise_for(lib.skv_generate(C.byref(s), _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), nthreads),
+                "generate")
+    return tokens, offsets, users, owners
+
+
+def generate_pool(spec: GenSpec):
+    lib = N.load_library()
+    n, L = spec.pool_size, spec.pool_tokens
+    tokens = np.empty(n * L, np.uint32)
+    offsets = np.empty(n + 1, np.uint64)
+    users = np.empty(n, np.uint64)
+    owners = np.empty(n, np.uint8)
+    s = spec.native()
+    N.raise_for(lib.skv_generate_pool(C.byref(s), _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners)),
+                "generate_pool")
+    return tokens, offsets, users, owners
