@@ -1,0 +1,10 @@
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt
+nproc >> gpurun_out/gpu.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu > gpurun_out/pytest1.log 2>&1
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench1.json 2> gpurun_out/bench1.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches1.csv python bench.py --steps 2 --warmup 1 --prompts 16384 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hash_scan -s 2 -c 1 -o gpurun_out/prof_hs1 python bench.py --steps 2 --warmup 1 --prompts 65536 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+ls -la gpurun_out

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -38,6 +39,13 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ck((x), #x)
+
+// every host sync point also surfaces launch failures (bad config, smem opt-in, ...)
+void sync_check(cudaStream_t s) {
+  ck(cudaGetLastError(), "kernel launch");
+  ck(cudaStreamSynchronize(s), "stream synchronize");
+  ck(cudaGetLastError(), "kernel execution");
+}
 
 template <typename T>
 T* dalloc(size_t n, std::vector<void*>& owned) {
@@ -123,6 +131,7 @@ struct skv_ctx {
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
   int hs_grid = 0;
   uint32_t hs_smem = 0;
+  skv::HSLayout hs_layout{};
   uint32_t rec_grid = 0;
 
   // pending batch (between admit and commit)
@@ -174,39 +183,69 @@ int guard(skv_ctx* c, F&& f) {
 // here with CompileError (documented in DESIGN.md).
 void upload_rules(skv_ctx* c, const skv_rules& r) {
   const auto& d = r.dfa;
-  const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 4;
-  if (static_cast<uint64_t>(S) * row > 65535)
+  const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 2;
+  const uint32_t norm = S * row;
+  if (C + 1 > 64) throw skv::CompileError("device DFA: more than 63 byte classes");
+  if (norm > skv::kAccRegion)
     throw skv::CompileError("device DFA: " + std::to_string(S) + " states x " + std::to_string(C + 1) +
-                            " columns exceed the 16-bit row offset");
+                            " columns exceed the 32 KB row region");
   if (d.rule_index.size() > 16) throw skv::CompileError("device DFA: more than 16 enabled rules");
-  std::vector<uint32_t> tab(static_cast<size_t>(S) * (C + 1) + 4, 0);
+  // accepting transitions -> copies of the target row in the region above 32 KB
+  std::map<std::pair<uint32_t, uint32_t>, uint32_t> copy_of;  // (target, acc) -> copy index
+  std::vector<std::pair<uint32_t, uint32_t>> copies;
+  auto copy_index = [&](uint32_t target, uint32_t acc) {
+    auto it = copy_of.emplace(std::make_pair(target, acc), static_cast<uint32_t>(copies.size()));
+    if (it.second) copies.emplace_back(target, acc);
+    return it.first->second;
+  };
+  std::vector<uint16_t> entry(static_cast<size_t>(S) * (C + 1), 0);
+  std::vector<uint32_t> full(static_cast<size_t>(S) * (C + 1), 0);
   for (uint32_t s = 0; s < S; ++s) {
     for (uint32_t k = 0; k <= C; ++k) {
-      uint32_t next_row = k < C ? static_cast<uint32_t>(d.next[s * C + k]) * row : 0;
-      tab[s * (C + 1) + k] = next_row | (d.acc[s * (C + 1) + k] << 16);
+      uint32_t acc = d.acc[s * (C + 1) + k];
+      uint32_t t = k < C ? d.next[s * C + k] : 0;
+      uint32_t fast = k < C ? t * row : 0;
+      if (acc) fast = skv::kAccRegion + copy_index(k < C ? t : UINT32_MAX, acc) * row;
+      entry[s * (C + 1) + k] = static_cast<uint16_t>(fast);
+      full[s * (C + 1) + k] = (acc << 16) | (k < C ? t * row : 0);
     }
   }
-  uint8_t class4[256];
-  for (int b = 0; b < 256; ++b) class4[b] = static_cast<uint8_t>(d.class_map[b] * 4);
-  size_t tab_bytes = ((S * (C + 1) * 4) + 15) & ~size_t(15);
+  const uint32_t fast_bytes = skv::kAccRegion + static_cast<uint32_t>(copies.size()) * row;
+  if (fast_bytes > 65535) throw skv::CompileError("device DFA: too many accepting transitions");
+  std::vector<uint8_t> fast(fast_bytes, 0);
+  std::memcpy(fast.data(), entry.data(), entry.size() * 2);
+  for (size_t j = 0; j < copies.size(); ++j)
+    if (copies[j].first != UINT32_MAX)  // EOS pseudo rows carry no transitions
+      std::memcpy(fast.data() + skv::kAccRegion + j * row, entry.data() + copies[j].first * (C + 1), row);
+  uint8_t class2[256];
+  for (int b = 0; b < 256; ++b) class2[b] = static_cast<uint8_t>(d.class_map[b] * 2);
+  const size_t fast_al = (fast_bytes + 15) & ~size_t(15);
+  const size_t full_bytes = full.size() * 4;
   void* buf = nullptr;
-  CK(cudaMalloc(&buf, tab_bytes + 256 + 64));
-  CK(cudaMemcpyAsync(buf, tab.data(), tab_bytes, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(static_cast<uint8_t*>(buf) + tab_bytes, class4, 256, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMalloc(&buf, fast_al + full_bytes + 256 + 64));
+  uint8_t* base = static_cast<uint8_t*>(buf);
+  CK(cudaMemcpyAsync(base, fast.data(), fast_bytes, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(base + fast_al, full.data(), full_bytes, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(base + fast_al + full_bytes, class2, 256, cudaMemcpyHostToDevice, c->stream));
+  sync_check(c->stream);
   if (c->rules_buf) CK(cudaFree(c->rules_buf));
   c->rules_buf = buf;
-  c->rules_dev.table = static_cast<uint32_t*>(buf);
-  c->rules_dev.class4 = static_cast<uint8_t*>(buf) + tab_bytes;
-  c->rules_dev.table_bytes = S * (C + 1) * 4;
+  c->rules_dev.fast = reinterpret_cast<uint16_t*>(base);
+  c->rules_dev.full = reinterpret_cast<uint32_t*>(base + fast_al);
+  c->rules_dev.class2 = base + fast_al + full_bytes;
+  c->rules_dev.fast_bytes = fast_bytes;
+  c->rules_dev.norm_bytes = norm;
+  c->rules_dev.row_bytes = row;
   c->rules_dev.start_row = d.start * row;
-  c->rules_dev.eos4 = C * 4;
+  c->rules_dev.eos2 = C * 2;
   c->rules_dev.n_enabled = static_cast<uint32_t>(d.rule_index.size());
   c->rules_host = r;
   c->rules_loaded = true;
-  c->hs_smem = skv::hash_scan_smem(c->rules_dev, c->cfg.block_tokens, c->cfg.window_tokens);
+  c->hs_layout = skv::hash_scan_layout(c->rules_dev, c->cfg.block_tokens, c->cfg.window_tokens);
+  c->hs_smem = c->hs_layout.total;
   if (c->hs_smem > 227 * 1024) throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB");
   c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem);
+  if (c->hs_grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -396,7 +435,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     if (rr != SKV_OK) throw skv::CompileError("default rules failed to compile");
     std::unique_ptr<skv_rules> hold(r);
     upload_rules(c.get(), *r);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_check(c->stream);
     return SKV_OK;
   });
   if (rc != SKV_OK) {
@@ -489,7 +528,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
     if (b->on_device) {
       CK(cudaMemcpyAsync(c->host_small, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      sync_check(s);
       n_blocks = c->host_small[0];
     }
     if (n_blocks > c->max_blocks) throw ArgError("batch has more blocks than max_tokens / block_tokens");
@@ -512,6 +551,12 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     a.d_out = c->bd;
     a.mask_out = c->bmask;
     a.first_sens = c->first_sens;
+    a.off_cls = c->hs_layout.off_cls;
+    a.off_raw = c->hs_layout.off_raw;
+    a.off_so = c->hs_layout.off_so;
+    a.off_xch = c->hs_layout.off_xch;
+    a.off_list = c->hs_layout.off_list;
+    a.stage = c->hs_layout.stage;
     skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, s);
     CK(cudaEventRecord(c->ev[2], s));
     // chained keys + labels, then the index probe (stage 3)
@@ -522,7 +567,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // stage 4: monitor record
     skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->matched, c->acc_off, N + 1, s);
     CK(cudaMemcpyAsync(c->host_small, c->acc_off + N, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     const uint32_t M = c->host_small[0];
     uint32_t launched = 5;
     if (M > 0) {
@@ -552,7 +597,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       out->matched_total = M;
     }
     CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     if (c->host_small[8 + 5] & 1u)
       throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
     c->times.hash_scan_ms = elapsed(c->ev[1], c->ev[2]);
@@ -595,7 +640,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     std::memcpy(&nn, c->host_small, 8);
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     c->entries += nn;
@@ -616,7 +661,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     const uint64_t epoch = ++c->epoch;  // advance_epoch (cache_index.hpp:296-299)
     const uint32_t stamp = static_cast<uint32_t>(epoch);
     CK(cudaMemcpyAsync(c->host_small, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     const int cur = c->cur, prev = 1 - c->cur;
     const uint32_t n_cur = c->host_small[1 + cur], n_prev = c->host_small[1 + prev];
     const uint32_t bound = n_cur + n_prev;
@@ -631,7 +676,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, n_prev, 1, s);
     skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, n_cur, 0, s);
     CK(cudaMemcpyAsync(c->host_small, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     const uint32_t ne = c->host_small[0];
     std::vector<skv_event> ev(ne);
     if (ne) CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
@@ -641,7 +686,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     reset[1 + cur] = n_cur;
     // counters[0] pool_count = 0; counters[1+prev] (new cur) = 0; counters[1+cur] (new prev) = n_cur
     CK(cudaMemcpyAsync(c->counters, reset, 12, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     c->cur = prev;
     CK(cudaEventRecord(c->ev[6], s));
     CK(cudaEventSynchronize(c->ev[6]));
@@ -671,7 +716,7 @@ int skv_set_tiers(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint8_
     CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dt, tiers, n, cudaMemcpyHostToDevice, s));
     skv::launch_set_tiers(c->ix, dh, dd, dt, static_cast<uint32_t>(n), s);
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;
   });
@@ -689,7 +734,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
     skv::launch_export(c->ix, dout, dn, s);
     uint32_t cnt = 0;
     CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     if (out && cnt) CK(cudaMemcpy(out, dout, std::min<size_t>(cnt, cap) * sizeof(skv_entry), cudaMemcpyDeviceToHost));
     for (void* p : tmp) cudaFree(p);
     if (n) *n = cnt;
@@ -716,7 +761,7 @@ int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {
     if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
     skv::launch_scan_text(dt, static_cast<uint32_t>(len), c->rules_dev, dm, s);
     CK(cudaMemcpyAsync(c->host_small, dm, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     *mask = c->host_small[0];
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;
@@ -734,7 +779,7 @@ int skv_token_seq_digest(skv_ctx* c, const uint32_t* tokens, size_t n, uint64_t*
     if (n) CK(cudaMemcpyAsync(dt, tokens, n * 4, cudaMemcpyHostToDevice, s));
     skv::launch_digest(dt, static_cast<uint32_t>(n), dd, s);
     CK(cudaMemcpyAsync(c->host_small, dd, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    sync_check(s);
     std::memcpy(digest, c->host_small, 8);
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;

@@ -38,14 +38,30 @@ struct __align__(16) Aux {
   uint32_t cand;                       // epoch stamp when this entry was an anomaly candidate
 };
 
-// Device form of the compiled rule DFA.  Entry (s, c) at byte offset s*row_bytes + 4c:
-// bits 0..15 = byte offset of the next state's row, bits 16..31 = enabled-rule mask.
+// Device forms of the compiled rule DFA (built by capi.cpp upload_rules).
+//
+// fast  (u16, SMEM-resident in k_hash_scan): row of state s at byte offset s*row_bytes,
+//        entry (s, c) at +2c = byte offset of the next row.  A transition that ACCEPTS
+//        some rule instead points at a copy of the target row placed at >= 32768
+//        (kAccRegion), so "this window matched something" is bit 15 of the OR of all
+//        visited offsets -- no per-step mask work.  Entries of the EOS column are 0 or a
+//        pseudo offset >= 32768.  [norm_bytes, 32768) is a gap the kernel reuses as
+//        staging space.
+// full  (u32, global, read through L1): entry (s, c) at index s*(C+1)+c =
+//        (enabled-rule mask << 16) | canonical next-row byte offset (fast format, < 32768).
+//        Used to compute the exact rule mask of the (rare) windows the fast pass flags,
+//        and by the per-call tier1_scan wrapper.
+constexpr uint32_t kAccRegion = 32768;
+
 struct DevRules {
-  uint32_t* table = nullptr;  // n_states * (n_classes + 1) entries
-  uint8_t* class4 = nullptr;  // [256] byte -> 4 * class
-  uint32_t table_bytes = 0;
-  uint32_t start_row = 0;
-  uint32_t eos4 = 0;          // 4 * n_classes
+  uint16_t* fast = nullptr;
+  uint32_t* full = nullptr;
+  uint8_t* class2 = nullptr;  // [256] byte -> 2 * class
+  uint32_t fast_bytes = 0;    // kAccRegion + accepting-copy rows
+  uint32_t norm_bytes = 0;    // n_states * row_bytes (< kAccRegion)
+  uint32_t row_bytes = 0;     // 2 * (n_classes + 1)
+  uint32_t start_row = 0;     // start * row_bytes
+  uint32_t eos2 = 0;          // 2 * n_classes
   uint32_t n_enabled = 0;
 };
 
@@ -62,6 +78,12 @@ struct HashScanArgs {
   uint64_t* d_out;
   uint32_t* mask_out;
   uint32_t* first_sens;
+  // dynamic shared-memory layout (hash_scan_layout)
+  uint32_t off_cls, off_raw, off_so, off_xch, off_list, stage;
+};
+
+struct HSLayout {
+  uint32_t stage, off_cls, off_raw, off_so, off_xch, off_list, total;
 };
 
 struct Index {
@@ -78,7 +100,7 @@ size_t scan_temp_bytes(uint32_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint32_t n,
                            cudaStream_t s);
 int hash_scan_grid(int device, uint32_t smem_bytes);
-uint32_t hash_scan_smem(const DevRules& r, uint32_t B, uint32_t W);
+HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s);
 void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n_prompts,
                   uint64_t* h, uint8_t* label, cudaStream_t s);

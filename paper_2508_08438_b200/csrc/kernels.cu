@@ -20,6 +20,8 @@
 namespace skv {
 namespace {
 
+__host__ __device__ inline uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+
 constexpr uint64_t kFnvOff = 0xcbf29ce484222325ULL;
 constexpr uint64_t kFnvP = 0x100000001b3ULL;
 constexpr uint64_t kFnvP4 = kFnvP * kFnvP * kFnvP * kFnvP;  // (h^t)*P^4 == update_u32(t) for t < 256
@@ -75,57 +77,67 @@ __global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uin
 // Persistent CTAs; CTA i owns global blocks [i*nb/G, (i+1)*nb/G).  Each iteration takes
 // a chunk of up to kHSThreads consecutive blocks (may span prompts), stages the chunk's
 // token span [first window start, last window end) HBM -> SMEM once with coalesced
-// 128-bit streaming loads (each token read from HBM exactly once), converting every
-// token to its pre-scaled DFA byte class and its raw byte.  Thread t then hashes
-// block t from the SMEM raw bytes and runs the SMEM-resident DFA over its window
-// (block + W right-context tokens, clipped at the prompt end) -- the window overlap
-// is served from SMEM, not HBM.
+// 128-bit streaming loads (every token is read from HBM exactly once), converting each
+// token to its pre-scaled DFA byte class and its raw byte.  Thread t then
+//   * hashes block t from the SMEM raw bytes (token_seq_digest, core.hpp:68-73);
+//   * runs the SMEM-resident u16 DFA over its own block and its first context block,
+//     OR-accumulating visited row offsets (bit 15 <=> some rule accepted);
+//   * takes the rest of its window (the second context block when W = 2B) from its
+//     right neighbour: both runs are in the same DFA state at that block boundary in
+//     >99% of windows (measured on config 2), so the neighbour's first-context scan IS
+//     this window's second-context scan; otherwise it scans the bytes itself.
+// Windows whose accumulator has bit 15 set (a rule matched) are compacted and rescanned
+// with the u32 table to get the exact rule mask (A.3).  The window overlap is served
+// from SMEM, never re-read from HBM.
 // ---------------------------------------------------------------------------------
 constexpr int kHSThreads = 256;
-constexpr int kSoEntries = kHSThreads + 1;
 
-__host__ __device__ inline uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
-__host__ __device__ inline uint32_t stage_bytes(uint32_t B, uint32_t W) {
-  return round16(kHSThreads * B + W + 16);
+__device__ __forceinline__ uint32_t lds16(const uint8_t* base, uint32_t off) {
+  return *reinterpret_cast<const uint16_t*>(base + off);
 }
 
-__device__ __forceinline__ uint32_t lds_u32(const uint8_t* base, uint32_t byte_off) {
-  return *reinterpret_cast<const uint32_t*>(base + byte_off);
-}
-
-__device__ __forceinline__ uint32_t dfa_window(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
-                                               uint32_t o, uint32_t end, uint32_t row, uint32_t eos4) {
+__device__ __forceinline__ uint32_t dfa_run(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
+                                            uint32_t o, uint32_t end, uint32_t row, uint32_t& orr) {
   uint32_t acc = 0;
   while (o < end && (o & 3)) {
-    uint32_t e = lds_u32(tab, row + cls[o]);
-    acc |= e;
-    row = e & 0xffffu;
-    ++o;
+    row = lds16(tab, row + cls[o++]);
+    acc |= row;
   }
   for (; o + 4 <= end; o += 4) {
-    uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t e = lds_u32(tab, row + ((w >> (8 * k)) & 0xffu));
-      acc |= e;
-      row = e & 0xffffu;
-    }
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
+    const uint32_t r0 = lds16(tab, row + (w & 0xffu));
+    const uint32_t r1 = lds16(tab, r0 + ((w >> 8) & 0xffu));
+    const uint32_t r2 = lds16(tab, r1 + ((w >> 16) & 0xffu));
+    row = lds16(tab, r2 + (w >> 24));
+    acc |= r0 | r1 | r2 | row;
   }
+  while (o < end) {
+    row = lds16(tab, row + cls[o++]);
+    acc |= row;
+  }
+  orr |= acc;
+  return row;
+}
+
+// exact rule mask of one window with the canonical u32 table (global, L1-resident)
+__device__ __forceinline__ uint32_t dfa_exact(const uint32_t* __restrict__ full, const uint8_t* __restrict__ cls,
+                                              uint32_t o, uint32_t end, uint32_t row, uint32_t eos2) {
+  uint32_t acc = 0;
   for (; o < end; ++o) {
-    uint32_t e = lds_u32(tab, row + cls[o]);
+    const uint32_t e = __ldg(full + ((row + cls[o]) >> 1));
     acc |= e;
     row = e & 0xffffu;
   }
-  acc |= lds_u32(tab, row + eos4);
+  acc |= __ldg(full + ((row + eos2) >> 1));
   return acc >> 16;
 }
 
 __device__ __forceinline__ uint64_t digest_bytes(const uint8_t* __restrict__ raw, uint32_t o, uint32_t n,
                                                  uint64_t h) {
-  uint32_t end = o + n;
+  const uint32_t end = o + n;
   while (o < end && (o & 3)) h = (h ^ raw[o++]) * kFnvP4;
   for (; o + 4 <= end; o += 4) {
-    uint32_t w = *reinterpret_cast<const uint32_t*>(raw + o);
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(raw + o);
 #pragma unroll
     for (int k = 0; k < 4; ++k) h = (h ^ ((w >> (8 * k)) & 0xffu)) * kFnvP4;
   }
@@ -135,9 +147,9 @@ __device__ __forceinline__ uint64_t digest_bytes(const uint8_t* __restrict__ raw
 
 // index of the last element <= x in so[0..n) (so[0] <= x guaranteed)
 __device__ __forceinline__ uint32_t so_search(const uint32_t* so, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, hi = n;  // invariant so[lo] <= x, so[hi] > x (virtual)
+  uint32_t lo = 0, hi = n;
   while (hi - lo > 1) {
-    uint32_t mid = (lo + hi) >> 1;
+    const uint32_t mid = (lo + hi) >> 1;
     if (so[mid] <= x)
       lo = mid;
     else
@@ -146,38 +158,60 @@ __device__ __forceinline__ uint32_t so_search(const uint32_t* so, uint32_t n, ui
   return lo;
 }
 
+struct WinGeo {
+  uint32_t gb, p, b, ws, we;
+};
+
+__device__ __forceinline__ WinGeo window_geo(const HashScanArgs& a, const uint32_t* so, uint32_t n_so, uint32_t pp,
+                                             uint32_t g, uint32_t t, uint64_t as) {
+  WinGeo w;
+  w.gb = g + t;
+  const uint32_t i = so_search(so, n_so, w.gb);
+  w.p = pp + i;
+  w.b = w.gb - so[i];
+  const uint64_t base = a.tok_off[w.p];
+  const uint64_t L = a.tok_off[w.p + 1] - base;
+  w.ws = static_cast<uint32_t>(base + static_cast<uint64_t>(w.b) * a.B - as);
+  const uint64_t wend = min(L, static_cast<uint64_t>(w.b) * a.B + a.B + a.W);
+  w.we = static_cast<uint32_t>(base + wend - as);
+  return w;
+}
+
 __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const uint32_t tb = round16(a.rules.table_bytes);
   uint8_t* tab = sm;
-  uint8_t* cmap = sm + tb;
-  uint32_t* so = reinterpret_cast<uint32_t*>(cmap + 256);
-  uint8_t* cls = reinterpret_cast<uint8_t*>(so) + round16(kSoEntries * 4);
-  const uint32_t stage = stage_bytes(a.B, a.W);
-  uint8_t* raw = cls + stage;
-  __shared__ uint32_t s_pp;
+  uint8_t* cls = sm + a.off_cls;
+  uint8_t* raw = sm + a.off_raw;
+  uint32_t* so = reinterpret_cast<uint32_t*>(sm + a.off_so);
+  uint32_t* xs_x = reinterpret_cast<uint32_t*>(sm + a.off_xch);
+  uint32_t* xs_y = xs_x + kHSThreads;
+  uint32_t* xs_o = xs_y + kHSThreads;
+  uint32_t* flag_list = reinterpret_cast<uint32_t*>(sm + a.off_list);
+  __shared__ uint8_t cmap[256];
+  __shared__ uint32_t s_pp, s_nflag;
 
   const uint32_t tid = threadIdx.x;
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.rules.table);
+  {  // DFA rows [0, norm) and accepting copies [32768, fast_bytes) -> SMEM
+    const uint32_t n0 = (a.rules.norm_bytes + 15) / 16;
+    const uint32_t n1 = (a.rules.fast_bytes - kAccRegion + 15) / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(a.rules.fast);
     uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (uint32_t i = tid; i < tb / 16; i += blockDim.x) dst[i] = src[i];
-    if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class4)[tid];
+    for (uint32_t i = tid; i < n0; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = tid; i < n1; i += blockDim.x) dst[kAccRegion / 16 + i] = src[kAccRegion / 16 + i];
+    if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
   }
   const uint32_t nb = a.n_blocks;
   const uint32_t G0 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * nb) / gridDim.x);
   const uint32_t G1 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x + 1) * nb) / gridDim.x);
   if (tid == 0 && G0 < G1) {
-    // prompt containing G0: last p with blk_off[p] <= G0 and blk_off[p+1] > G0
-    uint32_t lo = 0, hi = a.n_prompts;
+    uint32_t lo = 0, hi = a.n_prompts;  // prompt containing G0
     while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = (lo + hi) >> 1;
       if (a.blk_off[mid] <= G0)
         lo = mid;
       else
         hi = mid;
     }
-    while (a.blk_off[lo + 1] <= G0) ++lo;  // skip empty prompts
     s_pp = lo;
   }
   __syncthreads();
@@ -185,38 +219,38 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   uint32_t pp = s_pp;
   uint32_t g = G0;
   const uint32_t B = a.B, W = a.W;
+  const uint32_t start_row = a.rules.start_row, eos2 = a.rules.eos2;
   while (g < G1) {
-    for (uint32_t t = tid; t < kSoEntries; t += blockDim.x)
-      so[t] = a.blk_off[min(pp + t, a.n_prompts)];
+    for (uint32_t t = tid; t <= kHSThreads; t += blockDim.x) so[t] = a.blk_off[min(pp + t, a.n_prompts)];
+    if (tid == 0) s_nflag = 0;
     __syncthreads();
     uint32_t nw = min(static_cast<uint32_t>(kHSThreads), G1 - g);
-    uint32_t n_so = kSoEntries;
-    if (pp + kHSThreads <= a.n_prompts) {
+    uint32_t n_so = kHSThreads + 1;
+    if (pp + kHSThreads <= a.n_prompts)
       nw = min(nw, so[kHSThreads] - g);
-    } else {
+    else
       n_so = a.n_prompts - pp + 1;
-    }
     uint32_t lastg = g + nw - 1;
     uint32_t il = so_search(so, n_so, lastg);
-    uint64_t s_tok = a.tok_off[pp] + static_cast<uint64_t>(g - so[0]) * B;
+    const uint64_t s_tok = a.tok_off[pp] + static_cast<uint64_t>(g - so[0]) * B;
     uint64_t e_tok = min(a.tok_off[pp + il + 1],
                          a.tok_off[pp + il] + static_cast<uint64_t>(lastg - so[il] + 1) * B + W);
-    uint64_t as = s_tok & ~3ull;
-    if (e_tok - as > stage - 8) {  // too many prompt tails in the span: single-prompt chunk
+    const uint64_t as = s_tok & ~3ull;
+    if (e_tok - as > a.stage - 8) {  // too many prompt tails in the span: single-prompt chunk
       nw = min(nw, so[1] - g);
       lastg = g + nw - 1;
       il = 0;
       e_tok = min(a.tok_off[pp + 1], a.tok_off[pp] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
     }
-    // ---- stage tokens -> (class*4, raw byte), 4 tokens per 128-bit load
-    const uint32_t span = static_cast<uint32_t>(e_tok - as);
-    const uint32_t nq = (span + 3) >> 2;
+    n_so = il + 1;
+    // ---- stage tokens -> (2*class, raw byte); 4 tokens per 128-bit streaming load
+    const uint32_t nq = static_cast<uint32_t>((e_tok - as + 3) >> 2);
     uint32_t wide = 0;
     for (uint32_t q = tid; q < nq; q += blockDim.x) {
-      uint64_t gi = as + 4ull * q;
+      const uint64_t gi = as + 4ull * q;
       uint32_t t0, t1, t2, t3;
       if (gi + 4 <= a.n_tokens) {
-        uint4 v = ldg_stream(a.tokens + gi);
+        const uint4 v = ldg_stream(a.tokens + gi);
         t0 = v.x, t1 = v.y, t2 = v.z, t3 = v.w;
       } else {
         t0 = gi < a.n_tokens ? a.tokens[gi] : 0;
@@ -225,34 +259,65 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
         t3 = 0;
       }
       wide |= (t0 | t1 | t2 | t3) >> 8;
-      uint32_t c = cmap[t0 & 0xff] | (cmap[t1 & 0xff] << 8) | (cmap[t2 & 0xff] << 16) | (cmap[t3 & 0xff] << 24);
-      uint32_t r = (t0 & 0xff) | ((t1 & 0xff) << 8) | ((t2 & 0xff) << 16) | ((t3 & 0xff) << 24);
+      const uint32_t c = cmap[t0 & 0xff] | (cmap[t1 & 0xff] << 8) | (cmap[t2 & 0xff] << 16) |
+                         (static_cast<uint32_t>(cmap[t3 & 0xff]) << 24);
+      const uint32_t r = __byte_perm(__byte_perm(t0, t1, 0x0040), __byte_perm(t2, t3, 0x0040), 0x5410);
       reinterpret_cast<uint32_t*>(cls)[q] = c;
       reinterpret_cast<uint32_t*>(raw)[q] = r;
     }
     wide = __syncthreads_or(wide != 0);
-    if (tid < nw) {
-      uint32_t gb = g + tid;
-      uint32_t i = so_search(so, il + 1, gb);
-      uint32_t p = pp + i;
-      uint32_t b = gb - so[i];
-      uint64_t base = a.tok_off[p];
-      uint64_t L = a.tok_off[p + 1] - base;
-      uint32_t ws = static_cast<uint32_t>(base + static_cast<uint64_t>(b) * B - as);
-      uint64_t wend = min(L, static_cast<uint64_t>(b) * B + B + W);
-      uint32_t we = static_cast<uint32_t>(base + wend - as);
+    // ---- phase 1+2: digest, own block, first context block
+    WinGeo w{};
+    uint32_t Y = 0, orr = 0, e1 = 0;
+    const bool act = tid < nw;
+    if (act) {
+      w = window_geo(a, so, n_so, pp, g, tid, as);
       uint64_t dg;
       if (!wide) {
-        dg = digest_bytes(raw, ws, B, a.digest_init);
-      } else {  // some token >= 256 in this chunk: full update_u32 per token
+        dg = digest_bytes(raw, w.ws, B, a.digest_init);
+      } else {  // a token >= 256 in this chunk: full update_u32 per token
         dg = a.digest_init;
-        const uint32_t* tp = a.tokens + base + static_cast<uint64_t>(b) * B;
+        const uint32_t* tp = a.tokens + a.tok_off[w.p] + static_cast<uint64_t>(w.b) * B;
         for (uint32_t k = 0; k < B; ++k) dg = fnv_u32(dg, tp[k]);
       }
-      uint32_t mask = dfa_window(tab, cls, ws, we, a.rules.start_row, a.rules.eos4);
-      a.d_out[gb] = dg;
-      a.mask_out[gb] = mask;
-      if (mask) atomicMin(&a.first_sens[p], b);
+      a.d_out[w.gb] = dg;
+      const uint32_t X = dfa_run(tab, cls, w.ws, w.ws + B, start_row, orr);
+      e1 = min(w.we, w.ws + 2 * B);
+      uint32_t o1 = 0;
+      Y = dfa_run(tab, cls, w.ws + B, e1, X, o1);
+      orr |= o1;
+      xs_x[tid] = X;
+      xs_y[tid] = Y;
+      xs_o[tid] = o1;
+    }
+    __syncthreads();
+    // ---- phase 3: rest of the window, shared with the right neighbour when in sync
+    if (act) {
+      uint32_t fin = Y;
+      if (e1 < w.we) {
+        const bool share = w.we == w.ws + 3 * B && tid + 1 < nw && w.gb + 1 < so[w.p - pp + 1] &&
+                           xs_x[tid + 1] == Y;
+        if (share) {
+          orr |= xs_o[tid + 1];
+          fin = xs_y[tid + 1];
+        } else {
+          fin = dfa_run(tab, cls, e1, w.we, Y, orr);
+        }
+      }
+      orr |= lds16(tab, fin + eos2);
+      if (orr & kAccRegion)
+        flag_list[atomicAdd(&s_nflag, 1u)] = tid;
+      else
+        a.mask_out[w.gb] = 0;
+    }
+    __syncthreads();
+    // ---- exact rule masks of the windows that matched something (compacted)
+    const uint32_t nflag = s_nflag;
+    for (uint32_t i = tid; i < nflag; i += blockDim.x) {
+      const WinGeo f = window_geo(a, so, n_so, pp, g, flag_list[i], as);
+      const uint32_t mask = dfa_exact(a.rules.full, cls, f.ws, f.we, start_row, eos2);
+      a.mask_out[f.gb] = mask;
+      if (mask) atomicMin(&a.first_sens[f.p], f.b);
     }
     g += nw;
     if (tid == 0) {
@@ -655,14 +720,13 @@ __global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
 
 __global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const uint8_t* tab = reinterpret_cast<const uint8_t*>(r.table);
   uint32_t row = r.start_row, acc = 0;
   for (uint32_t i = 0; i < len; ++i) {
-    uint32_t e = *reinterpret_cast<const uint32_t*>(tab + row + r.class4[text[i]]);
+    const uint32_t e = r.full[(row + r.class2[text[i]]) >> 1];
     acc |= e;
     row = e & 0xffffu;
   }
-  acc |= *reinterpret_cast<const uint32_t*>(tab + row + r.eos4);
+  acc |= r.full[(row + r.eos2) >> 1];
   *mask = acc >> 16;
 }
 
@@ -696,18 +760,38 @@ void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, ui
   cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, n, s);
 }
 
-uint32_t hash_scan_smem(const DevRules& r, uint32_t B, uint32_t W) {
-  return round16(r.table_bytes) + 256 + round16(kSoEntries * 4) + 2 * stage_bytes(B, W);
+HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
+  // first-fit of the staging buffers into the unused gap [norm_bytes, 32768) of the
+  // u16 DFA table, else after the table
+  HSLayout L{};
+  L.stage = round16(kHSThreads * B + W + 16);
+  uint32_t gap = round16(r.norm_bytes), tail = round16(r.fast_bytes);
+  auto place = [&](uint32_t bytes) {
+    bytes = round16(bytes);
+    if (gap + bytes <= kAccRegion) {
+      uint32_t o = gap;
+      gap += bytes;
+      return o;
+    }
+    uint32_t o = tail;
+    tail += bytes;
+    return o;
+  };
+  L.off_cls = place(L.stage);
+  L.off_raw = place(L.stage);
+  L.off_so = place((kHSThreads + 1) * 4);
+  L.off_xch = place(3 * kHSThreads * 4);
+  L.off_list = place(kHSThreads * 4);
+  L.total = tail;
+  return L;
 }
 
 int hash_scan_grid(int device, uint32_t smem) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_hash_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  if (cudaFuncSetAttribute(k_hash_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+      cudaSuccess)
+    return -1;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, kHSThreads, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, kHSThreads, smem) != cudaSuccess) return -1;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (per_sm < 1) per_sm = 1;

@@ -92,6 +92,13 @@ class RuleSet:
                 m |= 1 << r
         return m
 
+    def to_rule_mask_array(self, device_masks: np.ndarray) -> np.ndarray:
+        out = np.zeros(len(device_masks), np.uint64)
+        dm = np.asarray(device_masks).astype(np.uint64)
+        for j, r in enumerate(self.enabled_rules()):
+            out |= ((dm >> np.uint64(j)) & np.uint64(1)) << np.uint64(r)
+        return out
+
     def categories(self, device_mask: int) -> list[str]:
         """Ordered, de-duplicated categories exactly as ``CompiledRuleSet::scan`` lists them
         (rule order of the hit rules, detection.hpp:160-166)."""

@@ -54,7 +54,7 @@ def run_scenario(ref, seed, B, W, n_batches, n_prompts, n_users, jump=0.3, u_pre
                  wide_p=0.0, rules_json=None):
     rng = np.random.default_rng(seed)
     trunks = make_trunks(rng, 12)
-    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=4096,
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 18, max_prompts=4096,
                        max_tokens=1 << 20, max_window_entries=1 << 15, entropy_jump=jump, u_pre_max=u_pre_max)
     fired = 0
     with AdmissionEngine(cfg) as eng:
