@@ -1,0 +1,130 @@
+"""GPU parity against committed golden vectors (generated from the unmodified reference by
+tests/golden/make_golden.py) and against the C restatement oracle -- neither needs
+/root/reference at run time."""
+import json
+import pathlib
+
+import numpy as np
+import pytest
+
+from oracle_c import OracleEngine, OracleRules
+from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, RuleSet
+from workloads import make_batch, make_trunks
+
+pytestmark = pytest.mark.gpu
+GOLD = pathlib.Path(__file__).resolve().parent / "golden"
+
+
+def cfg(**kw):
+    base = dict(block_tokens=16, window_tokens=32, index_capacity=1 << 18, max_prompts=4096, max_tokens=1 << 20,
+                max_window_entries=1 << 15)
+    base.update(kw)
+    return EngineConfig(**base)
+
+
+def test_config1_golden(gpu):
+    """Config 1 (1000 x 112-token reference-generated prompts, 4 users): two admission
+    rounds with commit + epoch, bit-exact against the reference's outputs."""
+    w = np.load(GOLD / "cfg1_workload.npz")
+    e = np.load(GOLD / "cfg1_expected.npz")
+    assert int(w["digest"][0]) == 0x1FF5DFD735EC52B0  # reference canonical_bytes() pin
+    tok = w["tokens"].astype(np.uint32)
+    with AdmissionEngine(cfg()) as eng:
+        rs = eng.rules
+        for rnd in (1, 2):
+            got = eng.admit(tok, w["offsets"], w["users"], w["owners"])
+            np.testing.assert_array_equal(got.block_h, e[f"r{rnd}_block_h"])
+            np.testing.assert_array_equal(got.block_d, e[f"r{rnd}_block_d"])
+            np.testing.assert_array_equal(rs.to_rule_mask_array(got.rule_mask), e[f"r{rnd}_mask"])
+            np.testing.assert_array_equal(got.label, e[f"r{rnd}_label"])
+            np.testing.assert_array_equal(got.decision, e[f"r{rnd}_decision"])
+            np.testing.assert_array_equal(got.matched_blocks, e[f"r{rnd}_matched_blocks"])
+            np.testing.assert_array_equal(got.lowest_tier, e[f"r{rnd}_lowest_tier"])
+            eng.commit()
+            ep, ev = eng.epoch_pass()
+            assert ep == int(e[f"r{rnd}_epoch"][0])
+            assert [(x.h, x.d, x.action, x.u_pre) for x in ev] == [tuple(map(int, r)) for r in e[f"r{rnd}_events"]]
+        x = eng.export()
+        for k in ("h", "d", "creator", "label", "owner", "tier", "hit_cur", "u_cnt", "hit_pre", "u_pre"):
+            np.testing.assert_array_equal(x[k].astype(np.uint64), e[f"export_{k}"].astype(np.uint64), k)
+
+
+def test_tier1_scan_known_answers(gpu):
+    """RuleEngine::tier1_scan known answers (test_detection.cpp:33-77) through the device."""
+    kats = json.loads((GOLD / "scan_kats.json").read_text())
+    with AdmissionEngine(cfg()) as eng:
+        for k in kats["kats"] + kats["rule_corpus_500_77"][:100]:
+            m = eng.tier1_scan(k["text"].encode("latin-1"))
+            assert eng.rules.to_rule_mask(m) == k["mask"], k["text"]
+            assert eng.rules.categories(m) == k["categories"], k["text"]
+
+
+def test_token_seq_digest_device(gpu):
+    import oracle_c
+    L = oracle_c.lib()
+    rng = np.random.default_rng(1)
+    with AdmissionEngine(cfg()) as eng:
+        for n in (0, 1, 7, 16, 33):
+            t = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+            assert eng.token_seq_digest(t) == L.orc_token_seq_digest(t.ctypes.data, n)
+
+
+@pytest.mark.parametrize("B,W", [(16, 32), (16, 16), (16, 40), (8, 4), (128, 32), (4, 0)])
+def test_vs_c_oracle_ragged(gpu, B, W):
+    """Ragged / empty / sub-block prompts, non-byte tokens, window shapes with and without
+    the neighbour-shared context block, against the C restatement."""
+    rng = np.random.default_rng(B * 1000 + W)
+    trunks = make_trunks(rng, 10)
+    orc = OracleEngine(OracleRules(), B=B, W=W)
+    with AdmissionEngine(cfg(block_tokens=B, window_tokens=W)) as eng:
+        for _ in range(4):
+            batch = make_batch(rng, trunks, 300, 4, wide_p=0.05, max_words=120 if B >= 64 else 40)
+            got = eng.admit(*batch)
+            exp = orc.admit(*batch)
+            np.testing.assert_array_equal(got.block_h, exp["block_h"])
+            np.testing.assert_array_equal(eng.rules.to_rule_mask_array(got.rule_mask), exp["mask"])
+            np.testing.assert_array_equal(got.label, exp["label"])
+            np.testing.assert_array_equal(got.matched_blocks, exp["matched_blocks"])
+            np.testing.assert_array_equal(got.decision, exp["decision"])
+            eng.commit()
+            orc.commit()
+            _, ev = eng.epoch_pass()
+            _, ev_o = orc.epoch()
+            assert [(x.h, x.d, x.action) for x in ev] == [(x[0], x[1], x[2]) for x in ev_o]
+    orc.close()
+
+
+def test_large_batch_properties(gpu):
+    """Config-2 sized batch (65,536 x 2,048): size-independent properties -- every prompt
+    matches exactly its 40-block pool prefix (pool pre-inserted, Public), labels are a
+    prefix-OR of the window masks, keys of identical pool prefixes coincide, and a
+    sample of prompts agrees with the C oracle."""
+    from paper_2508_08438_b200 import GenSpec, generate, generate_pool
+    spec = GenSpec(n_prompts=65536, prompt_tokens=2048, seed=1)
+    tok, off, users, owners = generate(spec)
+    ptok, poff, pusers, powners = generate_pool(spec)
+    with AdmissionEngine(cfg(max_prompts=65536, max_tokens=65536 * 2048, index_capacity=1 << 25,
+                             max_window_entries=1 << 16)) as eng:
+        eng.admit(ptok, poff, pusers, powners)
+        eng.commit()
+        eng.epoch_pass()
+        got = eng.admit(tok, off, users, owners)
+    nb = 128
+    assert got.n_blocks == 65536 * nb
+    assert (got.matched_blocks == 40).all()
+    lab = got.label.reshape(-1, nb)
+    sens = (got.rule_mask.reshape(-1, nb) != 0)
+    np.testing.assert_array_equal(lab == 0, np.logical_or.accumulate(sens, axis=1))
+    orc = OracleEngine(OracleRules(), B=16, W=32)
+    orc.admit(ptok, poff, pusers, powners)
+    orc.commit()
+    orc.epoch()
+    idx = np.arange(0, 65536, 4099)
+    sub_tok = np.concatenate([tok[i * 2048:(i + 1) * 2048] for i in idx])
+    sub_off = np.arange(len(idx) + 1, dtype=np.uint64) * 2048
+    exp = orc.admit(sub_tok, sub_off, users[idx], owners[idx])
+    sel = (idx[:, None] * nb + np.arange(nb)[None, :]).ravel()
+    np.testing.assert_array_equal(got.block_h[sel], exp["block_h"])
+    np.testing.assert_array_equal(eng.rules.to_rule_mask_array(got.rule_mask[sel]), exp["mask"])
+    np.testing.assert_array_equal(got.label[sel], exp["label"])
+    orc.close()
