@@ -219,14 +219,26 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
       std::memcpy(fast.data() + skv::kAccRegion + j * row, entry.data() + copies[j].first * (C + 1), row);
   uint8_t class2[256];
   for (int b = 0; b < 256; ++b) class2[b] = static_cast<uint8_t>(d.class_map[b] * 2);
+  std::vector<uint16_t> copy_acc(copies.size() + 1, 0);
+  for (size_t j = 0; j < copies.size(); ++j) copy_acc[j] = static_cast<uint16_t>(copies[j].second);
+  const uint32_t inv = static_cast<uint32_t>(((1ull << 32) + row - 1) / row);
+  for (uint32_t j = 0; j < copies.size(); ++j)  // exactness of the reciprocal on every copy offset
+    if (static_cast<uint32_t>((static_cast<uint64_t>(j * row) * inv) >> 32) != j)
+      throw skv::CompileError("device DFA: copy-row reciprocal not exact");
   const size_t fast_al = (fast_bytes + 15) & ~size_t(15);
   const size_t full_bytes = full.size() * 4;
+  const size_t acc_bytes = copy_acc.size() * 2;
   void* buf = nullptr;
-  CK(cudaMalloc(&buf, fast_al + full_bytes + 256 + 64));
+  CK(cudaMalloc(&buf, fast_al + full_bytes + 256 + acc_bytes + 64));
   uint8_t* base = static_cast<uint8_t*>(buf);
   CK(cudaMemcpyAsync(base, fast.data(), fast_bytes, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(base + fast_al, full.data(), full_bytes, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(base + fast_al + full_bytes, class2, 256, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(base + fast_al + full_bytes + 256, copy_acc.data(), acc_bytes, cudaMemcpyHostToDevice,
+                     c->stream));
+  c->rules_dev.copy_acc = reinterpret_cast<uint16_t*>(base + fast_al + full_bytes + 256);
+  c->rules_dev.n_copies = static_cast<uint32_t>(copies.size());
+  c->rules_dev.copy_inv = inv;
   sync_check(c->stream);
   if (c->rules_buf) CK(cudaFree(c->rules_buf));
   c->rules_buf = buf;
@@ -373,14 +385,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->cfg.index_capacity = cap;
     c->ix.cap = cap;
     c->ix.mask = cap - 1;
-    c->ix.rec = dalloc<skv::Rec>(cap, c->owned);
-    c->ix.stats = dalloc<skv::Stats>(cap, c->owned);
-    c->ix.aux = dalloc<skv::Aux>(cap, c->owned);
-    c->ix.claim = dalloc<unsigned long long>(cap, c->owned);
-    CK(cudaMemsetAsync(c->ix.rec, 0, cap * sizeof(skv::Rec), c->stream));
-    CK(cudaMemsetAsync(c->ix.stats, 0, cap * sizeof(skv::Stats), c->stream));
-    CK(cudaMemsetAsync(c->ix.aux, 0xff, cap * sizeof(skv::Aux), c->stream));
-    CK(cudaMemsetAsync(c->ix.claim, 0, cap * sizeof(unsigned long long), c->stream));
+    c->ix.e = dalloc<skv::Entry>(cap, c->owned);
+    skv::launch_init_entries(c->ix, c->stream);
     // monitor window
     c->pool_cap = static_cast<uint32_t>(cfg->max_window_entries);
     c->sets = dalloc<unsigned long long>(static_cast<size_t>(c->pool_cap) * skv::kMaxSetUsers, c->owned);
@@ -560,9 +566,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, s);
     CK(cudaEventRecord(c->ev[2], s));
     // chained keys + labels, then the index probe (stage 3)
-    skv::launch_chain(c->bd, c->blk_off, c->first_sens, N, c->bh, c->blabel, s);
-    skv::launch_probe(c->ix, c->bh, c->bd, c->blk_off, users, N, c->bdecision, c->bslot, c->matched, c->exist, c->tier,
-                      s);
+    skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, users, N, c->bh, c->blabel, c->bdecision,
+                            c->bslot, c->matched, c->exist, c->tier, s);
     CK(cudaEventRecord(c->ev[3], s));
     // stage 4: monitor record
     skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->matched, c->acc_off, N + 1, s);

@@ -1,11 +1,11 @@
 // ctx.hpp -- internal device-side layout shared by capi.cpp and kernels.cu.
 //
 // HBM layout of the flattened privacy-aware index (replaces the pointer radix tree of
-// reference cache_index.hpp:65-98,127-836):
-//   rec[cap]    32 B  key (h,d) + creator + parent slot + label/owner/tier/state
-//   stats[cap]  16 B  AccessStats window (hit_cur, u_cnt, hit_pre, u_pre)
-//   aux[cap]    16 B  child list links, user-set handle, candidate stamp
-//   claim[cap]   8 B  intra-batch first-creator arbitration (batch<<32 | ~prompt)
+// reference cache_index.hpp:65-98,127-836): one 64-B
+// Entry per slot,
+//   sector 0 (Rec, 32 B)  key (h,d) + creator + parent slot + label/owner/tier/state
+//   sector 1 (32 B)       AccessStats window (hit_cur, u_cnt, hit_pre, u_pre) and
+//                         Aux (child-list links, user-set handle, claim/candidate mark)
 // Open addressing with linear probing; a slot is empty iff its key is (0,0).
 #pragma once
 
@@ -35,8 +35,17 @@ struct __align__(16) Stats {
 struct __align__(16) Aux {
   uint32_t first_child, next_sibling;  // subtree walk for label propagation
   uint32_t set_idx;                    // user-set pool slot for the current window, kNone if untouched
-  uint32_t cand;                       // epoch stamp when this entry was an anomaly candidate
+  uint32_t mark;  // commit: intra-batch claim (~prompt, >= 2^31); epoch: candidate stamp (= epoch)
 };
+
+// One index slot = 64 B: sector 0 is everything the probe reads, sector 1 the monitor
+// window and tree links.
+struct __align__(64) Entry {
+  Rec rec;
+  Stats stats;
+  Aux aux;
+};
+static_assert(sizeof(Entry) == 64, "entry must be two 32-B sectors");
 
 // Device forms of the compiled rule DFA (built by capi.cpp upload_rules).
 //
@@ -63,6 +72,9 @@ struct DevRules {
   uint32_t start_row = 0;     // start * row_bytes
   uint32_t eos2 = 0;          // 2 * n_classes
   uint32_t n_enabled = 0;
+  uint16_t* copy_acc = nullptr;  // [n_copies] rule mask of accepting-copy row j
+  uint32_t n_copies = 0;
+  uint32_t copy_inv = 0;  // ceil(2^32 / row_bytes): j = umulhi(offset - kAccRegion, copy_inv)
 };
 
 struct HashScanArgs {
@@ -87,12 +99,11 @@ struct HSLayout {
 };
 
 struct Index {
-  Rec* rec = nullptr;
-  Stats* stats = nullptr;
-  Aux* aux = nullptr;
-  unsigned long long* claim = nullptr;
+  Entry* e = nullptr;
   uint64_t cap = 0, mask = 0;
 };
+
+void launch_init_entries(const Index& ix, cudaStream_t s);
 
 // kernel launchers (kernels.cu)
 void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, cudaStream_t s);
@@ -102,11 +113,9 @@ void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, ui
 int hash_scan_grid(int device, uint32_t smem_bytes);
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s);
-void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n_prompts,
-                  uint64_t* h, uint8_t* label, cudaStream_t s);
-void launch_probe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                  const uint64_t* users, uint32_t n_prompts, uint8_t* decision, uint32_t* slot,
-                  uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s);
+void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
+                        const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s);
 void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
                           const uint32_t* acc_off, uint32_t n_prompts, uint32_t* key, uint32_t* val,
                           cudaStream_t s);

@@ -80,15 +80,14 @@ __global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uin
 // 128-bit streaming loads (every token is read from HBM exactly once), converting each
 // token to its pre-scaled DFA byte class and its raw byte.  Thread t then
 //   * hashes block t from the SMEM raw bytes (token_seq_digest, core.hpp:68-73);
-//   * runs the SMEM-resident u16 DFA over its own block and its first context block,
-//     OR-accumulating visited row offsets (bit 15 <=> some rule accepted);
+//   * runs the SMEM-resident u16 DFA over its own block and its first context block
+//     (3 instructions + 1 LDS per byte; accepting transitions land in the copy region
+//     >= 32 KB and are decoded to the exact rule mask off the common path);
 //   * takes the rest of its window (the second context block when W = 2B) from its
 //     right neighbour: both runs are in the same DFA state at that block boundary in
 //     >99% of windows (measured on config 2), so the neighbour's first-context scan IS
 //     this window's second-context scan; otherwise it scans the bytes itself.
-// Windows whose accumulator has bit 15 set (a rule matched) are compacted and rescanned
-// with the u32 table to get the exact rule mask (A.3).  The window overlap is served
-// from SMEM, never re-read from HBM.
+// The window overlap is served from SMEM, never re-read from HBM.
 // ---------------------------------------------------------------------------------
 constexpr int kHSThreads = 256;
 
@@ -96,12 +95,23 @@ __device__ __forceinline__ uint32_t lds16(const uint8_t* base, uint32_t off) {
   return *reinterpret_cast<const uint16_t*>(base + off);
 }
 
+// Rule mask carried by an accepting-copy row offset r (>= kAccRegion):
+// copy index j = (r - kAccRegion) / row_bytes via a 32-bit reciprocal (exact: r is a
+// multiple of row_bytes), mask = acc_tab[j] (SMEM, u16).
+__device__ __forceinline__ uint32_t copy_mask(const uint16_t* acc_tab, uint32_t r, uint32_t inv) {
+  return (r & kAccRegion) ? acc_tab[__umulhi(r - kAccRegion, inv)] : 0u;
+}
+
+// Scan class bytes [o, end) from row; returns the final row offset and ORs the exact
+// enabled-rule mask of every accepting transition into *acc.  Accepting transitions are
+// rare, so the per-4-byte check is one OR-test and a predicated-off branch.
 __device__ __forceinline__ uint32_t dfa_run(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
-                                            uint32_t o, uint32_t end, uint32_t row, uint32_t& orr) {
-  uint32_t acc = 0;
+                                            const uint16_t* __restrict__ acc_tab, uint32_t inv, uint32_t o,
+                                            uint32_t end, uint32_t row, uint32_t* acc) {
+  uint32_t m = 0;
   while (o < end && (o & 3)) {
     row = lds16(tab, row + cls[o++]);
-    acc |= row;
+    m |= copy_mask(acc_tab, row, inv);
   }
   for (; o + 4 <= end; o += 4) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
@@ -109,27 +119,16 @@ __device__ __forceinline__ uint32_t dfa_run(const uint8_t* __restrict__ tab, con
     const uint32_t r1 = lds16(tab, r0 + ((w >> 8) & 0xffu));
     const uint32_t r2 = lds16(tab, r1 + ((w >> 16) & 0xffu));
     row = lds16(tab, r2 + (w >> 24));
-    acc |= r0 | r1 | r2 | row;
+    if ((r0 | r1 | r2 | row) & kAccRegion)
+      m |= copy_mask(acc_tab, r0, inv) | copy_mask(acc_tab, r1, inv) | copy_mask(acc_tab, r2, inv) |
+           copy_mask(acc_tab, row, inv);
   }
   while (o < end) {
     row = lds16(tab, row + cls[o++]);
-    acc |= row;
+    m |= copy_mask(acc_tab, row, inv);
   }
-  orr |= acc;
+  *acc |= m;
   return row;
-}
-
-// exact rule mask of one window with the canonical u32 table (global, L1-resident)
-__device__ __forceinline__ uint32_t dfa_exact(const uint32_t* __restrict__ full, const uint8_t* __restrict__ cls,
-                                              uint32_t o, uint32_t end, uint32_t row, uint32_t eos2) {
-  uint32_t acc = 0;
-  for (; o < end; ++o) {
-    const uint32_t e = __ldg(full + ((row + cls[o]) >> 1));
-    acc |= e;
-    row = e & 0xffffu;
-  }
-  acc |= __ldg(full + ((row + eos2) >> 1));
-  return acc >> 16;
 }
 
 __device__ __forceinline__ uint64_t digest_bytes(const uint8_t* __restrict__ raw, uint32_t o, uint32_t n,
@@ -186,9 +185,10 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   uint32_t* xs_x = reinterpret_cast<uint32_t*>(sm + a.off_xch);
   uint32_t* xs_y = xs_x + kHSThreads;
   uint32_t* xs_o = xs_y + kHSThreads;
-  uint32_t* flag_list = reinterpret_cast<uint32_t*>(sm + a.off_list);
+  uint16_t* acc_tab = reinterpret_cast<uint16_t*>(sm + a.off_list);
+  const uint32_t inv = a.rules.copy_inv;
   __shared__ uint8_t cmap[256];
-  __shared__ uint32_t s_pp, s_nflag;
+  __shared__ uint32_t s_pp;
 
   const uint32_t tid = threadIdx.x;
   {  // DFA rows [0, norm) and accepting copies [32768, fast_bytes) -> SMEM
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
     for (uint32_t i = tid; i < n0; i += blockDim.x) dst[i] = src[i];
     for (uint32_t i = tid; i < n1; i += blockDim.x) dst[kAccRegion / 16 + i] = src[kAccRegion / 16 + i];
     if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
+    for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
   }
   const uint32_t nb = a.n_blocks;
   const uint32_t G0 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * nb) / gridDim.x);
@@ -222,7 +223,6 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   const uint32_t start_row = a.rules.start_row, eos2 = a.rules.eos2;
   while (g < G1) {
     for (uint32_t t = tid; t <= kHSThreads; t += blockDim.x) so[t] = a.blk_off[min(pp + t, a.n_prompts)];
-    if (tid == 0) s_nflag = 0;
     __syncthreads();
     uint32_t nw = min(static_cast<uint32_t>(kHSThreads), G1 - g);
     uint32_t n_so = kHSThreads + 1;
@@ -281,10 +281,10 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
         for (uint32_t k = 0; k < B; ++k) dg = fnv_u32(dg, tp[k]);
       }
       a.d_out[w.gb] = dg;
-      const uint32_t X = dfa_run(tab, cls, w.ws, w.ws + B, start_row, orr);
+      const uint32_t X = dfa_run(tab, cls, acc_tab, inv, w.ws, w.ws + B, start_row, &orr);
       e1 = min(w.we, w.ws + 2 * B);
       uint32_t o1 = 0;
-      Y = dfa_run(tab, cls, w.ws + B, e1, X, o1);
+      Y = dfa_run(tab, cls, acc_tab, inv, w.ws + B, e1, X, &o1);
       orr |= o1;
       xs_x[tid] = X;
       xs_y[tid] = Y;
@@ -301,23 +301,12 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
           orr |= xs_o[tid + 1];
           fin = xs_y[tid + 1];
         } else {
-          fin = dfa_run(tab, cls, e1, w.we, Y, orr);
+          fin = dfa_run(tab, cls, acc_tab, inv, e1, w.we, Y, &orr);
         }
       }
-      orr |= lds16(tab, fin + eos2);
-      if (orr & kAccRegion)
-        flag_list[atomicAdd(&s_nflag, 1u)] = tid;
-      else
-        a.mask_out[w.gb] = 0;
-    }
-    __syncthreads();
-    // ---- exact rule masks of the windows that matched something (compacted)
-    const uint32_t nflag = s_nflag;
-    for (uint32_t i = tid; i < nflag; i += blockDim.x) {
-      const WinGeo f = window_geo(a, so, n_so, pp, g, flag_list[i], as);
-      const uint32_t mask = dfa_exact(a.rules.full, cls, f.ws, f.we, start_row, eos2);
-      a.mask_out[f.gb] = mask;
-      if (mask) atomicMin(&a.first_sens[f.p], f.b);
+      orr |= copy_mask(acc_tab, lds16(tab, fin + eos2), inv);
+      a.mask_out[w.gb] = orr;
+      if (orr) atomicMin(&a.first_sens[w.p], w.b);
     }
     g += nw;
     if (tid == 0) {
@@ -330,34 +319,11 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------------
-// K3a: chained prefix keys + inherited labels, one lane per prompt (the FNV chain is
-// serial along a prompt, so SIMD runs across prompts).
-// ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_chain(const uint64_t* __restrict__ d, const uint32_t* __restrict__ blk_off,
-                                               const uint32_t* __restrict__ first_sens, uint32_t n_prompts,
-                                               uint64_t* __restrict__ h_out, uint8_t* __restrict__ label) {
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_prompts) return;
-  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, fs = first_sens[p];
-  uint64_t h = 0;
-#pragma unroll 4
-  for (uint32_t b = 0; b < n; ++b) {
-    h = chain_key(h, d[bo + b]);
-    h_out[bo + b] = h;
-    label[bo + b] = b >= fs ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
-  }
-}
-
-// ---------------------------------------------------------------------------------
-// K3b: warp-cooperative index probe, one warp per prompt; 32 lanes probe 32
-// consecutive block keys; ballots give the first invisible (match length m) and the
-// first missing block (k, where the commit starts).
-// ---------------------------------------------------------------------------------
+// find_slot: used by set_tiers (point lookups)
 __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, Rec* out) {
   uint64_t s = slot_hash(h, d) & ix.mask;
   for (uint64_t i = 0; i <= ix.mask; ++i) {
-    const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(ix.rec + s);
+    const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
     ulonglong2 k = rp[0];
     if (k.x == h && k.y == d) {
       ulonglong2 m = rp[1];
@@ -377,42 +343,150 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
   return kNone;
 }
 
-__global__ void __launch_bounds__(256) k_probe(Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
-                                               const uint32_t* __restrict__ blk_off, const uint64_t* __restrict__ users,
-                                               uint32_t n_prompts, uint8_t* __restrict__ decision,
-                                               uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched,
-                                               uint32_t* __restrict__ exist, uint8_t* __restrict__ tier) {
-  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint32_t lane = lane_id();
-  if (p >= n_prompts) return;
-  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
-  uint64_t user = users[p];
-  uint32_t m = n, k = n, tmax = 0;
-  for (uint32_t base = 0; base < n; base += 32) {
-    uint32_t b = base + lane;
-    bool act = b < n, found = false, vis = false;
-    uint32_t slot = kNone;
-    Rec r{};
-    if (act) {
-      slot = find_slot(ix, hk[bo + b], dk[bo + b], &r);
-      found = slot != kNone;
-      vis = found && (r.label == SKV_LABEL_PUBLIC || r.creator == user);
-    }
-    uint32_t nf = __ballot_sync(0xffffffffu, act && !found);
-    uint32_t nv = __ballot_sync(0xffffffffu, act && !vis);
-    if (m == n && nv) m = base + __ffs(nv) - 1;
-    if (k == n && nf) k = base + __ffs(nf) - 1;
-    if (act) {
-      if (b < m) {
-        decision[bo + b] = r.label == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
-        tmax = max(tmax, static_cast<uint32_t>(r.tier));
-      }
-      if (b < k) slot_out[bo + b] = slot;
-    }
-    if (k != n) break;
+// ---------------------------------------------------------------------------------
+// K3: chained prefix keys + inherited labels + warp-cooperative index probe, fused.
+//
+// A warp owns 32 consecutive prompts.  For each 32-block tile it
+//   1. stages the tile's block digests HBM -> SMEM (one coalesced 256-B load per prompt);
+//   2. runs the serial FNV chain lane-per-prompt (A.2: SIMD across prompts, the chain
+//      is serial along one prompt) and the prefix-OR label (A.4);
+//   3. writes keys and labels back coalesced;
+//   4. probes the tile for every prompt whose commit point is still unknown: lanes =
+//      32 consecutive blocks, up to 4 prompts' first-slot loads in flight per lane;
+//      ballots give the first invisible block (match length m, A.5: label == Public
+//      or creator == user, cache_index.hpp:483-485) and the first missing block (k,
+//      where the commit starts).  Probing stops at the tile holding the first miss.
+// ---------------------------------------------------------------------------------
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kCPWarps = 2;  // 2 x 16.9 KB SMEM tiles per CTA
+constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
+
+struct Probe {
+  uint32_t slot;
+  uint64_t creator;
+  uint32_t meta;  // label | owner<<8 | tier<<16 | state<<24
+};
+
+__device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint64_t d, uint64_t s, ulonglong2 k,
+                                               ulonglong2 m) {
+  for (uint64_t i = 0; i <= ix.mask; ++i) {
+    if (k.x == h && k.y == d) return Probe{static_cast<uint32_t>(s), m.x, static_cast<uint32_t>(m.y >> 32)};
+    if (k.x == 0 && k.y == 0) break;
+    s = (s + 1) & ix.mask;
+    const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
+    k = rp[0];
+    m = rp[1];
   }
-  tmax = __reduce_max_sync(0xffffffffu, tmax);
-  if (lane == 0) {
+  return Probe{kNone, 0, 0};
+}
+
+__global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
+    Index ix, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
+    const uint32_t* __restrict__ first_sens, const uint64_t* __restrict__ users, uint32_t n_prompts,
+    uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
+    uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
+    uint8_t* __restrict__ tier) {
+  __shared__ uint64_t s_d[kCPWarps][32][kPitch];
+  __shared__ uint64_t s_h[kCPWarps][32][kPitch];
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  const uint32_t p0 = (blockIdx.x * kCPWarps + wid) * 32;
+  if (p0 >= n_prompts) return;
+  const uint32_t p = p0 + lane;
+  const bool has = p < n_prompts;
+  const uint32_t bo = has ? blk_off[p] : 0, n = has ? blk_off[p + 1] - bo : 0;
+  const uint32_t fs = has ? first_sens[p] : 0;
+  const uint64_t user = has ? users[p] : 0;
+  uint64_t (*td)[kPitch] = s_d[wid];
+  uint64_t (*th)[kPitch] = s_h[wid];
+  uint64_t h = 0;
+  uint32_t m = n, k = n, tmax = 0;  // m, k == n: not determined yet
+  const uint32_t nmax = __reduce_max_sync(kFull, n);
+  for (uint32_t t0 = 0; t0 < nmax; t0 += 32) {
+    const uint32_t b = t0 + lane;
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
+      if (b < nj) td[j][lane] = dk[bj + b];
+    }
+    __syncwarp();
+    const uint32_t cnt = n > t0 ? min(32u, n - t0) : 0u;
+    for (uint32_t c = 0; c < cnt; ++c) {
+      h = chain_key(h, td[lane][c]);
+      th[lane][c] = h;
+    }
+    __syncwarp();
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
+      const uint32_t fsj = __shfl_sync(kFull, fs, j);
+      if (b < nj) {
+        hk[bj + b] = th[j][lane];
+        label[bj + b] = b >= fsj ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
+      }
+    }
+    uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
+    while (todo) {
+      uint32_t js[4];
+      int ng = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        js[q] = todo ? static_cast<uint32_t>(__ffs(todo) - 1) : 32u;
+        if (todo) {
+          todo &= todo - 1;
+          ++ng;
+        }
+      }
+      // issue up to 4 independent first-slot loads per lane
+      ulonglong2 kk[4], mm[4];
+      uint64_t ss[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t j = js[q] & 31;
+        const uint32_t nj = __shfl_sync(kFull, n, j);
+        kk[q] = make_ulonglong2(0, 0);
+        mm[q] = make_ulonglong2(0, 0);
+        ss[q] = 0;
+        if (q < ng && b < nj) {
+          ss[q] = slot_hash(th[j][lane], td[j][lane]) & ix.mask;
+          const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[ss[q]].rec);
+          kk[q] = rp[0];
+          mm[q] = rp[1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q >= ng) break;
+        const uint32_t j = js[q];
+        const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
+        const uint64_t uj = __shfl_sync(kFull, user, j);
+        const uint32_t mj = __shfl_sync(kFull, m, j);
+        const bool act = b < nj;
+        Probe pr{kNone, 0, 0};
+        if (act) pr = probe_resolve(ix, th[j][lane], td[j][lane], ss[q], kk[q], mm[q]);
+        const bool found = pr.slot != kNone;
+        const uint32_t lab = pr.meta & 0xffu;
+        const bool vis = found && (lab == SKV_LABEL_PUBLIC || pr.creator == uj);
+        const uint32_t nf = __ballot_sync(kFull, act && !found);
+        const uint32_t nv = __ballot_sync(kFull, act && !vis);
+        const uint32_t new_m = (mj == nj && nv) ? t0 + __ffs(nv) - 1 : mj;
+        const uint32_t new_k = nf ? t0 + __ffs(nf) - 1 : nj;
+        uint32_t tm = 0;
+        if (act) {
+          if (b < new_m) {
+            decision[bj + b] = lab == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
+            tm = (pr.meta >> 16) & 0xffu;
+          }
+          if (b < new_k) slot_out[bj + b] = pr.slot;
+        }
+        tm = __reduce_max_sync(kFull, tm);
+        if (lane == j) {
+          m = new_m;
+          k = new_k;
+          tmax = max(tmax, tm);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (has) {
     matched[p] = m;
     exist[p] = k;
     tier[p] = static_cast<uint8_t>(tmax);
@@ -452,13 +526,13 @@ __global__ void __launch_bounds__(256) k_record(Index ix, const uint32_t* __rest
     const uint32_t slot = unique[r], cnt = counts[r], start = starts[r];
     uint32_t si = 0;
     if (lane == 0) {
-      si = ix.aux[slot].set_idx;
+      si = ix.e[slot].aux.set_idx;
       if (si == kNone) {
         si = atomicAdd(pool_count, 1u);
         if (si >= pool_cap) {
           atomicOr(err_flag, 1u);
         } else {
-          ix.aux[slot].set_idx = si;
+          ix.e[slot].aux.set_idx = si;
           set_size[si] = 0;
           touched[atomicAdd(n_touched, 1u)] = slot;
         }
@@ -512,8 +586,8 @@ __global__ void __launch_bounds__(256) k_record(Index ix, const uint32_t* __rest
     if (lane + 32 >= size0 && lane + 32 < size) set[lane + 32] = m1;
     if (lane == 0) {
       set_size[si] = size;
-      ix.stats[slot].hit_cur += cnt;
-      ix.stats[slot].u_cnt += add_total;
+      ix.e[slot].stats.hit_cur += cnt;
+      ix.e[slot].stats.u_cnt += add_total;
     }
   }
 }
@@ -545,14 +619,14 @@ __global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restr
   uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
-  const unsigned long long tag = (static_cast<unsigned long long>(batch) << 32) | (0xffffffffu - p);
+  const uint32_t tag = 0xffffffffu - p;  // >= 2^31: never equal to an epoch stamp
   for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
     uint64_t h = hk[bo + b], d = dk[bo + b];
     uint64_t s = slot_hash(h, d) & ix.mask;
     uint64_t i = 0;
     for (; i <= ix.mask; ++i) {
       unsigned long long ol, oh;
-      unsigned long long* kp = reinterpret_cast<unsigned long long*>(ix.rec + s);
+      unsigned long long* kp = reinterpret_cast<unsigned long long*>(&ix.e[s].rec);
       if (cas128(kp, 0ull, 0ull, h, d, &ol, &oh) || (ol == h && oh == d)) break;
       s = (s + 1) & ix.mask;
     }
@@ -560,7 +634,7 @@ __global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restr
       atomicOr(err_flag, 2u);
       return;
     }
-    atomicMax(&ix.claim[s], tag);
+    atomicMax(&ix.e[s].aux.mark, tag);
     slot_out[bo + b] = static_cast<uint32_t>(s);
   }
 }
@@ -573,20 +647,22 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint32_t* __rest
   uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
-  const unsigned long long tag = (static_cast<unsigned long long>(batch) << 32) | (0xffffffffu - p);
+  const uint32_t tag = 0xffffffffu - p;
   uint32_t mine = 0;
   for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
     uint32_t s = slot[bo + b];
-    if (ix.claim[s] != tag || ix.rec[s].state != 0) continue;
+    if (ix.e[s].aux.mark != tag || ix.e[s].rec.state != 0) continue;
     uint32_t parent = b > 0 ? slot[bo + b - 1] : kNone;
-    Rec& r = ix.rec[s];
-    r.creator = users[p];
-    r.parent = parent;
-    r.label = label[bo + b];
-    r.owner = owners ? owners[p] : 0;
-    r.tier = SKV_TIER_HBM;
-    r.state = 1;
-    if (parent != kNone) ix.aux[s].next_sibling = atomicExch(&ix.aux[parent].first_child, s);
+    // creator | parent, label, owner, tier=HBM, state=live: one 16-B store completing the
+    // key sector written by k_claim's CAS
+    const uint32_t meta = static_cast<uint32_t>(label[bo + b]) | (static_cast<uint32_t>(owners ? owners[p] : 0) << 8) |
+                          (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
+    ulonglong2 payload;
+    payload.x = users[p];
+    payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
+    reinterpret_cast<ulonglong2*>(&ix.e[s].rec)[1] = payload;
+    ix.e[s].aux.mark = 0;
+    if (parent != kNone) ix.e[s].aux.next_sibling = atomicExch(&ix.e[parent].aux.first_child, s);
     ++mine;
   }
   mine = __reduce_add_sync(0xffffffffu, mine);
@@ -613,14 +689,14 @@ __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, 
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_list) return;
   uint32_t s = list[i];
-  if (only_untouched && ix.aux[s].set_idx != kNone) return;
-  if (ix.rec[s].label != SKV_LABEL_PUBLIC) return;
-  Stats st = ix.stats[s];
+  if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
+  if (ix.e[s].rec.label != SKV_LABEL_PUBLIC) return;
+  Stats st = ix.e[s].stats;
   if (st.hit_pre == 0) return;
   double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
   double prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
   if ((now - prev) >= jump && static_cast<uint64_t>(st.u_pre) <= u_pre_max) {
-    ix.aux[s].cand = stamp;
+    ix.e[s].aux.mark = stamp;
     cands[atomicAdd(n_cands, 1u)] = s;
   }
 }
@@ -631,10 +707,10 @@ __global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_cands) return;
   uint32_t s = cands[i];
-  for (uint32_t a = ix.rec[s].parent; a != kNone; a = ix.rec[a].parent)
-    if (ix.aux[a].cand == stamp) return;
-  Stats st = ix.stats[s];
-  const Rec& r = ix.rec[s];
+  for (uint32_t a = ix.e[s].rec.parent; a != kNone; a = ix.e[a].rec.parent)
+    if (ix.e[a].aux.mark == stamp) return;
+  Stats st = ix.e[s].stats;
+  const Rec& r = ix.e[s].rec;
   uint32_t e = atomicAdd(n_events, 1u);
   DevEvent ev;
   ev.h = r.h;
@@ -654,19 +730,19 @@ __global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, 
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_fired) return;
   uint32_t root = fired[i];
-  uint8_t lab = ix.rec[root].owner == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
-  ix.rec[root].label = lab;
-  uint32_t cur = ix.aux[root].first_child;
+  uint8_t lab = ix.e[root].rec.owner == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+  ix.e[root].rec.label = lab;
+  uint32_t cur = ix.e[root].aux.first_child;
   while (cur != kNone) {
-    ix.rec[cur].label = lab;
-    uint32_t c = ix.aux[cur].first_child;
+    ix.e[cur].rec.label = lab;
+    uint32_t c = ix.e[cur].aux.first_child;
     if (c != kNone) {
       cur = c;
       continue;
     }
-    while (cur != root && ix.aux[cur].next_sibling == kNone) cur = ix.rec[cur].parent;
+    while (cur != root && ix.e[cur].aux.next_sibling == kNone) cur = ix.e[cur].rec.parent;
     if (cur == root) break;
-    cur = ix.aux[cur].next_sibling;
+    cur = ix.e[cur].aux.next_sibling;
   }
 }
 
@@ -676,14 +752,14 @@ __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const 
   if (i >= *n_list) return;
   uint32_t s = list[i];
   if (prev_list) {
-    if (ix.aux[s].set_idx != kNone) return;  // rolled by the current-window list
+    if (ix.e[s].aux.set_idx != kNone) return;  // rolled by the current-window list
     Stats z{0, 0, 0, 0};
-    ix.stats[s] = z;
+    ix.e[s].stats = z;
   } else {
-    Stats st = ix.stats[s];
+    Stats st = ix.e[s].stats;
     Stats r{0, 0, st.hit_cur, st.u_cnt};
-    ix.stats[s] = r;
-    ix.aux[s].set_idx = kNone;
+    ix.e[s].stats = r;
+    ix.e[s].aux.set_idx = kNone;
   }
 }
 
@@ -695,15 +771,15 @@ __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, cons
   if (i >= n) return;
   Rec r;
   uint32_t s = find_slot(ix, h[i], d[i], &r);
-  if (s != kNone) ix.rec[s].tier = tiers[i];
+  if (s != kNone) ix.e[s].rec.tier = tiers[i];
 }
 
 __global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
   uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s > ix.mask) return;
-  const Rec& r = ix.rec[s];
+  const Rec& r = ix.e[s].rec;
   if (r.h == 0 && r.d == 0) return;
-  Stats st = ix.stats[s];
+  Stats st = ix.e[s].stats;
   skv_entry e;
   e.h = r.h;
   e.d = r.d;
@@ -781,7 +857,7 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
   L.off_raw = place(L.stage);
   L.off_so = place((kHSThreads + 1) * 4);
   L.off_xch = place(3 * kHSThreads * 4);
-  L.off_list = place(kHSThreads * 4);
+  L.off_list = place(r.n_copies * 2);  // accepting-copy -> rule mask (u16)
   L.total = tail;
   return L;
 }
@@ -804,16 +880,12 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream
   k_hash_scan<<<g, kHSThreads, smem, s>>>(a);
 }
 
-void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n, uint64_t* h,
-                  uint8_t* label, cudaStream_t s) {
-  if (n) k_chain<<<cdiv(n, 128), 128, 0, s>>>(d, blk_off, first_sens, n, h, label);
-}
-
-void launch_probe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                  const uint64_t* users, uint32_t n, uint8_t* decision, uint32_t* slot, uint32_t* matched,
-                  uint32_t* exist, uint8_t* tier, cudaStream_t s) {
-  if (n) k_probe<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, users, n, decision, slot,
-                                                                          matched, exist, tier);
+void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
+                        const uint64_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s) {
+  if (n)
+    k_chain_probe<<<cdiv(n, 32 * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
+                                                                   decision, slot, matched, exist, tier);
 }
 
 void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
@@ -921,4 +993,23 @@ void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream
   k_digest<<<1, 32, 0, s>>>(tokens, n, out);
 }
 
+}  // namespace skv
+
+namespace skv {
+namespace {
+__global__ void k_init_entries(Index ix) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  ulonglong2* p = reinterpret_cast<ulonglong2*>(&ix.e[s]);
+  const ulonglong2 z = {0ull, 0ull};
+  p[0] = z;
+  p[1] = z;
+  p[2] = z;
+  p[3] = {0xffffffffffffffffull, 0x00000000ffffffffull};  // first_child, next_sibling, set_idx = none; mark = 0
+}
+}  // namespace
+
+void launch_init_entries(const Index& ix, cudaStream_t s) {
+  k_init_entries<<<static_cast<uint32_t>((ix.cap + 255) / 256), 256, 0, s>>>(ix);
+}
 }  // namespace skv
