@@ -638,9 +638,8 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     ++c->batch_id;
-    skv::launch_claim(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->p_n, c->batch_id, c->bslot, c->counters + 5, s);
-    skv::launch_commit(c->ix, c->blk_off, c->exist, c->blabel, c->p_users, c->p_owners, c->p_n, c->batch_id, c->bslot,
-                       c->n_new, s);
+    skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->p_users, c->p_owners, c->p_n, c->bslot,
+                       c->n_new, c->counters + 5, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));

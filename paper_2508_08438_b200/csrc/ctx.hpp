@@ -35,7 +35,7 @@ struct __align__(16) Stats {
 struct __align__(16) Aux {
   uint32_t first_child, next_sibling;  // subtree walk for label propagation
   uint32_t set_idx;                    // user-set pool slot for the current window, kNone if untouched
-  uint32_t mark;  // commit: intra-batch claim (~prompt, >= 2^31); epoch: candidate stamp (= epoch)
+  uint32_t mark;  // commit: intra-batch claim 0xffffffff-prompt (>= 2^31); epoch: candidate stamp (< 2^31)
 };
 
 // One index slot = 64 B: sector 0 is everything the probe reads, sector 1 the monitor
@@ -129,12 +129,9 @@ void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* coun
                    const uint32_t* n_runs, const uint32_t* vals, const uint64_t* users,
                    unsigned long long* sets, uint32_t* set_size, uint32_t pool_cap, uint32_t* pool_count,
                    uint32_t* touched, uint32_t* n_touched, uint32_t* err_flag, int grid, cudaStream_t s);
-void launch_claim(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                  const uint32_t* exist, uint32_t n_prompts, uint32_t batch, uint32_t* slot, uint32_t* err_flag,
-                  cudaStream_t s);
-void launch_commit(const Index& ix, const uint32_t* blk_off, const uint32_t* exist, const uint8_t* label,
-                   const uint64_t* users, const uint8_t* owners, uint32_t n_prompts, uint32_t batch,
-                   const uint32_t* slot, unsigned long long* n_new, cudaStream_t s);
+void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                   const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
+                   uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* err_flag, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
                              int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
                              uint32_t* n_cands, cudaStream_t s);

@@ -113,6 +113,26 @@ __device__ __forceinline__ uint32_t dfa_run(const uint8_t* __restrict__ tab, con
     row = lds16(tab, row + cls[o++]);
     m |= copy_mask(acc_tab, row, inv);
   }
+  // 16-byte groups: PRMT byte extraction, one acceptance test per group
+  for (; o + 16 <= end; o += 16) {
+    uint32_t r[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o + 4 * q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        row = lds16(tab, row + __byte_perm(w, 0u, 0x4440u + k));
+        r[4 * q + k] = row;
+      }
+    }
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) any |= r[q];
+    if (any & kAccRegion) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) m |= copy_mask(acc_tab, r[q], inv);
+    }
+  }
   for (; o + 4 <= end; o += 4) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
     const uint32_t r0 = lds16(tab, row + (w & 0xffu));
@@ -161,15 +181,16 @@ struct WinGeo {
   uint32_t gb, p, b, ws, we;
 };
 
-__device__ __forceinline__ WinGeo window_geo(const HashScanArgs& a, const uint32_t* so, uint32_t n_so, uint32_t pp,
-                                             uint32_t g, uint32_t t, uint64_t as) {
+// so[i] = blk_off[pp + i], so_tok[i] = tok_off[pp + i] (SMEM copies for the chunk)
+__device__ __forceinline__ WinGeo window_geo(const HashScanArgs& a, const uint32_t* so, const uint64_t* so_tok,
+                                             uint32_t n_so, uint32_t pp, uint32_t g, uint32_t t, uint64_t as) {
   WinGeo w;
   w.gb = g + t;
   const uint32_t i = so_search(so, n_so, w.gb);
   w.p = pp + i;
   w.b = w.gb - so[i];
-  const uint64_t base = a.tok_off[w.p];
-  const uint64_t L = a.tok_off[w.p + 1] - base;
+  const uint64_t base = so_tok[i];
+  const uint64_t L = so_tok[i + 1] - base;
   w.ws = static_cast<uint32_t>(base + static_cast<uint64_t>(w.b) * a.B - as);
   const uint64_t wend = min(L, static_cast<uint64_t>(w.b) * a.B + a.B + a.W);
   w.we = static_cast<uint32_t>(base + wend - as);
@@ -182,6 +203,7 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   uint8_t* cls = sm + a.off_cls;
   uint8_t* raw = sm + a.off_raw;
   uint32_t* so = reinterpret_cast<uint32_t*>(sm + a.off_so);
+  uint64_t* so_tok = reinterpret_cast<uint64_t*>(sm + a.off_so + round16((kHSThreads + 1) * 4));
   uint32_t* xs_x = reinterpret_cast<uint32_t*>(sm + a.off_xch);
   uint32_t* xs_y = xs_x + kHSThreads;
   uint32_t* xs_o = xs_y + kHSThreads;
@@ -222,27 +244,27 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
   const uint32_t B = a.B, W = a.W;
   const uint32_t start_row = a.rules.start_row, eos2 = a.rules.eos2;
   while (g < G1) {
-    for (uint32_t t = tid; t <= kHSThreads; t += blockDim.x) so[t] = a.blk_off[min(pp + t, a.n_prompts)];
+    for (uint32_t t = tid; t <= kHSThreads; t += blockDim.x) {
+      const uint32_t q = min(pp + t, a.n_prompts);
+      so[t] = a.blk_off[q];
+      so_tok[t] = a.tok_off[q];
+    }
     __syncthreads();
     uint32_t nw = min(static_cast<uint32_t>(kHSThreads), G1 - g);
-    uint32_t n_so = kHSThreads + 1;
-    if (pp + kHSThreads <= a.n_prompts)
-      nw = min(nw, so[kHSThreads] - g);
-    else
-      n_so = a.n_prompts - pp + 1;
+    if (pp + kHSThreads <= a.n_prompts) nw = min(nw, so[kHSThreads] - g);
     uint32_t lastg = g + nw - 1;
-    uint32_t il = so_search(so, n_so, lastg);
-    const uint64_t s_tok = a.tok_off[pp] + static_cast<uint64_t>(g - so[0]) * B;
-    uint64_t e_tok = min(a.tok_off[pp + il + 1],
-                         a.tok_off[pp + il] + static_cast<uint64_t>(lastg - so[il] + 1) * B + W);
+    // il = index of the prompt holding lastg = number of prompt starts in (g, lastg]
+    uint32_t il = __syncthreads_count(tid < kHSThreads && pp + tid + 1 <= a.n_prompts && so[tid + 1] <= lastg);
+    const uint64_t s_tok = so_tok[0] + static_cast<uint64_t>(g - so[0]) * B;
+    uint64_t e_tok = min(so_tok[il + 1], so_tok[il] + static_cast<uint64_t>(lastg - so[il] + 1) * B + W);
     const uint64_t as = s_tok & ~3ull;
     if (e_tok - as > a.stage - 8) {  // too many prompt tails in the span: single-prompt chunk
       nw = min(nw, so[1] - g);
       lastg = g + nw - 1;
       il = 0;
-      e_tok = min(a.tok_off[pp + 1], a.tok_off[pp] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
+      e_tok = min(so_tok[1], so_tok[0] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
     }
-    n_so = il + 1;
+    const uint32_t n_so = il + 1;
     // ---- stage tokens -> (2*class, raw byte); 4 tokens per 128-bit streaming load
     const uint32_t nq = static_cast<uint32_t>((e_tok - as + 3) >> 2);
     uint32_t wide = 0;
@@ -271,7 +293,7 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
     uint32_t Y = 0, orr = 0, e1 = 0;
     const bool act = tid < nw;
     if (act) {
-      w = window_geo(a, so, n_so, pp, g, tid, as);
+      w = window_geo(a, so, so_tok, n_so, pp, g, tid, as);
       uint64_t dg;
       if (!wide) {
         dg = digest_bytes(raw, w.ws, B, a.digest_init);
@@ -593,9 +615,7 @@ __global__ void __launch_bounds__(256) k_record(Index ix, const uint32_t* __rest
 }
 
 // ---------------------------------------------------------------------------------
-// K6: commit.  k_claim inserts the keys of new blocks (128-bit CAS on the key) and
-// arbitrates intra-batch duplicates with atomicMax(batch<<32 | ~prompt) -> lowest
-// prompt wins; k_commit lets each winner write its record and link it under its parent.
+// K6: commit (insert the new blocks of the batch).
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long long cmp_lo, unsigned long long cmp_hi,
                                        unsigned long long new_lo, unsigned long long new_hi,
@@ -612,61 +632,95 @@ __device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long l
   return *old_lo == cmp_lo && *old_hi == cmp_hi;
 }
 
-__global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
-                                               const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist,
-                                               uint32_t n_prompts, uint32_t batch, uint32_t* __restrict__ slot_out,
-                                               uint32_t* err_flag) {
-  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_prompts) return;
-  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
-  const uint32_t tag = 0xffffffffu - p;  // >= 2^31: never equal to an epoch stamp
-  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
-    uint64_t h = hk[bo + b], d = dk[bo + b];
-    uint64_t s = slot_hash(h, d) & ix.mask;
-    uint64_t i = 0;
-    for (; i <= ix.mask; ++i) {
-      unsigned long long ol, oh;
-      unsigned long long* kp = reinterpret_cast<unsigned long long*>(&ix.e[s].rec);
-      if (cas128(kp, 0ull, 0ull, h, d, &ol, &oh) || (ol == h && oh == d)) break;
-      s = (s + 1) & ix.mask;
-    }
-    if (i > ix.mask) {
-      atomicOr(err_flag, 2u);
-      return;
-    }
-    atomicMax(&ix.e[s].aux.mark, tag);
-    slot_out[bo + b] = static_cast<uint32_t>(s);
-  }
+__device__ __forceinline__ void st128_atomic(void* addr, unsigned long long lo, unsigned long long hi) {
+  asm volatile(
+      "{\n\t.reg .b128 n, d;\n\t"
+      "mov.b128 n, {%0, %1};\n\t"
+      "atom.global.exch.b128 d, [%2], n;\n\t}"
+      :
+      : "l"(lo), "l"(hi), "l"(addr)
+      : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_commit(Index ix, const uint32_t* __restrict__ blk_off,
+// Commit (A.7), one pass, no grid barrier.  Lanes of the warp of prompt p walk its new
+// blocks b >= k_p (k_p = first block missing before the batch, from k_chain_probe):
+//   * CAS the key into its slot; the thread whose CAS inserted it links the entry under
+//     its parent (the previous block's slot, same for every duplicate) exactly once;
+//   * intra-batch duplicates: mark = atomicMax(0xffffffff - p), i.e. the lowest prompt
+//     index wins (first creator in prompt order, cache_index.hpp:164-168).  Every
+//     claimant that was the best so far writes the payload of the CURRENT winner w --
+//     (users[w], label[w][b], owners[w], parent) is reconstructible by any thread --
+//     with a 128-bit atomic store, then re-reads mark and repeats until it is stable.
+//     The last store to the payload is therefore the final winner's.
+// Claim values are >= 2^31 and never collide with the epoch candidate stamps (< 2^31)
+// kept in the same word.
+__global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
+                                                const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
                                                 const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
-                                                uint32_t n_prompts, uint32_t batch, const uint32_t* __restrict__ slot,
-                                                unsigned long long* n_new) {
-  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                                                uint32_t n_prompts, uint32_t* __restrict__ slot_out,
+                                                unsigned long long* n_new, uint32_t* err_flag) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
-  uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  const uint32_t lane = lane_id();
+  const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
+  if (k0 >= n) return;
   const uint32_t tag = 0xffffffffu - p;
-  uint32_t mine = 0;
-  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
-    uint32_t s = slot[bo + b];
-    if (ix.e[s].aux.mark != tag || ix.e[s].rec.state != 0) continue;
-    uint32_t parent = b > 0 ? slot[bo + b - 1] : kNone;
-    // creator | parent, label, owner, tier=HBM, state=live: one 16-B store completing the
-    // key sector written by k_claim's CAS
-    const uint32_t meta = static_cast<uint32_t>(label[bo + b]) | (static_cast<uint32_t>(owners ? owners[p] : 0) << 8) |
-                          (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
-    ulonglong2 payload;
-    payload.x = users[p];
-    payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
-    reinterpret_cast<ulonglong2*>(&ix.e[s].rec)[1] = payload;
-    ix.e[s].aux.mark = 0;
-    if (parent != kNone) ix.e[s].aux.next_sibling = atomicExch(&ix.e[parent].aux.first_child, s);
-    ++mine;
+  // parent of the first new block: the last pre-existing block's slot (from the probe)
+  uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;
+  uint32_t inserted = 0;
+  for (uint32_t base = k0; base < n; base += 32) {
+    const uint32_t b = base + lane;
+    const bool act = b < n;
+    uint32_t s32 = kNone;
+    bool mine = false;
+    if (act) {
+      const uint64_t h = hk[bo + b], d = dk[bo + b];
+      uint64_t s = slot_hash(h, d) & ix.mask;
+      uint64_t i = 0;
+      for (; i <= ix.mask; ++i) {
+        unsigned long long ol, oh;
+        unsigned long long* kp = reinterpret_cast<unsigned long long*>(&ix.e[s].rec);
+        if (cas128(kp, 0ull, 0ull, h, d, &ol, &oh)) {
+          mine = true;
+          break;
+        }
+        if (ol == h && oh == d) break;
+        s = (s + 1) & ix.mask;
+      }
+      if (i > ix.mask) atomicOr(err_flag, 2u);
+      s32 = static_cast<uint32_t>(s);
+      slot_out[bo + b] = s32;
+    }
+    // parent slot: the previous block's slot (lane - 1, or the carry from the last round)
+    uint32_t parent = __shfl_up_sync(kFull, s32, 1);
+    if (lane == 0) parent = carry;
+    carry = __shfl_sync(kFull, s32, 31);
+    if (act && s32 != kNone) {
+      Entry& e = ix.e[s32];
+      const uint32_t old = atomicMax(&e.aux.mark, tag);
+      if (old < tag) {
+        for (;;) {
+          const uint32_t w = *reinterpret_cast<volatile uint32_t*>(&e.aux.mark);
+          const uint32_t pw = 0xffffffffu - w;
+          const uint32_t bw = blk_off[pw] + b;
+          const uint32_t meta = static_cast<uint32_t>(label[bw]) |
+                                (static_cast<uint32_t>(owners ? owners[pw] : 0) << 8) |
+                                (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
+          st128_atomic(reinterpret_cast<ulonglong2*>(&e.rec) + 1, users[pw],
+                       static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32));
+          __threadfence();
+          if (*reinterpret_cast<volatile uint32_t*>(&e.aux.mark) == w) break;
+        }
+      }
+      if (mine) {
+        if (parent != kNone) e.aux.next_sibling = atomicExch(&ix.e[parent].aux.first_child, s32);
+        ++inserted;
+      }
+    }
   }
-  mine = __reduce_add_sync(0xffffffffu, mine);
-  if (lane_id() == 0 && mine) atomicAdd(n_new, static_cast<unsigned long long>(mine));
+  inserted = __reduce_add_sync(kFull, inserted);
+  if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
 }
 
 // ---------------------------------------------------------------------------------
@@ -855,7 +909,7 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
   };
   L.off_cls = place(L.stage);
   L.off_raw = place(L.stage);
-  L.off_so = place((kHSThreads + 1) * 4);
+  L.off_so = place(round16((kHSThreads + 1) * 4) + (kHSThreads + 1) * 8);  // so[] + so_tok[]
   L.off_xch = place(3 * kHSThreads * 4);
   L.off_list = place(r.n_copies * 2);  // accepting-copy -> rule mask (u16)
   L.total = tail;
@@ -935,19 +989,12 @@ void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* coun
                                 touched, n_touched, err_flag);
 }
 
-void launch_claim(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                  const uint32_t* exist, uint32_t n, uint32_t batch, uint32_t* slot, uint32_t* err_flag,
-                  cudaStream_t s) {
-  if (n) k_claim<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, n, batch, slot,
-                                                                         err_flag);
-}
-
-void launch_commit(const Index& ix, const uint32_t* blk_off, const uint32_t* exist, const uint8_t* label,
-                   const uint64_t* users, const uint8_t* owners, uint32_t n, uint32_t batch, const uint32_t* slot,
-                   unsigned long long* n_new, cudaStream_t s) {
+void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
+                   const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
+                   uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* err_flag, cudaStream_t s) {
   if (n)
-    k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, blk_off, exist, label, users, owners, n,
-                                                                      batch, slot, n_new);
+    k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, label, users, owners,
+                                                                      n, slot, n_new, err_flag);
 }
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
