@@ -97,7 +97,7 @@ struct skv_ctx {
   uint32_t* set_size = nullptr;
   uint32_t pool_cap = 0;
   uint32_t* touched[2] = {nullptr, nullptr};
-  uint32_t* counters = nullptr;  // [0]=pool_count [1..2]=n_touched[2] [3]=n_cands [4]=n_events [5]=err_flag [6]=n_runs
+  uint32_t* counters = nullptr;  // [0]=pool_count [1..2]=n_touched[2] [3]=n_cands [4]=n_events [5]=err_flag [6]=n_runs [7]=n_fix
   unsigned long long* n_new = nullptr;
   int cur = 0;
   uint32_t* cands = nullptr;
@@ -126,6 +126,7 @@ struct skv_ctx {
   uint32_t* bslot = nullptr;
   uint32_t *key_a = nullptr, *key_b = nullptr, *val_a = nullptr, *val_b = nullptr;
   uint32_t *uniq = nullptr, *runs = nullptr, *starts = nullptr;
+  uint32_t* fix_list = nullptr;  // commit: duplicate-key slots + depths (2 x max_blocks)
   void* temp = nullptr;
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
@@ -428,6 +429,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->uniq = dalloc<uint32_t>(NB, c->owned);
     c->runs = dalloc<uint32_t>(NB, c->owned);
     c->starts = dalloc<uint32_t>(NB, c->owned);
+    c->fix_list = dalloc<uint32_t>(2 * NB, c->owned);
     size_t tb = std::max({skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
                           skv::sort_temp_bytes(static_cast<uint32_t>(NB), log2u(cap)),
                           skv::rle_temp_bytes(static_cast<uint32_t>(NB))});
@@ -637,9 +639,11 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       throw CapacityError("index capacity exhausted (eviction is not part of this path)");
     CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
+    CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));  // intra-batch duplicate fix-up count
     ++c->batch_id;
     skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->p_users, c->p_owners, c->p_n, c->bslot,
-                       c->n_new, c->counters + 5, s);
+                       c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
+                       static_cast<int>(c->rec_grid), s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));

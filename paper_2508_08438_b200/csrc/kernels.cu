@@ -632,26 +632,18 @@ __device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long l
   return *old_lo == cmp_lo && *old_hi == cmp_hi;
 }
 
-__device__ __forceinline__ void st128_atomic(void* addr, unsigned long long lo, unsigned long long hi) {
-  asm volatile(
-      "{\n\t.reg .b128 n, d;\n\t"
-      "mov.b128 n, {%0, %1};\n\t"
-      "atom.global.exch.b128 d, [%2], n;\n\t}"
-      :
-      : "l"(lo), "l"(hi), "l"(addr)
-      : "memory");
-}
-
-// Commit (A.7), one pass, no grid barrier.  Lanes of the warp of prompt p walk its new
-// blocks b >= k_p (k_p = first block missing before the batch, from k_chain_probe):
-//   * CAS the key into its slot; the thread whose CAS inserted it links the entry under
-//     its parent (the previous block's slot, same for every duplicate) exactly once;
-//   * intra-batch duplicates: mark = atomicMax(0xffffffff - p), i.e. the lowest prompt
-//     index wins (first creator in prompt order, cache_index.hpp:164-168).  Every
-//     claimant that was the best so far writes the payload of the CURRENT winner w --
-//     (users[w], label[w][b], owners[w], parent) is reconstructible by any thread --
-//     with a 128-bit atomic store, then re-reads mark and repeats until it is stable.
-//     The last store to the payload is therefore the final winner's.
+// Commit (A.7).  Lanes of the warp of prompt p walk its new blocks b >= k_p (k_p = the
+// first block missing before the batch, from k_chain_probe):
+//   * CAS the key into its slot.  The inserting thread writes ITS payload (creator,
+//     parent slot, label, owner, tier = HBM, live) with one 16-B store and links the
+//     entry under its parent (the previous block's slot -- identical for every
+//     duplicate of the key) exactly once;
+//   * every claimant also does mark = atomicMax(0xffffffff - p): the maximum is the
+//     lowest prompt index, i.e. the first creator in prompt order (cache_index.hpp:164-168);
+//   * a claimant whose CAS found the key already inserted by this batch is an
+//     intra-batch duplicate: it appends the slot to a (rare) fix-up list, and
+//     k_commit_fixup -- stream-ordered after this kernel, when every claim is final --
+//     rewrites the payload from the winning prompt.
 // Claim values are >= 2^31 and never collide with the epoch candidate stamps (< 2^31)
 // kept in the same word.
 __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
@@ -659,23 +651,27 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
                                                 const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
                                                 uint32_t n_prompts, uint32_t* __restrict__ slot_out,
-                                                unsigned long long* n_new, uint32_t* err_flag) {
+                                                unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
+                                                uint32_t fix_cap, uint32_t* err_flag) {
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   const uint32_t lane = lane_id();
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) return;
   const uint32_t tag = 0xffffffffu - p;
-  // parent of the first new block: the last pre-existing block's slot (from the probe)
-  uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;
+  const unsigned long long creator = users[p];
+  const uint32_t owner_bits = static_cast<uint32_t>(owners ? owners[p] : 0) << 8;
+  uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
   uint32_t inserted = 0;
   for (uint32_t base = k0; base < n; base += 32) {
     const uint32_t b = base + lane;
     const bool act = b < n;
     uint32_t s32 = kNone;
     bool mine = false;
+    uint32_t lab = 0;
     if (act) {
       const uint64_t h = hk[bo + b], d = dk[bo + b];
+      lab = label[bo + b];
       uint64_t s = slot_hash(h, d) & ix.mask;
       uint64_t i = 0;
       for (; i <= ix.mask; ++i) {
@@ -692,35 +688,53 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       s32 = static_cast<uint32_t>(s);
       slot_out[bo + b] = s32;
     }
-    // parent slot: the previous block's slot (lane - 1, or the carry from the last round)
     uint32_t parent = __shfl_up_sync(kFull, s32, 1);
     if (lane == 0) parent = carry;
     carry = __shfl_sync(kFull, s32, 31);
     if (act && s32 != kNone) {
       Entry& e = ix.e[s32];
-      const uint32_t old = atomicMax(&e.aux.mark, tag);
-      if (old < tag) {
-        for (;;) {
-          const uint32_t w = *reinterpret_cast<volatile uint32_t*>(&e.aux.mark);
-          const uint32_t pw = 0xffffffffu - w;
-          const uint32_t bw = blk_off[pw] + b;
-          const uint32_t meta = static_cast<uint32_t>(label[bw]) |
-                                (static_cast<uint32_t>(owners ? owners[pw] : 0) << 8) |
-                                (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
-          st128_atomic(reinterpret_cast<ulonglong2*>(&e.rec) + 1, users[pw],
-                       static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32));
-          __threadfence();
-          if (*reinterpret_cast<volatile uint32_t*>(&e.aux.mark) == w) break;
-        }
-      }
+      atomicMax(&e.aux.mark, tag);
       if (mine) {
+        const uint32_t meta = lab | owner_bits | (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
+        ulonglong2 payload;
+        payload.x = creator;
+        payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
+        reinterpret_cast<ulonglong2*>(&e.rec)[1] = payload;
         if (parent != kNone) e.aux.next_sibling = atomicExch(&ix.e[parent].aux.first_child, s32);
         ++inserted;
+      } else {
+        const uint32_t f = atomicAdd(n_fix, 1u);
+        if (f < fix_cap)
+          fix_list[f] = s32;
+        else
+          atomicOr(err_flag, 4u);
+        if (f < fix_cap) fix_list[fix_cap + f] = b;  // block depth of this key
       }
     }
   }
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
+}
+
+// Intra-batch duplicates: write the final winner's payload (all claims are complete).
+__global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
+                               const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
+                               const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
+                               uint32_t fix_cap) {
+  const uint32_t nf = min(*n_fix, fix_cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
+    Entry& e = ix.e[s];
+    const uint32_t pw = 0xffffffffu - e.aux.mark;
+    const uint32_t parent = e.rec.parent;
+    const uint32_t meta = static_cast<uint32_t>(label[blk_off[pw] + b]) |
+                          (static_cast<uint32_t>(owners ? owners[pw] : 0) << 8) |
+                          (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
+    ulonglong2 payload;
+    payload.x = users[pw];
+    payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
+    reinterpret_cast<ulonglong2*>(&e.rec)[1] = payload;
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -991,10 +1005,12 @@ void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* coun
 
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
                    const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
-                   uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* err_flag, cudaStream_t s) {
-  if (n)
-    k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, label, users, owners,
-                                                                      n, slot, n_new, err_flag);
+                   uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
+                   uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s) {
+  if (!n) return;
+  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, label, users, owners, n,
+                                                                    slot, n_new, fix_list, n_fix, fix_cap, err_flag);
+  k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap);
 }
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
