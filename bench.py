@@ -47,29 +47,41 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled through NVML every ~2 ms
+    while the timed region runs (the same counters nvidia-smi reports)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.sm, self.reasons = [], set()
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            return
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for name, const in self.REASONS.items():
+                        if bits & getattr(nv, const):
+                            self.reasons.add(name)
                 except Exception:
                     pass
-                self._stop.wait(0.1)
+                self._stop.wait(0.002)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -78,15 +90,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
-                          and "Not" not in r[2 + i]})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        s = sorted(self.sm)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
 
 
 def dist_env():
@@ -232,7 +240,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(step_fn):
+    def timed(step_fn, clocks=None):
         eng = fresh_engine()
         ext = torch.cuda.ExternalStream(eng.stream, device=dev)
         for k in range(warm):
@@ -240,14 +248,18 @@ def run_ours(args):
         hs, launches = [], 0
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if clocks:
+            clocks.start()
         e0.record(ext)
         for k in range(warm, warm + steps):
             step_fn(eng, k)
             t = eng.times()
             hs.append(t["hash_scan_ms"])
-            launches += t["kernels_launched"] + 2 + 6  # admit + commit (claim, commit) + epoch kernels
+            launches += t["kernels_launched"]  # admit + commit + epoch kernels of this step
         e1.record(ext)
         barrier()
+        if clocks:
+            clocks.stop()
         ms = e0.elapsed_time(e1)
         if world > 1:
             import torch.distributed as dist
@@ -259,8 +271,7 @@ def run_ours(args):
         return ms, hs, launches, last
 
     clocks = ClockSampler(local)
-    clocks.start()
-    ms_dev, hs, launches, last = timed(step_device)
+    ms_dev, hs, launches, last = timed(step_device, clocks)
     clk = clocks.stop()
     ms_e2e, _, _, _ = timed(step_host)
 

@@ -92,7 +92,8 @@ class CompiledRuleSet {
                                                           std::vector<std::string>* warnings = nullptr) {
     skv_rules* r = nullptr;
     char err[1024] = {0};
-    check(skv_rules_from_json(json.data(), json.size(), &r, err, sizeof(err)), err);
+    const int rc = skv_rules_from_json(json.data(), json.size(), &r, err, sizeof(err));
+    check(rc, err);
     auto set = std::shared_ptr<const CompiledRuleSet>(new CompiledRuleSet(r));
     if (warnings)
       for (size_t i = 0; i < skv_rules_warning_count(r); ++i) warnings->emplace_back(skv_rules_warning(r, i));
@@ -167,6 +168,9 @@ class AdmissionIndex {
     rules_ = CompiledRuleSet::defaults();
   }
   ~AdmissionIndex() { skv_destroy(ctx_); }
+
+  // the status is computed before the error string is fetched (argument order is unspecified)
+  void ok(int rc) const { check(rc, skv_last_error(ctx_)); }
   AdmissionIndex(const AdmissionIndex&) = delete;
   AdmissionIndex& operator=(const AdmissionIndex&) = delete;
 
@@ -174,7 +178,7 @@ class AdmissionIndex {
   std::shared_ptr<const CompiledRuleSet> load_rules_json(const std::string& json,
                                                          std::vector<std::string>* warnings = nullptr) {
     auto set = CompiledRuleSet::from_json(json, warnings);
-    check(skv_set_rules(ctx_, set->handle()), skv_last_error(ctx_));
+    ok(skv_set_rules(ctx_, set->handle()));
     rules_ = set;
     return set;
   }
@@ -183,14 +187,14 @@ class AdmissionIndex {
   // RuleEngine::tier1_scan (detection.hpp:217)
   DetectionVerdict tier1_scan(std::string_view text) {
     uint32_t mask = 0;
-    check(skv_tier1_scan(ctx_, text.data(), text.size(), &mask), skv_last_error(ctx_));
+    ok(skv_tier1_scan(ctx_, text.data(), text.size(), &mask));
     return rules_->verdict(mask);
   }
 
   // token_seq_digest (core.hpp:68-73)
   uint64_t token_seq_digest(const TokenSeq& seq) {
     uint64_t d = 0;
-    check(skv_token_seq_digest(ctx_, seq.data(), seq.size(), &d), skv_last_error(ctx_));
+    ok(skv_token_seq_digest(ctx_, seq.data(), seq.size(), &d));
     return d;
   }
 
@@ -221,7 +225,7 @@ class AdmissionIndex {
     skv_batch b{toks.data(), off.data(), users.data(), owners.data(), n, toks.size(), 0};
     skv_admit_out o{a.key_h.data(), a.key_d.data(), a.labels.data(), a.rule_masks.data(), a.decisions.data(),
                     a.matched_blocks.data(), tiers.data(), nullptr, 0, 0, 0};
-    check(skv_admit(ctx_, &b, &o), skv_last_error(ctx_));
+    ok(skv_admit(ctx_, &b, &o));
     for (uint32_t p = 0, acc = 0; p <= n; ++p) {
       a.block_offsets[p] = acc;
       if (p < n) acc += static_cast<uint32_t>((off[p + 1] - off[p]) / block_tokens_);
@@ -234,7 +238,7 @@ class AdmissionIndex {
   // Phase C: insert the last admitted batch (first creator wins).  Returns new entries.
   uint64_t commit() {
     uint64_t nn = 0;
-    check(skv_commit(ctx_, &nn), skv_last_error(ctx_));
+    ok(skv_commit(ctx_, &nn));
     return nn;
   }
 
@@ -243,7 +247,7 @@ class AdmissionIndex {
     std::vector<skv_event> buf(1 << 16);
     size_t n = 0;
     uint64_t ep = 0;
-    check(skv_epoch(ctx_, buf.data(), buf.size(), &n, &ep), skv_last_error(ctx_));
+    ok(skv_epoch(ctx_, buf.data(), buf.size(), &n, &ep));
     if (n > buf.size()) throw CapacityExhausted("more anomaly events than the facade buffer");
     std::vector<AnomalyEvent> out;
     for (size_t i = 0; i < n; ++i) {
