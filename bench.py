@@ -188,7 +188,7 @@ def run_ours(args):
     blocks_per_batch = n_local * (L // B)
     cap = 1 << max(20, int(np.ceil(np.log2((n_batches + 1) * blocks_per_batch * 1.7))))
     ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
-                        max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 21,
+                        max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 18,
                         device=local)
 
     # ---- inputs: distinct batches, generated into pinned host memory, copied to HBM

@@ -181,7 +181,8 @@ uint64_t skv_entry_count(skv_ctx* ctx);
 typedef struct {
   float hash_scan_ms, chain_probe_ms, record_ms, admit_total_ms, commit_ms, epoch_ms;
   uint64_t matched_total, accesses, new_blocks, touched_entries;
-  uint32_t kernels_launched;
+  uint64_t replayed_entries;  /* entries whose user set crossed 64 in the batch (ordered replay) */
+  uint32_t kernels_launched;  /* kernels of the last admit + commit + epoch */
 } skv_stage_times;
 int skv_last_times(skv_ctx* ctx, skv_stage_times* out);
 

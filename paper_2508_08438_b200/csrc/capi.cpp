@@ -93,11 +93,17 @@ struct skv_ctx {
   uint64_t entries = 0;
 
   // monitor window state
-  unsigned long long* sets = nullptr;
-  uint32_t* set_size = nullptr;
+  skv::SetHdr* set_hdr = nullptr;
+  ulonglong2* set_tab = nullptr;
+  uint32_t* batch_list = nullptr;  // entries touched by the current batch
+  uint32_t* replay = nullptr;      // entries needing an ordered monitor replay
+  uint32_t rec_batch = 0;          // admit-batch id (monitor stamps)
+  uint32_t wstart = 1;             // first batch id of the current monitor window
   uint32_t pool_cap = 0;
   uint32_t* touched[2] = {nullptr, nullptr};
-  uint32_t* counters = nullptr;  // [0]=pool_count [1..2]=n_touched[2] [3]=n_cands [4]=n_events [5]=err_flag [6]=n_runs [7]=n_fix
+  // [0]=pool_count [1..2]=n_touched[2] [3]=n_cands [4]=n_events [5]=err_flag [6]=n_batch
+  // [7]=n_fix [8]=n_replay [9]=n_keys [10]=matched_total
+  uint32_t* counters = nullptr;
   unsigned long long* n_new = nullptr;
   int cur = 0;
   uint32_t* cands = nullptr;
@@ -117,15 +123,13 @@ struct skv_ctx {
   uint32_t* matched = nullptr;
   uint32_t* exist = nullptr;
   uint8_t* tier = nullptr;
-  uint32_t* acc_off = nullptr;
   uint64_t* bh = nullptr;
   uint64_t* bd = nullptr;
   uint32_t* bmask = nullptr;
   uint8_t* blabel = nullptr;
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
-  uint32_t *key_a = nullptr, *key_b = nullptr, *val_a = nullptr, *val_b = nullptr;
-  uint32_t *uniq = nullptr, *runs = nullptr, *starts = nullptr;
+  unsigned long long *keys_a = nullptr, *keys_b = nullptr;  // ordered-replay access keys
   uint32_t* fix_list = nullptr;  // commit: duplicate-key slots + depths (2 x max_blocks)
   void* temp = nullptr;
   size_t temp_bytes = 0;
@@ -261,6 +265,23 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
   if (c->hs_grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
 }
 
+skv::MonCtx monitor_ctx(skv_ctx* c) {
+  skv::MonCtx m;
+  m.hdr = c->set_hdr;
+  m.tab = c->set_tab;
+  m.pool_cap = c->pool_cap;
+  m.pool_count = c->counters + 0;
+  m.touched = c->touched[c->cur];
+  m.n_touched = c->counters + 1 + c->cur;
+  m.batch_list = c->batch_list;
+  m.n_batch = c->counters + 6;
+  m.batch = ++c->rec_batch;
+  m.wstart = c->wstart;
+  m.err = c->counters + 5;
+  m.matched_total = c->counters + 10;
+  return m;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -350,7 +371,7 @@ void skv_config_default(skv_config* c) {
   c->index_capacity = 1ull << 20;
   c->max_prompts = 1ull << 16;
   c->max_tokens = 1ull << 24;
-  c->max_window_entries = 1ull << 18;
+  c->max_window_entries = 1ull << 16;
   c->entropy_jump = 0.3;  // MonitorConfig defaults (monitor.hpp:12-15)
   c->u_pre_max = 1;
 }
@@ -390,8 +411,10 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     skv::launch_init_entries(c->ix, c->stream);
     // monitor window
     c->pool_cap = static_cast<uint32_t>(cfg->max_window_entries);
-    c->sets = dalloc<unsigned long long>(static_cast<size_t>(c->pool_cap) * skv::kMaxSetUsers, c->owned);
-    c->set_size = dalloc<uint32_t>(c->pool_cap, c->owned);
+    c->set_hdr = dalloc<skv::SetHdr>(c->pool_cap, c->owned);
+    c->set_tab = dalloc<ulonglong2>(static_cast<size_t>(c->pool_cap) * skv::kSetSlots, c->owned);
+    c->batch_list = dalloc<uint32_t>(c->pool_cap, c->owned);
+    c->replay = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[0] = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[1] = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->counters = dalloc<uint32_t>(16, c->owned);
@@ -415,24 +438,17 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->matched = dalloc<uint32_t>(N + 1, c->owned);
     c->exist = dalloc<uint32_t>(N, c->owned);
     c->tier = dalloc<uint8_t>(N, c->owned);
-    c->acc_off = dalloc<uint32_t>(N + 1, c->owned);
     c->bh = dalloc<uint64_t>(NB, c->owned);
     c->bd = dalloc<uint64_t>(NB, c->owned);
     c->bmask = dalloc<uint32_t>(NB, c->owned);
     c->blabel = dalloc<uint8_t>(NB, c->owned);
     c->bdecision = dalloc<uint8_t>(NB, c->owned);
     c->bslot = dalloc<uint32_t>(NB, c->owned);
-    c->key_a = dalloc<uint32_t>(NB, c->owned);
-    c->key_b = dalloc<uint32_t>(NB, c->owned);
-    c->val_a = dalloc<uint32_t>(NB, c->owned);
-    c->val_b = dalloc<uint32_t>(NB, c->owned);
-    c->uniq = dalloc<uint32_t>(NB, c->owned);
-    c->runs = dalloc<uint32_t>(NB, c->owned);
-    c->starts = dalloc<uint32_t>(NB, c->owned);
+    c->keys_a = dalloc<unsigned long long>(NB, c->owned);
+    c->keys_b = dalloc<unsigned long long>(NB, c->owned);
     c->fix_list = dalloc<uint32_t>(2 * NB, c->owned);
-    size_t tb = std::max({skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
-                          skv::sort_temp_bytes(static_cast<uint32_t>(NB), log2u(cap)),
-                          skv::rle_temp_bytes(static_cast<uint32_t>(NB))});
+    size_t tb = std::max(skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
+                         skv::sort_keys_temp_bytes(static_cast<uint32_t>(NB), 32 + log2u(cap)));
     c->temp_bytes = tb;
     c->temp = dalloc<uint8_t>(tb, c->owned);
     CK(cudaMallocHost(&c->host_small, 64 * sizeof(uint32_t)));
@@ -568,25 +584,32 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, s);
     CK(cudaEventRecord(c->ev[2], s));
     // chained keys + labels, then the index probe (stage 3)
+    skv::MonCtx mon = monitor_ctx(c);
+    CK(cudaMemsetAsync(c->counters + 6, 0, 4, s));   // n_batch
+    CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, users, N, c->bh, c->blabel, c->bdecision,
-                            c->bslot, c->matched, c->exist, c->tier, s);
+                            c->bslot, c->matched, c->exist, c->tier, mon, s);
     CK(cudaEventRecord(c->ev[3], s));
-    // stage 4: monitor record
-    skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->matched, c->acc_off, N + 1, s);
-    CK(cudaMemcpyAsync(c->host_small, c->acc_off + N, 4, cudaMemcpyDeviceToHost, s));
+    // stage 4: monitor record -- hits and set inserts were recorded inside the probe;
+    // apply distinct counts, then replay (in prompt order) the rare entries whose
+    // tracked set crossed 64 users in this batch
+    skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
+    uint32_t launched = 5;  // block counts, scan (2), hash/scan, chain/probe
+    launched += 1;
+    CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 12, cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    const uint32_t M = c->host_small[0];
-    uint32_t launched = 5;
-    if (M > 0) {
-      const int bits = log2u(c->ix.cap);
-      skv::launch_emit_accesses(c->bslot, c->blk_off, c->matched, c->acc_off, N, c->key_a, c->val_a, s);
-      skv::launch_sort_pairs(c->temp, c->temp_bytes, c->key_a, c->key_b, c->val_a, c->val_b, M, bits, s);
-      skv::launch_rle(c->temp, c->temp_bytes, c->key_b, c->uniq, c->runs, c->counters + 6, M, s);
-      skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->runs, c->starts, M, s);
-      skv::launch_record(c->ix, c->uniq, c->runs, c->starts, c->counters + 6, c->val_b, users, c->sets, c->set_size,
-                         c->pool_cap, c->counters + 0, c->touched[c->cur], c->counters + 1 + c->cur,
-                         c->counters + 5, static_cast<int>(c->rec_grid), s);
-      launched += 5;
+    const uint32_t n_replay = c->host_small[0];
+    const uint32_t M = c->host_small[2];
+    if (n_replay > 0) {
+      skv::launch_replay_emit(c->ix, mon, c->bslot, c->blk_off, c->matched, N, c->keys_a, c->counters + 9, s);
+      CK(cudaMemcpyAsync(c->host_small, c->counters + 9, 4, cudaMemcpyDeviceToHost, s));
+      sync_check(s);
+      const uint32_t nk = c->host_small[0];
+      const int end_bit = 32 + log2u(c->ix.cap);
+      skv::launch_sort_keys(c->temp, c->temp_bytes, c->keys_a, c->keys_b, nk, end_bit, s);
+      skv::launch_record_replay(c->ix, mon, c->replay, c->counters + 8, c->keys_b, nk, users,
+                                static_cast<int>(c->rec_grid), s);
+      launched += 2 + 2 + (end_bit + 7) / 8;
     }
     CK(cudaEventRecord(c->ev[4], s));
     // outputs
@@ -613,6 +636,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->times.admit_total_ms = elapsed(c->ev[0], c->ev[4]);
     c->times.matched_total = M;
     c->times.accesses = M;
+    c->times.replayed_entries = n_replay;
     c->times.touched_entries = c->host_small[8 + 1 + c->cur];
     c->times.kernels_launched = launched;
     c->pending = true;
@@ -653,6 +677,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     c->entries += nn;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
+    c->times.kernels_launched += 2;  // k_commit, k_commit_fixup
     c->times.new_blocks = nn;
     c->pending = false;
     if (new_entries) *new_entries = nn;
@@ -696,9 +721,11 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     CK(cudaMemcpyAsync(c->counters, reset, 12, cudaMemcpyHostToDevice, s));
     sync_check(s);
     c->cur = prev;
+    c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
     CK(cudaEventRecord(c->ev[6], s));
     CK(cudaEventSynchronize(c->ev[6]));
     c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
+    c->times.kernels_launched += (n_cur ? 2 : 0) + (n_prev ? 2 : 0) + (bound ? 2 : 0);
     std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
       return x.h != y.h ? x.h < y.h : x.d < y.d;
     });

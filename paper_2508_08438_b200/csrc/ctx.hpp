@@ -103,6 +103,37 @@ struct Index {
   uint64_t cap = 0, mask = 0;
 };
 
+// Monitor user sets (AccessStats::user_set, access_stats.hpp:21-37), one per entry touched
+// in the current monitor window, allocated from a pool on first touch.  A set is a
+// 128-slot open-addressed table of {user, stamp} (128-bit CAS inserts); a slot is live iff
+// its stamp (admit-batch id) >= the window's first batch id, so tables never need
+// clearing.  `size` = users admitted before the current batch.
+constexpr uint32_t kSetSlots = 128;
+constexpr uint32_t kPendingSet = 0xfffffffeu;
+
+struct SetHdr {
+  uint32_t size;   // admitted members at the start of the current batch
+  uint32_t touch;  // last batch that touched the entry (batch-list dedupe)
+  uint32_t ovf;    // batch in which the first-64 boundary was crossed (needs ordered replay)
+  uint32_t pad;
+  unsigned long long cnt;  // (batch << 32) | distinct users inserted in that batch
+};
+
+struct MonCtx {
+  SetHdr* hdr;
+  ulonglong2* tab;  // pool_cap * kSetSlots
+  uint32_t pool_cap;
+  uint32_t* pool_count;
+  uint32_t* touched;    // entries touched in the current window
+  uint32_t* n_touched;
+  uint32_t* batch_list;  // entries touched by the current batch
+  uint32_t* n_batch;
+  uint32_t batch;   // admit-batch id (>= 1)
+  uint32_t wstart;  // first batch id of the current window
+  uint32_t* err;
+  uint32_t* matched_total;
+};
+
 void launch_init_entries(const Index& ix, cudaStream_t s);
 
 // kernel launchers (kernels.cu)
@@ -115,20 +146,19 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
-                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s);
-void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
-                          const uint32_t* acc_off, uint32_t n_prompts, uint32_t* key, uint32_t* val,
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
+                        cudaStream_t s);
+void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,
                           cudaStream_t s);
-size_t sort_temp_bytes(uint32_t n, int bits);
-void launch_sort_pairs(void* temp, size_t temp_bytes, uint32_t* key_in, uint32_t* key_out, uint32_t* val_in,
-                       uint32_t* val_out, uint32_t n, int bits, cudaStream_t s);
-size_t rle_temp_bytes(uint32_t n);
-void launch_rle(void* temp, size_t temp_bytes, const uint32_t* keys, uint32_t* unique, uint32_t* counts,
-                uint32_t* n_runs, uint32_t n, cudaStream_t s);
-void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* counts, const uint32_t* starts,
-                   const uint32_t* n_runs, const uint32_t* vals, const uint64_t* users,
-                   unsigned long long* sets, uint32_t* set_size, uint32_t pool_cap, uint32_t* pool_count,
-                   uint32_t* touched, uint32_t* n_touched, uint32_t* err_flag, int grid, cudaStream_t s);
+void launch_replay_emit(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
+                        const uint32_t* matched, uint32_t n_prompts, unsigned long long* keys, uint32_t* n_keys,
+                        cudaStream_t s);
+size_t sort_keys_temp_bytes(uint32_t n, int end_bit);
+void launch_sort_keys(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out, uint32_t n,
+                      int end_bit, cudaStream_t s);
+void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* replay, const uint32_t* n_replay,
+                          const unsigned long long* keys, uint32_t n_keys, const uint64_t* users, int grid,
+                          cudaStream_t s);
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
                    const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,

@@ -365,6 +365,266 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
   return kNone;
 }
 
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long long cmp_lo, unsigned long long cmp_hi,
+                                       unsigned long long new_lo, unsigned long long new_hi,
+                                       unsigned long long* old_lo, unsigned long long* old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(*old_lo), "=l"(*old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+  return *old_lo == cmp_lo && *old_hi == cmp_hi;
+}
+
+// ---------------------------------------------------------------------------------
+// Monitor record (A.6, AccessStats::record access_stats.hpp:27-37), fused into the probe.
+//
+// hit_cur is order-independent: one atomic per access.  The distinct-user count is
+// order-dependent only for an entry whose tracked set crosses 64 users within the
+// batch (which 64 get admitted depends on prompt order).  So every access inserts its
+// user into the entry's set table (128-bit CAS); a set that was already full (64
+// admitted users) counts every non-member access directly, again order-independent.
+// k_record_finish then applies the distinct-insert count of every touched entry whose
+// set did not cross 64 in this batch; the rare crossing entries are replayed in prompt
+// order by k_record_replay.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mix32(uint64_t u) {
+  u ^= u >> 33;
+  u *= 0xff51afd7ed558ccdULL;
+  u ^= u >> 33;
+  return static_cast<uint32_t>(u);
+}
+
+__device__ __forceinline__ ulonglong2 ld_relaxed128(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool cas128_dev(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val, ulonglong2* old) {
+  return cas128(reinterpret_cast<unsigned long long*>(addr), cmp.x, cmp.y, val.x, val.y, &old->x, &old->y);
+}
+
+// pool slot of the entry's set for this window (allocated on first touch)
+__device__ __forceinline__ uint32_t acquire_set(Entry& e, uint32_t slot, const MonCtx& M) {
+  volatile uint32_t* sp = &e.aux.set_idx;
+  uint32_t si = *sp;
+  if (si < kPendingSet) return si;
+  if (si == kNone && atomicCAS(const_cast<uint32_t*>(sp), kNone, kPendingSet) == kNone) {
+    si = atomicAdd(M.pool_count, 1u);
+    if (si >= M.pool_cap) {
+      atomicOr(M.err, 1u);
+      atomicExch(const_cast<uint32_t*>(sp), kNone);
+      return kNone;
+    }
+    SetHdr& h = M.hdr[si];
+    h.size = 0;
+    h.touch = 0;
+    h.ovf = 0;
+    h.cnt = 0;
+    M.touched[atomicAdd(M.n_touched, 1u)] = slot;
+    __threadfence();
+    atomicExch(const_cast<uint32_t*>(sp), si);
+    return si;
+  }
+  while ((si = *sp) == kPendingSet) {
+  }
+  return si;
+}
+
+__device__ __forceinline__ uint32_t count_insert(unsigned long long* cnt, uint32_t batch) {
+  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cnt);
+  for (;;) {
+    const unsigned long long nv = (static_cast<uint32_t>(old >> 32) == batch)
+                                      ? old + 1
+                                      : ((static_cast<unsigned long long>(batch) << 32) | 1ull);
+    const unsigned long long got = atomicCAS(cnt, old, nv);
+    if (got == old) return static_cast<uint32_t>(nv);
+    old = got;
+  }
+}
+
+__device__ void record_access(const Index& ix, const MonCtx& M, uint32_t slot, uint64_t user) {
+  Entry& e = ix.e[slot];
+  atomicAdd(&e.stats.hit_cur, 1u);
+  const uint32_t si = acquire_set(e, slot, M);
+  if (si == kNone) return;
+  SetHdr& hd = M.hdr[si];
+  if (atomicExch(&hd.touch, M.batch) != M.batch) M.batch_list[atomicAdd(M.n_batch, 1u)] = slot;
+  const uint32_t size = *reinterpret_cast<volatile uint32_t*>(&hd.size);
+  ulonglong2* tab = M.tab + static_cast<uint64_t>(si) * kSetSlots;
+  uint32_t pos = mix32(user) & (kSetSlots - 1);
+  for (uint32_t i = 0; i < kSetSlots;) {
+    const ulonglong2 v = ld_relaxed128(&tab[pos]);
+    const bool live = v.y >= M.wstart;
+    if (live && v.x == user) return;  // tracked already (access_stats.hpp:30)
+    if (live) {
+      pos = (pos + 1) & (kSetSlots - 1);
+      ++i;
+      continue;
+    }
+    if (size >= kMaxSetUsers) {  // saturated: an untracked user counts as new (access_stats.hpp:33)
+      atomicAdd(&e.stats.u_cnt, 1u);
+      return;
+    }
+    ulonglong2 old;
+    if (cas128_dev(&tab[pos], v, make_ulonglong2(user, M.batch), &old)) {
+      if (size + count_insert(&hd.cnt, M.batch) > kMaxSetUsers) atomicExch(&hd.ovf, M.batch);
+      return;
+    }
+    // lost the slot to a concurrent insert: re-examine the same position
+  }
+  atomicExch(&hd.ovf, M.batch);  // table full: resolve by ordered replay
+}
+
+__global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* n_replay) {
+  const uint32_t n = *M.n_batch;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t slot = M.batch_list[i];
+    Entry& e = ix.e[slot];
+    SetHdr& hd = M.hdr[e.aux.set_idx];
+    if (hd.ovf == M.batch) {
+      replay[atomicAdd(n_replay, 1u)] = slot;
+      continue;
+    }
+    const uint32_t c = static_cast<uint32_t>(hd.cnt >> 32) == M.batch ? static_cast<uint32_t>(hd.cnt) : 0u;
+    e.stats.u_cnt += c;
+    hd.size += c;
+  }
+}
+
+// accesses (slot << 32 | prompt) of the entries that need an ordered replay
+__global__ void k_replay_emit(Index ix, MonCtx M, const uint32_t* __restrict__ slot_in,
+                              const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ matched,
+                              uint32_t n_prompts, unsigned long long* keys, uint32_t* n_keys) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  const uint32_t bo = blk_off[p], m = matched[p];
+  for (uint32_t b = lane_id(); b < m; b += 32) {
+    const uint32_t s = slot_in[bo + b];
+    if (M.hdr[ix.e[s].aux.set_idx].ovf == M.batch)
+      keys[atomicAdd(n_keys, 1u)] = (static_cast<unsigned long long>(s) << 32) | p;
+  }
+}
+
+// One warp per replayed entry: the batch's accesses in prompt order against the set as
+// it stood before the batch, exactly as AccessStats::record (register-resident set,
+// __match_any_sync for repeats within a 32-access chunk); then rebuild the table.
+__global__ void __launch_bounds__(256) k_record_replay(Index ix, MonCtx M, const uint32_t* __restrict__ replay,
+                                                       const uint32_t* __restrict__ n_replay,
+                                                       const unsigned long long* __restrict__ keys, uint32_t n_keys,
+                                                       const uint64_t* __restrict__ users) {
+  const uint32_t lane = lane_id();
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < *n_replay; r += nw) {
+    const uint32_t slot = replay[r];
+    Entry& e = ix.e[slot];
+    const uint32_t si = e.aux.set_idx;
+    SetHdr& hd = M.hdr[si];
+    ulonglong2* tab = M.tab + static_cast<uint64_t>(si) * kSetSlots;
+    // pre-batch members (live stamps < batch), compacted into lanes: m0 = member lane, m1 = lane + 32
+    unsigned long long m0 = 0, m1 = 0, s0 = 0, s1 = 0;
+    uint32_t size = 0;
+    for (uint32_t base = 0; base < kSetSlots; base += 32) {
+      const ulonglong2 v = tab[base + lane];
+      const bool pre = v.y >= M.wstart && v.y < M.batch;
+      const uint32_t bal = __ballot_sync(kFull, pre);
+      for (uint32_t src = 0; src < 32; ++src) {
+        if (!(bal >> src & 1u)) continue;
+        const uint32_t rk = size + __popc(bal & ((1u << src) - 1u));
+        const unsigned long long ux = __shfl_sync(kFull, v.x, src), sy = __shfl_sync(kFull, v.y, src);
+        if (lane == (rk & 31)) {
+          if (rk < 32) {
+            m0 = ux;
+            s0 = sy;
+          } else if (rk < 64) {
+            m1 = ux;
+            s1 = sy;
+          }
+        }
+      }
+      size += __popc(bal);
+    }
+    size = min(size, kMaxSetUsers);
+    // this entry's accesses: [lo, hi) in the sorted key list
+    const unsigned long long k0 = static_cast<unsigned long long>(slot) << 32;
+    uint32_t lo = 0, hi = n_keys;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (keys[mid] < k0) lo = mid + 1; else hi = mid;
+    }
+    uint32_t end = lo, top = n_keys;
+    while (end < top) {
+      const uint32_t mid = (end + top) >> 1;
+      if ((keys[mid] >> 32) <= slot) end = mid + 1; else top = mid;
+    }
+    const uint32_t size0 = size;
+    uint32_t add_total = 0;
+    for (uint32_t c0 = lo; c0 < end; c0 += 32) {
+      const uint32_t i = c0 + lane;
+      const bool valid = i < end;
+      const unsigned long long u = valid ? users[static_cast<uint32_t>(keys[i])] : 0ull;
+      bool member = false;
+      for (uint32_t j = 0; j < size; ++j) {
+        const unsigned long long mj = __shfl_sync(kFull, j < 32 ? m0 : m1, j & 31);
+        member |= (mj == u);
+      }
+      const bool nonmem = valid && !member;
+      const uint32_t nm_mask = __ballot_sync(kFull, nonmem);
+      const uint32_t peers = __match_any_sync(kFull, u) & nm_mask;
+      const uint32_t leader = nonmem ? static_cast<uint32_t>(__ffs(peers) - 1) : 0u;
+      const bool is_leader = nonmem && leader == lane;
+      const uint32_t leaders = __ballot_sync(kFull, is_leader);
+      const uint32_t room = kMaxSetUsers - size;
+      const uint32_t lrank = __popc(leaders & ((1u << leader) - 1u));
+      const bool admitted = nonmem && lrank < room;
+      add_total += nonmem ? (admitted ? (is_leader ? 1u : 0u) : 1u) : 0u;
+      uint32_t adm = __ballot_sync(kFull, is_leader && admitted);
+      uint32_t pos = size;
+      while (adm) {
+        const uint32_t ll = __ffs(adm) - 1;
+        adm &= adm - 1;
+        const unsigned long long v = __shfl_sync(kFull, u, ll);
+        if (lane == (pos & 31)) {
+          if (pos < 32) {
+            m0 = v;
+            s0 = M.batch;
+          } else {
+            m1 = v;
+            s1 = M.batch;
+          }
+        }
+        ++pos;
+      }
+      size = pos;
+    }
+    add_total = __reduce_add_sync(kFull, add_total);
+    // rebuild the table with exactly the admitted users
+    for (uint32_t base = 0; base < kSetSlots; base += 32) tab[base + lane] = make_ulonglong2(0ull, 0ull);
+    __syncwarp();
+    for (uint32_t j = 0; j < size; ++j) {
+      const unsigned long long u = __shfl_sync(kFull, j < 32 ? m0 : m1, j & 31);
+      const unsigned long long st = __shfl_sync(kFull, j < 32 ? s0 : s1, j & 31);
+      if (lane == 0) {
+        uint32_t pos = mix32(u) & (kSetSlots - 1);
+        while (tab[pos].y != 0) pos = (pos + 1) & (kSetSlots - 1);
+        tab[pos] = make_ulonglong2(u, st);
+      }
+    }
+    if (lane == 0) {
+      e.stats.u_cnt += add_total;
+      hd.size = size;
+    }
+    (void)size0;
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // K3: chained prefix keys + inherited labels + warp-cooperative index probe, fused.
 //
@@ -379,7 +639,6 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
 //      or creator == user, cache_index.hpp:483-485) and the first missing block (k,
 //      where the commit starts).  Probing stops at the tile holding the first miss.
 // ---------------------------------------------------------------------------------
-constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kCPWarps = 2;  // 2 x 16.9 KB SMEM tiles per CTA
 constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
 
@@ -407,7 +666,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     const uint32_t* __restrict__ first_sens, const uint64_t* __restrict__ users, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
-    uint8_t* __restrict__ tier) {
+    uint8_t* __restrict__ tier, MonCtx mon) {
   __shared__ uint64_t s_d[kCPWarps][32][kPitch];
   __shared__ uint64_t s_h[kCPWarps][32][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -495,6 +754,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
           if (b < new_m) {
             decision[bj + b] = lab == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
             tm = (pr.meta >> 16) & 0xffu;
+            record_access(ix, mon, pr.slot, uj);  // A.6: monitor record of every matched block
           }
           if (b < new_k) slot_out[bj + b] = pr.slot;
         }
@@ -513,124 +773,13 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     exist[p] = k;
     tier[p] = static_cast<uint8_t>(tmax);
   }
-}
-
-// ---------------------------------------------------------------------------------
-// K4: monitor record.  Accesses (slot, prompt) are emitted in prompt order, stably
-// radix-sorted by slot, run-length encoded; one warp replays each entry's accesses in
-// global order with the tracked user set (<= 64) in registers, reproducing the
-// order-dependent saturating count of AccessStats::record exactly.
-// ---------------------------------------------------------------------------------
-__global__ void k_emit_accesses(const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
-                                const uint32_t* __restrict__ matched, const uint32_t* __restrict__ acc_off,
-                                uint32_t n_prompts, uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
-  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_prompts) return;
-  uint32_t bo = blk_off[p], m = matched[p], ao = acc_off[p];
-  for (uint32_t b = lane_id(); b < m; b += 32) {
-    key[ao + b] = slot[bo + b];
-    val[ao + b] = p;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_record(Index ix, const uint32_t* __restrict__ unique,
-                                                const uint32_t* __restrict__ counts,
-                                                const uint32_t* __restrict__ starts,
-                                                const uint32_t* __restrict__ n_runs_p,
-                                                const uint32_t* __restrict__ vals, const uint64_t* __restrict__ users,
-                                                unsigned long long* __restrict__ sets, uint32_t* __restrict__ set_size,
-                                                uint32_t pool_cap, uint32_t* pool_count, uint32_t* touched,
-                                                uint32_t* n_touched, uint32_t* err_flag) {
-  const uint32_t lane = lane_id();
-  const uint32_t n_runs = *n_runs_p;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_runs; r += nwarps) {
-    const uint32_t slot = unique[r], cnt = counts[r], start = starts[r];
-    uint32_t si = 0;
-    if (lane == 0) {
-      si = ix.e[slot].aux.set_idx;
-      if (si == kNone) {
-        si = atomicAdd(pool_count, 1u);
-        if (si >= pool_cap) {
-          atomicOr(err_flag, 1u);
-        } else {
-          ix.e[slot].aux.set_idx = si;
-          set_size[si] = 0;
-          touched[atomicAdd(n_touched, 1u)] = slot;
-        }
-      }
-    }
-    si = __shfl_sync(0xffffffffu, si, 0);
-    if (si >= pool_cap) continue;
-    unsigned long long* set = sets + static_cast<uint64_t>(si) * kMaxSetUsers;
-    uint32_t size = set_size[si];
-    unsigned long long m0 = lane < size ? set[lane] : 0ull;
-    unsigned long long m1 = lane + 32 < size ? set[lane + 32] : 0ull;
-    const uint32_t size0 = size;
-    uint32_t add_total = 0;
-    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
-      uint32_t i = c0 + lane;
-      bool valid = i < cnt;
-      unsigned long long u = valid ? users[vals[start + i]] : 0ull;
-      bool member = false;
-      for (uint32_t j = 0; j < size; ++j) {
-        unsigned long long mj = __shfl_sync(0xffffffffu, j < 32 ? m0 : m1, j & 31);
-        member |= (mj == u);
-      }
-      bool nonmem = valid && !member;
-      uint32_t nm_mask = __ballot_sync(0xffffffffu, nonmem);
-      uint32_t peers = __match_any_sync(0xffffffffu, u) & nm_mask;
-      uint32_t leader = nonmem ? static_cast<uint32_t>(__ffs(peers) - 1) : 0u;
-      bool is_leader = nonmem && leader == lane;
-      uint32_t leaders = __ballot_sync(0xffffffffu, is_leader);
-      uint32_t room = kMaxSetUsers - size;
-      uint32_t lrank = __popc(leaders & ((1u << leader) - 1u));
-      bool admitted = nonmem && lrank < room;
-      add_total += nonmem ? (admitted ? (is_leader ? 1u : 0u) : 1u) : 0u;
-      uint32_t adm = __ballot_sync(0xffffffffu, is_leader && admitted);
-      uint32_t pos = size;
-      while (adm) {
-        uint32_t ll = __ffs(adm) - 1;
-        adm &= adm - 1;
-        unsigned long long v = __shfl_sync(0xffffffffu, u, ll);
-        if (lane == (pos & 31)) {
-          if (pos < 32)
-            m0 = v;
-          else
-            m1 = v;
-        }
-        ++pos;
-      }
-      size = pos;
-    }
-    add_total = __reduce_add_sync(0xffffffffu, add_total);
-    if (lane >= size0 && lane < size) set[lane] = m0;
-    if (lane + 32 >= size0 && lane + 32 < size) set[lane + 32] = m1;
-    if (lane == 0) {
-      set_size[si] = size;
-      ix.e[slot].stats.hit_cur += cnt;
-      ix.e[slot].stats.u_cnt += add_total;
-    }
-  }
+  const uint32_t msum = __reduce_add_sync(kFull, has ? m : 0u);
+  if (lane == 0 && msum) atomicAdd(mon.matched_total, msum);
 }
 
 // ---------------------------------------------------------------------------------
 // K6: commit (insert the new blocks of the batch).
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long long cmp_lo, unsigned long long cmp_hi,
-                                       unsigned long long new_lo, unsigned long long new_hi,
-                                       unsigned long long* old_lo, unsigned long long* old_hi) {
-  asm volatile(
-      "{\n\t.reg .b128 c, n, d;\n\t"
-      "mov.b128 c, {%2, %3};\n\t"
-      "mov.b128 n, {%4, %5};\n\t"
-      "atom.global.cas.b128 d, [%6], c, n;\n\t"
-      "mov.b128 {%0, %1}, d;\n\t}"
-      : "=l"(*old_lo), "=l"(*old_hi)
-      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
-      : "memory");
-  return *old_lo == cmp_lo && *old_hi == cmp_hi;
-}
 
 // Commit (A.7).  Lanes of the warp of prompt p walk its new blocks b >= k_p (k_p = the
 // first block missing before the batch, from k_chain_probe):
@@ -950,43 +1099,11 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint64_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
-                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, cudaStream_t s) {
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
+                        cudaStream_t s) {
   if (n)
     k_chain_probe<<<cdiv(n, 32 * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
-                                                                   decision, slot, matched, exist, tier);
-}
-
-void launch_emit_accesses(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
-                          const uint32_t* acc_off, uint32_t n, uint32_t* key, uint32_t* val, cudaStream_t s) {
-  if (n)
-    k_emit_accesses<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(slot, blk_off, matched, acc_off, n, key,
-                                                                            val);
-}
-
-size_t sort_temp_bytes(uint32_t n, int bits) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), n, 0, bits);
-  return bytes;
-}
-
-void launch_sort_pairs(void* temp, size_t temp_bytes, uint32_t* key_in, uint32_t* key_out, uint32_t* val_in,
-                       uint32_t* val_out, uint32_t n, int bits, cudaStream_t s) {
-  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key_in, key_out, val_in, val_out, n, 0, bits, s);
-}
-
-size_t rle_temp_bytes(uint32_t n) {
-  size_t bytes = 0;
-  cub::DeviceRunLengthEncode::Encode(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
-                                     static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                     static_cast<uint32_t*>(nullptr), n);
-  return bytes;
-}
-
-void launch_rle(void* temp, size_t temp_bytes, const uint32_t* keys, uint32_t* unique, uint32_t* counts,
-                uint32_t* n_runs, uint32_t n, cudaStream_t s) {
-  cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, keys, unique, counts, n_runs, n, s);
+                                                                   decision, slot, matched, exist, tier, mon);
 }
 
 uint32_t record_grid(int device) {
@@ -995,12 +1112,35 @@ uint32_t record_grid(int device) {
   return static_cast<uint32_t>(sms) * 8;
 }
 
-void launch_record(const Index& ix, const uint32_t* unique, const uint32_t* counts, const uint32_t* starts,
-                   const uint32_t* n_runs, const uint32_t* vals, const uint64_t* users, unsigned long long* sets,
-                   uint32_t* set_size, uint32_t pool_cap, uint32_t* pool_count, uint32_t* touched,
-                   uint32_t* n_touched, uint32_t* err_flag, int grid, cudaStream_t s) {
-  k_record<<<grid, 256, 0, s>>>(ix, unique, counts, starts, n_runs, vals, users, sets, set_size, pool_cap, pool_count,
-                                touched, n_touched, err_flag);
+void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,
+                          cudaStream_t s) {
+  k_record_finish<<<grid, 256, 0, s>>>(ix, mon, replay, n_replay);
+}
+
+void launch_replay_emit(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
+                        const uint32_t* matched, uint32_t n, unsigned long long* keys, uint32_t* n_keys,
+                        cudaStream_t s) {
+  if (n)
+    k_replay_emit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, mon, slot, blk_off, matched, n, keys,
+                                                                          n_keys);
+}
+
+size_t sort_keys_temp_bytes(uint32_t n, int end_bit) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, static_cast<const unsigned long long*>(nullptr),
+                                 static_cast<unsigned long long*>(nullptr), n, 0, end_bit);
+  return bytes;
+}
+
+void launch_sort_keys(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out, uint32_t n,
+                      int end_bit, cudaStream_t s) {
+  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, n, 0, end_bit, s);
+}
+
+void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* replay, const uint32_t* n_replay,
+                          const unsigned long long* keys, uint32_t n_keys, const uint64_t* users, int grid,
+                          cudaStream_t s) {
+  k_record_replay<<<grid, 256, 0, s>>>(ix, mon, replay, n_replay, keys, n_keys, users);
 }
 
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,

@@ -156,7 +156,7 @@ class EngineConfig:
     index_capacity: int = 1 << 20
     max_prompts: int = 1 << 16
     max_tokens: int = 1 << 24
-    max_window_entries: int = 1 << 18
+    max_window_entries: int = 1 << 16
     entropy_jump: float = 0.3
     u_pre_max: int = 1
     device: int = 0

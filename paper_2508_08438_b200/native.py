@@ -113,7 +113,8 @@ class StageTimes(C.Structure):
     _fields_ = [("hash_scan_ms", C.c_float), ("chain_probe_ms", C.c_float), ("record_ms", C.c_float),
                 ("admit_total_ms", C.c_float), ("commit_ms", C.c_float), ("epoch_ms", C.c_float),
                 ("matched_total", C.c_uint64), ("accesses", C.c_uint64), ("new_blocks", C.c_uint64),
-                ("touched_entries", C.c_uint64), ("kernels_launched", C.c_uint32)]
+                ("touched_entries", C.c_uint64), ("replayed_entries", C.c_uint64),
+                ("kernels_launched", C.c_uint32)]
 
 
 class GenSpec(C.Structure):
