@@ -273,8 +273,6 @@ skv::MonCtx monitor_ctx(skv_ctx* c) {
   m.pool_count = c->counters + 0;
   m.touched = c->touched[c->cur];
   m.n_touched = c->counters + 1 + c->cur;
-  m.batch_list = c->batch_list;
-  m.n_batch = c->counters + 6;
   m.batch = ++c->rec_batch;
   m.wstart = c->wstart;
   m.err = c->counters + 5;
@@ -593,9 +591,9 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // stage 4: monitor record -- hits and set inserts were recorded inside the probe;
     // apply distinct counts, then replay (in prompt order) the rare entries whose
     // tracked set crossed 64 users in this batch
+    skv::launch_record(c->ix, mon, c->bslot, c->blk_off, c->matched, users, N, s);
     skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
-    uint32_t launched = 5;  // block counts, scan (2), hash/scan, chain/probe
-    launched += 1;
+    uint32_t launched = 7;  // block counts, scan (2), hash/scan, chain/probe, record, finish
     CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 12, cudaMemcpyDeviceToHost, s));
     sync_check(s);
     const uint32_t n_replay = c->host_small[0];

@@ -113,7 +113,7 @@ constexpr uint32_t kPendingSet = 0xfffffffeu;
 
 struct SetHdr {
   uint32_t size;   // admitted members at the start of the current batch
-  uint32_t touch;  // last batch that touched the entry (batch-list dedupe)
+  uint32_t touch;  // unused
   uint32_t ovf;    // batch in which the first-64 boundary was crossed (needs ordered replay)
   uint32_t pad;
   unsigned long long cnt;  // (batch << 32) | distinct users inserted in that batch
@@ -126,8 +126,6 @@ struct MonCtx {
   uint32_t* pool_count;
   uint32_t* touched;    // entries touched in the current window
   uint32_t* n_touched;
-  uint32_t* batch_list;  // entries touched by the current batch
-  uint32_t* n_batch;
   uint32_t batch;   // admit-batch id (>= 1)
   uint32_t wstart;  // first batch id of the current window
   uint32_t* err;
@@ -148,6 +146,8 @@ void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_
                         const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
                         cudaStream_t s);
+void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
+                   const uint32_t* matched, const uint64_t* users, uint32_t n_prompts, cudaStream_t s);
 void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,
                           cudaStream_t s);
 void launch_replay_emit(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,

@@ -456,7 +456,6 @@ __device__ void record_access(const Index& ix, const MonCtx& M, uint32_t slot, u
   const uint32_t si = acquire_set(e, slot, M);
   if (si == kNone) return;
   SetHdr& hd = M.hdr[si];
-  if (atomicExch(&hd.touch, M.batch) != M.batch) M.batch_list[atomicAdd(M.n_batch, 1u)] = slot;
   const uint32_t size = *reinterpret_cast<volatile uint32_t*>(&hd.size);
   ulonglong2* tab = M.tab + static_cast<uint64_t>(si) * kSetSlots;
   uint32_t pos = mix32(user) & (kSetSlots - 1);
@@ -483,10 +482,11 @@ __device__ void record_access(const Index& ix, const MonCtx& M, uint32_t slot, u
   atomicExch(&hd.ovf, M.batch);  // table full: resolve by ordered replay
 }
 
+// one thread per entry touched in the current monitor window
 __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* n_replay) {
-  const uint32_t n = *M.n_batch;
+  const uint32_t n = *M.n_touched;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t slot = M.batch_list[i];
+    const uint32_t slot = M.touched[i];
     Entry& e = ix.e[slot];
     SetHdr& hd = M.hdr[e.aux.set_idx];
     if (hd.ovf == M.batch) {
@@ -497,6 +497,18 @@ __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* 
     e.stats.u_cnt += c;
     hd.size += c;
   }
+}
+
+// A.6 record, one warp per prompt, lanes = its matched blocks (order-independent part)
+__global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32_t* __restrict__ slot_in,
+                                                const uint32_t* __restrict__ blk_off,
+                                                const uint32_t* __restrict__ matched,
+                                                const uint64_t* __restrict__ users, uint32_t n_prompts) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  const uint32_t bo = blk_off[p], m = matched[p];
+  const uint64_t u = users[p];
+  for (uint32_t b = lane_id(); b < m; b += 32) record_access(ix, M, slot_in[bo + b], u);
 }
 
 // accesses (slot << 32 | prompt) of the entries that need an ordered replay
@@ -754,7 +766,6 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
           if (b < new_m) {
             decision[bj + b] = lab == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
             tm = (pr.meta >> 16) & 0xffu;
-            record_access(ix, mon, pr.slot, uj);  // A.6: monitor record of every matched block
           }
           if (b < new_k) slot_out[bj + b] = pr.slot;
         }
@@ -1110,6 +1121,12 @@ uint32_t record_grid(int device) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   return static_cast<uint32_t>(sms) * 8;
+}
+
+void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
+                   const uint32_t* matched, const uint64_t* users, uint32_t n, cudaStream_t s) {
+  if (n)
+    k_record<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, mon, slot, blk_off, matched, users, n);
 }
 
 void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,
