@@ -200,12 +200,17 @@ def run_ours(args):
         tok_pin = torch.empty(n_local * L, dtype=torch.int32, pin_memory=True)
         tok_np = tok_pin.numpy().view(np.uint32)
         _, off, users, owners = generate(spec, tokens_out=tok_np)
-        host.append((tok_pin, tok_np, off, users, owners))
-    for (tok_pin, _, off, users, owners) in host:
+        # every host input of the e2e arm lives in pinned memory (async H2D)
+        pins = [torch.from_numpy(a.view(v)).pin_memory() for a, v in
+                ((off, np.int64), (users, np.int64), (owners, np.uint8))]
+        off_p, users_p, owners_p = (t.numpy() for t in pins)
+        host.append((tok_pin, tok_np, off_p.view(np.uint64), users_p.view(np.uint64), owners_p, pins))
+    for (tok_pin, _, off, users, owners, _) in host:
         devb.append((tok_pin.to(dev, non_blocking=True), torch.from_numpy(off.view(np.int64)).to(dev),
                      torch.from_numpy(users.view(np.int64)).to(dev), torch.from_numpy(owners).to(dev)))
     torch.cuda.synchronize()
     pool = generate_pool(spec)
+    pipeline = not args.no_pipeline
 
     def fresh_engine():
         eng = AdmissionEngine(ecfg)
@@ -214,23 +219,33 @@ def run_ours(args):
         eng.epoch_pass()
         return eng
 
-    def step_device(eng, k):
+    def dev_batch(k):
         t, o, u, w = devb[k]
-        b = N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, n_local * L, 1)
-        eng.admit_raw(b)
+        return N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, n_local * L, 1)
+
+    def host_batch(k):
+        _, tok, off, users, owners, _ = host[k]
+        return N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
+                       n_local * L, 0)
+
+    # one step = admit(k) [+ stage batch k+1's stages 1-2 (and, e2e, its H2D) on the side
+    # stream, overlapping] + commit(k) + epoch; nxt is None at the edge of a timed region
+    def step_device(eng, k, nxt):
+        eng.admit_raw(dev_batch(k))
+        if nxt is not None:
+            eng.prefetch_raw(dev_batch(nxt))
         eng.commit()
         eng.epoch_pass()
 
     # outputs returned to the host in the e2e arm: labels per block + match length per prompt
-    out_label = np.empty(blocks_per_batch, np.uint8)
-    out_match = np.empty(n_local, np.uint32)
+    out_label = torch.empty(blocks_per_batch, dtype=torch.uint8, pin_memory=True)
+    out_match = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
 
-    def step_host(eng, k):
-        _, tok, off, users, owners = host[k]
-        b = N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
-                    n_local * L, 0)
-        o = N.AdmitOut(None, None, out_label.ctypes.data, None, None, out_match.ctypes.data, None, None, 0, 0, 0)
-        eng.admit_raw(b, o)
+    def step_host(eng, k, nxt):
+        o = N.AdmitOut(None, None, out_label.data_ptr(), None, None, out_match.data_ptr(), None, None, 0, 0, 0)
+        eng.admit_raw(host_batch(k), o)
+        if nxt is not None:
+            eng.prefetch_raw(host_batch(nxt))
         eng.commit()
         eng.epoch_pass()
 
@@ -244,17 +259,19 @@ def run_ours(args):
         eng = fresh_engine()
         ext = torch.cuda.ExternalStream(eng.stream, device=dev)
         for k in range(warm):
-            step_fn(eng, k)
+            step_fn(eng, k, k + 1 if pipeline and k + 1 < warm else None)
         hs, launches = [], 0
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if clocks:
             clocks.start()
         e0.record(ext)
+        pf = 0
         for k in range(warm, warm + steps):
-            step_fn(eng, k)
+            step_fn(eng, k, k + 1 if pipeline and k + 1 < warm + steps else None)
             t = eng.times()
             hs.append(t["hash_scan_ms"])
+            pf += t["prefetched"]
             launches += t["kernels_launched"]  # admit + commit + epoch kernels of this step
         e1.record(ext)
         barrier()
@@ -268,12 +285,12 @@ def run_ours(args):
             ms = float(x.item())
         last = eng.times()
         eng.close()
-        return ms, hs, launches, last
+        return ms, hs, launches, last, pf
 
     clocks = ClockSampler(local)
-    ms_dev, hs, launches, last = timed(step_device, clocks)
+    ms_dev, hs, launches, last, pf_dev = timed(step_device, clocks)
     clk = clocks.stop()
-    ms_e2e, _, _, _ = timed(step_host)
+    ms_e2e, _, _, _, pf_e2e = timed(step_host)
 
     total_blocks = blocks_per_batch * steps * world
     value = total_blocks / (ms_dev / 1e3)
@@ -307,7 +324,10 @@ def run_ours(args):
         "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
                                f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
                    "global_batch_prompts": n_local * world, "l2": "inputs 512 MiB/step > L2, distinct batch per step",
-                   "step": "admit + commit + epoch", "parallelism": f"replicas x{world}"},
+                   "step": "admit + commit + epoch", "parallelism": f"replicas x{world}",
+                   "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
+                                f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
+                                if pipeline else "off")},
         "stage_ms_last": {k: round(float(last[k]), 4) for k in ("hash_scan_ms", "chain_probe_ms", "record_ms",
                                                                   "admit_total_ms", "commit_ms", "epoch_ms")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -334,6 +354,7 @@ def main():
     ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

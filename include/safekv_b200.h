@@ -149,6 +149,15 @@ typedef struct {
 } skv_admit_out;
 
 int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
+/* Cross-batch pipelining: stage the NEXT device-resident batch's digests and window
+ * rule masks (stages 1-2, which read no index state) on a side stream, so they overlap
+ * the pending batch's commit/epoch.  The next skv_admit with the same tokens/offsets
+ * pointers and sizes consumes them; any other admit, or skv_set_rules, drops them.
+ * The caller must keep the batch's device buffers unchanged until that admit.  Host
+ * batches and unaligned tokens are accepted and ignored (admitted inline).  Results
+ * are identical with or without prefetch; there is no reference counterpart (the
+ * reference admits one prompt at a time). */
+int skv_prefetch(skv_ctx* ctx, const skv_batch* next);
 /* Insert the new blocks of the last admitted batch (first creator wins; intra-batch
  * duplicates are won by the lowest prompt index).  new_entries may be NULL. */
 int skv_commit(skv_ctx* ctx, uint64_t* new_entries);
@@ -183,6 +192,7 @@ typedef struct {
   uint64_t matched_total, accesses, new_blocks, touched_entries;
   uint64_t replayed_entries;  /* entries whose user set crossed 64 in the batch (ordered replay) */
   uint32_t kernels_launched;  /* kernels of the last admit + commit + epoch */
+  uint32_t prefetched;        /* 1: the last admit consumed stages 1-2 staged by skv_prefetch */
 } skv_stage_times;
 int skv_last_times(skv_ctx* ctx, skv_stage_times* out);
 

@@ -95,7 +95,6 @@ struct skv_ctx {
   // monitor window state
   skv::SetHdr* set_hdr = nullptr;
   ulonglong2* set_tab = nullptr;
-  uint32_t* batch_list = nullptr;  // entries touched by the current batch
   uint32_t* replay = nullptr;      // entries needing an ordered monitor replay
   uint32_t rec_batch = 0;          // admit-batch id (monitor stamps)
   uint32_t wstart = 1;             // first batch id of the current monitor window
@@ -149,6 +148,29 @@ struct skv_ctx {
 
   cudaEvent_t ev[8] = {};
   skv_stage_times times{};
+
+  // cross-batch pipelining (skv_prefetch): stages 1-2 of the next batch on a side stream
+  // into the alternate buffer set {counts, blk_off, first_sens, bd, bmask}
+  cudaStream_t side = nullptr;
+  cudaEvent_t pf_done = nullptr;
+  uint32_t *alt_counts = nullptr, *alt_blk_off = nullptr, *alt_first_sens = nullptr, *alt_bmask = nullptr;
+  uint64_t* alt_bd = nullptr;
+  bool pf_valid = false;
+  cudaEvent_t pf_ev[2] = {};  // bracket the last prefetched hash/scan (side stream)
+  void* side_temp = nullptr;
+  size_t side_temp_bytes = 0;
+  bool pf_on_device = false;
+  const void* pf_tokens = nullptr;
+  const void* pf_offsets = nullptr;
+  const void* pf_users = nullptr;
+  const void* pf_owners = nullptr;
+  // host-batch staging set (skv_prefetch of a host batch copies into it on the side stream)
+  uint32_t* alt_tokens = nullptr;
+  uint64_t* alt_off = nullptr;
+  uint64_t* alt_users = nullptr;
+  uint8_t* alt_owners = nullptr;
+  uint32_t pf_n = 0;
+  uint64_t pf_ntok = 0;
 };
 
 namespace {
@@ -280,6 +302,46 @@ skv::MonCtx monitor_ctx(skv_ctx* c) {
   return m;
 }
 
+// Stages 1+2 on stream `st`: digests, window rule masks and first sensitive block of a
+// batch whose block offsets are already in blk_off (the kernel reads the block count
+// from blk_off[N], so no host round trip is needed).
+void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t* off, uint32_t N, uint64_t n_tokens,
+             uint64_t nb_hint, uint32_t* blk_off, uint32_t* first_sens, uint64_t* bd, uint32_t* bmask) {
+  skv::HashScanArgs a;
+  a.tokens = tokens;
+  a.tok_off = off;
+  a.blk_off = blk_off;
+  a.n_prompts = N;
+  a.n_tokens = n_tokens;
+  a.n_blocks = static_cast<uint32_t>(nb_hint);  // grid-size hint only; 0 = unknown
+  a.B = c->cfg.block_tokens;
+  a.W = c->cfg.window_tokens;
+  a.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, a.B);
+  a.rules = c->rules_dev;
+  a.d_out = bd;
+  a.mask_out = bmask;
+  a.first_sens = first_sens;
+  a.off_cls = c->hs_layout.off_cls;
+  a.off_raw = c->hs_layout.off_raw;
+  a.off_so = c->hs_layout.off_so;
+  a.off_xch = c->hs_layout.off_xch;
+  a.off_list = c->hs_layout.off_list;
+  a.stage = c->hs_layout.stage;
+  skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, st);
+}
+
+// Offsets of a host batch: [0, n_tokens], non-decreasing.  Returns the block count.
+uint64_t host_block_count(const skv_batch* b, uint32_t B) {
+  const uint32_t N = b->n_prompts;
+  if (b->offsets[0] != 0 || b->offsets[N] != b->n_tokens) throw ArgError("offsets must span [0, n_tokens]");
+  uint64_t n_blocks = 0;
+  for (uint32_t p = 0; p < N; ++p) {
+    if (b->offsets[p + 1] < b->offsets[p]) throw ArgError("offsets must be non-decreasing");
+    n_blocks += (b->offsets[p + 1] - b->offsets[p]) / B;
+  }
+  return n_blocks;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -398,6 +460,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     if (prop.major != 10)
       throw CudaError("device " + std::string(prop.name) + " is not sm_100 (built for sm_100a only)");
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->pf_done, cudaEventDisableTiming));
+    for (auto& ev : c->pf_ev) CK(cudaEventCreate(&ev));
     for (auto& ev : c->ev) CK(cudaEventCreate(&ev));
     // index
     uint64_t cap = next_pow2(std::max<uint64_t>(cfg->index_capacity, 1024));
@@ -411,7 +476,6 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->pool_cap = static_cast<uint32_t>(cfg->max_window_entries);
     c->set_hdr = dalloc<skv::SetHdr>(c->pool_cap, c->owned);
     c->set_tab = dalloc<ulonglong2>(static_cast<size_t>(c->pool_cap) * skv::kSetSlots, c->owned);
-    c->batch_list = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->replay = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[0] = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[1] = dalloc<uint32_t>(c->pool_cap, c->owned);
@@ -439,6 +503,11 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->bh = dalloc<uint64_t>(NB, c->owned);
     c->bd = dalloc<uint64_t>(NB, c->owned);
     c->bmask = dalloc<uint32_t>(NB, c->owned);
+    c->alt_counts = dalloc<uint32_t>(N + 1, c->owned);
+    c->alt_blk_off = dalloc<uint32_t>(N + 1, c->owned);
+    c->alt_first_sens = dalloc<uint32_t>(N, c->owned);
+    c->alt_bd = dalloc<uint64_t>(NB, c->owned);
+    c->alt_bmask = dalloc<uint32_t>(NB, c->owned);
     c->blabel = dalloc<uint8_t>(NB, c->owned);
     c->bdecision = dalloc<uint8_t>(NB, c->owned);
     c->bslot = dalloc<uint32_t>(NB, c->owned);
@@ -448,6 +517,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     size_t tb = std::max(skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
                          skv::sort_keys_temp_bytes(static_cast<uint32_t>(NB), 32 + log2u(cap)));
     c->temp_bytes = tb;
+    c->side_temp_bytes = skv::scan_temp_bytes(static_cast<uint32_t>(N + 1));
+    c->side_temp = dalloc<uint8_t>(c->side_temp_bytes, c->owned);
     c->temp = dalloc<uint8_t>(tb, c->owned);
     CK(cudaMallocHost(&c->host_small, 64 * sizeof(uint32_t)));
     c->rec_grid = skv::record_grid(c->device);
@@ -480,6 +551,13 @@ int skv_destroy(skv_ctx* c) {
   if (c->host_small) cudaFreeHost(c->host_small);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->pf_done) cudaEventDestroy(c->pf_done);
+  for (auto ev : c->pf_ev)
+    if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return SKV_OK;
@@ -491,6 +569,8 @@ int skv_set_rules(skv_ctx* c, const skv_rules* r) {
   if (!c || !r) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    if (c->pf_valid) CK(cudaStreamSynchronize(c->side));
+    c->pf_valid = false;  // a staged scan used the previous rule snapshot
     upload_rules(c, *r);
     return SKV_OK;
   });
@@ -521,17 +601,26 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const uint64_t* users;
     const uint8_t* owners;
     uint64_t n_blocks = 0;
+    // stages 1+2 (and for host batches the H2D) were staged by skv_prefetch for exactly this batch?
+    const bool use_pf = c->pf_valid && c->pf_on_device == (b->on_device != 0) && c->pf_tokens == b->tokens &&
+                        c->pf_offsets == b->offsets && c->pf_users == b->users && c->pf_owners == b->owners &&
+                        c->pf_n == N && c->pf_ntok == b->n_tokens;
+    if (c->pf_valid && !use_pf) CK(cudaStreamSynchronize(c->side));  // stale prefetch: drop it
+    c->pf_valid = false;
     CK(cudaEventRecord(c->ev[0], s));
     if (!b->on_device) {
-      if (b->offsets[0] != 0 || b->offsets[N] != b->n_tokens) throw ArgError("offsets must span [0, n_tokens]");
-      for (uint32_t p = 0; p < N; ++p) {
-        if (b->offsets[p + 1] < b->offsets[p]) throw ArgError("offsets must be non-decreasing");
-        n_blocks += (b->offsets[p + 1] - b->offsets[p]) / B;
+      n_blocks = host_block_count(b, B);
+      if (use_pf) {
+        std::swap(c->d_tokens, c->alt_tokens);
+        std::swap(c->d_off, c->alt_off);
+        std::swap(c->d_users, c->alt_users);
+        std::swap(c->d_owners, c->alt_owners);
+      } else {
+        CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c->d_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c->d_users, b->users, N * 8ull, cudaMemcpyHostToDevice, s));
+        if (b->owners) CK(cudaMemcpyAsync(c->d_owners, b->owners, N, cudaMemcpyHostToDevice, s));
       }
-      CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(c->d_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(c->d_users, b->users, N * 8ull, cudaMemcpyHostToDevice, s));
-      if (b->owners) CK(cudaMemcpyAsync(c->d_owners, b->owners, N, cudaMemcpyHostToDevice, s));
       tokens = c->d_tokens;
       off = c->d_off;
       users = c->d_users;
@@ -546,44 +635,33 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       users = b->users;
       owners = b->owners;
     }
-    skv::launch_block_counts(off, N, B, c->counts, s);
-    skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
+    if (use_pf) {
+      CK(cudaStreamWaitEvent(s, c->pf_done, 0));
+      std::swap(c->counts, c->alt_counts);
+      std::swap(c->blk_off, c->alt_blk_off);
+      std::swap(c->first_sens, c->alt_first_sens);
+      std::swap(c->bd, c->alt_bd);
+      std::swap(c->bmask, c->alt_bmask);
+    } else {
+      skv::launch_block_counts(off, N, B, c->counts, s);
+      skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
+    }
     if (b->on_device) {
       CK(cudaMemcpyAsync(c->host_small, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
       sync_check(s);
       n_blocks = c->host_small[0];
     }
     if (n_blocks > c->max_blocks) throw ArgError("batch has more blocks than max_tokens / block_tokens");
-    CK(cudaMemsetAsync(c->first_sens, 0xff, N * 4ull, s));
+    if (!use_pf) CK(cudaMemsetAsync(c->first_sens, 0xff, N * 4ull, s));
     CK(cudaMemsetAsync(c->bdecision, 0, std::max<uint64_t>(n_blocks, 1), s));
     CK(cudaMemsetAsync(c->matched + N, 0, 4, s));
     CK(cudaEventRecord(c->ev[1], s));
-    // stages 1+2: digest + rule-tier window scan
-    skv::HashScanArgs a;
-    a.tokens = tokens;
-    a.tok_off = off;
-    a.blk_off = c->blk_off;
-    a.n_prompts = N;
-    a.n_tokens = b->n_tokens;
-    a.n_blocks = static_cast<uint32_t>(n_blocks);
-    a.B = B;
-    a.W = c->cfg.window_tokens;
-    a.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, B);
-    a.rules = c->rules_dev;
-    a.d_out = c->bd;
-    a.mask_out = c->bmask;
-    a.first_sens = c->first_sens;
-    a.off_cls = c->hs_layout.off_cls;
-    a.off_raw = c->hs_layout.off_raw;
-    a.off_so = c->hs_layout.off_so;
-    a.off_xch = c->hs_layout.off_xch;
-    a.off_list = c->hs_layout.off_list;
-    a.stage = c->hs_layout.stage;
-    skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, s);
+    // stages 1+2: digest + rule-tier window scan (unless staged by skv_prefetch)
+    if (!use_pf)
+      stage12(c, s, tokens, off, N, b->n_tokens, n_blocks, c->blk_off, c->first_sens, c->bd, c->bmask);
     CK(cudaEventRecord(c->ev[2], s));
     // chained keys + labels, then the index probe (stage 3)
     skv::MonCtx mon = monitor_ctx(c);
-    CK(cudaMemsetAsync(c->counters + 6, 0, 4, s));   // n_batch
     CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, users, N, c->bh, c->blabel, c->bdecision,
                             c->bslot, c->matched, c->exist, c->tier, mon, s);
@@ -628,7 +706,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     sync_check(s);
     if (c->host_small[8 + 5] & 1u)
       throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
-    c->times.hash_scan_ms = elapsed(c->ev[1], c->ev[2]);
+    c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
+    c->times.prefetched = use_pf ? 1 : 0;
     c->times.chain_probe_ms = elapsed(c->ev[2], c->ev[3]);
     c->times.record_ms = elapsed(c->ev[3], c->ev[4]);
     c->times.admit_total_ms = elapsed(c->ev[0], c->ev[4]);
@@ -642,6 +721,64 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->p_blocks = n_blocks;
     c->p_users = users;
     c->p_owners = owners;
+    return SKV_OK;
+  });
+}
+
+int skv_prefetch(skv_ctx* c, const skv_batch* b) {
+  if (!c || !b) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (c->pf_valid) CK(cudaStreamSynchronize(c->side));
+    c->pf_valid = false;
+    const uint32_t N = b->n_prompts;
+    // anything the pipeline cannot stage is admitted inline by skv_admit (which also
+    // reports its argument errors)
+    if (N == 0 || N > c->max_prompts || b->n_tokens > c->max_tokens || !b->tokens || !b->offsets || !b->users)
+      return SKV_OK;
+    cudaStream_t st = c->side;
+    const uint32_t* tokens = b->tokens;
+    const uint64_t* off = b->offsets;
+    uint64_t nb_hint = 0;
+    if (!b->on_device) {
+      // host batch: H2D into the alternate staging set on the side stream
+      try {
+        nb_hint = host_block_count(b, c->cfg.block_tokens);
+      } catch (const ArgError&) {
+        return SKV_OK;
+      }
+      if (!c->alt_tokens) {  // allocated on first use (max_tokens x 4 B)
+        c->alt_tokens = dalloc<uint32_t>(c->max_tokens + 4, c->owned);
+        c->alt_off = dalloc<uint64_t>(c->max_prompts + 1, c->owned);
+        c->alt_users = dalloc<uint64_t>(c->max_prompts, c->owned);
+        c->alt_owners = dalloc<uint8_t>(c->max_prompts, c->owned);
+      }
+      CK(cudaMemcpyAsync(c->alt_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->alt_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->alt_users, b->users, N * 8ull, cudaMemcpyHostToDevice, st));
+      if (b->owners) CK(cudaMemcpyAsync(c->alt_owners, b->owners, N, cudaMemcpyHostToDevice, st));
+      tokens = c->alt_tokens;
+      off = c->alt_off;
+    } else if (reinterpret_cast<uintptr_t>(b->tokens) % 16) {
+      return SKV_OK;
+    }
+    CK(cudaEventRecord(c->pf_ev[0], st));
+    skv::launch_block_counts(off, N, c->cfg.block_tokens, c->alt_counts, st);
+    skv::launch_exclusive_scan(c->side_temp, c->side_temp_bytes, c->alt_counts, c->alt_blk_off, N + 1, st);
+    CK(cudaMemsetAsync(c->alt_first_sens, 0xff, N * 4ull, st));
+    stage12(c, st, tokens, off, N, b->n_tokens, nb_hint, c->alt_blk_off, c->alt_first_sens, c->alt_bd,
+            c->alt_bmask);
+    CK(cudaEventRecord(c->pf_done, st));
+    CK(cudaEventRecord(c->pf_ev[1], st));
+    CK(cudaGetLastError());
+    c->pf_valid = true;
+    c->pf_on_device = b->on_device != 0;
+    c->pf_tokens = b->tokens;
+    c->pf_offsets = b->offsets;
+    c->pf_users = b->users;
+    c->pf_owners = b->owners;
+    c->pf_n = N;
+    c->pf_ntok = b->n_tokens;
     return SKV_OK;
   });
 }

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
     if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
     for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
   }
-  const uint32_t nb = a.n_blocks;
+  const uint32_t nb = a.blk_off[a.n_prompts];  // device-side block count (no host round trip)
   const uint32_t G0 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * nb) / gridDim.x);
   const uint32_t G1 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x + 1) * nb) / gridDim.x);
   if (tid == 0 && G0 < G1) {
@@ -265,6 +265,19 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
       e_tok = min(so_tok[1], so_tok[0] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
     }
     const uint32_t n_so = il + 1;
+    // ---- TMA bulk prefetch of the next chunk's token span into L2 (it starts where this
+    // span's right context begins); the staging loads of the next iteration then hit L2
+    if (tid == 0 && g + nw < G1) {
+      const uint64_t nxt = (e_tok > W ? e_tok - W : 0) & ~3ull;
+      const uint64_t lim = a.n_tokens & ~3ull;
+      if (nxt < lim) {
+        const uint64_t bytes = min(static_cast<uint64_t>(a.stage) * 4, (lim - nxt) * 4) & ~15ull;
+        if (bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.tokens + nxt),
+                       "r"(static_cast<uint32_t>(bytes))
+                       : "memory");
+      }
+    }
     // ---- stage tokens -> (2*class, raw byte); 4 tokens per 128-bit streaming load
     const uint32_t nq = static_cast<uint32_t>((e_tok - as + 3) >> 2);
     uint32_t wide = 0;
@@ -696,10 +709,15 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
   const uint32_t nmax = __reduce_max_sync(kFull, n);
   for (uint32_t t0 = 0; t0 < nmax; t0 += 32) {
     const uint32_t b = t0 + lane;
+    // all 32 prompts' digest rows in flight at once (cp.async: global -> SMEM, no registers)
     for (uint32_t j = 0; j < 32; ++j) {
       const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
-      if (b < nj) td[j][lane] = dk[bj + b];
+      if (b < nj) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&td[j][lane]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(dk + bj + b) : "memory");
+      }
     }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     const uint32_t cnt = n > t0 ? min(32u, n - t0) : 0u;
     for (uint32_t c = 0; c < cnt; ++c) {
@@ -833,6 +851,9 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       const uint64_t h = hk[bo + b], d = dk[bo + b];
       lab = label[bo + b];
       uint64_t s = slot_hash(h, d) & ix.mask;
+      // both 32-B sectors of the home entry in one DRAM burst: the CAS (sector 0) and the
+      // claim/link writes (sector 1) then hit L2
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(&ix.e[s]) : "memory");
       uint64_t i = 0;
       for (; i <= ix.mask; ++i) {
         unsigned long long ol, oh;
@@ -1103,8 +1124,9 @@ int hash_scan_grid(int device, uint32_t smem) {
 }
 
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s) {
-  if (a.n_blocks == 0) return;
-  uint32_t g = std::min<uint32_t>(grid, a.n_blocks);
+  // a.n_blocks is a host-side hint (0 = unknown); the kernel reads the count from blk_off[N]
+  const uint32_t g = a.n_blocks ? std::min<uint32_t>(grid, a.n_blocks) : static_cast<uint32_t>(grid);
+  if (a.n_prompts == 0 || g == 0) return;
   k_hash_scan<<<g, kHSThreads, smem, s>>>(a);
 }
 

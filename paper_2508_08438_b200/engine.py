@@ -238,7 +238,26 @@ class AdmissionEngine:
         """Zero-copy entry point: device (or host) pointers supplied by the caller."""
         self._check(self._lib.skv_admit(self._h, C.byref(batch), C.byref(out) if out is not None else None))
 
+    def prefetch(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,
+                 owners: Optional[np.ndarray] = None) -> None:
+        """Cross-batch pipelining (skv_prefetch): start the H2D copy and stages 1-2 of the
+        NEXT host batch on the engine's side stream; call between ``admit`` and ``commit``
+        of the current batch.  The following ``admit`` of the same arrays consumes it.
+        Arrays should already be contiguous with the ABI dtypes (uint32/uint64/uint64/uint8),
+        ideally pinned, so that ``admit`` sees the same buffers."""
+        arrs = (np.ascontiguousarray(tokens, dtype=np.uint32), np.ascontiguousarray(offsets, dtype=np.uint64),
+                np.ascontiguousarray(users, dtype=np.uint64),
+                None if owners is None else np.ascontiguousarray(owners, dtype=np.uint8))
+        self._pf_keep = arrs  # the async copy reads these until the next admit
+        b = N.Batch(_ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), len(arrs[1]) - 1, len(arrs[0]), 0)
+        self._check(self._lib.skv_prefetch(self._h, C.byref(b)))
+
+    def prefetch_raw(self, batch: N.Batch) -> None:
+        """skv_prefetch with caller-owned (device or host) pointers."""
+        self._check(self._lib.skv_prefetch(self._h, C.byref(batch)))
+
     # --------------------------------------------------------------- phase C
+
     def commit(self) -> int:
         n = C.c_uint64()
         self._check(self._lib.skv_commit(self._h, C.byref(n)))

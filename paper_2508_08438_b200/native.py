@@ -114,7 +114,7 @@ class StageTimes(C.Structure):
                 ("admit_total_ms", C.c_float), ("commit_ms", C.c_float), ("epoch_ms", C.c_float),
                 ("matched_total", C.c_uint64), ("accesses", C.c_uint64), ("new_blocks", C.c_uint64),
                 ("touched_entries", C.c_uint64), ("replayed_entries", C.c_uint64),
-                ("kernels_launched", C.c_uint32)]
+                ("kernels_launched", C.c_uint32), ("prefetched", C.c_uint32)]
 
 
 class GenSpec(C.Structure):
@@ -145,6 +145,7 @@ SIGNATURES = {
     "skv_set_rules": (C.c_int, [C.c_void_p, C.c_void_p]),
     "skv_stream": (C.c_void_p, [C.c_void_p]),
     "skv_admit": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(AdmitOut)]),
+    "skv_prefetch": (C.c_int, [C.c_void_p, C.POINTER(Batch)]),
     "skv_commit": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "skv_epoch": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t),
                             C.POINTER(C.c_uint64)]),
