@@ -192,11 +192,15 @@ def run_ours(args):
                         device=local)
 
     # ---- inputs: distinct batches, generated into pinned host memory, copied to HBM
+    # N > 1: prefix-forest partitioning -- every rank admits the first n_local prompts of
+    # the global sequence that skv_route assigns to it (disjoint index forests, no
+    # data-path collective)
     spec = GenSpec(n_prompts=n_local, prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
-                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"])
+                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"],
+                   route_world=world, route_rank=rank, route_block_tokens=B)
     host, devb = [], []
     for k in range(n_batches):
-        spec.prompt_id_base = (k + 1) * 100_000_000 + rank * n_local
+        spec.prompt_id_base = (k + 1) * 100_000_000
         tok_pin = torch.empty(n_local * L, dtype=torch.int32, pin_memory=True)
         tok_np = tok_pin.numpy().view(np.uint32)
         _, off, users, owners = generate(spec, tokens_out=tok_np)
@@ -209,7 +213,7 @@ def run_ours(args):
         devb.append((tok_pin.to(dev, non_blocking=True), torch.from_numpy(off.view(np.int64)).to(dev),
                      torch.from_numpy(users.view(np.int64)).to(dev), torch.from_numpy(owners).to(dev)))
     torch.cuda.synchronize()
-    pool = generate_pool(spec)
+    pool = generate_pool(spec, rank)  # this rank's share of the pre-inserted pool
     pipeline = not args.no_pipeline
 
     def fresh_engine():
@@ -324,7 +328,8 @@ def run_ours(args):
         "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
                                f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
                    "global_batch_prompts": n_local * world, "l2": "inputs 512 MiB/step > L2, distinct batch per step",
-                   "step": "admit + commit + epoch", "parallelism": f"replicas x{world}",
+                   "step": "admit + commit + epoch", "parallelism": (f"prefix-forest partitioned x{world} (skv_route; no data-path collective)"
+                                   if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
                                 f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
                                 if pipeline else "off")},

@@ -215,10 +215,21 @@ typedef struct {
   uint32_t pii_mix;                   /* 1: config-3 mix (60% none, 30% one per 2 KiB, 10% one per 256 B) */
   uint64_t seed;
   uint64_t prompt_id_base;            /* global id of prompt 0 (sharding)  */
+  /* prefix-forest partitioning: with route_world > 1 the batch is the first n_prompts
+   * global ids >= prompt_id_base whose prompt skv_route()s to route_rank */
+  uint32_t route_world, route_rank, route_block_tokens, pad_;
+  uint64_t* prompt_ids_out;           /* optional: global id of each generated prompt */
 } skv_gen_spec;
 /* Writes n_prompts*prompt_tokens tokens and n_prompts+1 offsets; users/owners may be NULL. */
 int skv_generate(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
                  uint8_t* owners, int nthreads);
+/* Multi-GPU router (host): rank of each prompt = a hash of the key h_0 of its first full
+ * block, i.e. of the root of its path in the prefix forest.  Every index entry a prompt
+ * can touch lies in that root's tree, so ranks own disjoint forests and admit/commit/
+ * monitor/epoch need no cross-rank exchange.  Prompts without a
+ * full block go to prompt_id % world (prompt_ids may be NULL: index p). */
+int skv_route(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
+              const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out);
 /* The pool prefixes themselves (pool_size prompts of pool_tokens). */
 int skv_generate_pool(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
                       uint8_t* owners);

@@ -2,10 +2,11 @@
 lookup -> entropy monitor) behind the C ABI of include/safekv_b200.h."""
 from .native import (CapacityExhausted, CompileError, ConfigError, CudaError, ParseError, SkvError, StateError,
                      load_library)
-from .engine import AdmissionEngine, AdmitResult, AnomalyEvent, EngineConfig, GenSpec, RuleSet, generate, generate_pool
+from .engine import (AdmissionEngine, AdmitResult, AnomalyEvent, EngineConfig, GenSpec, RuleSet, generate,
+                     generate_pool, route, split_batch)
 
 __all__ = [
     "AdmissionEngine", "AdmitResult", "AnomalyEvent", "EngineConfig", "GenSpec", "RuleSet", "generate",
-    "generate_pool", "load_library", "SkvError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
+    "generate_pool", "route", "split_batch", "load_library", "SkvError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
     "CudaError", "StateError",
 ]

@@ -100,6 +100,37 @@ std::string make_secret(size_t family, SplitMix64& rng) {
   }
 }
 
+// ---- prefix-forest routing (multi-GPU partitioning)
+constexpr uint64_t kFnvOff = 0xcbf29ce484222325ULL, kFnvP = 0x100000001b3ULL;
+
+uint64_t fnv_u32(uint64_t h, uint32_t v) {
+  for (int i = 0; i < 4; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * kFnvP;
+  return h;
+}
+uint64_t fnv_u64(uint64_t h, uint64_t v) { return fnv_u32(fnv_u32(h, static_cast<uint32_t>(v)), v >> 32); }
+
+// key h_0 of a prompt's first full block: FNV(u64 0 || u64 d_0), d_0 = token_seq_digest
+// (core.hpp:68-73) of tokens [0, B) -- the root of the prompt's path in the prefix forest
+uint64_t root_key(const uint32_t* t, uint32_t B) {
+  uint64_t d = fnv_u32(kFnvOff, B);
+  for (uint32_t i = 0; i < B; ++i) d = fnv_u32(d, t[i]);
+  return fnv_u64(fnv_u64(kFnvOff, 0), d);
+}
+
+uint32_t rank_of_root(uint64_t h0, uint32_t world) {
+  uint64_t z = h0 + 0x9e3779b97f4a7c15ULL;  // SplitMix64 finalizer, then multiply-high range map
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  return static_cast<uint32_t>((static_cast<unsigned __int128>(z) * world) >> 64);
+}
+
+uint32_t route_one(const uint32_t* t, uint64_t len, uint32_t B, uint64_t prompt_id, uint32_t world) {
+  if (world <= 1) return 0;
+  if (len < B) return static_cast<uint32_t>(prompt_id % world);  // no index interaction
+  return rank_of_root(root_key(t, B), world);
+}
+
 constexpr uint64_t kPoolTag = 0x706f6f6c00000000ULL;   // "pool"
 constexpr uint64_t kPoolUniq = 0x10000000000ULL;       // filler counters of pool prefixes
 constexpr uint64_t kBodyUniq = 0x20000000000ULL;       // filler counters of prompt bodies
@@ -151,28 +182,71 @@ int skv_generate_pool(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets
   return SKV_OK;
 }
 
+int skv_route(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
+              const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out) {
+  if (!offsets || !rank_out || (n_prompts && !tokens) || block_tokens == 0 || world == 0) return SKV_ERR_ARG;
+  for (uint32_t p = 0; p < n_prompts; ++p) {
+    if (offsets[p + 1] < offsets[p]) return SKV_ERR_ARG;
+    rank_out[p] = route_one(tokens + offsets[p], offsets[p + 1] - offsets[p], block_tokens,
+                            prompt_ids ? prompt_ids[p] : p, world);
+  }
+  return SKV_OK;
+}
+
 int skv_generate(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets, uint64_t* users, uint8_t* owners,
                  int nthreads) {
   if (!s || !tokens || !offsets) return SKV_ERR_ARG;
   if (s->n_users == 0 || s->prompt_tokens == 0) return SKV_ERR_CONFIG;
   if (s->shared_fraction > 0 && (s->pool_size == 0 || s->pool_tokens >= s->prompt_tokens)) return SKV_ERR_CONFIG;
+  if (s->route_world > 1 && (s->route_rank >= s->route_world || s->route_block_tokens == 0)) return SKV_ERR_CONFIG;
   const uint64_t N = s->n_prompts, L = s->prompt_tokens;
   std::vector<std::string> pool;
   if (s->shared_fraction > 0)
     for (uint64_t i = 0; i < s->pool_size; ++i) pool.push_back(pool_prefix(*s, i));
+  auto text_of = [&](uint64_t gid) {
+    SplitMix64 rng(derive_seed(s->seed, gid));
+    std::string text;
+    if (s->shared_fraction > 0 && rng.next_double() < s->shared_fraction) text = pool[rng.next_below(s->pool_size)];
+    text += body(*s, gid, L - text.size(), rng);
+    return text;
+  };
+  // global prompt ids of the batch: prompt_id_base + [0, N), or -- routed -- the first N
+  // ids from prompt_id_base on whose prompt routes to route_rank (skv_route)
+  std::vector<uint64_t> gids(N);
+  if (s->route_world <= 1) {
+    for (uint64_t p = 0; p < N; ++p) gids[p] = s->prompt_id_base + p;
+  } else {
+    const uint32_t B = s->route_block_tokens, G = s->route_world;
+    std::vector<int> pool_rank(pool.size(), -1);
+    std::vector<uint32_t> tb(B);
+    auto tok_rank = [&](const std::string& t, uint64_t gid) {
+      if (t.size() < B) return static_cast<uint32_t>(gid % G);
+      for (uint32_t i = 0; i < B; ++i) tb[i] = static_cast<unsigned char>(t[i]);
+      return route_one(tb.data(), t.size(), B, gid, G);
+    };
+    for (uint64_t gid = s->prompt_id_base, p = 0; p < N; ++gid) {
+      SplitMix64 rng(derive_seed(s->seed, gid));
+      uint32_t r;
+      if (s->shared_fraction > 0 && rng.next_double() < s->shared_fraction && s->pool_tokens >= B) {
+        const uint64_t i = rng.next_below(s->pool_size);  // the first B tokens are the pool prefix's
+        if (pool_rank[i] < 0) pool_rank[i] = static_cast<int>(tok_rank(pool[i], gid));
+        r = static_cast<uint32_t>(pool_rank[i]);
+      } else {
+        r = tok_rank(text_of(gid), gid);
+      }
+      if (r == s->route_rank) gids[p++] = gid;
+    }
+  }
   auto work = [&](uint64_t p0, uint64_t p1) {
     for (uint64_t p = p0; p < p1; ++p) {
-      uint64_t gid = s->prompt_id_base + p;
-      SplitMix64 rng(derive_seed(s->seed, gid));
-      std::string text;
-      if (s->shared_fraction > 0 && rng.next_double() < s->shared_fraction)
-        text = pool[rng.next_below(s->pool_size)];
-      text += body(*s, gid, L - text.size(), rng);
+      const uint64_t gid = gids[p];
+      std::string text = text_of(gid);
       uint32_t* t = tokens + p * L;
       for (uint64_t k = 0; k < L; ++k) t[k] = static_cast<unsigned char>(text[k]);
       offsets[p] = p * L;
       if (users) users[p] = s->first_user + gid % s->n_users;
       if (owners) owners[p] = 0;
+      if (s->prompt_ids_out) s->prompt_ids_out[p] = gid;
     }
   };
   if (nthreads <= 0) nthreads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));

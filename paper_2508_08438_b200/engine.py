@@ -336,28 +336,73 @@ class GenSpec:
     pii_mix: int = 0
     seed: int = 1
     prompt_id_base: int = 0
+    # prefix-forest partitioning: emit the first n_prompts ids routed to route_rank
+    route_world: int = 1
+    route_rank: int = 0
+    route_block_tokens: int = 16
 
-    def native(self) -> N.GenSpec:
+    def native(self, ids_out: Optional[np.ndarray] = None) -> N.GenSpec:
         return N.GenSpec(self.n_prompts, self.prompt_tokens, self.n_users, self.first_user, self.pool_size,
                          self.pool_tokens, self.shared_fraction, self.pii_per_kib, self.pii_mix, self.seed,
-                         self.prompt_id_base)
+                         self.prompt_id_base, self.route_world, self.route_rank, self.route_block_tokens, 0,
+                         _ptr(ids_out))
 
 
-def generate(spec: GenSpec, nthreads: int = 0, tokens_out: Optional[np.ndarray] = None):
-    """Deterministic synthetic batch (host).  Returns tokens, offsets, users, owners."""
+def generate(spec: GenSpec, nthreads: int = 0, tokens_out: Optional[np.ndarray] = None,
+             return_ids: bool = False):
+    """Deterministic synthetic batch (host).  Returns tokens, offsets, users, owners
+    (+ the global prompt ids with ``return_ids``)."""
     lib = N.load_library()
     n, L = spec.n_prompts, spec.prompt_tokens
     tokens = tokens_out if tokens_out is not None else np.empty(n * L, np.uint32)
     offsets = np.empty(n + 1, np.uint64)
     users = np.empty(n, np.uint64)
     owners = np.empty(n, np.uint8)
-    s = spec.native()
+    ids = np.empty(n, np.uint64)
+    s = spec.native(ids)
     N.raise_for(lib.skv_generate(C.byref(s), _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), nthreads),
                 "generate")
-    return tokens, offsets, users, owners
+    return (tokens, offsets, users, owners, ids) if return_ids else (tokens, offsets, users, owners)
 
 
-def generate_pool(spec: GenSpec):
+def route(tokens: np.ndarray, offsets: np.ndarray, world: int, block_tokens: int,
+          prompt_ids: Optional[np.ndarray] = None) -> np.ndarray:
+    """skv_route: owning rank of every prompt under prefix-forest partitioning (host)."""
+    lib = N.load_library()
+    tokens = np.ascontiguousarray(tokens, np.uint32)
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    n = len(offsets) - 1
+    ids = None if prompt_ids is None else np.ascontiguousarray(prompt_ids, np.uint64)
+    out = np.empty(n, np.uint32)
+    N.raise_for(lib.skv_route(_ptr(tokens), _ptr(offsets), n, block_tokens, _ptr(ids), world, _ptr(out)), "route")
+    return out
+
+
+def split_batch(tokens, offsets, users, owners, ranks: np.ndarray, rank: int):
+    """The sub-batch of the prompts routed to ``rank``, in their original (global) order."""
+    tokens = np.asarray(tokens)
+    offsets = np.asarray(offsets, np.uint64)
+    sel = np.flatnonzero(ranks == rank)
+    lens = (offsets[1:] - offsets[:-1])[sel]
+    off = np.zeros(len(sel) + 1, np.uint64)
+    np.cumsum(lens, out=off[1:])
+    parts = [tokens[int(offsets[p]):int(offsets[p + 1])] for p in sel]
+    tok = np.concatenate(parts).astype(np.uint32) if parts else np.zeros(0, np.uint32)
+    own = None if owners is None else np.asarray(owners, np.uint8)[sel]
+    return tok, off, np.asarray(users, np.uint64)[sel], own
+
+
+def generate_pool(spec: GenSpec, rank: Optional[int] = None):
+    """The shared-prefix pool; with ``rank`` (and spec.route_world > 1) only the
+    prefixes whose prefix-forest root is owned by that rank."""
+    toks, off, users, owners = _generate_pool(spec)
+    if rank is None or spec.route_world <= 1:
+        return toks, off, users, owners
+    ranks = route(toks, off, spec.route_world, spec.route_block_tokens)
+    return split_batch(toks, off, users, owners, ranks, rank)
+
+
+def _generate_pool(spec: GenSpec):
     lib = N.load_library()
     n, L = spec.pool_size, spec.pool_tokens
     tokens = np.empty(n * L, np.uint32)
