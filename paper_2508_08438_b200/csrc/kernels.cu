@@ -52,6 +52,13 @@ __device__ __forceinline__ uint64_t slot_hash(uint64_t h, uint64_t d) {
   return x;
 }
 
+// Home slot of a key: the first entry of a 128-B line (2 x 64-B entries).  Linear
+// probing from there visits the line's second entry before leaving the line, so one
+// line fetch covers the first two probe positions.
+__device__ __forceinline__ uint64_t home_slot(const Index& ix, uint64_t h, uint64_t d) {
+  return slot_hash(h, d) & ix.mask & ~1ull;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ uint4 ldg_stream(const uint32_t* p) {
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
 
 // find_slot: used by set_tiers (point lookups)
 __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, Rec* out) {
-  uint64_t s = slot_hash(h, d) & ix.mask;
+  uint64_t s = home_slot(ix, h, d);
   for (uint64_t i = 0; i <= ix.mask; ++i) {
     const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
     ulonglong2 k = rp[0];
@@ -463,9 +470,9 @@ __device__ __forceinline__ uint32_t count_insert(unsigned long long* cnt, uint32
   }
 }
 
-__device__ void record_access(const Index& ix, const MonCtx& M, uint32_t slot, uint64_t user) {
+// the distinct-user part of AccessStats::record (the hit count is applied by the caller)
+__device__ void record_user(const Index& ix, const MonCtx& M, uint32_t slot, uint64_t user) {
   Entry& e = ix.e[slot];
-  atomicAdd(&e.stats.hit_cur, 1u);
   const uint32_t si = acquire_set(e, slot, M);
   if (si == kNone) return;
   SetHdr& hd = M.hdr[si];
@@ -513,15 +520,45 @@ __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* 
 }
 
 // A.6 record, one warp per prompt, lanes = its matched blocks (order-independent part)
+// Warp = prompt, lanes = its matched blocks, kRecRounds x 32 accesses with their
+// dependent loads in flight together.  Fast path (the common case once an entry's set
+// exists): the user already sits at its home position of the set table -> nothing but
+// the hit count changes.  Everything else takes the full record_user path.
+constexpr int kRecRounds = 4;
+
 __global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32_t* __restrict__ slot_in,
                                                 const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ matched,
                                                 const uint64_t* __restrict__ users, uint32_t n_prompts) {
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
-  const uint32_t bo = blk_off[p], m = matched[p];
+  const uint32_t bo = blk_off[p], m = matched[p], lane = lane_id();
   const uint64_t u = users[p];
-  for (uint32_t b = lane_id(); b < m; b += 32) record_access(ix, M, slot_in[bo + b], u);
+  const uint32_t pos = mix32(u) & (kSetSlots - 1);
+  for (uint32_t base = 0; base < m; base += 32 * kRecRounds) {
+    uint32_t sl[kRecRounds], si[kRecRounds];
+#pragma unroll
+    for (int r = 0; r < kRecRounds; ++r) {
+      const uint32_t b = base + 32 * r + lane;
+      sl[r] = b < m ? slot_in[bo + b] : kNone;
+    }
+#pragma unroll
+    for (int r = 0; r < kRecRounds; ++r)
+      if (sl[r] != kNone) {
+        atomicAdd(&ix.e[sl[r]].stats.hit_cur, 1u);
+        si[r] = *reinterpret_cast<volatile uint32_t*>(&ix.e[sl[r]].aux.set_idx);
+      }
+    ulonglong2 v[kRecRounds];
+#pragma unroll
+    for (int r = 0; r < kRecRounds; ++r) {
+      v[r] = make_ulonglong2(0, 0);
+      if (sl[r] != kNone && si[r] < kPendingSet) v[r] = ld_relaxed128(&M.tab[static_cast<uint64_t>(si[r]) * kSetSlots + pos]);
+    }
+#pragma unroll
+    for (int r = 0; r < kRecRounds; ++r)
+      if (sl[r] != kNone && !(si[r] < kPendingSet && v[r].x == u && v[r].y >= M.wstart))
+        record_user(ix, M, sl[r], u);
+  }
 }
 
 // accesses (slot << 32 | prompt) of the entries that need an ordered replay
@@ -664,7 +701,9 @@ __global__ void __launch_bounds__(256) k_record_replay(Index ix, MonCtx M, const
 //      or creator == user, cache_index.hpp:483-485) and the first missing block (k,
 //      where the commit starts).  Probing stops at the tile holding the first miss.
 // ---------------------------------------------------------------------------------
-constexpr int kCPWarps = 2;  // 2 x 16.9 KB SMEM tiles per CTA
+constexpr int kCPWarps = 2;     // warps per CTA (8.4 KB of SMEM tiles each)
+constexpr int kCPPrompts = 16;  // prompts per warp: 4096 warps for config 2 (latency-bound chain + probes)
+constexpr int kCPInFlight = 8;  // prompts whose probe loads are in flight together
 constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
 
 struct Probe {
@@ -692,13 +731,13 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
     uint8_t* __restrict__ tier, MonCtx mon) {
-  __shared__ uint64_t s_d[kCPWarps][32][kPitch];
-  __shared__ uint64_t s_h[kCPWarps][32][kPitch];
+  __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
+  __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  const uint32_t p0 = (blockIdx.x * kCPWarps + wid) * 32;
+  const uint32_t p0 = (blockIdx.x * kCPWarps + wid) * kCPPrompts;
   if (p0 >= n_prompts) return;
   const uint32_t p = p0 + lane;
-  const bool has = p < n_prompts;
+  const bool has = lane < kCPPrompts && p < n_prompts;
   const uint32_t bo = has ? blk_off[p] : 0, n = has ? blk_off[p + 1] - bo : 0;
   const uint32_t fs = has ? first_sens[p] : 0;
   const uint64_t user = has ? users[p] : 0;
@@ -709,8 +748,8 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
   const uint32_t nmax = __reduce_max_sync(kFull, n);
   for (uint32_t t0 = 0; t0 < nmax; t0 += 32) {
     const uint32_t b = t0 + lane;
-    // all 32 prompts' digest rows in flight at once (cp.async: global -> SMEM, no registers)
-    for (uint32_t j = 0; j < 32; ++j) {
+    // all the warp's prompts' digest rows in flight at once (cp.async: global -> SMEM)
+    for (uint32_t j = 0; j < kCPPrompts; ++j) {
       const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
       if (b < nj) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&td[j][lane]));
@@ -725,7 +764,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
       th[lane][c] = h;
     }
     __syncwarp();
-    for (uint32_t j = 0; j < 32; ++j) {
+    for (uint32_t j = 0; j < kCPPrompts; ++j) {
       const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
       const uint32_t fsj = __shfl_sync(kFull, fs, j);
       if (b < nj) {
@@ -735,35 +774,35 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     }
     uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
     while (todo) {
-      uint32_t js[4];
+      uint32_t js[kCPInFlight];
       int ng = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kCPInFlight; ++q) {
         js[q] = todo ? static_cast<uint32_t>(__ffs(todo) - 1) : 32u;
         if (todo) {
           todo &= todo - 1;
           ++ng;
         }
       }
-      // issue up to 4 independent first-slot loads per lane
-      ulonglong2 kk[4], mm[4];
-      uint64_t ss[4];
+      // issue up to kCPInFlight independent first-slot loads per lane
+      ulonglong2 kk[kCPInFlight], mm[kCPInFlight];
+      uint64_t ss[kCPInFlight];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t j = js[q] & 31;
+      for (int q = 0; q < kCPInFlight; ++q) {
+        const uint32_t j = js[q] & (kCPPrompts - 1);
         const uint32_t nj = __shfl_sync(kFull, n, j);
         kk[q] = make_ulonglong2(0, 0);
         mm[q] = make_ulonglong2(0, 0);
         ss[q] = 0;
         if (q < ng && b < nj) {
-          ss[q] = slot_hash(th[j][lane], td[j][lane]) & ix.mask;
+          ss[q] = home_slot(ix, th[j][lane], td[j][lane]);
           const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[ss[q]].rec);
           kk[q] = rp[0];
           mm[q] = rp[1];
         }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kCPInFlight; ++q) {
         if (q >= ng) break;
         const uint32_t j = js[q];
         const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
@@ -824,6 +863,8 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 //     rewrites the payload from the winning prompt.
 // Claim values are >= 2^31 and never collide with the epoch candidate stamps (< 2^31)
 // kept in the same word.
+constexpr int kCommitRounds = 4;
+
 __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
                                                 const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
@@ -831,6 +872,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
                                                 uint32_t n_prompts, uint32_t* __restrict__ slot_out,
                                                 unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                                                 uint32_t fix_cap, uint32_t* err_flag) {
+  constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   const uint32_t lane = lane_id();
@@ -841,57 +883,123 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
   const uint32_t owner_bits = static_cast<uint32_t>(owners ? owners[p] : 0) << 8;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
   uint32_t inserted = 0;
-  for (uint32_t base = k0; base < n; base += 32) {
-    const uint32_t b = base + lane;
-    const bool act = b < n;
-    uint32_t s32 = kNone;
-    bool mine = false;
-    uint32_t lab = 0;
-    if (act) {
-      const uint64_t h = hk[bo + b], d = dk[bo + b];
-      lab = label[bo + b];
-      uint64_t s = slot_hash(h, d) & ix.mask;
-      // both 32-B sectors of the home entry in one DRAM burst: the CAS (sector 0) and the
-      // claim/link writes (sector 1) then hit L2
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(&ix.e[s]) : "memory");
-      uint64_t i = 0;
-      for (; i <= ix.mask; ++i) {
-        unsigned long long ol, oh;
-        unsigned long long* kp = reinterpret_cast<unsigned long long*>(&ix.e[s].rec);
-        if (cas128(kp, 0ull, 0ull, h, d, &ol, &oh)) {
-          mine = true;
-          break;
-        }
-        if (ol == h && oh == d) break;
-        s = (s + 1) & ix.mask;
+  for (uint32_t base = k0; base < n; base += 32 * R) {
+    uint64_t h[R], d[R];
+    uint32_t s32[R], lab[R];
+    bool mine[R];
+    // claims: the first CAS of every round is issued before any result is awaited, so a
+    // warp keeps R random DRAM round trips in flight instead of serialising them
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t b = base + 32 * r + lane;
+      s32[r] = kNone;
+      mine[r] = false;
+      lab[r] = 0;
+      if (b < n) {
+        h[r] = hk[bo + b];
+        d[r] = dk[bo + b];
+        lab[r] = label[bo + b];
       }
-      if (i > ix.mask) atomicOr(err_flag, 2u);
-      s32 = static_cast<uint32_t>(s);
-      slot_out[bo + b] = s32;
     }
-    uint32_t parent = __shfl_up_sync(kFull, s32, 1);
-    if (lane == 0) parent = carry;
-    carry = __shfl_sync(kFull, s32, 31);
-    if (act && s32 != kNone) {
-      Entry& e = ix.e[s32];
+    // claims.  1) plain loads of both keys of every round's home line, all in flight
+    // together (one DRAM round trip); 2) CAS on the first of the two that is empty or
+    // already holds the key -- the line is in L2 now; 3) rare: the line is full or the
+    // CAS lost a race to another key -> linear probing with CAS, every pending round's
+    // next CAS again in flight together.
+    uint64_t sl[R];
+    ulonglong2 k0v[R], k1v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sl[r] = 0;
+      if (base + 32 * r + lane < n) {
+        sl[r] = home_slot(ix, h[r], d[r]);
+        k0v[r] = ld_relaxed128(reinterpret_cast<const ulonglong2*>(&ix.e[sl[r]].rec));
+        k1v[r] = ld_relaxed128(reinterpret_cast<const ulonglong2*>(&ix.e[sl[r] + 1].rec));
+      }
+    }
+    unsigned long long ol[R], oh[R];
+    bool pend[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      pend[r] = false;
+      if (base + 32 * r + lane >= n) continue;
+      const bool f0 = (k0v[r].x == 0 && k0v[r].y == 0) || (k0v[r].x == h[r] && k0v[r].y == d[r]);
+      const bool f1 = (k1v[r].x == 0 && k1v[r].y == 0) || (k1v[r].x == h[r] && k1v[r].y == d[r]);
+      if (!f0) sl[r] = f1 ? sl[r] + 1 : (sl[r] + 2) & ix.mask;
+      mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
+                       &oh[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
+    for (uint64_t i = 1;; ++i) {
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) any |= pend[r];
+      if (!any) break;
+      if (i > ix.mask) {  // table full
+        atomicOr(err_flag, 2u);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (pend[r]) {
+            pend[r] = false;
+            sl[r] = ~0ull;
+          }
+        break;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (pend[r]) {
+          sl[r] = (sl[r] + 1) & ix.mask;
+          mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
+                           &oh[r]);
+        }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (pend[r]) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (base + 32 * r + lane >= n || sl[r] == ~0ull) continue;
+      s32[r] = static_cast<uint32_t>(sl[r]);
+      slot_out[bo + base + 32 * r + lane] = s32[r];
+    }
+    // payloads, first-creator marks and parent links (parent = previous block's slot)
+    uint32_t par[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      par[r] = __shfl_up_sync(kFull, s32[r], 1);
+      if (lane == 0) par[r] = carry;
+      carry = __shfl_sync(kFull, s32[r], 31);
+    }
+    uint32_t sib[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sib[r] = kNone;
+      if (s32[r] == kNone) continue;
+      Entry& e = ix.e[s32[r]];
       atomicMax(&e.aux.mark, tag);
-      if (mine) {
-        const uint32_t meta = lab | owner_bits | (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
+      if (mine[r]) {
+        const uint32_t meta = lab[r] | owner_bits | (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
         ulonglong2 payload;
         payload.x = creator;
-        payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
+        payload.y = static_cast<unsigned long long>(par[r]) | (static_cast<unsigned long long>(meta) << 32);
         reinterpret_cast<ulonglong2*>(&e.rec)[1] = payload;
-        if (parent != kNone) e.aux.next_sibling = atomicExch(&ix.e[parent].aux.first_child, s32);
+        if (par[r] != kNone) sib[r] = atomicExch(&ix.e[par[r]].aux.first_child, s32[r]);
         ++inserted;
       } else {
         const uint32_t f = atomicAdd(n_fix, 1u);
-        if (f < fix_cap)
-          fix_list[f] = s32;
-        else
+        if (f < fix_cap) {
+          fix_list[f] = s32[r];
+          fix_list[fix_cap + f] = base + 32 * r + lane;  // block depth of this key
+        } else {
           atomicOr(err_flag, 4u);
-        if (f < fix_cap) fix_list[fix_cap + f] = b;  // block depth of this key
+        }
       }
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (mine[r] && par[r] != kNone) ix.e[s32[r]].aux.next_sibling = sib[r];
   }
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
@@ -1135,7 +1243,7 @@ void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
                         cudaStream_t s) {
   if (n)
-    k_chain_probe<<<cdiv(n, 32 * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
+    k_chain_probe<<<cdiv(n, kCPPrompts * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
                                                                    decision, slot, matched, exist, tier, mon);
 }
 
