@@ -282,8 +282,9 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
   c->rules_loaded = true;
   c->hs_layout = skv::hash_scan_layout(c->rules_dev, c->cfg.block_tokens, c->cfg.window_tokens);
   c->hs_smem = c->hs_layout.total;
-  if (c->hs_smem > 227 * 1024) throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB");
-  c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem);
+  if (c->hs_layout.warps == 0 || c->hs_smem > 227 * 1024)
+    throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB (block_tokens too large)");
+  c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem, 32 * c->hs_layout.warps);
   if (c->hs_grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
 }
 
@@ -321,13 +322,12 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
   a.d_out = bd;
   a.mask_out = bmask;
   a.first_sens = first_sens;
-  a.off_cls = c->hs_layout.off_cls;
-  a.off_raw = c->hs_layout.off_raw;
-  a.off_so = c->hs_layout.off_so;
-  a.off_xch = c->hs_layout.off_xch;
   a.off_list = c->hs_layout.off_list;
   a.stage = c->hs_layout.stage;
-  skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, st);
+  a.buf_gap = c->hs_layout.buf_gap;
+  a.n_gap = c->hs_layout.n_gap;
+  a.buf_tail = c->hs_layout.buf_tail;
+  skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, 32 * c->hs_layout.warps, st);
 }
 
 // Offsets of a host batch: [0, n_tokens], non-decreasing.  Returns the block count.

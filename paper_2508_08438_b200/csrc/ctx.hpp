@@ -91,11 +91,11 @@ struct HashScanArgs {
   uint32_t* mask_out;
   uint32_t* first_sens;
   // dynamic shared-memory layout (hash_scan_layout)
-  uint32_t off_cls, off_raw, off_so, off_xch, off_list, stage;
+  uint32_t off_list, stage, buf_gap, n_gap, buf_tail;  // hash_scan_layout
 };
 
 struct HSLayout {
-  uint32_t stage, off_cls, off_raw, off_so, off_xch, off_list, total;
+  uint32_t stage, off_list, buf_gap, n_gap, buf_tail, warps, total;
 };
 
 struct Index {
@@ -139,9 +139,9 @@ void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32
 size_t scan_temp_bytes(uint32_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint32_t n,
                            cudaStream_t s);
-int hash_scan_grid(int device, uint32_t smem_bytes);
+int hash_scan_grid(int device, uint32_t smem_bytes, uint32_t threads);
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
-void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s);
+void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,

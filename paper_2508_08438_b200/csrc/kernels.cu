@@ -60,6 +60,7 @@ __device__ __forceinline__ uint64_t home_slot(const Index& ix, uint64_t h, uint6
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ldg_stream(const uint32_t* p) {
   uint4 r;
@@ -81,22 +82,36 @@ __global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uin
 // ---------------------------------------------------------------------------------
 // K12: fused block digest + rule-DFA window scan.
 //
-// Persistent CTAs; CTA i owns global blocks [i*nb/G, (i+1)*nb/G).  Each iteration takes
-// a chunk of up to kHSThreads consecutive blocks (may span prompts), stages the chunk's
-// token span [first window start, last window end) HBM -> SMEM once with coalesced
-// 128-bit streaming loads (every token is read from HBM exactly once), converting each
-// token to its pre-scaled DFA byte class and its raw byte.  Thread t then
-//   * hashes block t from the SMEM raw bytes (token_seq_digest, core.hpp:68-73);
-//   * runs the SMEM-resident u16 DFA over its own block and its first context block
-//     (3 instructions + 1 LDS per byte; accepting transitions land in the copy region
-//     >= 32 KB and are decoded to the exact rule mask off the common path);
-//   * takes the rest of its window (the second context block when W = 2B) from its
-//     right neighbour: both runs are in the same DFA state at that block boundary in
-//     >99% of windows (measured on config 2), so the neighbour's first-context scan IS
-//     this window's second-context scan; otherwise it scans the bytes itself.
-// The window overlap is served from SMEM, never re-read from HBM.
+// Warp-autonomous persistent kernel: warp w of the grid owns global blocks
+// [w*nb/NW, (w+1)*nb/NW) and walks them in chunks of 32 consecutive blocks (a chunk may
+// span prompts), with no CTA-wide barrier after the DFA table load.  Per chunk:
+//   staging  the chunk's token span [first window start, last window end) HBM -> the
+//            warp's SMEM buffers with coalesced 128-bit streaming loads (every token is
+//            read from HBM once; only the W-token right context of the last window is
+//            re-read by the next chunk, from L2), converted to pre-scaled DFA byte
+//            classes and raw bytes.  The next chunk's span is prefetched into L2 by TMA.
+//   lane l owns window l (block b of prompt p, window [bB, min(L, bB+B+W))):
+//   phase A  digest of block b (token_seq_digest, core.hpp:68-73) and the DFA run over
+//            block b from the start state; records the state after kConv bytes (Z),
+//            after W' = min(W,B) bytes (SW) and at the block end (X).
+//   phase B  window l continues over the next block from X.  Window l+1 (block b+1)
+//            ran those bytes from the start state; two runs of a DFA in the same state
+//            at the same byte are identical from there on, so after kConv bytes window
+//            l compares its state with lane l+1's Z: equal (the common case -- the runs
+//            synchronise within a few bytes) -> window l's run over the rest of that
+//            block IS window l+1's own-block run (its row-OR and state SW are reused
+//            through a shuffle); otherwise window l steps the bytes itself.
+//   phase C  (W = 2B) the same argument at the second block boundary: if window l is in
+//            lane l+1's phase-B start state X, window l's last block is lane l+1's
+//            phase-B run.
+// So a window costs B + kConv DFA steps instead of B + W.  The fast pass only tracks
+// WHETHER an accepting transition was taken (bit 15 of the OR of visited row offsets:
+// accepting transitions land in copy rows >= 32 KB); the exact enabled-rule mask of the
+// few windows that accepted is recomputed per flagged segment (own block / first /
+// second context block) from its known start state, one lane per segment.
 // ---------------------------------------------------------------------------------
-constexpr int kHSThreads = 256;
+constexpr uint32_t kHSWarps = 16;  // warps per CTA (fewer when the staging buffers do not fit)
+constexpr uint32_t kConv = 4;  // context bytes stepped before comparing with the neighbour's run
 
 __device__ __forceinline__ uint32_t lds16(const uint8_t* base, uint32_t off) {
   return *reinterpret_cast<const uint16_t*>(base + off);
@@ -109,52 +124,44 @@ __device__ __forceinline__ uint32_t copy_mask(const uint16_t* acc_tab, uint32_t 
   return (r & kAccRegion) ? acc_tab[__umulhi(r - kAccRegion, inv)] : 0u;
 }
 
-// Scan class bytes [o, end) from row; returns the final row offset and ORs the exact
-// enabled-rule mask of every accepting transition into *acc.  Accepting transitions are
-// rare, so the per-4-byte check is one OR-test and a predicated-off branch.
-__device__ __forceinline__ uint32_t dfa_run(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
-                                            const uint16_t* __restrict__ acc_tab, uint32_t inv, uint32_t o,
-                                            uint32_t end, uint32_t row, uint32_t* acc) {
+// 4 DFA steps over the 4 class bytes of w; the visited row offsets are OR-ed into acc
+__device__ __forceinline__ uint32_t step4(const uint8_t* __restrict__ tab, uint32_t row, uint32_t w,
+                                          uint32_t& acc) {
+  const uint32_t r0 = lds16(tab, row + __byte_perm(w, 0u, 0x4440u));
+  const uint32_t r1 = lds16(tab, r0 + __byte_perm(w, 0u, 0x4441u));
+  const uint32_t r2 = lds16(tab, r1 + __byte_perm(w, 0u, 0x4442u));
+  const uint32_t r3 = lds16(tab, r2 + __byte_perm(w, 0u, 0x4443u));
+  acc |= r0 | r1 | r2 | r3;
+  return r3;
+}
+
+// DFA run over cls[o, end) from row (any alignment); OR of visited rows into acc
+__device__ __forceinline__ uint32_t run_or(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
+                                           uint32_t o, uint32_t end, uint32_t row, uint32_t& acc) {
   uint32_t m = 0;
   while (o < end && (o & 3)) {
     row = lds16(tab, row + cls[o++]);
-    m |= copy_mask(acc_tab, row, inv);
+    m |= row;
   }
-  // 16-byte groups: PRMT byte extraction, one acceptance test per group
-  for (; o + 16 <= end; o += 16) {
-    uint32_t r[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o + 4 * q);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        row = lds16(tab, row + __byte_perm(w, 0u, 0x4440u + k));
-        r[4 * q + k] = row;
-      }
-    }
-    uint32_t any = 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) any |= r[q];
-    if (any & kAccRegion) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) m |= copy_mask(acc_tab, r[q], inv);
-    }
-  }
-  for (; o + 4 <= end; o += 4) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(cls + o);
-    const uint32_t r0 = lds16(tab, row + (w & 0xffu));
-    const uint32_t r1 = lds16(tab, r0 + ((w >> 8) & 0xffu));
-    const uint32_t r2 = lds16(tab, r1 + ((w >> 16) & 0xffu));
-    row = lds16(tab, r2 + (w >> 24));
-    if ((r0 | r1 | r2 | row) & kAccRegion)
-      m |= copy_mask(acc_tab, r0, inv) | copy_mask(acc_tab, r1, inv) | copy_mask(acc_tab, r2, inv) |
-           copy_mask(acc_tab, row, inv);
-  }
+  for (; o + 4 <= end; o += 4) row = step4(tab, row, *reinterpret_cast<const uint32_t*>(cls + o), m);
   while (o < end) {
     row = lds16(tab, row + cls[o++]);
+    m |= row;
+  }
+  acc |= m;
+  return row;
+}
+
+// exact run: the enabled-rule mask of every accepting transition OR-ed into *mask
+__device__ __forceinline__ uint32_t run_exact(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cls,
+                                              const uint16_t* __restrict__ acc_tab, uint32_t inv, uint32_t o,
+                                              uint32_t end, uint32_t row, uint32_t* mask) {
+  uint32_t m = 0;
+  for (; o < end; ++o) {
+    row = lds16(tab, row + cls[o]);
     m |= copy_mask(acc_tab, row, inv);
   }
-  *acc |= m;
+  *mask |= m;
   return row;
 }
 
@@ -165,61 +172,132 @@ __device__ __forceinline__ uint64_t digest_bytes(const uint8_t* __restrict__ raw
   for (; o + 4 <= end; o += 4) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(raw + o);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) h = (h ^ ((w >> (8 * k)) & 0xffu)) * kFnvP4;
+    for (int k = 0; k < 4; ++k) h = (h ^ __byte_perm(w, 0u, 0x4440u + k)) * kFnvP4;
   }
   for (; o < end; ++o) h = (h ^ raw[o]) * kFnvP4;
   return h;
 }
 
-// index of the last element <= x in so[0..n) (so[0] <= x guaranteed)
-__device__ __forceinline__ uint32_t so_search(const uint32_t* so, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (so[mid] <= x)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  return lo;
+__device__ __forceinline__ uint64_t digest16(uint4 v, uint64_t h) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h = (h ^ __byte_perm(w[q], 0u, 0x4440u + k)) * kFnvP4;
+  return h;
 }
 
-struct WinGeo {
-  uint32_t gb, p, b, ws, we;
+__device__ __forceinline__ void stage4(uint8_t* cls, uint8_t* raw, const uint8_t* cmap, uint32_t q, uint32_t t0,
+                                       uint32_t t1, uint32_t t2, uint32_t t3, uint32_t& wide) {
+  wide |= t0 | t1 | t2 | t3;
+  const uint32_t c = cmap[t0 & 0xff] | (cmap[t1 & 0xff] << 8) | (cmap[t2 & 0xff] << 16) |
+                     (static_cast<uint32_t>(cmap[t3 & 0xff]) << 24);
+  reinterpret_cast<uint32_t*>(cls)[q] = c;
+  reinterpret_cast<uint32_t*>(raw)[q] = __byte_perm(__byte_perm(t0, t1, 0x0040), __byte_perm(t2, t3, 0x0040), 0x5410);
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, uint32_t src) {
+  const uint32_t lo = __shfl_sync(kFull, static_cast<uint32_t>(v), src);
+  const uint32_t hi = __shfl_sync(kFull, static_cast<uint32_t>(v >> 32), src);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// Deferred exact-mask task: a flagged segment (<= 16 tokens) of a window, its start row
+// and where its mask goes.  32 B, one SMEM slot.
+struct SegTask {
+  unsigned long long tok;  // first token index of the segment
+  uint32_t meta;           // start row | len << 16
+  uint32_t gb, p, b;
+  uint32_t pad;
 };
 
-// so[i] = blk_off[pp + i], so_tok[i] = tok_off[pp + i] (SMEM copies for the chunk)
-__device__ __forceinline__ WinGeo window_geo(const HashScanArgs& a, const uint32_t* so, const uint64_t* so_tok,
-                                             uint32_t n_so, uint32_t pp, uint32_t g, uint32_t t, uint64_t as) {
-  WinGeo w;
-  w.gb = g + t;
-  const uint32_t i = so_search(so, n_so, w.gb);
-  w.p = pp + i;
-  w.b = w.gb - so[i];
-  const uint64_t base = so_tok[i];
-  const uint64_t L = so_tok[i + 1] - base;
-  w.ws = static_cast<uint32_t>(base + static_cast<uint64_t>(w.b) * a.B - as);
-  const uint64_t wend = min(L, static_cast<uint64_t>(w.b) * a.B + a.B + a.W);
-  w.we = static_cast<uint32_t>(base + wend - as);
-  return w;
+// exact run over tokens[tok, tok+len) (len <= 16) from row: OR of the enabled-rule masks
+// of every accepting transition
+__device__ __forceinline__ uint32_t exact_tokens(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cmap,
+                                                 const uint16_t* __restrict__ acc_tab, uint32_t inv,
+                                                 const uint32_t* __restrict__ tokens, uint64_t tok, uint32_t len,
+                                                 uint32_t row) {
+  uint32_t t[16];
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) t[j] = j < len ? tokens[tok + j] : 0u;
+  uint32_t m = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) {
+    if (j < len) {
+      row = lds16(tab, row + cmap[t[j] & 0xffu]);
+      m |= copy_mask(acc_tab, row, inv);
+    }
+  }
+  return m;
 }
 
-__global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
+__device__ __forceinline__ void flush_tasks(const SegTask* q, uint32_t qn, uint32_t lane, const uint8_t* tab,
+                                            const uint8_t* cmap, const uint16_t* acc_tab, uint32_t inv,
+                                            const HashScanArgs& a) {
+  __syncwarp();
+  if (lane < qn) {
+    const SegTask t = q[lane];
+    const uint32_t m = exact_tokens(tab, cmap, acc_tab, inv, a.tokens, t.tok, t.meta >> 16, t.meta & 0xffffu);
+    if (m) {
+      atomicOr(&a.mask_out[t.gb], m);
+      atomicMin(&a.first_sens[t.p], t.b);
+    }
+  }
+  __syncwarp();
+}
+
+// DFA run over tokens[o, e) from row (global loads, L1/L2 hits: the warp has just read
+// these lines); OR of the visited rows into acc.  Used off the fast path only.
+__device__ __forceinline__ uint32_t run_tokens(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cmap,
+                                               const uint32_t* __restrict__ tokens, uint64_t o, uint64_t e,
+                                               uint32_t row, uint32_t& acc) {
+  uint32_t m = 0;
+  for (; o < e; ++o) {
+    row = lds16(tab, row + cmap[tokens[o] & 0xffu]);
+    m |= row;
+  }
+  acc |= m;
+  return row;
+}
+
+// FNV-1a step of a byte token: (h ^ t) * P^4 mod 2^64 in four 32-bit multiplies
+__device__ __forceinline__ uint64_t fnv_tok(uint64_t h, uint32_t t) {
+  const uint32_t lo = static_cast<uint32_t>(h) ^ t, hi = static_cast<uint32_t>(h >> 32);
+  uint32_t rlo, rhi;
+  asm("{\n\t.reg .u32 c;\n\t"
+      "mul.lo.u32 c, %2, %4;\n\t"
+      "mad.lo.u32 c, %3, %5, c;\n\t"
+      "mul.lo.u32 %0, %3, %4;\n\t"
+      "mad.hi.u32 %1, %3, %4, c;\n\t}"
+      : "=r"(rlo), "=r"(rhi)
+      : "r"(hi), "r"(lo), "r"(static_cast<uint32_t>(kFnvP4)), "r"(static_cast<uint32_t>(kFnvP4 >> 32)));
+  return (static_cast<uint64_t>(rhi) << 32) | rlo;
+}
+
+__device__ __forceinline__ void ldg_tokens16(const uint32_t* p, uint32_t (&t)[16], bool a8) {
+  if (a8) {  // 32-B aligned: two 256-bit loads
+#pragma unroll
+    for (uint32_t k = 0; k < 2; ++k)
+      asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(t[8 * k]), "=r"(t[8 * k + 1]), "=r"(t[8 * k + 2]), "=r"(t[8 * k + 3]), "=r"(t[8 * k + 4]),
+                     "=r"(t[8 * k + 5]), "=r"(t[8 * k + 6]), "=r"(t[8 * k + 7])
+                   : "l"(p + 8 * k));
+  } else {
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + 4 * k);
+      t[4 * k] = v.x, t[4 * k + 1] = v.y, t[4 * k + 2] = v.z, t[4 * k + 3] = v.w;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* tab = sm;
-  uint8_t* cls = sm + a.off_cls;
-  uint8_t* raw = sm + a.off_raw;
-  uint32_t* so = reinterpret_cast<uint32_t*>(sm + a.off_so);
-  uint64_t* so_tok = reinterpret_cast<uint64_t*>(sm + a.off_so + round16((kHSThreads + 1) * 4));
-  uint32_t* xs_x = reinterpret_cast<uint32_t*>(sm + a.off_xch);
-  uint32_t* xs_y = xs_x + kHSThreads;
-  uint32_t* xs_o = xs_y + kHSThreads;
   uint16_t* acc_tab = reinterpret_cast<uint16_t*>(sm + a.off_list);
-  const uint32_t inv = a.rules.copy_inv;
   __shared__ uint8_t cmap[256];
-  __shared__ uint32_t s_pp;
-
-  const uint32_t tid = threadIdx.x;
+  __shared__ SegTask s_q[kHSWarps][32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   {  // DFA rows [0, norm) and accepting copies [32768, fast_bytes) -> SMEM
     const uint32_t n0 = (a.rules.norm_bytes + 15) / 16;
     const uint32_t n1 = (a.rules.fast_bytes - kAccRegion + 15) / 16;
@@ -230,11 +308,18 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
     if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
     for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
   }
-  const uint32_t nb = a.blk_off[a.n_prompts];  // device-side block count (no host round trip)
-  const uint32_t G0 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * nb) / gridDim.x);
-  const uint32_t G1 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x + 1) * nb) / gridDim.x);
-  if (tid == 0 && G0 < G1) {
-    uint32_t lo = 0, hi = a.n_prompts;  // prompt containing G0
+  __syncthreads();
+  SegTask* q = s_q[wid];
+  const uint32_t* __restrict__ tokens = a.tokens;
+  const uint32_t inv = a.rules.copy_inv;
+  const uint32_t N = a.n_prompts;
+  const uint32_t nb = a.blk_off[N];  // device-side block count (no host round trip)
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + wid, TW = static_cast<uint64_t>(gridDim.x) * nwarps;
+  const uint32_t G0 = static_cast<uint32_t>(gw * nb / TW), G1 = static_cast<uint32_t>((gw + 1) * nb / TW);
+  if (G0 >= G1) return;
+  uint32_t pp = 0;
+  {  // prompt containing G0
+    uint32_t lo = 0, hi = N;
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (a.blk_off[mid] <= G0)
@@ -242,123 +327,219 @@ __global__ void __launch_bounds__(kHSThreads) k_hash_scan(HashScanArgs a) {
       else
         hi = mid;
     }
-    s_pp = lo;
+    pp = lo;
   }
-  __syncthreads();
-  if (G0 >= G1) return;
-  uint32_t pp = s_pp;
-  uint32_t g = G0;
+  uint32_t g = G0, qn = 0;
   const uint32_t B = a.B, W = a.W;
+  const uint32_t Wp = min(W, B), kc = min(kConv, Wp);
   const uint32_t start_row = a.rules.start_row, eos2 = a.rules.eos2;
+  const bool b16 = B == 16 && W >= kConv;
+  const bool defer = W <= 2 * B && B <= 16;  // every flagged segment fits one 16-token task
+  // prompt metadata of prompts pbase .. pbase+32 held in lanes (so = first block, st = first
+  // token); reloaded only when a chunk reaches past it
+  uint32_t pbase = 0xffffffffu, so = 0, so32 = 0;
+  uint64_t st = 0, st32 = 0;
   while (g < G1) {
-    for (uint32_t t = tid; t <= kHSThreads; t += blockDim.x) {
-      const uint32_t q = min(pp + t, a.n_prompts);
-      so[t] = a.blk_off[q];
-      so_tok[t] = a.tok_off[q];
+    if (pp < pbase || pp >= pbase + 31 || (so32 <= g + 31 && pbase + 32 < N && pp > pbase)) {
+      pbase = pp;
+      const uint32_t pl = min(pp + lane, N), p32 = min(pp + 32, N);
+      so = a.blk_off[pl];
+      st = a.tok_off[pl];
+      so32 = a.blk_off[p32];
+      st32 = a.tok_off[p32];
     }
-    __syncthreads();
-    uint32_t nw = min(static_cast<uint32_t>(kHSThreads), G1 - g);
-    if (pp + kHSThreads <= a.n_prompts) nw = min(nw, so[kHSThreads] - g);
-    uint32_t lastg = g + nw - 1;
-    // il = index of the prompt holding lastg = number of prompt starts in (g, lastg]
-    uint32_t il = __syncthreads_count(tid < kHSThreads && pp + tid + 1 <= a.n_prompts && so[tid + 1] <= lastg);
-    const uint64_t s_tok = so_tok[0] + static_cast<uint64_t>(g - so[0]) * B;
-    uint64_t e_tok = min(so_tok[il + 1], so_tok[il] + static_cast<uint64_t>(lastg - so[il] + 1) * B + W);
-    const uint64_t as = s_tok & ~3ull;
-    if (e_tok - as > a.stage - 8) {  // too many prompt tails in the span: single-prompt chunk
-      nw = min(nw, so[1] - g);
-      lastg = g + nw - 1;
-      il = 0;
-      e_tok = min(so_tok[1], so_tok[0] + static_cast<uint64_t>(lastg - so[0] + 1) * B + W);
-    }
-    const uint32_t n_so = il + 1;
-    // ---- TMA bulk prefetch of the next chunk's token span into L2 (it starts where this
-    // span's right context begins); the staging loads of the next iteration then hit L2
-    if (tid == 0 && g + nw < G1) {
-      const uint64_t nxt = (e_tok > W ? e_tok - W : 0) & ~3ull;
-      const uint64_t lim = a.n_tokens & ~3ull;
-      if (nxt < lim) {
-        const uint64_t bytes = min(static_cast<uint64_t>(a.stage) * 4, (lim - nxt) * 4) & ~15ull;
-        if (bytes)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.tokens + nxt),
-                       "r"(static_cast<uint32_t>(bytes))
-                       : "memory");
-      }
-    }
-    // ---- stage tokens -> (2*class, raw byte); 4 tokens per 128-bit streaming load
-    const uint32_t nq = static_cast<uint32_t>((e_tok - as + 3) >> 2);
-    uint32_t wide = 0;
-    for (uint32_t q = tid; q < nq; q += blockDim.x) {
-      const uint64_t gi = as + 4ull * q;
-      uint32_t t0, t1, t2, t3;
-      if (gi + 4 <= a.n_tokens) {
-        const uint4 v = ldg_stream(a.tokens + gi);
-        t0 = v.x, t1 = v.y, t2 = v.z, t3 = v.w;
+    const uint32_t d = pp - pbase;  // lane of prompt pp
+    // ---- chunk: up to 32 consecutive blocks within the loaded prompts
+    uint32_t nw = min(32u, G1 - g);
+    if (pbase + 32 <= N) nw = min(nw, so32 - g);
+    const uint32_t lastg = g + nw - 1;
+    // prompt starts inside the chunk (lanes > d whose first block is <= lastg)
+    const uint32_t starts = __ballot_sync(kFull, lane > d && so <= lastg);
+    const uint32_t il = __popc(starts);
+    // windows >= nout are helpers: their phase A/B results serve the windows before
+    // them, and they are redone as the first windows of the next chunk
+    const uint32_t nout = (g + nw == G1 || nw <= 2) ? nw : nw - 2;
+    const uint32_t gb = g + lane;
+    uint32_t i, bm;  // prompt lane of this window; bit w = a prompt starts at window w
+    if (il == 0) {   // the whole chunk lies in prompt pp
+      i = d;
+      bm = 0;
+    } else {
+      const uint32_t pos = ((starts >> lane) & 1u) ? so - g : 32u;
+      bm = __reduce_or_sync(kFull, pos < 32 ? 1u << pos : 0u);
+      if (__popc(bm) == il) {  // distinct starts (no empty prompt inside the chunk)
+        i = d + __popc(bm & (0xffffffffu >> (31 - lane)));
       } else {
-        t0 = gi < a.n_tokens ? a.tokens[gi] : 0;
-        t1 = gi + 1 < a.n_tokens ? a.tokens[gi + 1] : 0;
-        t2 = gi + 2 < a.n_tokens ? a.tokens[gi + 2] : 0;
-        t3 = 0;
-      }
-      wide |= (t0 | t1 | t2 | t3) >> 8;
-      const uint32_t c = cmap[t0 & 0xff] | (cmap[t1 & 0xff] << 8) | (cmap[t2 & 0xff] << 16) |
-                         (static_cast<uint32_t>(cmap[t3 & 0xff]) << 24);
-      const uint32_t r = __byte_perm(__byte_perm(t0, t1, 0x0040), __byte_perm(t2, t3, 0x0040), 0x5410);
-      reinterpret_cast<uint32_t*>(cls)[q] = c;
-      reinterpret_cast<uint32_t*>(raw)[q] = r;
-    }
-    wide = __syncthreads_or(wide != 0);
-    // ---- phase 1+2: digest, own block, first context block
-    WinGeo w{};
-    uint32_t Y = 0, orr = 0, e1 = 0;
-    const bool act = tid < nw;
-    if (act) {
-      w = window_geo(a, so, so_tok, n_so, pp, g, tid, as);
-      uint64_t dg;
-      if (!wide) {
-        dg = digest_bytes(raw, w.ws, B, a.digest_init);
-      } else {  // a token >= 256 in this chunk: full update_u32 per token
-        dg = a.digest_init;
-        const uint32_t* tp = a.tokens + a.tok_off[w.p] + static_cast<uint64_t>(w.b) * B;
-        for (uint32_t k = 0; k < B; ++k) dg = fnv_u32(dg, tp[k]);
-      }
-      a.d_out[w.gb] = dg;
-      const uint32_t X = dfa_run(tab, cls, acc_tab, inv, w.ws, w.ws + B, start_row, &orr);
-      e1 = min(w.we, w.ws + 2 * B);
-      uint32_t o1 = 0;
-      Y = dfa_run(tab, cls, acc_tab, inv, w.ws + B, e1, X, &o1);
-      orr |= o1;
-      xs_x[tid] = X;
-      xs_y[tid] = Y;
-      xs_o[tid] = o1;
-    }
-    __syncthreads();
-    // ---- phase 3: rest of the window, shared with the right neighbour when in sync
-    if (act) {
-      uint32_t fin = Y;
-      if (e1 < w.we) {
-        const bool share = w.we == w.ws + 3 * B && tid + 1 < nw && w.gb + 1 < so[w.p - pp + 1] &&
-                           xs_x[tid + 1] == Y;
-        if (share) {
-          orr |= xs_o[tid + 1];
-          fin = xs_y[tid + 1];
-        } else {
-          fin = dfa_run(tab, cls, acc_tab, inv, e1, w.we, Y, &orr);
+        i = d;
+#pragma unroll
+        for (uint32_t s = 16; s >= 1; s >>= 1) {
+          const uint32_t v = __shfl_sync(kFull, so, min(i + s, 31u));
+          if (i + s <= d + il && v <= gb) i += s;
         }
       }
-      orr |= copy_mask(acc_tab, lds16(tab, fin + eos2), inv);
-      a.mask_out[w.gb] = orr;
-      if (orr) atomicMin(&a.first_sens[w.p], w.b);
     }
-    g += nw;
-    if (tid == 0) {
-      uint32_t np = pp + il;
-      while (np < a.n_prompts && a.blk_off[np + 1] <= g) ++np;
-      s_pp = np;
+    const uint32_t i1 = min(i + 1, 31u);
+    const uint64_t t_i = shfl64(st, i), t_1 = shfl64(st, i1);
+    const uint32_t so_i = __shfl_sync(kFull, so, i);
+    const uint64_t t_i1 = i + 1 < 32 ? t_1 : st32;  // end of prompt pbase + i
+    const uint32_t b = gb - so_i, p = pbase + i;
+    const uint64_t ws = t_i + static_cast<uint64_t>(b) * B;
+    const uint64_t we = min(t_i1, ws + B + W);
+    const bool act = lane < nw, out = lane < nout;
+    const bool nbr = lane + 1 < nw && !((bm >> (lane + 1)) & 1u);  // block b+1: same prompt, this chunk
+    // ---- phase A: the block's tokens, digest, DFA over the block from the start state
+    uint32_t A = 0, X = 0, Z = 0, SW = 0, amid = 0, cw0 = 0;
+    if (act) {
+      uint64_t dg = a.digest_init;
+      if (b16 && (ws & 3) == 0) {
+        uint32_t t[16];
+        ldg_tokens16(tokens + ws, t, (ws & 7) == 0);
+        uint32_t any = 0, c[16];
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) {
+          any |= t[k];
+          c[k] = cmap[t[k] & 0xffu];
+        }
+        // digest and DFA are independent chains in one basic block
+        uint32_t row = start_row, alo = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) {
+          dg = fnv_tok(dg, t[k]);
+          row = lds16(tab, row + c[k]);
+          if (k < 4) {
+            alo |= row;
+          } else {
+            amid |= row;
+          }
+          if (k == 3) Z = row;
+        }
+        X = SW = row;
+        A = alo | amid;
+        cw0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+        if (any >> 8) {  // a token >= 256: full update_u32 per token
+          dg = a.digest_init;
+#pragma unroll 1
+          for (uint32_t k = 0; k < 16; ++k) dg = fnv_u32(dg, tokens[ws + k]);
+        }
+      } else {  // generic shape / alignment: token by token
+        uint32_t row = start_row;
+        for (uint32_t k = 0; k < B; ++k) {
+          const uint32_t tk = tokens[ws + k];
+          dg = fnv_u32(dg, tk);
+          const uint32_t ck = cmap[tk & 0xffu];
+          row = lds16(tab, row + ck);
+          if (k < kc) {
+            A |= row;
+          } else if (k < Wp) {
+            amid |= row;
+          } else {
+            A |= row;
+          }
+          if (k + 1 == kc) Z = row;
+          if (k + 1 == Wp) SW = row;
+          if (k < 4) cw0 |= ck << (8 * k);
+        }
+        if (kc == 0) Z = start_row;
+        if (Wp == 0) SW = start_row;
+        X = row;
+        A |= amid;
+      }
+      if (out) a.d_out[gb] = dg;
     }
-    __syncthreads();
-    pp = s_pp;
+    // ---- phase B: [ws+B, min(we, ws+B+W')), shared with window l+1 once the runs meet
+    const uint32_t nZ = __shfl_down_sync(kFull, Z | ((amid & kAccRegion) << 1), 1);
+    const uint32_t nSW = __shfl_down_sync(kFull, SW, 1);
+    const uint32_t nX = __shfl_down_sync(kFull, X, 1);
+    const uint32_t ncw = __shfl_down_sync(kFull, cw0, 1);
+    uint32_t Y = X, C = 0;
+    const uint64_t sb = ws + B, eb = min(we, ws + B + Wp);
+    if (act && lane <= nout && sb < eb) {  // window nout's run serves window nout-1's phase C
+      if (nbr && kc == kConv) {
+        uint32_t ac = 0;
+        const uint32_t V = step4(tab, X, ncw, ac);
+        if (V == (nZ & 0xffffu)) {
+          C = ac | (nZ >> 1);  // bit 16 (neighbour's rows over [kConv, W')) -> bit 15
+          Y = nSW;
+        } else {
+          Y = run_tokens(tab, cmap, tokens, sb + kConv, eb, V, C);
+          C |= ac;
+        }
+      } else {
+        Y = run_tokens(tab, cmap, tokens, sb, eb, X, C);
+      }
+    }
+    // ---- phase C: [ws+2B, we) (W > B); end-of-window transition; flags
+    const uint32_t Cf = C & kAccRegion;
+    const uint32_t nYC = __shfl_down_sync(kFull, Y | (Cf << 1), 1);
+    uint32_t f = 0;
+    const uint64_t sc = ws + 2 * B;
+    if (out) {
+      uint32_t fin = Y, C2 = 0;
+      if (W > B && sc < we) {
+        if (W == 2 * B && nbr && Y == nX) {
+          C2 = nYC >> 1;
+          fin = nYC & 0xffffu;
+        } else {
+          fin = run_tokens(tab, cmap, tokens, sc, we, Y, C2);
+        }
+      }
+      const uint32_t me = copy_mask(acc_tab, lds16(tab, fin + eos2), inv);  // end-of-window transition
+      a.mask_out[gb] = me;
+      if (me) atomicMin(&a.first_sens[p], b);
+      f = ((A & kAccRegion) ? 1u : 0u) | (Cf ? 2u : 0u) | ((C2 & kAccRegion) ? 4u : 0u);
+    }
+    // ---- exact rule masks of the flagged segments
+    if (__any_sync(kFull, f != 0)) {
+      __syncwarp();
+      for (uint32_t s = 0; s < 3; ++s) {
+        const uint32_t ms = __ballot_sync(kFull, (f >> s) & 1u);
+        if (!ms) continue;
+        const bool mine = (ms >> lane) & 1u;
+        uint64_t o, e;
+        uint32_t row;
+        if (s == 0) {
+          o = ws, e = ws + B, row = start_row;
+        } else if (s == 1) {
+          o = sb, e = eb, row = X;
+        } else {
+          o = sc, e = we, row = Y;
+        }
+        if (defer) {  // queue: slot = qn + rank among this round's tasks; run 32 at a time
+          const uint32_t n = __popc(ms);
+          if (qn + n > 32) {
+            flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
+            qn = 0;
+          }
+          if (mine) {
+            SegTask t;
+            t.tok = o;
+            t.meta = row | (static_cast<uint32_t>(e - o) << 16);
+            t.gb = gb, t.p = p, t.b = b, t.pad = 0;
+            q[qn + __popc(ms & ((1u << lane) - 1u))] = t;
+          }
+          qn += n;
+        } else if (mine) {  // in place (segments longer than 16 tokens)
+          uint32_t m = 0;
+          for (; o < e; ++o) {
+            row = lds16(tab, row + cmap[tokens[o] & 0xffu]);
+            m |= copy_mask(acc_tab, row, inv);
+          }
+          if (m) {
+            atomicOr(&a.mask_out[gb], m);
+            atomicMin(&a.first_sens[p], b);
+          }
+        }
+      }
+    }
+    // ---- next chunk
+    g += nout;
+    pp = pbase + d + __popc(__ballot_sync(kFull, lane > d && so <= g));  // last loaded prompt start <= g
+    if (pp == pbase + 31 && pbase + 32 <= N && so32 <= g) {  // past the loaded prompts
+      pp = pbase + 32;
+      while (pp < N && a.blk_off[pp + 1] <= g) ++pp;
+    }
   }
+  flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
 }
 
 // find_slot: used by set_tiers (point lookups)
@@ -384,8 +565,6 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
   }
   return kNone;
 }
-
-constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long long cmp_lo, unsigned long long cmp_hi,
                                        unsigned long long new_lo, unsigned long long new_hi,
@@ -1194,48 +1373,44 @@ void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, ui
 }
 
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
-  // first-fit of the staging buffers into the unused gap [norm_bytes, 32768) of the
-  // u16 DFA table, else after the table
+  // the accepting-copy masks go into the unused gap [norm_bytes, 32768) of the u16 DFA
+  // table when they fit; the tokens are read straight from HBM (no staging buffers)
+  (void)B;
+  (void)W;
   HSLayout L{};
-  L.stage = round16(kHSThreads * B + W + 16);
   uint32_t gap = round16(r.norm_bytes), tail = round16(r.fast_bytes);
-  auto place = [&](uint32_t bytes) {
-    bytes = round16(bytes);
-    if (gap + bytes <= kAccRegion) {
-      uint32_t o = gap;
-      gap += bytes;
-      return o;
-    }
-    uint32_t o = tail;
-    tail += bytes;
-    return o;
-  };
-  L.off_cls = place(L.stage);
-  L.off_raw = place(L.stage);
-  L.off_so = place(round16((kHSThreads + 1) * 4) + (kHSThreads + 1) * 8);  // so[] + so_tok[]
-  L.off_xch = place(3 * kHSThreads * 4);
-  L.off_list = place(r.n_copies * 2);  // accepting-copy -> rule mask (u16)
+  const uint32_t acc = round16(r.n_copies * 2 + 2);
+  if (gap + acc <= kAccRegion) {
+    L.off_list = gap;
+  } else {
+    L.off_list = tail;
+    tail += acc;
+  }
+  L.warps = kHSWarps;
   L.total = tail;
   return L;
 }
 
-int hash_scan_grid(int device, uint32_t smem) {
+int hash_scan_grid(int device, uint32_t smem, uint32_t threads) {
   if (cudaFuncSetAttribute(k_hash_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
       cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, kHSThreads, smem) != cudaSuccess) return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, static_cast<int>(threads), smem) !=
+      cudaSuccess)
+    return -1;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (per_sm < 1) per_sm = 1;
   return per_sm * sms;
 }
 
-void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, cudaStream_t s) {
+void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s) {
   // a.n_blocks is a host-side hint (0 = unknown); the kernel reads the count from blk_off[N]
-  const uint32_t g = a.n_blocks ? std::min<uint32_t>(grid, a.n_blocks) : static_cast<uint32_t>(grid);
+  const uint32_t wpc = threads / 32;
+  const uint32_t g = a.n_blocks ? std::min<uint32_t>(grid, (a.n_blocks + wpc - 1) / wpc) : static_cast<uint32_t>(grid);
   if (a.n_prompts == 0 || g == 0) return;
-  k_hash_scan<<<g, kHSThreads, smem, s>>>(a);
+  k_hash_scan<<<g, threads, smem, s>>>(a);
 }
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,

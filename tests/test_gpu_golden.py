@@ -94,6 +94,31 @@ def test_vs_c_oracle_ragged(gpu, B, W):
     orc.close()
 
 
+@pytest.mark.parametrize("W", [32, 16, 20])
+def test_vs_c_oracle_aligned_dense(gpu, W):
+    """Block-aligned prompts (the vectorised 16-token path of k_hash_scan) with dense PII:
+    many windows accept, so the deferred exact-mask queue overflows and flushes."""
+    B = 16
+    rng = np.random.default_rng(7000 + W)
+    trunks = make_trunks(rng, 10, pii_p=0.4)
+    orc = OracleEngine(OracleRules(), B=B, W=W)
+    with AdmissionEngine(cfg(block_tokens=B, window_tokens=W)) as eng:
+        for _ in range(3):
+            batch = make_batch(rng, trunks, 400, 4, pii_p=0.35, max_words=60, align=16)
+            got = eng.admit(*batch)
+            exp = orc.admit(*batch)
+            np.testing.assert_array_equal(got.block_d, exp["block_d"])
+            np.testing.assert_array_equal(got.block_h, exp["block_h"])
+            np.testing.assert_array_equal(eng.rules.to_rule_mask_array(got.rule_mask), exp["mask"])
+            np.testing.assert_array_equal(got.label, exp["label"])
+            np.testing.assert_array_equal(got.matched_blocks, exp["matched_blocks"])
+            eng.commit()
+            orc.commit()
+            eng.epoch_pass()
+            orc.epoch()
+    orc.close()
+
+
 def test_large_batch_properties(gpu):
     """Config-2 sized batch (65,536 x 2,048): size-independent properties -- every prompt
     matches exactly its 40-block pool prefix (pool pre-inserted, Public), labels are a

@@ -38,7 +38,8 @@ def make_trunks(rng, n_trunks, pii_p=0.15):
 
 
 def make_batch(rng, trunks, n_prompts, n_users, business_p=0.3, pii_p=0.08, wide_p=0.0, max_words=40,
-               user_base=1):
+               user_base=1, align=0):
+    """align > 0: every prompt length is cut down to a multiple of `align` tokens."""
     toks, offs, users, owners = [], [0], [], []
     for _ in range(n_prompts):
         r = rng.random()
@@ -51,6 +52,8 @@ def make_batch(rng, trunks, n_prompts, n_users, business_p=0.3, pii_p=0.08, wide
             cut = int(rng.integers(0, len(t) + 1)) if rng.random() < 0.3 else len(t)
             text = t[:cut] + _text(rng, int(rng.integers(0, max_words)), pii_p)
         arr = np.frombuffer(text, np.uint8).astype(np.uint32)
+        if align:
+            arr = arr[: len(arr) - len(arr) % align]
         if wide_p and len(arr) and rng.random() < wide_p:
             k = int(rng.integers(len(arr)))
             arr[k] = arr[k] | (int(rng.integers(1, 1 << 20)) << 8)
