@@ -44,3 +44,11 @@ clean:
 	rm -rf $(BUILD) $(LIB)
 
 .PHONY: all oracle sass clean
+
+# A/B variants of the CUDA library (tools/ab.sh): make variant V=name VFLAGS="-DFOO=1"
+variant: $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o
+	mkdir -p variants/$(V)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/kernels.cu -o variants/$(V)/kernels.o 2> variants/$(V)/ptxas.log || (cat variants/$(V)/ptxas.log; exit 1)
+	$(NVCC) $(ARCH) -shared -o variants/$(V)/libsafekv_b200.so variants/$(V)/kernels.o $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o -lcudart_static -lpthread -ldl -lrt
+
+.PHONY: variant

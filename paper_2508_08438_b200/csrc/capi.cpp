@@ -225,22 +225,25 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
     if (it.second) copies.emplace_back(target, acc);
     return it.first->second;
   };
+  // rows are placed at the top of the 32 KB region, [row_base, 32768), so that the
+  // SMEM-resident part [row_base, fast_bytes) is contiguous (no gap before the copies)
+  const uint32_t row_base = skv::kAccRegion - ((norm + 15) & ~15u);
   std::vector<uint16_t> entry(static_cast<size_t>(S) * (C + 1), 0);
   std::vector<uint32_t> full(static_cast<size_t>(S) * (C + 1), 0);
   for (uint32_t s = 0; s < S; ++s) {
     for (uint32_t k = 0; k <= C; ++k) {
       uint32_t acc = d.acc[s * (C + 1) + k];
       uint32_t t = k < C ? d.next[s * C + k] : 0;
-      uint32_t fast = k < C ? t * row : 0;
+      uint32_t fast = k < C ? row_base + t * row : 0;
       if (acc) fast = skv::kAccRegion + copy_index(k < C ? t : UINT32_MAX, acc) * row;
       entry[s * (C + 1) + k] = static_cast<uint16_t>(fast);
-      full[s * (C + 1) + k] = (acc << 16) | (k < C ? t * row : 0);
+      full[s * (C + 1) + k] = (acc << 16) | (k < C ? row_base + t * row : 0);
     }
   }
   const uint32_t fast_bytes = skv::kAccRegion + static_cast<uint32_t>(copies.size()) * row;
   if (fast_bytes > 65535) throw skv::CompileError("device DFA: too many accepting transitions");
   std::vector<uint8_t> fast(fast_bytes, 0);
-  std::memcpy(fast.data(), entry.data(), entry.size() * 2);
+  std::memcpy(fast.data() + row_base, entry.data(), entry.size() * 2);
   for (size_t j = 0; j < copies.size(); ++j)
     if (copies[j].first != UINT32_MAX)  // EOS pseudo rows carry no transitions
       std::memcpy(fast.data() + skv::kAccRegion + j * row, entry.data() + copies[j].first * (C + 1), row);
@@ -275,7 +278,8 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
   c->rules_dev.fast_bytes = fast_bytes;
   c->rules_dev.norm_bytes = norm;
   c->rules_dev.row_bytes = row;
-  c->rules_dev.start_row = d.start * row;
+  c->rules_dev.start_row = row_base + d.start * row;
+  c->rules_dev.row_base = row_base;
   c->rules_dev.eos2 = C * 2;
   c->rules_dev.n_enabled = static_cast<uint32_t>(d.rule_index.size());
   c->rules_host = r;

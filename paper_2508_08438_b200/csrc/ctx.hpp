@@ -49,13 +49,14 @@ static_assert(sizeof(Entry) == 64, "entry must be two 32-B sectors");
 
 // Device forms of the compiled rule DFA (built by capi.cpp upload_rules).
 //
-// fast  (u16, SMEM-resident in k_hash_scan): row of state s at byte offset s*row_bytes,
+// fast  (u16, SMEM-resident in k_hash_scan): row of state s at byte offset
+//        row_base + s*row_bytes (the rows end at 32768, so [row_base, fast_bytes) is one
+//        contiguous SMEM image),
 //        entry (s, c) at +2c = byte offset of the next row.  A transition that ACCEPTS
 //        some rule instead points at a copy of the target row placed at >= 32768
 //        (kAccRegion), so "this window matched something" is bit 15 of the OR of all
 //        visited offsets -- no per-step mask work.  Entries of the EOS column are 0 or a
-//        pseudo offset >= 32768.  [norm_bytes, 32768) is a gap the kernel reuses as
-//        staging space.
+//        pseudo offset >= 32768.
 // full  (u32, global, read through L1): entry (s, c) at index s*(C+1)+c =
 //        (enabled-rule mask << 16) | canonical next-row byte offset (fast format, < 32768).
 //        Used to compute the exact rule mask of the (rare) windows the fast pass flags,
@@ -68,6 +69,7 @@ struct DevRules {
   uint8_t* class2 = nullptr;  // [256] byte -> 2 * class
   uint32_t fast_bytes = 0;    // kAccRegion + accepting-copy rows
   uint32_t norm_bytes = 0;    // n_states * row_bytes (< kAccRegion)
+  uint32_t row_base = 0;      // offset of state 0's row: rows fill [row_base, kAccRegion)
   uint32_t row_bytes = 0;     // 2 * (n_classes + 1)
   uint32_t start_row = 0;     // start * row_bytes
   uint32_t eos2 = 0;          // 2 * n_classes

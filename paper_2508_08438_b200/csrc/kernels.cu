@@ -110,7 +110,10 @@ __global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uin
 // few windows that accepted is recomputed per flagged segment (own block / first /
 // second context block) from its known start state, one lane per segment.
 // ---------------------------------------------------------------------------------
-constexpr uint32_t kHSWarps = 16;  // warps per CTA (fewer when the staging buffers do not fit)
+#ifndef SKV_HS_WARPS
+#define SKV_HS_WARPS 16
+#endif
+constexpr uint32_t kHSWarps = SKV_HS_WARPS;  // warps per CTA
 constexpr uint32_t kConv = 4;  // context bytes stepped before comparing with the neighbour's run
 
 __device__ __forceinline__ uint32_t lds16(const uint8_t* base, uint32_t off) {
@@ -249,7 +252,7 @@ __device__ __forceinline__ void flush_tasks(const SegTask* q, uint32_t qn, uint3
 // DFA run over tokens[o, e) from row (global loads, L1/L2 hits: the warp has just read
 // these lines); OR of the visited rows into acc.  Used off the fast path only.
 __device__ __forceinline__ uint32_t run_tokens(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ cmap,
-                                               const uint32_t* __restrict__ tokens, uint64_t o, uint64_t e,
+                                               const uint32_t* __restrict__ tokens, uint32_t o, uint32_t e,
                                                uint32_t row, uint32_t& acc) {
   uint32_t m = 0;
   for (; o < e; ++o) {
@@ -291,20 +294,22 @@ __device__ __forceinline__ void ldg_tokens16(const uint32_t* p, uint32_t (&t)[16
   }
 }
 
-__global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
+#ifndef SKV_HS_MINB
+#define SKV_HS_MINB 2
+#endif
+__global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashScanArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  uint8_t* tab = sm;
+  // row offsets index the DFA image [row_base, fast_bytes), which sits at sm[0..)
+  const uint8_t* tab = sm - a.rules.row_base;
   uint16_t* acc_tab = reinterpret_cast<uint16_t*>(sm + a.off_list);
   __shared__ uint8_t cmap[256];
   __shared__ SegTask s_q[kHSWarps][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
-  {  // DFA rows [0, norm) and accepting copies [32768, fast_bytes) -> SMEM
-    const uint32_t n0 = (a.rules.norm_bytes + 15) / 16;
-    const uint32_t n1 = (a.rules.fast_bytes - kAccRegion + 15) / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(a.rules.fast);
-    uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (uint32_t i = tid; i < n0; i += blockDim.x) dst[i] = src[i];
-    for (uint32_t i = tid; i < n1; i += blockDim.x) dst[kAccRegion / 16 + i] = src[kAccRegion / 16 + i];
+  {  // DFA rows and accepting copies [row_base, fast_bytes) -> SMEM
+    const uint32_t n = (a.rules.fast_bytes - a.rules.row_base + 15) / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(a.rules.fast) + a.rules.row_base / 16;
+    uint4* dst = reinterpret_cast<uint4*>(sm);
+    for (uint32_t i = tid; i < n; i += blockDim.x) dst[i] = src[i];
     if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
     for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
   }
@@ -378,33 +383,45 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
         }
       }
     }
+    // token positions relative to T0 = the chunk's first window start (32-bit)
+    const uint64_t T0 = shfl64(st, d) + static_cast<uint64_t>(g - __shfl_sync(kFull, so, d)) * B;
+    const uint32_t* __restrict__ tk0 = tokens + T0;
+    const uint32_t rel = static_cast<uint32_t>(st - T0), rel32 = static_cast<uint32_t>(st32 - T0);
     const uint32_t i1 = min(i + 1, 31u);
-    const uint64_t t_i = shfl64(st, i), t_1 = shfl64(st, i1);
+    const uint32_t r_i = __shfl_sync(kFull, rel, i), r_1 = __shfl_sync(kFull, rel, i1);
     const uint32_t so_i = __shfl_sync(kFull, so, i);
-    const uint64_t t_i1 = i + 1 < 32 ? t_1 : st32;  // end of prompt pbase + i
+    const uint32_t r_i1 = i + 1 < 32 ? r_1 : rel32;  // end of prompt pbase + i
     const uint32_t b = gb - so_i, p = pbase + i;
-    const uint64_t ws = t_i + static_cast<uint64_t>(b) * B;
-    const uint64_t we = min(t_i1, ws + B + W);
+    const uint32_t ws = r_i + b * B;
+    const uint32_t we = min(r_i1, ws + B + W);
     const bool act = lane < nw, out = lane < nout;
     const bool nbr = lane + 1 < nw && !((bm >> (lane + 1)) & 1u);  // block b+1: same prompt, this chunk
     // ---- phase A: the block's tokens, digest, DFA over the block from the start state
     uint32_t A = 0, X = 0, Z = 0, SW = 0, amid = 0, cw0 = 0;
     if (act) {
       uint64_t dg = a.digest_init;
-      if (b16 && (ws & 3) == 0) {
+      const uint32_t al = static_cast<uint32_t>(T0) + ws;  // alignment of the absolute position
+      if (b16 && (al & 3) == 0) {
         uint32_t t[16];
-        ldg_tokens16(tokens + ws, t, (ws & 7) == 0);
-        uint32_t any = 0, c[16];
+        ldg_tokens16(tk0 + ws, t, (al & 7) == 0);
+        uint32_t any = 0;
 #pragma unroll
-        for (uint32_t k = 0; k < 16; ++k) {
-          any |= t[k];
-          c[k] = cmap[t[k] & 0xffu];
+        for (uint32_t k = 0; k < 16; ++k) any |= t[k];
+        if (any >> 8) {  // a token >= 256: full update_u32 digest, low bytes for the scan
+#pragma unroll 1
+          for (uint32_t k = 0; k < 16; ++k) dg = fnv_u32(dg, tk0[ws + k]);
+#pragma unroll
+          for (uint32_t k = 0; k < 16; ++k) t[k] &= 0xffu;
         }
+        uint32_t c[16];
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) c[k] = cmap[t[k]];
         // digest and DFA are independent chains in one basic block
+        uint64_t h = a.digest_init;
         uint32_t row = start_row, alo = 0;
 #pragma unroll
         for (uint32_t k = 0; k < 16; ++k) {
-          dg = fnv_tok(dg, t[k]);
+          h = fnv_tok(h, t[k]);
           row = lds16(tab, row + c[k]);
           if (k < 4) {
             alo |= row;
@@ -413,20 +430,16 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
           }
           if (k == 3) Z = row;
         }
+        if (!(any >> 8)) dg = h;
         X = SW = row;
         A = alo | amid;
         cw0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-        if (any >> 8) {  // a token >= 256: full update_u32 per token
-          dg = a.digest_init;
-#pragma unroll 1
-          for (uint32_t k = 0; k < 16; ++k) dg = fnv_u32(dg, tokens[ws + k]);
-        }
       } else {  // generic shape / alignment: token by token
         uint32_t row = start_row;
         for (uint32_t k = 0; k < B; ++k) {
-          const uint32_t tk = tokens[ws + k];
-          dg = fnv_u32(dg, tk);
-          const uint32_t ck = cmap[tk & 0xffu];
+          const uint32_t tv = tk0[ws + k];
+          dg = fnv_u32(dg, tv);
+          const uint32_t ck = cmap[tv & 0xffu];
           row = lds16(tab, row + ck);
           if (k < kc) {
             A |= row;
@@ -450,9 +463,9 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
     const uint32_t nZ = __shfl_down_sync(kFull, Z | ((amid & kAccRegion) << 1), 1);
     const uint32_t nSW = __shfl_down_sync(kFull, SW, 1);
     const uint32_t nX = __shfl_down_sync(kFull, X, 1);
-    const uint32_t ncw = __shfl_down_sync(kFull, cw0, 1);
+    const uint32_t ncw = __shfl_down_sync(kFull, cw0, 1);  // the next block's first classes
     uint32_t Y = X, C = 0;
-    const uint64_t sb = ws + B, eb = min(we, ws + B + Wp);
+    const uint32_t sb = ws + B, eb = min(we, ws + B + Wp);
     if (act && lane <= nout && sb < eb) {  // window nout's run serves window nout-1's phase C
       if (nbr && kc == kConv) {
         uint32_t ac = 0;
@@ -461,18 +474,18 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
           C = ac | (nZ >> 1);  // bit 16 (neighbour's rows over [kConv, W')) -> bit 15
           Y = nSW;
         } else {
-          Y = run_tokens(tab, cmap, tokens, sb + kConv, eb, V, C);
+          Y = run_tokens(tab, cmap, tk0, sb + kConv, eb, V, C);
           C |= ac;
         }
       } else {
-        Y = run_tokens(tab, cmap, tokens, sb, eb, X, C);
+        Y = run_tokens(tab, cmap, tk0, sb, eb, X, C);
       }
     }
     // ---- phase C: [ws+2B, we) (W > B); end-of-window transition; flags
     const uint32_t Cf = C & kAccRegion;
     const uint32_t nYC = __shfl_down_sync(kFull, Y | (Cf << 1), 1);
     uint32_t f = 0;
-    const uint64_t sc = ws + 2 * B;
+    const uint32_t sc = ws + 2 * B;
     if (out) {
       uint32_t fin = Y, C2 = 0;
       if (W > B && sc < we) {
@@ -480,7 +493,7 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
           C2 = nYC >> 1;
           fin = nYC & 0xffffu;
         } else {
-          fin = run_tokens(tab, cmap, tokens, sc, we, Y, C2);
+          fin = run_tokens(tab, cmap, tk0, sc, we, Y, C2);
         }
       }
       const uint32_t me = copy_mask(acc_tab, lds16(tab, fin + eos2), inv);  // end-of-window transition
@@ -495,8 +508,7 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
         const uint32_t ms = __ballot_sync(kFull, (f >> s) & 1u);
         if (!ms) continue;
         const bool mine = (ms >> lane) & 1u;
-        uint64_t o, e;
-        uint32_t row;
+        uint32_t o, e, row;
         if (s == 0) {
           o = ws, e = ws + B, row = start_row;
         } else if (s == 1) {
@@ -512,8 +524,8 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
           }
           if (mine) {
             SegTask t;
-            t.tok = o;
-            t.meta = row | (static_cast<uint32_t>(e - o) << 16);
+            t.tok = T0 + o;
+            t.meta = row | ((e - o) << 16);
             t.gb = gb, t.p = p, t.b = b, t.pad = 0;
             q[qn + __popc(ms & ((1u << lane) - 1u))] = t;
           }
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(kHSWarps * 32) k_hash_scan(HashScanArgs a) {
         } else if (mine) {  // in place (segments longer than 16 tokens)
           uint32_t m = 0;
           for (; o < e; ++o) {
-            row = lds16(tab, row + cmap[tokens[o] & 0xffu]);
+            row = lds16(tab, row + cmap[tk0[o] & 0xffu]);
             m |= copy_mask(acc_tab, row, inv);
           }
           if (m) {
@@ -1334,11 +1346,11 @@ __global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint3
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t row = r.start_row, acc = 0;
   for (uint32_t i = 0; i < len; ++i) {
-    const uint32_t e = r.full[(row + r.class2[text[i]]) >> 1];
+    const uint32_t e = r.full[(row - r.row_base + r.class2[text[i]]) >> 1];
     acc |= e;
     row = e & 0xffffu;
   }
-  acc |= r.full[(row + r.eos2) >> 1];
+  acc |= r.full[(row - r.row_base + r.eos2) >> 1];
   *mask = acc >> 16;
 }
 
@@ -1373,21 +1385,14 @@ void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, ui
 }
 
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
-  // the accepting-copy masks go into the unused gap [norm_bytes, 32768) of the u16 DFA
-  // table when they fit; the tokens are read straight from HBM (no staging buffers)
+  // dynamic SMEM = the DFA image [row_base, fast_bytes) + the accepting-copy masks; the
+  // tokens are read straight from HBM (no staging buffers)
   (void)B;
   (void)W;
   HSLayout L{};
-  uint32_t gap = round16(r.norm_bytes), tail = round16(r.fast_bytes);
-  const uint32_t acc = round16(r.n_copies * 2 + 2);
-  if (gap + acc <= kAccRegion) {
-    L.off_list = gap;
-  } else {
-    L.off_list = tail;
-    tail += acc;
-  }
+  L.off_list = round16(r.fast_bytes - r.row_base);
   L.warps = kHSWarps;
-  L.total = tail;
+  L.total = L.off_list + round16(r.n_copies * 2 + 2);
   return L;
 }
 
