@@ -1054,7 +1054,10 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 //     rewrites the payload from the winning prompt.
 // Claim values are >= 2^31 and never collide with the epoch candidate stamps (< 2^31)
 // kept in the same word.
-constexpr int kCommitRounds = 4;
+#ifndef SKV_COMMIT_ROUNDS
+#define SKV_COMMIT_ROUNDS 2
+#endif
+constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 
 __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
                                                 const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
@@ -1092,31 +1095,19 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
         lab[r] = label[bo + b];
       }
     }
-    // claims.  1) plain loads of both keys of every round's home line, all in flight
-    // together (one DRAM round trip); 2) CAS on the first of the two that is empty or
-    // already holds the key -- the line is in L2 now; 3) rare: the line is full or the
-    // CAS lost a race to another key -> linear probing with CAS, every pending round's
-    // next CAS again in flight together.
+    // claims: a 128-bit CAS straight on every round's home slot, all rounds in flight
+    // together (one DRAM round trip; the CAS returns the resident key, so no separate
+    // load is needed); rare: the slot holds another key or the CAS lost a race -> linear
+    // probing with CAS, every pending round's next CAS again in flight together.
     uint64_t sl[R];
-    ulonglong2 k0v[R], k1v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      sl[r] = 0;
-      if (base + 32 * r + lane < n) {
-        sl[r] = home_slot(ix, h[r], d[r]);
-        k0v[r] = ld_relaxed128(reinterpret_cast<const ulonglong2*>(&ix.e[sl[r]].rec));
-        k1v[r] = ld_relaxed128(reinterpret_cast<const ulonglong2*>(&ix.e[sl[r] + 1].rec));
-      }
-    }
     unsigned long long ol[R], oh[R];
     bool pend[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+      sl[r] = 0;
       pend[r] = false;
       if (base + 32 * r + lane >= n) continue;
-      const bool f0 = (k0v[r].x == 0 && k0v[r].y == 0) || (k0v[r].x == h[r] && k0v[r].y == d[r]);
-      const bool f1 = (k1v[r].x == 0 && k1v[r].y == 0) || (k1v[r].x == h[r] && k1v[r].y == d[r]);
-      if (!f0) sl[r] = f1 ? sl[r] + 1 : (sl[r] + 2) & ix.mask;
+      sl[r] = home_slot(ix, h[r], d[r]);
       mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
                        &oh[r]);
     }
