@@ -174,7 +174,8 @@ typedef struct {
 /* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d). */
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
 
-/* Tier tags of existing entries (demote, cache_index.hpp:362-381). */
+/* Tier tags of existing entries (demote, cache_index.hpp:362-381): an entry's tier only
+ * moves down HBM -> DRAM -> SSD, so it becomes max(current, tag). */
 int skv_set_tiers(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, size_t n);
 
 typedef struct {
@@ -195,6 +196,29 @@ typedef struct {
   uint32_t prefetched;        /* 1: the last admit consumed stages 1-2 staged by skv_prefetch */
 } skv_stage_times;
 int skv_last_times(skv_ctx* ctx, skv_stage_times* out);
+
+/* ------------------------------------------------------------------------------
+ * Serving observables of the last skv_admit.  The probe records, per
+ * matched block, its tier and whether the requesting user created it; this epilogue turns
+ * them into the reference's per-request TTFT and reuse attribution.
+ * ------------------------------------------------------------------------------ */
+/* CostModel (serving_sim.hpp:25-57) */
+typedef struct {
+  double t_base_ms, c_prefill_ms;
+  double tier_penalty_ms[3]; /* HBM, DRAM, SSD */
+  double noise_sigma_ms;
+  uint64_t seed;
+} skv_cost_model;
+void skv_cost_model_default(skv_cost_model* m);
+/* CostModel::validate (serving_sim.hpp:35-42) -> SKV_ERR_CONFIG on a bad model. */
+int skv_set_cost_model(skv_ctx* ctx, const skv_cost_model* m);
+/* Per prompt of the last admitted batch: ttft_ms = CostModel::ttft(L_p, match,
+ * request_id) (serving_sim.hpp:50-56), one KV handle of B tokens per matched block;
+ * intra/inter_tokens = ServingSimulator::attribute_reuse (serving_sim.hpp:313-324).
+ * request_ids may be NULL (= running admission index of the prompt).  Any output may be
+ * NULL; on_device applies to request_ids and the outputs.  Valid until the next admit. */
+int skv_admit_ttft(skv_ctx* ctx, const uint64_t* request_ids, double* ttft_ms, uint32_t* intra_tokens,
+                   uint32_t* inter_tokens, int on_device);
 
 /* Per-call wrappers (batch of one, still on the device) for the facade:
  * RuleEngine::tier1_scan (detection.hpp:217) and token_seq_digest (core.hpp:68). */

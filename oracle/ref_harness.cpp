@@ -22,6 +22,7 @@
 #include <safekv/core.hpp>
 #include <safekv/detection.hpp>
 #include <safekv/monitor.hpp>
+#include <safekv/serving_sim.hpp>
 #include <safekv/util.hpp>
 #include <safekv/workload.hpp>
 
@@ -234,6 +235,14 @@ struct RefEngine {
     std::vector<uint8_t> labels;  // 0 Private, 1 Public (SensitivityLabel values)
   };
   std::vector<Pending> pending;
+  // the last admit's matches, re-expressed in tokens (one KvHandle of B tokens per
+  // matched block) for CostModel::ttft and attribute_reuse
+  struct Served {
+    uint64_t input_tokens = 0;
+    UserId user;
+    MatchResult m;
+  };
+  std::vector<Served> served;
   int nthreads = 1;
 };
 
@@ -274,6 +283,7 @@ int ref_engine_admit(void* ev, const uint32_t* tok, const uint64_t* off, const u
   ref_scan_windows(e->rules_box, tok, off, n_prompts, B, e->W, mask.data(), e->nthreads);
   ref_block_keys(tok, off, n_prompts, B, out_h, out_d);
   e->pending.clear();
+  e->served.assign(n_prompts, {});
   for (uint32_t p = 0; p < n_prompts; ++p) {
     uint64_t n = boff[p + 1] - boff[p];
     RefEngine::Pending pd;
@@ -311,11 +321,49 @@ int ref_engine_admit(void* ev, const uint32_t* tok, const uint64_t* off, const u
         out_decision[boff[p] + b] = nd->label == SensitivityLabel::Public ? 1 : 2;
         e->mon->record_access(nd, pd.user);
       }
+      RefEngine::Served& sv = e->served[p];
+      sv.m = mr;
+      sv.m.matched_tokens = mr.matched_tokens * B;
+      for (KvHandle& h : sv.m.handles) h.token_count = B;
     }
+    e->served[p].input_tokens = off[p + 1] - off[p];
+    e->served[p].user = pd.user;
     for (uint64_t b = m; b < n; ++b) out_decision[boff[p] + b] = 0;
     out_matched[p] = m;
     out_tier[p] = tier;
     e->pending.push_back(std::move(pd));
+  }
+  return 0;
+}
+
+// Serving observables of the last admit: CostModel::ttft (serving_sim.hpp:50-56) on the
+// token-scaled match, and ServingSimulator::attribute_reuse (serving_sim.hpp:313-324,
+// private there, restated here line for line with node span = B tokens).
+int ref_engine_ttft(void* ev, const uint64_t* request_ids, double t_base, double c_prefill, double pen_dram,
+                    double pen_ssd, double sigma, uint64_t seed, double* out_ttft, uint32_t* out_intra,
+                    uint32_t* out_inter) {
+  auto* e = static_cast<RefEngine*>(ev);
+  CostModel cm;
+  cm.t_base_ms = t_base;
+  cm.c_prefill_ms = c_prefill;
+  cm.tier_penalty_ms = {0.0, pen_dram, pen_ssd};
+  cm.noise_sigma_ms = sigma;
+  cm.seed = seed;
+  for (size_t p = 0; p < e->served.size(); ++p) {
+    const auto& sv = e->served[p];
+    out_ttft[p] = cm.ttft(sv.input_tokens, sv.m, request_ids ? request_ids[p] : p);
+    uint64_t counted = 0, intra = 0, inter = 0;
+    for (size_t i = 0; i < sv.m.path.size(); ++i) {
+      NodeRef n = sv.m.path[i];
+      uint64_t covered = std::min<uint64_t>(static_cast<uint64_t>(n->span()) * e->B, sv.m.matched_tokens - counted);
+      counted += covered;
+      if (n->creator == sv.user)
+        intra += covered;
+      else
+        inter += covered;
+    }
+    out_intra[p] = static_cast<uint32_t>(intra);
+    out_inter[p] = static_cast<uint32_t>(inter);
   }
   return 0;
 }

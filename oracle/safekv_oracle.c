@@ -11,6 +11,7 @@
  */
 #include "safekv_oracle.h"
 
+#include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -713,6 +714,11 @@ typedef struct {
   uint32_t n;
   uint64_t user;
   uint8_t owner;
+  /* serving observables of the lookup (CostModel::ttft / attribute_reuse inputs) */
+  uint64_t L;
+  uint32_t m;
+  uint8_t* mtier; /* tier of matched block b */
+  uint8_t* mown;  /* creator == user for matched block b */
 } Pend;
 
 typedef struct {
@@ -796,6 +802,8 @@ static void clear_pending(Eng* g) {
     free(g->pend[i].h);
     free(g->pend[i].d);
     free(g->pend[i].label);
+    free(g->pend[i].mtier);
+    free(g->pend[i].mown);
   }
   free(g->pend);
   g->pend = NULL;
@@ -840,6 +848,9 @@ int orc_engine_admit(void* p, const uint32_t* tok, const uint64_t* off, const ui
     pd->h = (uint64_t*)malloc((n ? n : 1) * 8);
     pd->d = (uint64_t*)malloc((n ? n : 1) * 8);
     pd->label = (uint8_t*)malloc(n ? n : 1);
+    pd->mtier = (uint8_t*)malloc(n ? n : 1);
+    pd->mown = (uint8_t*)malloc(n ? n : 1);
+    pd->L = L;
     uint64_t h = 0;
     int sens = 0;
     for (uint64_t b = 0; b < n; ++b) {
@@ -866,15 +877,61 @@ int orc_engine_admit(void* p, const uint32_t* tok, const uint64_t* off, const ui
       if (!(en->label == L_PUBLIC || en->creator == pd->user)) break;
       out_decision[k + b] = en->label == L_PUBLIC ? 1 : 2;
       if (en->tier > tier) tier = en->tier;
+      pd->mtier[b] = en->tier;
+      pd->mown[b] = en->creator == pd->user;
       record(en, pd->user); /* A.6 record, prompt order */
       mt++;
     }
     for (uint64_t b = mt; b < n; ++b) out_decision[k + b] = 0;
+    pd->m = mt;
     out_matched[q] = mt;
     out_tier[q] = tier;
     k += n;
   }
   free(win);
+  return 0;
+}
+
+/* Serving observables of the last admit.  CostModel::ttft (serving_sim.hpp:50-56):
+ * t = t_base + c_prefill * (L - m*B), then + penalty[tier] * B per matched block in path
+ * order, + sigma * Box-Muller normal of SplitMix64(derive_seed(seed, request_id))
+ * (util.hpp:14-55), floored at t_base.  attribute_reuse (serving_sim.hpp:313-324):
+ * matched tokens on entries the user created (intra) or others created (inter). */
+static uint64_t sm64(uint64_t* st) {
+  uint64_t z = (*st += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+int orc_engine_ttft(void* p, const uint64_t* request_ids, double t_base, double c_prefill, double pen_dram,
+                    double pen_ssd, double sigma, uint64_t seed, double* out_ttft, uint32_t* out_intra,
+                    uint32_t* out_inter) {
+  Eng* g = (Eng*)p;
+  const double pen[3] = {0.0, pen_dram, pen_ssd};
+  for (uint32_t q = 0; q < g->npend; ++q) {
+    const Pend* pd = &g->pend[q];
+    double t = t_base + c_prefill * (double)(pd->L - (uint64_t)pd->m * g->B);
+    uint32_t own = 0;
+    for (uint32_t b = 0; b < pd->m; ++b) {
+      t += pen[pd->mtier[b]] * (double)g->B;
+      own += pd->mown[b];
+    }
+    double noise = 0.0;
+    if (sigma != 0.0) {
+      const uint64_t rid = request_ids ? request_ids[q] : q;
+      uint64_t st = seed ^ (0x51a1c9e3b7d24f85ULL * (rid + 1));
+      uint64_t st2 = sm64(&st);
+      double u1 = (double)(sm64(&st2) >> 11) * 0x1.0p-53;
+      const double u2 = (double)(sm64(&st2) >> 11) * 0x1.0p-53;
+      if (u1 <= 0.0) u1 = 0x1.0p-53;
+      noise = sigma * (sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+    }
+    t += noise;
+    out_ttft[q] = t < t_base ? t_base : t;
+    out_intra[q] = own * g->B;
+    out_inter[q] = (pd->m - own) * g->B;
+  }
   return 0;
 }
 
@@ -916,7 +973,7 @@ int orc_engine_set_tiers(void* p, const uint32_t* tok, const uint64_t* off, uint
       h = orc_chain(h, d);
       long x = find(g, h, d);
       if (x < 0) return -1;
-      g->e[x].tier = tiers[k];
+      if (tiers[k] > g->e[x].tier) g->e[x].tier = tiers[k]; /* demote: tiers only move down */
     }
   }
   return 0;

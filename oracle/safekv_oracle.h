@@ -30,6 +30,9 @@ int orc_engine_admit(void* e, const uint32_t* tok, const uint64_t* off, const ui
                      uint64_t* out_mask, uint8_t* out_label, uint8_t* out_decision, uint32_t* out_matched,
                      uint8_t* out_tier);
 int orc_engine_commit(void* e);
+int orc_engine_ttft(void* e, const uint64_t* request_ids, double t_base, double c_prefill, double pen_dram,
+                    double pen_ssd, double sigma, uint64_t seed, double* out_ttft, uint32_t* out_intra,
+                    uint32_t* out_inter);
 int orc_engine_set_tiers(void* e, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts,
                          const uint8_t* tiers);
 int orc_engine_epoch(void* e, uint64_t* out_epoch, size_t cap, uint64_t* ev_h, uint64_t* ev_d, uint8_t* ev_action,

@@ -128,6 +128,16 @@ struct skv_ctx {
   uint8_t* blabel = nullptr;
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
+  uint8_t* bmeta = nullptr;    // per matched block: tier | creator == user << 2 (TTFT epilogue)
+  uint32_t* plen = nullptr;    // tokens per prompt of the last admitted batch
+  uint32_t* alt_plen = nullptr;
+  double* d_ttft = nullptr;    // skv_admit_ttft scratch
+  uint32_t* d_intra = nullptr;
+  uint32_t* d_inter = nullptr;
+  uint64_t* d_reqid = nullptr;
+  skv::CostModelDev cost{};
+  uint64_t admitted_prompts = 0;  // request ids of the last batch default to [admitted_prompts - N, ...)
+  uint32_t last_n = 0;            // prompts of the last skv_admit
   unsigned long long *keys_a = nullptr, *keys_b = nullptr;  // ordered-replay access keys
   uint32_t* fix_list = nullptr;  // commit: duplicate-key slots + depths (2 x max_blocks)
   void* temp = nullptr;
@@ -515,6 +525,13 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->blabel = dalloc<uint8_t>(NB, c->owned);
     c->bdecision = dalloc<uint8_t>(NB, c->owned);
     c->bslot = dalloc<uint32_t>(NB, c->owned);
+    c->bmeta = dalloc<uint8_t>(NB, c->owned);
+    c->plen = dalloc<uint32_t>(N, c->owned);
+    c->alt_plen = dalloc<uint32_t>(N, c->owned);
+    c->d_ttft = dalloc<double>(N, c->owned);
+    c->d_intra = dalloc<uint32_t>(N, c->owned);
+    c->d_inter = dalloc<uint32_t>(N, c->owned);
+    c->d_reqid = dalloc<uint64_t>(N, c->owned);
     c->keys_a = dalloc<unsigned long long>(NB, c->owned);
     c->keys_b = dalloc<unsigned long long>(NB, c->owned);
     c->fix_list = dalloc<uint32_t>(2 * NB, c->owned);
@@ -596,6 +613,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       c->pending = true;
       c->p_n = 0;
       c->p_blocks = 0;
+      c->last_n = 0;
       return SKV_OK;
     }
     if (!b->tokens || !b->offsets || !b->users) throw ArgError("null batch pointer");
@@ -642,12 +660,13 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     if (use_pf) {
       CK(cudaStreamWaitEvent(s, c->pf_done, 0));
       std::swap(c->counts, c->alt_counts);
+      std::swap(c->plen, c->alt_plen);
       std::swap(c->blk_off, c->alt_blk_off);
       std::swap(c->first_sens, c->alt_first_sens);
       std::swap(c->bd, c->alt_bd);
       std::swap(c->bmask, c->alt_bmask);
     } else {
-      skv::launch_block_counts(off, N, B, c->counts, s);
+      skv::launch_block_counts(off, N, B, c->counts, c->plen, s);
       skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
     }
     if (b->on_device) {
@@ -668,7 +687,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::MonCtx mon = monitor_ctx(c);
     CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, users, N, c->bh, c->blabel, c->bdecision,
-                            c->bslot, c->matched, c->exist, c->tier, mon, s);
+                            c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, s);
     CK(cudaEventRecord(c->ev[3], s));
     // stage 4: monitor record -- hits and set inserts were recorded inside the probe;
     // apply distinct counts, then replay (in prompt order) the rare entries whose
@@ -725,6 +744,64 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->p_blocks = n_blocks;
     c->p_users = users;
     c->p_owners = owners;
+    c->last_n = N;
+    c->admitted_prompts += N;
+    return SKV_OK;
+  });
+}
+
+// ------------------------------------------------------------------ serving observables
+void skv_cost_model_default(skv_cost_model* m) {
+  if (!m) return;
+  *m = skv_cost_model{};
+  m->t_base_ms = 10.0;  // CostModel defaults (serving_sim.hpp:29-33)
+  m->c_prefill_ms = 1.0;
+  m->tier_penalty_ms[0] = 0.0;
+  m->tier_penalty_ms[1] = 0.2;
+  m->tier_penalty_ms[2] = 0.5;
+  m->noise_sigma_ms = 0.0;
+  m->seed = 0;
+}
+
+int skv_set_cost_model(skv_ctx* c, const skv_cost_model* m) {
+  if (!c || !m) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    // CostModel::validate (serving_sim.hpp:35-42)
+    if (m->tier_penalty_ms[1] < 0 || m->tier_penalty_ms[2] < m->tier_penalty_ms[1])
+      throw skv::ConfigError("cost: tier penalties must satisfy 0 <= DRAM <= SSD");
+    if (m->c_prefill_ms <= m->tier_penalty_ms[2])
+      throw skv::ConfigError("cost: c_prefill must exceed the SSD reload penalty");
+    if (m->noise_sigma_ms < 0) throw skv::ConfigError("cost: noise_sigma must be non-negative");
+    c->cost.t_base = m->t_base_ms;
+    c->cost.c_prefill = m->c_prefill_ms;
+    for (int t = 0; t < 3; ++t) c->cost.penalty[t] = m->tier_penalty_ms[t];
+    c->cost.sigma = m->noise_sigma_ms;
+    c->cost.seed = m->seed;
+    return SKV_OK;
+  });
+}
+
+int skv_admit_ttft(skv_ctx* c, const uint64_t* request_ids, double* ttft_ms, uint32_t* intra_tokens,
+                   uint32_t* inter_tokens, int on_device) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    const uint32_t N = c->last_n;
+    if (N == 0) return SKV_OK;
+    cudaStream_t s = c->stream;
+    const cudaMemcpyKind in = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind outk = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const uint64_t* rid = nullptr;
+    if (request_ids) {
+      CK(cudaMemcpyAsync(c->d_reqid, request_ids, N * 8ull, in, s));
+      rid = c->d_reqid;
+    }
+    skv::launch_ttft(c->blk_off, c->matched, c->plen, c->bmeta, rid, c->admitted_prompts - N, N,
+                     c->cfg.block_tokens, c->cost, c->d_ttft, c->d_intra, c->d_inter, s);
+    if (ttft_ms) CK(cudaMemcpyAsync(ttft_ms, c->d_ttft, N * 8ull, outk, s));
+    if (intra_tokens) CK(cudaMemcpyAsync(intra_tokens, c->d_intra, N * 4ull, outk, s));
+    if (inter_tokens) CK(cudaMemcpyAsync(inter_tokens, c->d_inter, N * 4ull, outk, s));
+    sync_check(s);
     return SKV_OK;
   });
 }
@@ -767,7 +844,7 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
       return SKV_OK;
     }
     CK(cudaEventRecord(c->pf_ev[0], st));
-    skv::launch_block_counts(off, N, c->cfg.block_tokens, c->alt_counts, st);
+    skv::launch_block_counts(off, N, c->cfg.block_tokens, c->alt_counts, c->alt_plen, st);
     skv::launch_exclusive_scan(c->side_temp, c->side_temp_bytes, c->alt_counts, c->alt_blk_off, N + 1, st);
     CK(cudaMemsetAsync(c->alt_first_sens, 0xff, N * 4ull, st));
     stage12(c, st, tokens, off, N, b->n_tokens, nb_hint, c->alt_blk_off, c->alt_first_sens, c->alt_bd,

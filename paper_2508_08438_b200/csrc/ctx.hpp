@@ -134,10 +134,22 @@ struct MonCtx {
   uint32_t* matched_total;
 };
 
+// CostModel (serving_sim.hpp:25-57) in device form
+struct CostModelDev {
+  double t_base = 10.0, c_prefill = 1.0;
+  double penalty[4] = {0.0, 0.2, 0.5, 0.0};  // HBM, DRAM, SSD (index 3 unused)
+  double sigma = 0.0;
+  uint64_t seed = 0;
+};
+
 void launch_init_entries(const Index& ix, cudaStream_t s);
+void launch_ttft(const uint32_t* blk_off, const uint32_t* matched, const uint32_t* plen, const uint8_t* bmeta,
+                 const uint64_t* request_ids, uint64_t request_base, uint32_t n, uint32_t B, const CostModelDev& cm,
+                 double* ttft, uint32_t* intra, uint32_t* inter, cudaStream_t s);
 
 // kernel launchers (kernels.cu)
-void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, cudaStream_t s);
+void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, uint32_t* plen,
+                         cudaStream_t s);
 size_t scan_temp_bytes(uint32_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint32_t n,
                            cudaStream_t s);
@@ -146,8 +158,8 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
-                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
-                        cudaStream_t s);
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
+                        const MonCtx& mon, cudaStream_t s);
 void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
                    const uint32_t* matched, const uint64_t* users, uint32_t n_prompts, cudaStream_t s);
 void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,

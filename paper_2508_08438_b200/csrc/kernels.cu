@@ -73,10 +73,62 @@ __device__ __forceinline__ uint4 ldg_stream(const uint32_t* p) {
 // ---------------------------------------------------------------------------------
 // K0: blocks per prompt
 // ---------------------------------------------------------------------------------
-__global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uint32_t B, uint32_t* counts) {
+__global__ void k_block_counts(const uint64_t* __restrict__ off, uint32_t n, uint32_t B, uint32_t* counts,
+                               uint32_t* plen) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) counts[p] = static_cast<uint32_t>((off[p + 1] - off[p]) / B);
+  if (p < n) {
+    const uint64_t L = off[p + 1] - off[p];
+    counts[p] = static_cast<uint32_t>(L / B);
+    plen[p] = static_cast<uint32_t>(min(L, static_cast<uint64_t>(0xffffffffu)));
+  }
   if (p == n) counts[p] = 0;
+}
+
+// ---------------------------------------------------------------------------------
+// Serving observables of an admitted batch (probe epilogue): per prompt
+//   ttft = max(t_base + c_prefill * (L - m*B) + sum_{b<m} penalty[tier_b] * B + noise, t_base)
+// in the reference's summation order (CostModel::ttft, serving_sim.hpp:50-56; one
+// handle per matched block), noise = sigma * Box-Muller normal of
+// SplitMix64(derive_seed(seed, request_id)) (util.hpp:14-55), and the reuse attribution
+// of ServingSimulator::attribute_reuse (serving_sim.hpp:313-324): matched tokens on
+// entries the user created (intra) vs created by others (inter).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {
+  uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_ttft(const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ matched,
+                       const uint32_t* __restrict__ plen, const uint8_t* __restrict__ bmeta,
+                       const uint64_t* __restrict__ request_ids, uint64_t request_base, uint32_t n, uint32_t B,
+                       CostModelDev cm, double* __restrict__ ttft, uint32_t* __restrict__ intra,
+                       uint32_t* __restrict__ inter) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t m = matched[p], bo = blk_off[p];
+  double t = cm.t_base + cm.c_prefill * static_cast<double>(static_cast<uint64_t>(plen[p]) - static_cast<uint64_t>(m) * B);
+  uint32_t own = 0;
+  for (uint32_t b = 0; b < m; ++b) {
+    const uint32_t x = bmeta[bo + b];
+    t += cm.penalty[x & 3u] * static_cast<double>(B);
+    own += x >> 2;
+  }
+  double noise = 0.0;
+  if (cm.sigma != 0.0) {
+    const uint64_t rid = request_ids ? request_ids[p] : request_base + p;
+    uint64_t st = cm.seed ^ (0x51a1c9e3b7d24f85ULL * (rid + 1));
+    uint64_t st2 = splitmix_next(st);  // derive_seed(seed, request_id)
+    const double u1r = static_cast<double>(splitmix_next(st2) >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(splitmix_next(st2) >> 11) * 0x1.0p-53;
+    const double u1 = u1r <= 0.0 ? 0x1.0p-53 : u1r;
+    noise = cm.sigma * (sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+  }
+  t += noise;
+  ttft[p] = t > cm.t_base ? t : cm.t_base;
+  intra[p] = own * B;
+  inter[p] = (m - own) * B;
 }
 
 // ---------------------------------------------------------------------------------
@@ -921,7 +973,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     const uint32_t* __restrict__ first_sens, const uint64_t* __restrict__ users, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
-    uint8_t* __restrict__ tier, MonCtx mon) {
+    uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon) {
   __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
   __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -1014,6 +1066,8 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
           if (b < new_m) {
             decision[bj + b] = lab == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
             tm = (pr.meta >> 16) & 0xffu;
+            // TTFT epilogue inputs: the matched block's tier and whether the user created it
+            bmeta[bj + b] = static_cast<uint8_t>(tm | ((pr.creator == uj) ? 4u : 0u));
           }
           if (b < new_k) slot_out[bj + b] = pr.slot;
         }
@@ -1310,7 +1364,19 @@ __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, cons
   if (i >= n) return;
   Rec r;
   uint32_t s = find_slot(ix, h[i], d[i], &r);
-  if (s != kNone) ix.e[s].rec.tier = tiers[i];
+  if (s == kNone) return;
+  // demote (cache_index.hpp:362-381): a tier only moves down HBM -> DRAM -> SSD, so
+  // repeated tags of one entry keep the slowest (the reference's demote-until loop)
+  uint32_t* meta = reinterpret_cast<uint32_t*>(&ix.e[s].rec.label);
+  uint32_t old = *meta;
+  for (;;) {
+    const uint32_t t = max((old >> 16) & 0xffu, static_cast<uint32_t>(tiers[i]));
+    const uint32_t nv = (old & ~0x00ff0000u) | (t << 16);
+    if (nv == old) break;
+    const uint32_t got = atomicCAS(meta, old, nv);
+    if (got == old) break;
+    old = got;
+  }
 }
 
 __global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
@@ -1359,8 +1425,17 @@ inline uint32_t cdiv(uint64_t a, uint64_t b) { return static_cast<uint32_t>((a +
 // =================================================================================
 // launchers
 // =================================================================================
-void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, cudaStream_t s) {
-  k_block_counts<<<cdiv(n + 1, 256), 256, 0, s>>>(tok_off, n, B, counts);
+void launch_block_counts(const uint64_t* tok_off, uint32_t n, uint32_t B, uint32_t* counts, uint32_t* plen,
+                         cudaStream_t s) {
+  k_block_counts<<<cdiv(n + 1, 256), 256, 0, s>>>(tok_off, n, B, counts, plen);
+}
+
+void launch_ttft(const uint32_t* blk_off, const uint32_t* matched, const uint32_t* plen, const uint8_t* bmeta,
+                 const uint64_t* request_ids, uint64_t request_base, uint32_t n, uint32_t B, const CostModelDev& cm,
+                 double* ttft, uint32_t* intra, uint32_t* inter, cudaStream_t s) {
+  if (n)
+    k_ttft<<<cdiv(n, 256), 256, 0, s>>>(blk_off, matched, plen, bmeta, request_ids, request_base, n, B, cm, ttft,
+                                        intra, inter);
 }
 
 size_t scan_temp_bytes(uint32_t n) {
@@ -1411,11 +1486,11 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint64_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
-                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, const MonCtx& mon,
-                        cudaStream_t s) {
+                        uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
+                        const MonCtx& mon, cudaStream_t s) {
   if (n)
     k_chain_probe<<<cdiv(n, kCPPrompts * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
-                                                                   decision, slot, matched, exist, tier, mon);
+                                                                   decision, slot, matched, exist, tier, bmeta, mon);
 }
 
 uint32_t record_grid(int device) {
@@ -1466,7 +1541,19 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s) {
   if (!n) return;
-  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, exist, label, users, owners, n,
+#ifdef SKV_COMMIT_CTAS_PER_SM
+  // cap the resident CTAs per SM (fewer claims in flight -> the follow-up accesses of a
+  // claimed entry still find its line in L2)
+  static const uint32_t pad = [] {
+    const uint32_t b = (228u * 1024u) / SKV_COMMIT_CTAS_PER_SM - 1024u;
+    cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
+    return b;
+  }();
+  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, pad, s>>>(
+#else
+  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
+#endif
+ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap);
 }

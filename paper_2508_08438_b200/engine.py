@@ -278,6 +278,25 @@ class AdmissionEngine:
         return int(ep.value), evs
 
     # --------------------------------------------------------------- misc
+    # --------------------------------------------------------------- serving observables
+
+    def set_cost_model(self, t_base_ms: float = 10.0, c_prefill_ms: float = 1.0,
+                       tier_penalty_ms: Sequence[float] = (0.0, 0.2, 0.5), noise_sigma_ms: float = 0.0,
+                       seed: int = 0) -> None:
+        """``CostModel`` (serving_sim.hpp:25-57); raises ConfigError like CostModel::validate."""
+        m = N.CostModel(t_base_ms, c_prefill_ms, (C.c_double * 3)(*tier_penalty_ms), noise_sigma_ms, seed)
+        self._check(self._lib.skv_set_cost_model(self._h, C.byref(m)))
+
+    def ttft(self, n_prompts: int, request_ids: Optional[np.ndarray] = None):
+        """Per prompt of the last admit: (ttft_ms, intra_tokens, inter_tokens) --
+        CostModel::ttft (serving_sim.hpp:50-56) and attribute_reuse (:313-324)."""
+        out = np.zeros(n_prompts, np.float64)
+        intra = np.zeros(n_prompts, np.uint32)
+        inter = np.zeros(n_prompts, np.uint32)
+        rid = None if request_ids is None else np.ascontiguousarray(request_ids, np.uint64)
+        self._check(self._lib.skv_admit_ttft(self._h, _ptr(rid), _ptr(out), _ptr(intra), _ptr(inter), 0))
+        return out, intra, inter
+
     def set_tiers(self, h: np.ndarray, d: np.ndarray, tiers: np.ndarray):
         h = np.ascontiguousarray(h, np.uint64)
         d = np.ascontiguousarray(d, np.uint64)

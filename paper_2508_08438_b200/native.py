@@ -117,6 +117,11 @@ class StageTimes(C.Structure):
                 ("kernels_launched", C.c_uint32), ("prefetched", C.c_uint32)]
 
 
+class CostModel(C.Structure):
+    _fields_ = [("t_base_ms", C.c_double), ("c_prefill_ms", C.c_double), ("tier_penalty_ms", C.c_double * 3),
+                ("noise_sigma_ms", C.c_double), ("seed", C.c_uint64)]
+
+
 class GenSpec(C.Structure):
     _fields_ = [("n_prompts", C.c_uint64), ("prompt_tokens", C.c_uint64), ("n_users", C.c_uint64),
                 ("first_user", C.c_uint64), ("pool_size", C.c_uint64), ("pool_tokens", C.c_uint64),
@@ -155,6 +160,9 @@ SIGNATURES = {
     "skv_export": (C.c_int, [C.c_void_p, C.POINTER(Entry), C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_entry_count": (C.c_uint64, [C.c_void_p]),
     "skv_last_times": (C.c_int, [C.c_void_p, C.POINTER(StageTimes)]),
+    "skv_cost_model_default": (None, [C.POINTER(CostModel)]),
+    "skv_set_cost_model": (C.c_int, [C.c_void_p, C.POINTER(CostModel)]),
+    "skv_admit_ttft": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "skv_generate": (C.c_int, [C.POINTER(GenSpec), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),

@@ -48,6 +48,8 @@ def load_ref():
         "ref_engine_admit": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp, vp, vp, vp, vp, vp]),
         "ref_engine_commit": (C.c_int, [vp]),
         "ref_engine_set_tiers": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
+        "ref_engine_ttft": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_uint64, vp, vp, vp]),
         "ref_engine_epoch": (C.c_int, [vp, u64p, sz, vp, vp, vp, vp, vp, vp, C.POINTER(sz)]),
         "ref_engine_export": (sz, [vp, sz, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "ref_workload_generate": (vp, [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double,
@@ -122,6 +124,17 @@ class RefEngine:
 
     def commit(self):
         assert self.L.ref_engine_commit(self.h) == 0
+
+    def ttft(self, n, model, request_ids=None):
+        """CostModel::ttft + attribute_reuse of the last admit (model: dict of skv_cost_model fields)."""
+        out = np.zeros(n, np.float64)
+        intra = np.zeros(n, np.uint32)
+        inter = np.zeros(n, np.uint32)
+        rid = None if request_ids is None else np.ascontiguousarray(request_ids, np.uint64)
+        pen = model["tier_penalty_ms"]
+        assert self.L.ref_engine_ttft(self.h, _p(rid), model["t_base_ms"], model["c_prefill_ms"], pen[1], pen[2],
+                                      model["noise_sigma_ms"], model["seed"], _p(out), _p(intra), _p(inter)) == 0
+        return out, intra, inter
 
     def set_tiers(self, tokens, offsets, tiers):
         tokens = np.ascontiguousarray(tokens, np.uint32)

@@ -131,6 +131,48 @@ def test_engine_vs_reference(ref, orules, B, W, users):
     oe.close()
 
 
+COST_MODELS = [
+    dict(t_base_ms=10.0, c_prefill_ms=1.0, tier_penalty_ms=(0.0, 0.2, 0.5), noise_sigma_ms=0.0, seed=0),
+    dict(t_base_ms=3.5, c_prefill_ms=0.7, tier_penalty_ms=(0.0, 0.13, 0.31), noise_sigma_ms=2.5, seed=99),
+]
+
+
+@pytest.mark.parametrize("model", COST_MODELS)
+def test_ttft_and_reuse_vs_reference(ref, orules, model):
+    """CostModel::ttft (serving_sim.hpp:50-56) and attribute_reuse (:313-324) on the
+    C restatement vs the reference's own CostModel, over tiered, partly private indexes.
+    Bit-exact without noise; with Box-Muller noise within 1e-12 relative (libm log/cos)."""
+    from refh import RefEngine, RefRules
+    B, W = 8, 16
+    rng = np.random.default_rng(77)
+    trunks = make_trunks(rng, 10)
+    re_ = RefEngine(ref, RefRules(ref), B=B, W=W)
+    oe = OracleEngine(orules, B=B, W=W)
+    for k in range(4):
+        batch = make_batch(rng, trunks, 150, 5)
+        re_.admit(*batch)
+        oe.admit(*batch)
+        n = len(batch[1]) - 1
+        rid = np.arange(1000 * k, 1000 * k + n, dtype=np.uint64)
+        ta, ia, xa = re_.ttft(n, model, rid)
+        tb, ib, xb = oe.ttft(n, model, rid)
+        np.testing.assert_array_equal(ia, ib)
+        np.testing.assert_array_equal(xa, xb)
+        if model["noise_sigma_ms"] == 0:
+            np.testing.assert_array_equal(ta, tb)
+        else:
+            np.testing.assert_allclose(ta, tb, rtol=1e-12, atol=0)
+        re_.commit()
+        oe.commit()
+        # tier tags on a fresh share of the committed blocks
+        nb = int(((batch[1][1:] - batch[1][:-1]) // B).sum())
+        tiers = rng.integers(0, 3, nb).astype(np.uint8)
+        re_.set_tiers(batch[0], batch[1], tiers)
+        oe.set_tiers(batch[0], batch[1], tiers)
+    re_.close()
+    oe.close()
+
+
 def test_monitor_burst_downgrade():
     """test_monitor.cpp:101-120 restated through the batch engine: a block used by one
     user in the previous window and by a cross-user burst now is downgraded to Private
