@@ -95,11 +95,12 @@ typedef struct {
   uint32_t block_tokens;       /* B: tokens per KV block (multiple of 4, 4..4096)     */
   uint32_t window_tokens;      /* W: right-context tokens of a block's scan window    */
   uint64_t index_capacity;     /* entry slots (rounded up to a power of two)          */
-  uint64_t max_prompts;        /* per batch                                           */
+  uint64_t max_prompts;        /* per batch (<= 2^24)                                 */
   uint64_t max_tokens;         /* per batch                                           */
   uint64_t max_window_entries; /* distinct entries touched per monitor window         */
   double entropy_jump;         /* MonitorConfig::entropy_jump (monitor.hpp:12)        */
   uint64_t u_pre_max;          /* MonitorConfig::u_pre_max    (monitor.hpp:13)        */
+  uint64_t max_users;          /* distinct UserIds the context can intern (creators)  */
 } skv_config;
 
 void skv_config_default(skv_config* c);

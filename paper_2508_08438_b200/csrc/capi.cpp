@@ -139,7 +139,9 @@ struct skv_ctx {
   uint64_t admitted_prompts = 0;  // request ids of the last batch default to [admitted_prompts - N, ...)
   uint32_t last_n = 0;            // prompts of the last skv_admit
   unsigned long long *keys_a = nullptr, *keys_b = nullptr;  // ordered-replay access keys
-  uint32_t* fix_list = nullptr;  // commit: duplicate-key slots + depths (2 x max_blocks)
+  uint32_t* fix_list = nullptr;  // commit: duplicate-key slots, depths, prompts (3 x max_blocks)
+  skv::UserTable users_tab{};     // interned UserIds (Rec::creator)
+  uint32_t* uidx = nullptr;       // interned user of every prompt of the last admit
   void* temp = nullptr;
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
@@ -448,6 +450,7 @@ void skv_config_default(skv_config* c) {
   c->max_window_entries = 1ull << 16;
   c->entropy_jump = 0.3;  // MonitorConfig defaults (monitor.hpp:12-15)
   c->u_pre_max = 1;
+  c->max_users = 1ull << 20;
 }
 
 int skv_create(const skv_config* cfg, skv_ctx** out) {
@@ -458,7 +461,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     const uint32_t B = cfg->block_tokens;
     if (B < 4 || B > 4096 || B % 4) throw skv::ConfigError("block_tokens must be a multiple of 4 in [4, 4096]");
     if (cfg->window_tokens > 4096) throw skv::ConfigError("window_tokens must be <= 4096");
-    if (cfg->max_prompts == 0 || cfg->max_prompts >= (1ull << 31)) throw skv::ConfigError("bad max_prompts");
+    if (cfg->max_prompts == 0 || cfg->max_prompts > skv::kMaxBatchPrompts)
+      throw skv::ConfigError("max_prompts must be in [1, 2^24]");
+    if (cfg->max_users == 0 || cfg->max_users >= (1ull << 30)) throw skv::ConfigError("bad max_users");
     if (cfg->max_tokens / B >= (1ull << 31)) throw skv::ConfigError("max_tokens / block_tokens must be < 2^31");
     if (cfg->max_window_entries == 0 || cfg->max_window_entries >= (1ull << 31))
       throw skv::ConfigError("bad max_window_entries");
@@ -534,7 +539,22 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->d_reqid = dalloc<uint64_t>(N, c->owned);
     c->keys_a = dalloc<unsigned long long>(NB, c->owned);
     c->keys_b = dalloc<unsigned long long>(NB, c->owned);
-    c->fix_list = dalloc<uint32_t>(2 * NB, c->owned);
+    c->fix_list = dalloc<uint32_t>(3 * NB, c->owned);
+    c->uidx = dalloc<uint32_t>(N, c->owned);
+    {  // user table: 2x slots, keys = kNoUser, idx = 0, index 0 reserved for UserId ~0
+      uint32_t slots = 1;
+      while (slots < 2 * cfg->max_users) slots <<= 1;
+      c->users_tab.keys = dalloc<unsigned long long>(slots, c->owned);
+      c->users_tab.idx = dalloc<uint32_t>(slots, c->owned);
+      c->users_tab.rev = dalloc<uint64_t>(cfg->max_users + 1, c->owned);
+      c->users_tab.count = dalloc<uint32_t>(1, c->owned);
+      c->users_tab.mask = slots - 1;
+      c->users_tab.cap = static_cast<uint32_t>(cfg->max_users + 1);
+      CK(cudaMemsetAsync(c->users_tab.keys, 0xff, slots * 8ull, c->stream));
+      CK(cudaMemsetAsync(c->users_tab.idx, 0, slots * 4ull, c->stream));
+      CK(cudaMemsetAsync(c->users_tab.rev, 0xff, 8, c->stream));
+      CK(cudaMemsetAsync(c->users_tab.count, 0, 4, c->stream));
+    }
     size_t tb = std::max(skv::scan_temp_bytes(static_cast<uint32_t>(std::max(N + 1, NB))),
                          skv::sort_keys_temp_bytes(static_cast<uint32_t>(NB), 32 + log2u(cap)));
     c->temp_bytes = tb;
@@ -686,7 +706,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // chained keys + labels, then the index probe (stage 3)
     skv::MonCtx mon = monitor_ctx(c);
     CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
-    skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, users, N, c->bh, c->blabel, c->bdecision,
+    skv::launch_intern_users(c->users_tab, users, N, c->uidx, c->counters + 5, s);
+    skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
                             c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, s);
     CK(cudaEventRecord(c->ev[3], s));
     // stage 4: monitor record -- hits and set inserts were recorded inside the probe;
@@ -694,7 +715,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // tracked set crossed 64 users in this batch
     skv::launch_record(c->ix, mon, c->bslot, c->blk_off, c->matched, users, N, s);
     skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
-    uint32_t launched = 7;  // block counts, scan (2), hash/scan, chain/probe, record, finish
+    uint32_t launched = 8;  // block counts, scan (2), hash/scan, intern, chain/probe, record, finish
     CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 12, cudaMemcpyDeviceToHost, s));
     sync_check(s);
     const uint32_t n_replay = c->host_small[0];
@@ -729,6 +750,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     sync_check(s);
     if (c->host_small[8 + 5] & 1u)
       throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
+    if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
     c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
     c->times.prefetched = use_pf ? 1 : 0;
     c->times.chain_probe_ms = elapsed(c->ev[2], c->ev[3]);
@@ -881,7 +903,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));  // intra-batch duplicate fix-up count
     ++c->batch_id;
-    skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->p_users, c->p_owners, c->p_n, c->bslot,
+    skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), s);
     CK(cudaEventRecord(c->ev[6], s));
@@ -893,7 +915,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     c->entries += nn;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += 2;  // k_commit, k_commit_fixup
+    c->times.kernels_launched += 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
     c->times.new_blocks = nn;
     c->pending = false;
     if (new_entries) *new_entries = nn;
@@ -982,7 +1004,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
     uint32_t* dn = dalloc<uint32_t>(1, tmp);
     cudaStream_t s = c->stream;
     CK(cudaMemsetAsync(dn, 0, 4, s));
-    skv::launch_export(c->ix, dout, dn, s);
+    skv::launch_export(c->ix, c->users_tab.rev, dout, dn, s);
     uint32_t cnt = 0;
     CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);

@@ -18,34 +18,56 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kMaxSetUsers = 64;  // AccessStats::kMaxTrackedUsers (access_stats.hpp:15)
 
 struct __align__(32) Rec {
-  uint64_t h, d;      // chained prefix key, block digest
-  uint64_t creator;   // UserId of the first inserter
-  uint32_t parent;    // slot of the previous block's entry, kNone for block 0
-  uint8_t label;      // SensitivityLabel
-  uint8_t owner;      // OwnerClass
-  uint8_t tier;       // MemTier
-  uint8_t state;      // 0 empty/claimed-unwritten, 1 live
+  uint64_t h, d;         // chained prefix key, block digest
+  uint32_t creator;      // interned UserId of the first inserter (UserTable index)
+  uint32_t meta;         // label:2 | owner:1 | tier:2 | live:1 | - :2 | claiming prompt:24 (meta_* helpers)
+  uint32_t parent;       // slot of the previous block's entry, kNone for block 0
+  uint32_t first_child;  // subtree walk for label propagation (children chained by Aux::next_sibling)
 };
 static_assert(sizeof(Rec) == 32, "record must be one 32-B sector");
+
+__host__ __device__ inline uint32_t meta_label(uint32_t m) { return m & 3u; }
+__host__ __device__ inline uint32_t meta_owner(uint32_t m) { return (m >> 2) & 1u; }
+__host__ __device__ inline uint32_t meta_tier(uint32_t m) { return (m >> 3) & 3u; }
+__host__ __device__ inline uint32_t meta_prompt(uint32_t m) { return m >> 8; }
+__host__ __device__ inline uint32_t make_meta(uint32_t label, uint32_t owner, uint32_t tier, uint32_t prompt) {
+  return (label & 3u) | ((owner & 1u) << 2) | ((tier & 3u) << 3) | (1u << 5) | (prompt << 8);
+}
+constexpr uint32_t kMaxBatchPrompts = 1u << 24;  // the claiming-prompt field of Rec::meta
 
 struct __align__(16) Stats {
   uint32_t hit_cur, u_cnt, hit_pre, u_pre;
 };
 
 struct __align__(16) Aux {
-  uint32_t first_child, next_sibling;  // subtree walk for label propagation
-  uint32_t set_idx;                    // user-set pool slot for the current window, kNone if untouched
-  uint32_t mark;  // commit: intra-batch claim 0xffffffff-prompt (>= 2^31); epoch: candidate stamp (< 2^31)
+  uint32_t next_sibling;  // next child of the same parent (written only when the parent already had one)
+  uint32_t set_idx;       // user-set pool slot for the current window, kNone if untouched
+  uint32_t mark;          // epoch: candidate stamp
+  uint32_t spare;
 };
 
-// One index slot = 64 B: sector 0 is everything the probe reads, sector 1 the monitor
-// window and tree links.
+// One index slot = 64 B.  Sector 0 (Rec) is everything a probe reads AND everything an
+// insert writes (claim CAS, payload, the parent's first_child): a commit touches one
+// sector per new block.  Sector 1 holds the monitor window and the sibling link.
 struct __align__(64) Entry {
   Rec rec;
   Stats stats;
   Aux aux;
 };
 static_assert(sizeof(Entry) == 64, "entry must be two 32-B sectors");
+
+// Interned user ids (UserId::value -> u32), so that a record's creator fits sector 0.
+// Open addressing on keys (empty = kNoUser); idx[slot] = index + 1 once assigned;
+// rev[index] = the UserId.
+constexpr unsigned long long kNoUser = ~0ull;
+struct UserTable {
+  unsigned long long* keys = nullptr;
+  uint32_t* idx = nullptr;
+  uint64_t* rev = nullptr;
+  uint32_t* count = nullptr;
+  uint32_t mask = 0;   // slots - 1
+  uint32_t cap = 0;    // max distinct users
+};
 
 // Device forms of the compiled rule DFA (built by capi.cpp upload_rules).
 //
@@ -143,6 +165,8 @@ struct CostModelDev {
 };
 
 void launch_init_entries(const Index& ix, cudaStream_t s);
+void launch_intern_users(const UserTable& t, const uint64_t* users, uint32_t n, uint32_t* uidx, uint32_t* err,
+                         cudaStream_t s);
 void launch_ttft(const uint32_t* blk_off, const uint32_t* matched, const uint32_t* plen, const uint8_t* bmeta,
                  const uint64_t* request_ids, uint64_t request_base, uint32_t n, uint32_t B, const CostModelDev& cm,
                  double* ttft, uint32_t* intra, uint32_t* inter, cudaStream_t s);
@@ -157,7 +181,7 @@ int hash_scan_grid(int device, uint32_t smem_bytes, uint32_t threads);
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
-                        const uint64_t* users, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
+                        const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
                         const MonCtx& mon, cudaStream_t s);
 void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
@@ -174,7 +198,7 @@ void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* re
                           const unsigned long long* keys, uint32_t n_keys, const uint64_t* users, int grid,
                           cudaStream_t s);
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                   const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
+                   const uint32_t* exist, const uint8_t* label, const uint32_t* uidx, const uint8_t* owners,
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
@@ -189,7 +213,7 @@ void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_
                        cudaStream_t s);
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n,
                       cudaStream_t s);
-void launch_export(const Index& ix, void* out, uint32_t* n_out, cudaStream_t s);
+void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s);
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);

@@ -613,15 +613,7 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
     const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
     ulonglong2 k = rp[0];
     if (k.x == h && k.y == d) {
-      ulonglong2 m = rp[1];
-      out->h = h;
-      out->d = d;
-      out->creator = m.x;
-      out->parent = static_cast<uint32_t>(m.y);
-      out->label = static_cast<uint8_t>(m.y >> 32);
-      out->owner = static_cast<uint8_t>(m.y >> 40);
-      out->tier = static_cast<uint8_t>(m.y >> 48);
-      out->state = static_cast<uint8_t>(m.y >> 56);
+      *out = ix.e[s].rec;
       return static_cast<uint32_t>(s);
     }
     if (k.x == 0 && k.y == 0) return kNone;
@@ -951,14 +943,15 @@ constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free t
 
 struct Probe {
   uint32_t slot;
-  uint64_t creator;
-  uint32_t meta;  // label | owner<<8 | tier<<16 | state<<24
+  uint32_t creator;  // interned user index
+  uint32_t meta;     // Rec::meta
 };
 
 __device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint64_t d, uint64_t s, ulonglong2 k,
                                                ulonglong2 m) {
   for (uint64_t i = 0; i <= ix.mask; ++i) {
-    if (k.x == h && k.y == d) return Probe{static_cast<uint32_t>(s), m.x, static_cast<uint32_t>(m.y >> 32)};
+    if (k.x == h && k.y == d)
+      return Probe{static_cast<uint32_t>(s), static_cast<uint32_t>(m.x), static_cast<uint32_t>(m.x >> 32)};
     if (k.x == 0 && k.y == 0) break;
     s = (s + 1) & ix.mask;
     const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
@@ -970,7 +963,7 @@ __device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint
 
 __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     Index ix, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
-    const uint32_t* __restrict__ first_sens, const uint64_t* __restrict__ users, uint32_t n_prompts,
+    const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
     uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon) {
@@ -983,7 +976,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
   const bool has = lane < kCPPrompts && p < n_prompts;
   const uint32_t bo = has ? blk_off[p] : 0, n = has ? blk_off[p + 1] - bo : 0;
   const uint32_t fs = has ? first_sens[p] : 0;
-  const uint64_t user = has ? users[p] : 0;
+  const uint32_t user = has ? uidx[p] : 0xffffffffu;
   uint64_t (*td)[kPitch] = s_d[wid];
   uint64_t (*th)[kPitch] = s_h[wid];
   uint64_t h = 0;
@@ -1049,13 +1042,13 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
         if (q >= ng) break;
         const uint32_t j = js[q];
         const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
-        const uint64_t uj = __shfl_sync(kFull, user, j);
+        const uint32_t uj = __shfl_sync(kFull, user, j);
         const uint32_t mj = __shfl_sync(kFull, m, j);
         const bool act = b < nj;
         Probe pr{kNone, 0, 0};
         if (act) pr = probe_resolve(ix, th[j][lane], td[j][lane], ss[q], kk[q], mm[q]);
         const bool found = pr.slot != kNone;
-        const uint32_t lab = pr.meta & 0xffu;
+        const uint32_t lab = meta_label(pr.meta);
         const bool vis = found && (lab == SKV_LABEL_PUBLIC || pr.creator == uj);
         const uint32_t nf = __ballot_sync(kFull, act && !found);
         const uint32_t nv = __ballot_sync(kFull, act && !vis);
@@ -1065,7 +1058,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
         if (act) {
           if (b < new_m) {
             decision[bj + b] = lab == SKV_LABEL_PUBLIC ? SKV_PUBLIC_HIT : SKV_OWNER_HIT;
-            tm = (pr.meta >> 16) & 0xffu;
+            tm = meta_tier(pr.meta);
             // TTFT epilogue inputs: the matched block's tier and whether the user created it
             bmeta[bj + b] = static_cast<uint8_t>(tm | ((pr.creator == uj) ? 4u : 0u));
           }
@@ -1100,14 +1093,15 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 //     parent slot, label, owner, tier = HBM, live) with one 16-B store and links the
 //     entry under its parent (the previous block's slot -- identical for every
 //     duplicate of the key) exactly once;
-//   * every claimant also does mark = atomicMax(0xffffffff - p): the maximum is the
-//     lowest prompt index, i.e. the first creator in prompt order (cache_index.hpp:164-168);
+//   * the inserter records its prompt index in Rec::meta;
 //   * a claimant whose CAS found the key already inserted by this batch is an
-//     intra-batch duplicate: it appends the slot to a (rare) fix-up list, and
-//     k_commit_fixup -- stream-ordered after this kernel, when every claim is final --
-//     rewrites the payload from the winning prompt.
-// Claim values are >= 2^31 and never collide with the epoch candidate stamps (< 2^31)
-// kept in the same word.
+//     intra-batch duplicate: it appends (slot, depth, prompt) to a (rare) fix-up list.
+//     Stream-ordered after this kernel, k_commit_fixup_min folds the duplicates'
+//     prompts into Rec::meta with atomicMin (lowest prompt = first creator in prompt
+//     order, cache_index.hpp:164-168) and k_commit_fixup rewrites the payload from the
+//     winning prompt.
+// Everything an insert writes is in sector 0 of the entry (the sibling link only on a
+// branch), so a new block costs one DRAM sector round trip.
 #ifndef SKV_COMMIT_ROUNDS
 #define SKV_COMMIT_ROUNDS 2
 #endif
@@ -1116,7 +1110,7 @@ constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
                                                 const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
-                                                const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
+                                                const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                                 uint32_t n_prompts, uint32_t* __restrict__ slot_out,
                                                 unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                                                 uint32_t fix_cap, uint32_t* err_flag) {
@@ -1126,9 +1120,8 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
   const uint32_t lane = lane_id();
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) return;
-  const uint32_t tag = 0xffffffffu - p;
-  const unsigned long long creator = users[p];
-  const uint32_t owner_bits = static_cast<uint32_t>(owners ? owners[p] : 0) << 8;
+  const uint32_t creator = uidx[p];
+  const uint32_t owner = owners ? owners[p] : 0u;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
   uint32_t inserted = 0;
   for (uint32_t base = k0; base < n; base += 32 * R) {
@@ -1200,7 +1193,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       s32[r] = static_cast<uint32_t>(sl[r]);
       slot_out[bo + base + 32 * r + lane] = s32[r];
     }
-    // payloads, first-creator marks and parent links (parent = previous block's slot)
+    // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1214,51 +1207,56 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       sib[r] = kNone;
       if (s32[r] == kNone) continue;
       Entry& e = ix.e[s32[r]];
-      atomicMax(&e.aux.mark, tag);
       if (mine[r]) {
-        const uint32_t meta = lab[r] | owner_bits | (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
-        ulonglong2 payload;
-        payload.x = creator;
-        payload.y = static_cast<unsigned long long>(par[r]) | (static_cast<unsigned long long>(meta) << 32);
-        reinterpret_cast<ulonglong2*>(&e.rec)[1] = payload;
-        if (par[r] != kNone) sib[r] = atomicExch(&ix.e[par[r]].aux.first_child, s32[r]);
+        // creator + meta (with this prompt as the claimant) in one 8-B store, then the
+        // parent slot; first_child is left alone (a duplicate claimant may already be
+        // linking a child under this entry)
+        const uint32_t meta = make_meta(lab[r], owner, SKV_TIER_HBM, p);
+        *reinterpret_cast<uint2*>(&e.rec.creator) = make_uint2(creator, meta);
+        e.rec.parent = par[r];
+        if (par[r] != kNone) sib[r] = atomicExch(&ix.e[par[r]].rec.first_child, s32[r]);
         ++inserted;
       } else {
         const uint32_t f = atomicAdd(n_fix, 1u);
         if (f < fix_cap) {
           fix_list[f] = s32[r];
           fix_list[fix_cap + f] = base + 32 * r + lane;  // block depth of this key
+          fix_list[2 * fix_cap + f] = p;
         } else {
           atomicOr(err_flag, 4u);
         }
       }
     }
+    // a child chained in front of existing siblings (branching only: under a fresh
+    // parent the exchange returns kNone, which is the init value)
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (mine[r] && par[r] != kNone) ix.e[s32[r]].aux.next_sibling = sib[r];
+      if (mine[r] && sib[r] != kNone) ix.e[s32[r]].aux.next_sibling = sib[r];
   }
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
 }
 
-// Intra-batch duplicates: write the final winner's payload (all claims are complete).
+// Intra-batch duplicates, pass 1: lowest claiming prompt (all claims are complete).
+__global__ void k_commit_fixup_min(Index ix, const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
+                                   uint32_t fix_cap) {
+  const uint32_t nf = min(*n_fix, fix_cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x)
+    atomicMin(&ix.e[fix_list[i]].rec.meta, (fix_list[2 * fix_cap + i] << 8) | 0xffu);
+}
+
+// Pass 2: the winner's payload (creator, label, owner, tier = HBM, live, winner prompt).
 __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
-                               const uint64_t* __restrict__ users, const uint8_t* __restrict__ owners,
+                               const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
                                uint32_t fix_cap) {
   const uint32_t nf = min(*n_fix, fix_cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
-    Entry& e = ix.e[s];
-    const uint32_t pw = 0xffffffffu - e.aux.mark;
-    const uint32_t parent = e.rec.parent;
-    const uint32_t meta = static_cast<uint32_t>(label[blk_off[pw] + b]) |
-                          (static_cast<uint32_t>(owners ? owners[pw] : 0) << 8) |
-                          (static_cast<uint32_t>(SKV_TIER_HBM) << 16) | (1u << 24);
-    ulonglong2 payload;
-    payload.x = users[pw];
-    payload.y = static_cast<unsigned long long>(parent) | (static_cast<unsigned long long>(meta) << 32);
-    reinterpret_cast<ulonglong2*>(&e.rec)[1] = payload;
+    Rec& r = ix.e[s].rec;
+    const uint32_t pw = meta_prompt(r.meta);
+    const uint32_t meta = make_meta(label[blk_off[pw] + b], owners ? owners[pw] : 0u, SKV_TIER_HBM, pw);
+    *reinterpret_cast<uint2*>(&r.creator) = make_uint2(uidx[pw], meta);
   }
 }
 
@@ -1283,7 +1281,7 @@ __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, 
   if (i >= *n_list) return;
   uint32_t s = list[i];
   if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
-  if (ix.e[s].rec.label != SKV_LABEL_PUBLIC) return;
+  if (meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
   Stats st = ix.e[s].stats;
   if (st.hit_pre == 0) return;
   double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
@@ -1308,8 +1306,8 @@ __global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const
   DevEvent ev;
   ev.h = r.h;
   ev.d = r.d;
-  ev.owner = r.owner;
-  ev.action = r.owner == 0 ? SKV_ACTION_DOWNGRADE : SKV_ACTION_RESTRICT;
+  ev.owner = static_cast<uint8_t>(meta_owner(r.meta));
+  ev.action = ev.owner == 0 ? SKV_ACTION_DOWNGRADE : SKV_ACTION_RESTRICT;
   for (int k = 0; k < 6; ++k) ev.pad[k] = 0;
   ev.now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
   ev.prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
@@ -1323,12 +1321,12 @@ __global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, 
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_fired) return;
   uint32_t root = fired[i];
-  uint8_t lab = ix.e[root].rec.owner == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
-  ix.e[root].rec.label = lab;
-  uint32_t cur = ix.e[root].aux.first_child;
+  const uint32_t lab = meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+  ix.e[root].rec.meta = (ix.e[root].rec.meta & ~3u) | lab;
+  uint32_t cur = ix.e[root].rec.first_child;
   while (cur != kNone) {
-    ix.e[cur].rec.label = lab;
-    uint32_t c = ix.e[cur].aux.first_child;
+    ix.e[cur].rec.meta = (ix.e[cur].rec.meta & ~3u) | lab;
+    uint32_t c = ix.e[cur].rec.first_child;
     if (c != kNone) {
       cur = c;
       continue;
@@ -1367,11 +1365,11 @@ __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, cons
   if (s == kNone) return;
   // demote (cache_index.hpp:362-381): a tier only moves down HBM -> DRAM -> SSD, so
   // repeated tags of one entry keep the slowest (the reference's demote-until loop)
-  uint32_t* meta = reinterpret_cast<uint32_t*>(&ix.e[s].rec.label);
+  uint32_t* meta = &ix.e[s].rec.meta;
   uint32_t old = *meta;
   for (;;) {
-    const uint32_t t = max((old >> 16) & 0xffu, static_cast<uint32_t>(tiers[i]));
-    const uint32_t nv = (old & ~0x00ff0000u) | (t << 16);
+    const uint32_t t = max(meta_tier(old), static_cast<uint32_t>(tiers[i]));
+    const uint32_t nv = (old & ~(3u << 3)) | (t << 3);
     if (nv == old) break;
     const uint32_t got = atomicCAS(meta, old, nv);
     if (got == old) break;
@@ -1379,7 +1377,7 @@ __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, cons
   }
 }
 
-__global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
+__global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_entry* out, uint32_t* n_out) {
   uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s > ix.mask) return;
   const Rec& r = ix.e[s].rec;
@@ -1388,10 +1386,10 @@ __global__ void k_export(Index ix, skv_entry* out, uint32_t* n_out) {
   skv_entry e;
   e.h = r.h;
   e.d = r.d;
-  e.creator = r.creator;
-  e.label = r.label;
-  e.owner = r.owner;
-  e.tier = r.tier;
+  e.creator = user_rev[r.creator];
+  e.label = static_cast<uint8_t>(meta_label(r.meta));
+  e.owner = static_cast<uint8_t>(meta_owner(r.meta));
+  e.tier = static_cast<uint8_t>(meta_tier(r.meta));
   e.hit_cur = st.hit_cur;
   e.u_cnt = st.u_cnt;
   e.hit_pre = st.hit_pre;
@@ -1485,7 +1483,7 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 }
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
-                        const uint64_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
+                        const uint32_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
                         const MonCtx& mon, cudaStream_t s) {
   if (n)
@@ -1537,7 +1535,7 @@ void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* re
 }
 
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
-                   const uint32_t* exist, const uint8_t* label, const uint64_t* users, const uint8_t* owners,
+                   const uint32_t* exist, const uint8_t* label, const uint32_t* users, const uint8_t* owners,
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s) {
   if (!n) return;
@@ -1555,6 +1553,7 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
 #endif
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag);
+  k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap);
 }
 
@@ -1589,8 +1588,8 @@ void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, con
   if (n) k_set_tiers<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, tiers, n);
 }
 
-void launch_export(const Index& ix, void* out, uint32_t* n_out, cudaStream_t s) {
-  k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, static_cast<skv_entry*>(out), n_out);
+void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s) {
+  k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, user_rev, static_cast<skv_entry*>(out), n_out);
 }
 
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s) {
@@ -1610,12 +1609,52 @@ __global__ void k_init_entries(Index ix) {
   if (s > ix.mask) return;
   ulonglong2* p = reinterpret_cast<ulonglong2*>(&ix.e[s]);
   const ulonglong2 z = {0ull, 0ull};
-  p[0] = z;
-  p[1] = z;
-  p[2] = z;
-  p[3] = {0xffffffffffffffffull, 0x00000000ffffffffull};  // first_child, next_sibling, set_idx = none; mark = 0
+  p[0] = z;                                        // key (0,0) = empty
+  p[1] = {0ull, 0xffffffffffffffffull};            // creator, meta = 0; parent, first_child = none
+  p[2] = z;                                        // AccessStats window
+  p[3] = {0xffffffffffffffffull, 0ull};            // next_sibling, set_idx = none; mark = 0
 }
 }  // namespace
+
+// UserId -> u32 index (insert if absent).  One thread per prompt; the slot's inserter
+// allocates the index, everyone else waits for it to be published.
+__global__ void k_intern_users(UserTable t, const uint64_t* __restrict__ users, uint32_t n, uint32_t* __restrict__ uidx,
+                               uint32_t* err) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const unsigned long long u = users[p];
+  if (u == kNoUser) {  // index 0 is reserved for the one UserId equal to the empty marker
+    uidx[p] = 0;
+    return;
+  }
+  uint32_t s = static_cast<uint32_t>(slot_hash(u, 0x5bd1e995ull)) & t.mask;
+  for (uint32_t i = 0; i <= t.mask; ++i, s = (s + 1) & t.mask) {
+    unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(&t.keys[s]);
+    if (k == kNoUser) k = atomicCAS(&t.keys[s], kNoUser, u);
+    if (k == kNoUser) {  // inserted: allocate (index 0 is reserved)
+      const uint32_t id = atomicAdd(t.count, 1u) + 1;
+      if (id >= t.cap) atomicOr(err, 8u);
+      if (id < t.cap) t.rev[id] = u;
+      __threadfence();
+      atomicExch(&t.idx[s], id + 1);
+      uidx[p] = id;
+      return;
+    }
+    if (k == u) {
+      uint32_t v;
+      while ((v = *reinterpret_cast<volatile uint32_t*>(&t.idx[s])) == 0) {
+      }
+      uidx[p] = v - 1;
+      return;
+    }
+  }
+  atomicOr(err, 8u);
+}
+
+void launch_intern_users(const UserTable& t, const uint64_t* users, uint32_t n, uint32_t* uidx, uint32_t* err,
+                         cudaStream_t s) {
+  if (n) k_intern_users<<<cdiv(n, 256), 256, 0, s>>>(t, users, n, uidx, err);
+}
 
 void launch_init_entries(const Index& ix, cudaStream_t s) {
   k_init_entries<<<static_cast<uint32_t>((ix.cap + 255) / 256), 256, 0, s>>>(ix);

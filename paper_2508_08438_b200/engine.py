@@ -159,6 +159,7 @@ class EngineConfig:
     max_window_entries: int = 1 << 16
     entropy_jump: float = 0.3
     u_pre_max: int = 1
+    max_users: int = 1 << 20
     device: int = 0
 
 

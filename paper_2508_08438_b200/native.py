@@ -82,7 +82,8 @@ class DfaView(C.Structure):
 class Config(C.Structure):
     _fields_ = [("device", C.c_int), ("block_tokens", C.c_uint32), ("window_tokens", C.c_uint32),
                 ("index_capacity", C.c_uint64), ("max_prompts", C.c_uint64), ("max_tokens", C.c_uint64),
-                ("max_window_entries", C.c_uint64), ("entropy_jump", C.c_double), ("u_pre_max", C.c_uint64)]
+                ("max_window_entries", C.c_uint64), ("entropy_jump", C.c_double), ("u_pre_max", C.c_uint64),
+                ("max_users", C.c_uint64)]
 
 
 class Batch(C.Structure):
