@@ -1124,6 +1124,11 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
   const uint32_t owner = owners ? owners[p] : 0u;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
   uint32_t inserted = 0;
+  // sibling links of the previous round set, applied once the next set's claims are in
+  // flight (the exchange results are not waited for on the critical path)
+  uint32_t q_slot[R], q_sib[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) q_sib[r] = kNone, q_slot[r] = kNone;
   for (uint32_t base = k0; base < n; base += 32 * R) {
     uint64_t h[R], d[R];
     uint32_t s32[R], lab[R];
@@ -1158,6 +1163,9 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
                        &oh[r]);
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
@@ -1228,11 +1236,16 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       }
     }
     // a child chained in front of existing siblings (branching only: under a fresh
-    // parent the exchange returns kNone, which is the init value)
+    // parent the exchange returns kNone, which is the init value) -- deferred
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (mine[r] && sib[r] != kNone) ix.e[s32[r]].aux.next_sibling = sib[r];
+    for (int r = 0; r < R; ++r) {
+      q_slot[r] = s32[r];
+      q_sib[r] = mine[r] ? sib[r] : kNone;
+    }
   }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
 }
