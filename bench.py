@@ -175,9 +175,16 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        # NCCL over NVLink when every rank has its own GPU (the timing barrier and the
+        # max-over-ranks reduction are the only collectives); gloo when ranks share a GPU
+        # (a functional check of the N > 1 path on a box with fewer GPUs than ranks)
+        backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
+        dist.init_process_group(backend, init_method="env://")
+    # one process per GPU; with more ranks than visible GPUs (a functional check of the
+    # N > 1 path on a small box) ranks share devices round-robin
+    gpu = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     c = dict(CFG2)
     if args.prompts:
         c["n_prompts"] = args.prompts
@@ -189,7 +196,7 @@ def run_ours(args):
     cap = 1 << max(20, int(np.ceil(np.log2((n_batches + 1) * blocks_per_batch * 1.7))))
     ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
                         max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 18,
-                        device=local)
+                        device=gpu)
 
     # ---- inputs: distinct batches, generated into pinned host memory, copied to HBM
     # N > 1: prefix-forest partitioning -- every rank admits the first n_local prompts of
@@ -285,14 +292,14 @@ def run_ours(args):
         ms = e0.elapsed_time(e1)
         if world > 1:
             import torch.distributed as dist
-            x = torch.tensor([ms], device=dev)
+            x = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             ms = float(x.item())
         last = eng.times()
         eng.close()
         return ms, hs, launches, last, pf
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     ms_dev, hs, launches, last, pf_dev = timed(step_device, clocks)
     clk = clocks.stop()
     ms_e2e, _, _, _, pf_e2e = timed(step_host)
@@ -333,7 +340,7 @@ def run_ours(args):
         "dtype": "u32 tokens / u64 keys (integer), f64 entropy", "data": "synthetic (deterministic generator)",
         "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
                                f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
-                   "global_batch_prompts": n_local * world, "l2": "inputs 512 MiB/step > L2, distinct batch per step",
+                   "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
                    "step": "admit + commit + epoch", "parallelism": (f"prefix-forest partitioned x{world} (skv_route; no data-path collective)"
                                    if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
