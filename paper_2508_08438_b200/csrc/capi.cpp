@@ -152,6 +152,12 @@ struct skv_ctx {
 
   // pending batch (between admit and commit)
   bool pending = false;
+  // monitor records of the last admit, executed inside the commit kernel (overlapping
+  // the claims), or on their own when the batch is not committed
+  bool rec_pending = false;
+  skv::MonCtx rec_mon{};
+  const uint64_t* rec_users = nullptr;
+  uint32_t rec_n = 0;
   uint32_t p_n = 0;
   uint64_t p_blocks = 0;
   const uint64_t* p_users = nullptr;
@@ -619,6 +625,44 @@ int skv_set_rules(skv_ctx* c, const skv_rules* r) {
 
 void* skv_stream(skv_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
+// ------------------------------------------------------------------ monitor records
+// AccessStats::record of the last admitted batch (A.6): the per-access part ran inside
+// k_commit (or k_record); this applies the distinct-user counts and replays, in prompt
+// order, the rare entries whose tracked set crossed 64 users in the batch.
+uint32_t finish_record(skv_ctx* c, cudaStream_t s) {
+  const skv::MonCtx& mon = c->rec_mon;
+  skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
+  uint32_t launched = 1;
+  CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->host_small + 1, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+  sync_check(s);
+  c->rec_pending = false;
+  if (c->host_small[1] & 1u)
+    throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
+  const uint32_t n_replay = c->host_small[0];
+  c->times.replayed_entries = n_replay;
+  if (n_replay > 0) {
+    skv::launch_replay_emit(c->ix, mon, c->bslot, c->blk_off, c->matched, c->rec_n, c->keys_a, c->counters + 9, s);
+    CK(cudaMemcpyAsync(c->host_small, c->counters + 9, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    const uint32_t nk = c->host_small[0];
+    const int end_bit = 32 + log2u(c->ix.cap);
+    skv::launch_sort_keys(c->temp, c->temp_bytes, c->keys_a, c->keys_b, nk, end_bit, s);
+    skv::launch_record_replay(c->ix, mon, c->replay, c->counters + 8, c->keys_b, nk, c->rec_users,
+                              static_cast<int>(c->rec_grid), s);
+    launched += 2 + 2 + (end_bit + 7) / 8;
+  }
+  return launched;
+}
+
+// records of a batch that is not committed (next admit, epoch or export first)
+void flush_record(skv_ctx* c) {
+  if (!c->rec_pending) return;
+  cudaStream_t s = c->stream;
+  skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, s);
+  finish_record(c, s);
+}
+
 // ------------------------------------------------------------------ admission
 int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
   if (!c || !b) return SKV_ERR_ARG;
@@ -628,6 +672,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const uint32_t B = c->cfg.block_tokens;
     if (N > c->max_prompts) throw ArgError("n_prompts exceeds max_prompts");
     if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
+    flush_record(c);  // the previous batch was admitted but not committed
     if (N == 0) {
       if (out) out->n_blocks = 0, out->matched_total = 0;
       c->pending = true;
@@ -710,27 +755,17 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
                             c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, s);
     CK(cudaEventRecord(c->ev[3], s));
-    // stage 4: monitor record -- hits and set inserts were recorded inside the probe;
-    // apply distinct counts, then replay (in prompt order) the rare entries whose
-    // tracked set crossed 64 users in this batch
-    skv::launch_record(c->ix, mon, c->bslot, c->blk_off, c->matched, users, N, s);
-    skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
-    uint32_t launched = 8;  // block counts, scan (2), hash/scan, intern, chain/probe, record, finish
-    CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 12, cudaMemcpyDeviceToHost, s));
+    // stage 4: the monitor records (AccessStats::record of every matched block, in
+    // prompt order) run inside the commit kernel, overlapping the claims' DRAM round
+    // trips; a batch that is not committed gets them from flush_record
+    c->rec_pending = true;
+    c->rec_mon = mon;
+    c->rec_users = users;
+    c->rec_n = N;
+    uint32_t launched = 6;  // block counts, scan (2), hash/scan, intern, chain/probe
+    CK(cudaMemcpyAsync(c->host_small, c->counters + 10, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    const uint32_t n_replay = c->host_small[0];
-    const uint32_t M = c->host_small[2];
-    if (n_replay > 0) {
-      skv::launch_replay_emit(c->ix, mon, c->bslot, c->blk_off, c->matched, N, c->keys_a, c->counters + 9, s);
-      CK(cudaMemcpyAsync(c->host_small, c->counters + 9, 4, cudaMemcpyDeviceToHost, s));
-      sync_check(s);
-      const uint32_t nk = c->host_small[0];
-      const int end_bit = 32 + log2u(c->ix.cap);
-      skv::launch_sort_keys(c->temp, c->temp_bytes, c->keys_a, c->keys_b, nk, end_bit, s);
-      skv::launch_record_replay(c->ix, mon, c->replay, c->counters + 8, c->keys_b, nk, users,
-                                static_cast<int>(c->rec_grid), s);
-      launched += 2 + 2 + (end_bit + 7) / 8;
-    }
+    const uint32_t M = c->host_small[0];
     CK(cudaEventRecord(c->ev[4], s));
     // outputs
     if (out) {
@@ -748,8 +783,6 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     }
     CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    if (c->host_small[8 + 5] & 1u)
-      throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
     if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
     c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
     c->times.prefetched = use_pf ? 1 : 0;
@@ -758,7 +791,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->times.admit_total_ms = elapsed(c->ev[0], c->ev[4]);
     c->times.matched_total = M;
     c->times.accesses = M;
-    c->times.replayed_entries = n_replay;
+    c->times.replayed_entries = 0;
     c->times.touched_entries = c->host_small[8 + 1 + c->cur];
     c->times.kernels_launched = launched;
     c->pending = true;
@@ -903,9 +936,12 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));  // intra-batch duplicate fix-up count
     ++c->batch_id;
+    const bool rec = c->rec_pending;  // the batch's monitor records ride along (see skv_admit)
     skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
-                       static_cast<int>(c->rec_grid), s);
+                       static_cast<int>(c->rec_grid), c->matched, c->rec_users, rec ? &c->rec_mon : nullptr, s);
+    uint32_t launched = 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
+    if (rec) launched += finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
@@ -915,7 +951,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     c->entries += nn;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
+    c->times.kernels_launched += launched;
     c->times.new_blocks = nn;
     c->pending = false;
     if (new_entries) *new_entries = nn;
@@ -927,6 +963,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    flush_record(c);
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev[5], s));
     const uint64_t epoch = ++c->epoch;  // advance_epoch (cache_index.hpp:296-299)
@@ -999,6 +1036,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    flush_record(c);
     std::vector<void*> tmp;
     skv_entry* dout = dalloc<skv_entry>(std::max<uint64_t>(c->entries, 1), tmp);
     uint32_t* dn = dalloc<uint32_t>(1, tmp);

@@ -200,7 +200,8 @@ void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* re
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
                    const uint32_t* exist, const uint8_t* label, const uint32_t* uidx, const uint8_t* owners,
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
-                   uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s);
+                   uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
+                   const uint64_t* users64, const MonCtx* mon, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
                              int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
                              uint32_t* n_cands, cudaStream_t s);

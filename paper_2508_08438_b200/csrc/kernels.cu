@@ -761,14 +761,8 @@ __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* 
 // the hit count changes.  Everything else takes the full record_user path.
 constexpr int kRecRounds = 4;
 
-__global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32_t* __restrict__ slot_in,
-                                                const uint32_t* __restrict__ blk_off,
-                                                const uint32_t* __restrict__ matched,
-                                                const uint64_t* __restrict__ users, uint32_t n_prompts) {
-  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_prompts) return;
-  const uint32_t bo = blk_off[p], m = matched[p], lane = lane_id();
-  const uint64_t u = users[p];
+__device__ __forceinline__ void record_prompt(const Index& ix, const MonCtx& M, const uint32_t* __restrict__ slot_in,
+                                              uint32_t bo, uint32_t m, uint64_t u, uint32_t lane) {
   const uint32_t pos = mix32(u) & (kSetSlots - 1);
   for (uint32_t base = 0; base < m; base += 32 * kRecRounds) {
     uint32_t sl[kRecRounds], si[kRecRounds];
@@ -794,6 +788,15 @@ __global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32
       if (sl[r] != kNone && !(si[r] < kPendingSet && v[r].x == u && v[r].y >= M.wstart))
         record_user(ix, M, sl[r], u);
   }
+}
+
+__global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32_t* __restrict__ slot_in,
+                                                const uint32_t* __restrict__ blk_off,
+                                                const uint32_t* __restrict__ matched,
+                                                const uint64_t* __restrict__ users, uint32_t n_prompts) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_prompts) return;
+  record_prompt(ix, M, slot_in, blk_off[p], matched[p], users[p], lane_id());
 }
 
 // accesses (slot << 32 | prompt) of the entries that need an ordered replay
@@ -1113,13 +1116,18 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
                                                 const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                                 uint32_t n_prompts, uint32_t* __restrict__ slot_out,
                                                 unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
-                                                uint32_t fix_cap, uint32_t* err_flag) {
+                                                uint32_t fix_cap, uint32_t* err_flag,
+                                                const uint32_t* __restrict__ matched,
+                                                const uint64_t* __restrict__ users, MonCtx M, int with_record) {
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   const uint32_t lane = lane_id();
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
-  if (k0 >= n) return;
+  if (k0 >= n) {
+    if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+    return;
+  }
   const uint32_t creator = uidx[p];
   const uint32_t owner = owners ? owners[p] : 0u;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
@@ -1166,6 +1174,10 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
+    // the batch's monitor records (AccessStats::record of the matched blocks, which
+    // precede block k0) run while the first claims are in flight: L2 atomics overlap the
+    // claims' DRAM round trips (record and commit touch disjoint fields)
+    if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
@@ -1550,22 +1562,14 @@ void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* re
 void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off,
                    const uint32_t* exist, const uint8_t* label, const uint32_t* users, const uint8_t* owners,
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
-                   uint32_t fix_cap, uint32_t* err_flag, int fix_grid, cudaStream_t s) {
+                   uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
+                   const uint64_t* users64, const MonCtx* mon, cudaStream_t s) {
+  const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
-#ifdef SKV_COMMIT_CTAS_PER_SM
-  // cap the resident CTAs per SM (fewer claims in flight -> the follow-up accesses of a
-  // claimed entry still find its line in L2)
-  static const uint32_t pad = [] {
-    const uint32_t b = (228u * 1024u) / SKV_COMMIT_CTAS_PER_SM - 1024u;
-    cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
-    return b;
-  }();
-  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, pad, s>>>(
-#else
   k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
-#endif
 ix, h, d, blk_off, exist, label, users, owners, n,
-                                                                    slot, n_new, fix_list, n_fix, fix_cap, err_flag);
+                                                                    slot, n_new, fix_list, n_fix, fix_cap, err_flag,
+                                                                    matched, users64, M, mon ? 1 : 0);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap);
 }
