@@ -629,17 +629,17 @@ void* skv_stream(skv_ctx* c) { return c ? static_cast<void*>(c->stream) : nullpt
 // AccessStats::record of the last admitted batch (A.6): the per-access part ran inside
 // k_commit (or k_record); this applies the distinct-user counts and replays, in prompt
 // order, the rare entries whose tracked set crossed 64 users in the batch.
-uint32_t finish_record(skv_ctx* c, cudaStream_t s) {
+// Enqueue the distinct-count pass; the caller reads counters[8] (replay count) and
+// counters[5] (errors) back with its own synchronisation and calls replay_record.
+void finish_record(skv_ctx* c, cudaStream_t s) {
+  skv::launch_record_finish(c->ix, c->rec_mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
+}
+
+uint32_t replay_record(skv_ctx* c, cudaStream_t s, uint32_t n_replay, uint32_t err) {
   const skv::MonCtx& mon = c->rec_mon;
-  skv::launch_record_finish(c->ix, mon, c->replay, c->counters + 8, static_cast<int>(c->rec_grid), s);
   uint32_t launched = 1;
-  CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(c->host_small + 1, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
-  sync_check(s);
   c->rec_pending = false;
-  if (c->host_small[1] & 1u)
-    throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
-  const uint32_t n_replay = c->host_small[0];
+  if (err & 1u) throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
   c->times.replayed_entries = n_replay;
   if (n_replay > 0) {
     skv::launch_replay_emit(c->ix, mon, c->bslot, c->blk_off, c->matched, c->rec_n, c->keys_a, c->counters + 9, s);
@@ -661,6 +661,10 @@ void flush_record(skv_ctx* c) {
   cudaStream_t s = c->stream;
   skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, s);
   finish_record(c, s);
+  CK(cudaMemcpyAsync(c->host_small, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->host_small + 1, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+  sync_check(s);
+  replay_record(c, s, c->host_small[0], c->host_small[1]);
 }
 
 // ------------------------------------------------------------------ admission
@@ -734,19 +738,23 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       skv::launch_block_counts(off, N, B, c->counts, c->plen, s);
       skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
     }
-    if (b->on_device) {
+    // a device batch's block count is read back with the admit's single sync at the end
+    // (before it only when the caller wants per-block outputs sized by it); until then
+    // n_tokens / B bounds it (<= max_blocks since n_tokens <= max_tokens)
+    const bool nb_known = !b->on_device;
+    if (b->on_device && out) {
       CK(cudaMemcpyAsync(c->host_small, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
       sync_check(s);
       n_blocks = c->host_small[0];
     }
-    if (n_blocks > c->max_blocks) throw ArgError("batch has more blocks than max_tokens / block_tokens");
+    const uint64_t nb_bound = (b->on_device && !out) ? b->n_tokens / B : n_blocks;
     if (!use_pf) CK(cudaMemsetAsync(c->first_sens, 0xff, N * 4ull, s));
-    CK(cudaMemsetAsync(c->bdecision, 0, std::max<uint64_t>(n_blocks, 1), s));
+    CK(cudaMemsetAsync(c->bdecision, 0, std::max<uint64_t>(nb_bound, 1), s));
     CK(cudaMemsetAsync(c->matched + N, 0, 4, s));
     CK(cudaEventRecord(c->ev[1], s));
     // stages 1+2: digest + rule-tier window scan (unless staged by skv_prefetch)
     if (!use_pf)
-      stage12(c, s, tokens, off, N, b->n_tokens, n_blocks, c->blk_off, c->first_sens, c->bd, c->bmask);
+      stage12(c, s, tokens, off, N, b->n_tokens, nb_bound, c->blk_off, c->first_sens, c->bd, c->bmask);
     CK(cudaEventRecord(c->ev[2], s));
     // chained keys + labels, then the index probe (stage 3)
     skv::MonCtx mon = monitor_ctx(c);
@@ -763,11 +771,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->rec_users = users;
     c->rec_n = N;
     uint32_t launched = 6;  // block counts, scan (2), hash/scan, intern, chain/probe
-    CK(cudaMemcpyAsync(c->host_small, c->counters + 10, 4, cudaMemcpyDeviceToHost, s));
-    sync_check(s);
-    const uint32_t M = c->host_small[0];
     CK(cudaEventRecord(c->ev[4], s));
-    // outputs
+    // outputs (per-prompt ones and the summary need no block count)
     if (out) {
       cudaMemcpyKind k = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
       if (out->block_h) CK(cudaMemcpyAsync(out->block_h, c->bh, n_blocks * 8, k, s));
@@ -778,11 +783,18 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       if (out->matched_blocks) CK(cudaMemcpyAsync(out->matched_blocks, c->matched, N * 4ull, k, s));
       if (out->lowest_tier) CK(cudaMemcpyAsync(out->lowest_tier, c->tier, N, k, s));
       if (out->block_offsets) CK(cudaMemcpyAsync(out->block_offsets, c->blk_off, (N + 1) * 4ull, k, s));
+    }
+    // the admit's one synchronisation: counters (errors, touched entries, matched
+    // total) and, for a device batch, the block count
+    CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 11 * 4, cudaMemcpyDeviceToHost, s));
+    if (!nb_known && !out) CK(cudaMemcpyAsync(c->host_small + 20, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    if (!nb_known && !out) n_blocks = c->host_small[20];
+    const uint32_t M = c->host_small[8 + 10];
+    if (out) {
       out->n_blocks = n_blocks;
       out->matched_total = M;
     }
-    CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
-    sync_check(s);
     if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
     c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
     c->times.prefetched = use_pf ? 1 : 0;
@@ -941,14 +953,16 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users, rec ? &c->rec_mon : nullptr, s);
     uint32_t launched = 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
-    if (rec) launched += finish_record(c, s);
+    if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
-    sync_check(s);
+    CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
     std::memcpy(&nn, c->host_small, 8);
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
+    if (rec) launched += replay_record(c, s, c->host_small[5], c->host_small[4]);
     c->entries += nn;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
     c->times.kernels_launched += launched;
@@ -968,39 +982,38 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     CK(cudaEventRecord(c->ev[5], s));
     const uint64_t epoch = ++c->epoch;  // advance_epoch (cache_index.hpp:296-299)
     const uint32_t stamp = static_cast<uint32_t>(epoch);
-    CK(cudaMemcpyAsync(c->host_small, c->counters, 8 * 4, cudaMemcpyDeviceToHost, s));
-    sync_check(s);
+    // grids cover the window lists' capacity; the kernels read the list lengths on the
+    // device, so the epoch needs no host round trip before its kernels
     const int cur = c->cur, prev = 1 - c->cur;
-    const uint32_t n_cur = c->host_small[1 + cur], n_prev = c->host_small[1 + prev];
-    const uint32_t bound = n_cur + n_prev;
+    const uint32_t bound = 2 * c->pool_cap;
     CK(cudaMemsetAsync(c->counters + 3, 0, 8, s));  // n_cands, n_events
-    skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, n_cur, 0, stamp, c->cfg.entropy_jump,
-                                 c->cfg.u_pre_max, c->cands, c->counters + 3, s);
-    skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, n_prev, 1, stamp,
+    skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, stamp,
+                                 c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+    skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, stamp,
                                  c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
     skv::launch_epoch_fire(c->ix, c->cands, c->counters + 3, bound, stamp, epoch, c->events, c->counters + 4, c->fired,
                            s);
     skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
-    skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, n_prev, 1, s);
-    skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, n_cur, 0, s);
+    skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s);
+    skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s);
     CK(cudaMemcpyAsync(c->host_small, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
+    // swap windows: the current list becomes the previous one (its count stays where it
+    // is); the pool and the new current list start empty
+    CK(cudaMemsetAsync(c->counters, 0, 4, s));
+    CK(cudaMemsetAsync(c->counters + 1 + prev, 0, 4, s));
     sync_check(s);
     const uint32_t ne = c->host_small[0];
     std::vector<skv_event> ev(ne);
-    if (ne) CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
-    // swap windows: the current list becomes the previous one
-    uint32_t reset[3] = {0, 0, 0};
-    reset[1 + prev] = 0;
-    reset[1 + cur] = n_cur;
-    // counters[0] pool_count = 0; counters[1+prev] (new cur) = 0; counters[1+cur] (new prev) = n_cur
-    CK(cudaMemcpyAsync(c->counters, reset, 12, cudaMemcpyHostToDevice, s));
-    sync_check(s);
+    if (ne) {
+      CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
+      sync_check(s);
+    }
     c->cur = prev;
     c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
     CK(cudaEventRecord(c->ev[6], s));
     CK(cudaEventSynchronize(c->ev[6]));
     c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += (n_cur ? 2 : 0) + (n_prev ? 2 : 0) + (bound ? 2 : 0);
+    c->times.kernels_launched += 6;
     std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
       return x.h != y.h ? x.h < y.h : x.d < y.d;
     });
