@@ -273,6 +273,35 @@ class AdmissionIndex {
     return commit();
   }
 
+  // CostModel (serving_sim.hpp:25-57); CostModel::validate failures throw ConfigError
+  struct CostModel {
+    double t_base_ms = 10.0;
+    double c_prefill_ms = 1.0;
+    double tier_penalty_ms[3] = {0.0, 0.2, 0.5};  // HBM, DRAM, SSD
+    double noise_sigma_ms = 0.0;
+    uint64_t seed = 0;
+  };
+  void set_cost_model(const CostModel& m) {
+    skv_cost_model c{m.t_base_ms, m.c_prefill_ms, {m.tier_penalty_ms[0], m.tier_penalty_ms[1], m.tier_penalty_ms[2]},
+                     m.noise_sigma_ms, m.seed};
+    ok(skv_set_cost_model(ctx_, &c));
+  }
+  // Per request of the last admit: CostModel::ttft (serving_sim.hpp:50-56) and the
+  // reuse attribution of ServingSimulator::attribute_reuse (serving_sim.hpp:313-324).
+  struct Served {
+    std::vector<double> ttft_ms;
+    std::vector<uint32_t> intra_tokens, inter_tokens;
+  };
+  Served served(size_t n_requests, const std::vector<uint64_t>* request_ids = nullptr) {
+    Served s;
+    s.ttft_ms.resize(n_requests);
+    s.intra_tokens.resize(n_requests);
+    s.inter_tokens.resize(n_requests);
+    ok(skv_admit_ttft(ctx_, request_ids ? request_ids->data() : nullptr, s.ttft_ms.data(), s.intra_tokens.data(),
+                      s.inter_tokens.data(), 0));
+    return s;
+  }
+
   uint64_t entry_count() { return skv_entry_count(ctx_); }
   skv_ctx* handle() { return ctx_; }
 

@@ -212,6 +212,38 @@ int main() {
     }
     CHECK(hit);
   }
+  // test_serving_sim.cpp:36-67 (block-granular: public blocks of 8 tokens, HBM)
+  {
+    AdmissionIndex ix(&(const skv_config&)small_cfg(8));
+    ix.set_cost_model(AdmissionIndex::CostModel{});
+    TokenSeq text(96, 'q');
+    ix.admit({AdmissionIndex::Request{&text, UserId{1}}});
+    auto cold = ix.served(1);
+    CHECK(std::fabs(cold.ttft_ms[0] - 106.0) < 1e-12);  // t_base 10 + 1 ms * 96 (cold cache)
+    ix.commit();
+    ix.admit({AdmissionIndex::Request{&text, UserId{2}}});
+    auto hit = ix.served(1);
+    CHECK(std::fabs(hit.ttft_ms[0] - 10.0) < 1e-12);  // full public HBM hit: base time only
+    CHECK(hit.inter_tokens[0] == 96 && hit.intra_tokens[0] == 0);
+    ix.commit();
+    double prev = 1e18;
+    for (size_t matched = 8; matched <= 96; matched += 8) {  // strictly decreasing with the match
+      TokenSeq probe(text.begin(), text.begin() + matched);
+      probe.resize(96, '!');
+      ix.admit({AdmissionIndex::Request{&probe, UserId{100 + matched}}});
+      double t = ix.served(1).ttft_ms[0];
+      CHECK(t < prev);
+      prev = t;
+    }
+    // test_serving_sim.cpp:258-267 CostModel::validate
+    AdmissionIndex::CostModel broken;
+    broken.c_prefill_ms = 0.1;
+    CHECK(throws<ConfigError>([&] { ix.set_cost_model(broken); }));
+    AdmissionIndex::CostModel neg;
+    neg.tier_penalty_ms[1] = 0.9;
+    neg.tier_penalty_ms[2] = 0.5;
+    CHECK(throws<ConfigError>([&] { ix.set_cost_model(neg); }));
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
