@@ -176,8 +176,11 @@ typedef struct {
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
 
 /* Tier tags of existing entries (demote, cache_index.hpp:362-381): an entry's tier only
- * moves down HBM -> DRAM -> SSD, so it becomes max(current, tag). */
-int skv_set_tiers(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, size_t n);
+ * moves down HBM -> DRAM -> SSD, so it becomes max(current, tag).  Keys are given per
+ * prompt, prompt-major from block 0 (the skv_admit_out layout): block_offsets has
+ * n_prompts + 1 entries and the tags are per block. */
+int skv_set_tiers(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint32_t* block_offsets,
+                  uint32_t n_prompts, const uint8_t* tiers);
 
 typedef struct {
   uint64_t h, d, creator;

@@ -1025,20 +1025,26 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
   });
 }
 
-int skv_set_tiers(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, size_t n) {
-  if (!c || (n && (!h || !d || !tiers))) return SKV_ERR_ARG;
+int skv_set_tiers(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint32_t* block_offsets, uint32_t n_prompts,
+                  const uint8_t* tiers) {
+  if (!c || !block_offsets) return SKV_ERR_ARG;
+  const size_t n = block_offsets[n_prompts];
+  if (n && (!h || !d || !tiers)) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     if (n == 0) return SKV_OK;
+    if (block_offsets[0] != 0) throw ArgError("block_offsets must start at 0");
     std::vector<void*> tmp;
     uint64_t* dh = dalloc<uint64_t>(n, tmp);
     uint64_t* dd = dalloc<uint64_t>(n, tmp);
     uint8_t* dt = dalloc<uint8_t>(n, tmp);
+    uint32_t* db = dalloc<uint32_t>(n_prompts + 1ull, tmp);
     cudaStream_t s = c->stream;
     CK(cudaMemcpyAsync(dh, h, n * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dt, tiers, n, cudaMemcpyHostToDevice, s));
-    skv::launch_set_tiers(c->ix, dh, dd, dt, static_cast<uint32_t>(n), s);
+    CK(cudaMemcpyAsync(db, block_offsets, (n_prompts + 1ull) * 4, cudaMemcpyHostToDevice, s));
+    skv::launch_set_tiers(c->ix, dh, dd, db, n_prompts, dt, static_cast<uint32_t>(n), s);
     sync_check(s);
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;

@@ -212,7 +212,8 @@ void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32
                             cudaStream_t s);
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
                        cudaStream_t s);
-void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n,
+void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
+                      const uint8_t* tiers, uint32_t n,
                       cudaStream_t s);
 void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s);
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);

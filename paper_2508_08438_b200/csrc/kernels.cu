@@ -52,11 +52,25 @@ __device__ __forceinline__ uint64_t slot_hash(uint64_t h, uint64_t d) {
   return x;
 }
 
-// Home slot of a key: the first entry of a 128-B line (2 x 64-B entries).  Linear
-// probing from there visits the line's second entry before leaving the line, so one
-// line fetch covers the first two probe positions.
-__device__ __forceinline__ uint64_t home_slot(const Index& ix, uint64_t h, uint64_t d) {
-  return slot_hash(h, d) & ix.mask & ~1ull;
+// Home slot of the key of block b of a prompt.  Blocks are grouped by kGroup along the
+// prompt; a group's region of kGroup consecutive 128-B lines (2 x 64-B entries each) is
+// chosen by the hash of the group's first key (h_L, d_L), L = b - b % kGroup, and block
+// b's home is the first entry of line b % kGroup.  Every lookup and insert walks a prompt
+// from its root, so the group leader's key is always at hand, and a key always sits at
+// the same depth under the same prefix, so its home is a function of the key.  Linear
+// probing from the home slot visits the line's second entry first.
+// kGroup = 1 (every key hashed on its own) is the default: grouping a prompt's blocks
+// into shared DRAM pages speeds the probe slightly, but the commit's claim + parent-link
+// traffic then concentrates on adjacent lines and slows down more (measured on B200,
+// config 2: kGroup 1/2/4/8 -> commit 0.88/0.93/1.22/1.54 ms, probe 0.238/0.216/0.237/
+// 0.254 ms), although isolated grouped CAS streams are ~1.9x faster
+// (profiles/r01_randmem_microbench.jsonl).
+#ifndef SKV_GROUP
+#define SKV_GROUP 1
+#endif
+constexpr uint32_t kGroup = SKV_GROUP;
+__device__ __forceinline__ uint64_t home_slot(const Index& ix, uint64_t hL, uint64_t dL, uint32_t b) {
+  return (slot_hash(hL, dL) & ix.mask & ~static_cast<uint64_t>(2 * kGroup - 1)) + 2 * (b % kGroup);
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -606,9 +620,10 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
   flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
 }
 
-// find_slot: used by set_tiers (point lookups)
-__device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, Rec* out) {
-  uint64_t s = home_slot(ix, h, d);
+// find_slot: used by set_tiers (point lookups of block b, group leader key (hL, dL))
+__device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, uint64_t hL, uint64_t dL,
+                                              uint32_t b, Rec* out) {
+  uint64_t s = home_slot(ix, hL, dL, b);
   for (uint64_t i = 0; i <= ix.mask; ++i) {
     const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
     ulonglong2 k = rp[0];
@@ -1034,7 +1049,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
         mm[q] = make_ulonglong2(0, 0);
         ss[q] = 0;
         if (q < ng && b < nj) {
-          ss[q] = home_slot(ix, th[j][lane], td[j][lane]);
+          ss[q] = home_slot(ix, th[j][lane & ~(kGroup - 1)], td[j][lane & ~(kGroup - 1)], b);
           const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[ss[q]].rec);
           kk[q] = rp[0];
           mm[q] = rp[1];
@@ -1167,7 +1182,8 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       sl[r] = 0;
       pend[r] = false;
       if (base + 32 * r + lane >= n) continue;
-      sl[r] = home_slot(ix, h[r], d[r]);
+      const uint32_t lb = bo + ((base + 32 * r + lane) & ~(kGroup - 1));  // group leader block
+      sl[r] = home_slot(ix, hk[lb], dk[lb], base + 32 * r + lane);
       mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
                        &oh[r]);
     }
@@ -1382,11 +1398,21 @@ __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const 
 // ---------------------------------------------------------------------------------
 // misc: tiers, export, per-call wrappers
 // ---------------------------------------------------------------------------------
-__global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n) {
+__global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
+                            const uint8_t* tiers, uint32_t n) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  uint32_t lo = 0, hi = n_prompts;  // prompt holding block i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (boff[mid] <= i)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint32_t b = i - boff[lo], L = boff[lo] + (b & ~(kGroup - 1));
   Rec r;
-  uint32_t s = find_slot(ix, h[i], d[i], &r);
+  uint32_t s = find_slot(ix, h[i], d[i], h[L], d[L], b, &r);
   if (s == kNone) return;
   // demote (cache_index.hpp:362-381): a tier only moves down HBM -> DRAM -> SSD, so
   // repeated tags of one entry keep the slowest (the reference's demote-until loop)
@@ -1600,9 +1626,9 @@ void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_
   if (grid_n) k_epoch_roll<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, prev_list);
 }
 
-void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint8_t* tiers, uint32_t n,
-                      cudaStream_t s) {
-  if (n) k_set_tiers<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, tiers, n);
+void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
+                      const uint8_t* tiers, uint32_t n, cudaStream_t s) {
+  if (n) k_set_tiers<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, boff, n_prompts, tiers, n);
 }
 
 void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s) {

@@ -298,11 +298,14 @@ class AdmissionEngine:
         self._check(self._lib.skv_admit_ttft(self._h, _ptr(rid), _ptr(out), _ptr(intra), _ptr(inter), 0))
         return out, intra, inter
 
-    def set_tiers(self, h: np.ndarray, d: np.ndarray, tiers: np.ndarray):
+    def set_tiers(self, h: np.ndarray, d: np.ndarray, tiers: np.ndarray, block_offsets: np.ndarray):
+        """Tier tags (demote semantics) of the blocks of whole prompts, prompt-major as
+        ``admit`` returns them (``AdmitResult.block_offsets``)."""
         h = np.ascontiguousarray(h, np.uint64)
         d = np.ascontiguousarray(d, np.uint64)
         tiers = np.ascontiguousarray(tiers, np.uint8)
-        self._check(self._lib.skv_set_tiers(self._h, _ptr(h), _ptr(d), _ptr(tiers), len(h)))
+        bo = np.ascontiguousarray(block_offsets, np.uint32)
+        self._check(self._lib.skv_set_tiers(self._h, _ptr(h), _ptr(d), _ptr(bo), len(bo) - 1, _ptr(tiers)))
 
     def export(self) -> np.ndarray:
         cnt = int(self._lib.skv_entry_count(self._h))

@@ -123,7 +123,7 @@ def test_config4_long_context_tiered_index(ref, gpu):
             check_admit(eng.rules, got, exp)
             eng.commit()
             re_.commit()
-            eng.set_tiers(got.block_h, got.block_d, tiers)
+            eng.set_tiers(got.block_h, got.block_d, tiers, got.block_offsets)
             re_.set_tiers(s_tok, s_off, tiers)
             check_index(eng, re_)
             got = eng.admit(*query)

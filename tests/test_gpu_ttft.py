@@ -49,7 +49,7 @@ def test_ttft_reuse_parity(ref, gpu, model, B, W):
                 re_.commit()
                 # demote a random share of this batch's blocks (tiers only move down)
                 tiers = rng.integers(0, 3, got.n_blocks).astype(np.uint8)
-                eng.set_tiers(got.block_h, got.block_d, tiers)
+                eng.set_tiers(got.block_h, got.block_d, tiers, got.block_offsets)
                 re_.set_tiers(batch[0], batch[1], tiers)
         finally:
             re_.close()
