@@ -272,7 +272,7 @@ def run_ours(args):
         ext = torch.cuda.ExternalStream(eng.stream, device=dev)
         for k in range(warm):
             step_fn(eng, k, k + 1 if pipe and k + 1 < warm else None)
-        hs, launches = [], 0
+        hs, launches, per = [], 0, []
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if clocks:
@@ -285,6 +285,7 @@ def run_ours(args):
             hs.append(t["hash_scan_ms"])
             pf += t["prefetched"]
             launches += t["kernels_launched"]  # admit + commit + epoch kernels of this step
+            per.append(t)
         e1.record(ext)
         barrier()
         if clocks:
@@ -297,11 +298,13 @@ def run_ours(args):
             ms = float(x.item())
         last = eng.times()
         eng.close()
+        timed.per_step = per
         return ms, hs, launches, last, pf
 
     clocks = ClockSampler(gpu)
     ms_dev, hs, launches, last, pf_dev = timed(step_device, clocks)
     clk = clocks.stop()
+    per_dev = timed.per_step
     ms_e2e, _, _, _, pf_e2e = timed(step_host)
     hs_overlapped = float(np.mean(hs))
     if pipeline:
@@ -332,6 +335,29 @@ def run_ours(args):
             cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
                    "sample": f"{args.cpu_sample} prompts of config 2 (pool pre-inserted), 1 batch: "
                              f"{r['seconds']:.1f} s"}
+    # where the rest of the step goes: the commit is bound by random 128-bit CAS into the
+    # index (one claim per new block), measured against the randmem ceiling
+    cas_ceiling = None
+    rp = ROOT / "profiles" / "r01_randmem_microbench.jsonl"
+    if rp.exists():
+        rows = [json.loads(l) for l in rp.read_text().splitlines() if l.strip().startswith("{")]
+        cas = [r for r in rows if r.get("op") == "cas128"]
+        if cas:
+            cas_ceiling = max(cas, key=lambda r: r["table_mb"])["Gops"]
+    commit_ms = float(np.mean([t["commit_ms"] for t in per_dev]))
+    new_blocks = float(np.mean([t["new_blocks"] for t in per_dev]))
+    probe_ms = float(np.mean([t["chain_probe_ms"] for t in per_dev]))
+    claims = new_blocks / (commit_ms / 1e3) / 1e9 if commit_ms > 0 else None
+    breakdown = {
+        "commit_ms": round(commit_ms, 4), "new_blocks_per_step": new_blocks,
+        "commit_claims_gps": claims, "random_cas128_ceiling_gps": cas_ceiling,
+        "commit_frac_of_cas_ceiling": (claims / cas_ceiling) if (claims and cas_ceiling) else None,
+        "chain_probe_ms": round(probe_ms, 4),
+        "matched_blocks_per_step": float(np.mean([t["matched_total"] for t in per_dev])),
+        "epoch_ms": round(float(np.mean([t["epoch_ms"] for t in per_dev])), 4),
+        "note": "commit_ms includes the batch's monitor records (run inside k_commit); hash/scan of the next "
+                "batch overlaps it on a side stream",
+    }
     h2d = n_local * L * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
     d2h = blocks_per_batch + n_local * 4
     line = {
@@ -355,6 +381,7 @@ def run_ours(args):
                      "avg_launch_ms_overlapped": hs_overlapped},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "step_breakdown": breakdown,
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -155,6 +155,9 @@ struct skv_ctx {
   // monitor records of the last admit, executed inside the commit kernel (overlapping
   // the claims), or on their own when the batch is not committed
   bool rec_pending = false;
+  bool adm_lazy = false;  // the last admit's readbacks are pending (resolve_admit)
+  bool adm_use_pf = false;
+  uint32_t adm_launched = 0;
   skv::MonCtx rec_mon{};
   const uint64_t* rec_users = nullptr;
   uint32_t rec_n = 0;
@@ -668,6 +671,15 @@ void flush_record(skv_ctx* c) {
 }
 
 // ------------------------------------------------------------------ admission
+void resolve_admit(skv_ctx* c);
+
+// a lazily admitted batch's readbacks must have landed before the host looks at them
+void ensure_admit_resolved(skv_ctx* c) {
+  if (!c->adm_lazy) return;
+  sync_check(c->stream);
+  resolve_admit(c);
+}
+
 int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
@@ -676,6 +688,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const uint32_t B = c->cfg.block_tokens;
     if (N > c->max_prompts) throw ArgError("n_prompts exceeds max_prompts");
     if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
+    ensure_admit_resolved(c);
     flush_record(c);  // the previous batch was admitted but not committed
     if (N == 0) {
       if (out) out->n_blocks = 0, out->matched_total = 0;
@@ -784,18 +797,43 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       if (out->lowest_tier) CK(cudaMemcpyAsync(out->lowest_tier, c->tier, N, k, s));
       if (out->block_offsets) CK(cudaMemcpyAsync(out->block_offsets, c->blk_off, (N + 1) * 4ull, k, s));
     }
-    // the admit's one synchronisation: counters (errors, touched entries, matched
-    // total) and, for a device batch, the block count
+    // counters (errors, touched entries, matched total) and, for a device batch, the
+    // block count.  With outputs requested the admit synchronises here; a device batch
+    // admitted without outputs does not (the commit that follows is queued right behind
+    // it) and these are read with the commit's synchronisation (resolve_admit)
     CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 11 * 4, cudaMemcpyDeviceToHost, s));
     if (!nb_known && !out) CK(cudaMemcpyAsync(c->host_small + 20, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
+    c->adm_lazy = !out && b->on_device;
+    c->adm_use_pf = use_pf;
+    c->adm_launched = launched;
+    c->pending = true;
+    c->p_n = N;
+    c->p_blocks = nb_known ? n_blocks : nb_bound;  // exact after resolve_admit
+    c->p_users = users;
+    c->p_owners = owners;
+    c->last_n = N;
+    c->admitted_prompts += N;
+    if (c->adm_lazy) return SKV_OK;
     sync_check(s);
-    if (!nb_known && !out) n_blocks = c->host_small[20];
-    const uint32_t M = c->host_small[8 + 10];
+    resolve_admit(c);
+    if (!nb_known) n_blocks = c->p_blocks;
     if (out) {
       out->n_blocks = n_blocks;
-      out->matched_total = M;
+      out->matched_total = c->times.matched_total;
     }
-    if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
+    return SKV_OK;
+  });
+}
+
+// Host-side bookkeeping of the last admit once its readbacks have landed.
+void resolve_admit(skv_ctx* c) {
+  const uint32_t M = c->host_small[8 + 10];
+  if (c->adm_lazy) c->p_blocks = c->host_small[20];
+  c->adm_lazy = false;
+  if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
+  const bool use_pf = c->adm_use_pf;
+  const uint32_t launched = c->adm_launched;
+  {
     c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
     c->times.prefetched = use_pf ? 1 : 0;
     c->times.chain_probe_ms = elapsed(c->ev[2], c->ev[3]);
@@ -806,15 +844,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     c->times.replayed_entries = 0;
     c->times.touched_entries = c->host_small[8 + 1 + c->cur];
     c->times.kernels_launched = launched;
-    c->pending = true;
-    c->p_n = N;
-    c->p_blocks = n_blocks;
-    c->p_users = users;
-    c->p_owners = owners;
-    c->last_n = N;
-    c->admitted_prompts += N;
-    return SKV_OK;
-  });
+  }
 }
 
 // ------------------------------------------------------------------ serving observables
@@ -853,6 +883,7 @@ int skv_admit_ttft(skv_ctx* c, const uint64_t* request_ids, double* ttft_ms, uin
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
     const uint32_t N = c->last_n;
     if (N == 0) return SKV_OK;
     cudaStream_t s = c->stream;
@@ -960,6 +991,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
+    if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
     std::memcpy(&nn, c->host_small, 8);
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     if (rec) launched += replay_record(c, s, c->host_small[5], c->host_small[4]);
@@ -977,6 +1009,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
     flush_record(c);
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev[5], s));
@@ -1055,6 +1088,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
     flush_record(c);
     std::vector<void*> tmp;
     skv_entry* dout = dalloc<skv_entry>(std::max<uint64_t>(c->entries, 1), tmp);
@@ -1076,8 +1110,11 @@ uint64_t skv_entry_count(skv_ctx* c) { return c ? c->entries : 0; }
 
 int skv_last_times(skv_ctx* c, skv_stage_times* out) {
   if (!c || !out) return SKV_ERR_ARG;
-  *out = c->times;
-  return SKV_OK;
+  return guard(c, [&] {
+    ensure_admit_resolved(c);
+    *out = c->times;
+    return SKV_OK;
+  });
 }
 
 int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {

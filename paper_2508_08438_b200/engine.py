@@ -268,7 +268,9 @@ class AdmissionEngine:
     def epoch_pass(self, cap: int = 1 << 16) -> tuple[int, list[AnomalyEvent]]:
         """advance_epoch + ``EntropyMonitor::epoch_pass`` (monitor.hpp:85-99): returns the
         epoch number and the fired events sorted by entry key."""
-        buf = (N.Event * cap)()
+        buf = getattr(self, "_evbuf", None)
+        if buf is None or len(buf) < cap:  # one event buffer per engine (no per-call 3 MB allocation)
+            buf = self._evbuf = (N.Event * cap)()
         n = C.c_size_t()
         ep = C.c_uint64()
         self._check(self._lib.skv_epoch(self._h, buf, cap, C.byref(n), C.byref(ep)))
