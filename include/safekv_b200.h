@@ -175,6 +175,20 @@ typedef struct {
 /* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d). */
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
 
+/* Label landing.  With pending != 0, skv_commit stores new entries
+ * as PendingPrivate (visible to their creator only, like the reference's freshly inserted
+ * nodes, cache_index.hpp:196-198) instead of the rule-tier labels, and the caller lands
+ * the labels later, e.g. when an asynchronous detector finishes. */
+int skv_set_label_policy(skv_ctx* ctx, int pending);
+/* RadixCacheIndex::resolve_block (cache_index.hpp:321-343) per prompt: the classification
+ * block of prompt p is its blocks [first_block[p], n_p) (keys prompt-major from block 0,
+ * block_offsets as for skv_set_tiers), landed with labels[p]: Public labels every block of
+ * the span without propagation; Private / Restricted label the span's top block and every
+ * descendant.  Within one call, Public landings apply first, then Private, then
+ * Restricted (so overlapping private landings resolve to the stricter label). */
+int skv_resolve_blocks(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint32_t* block_offsets,
+                       uint32_t n_prompts, const uint32_t* first_block, const uint8_t* labels);
+
 /* Tier tags of existing entries (demote, cache_index.hpp:362-381): an entry's tier only
  * moves down HBM -> DRAM -> SSD, so it becomes max(current, tag).  Keys are given per
  * prompt, prompt-major from block 0 (the skv_admit_out layout): block_offsets has

@@ -244,6 +244,7 @@ struct RefEngine {
   };
   std::vector<Served> served;
   int nthreads = 1;
+  bool pending_labels = false;  // commit leaves new nodes PendingPrivate (insert's label)
 };
 
 void* ref_engine_create(void* rules, uint32_t B, uint32_t W, double jump, uint64_t u_pre_max) {
@@ -368,6 +369,40 @@ int ref_engine_ttft(void* ev, const uint64_t* request_ids, double t_base, double
   return 0;
 }
 
+void ref_engine_set_pending(void* ev, int pending) { static_cast<RefEngine*>(ev)->pending_labels = pending != 0; }
+
+// Label landing: RadixCacheIndex::resolve_block (cache_index.hpp:321-343) of each prompt's
+// span [first[p], n_p) with labels[p] (propagate = the label is private), in the batched
+// order of skv_resolve_blocks: all Public landings, then Private, then Restricted.
+int ref_engine_resolve(void* ev, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts, const uint32_t* first,
+                       const uint8_t* labels) {
+  auto* e = static_cast<RefEngine*>(ev);
+  const uint32_t B = e->B;
+  const uint8_t order[3] = {static_cast<uint8_t>(SensitivityLabel::Public),
+                            static_cast<uint8_t>(SensitivityLabel::Private),
+                            static_cast<uint8_t>(SensitivityLabel::Restricted)};
+  for (uint8_t want : order) {
+    for (uint32_t p = 0; p < n_prompts; ++p) {
+      if (labels[p] != want) continue;
+      const uint64_t n = (off[p + 1] - off[p]) / B;
+      if (first[p] >= n) continue;
+      TokenSeq ids;
+      for (uint64_t b = 0; b < n; ++b) {
+        std::vector<uint32_t> content(tok + off[p] + b * B, tok + off[p] + (b + 1) * B);
+        auto it = e->intern.find(content);
+        if (it == e->intern.end()) return -1;
+        ids.push_back(it->second);
+      }
+      NodeRef terminal = e->idx->find_node(ids);
+      if (!terminal) return -1;
+      const auto lab = static_cast<SensitivityLabel>(want);
+      const bool priv = lab != SensitivityLabel::Public;
+      e->idx->resolve_block(terminal, static_cast<uint32_t>(n - first[p]), lab, priv, priv ? 0 : 1);
+    }
+  }
+  return 0;
+}
+
 // Phase C (A.7): insert in prompt order, one node per block, labels applied per block.
 int ref_engine_commit(void* ev) {
   auto* e = static_cast<RefEngine*>(ev);
@@ -379,6 +414,7 @@ int ref_engine_commit(void* ev) {
     if (fresh == 0) continue;
     size_t k0 = n - fresh;
     for (size_t k = k0 + 1; k < n; ++k) e->idx->ensure_boundary(pd.ids, k);
+    if (e->pending_labels) continue;
     for (size_t b = k0; b < n; ++b) {
       TokenSeq pre(pd.ids.begin(), pd.ids.begin() + b + 1);
       NodeRef nd = e->idx->find_node(pre);

@@ -155,6 +155,7 @@ struct skv_ctx {
   // monitor records of the last admit, executed inside the commit kernel (overlapping
   // the claims), or on their own when the batch is not committed
   bool rec_pending = false;
+  bool pending_labels = false;  // skv_set_label_policy: new entries start PendingPrivate
   bool adm_lazy = false;  // the last admit's readbacks are pending (resolve_admit)
   bool adm_use_pf = false;
   uint32_t adm_launched = 0;
@@ -982,7 +983,8 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     const bool rec = c->rec_pending;  // the batch's monitor records ride along (see skv_admit)
     skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
-                       static_cast<int>(c->rec_grid), c->matched, c->rec_users, rec ? &c->rec_mon : nullptr, s);
+                       static_cast<int>(c->rec_grid), c->matched, c->rec_users, rec ? &c->rec_mon : nullptr,
+                       c->pending_labels ? 1 : 0, s);
     uint32_t launched = 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
     if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
@@ -1054,6 +1056,50 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
       for (size_t i = 0; i < ev.size() && i < cap; ++i) events[i] = ev[i];
     if (n_events) *n_events = ev.size();
     if (epoch_out) *epoch_out = epoch;
+    return SKV_OK;
+  });
+}
+
+int skv_set_label_policy(skv_ctx* c, int pending) {
+  if (!c) return SKV_ERR_ARG;
+  c->pending_labels = pending != 0;
+  return SKV_OK;
+}
+
+int skv_resolve_blocks(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint32_t* block_offsets,
+                       uint32_t n_prompts, const uint32_t* first_block, const uint8_t* labels) {
+  if (!c || !block_offsets || (n_prompts && (!first_block || !labels))) return SKV_ERR_ARG;
+  const size_t n = block_offsets[n_prompts];
+  if (n && (!h || !d)) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (n_prompts == 0) return SKV_OK;
+    if (block_offsets[0] != 0) throw ArgError("block_offsets must start at 0");
+    for (uint32_t p = 0; p < n_prompts; ++p) {
+      if (labels[p] != SKV_LABEL_PUBLIC && labels[p] != SKV_LABEL_PRIVATE && labels[p] != SKV_LABEL_RESTRICTED)
+        throw ArgError("resolve: labels must be Private, Public or Restricted");
+      if (first_block[p] > block_offsets[p + 1] - block_offsets[p]) throw ArgError("resolve: first_block past prompt");
+    }
+    ensure_admit_resolved(c);
+    std::vector<void*> tmp;
+    uint64_t* dh = dalloc<uint64_t>(std::max<size_t>(n, 1), tmp);
+    uint64_t* dd = dalloc<uint64_t>(std::max<size_t>(n, 1), tmp);
+    uint32_t* db = dalloc<uint32_t>(n_prompts + 1ull, tmp);
+    uint32_t* df = dalloc<uint32_t>(n_prompts, tmp);
+    uint8_t* dl = dalloc<uint8_t>(n_prompts, tmp);
+    uint32_t* miss = dalloc<uint32_t>(1, tmp);
+    cudaStream_t s = c->stream;
+    if (n) CK(cudaMemcpyAsync(dh, h, n * 8, cudaMemcpyHostToDevice, s));
+    if (n) CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(db, block_offsets, (n_prompts + 1ull) * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(df, first_block, n_prompts * 4ull, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dl, labels, n_prompts, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(miss, 0, 4, s));
+    skv::launch_resolve(c->ix, dh, dd, db, n_prompts, df, dl, static_cast<uint32_t>(n), miss, s);
+    CK(cudaMemcpyAsync(c->host_small + 24, miss, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    for (void* q : tmp) cudaFree(q);
+    if (c->host_small[24]) throw ArgError("resolve: a block of a classification span is not in the index");
     return SKV_OK;
   });
 }

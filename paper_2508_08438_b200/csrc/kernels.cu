@@ -1133,7 +1133,8 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
                                                 unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                                                 uint32_t fix_cap, uint32_t* err_flag,
                                                 const uint32_t* __restrict__ matched,
-                                                const uint64_t* __restrict__ users, MonCtx M, int with_record) {
+                                                const uint64_t* __restrict__ users, MonCtx M, int with_record,
+                                                int pending_labels) {
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
@@ -1247,7 +1248,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
         // creator + meta (with this prompt as the claimant) in one 8-B store, then the
         // parent slot; first_child is left alone (a duplicate claimant may already be
         // linking a child under this entry)
-        const uint32_t meta = make_meta(lab[r], owner, SKV_TIER_HBM, p);
+        const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owner, SKV_TIER_HBM, p);
         *reinterpret_cast<uint2*>(&e.rec.creator) = make_uint2(creator, meta);
         e.rec.parent = par[r];
         if (par[r] != kNone) sib[r] = atomicExch(&ix.e[par[r]].rec.first_child, s32[r]);
@@ -1290,13 +1291,14 @@ __global__ void k_commit_fixup_min(Index ix, const uint32_t* __restrict__ fix_li
 __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
                                const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
-                               uint32_t fix_cap) {
+                               uint32_t fix_cap, int pending_labels) {
   const uint32_t nf = min(*n_fix, fix_cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
     Rec& r = ix.e[s].rec;
     const uint32_t pw = meta_prompt(r.meta);
-    const uint32_t meta = make_meta(label[blk_off[pw] + b], owners ? owners[pw] : 0u, SKV_TIER_HBM, pw);
+    const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : label[blk_off[pw] + b],
+                                    owners ? owners[pw] : 0u, SKV_TIER_HBM, pw);
     *reinterpret_cast<uint2*>(&r.creator) = make_uint2(uidx[pw], meta);
   }
 }
@@ -1398,6 +1400,81 @@ __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const 
 // ---------------------------------------------------------------------------------
 // misc: tiers, export, per-call wrappers
 // ---------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------
+// Label landing (RadixCacheIndex::resolve_block, cache_index.hpp:321-343): the
+// classification block of prompt p is its blocks [first[p], n_p) (keys prompt-major from
+// block 0).  Public: every block of the chain, no propagation (promotion never
+// propagates, :657-662).  Private / Restricted: set_label on the chain's top block with
+// propagation to every descendant (:663-666, apply_label_subtree :679-686).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prompt_of(const uint32_t* boff, uint32_t n_prompts, uint32_t i) {
+  uint32_t lo = 0, hi = n_prompts;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (boff[mid] <= i)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void set_meta_label(Rec& r, uint32_t lab) {
+  uint32_t old = r.meta;
+  for (;;) {
+    const uint32_t nv = (old & ~3u) | lab;
+    if (nv == old) return;
+    const uint32_t got = atomicCAS(&r.meta, old, nv);
+    if (got == old) return;
+    old = got;
+  }
+}
+
+__global__ void k_resolve_public(Index ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff,
+                                 uint32_t n_prompts, const uint32_t* first, const uint8_t* labels, uint32_t n,
+                                 uint32_t* missing) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t p = prompt_of(boff, n_prompts, i);
+  const uint32_t b = i - boff[p];
+  if (labels[p] != SKV_LABEL_PUBLIC || b < first[p]) return;
+  const uint32_t L = boff[p] + (b & ~(kGroup - 1));
+  Rec r;
+  const uint32_t s = find_slot(ix, h[i], d[i], h[L], d[L], b, &r);
+  if (s == kNone) {
+    atomicAdd(missing, 1u);
+    return;
+  }
+  set_meta_label(ix.e[s].rec, SKV_LABEL_PUBLIC);
+}
+
+__global__ void k_resolve_private(Index ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff,
+                                  uint32_t n_prompts, const uint32_t* first, const uint8_t* labels, uint32_t lab,
+                                  uint32_t* missing) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_prompts || labels[p] != lab || boff[p] + first[p] >= boff[p + 1]) return;
+  const uint32_t b = first[p], i = boff[p] + b, L = boff[p] + (b & ~(kGroup - 1));
+  Rec r;
+  const uint32_t root = find_slot(ix, h[i], d[i], h[L], d[L], b, &r);
+  if (root == kNone) {
+    atomicAdd(missing, 1u);
+    return;
+  }
+  set_meta_label(ix.e[root].rec, lab);
+  uint32_t cur = ix.e[root].rec.first_child;
+  while (cur != kNone) {
+    set_meta_label(ix.e[cur].rec, lab);
+    const uint32_t c = ix.e[cur].rec.first_child;
+    if (c != kNone) {
+      cur = c;
+      continue;
+    }
+    while (cur != root && ix.e[cur].aux.next_sibling == kNone) cur = ix.e[cur].rec.parent;
+    if (cur == root) break;
+    cur = ix.e[cur].aux.next_sibling;
+  }
+}
+
 __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                             const uint8_t* tiers, uint32_t n) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1589,15 +1666,17 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    const uint32_t* exist, const uint8_t* label, const uint32_t* users, const uint8_t* owners,
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
-                   const uint64_t* users64, const MonCtx* mon, cudaStream_t s) {
+                   const uint64_t* users64, const MonCtx* mon, int pending_labels, cudaStream_t s) {
   const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
   k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag,
-                                                                    matched, users64, M, mon ? 1 : 0);
+                                                                    matched, users64, M, mon ? 1 : 0,
+                                                                    pending_labels);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
-  k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap);
+  k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
+                                          pending_labels);
 }
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
@@ -1624,6 +1703,17 @@ void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
                        cudaStream_t s) {
   if (grid_n) k_epoch_roll<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, prev_list);
+}
+
+void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
+                    const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s) {
+  if (!n_prompts) return;
+  if (n) k_resolve_public<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, boff, n_prompts, first, labels, n, missing);
+  // severity order: Private landings, then Restricted (a Restricted ancestor wins an overlap)
+  k_resolve_private<<<cdiv(n_prompts, 128), 128, 0, s>>>(ix, h, d, boff, n_prompts, first, labels,
+                                                          SKV_LABEL_PRIVATE, missing);
+  k_resolve_private<<<cdiv(n_prompts, 128), 128, 0, s>>>(ix, h, d, boff, n_prompts, first, labels,
+                                                          SKV_LABEL_RESTRICTED, missing);
 }
 
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,

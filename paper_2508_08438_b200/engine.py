@@ -300,6 +300,23 @@ class AdmissionEngine:
         self._check(self._lib.skv_admit_ttft(self._h, _ptr(rid), _ptr(out), _ptr(intra), _ptr(inter), 0))
         return out, intra, inter
 
+    def set_label_policy(self, pending: bool) -> None:
+        """New entries start PendingPrivate until their labels are landed (resolve_blocks)."""
+        self._check(self._lib.skv_set_label_policy(self._h, 1 if pending else 0))
+
+    def resolve_blocks(self, h: np.ndarray, d: np.ndarray, block_offsets: np.ndarray, first_block: np.ndarray,
+                       labels: np.ndarray) -> None:
+        """``RadixCacheIndex::resolve_block`` (cache_index.hpp:321-343) of each prompt's
+        classification span [first_block, n) with its label (Public: no propagation;
+        Private/Restricted: span top + descendants)."""
+        h = np.ascontiguousarray(h, np.uint64)
+        d = np.ascontiguousarray(d, np.uint64)
+        bo = np.ascontiguousarray(block_offsets, np.uint32)
+        fb = np.ascontiguousarray(first_block, np.uint32)
+        lab = np.ascontiguousarray(labels, np.uint8)
+        self._check(self._lib.skv_resolve_blocks(self._h, _ptr(h), _ptr(d), _ptr(bo), len(bo) - 1, _ptr(fb),
+                                                 _ptr(lab)))
+
     def set_tiers(self, h: np.ndarray, d: np.ndarray, tiers: np.ndarray, block_offsets: np.ndarray):
         """Tier tags (demote semantics) of the blocks of whole prompts, prompt-major as
         ``admit`` returns them (``AdmitResult.block_offsets``)."""

@@ -157,6 +157,9 @@ SIGNATURES = {
     "skv_commit": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "skv_epoch": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t),
                             C.POINTER(C.c_uint64)]),
+    "skv_set_label_policy": (C.c_int, [C.c_void_p, C.c_int]),
+    "skv_resolve_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                     C.c_void_p]),
     "skv_set_tiers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_export": (C.c_int, [C.c_void_p, C.POINTER(Entry), C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_entry_count": (C.c_uint64, [C.c_void_p]),

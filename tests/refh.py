@@ -48,6 +48,8 @@ def load_ref():
         "ref_engine_admit": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp, vp, vp, vp, vp, vp]),
         "ref_engine_commit": (C.c_int, [vp]),
         "ref_engine_set_tiers": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
+        "ref_engine_set_pending": (None, [vp, C.c_int]),
+        "ref_engine_resolve": (C.c_int, [vp, vp, vp, C.c_uint32, vp, vp]),
         "ref_engine_ttft": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                       C.c_uint64, vp, vp, vp]),
         "ref_engine_epoch": (C.c_int, [vp, u64p, sz, vp, vp, vp, vp, vp, vp, C.POINTER(sz)]),
@@ -124,6 +126,16 @@ class RefEngine:
 
     def commit(self):
         assert self.L.ref_engine_commit(self.h) == 0
+
+    def set_pending(self, pending: bool):
+        self.L.ref_engine_set_pending(self.h, 1 if pending else 0)
+
+    def resolve(self, tokens, offsets, first_block, labels):
+        tokens = np.ascontiguousarray(tokens, np.uint32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        fb = np.ascontiguousarray(first_block, np.uint32)
+        lab = np.ascontiguousarray(labels, np.uint8)
+        assert self.L.ref_engine_resolve(self.h, _p(tokens), _p(offsets), len(offsets) - 1, _p(fb), _p(lab)) == 0
 
     def ttft(self, n, model, request_ids=None):
         """CostModel::ttft + attribute_reuse of the last admit (model: dict of skv_cost_model fields)."""
