@@ -774,7 +774,10 @@ __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* 
 // dependent loads in flight together.  Fast path (the common case once an entry's set
 // exists): the user already sits at its home position of the set table -> nothing but
 // the hit count changes.  Everything else takes the full record_user path.
-constexpr int kRecRounds = 4;
+#ifndef SKV_KRECROUNDS
+#define SKV_KRECROUNDS 1
+#endif
+constexpr int kRecRounds = SKV_KRECROUNDS;
 
 __device__ __forceinline__ void record_prompt(const Index& ix, const MonCtx& M, const uint32_t* __restrict__ slot_in,
                                               uint32_t bo, uint32_t m, uint64_t u, uint32_t lane) {
@@ -954,9 +957,18 @@ __global__ void __launch_bounds__(256) k_record_replay(Index ix, MonCtx M, const
 //      or creator == user, cache_index.hpp:483-485) and the first missing block (k,
 //      where the commit starts).  Probing stops at the tile holding the first miss.
 // ---------------------------------------------------------------------------------
-constexpr int kCPWarps = 2;     // warps per CTA (8.4 KB of SMEM tiles each)
-constexpr int kCPPrompts = 16;  // prompts per warp: 4096 warps for config 2 (latency-bound chain + probes)
-constexpr int kCPInFlight = 8;  // prompts whose probe loads are in flight together
+#ifndef SKV_KCPWARPS
+#define SKV_KCPWARPS 2
+#endif
+constexpr int kCPWarps = SKV_KCPWARPS;     // warps per CTA (8.4 KB of SMEM tiles each)
+#ifndef SKV_KCPPROMPTS
+#define SKV_KCPPROMPTS 16
+#endif
+constexpr int kCPPrompts = SKV_KCPPROMPTS;  // prompts per warp: 4096 warps for config 2 (latency-bound chain + probes)
+#ifndef SKV_KCPINFLIGHT
+#define SKV_KCPINFLIGHT 8
+#endif
+constexpr int kCPInFlight = SKV_KCPINFLIGHT;  // prompts whose probe loads are in flight together
 constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
 
 struct Probe {

@@ -24,6 +24,7 @@ with AdmissionEngine(cfg) as eng:
     for k in range(8):
         eng.admit_raw(b)
         eng.commit()
+        eng.epoch_pass()
         res.append(eng.times()["hash_scan_ms"])
     print("hash_scan_ms", [round(x, 4) for x in res])
     res = []
@@ -31,5 +32,6 @@ with AdmissionEngine(cfg) as eng:
         eng.prefetch_raw(b)
         eng.admit_raw(b)
         eng.commit()
+        eng.epoch_pass()
         res.append(eng.times()["hash_scan_ms"])
     print("prefetched hash_scan_ms", [round(x, 4) for x in res])
