@@ -193,7 +193,16 @@ def run_ours(args):
     steps, warm = args.steps, args.warmup
     n_batches = steps + warm
     blocks_per_batch = n_local * (L // B)
-    cap = 1 << max(20, int(np.ceil(np.log2((n_batches + 1) * blocks_per_batch * 1.7))))
+    # index sized for HBM: load factor <= ~1/6 after the run (34 GB at the default run
+    # length), so linear probing almost never leaves the home slot; ranks sharing a device
+    # split half of its memory, never below load 0.6
+    need = (n_batches + 1) * blocks_per_batch
+    ranks_per_dev = -(-world // max(torch.cuda.device_count(), 1))
+    budget = torch.cuda.get_device_properties(gpu).total_memory // 2 // ranks_per_dev // 64
+    cap = 1 << max(20, min(int(np.ceil(np.log2(need * 6))), int(np.floor(np.log2(max(budget, 1))))),
+                   int(np.ceil(np.log2(need * 1.7))))
+    if args.index_log2:
+        cap = 1 << args.index_log2
     ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
                         max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 18,
                         device=gpu)
@@ -367,7 +376,9 @@ def run_ours(args):
         "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
                                f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
                    "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
-                   "step": "admit + commit + epoch", "parallelism": (f"prefix-forest partitioned x{world} (skv_route; no data-path collective)"
+                   "step": "admit + commit + epoch",
+                   "index": f"{cap} slots x 64 B ({cap * 64 / 2**30:.0f} GiB), load {need / cap:.2f} at run end",
+                   "parallelism": (f"prefix-forest partitioned x{world} (skv_route; no data-path collective)"
                                    if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
                                 f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
@@ -401,6 +412,7 @@ def main():
     ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
     args = ap.parse_args()
     if args.impl == "reference":

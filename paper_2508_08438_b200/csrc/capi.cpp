@@ -139,7 +139,7 @@ struct skv_ctx {
   uint64_t admitted_prompts = 0;  // request ids of the last batch default to [admitted_prompts - N, ...)
   uint32_t last_n = 0;            // prompts of the last skv_admit
   unsigned long long *keys_a = nullptr, *keys_b = nullptr;  // ordered-replay access keys
-  uint32_t* fix_list = nullptr;  // commit: duplicate-key slots, depths, prompts (3 x max_blocks)
+  uint32_t* fix_list = nullptr;  // commit: duplicate-key slots, depths, prompts, late children (4 x max_blocks)
   skv::UserTable users_tab{};     // interned UserIds (Rec::creator)
   uint32_t* uidx = nullptr;       // interned user of every prompt of the last admit
   void* temp = nullptr;
@@ -549,7 +549,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->d_reqid = dalloc<uint64_t>(N, c->owned);
     c->keys_a = dalloc<unsigned long long>(NB, c->owned);
     c->keys_b = dalloc<unsigned long long>(NB, c->owned);
-    c->fix_list = dalloc<uint32_t>(3 * NB, c->owned);
+    c->fix_list = dalloc<uint32_t>(4 * NB, c->owned);
     c->uidx = dalloc<uint32_t>(N, c->owned);
     {  // user table: 2x slots, keys = kNoUser, idx = 0, index 0 reserved for UserId ~0
       uint32_t slots = 1;

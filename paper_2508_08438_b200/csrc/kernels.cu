@@ -677,6 +677,34 @@ __device__ __forceinline__ ulonglong2 ld_relaxed128(const ulonglong2* p) {
   return v;
 }
 
+// Two independent 128-bit claims (compare with empty = 0) issued back to back in one asm
+// block: the results are copied out only after both are in flight (separate asm
+// statements let the register allocator place a copy of the first result -- a wait on
+// its DRAM round trip -- before the second CAS).  Predicated off -> old = all ones.
+__device__ __forceinline__ void cas128_empty_x2(unsigned long long* a0, unsigned long long* a1, bool p0, bool p1,
+                                                unsigned long long n0l, unsigned long long n0h,
+                                                unsigned long long n1l, unsigned long long n1h,
+                                                unsigned long long* o0l, unsigned long long* o0h,
+                                                unsigned long long* o1l, unsigned long long* o1h) {
+  asm volatile(
+      "{\n\t.reg .pred q0, q1;\n\t.reg .b128 z, d0, d1, n0, n1;\n\t"
+      "setp.ne.u32 q0, %4, 0;\n\t"
+      "setp.ne.u32 q1, %5, 0;\n\t"
+      "mov.b128 z, {0, 0};\n\t"
+      "mov.b128 d0, {-1, -1};\n\t"
+      "mov.b128 d1, {-1, -1};\n\t"
+      "mov.b128 n0, {%6, %7};\n\t"
+      "mov.b128 n1, {%8, %9};\n\t"
+      "@q0 atom.global.cas.b128 d0, [%10], z, n0;\n\t"
+      "@q1 atom.global.cas.b128 d1, [%11], z, n1;\n\t"
+      "mov.b128 {%0, %1}, d0;\n\t"
+      "mov.b128 {%2, %3}, d1;\n\t}"
+      : "=l"(*o0l), "=l"(*o0h), "=l"(*o1l), "=l"(*o1h)
+      : "r"(static_cast<uint32_t>(p0)), "r"(static_cast<uint32_t>(p1)), "l"(n0l), "l"(n0h), "l"(n1l), "l"(n1h),
+        "l"(a0), "l"(a1)
+      : "memory");
+}
+
 __device__ __forceinline__ bool cas128_dev(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val, ulonglong2* old) {
   return cas128(reinterpret_cast<unsigned long long*>(addr), cmp.x, cmp.y, val.x, val.y, &old->x, &old->y);
 }
@@ -1153,12 +1181,16 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
   const uint32_t lane = lane_id();
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) {
+#ifndef SKV_EXP_NOREC
     if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+#endif
     return;
   }
   const uint32_t creator = uidx[p];
   const uint32_t owner = owners ? owners[p] : 0u;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
+  bool carry_mine = false;     // previous block's key claimed by this prompt (first new block: old parent)
+  uint32_t carry_fix = kNone;  // previous block's duplicate fix-up entry, if it was a duplicate
   uint32_t inserted = 0;
   // sibling links of the previous round set, applied once the next set's claims are in
   // flight (the exchange results are not waited for on the critical path)
@@ -1177,6 +1209,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       s32[r] = kNone;
       mine[r] = false;
       lab[r] = 0;
+      h[r] = d[r] = 0;
       if (b < n) {
         h[r] = hk[bo + b];
         d[r] = dk[bo + b];
@@ -1190,23 +1223,39 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
     uint64_t sl[R];
     unsigned long long ol[R], oh[R];
     bool pend[R];
+    // every round's home slot first (group leader = lane rounded down to kGroup, same
+    // round), then the CASes back to back: no load between two claims, so the compiler
+    // cannot place a wait for the first claim's result before the second is issued
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      sl[r] = 0;
+      const uint64_t hL = __shfl_sync(kFull, h[r], lane & ~(kGroup - 1));
+      const uint64_t dL = __shfl_sync(kFull, d[r], lane & ~(kGroup - 1));
+      sl[r] = home_slot(ix, hL, dL, base + 32 * r + lane);
       pend[r] = false;
-      if (base + 32 * r + lane >= n) continue;
-      const uint32_t lb = bo + ((base + 32 * r + lane) & ~(kGroup - 1));  // group leader block
-      sl[r] = home_slot(ix, hk[lb], dk[lb], base + 32 * r + lane);
-      mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
-                       &oh[r]);
     }
+    if constexpr (R == 2) {
+      cas128_empty_x2(reinterpret_cast<unsigned long long*>(&ix.e[sl[0]].rec),
+                      reinterpret_cast<unsigned long long*>(&ix.e[sl[1]].rec), base + lane < n, base + 32 + lane < n,
+                      h[0], d[0], h[1], d[1], &ol[0], &oh[0], &ol[1], &oh[1]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ol[r] = oh[r] = ~0ull;
+        if (base + 32 * r + lane < n)
+          cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r], &oh[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) mine[r] = (ol[r] | oh[r]) == 0ull;
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
     // the batch's monitor records (AccessStats::record of the matched blocks, which
     // precede block k0) run while the first claims are in flight: L2 atomics overlap the
     // claims' DRAM round trips (record and commit touch disjoint fields)
+#ifndef SKV_EXP_NOREC
     if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+#endif
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
@@ -1244,26 +1293,59 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
     }
     // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
+    bool pmine[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       par[r] = __shfl_up_sync(kFull, s32[r], 1);
-      if (lane == 0) par[r] = carry;
+      pmine[r] = __shfl_up_sync(kFull, mine[r], 1);
+      if (lane == 0) par[r] = carry, pmine[r] = carry_mine;
       carry = __shfl_sync(kFull, s32[r], 31);
+      carry_mine = __shfl_sync(kFull, mine[r], 31);
     }
-    uint32_t sib[R];
+    // this prompt's own child of each block, when this prompt claimed it and it is in
+    // this iteration (lane + 1, or the next round's lane 0); the last lane of the last
+    // round links its child from the next iteration by a plain store instead
+    uint32_t own_child[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t cs = __shfl_down_sync(kFull, s32[r], 1);
+      const bool cm = __shfl_down_sync(kFull, mine[r], 1);
+      uint32_t ns = kNone;
+      bool nm = false;
+      if (r + 1 < R) {
+        ns = __shfl_sync(kFull, s32[r + 1 < R ? r + 1 : r], 0);
+        nm = __shfl_sync(kFull, mine[r + 1 < R ? r + 1 : r], 0);
+      }
+      own_child[r] = lane < 31 ? (cm ? cs : kNone) : (nm ? ns : kNone);
+    }
+    uint32_t sib[R], fidx[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       sib[r] = kNone;
+      fidx[r] = kNone;
       if (s32[r] == kNone) continue;
       Entry& e = ix.e[s32[r]];
+#ifdef SKV_EXP_NOPAY
+      if (mine[r]) { ++inserted; continue; }
+#endif
       if (mine[r]) {
-        // creator + meta (with this prompt as the claimant) in one 8-B store, then the
-        // parent slot; first_child is left alone (a duplicate claimant may already be
-        // linking a child under this entry)
+        // creator, meta (with this prompt as the claimant), parent and this prompt's own
+        // child in ONE 16-B store: no other child is linked under a fresh entry inside
+        // this kernel (other prompts' children of it are duplicate claimants' and are
+        // linked by the fix-up pass)
         const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owner, SKV_TIER_HBM, p);
-        *reinterpret_cast<uint2*>(&e.rec.creator) = make_uint2(creator, meta);
-        e.rec.parent = par[r];
-        if (par[r] != kNone) sib[r] = atomicExch(&ix.e[par[r]].rec.first_child, s32[r]);
+        *reinterpret_cast<uint4*>(&e.rec.creator) = make_uint4(creator, meta, par[r], own_child[r]);
+        // the parent link: under a parent that existed before the batch children race ->
+        // exchange; under a parent this prompt claimed, the parent's own 16-B store wrote
+        // the link, except across iterations (plain store); under a parent another
+        // prompt claimed -> linked by the fix-up pass
+        if (par[r] != kNone) {
+          const uint32_t b = base + 32 * r + lane;
+          if (b == k0)
+            sib[r] = atomicExch(&ix.e[par[r]].rec.first_child, s32[r]);
+          else if (pmine[r] && lane == 0 && r == 0)
+            ix.e[par[r]].rec.first_child = s32[r];
+        }
         ++inserted;
       } else {
         const uint32_t f = atomicAdd(n_fix, 1u);
@@ -1271,10 +1353,21 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
           fix_list[f] = s32[r];
           fix_list[fix_cap + f] = base + 32 * r + lane;  // block depth of this key
           fix_list[2 * fix_cap + f] = p;
+          fix_list[3 * fix_cap + f] = kNone;  // this prompt's child under the duplicate, if it claimed one
+          fidx[r] = f;
         } else {
           atomicOr(err_flag, 4u);
         }
       }
+    }
+    __syncwarp();
+    // a claimed block under a duplicate parent: hand the link to the parent's fix-up entry
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t pf = __shfl_up_sync(kFull, fidx[r], 1);
+      if (lane == 0) pf = carry_fix;
+      carry_fix = __shfl_sync(kFull, fidx[r], 31);
+      if (mine[r] && pf != kNone) fix_list[3 * fix_cap + pf] = s32[r];
     }
     // a child chained in front of existing siblings (branching only: under a fresh
     // parent the exchange returns kNone, which is the init value) -- deferred
@@ -1312,6 +1405,12 @@ __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, c
     const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : label[blk_off[pw] + b],
                                     owners ? owners[pw] : 0u, SKV_TIER_HBM, pw);
     *reinterpret_cast<uint2*>(&r.creator) = make_uint2(uidx[pw], meta);
+    // the duplicate claimant's own child under this entry (k_commit left it unlinked)
+    const uint32_t c = fix_list[3 * fix_cap + i];
+    if (c != kNone) {
+      const uint32_t sib = atomicExch(&r.first_child, c);
+      if (sib != kNone) ix.e[c].aux.next_sibling = sib;
+    }
   }
 }
 
