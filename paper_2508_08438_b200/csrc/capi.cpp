@@ -126,6 +126,7 @@ struct skv_ctx {
   uint64_t* bd = nullptr;
   uint32_t* bmask = nullptr;
   uint8_t* blabel = nullptr;
+  uint8_t* bown = nullptr;  // commit: 1 iff this block's claim inserted its key
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
   uint8_t* bmeta = nullptr;    // per matched block: tier | creator == user << 2 (TTFT epilogue)
@@ -146,6 +147,7 @@ struct skv_ctx {
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
   int hs_grid = 0;
+  int n_sm = 148;
   uint32_t hs_smem = 0;
   skv::HSLayout hs_layout{};
   uint32_t rec_grid = 0;
@@ -488,6 +490,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     CK(cudaGetDeviceProperties(&prop, c->device));
     if (prop.major != 10)
       throw CudaError("device " + std::string(prop.name) + " is not sm_100 (built for sm_100a only)");
+    c->n_sm = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->pf_done, cudaEventDisableTiming));
@@ -538,6 +541,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->alt_bd = dalloc<uint64_t>(NB, c->owned);
     c->alt_bmask = dalloc<uint32_t>(NB, c->owned);
     c->blabel = dalloc<uint8_t>(NB, c->owned);
+    c->bown = dalloc<uint8_t>(NB, c->owned);
     c->bdecision = dalloc<uint8_t>(NB, c->owned);
     c->bslot = dalloc<uint32_t>(NB, c->owned);
     c->bmeta = dalloc<uint8_t>(NB, c->owned);
@@ -984,8 +988,8 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users, rec ? &c->rec_mon : nullptr,
-                       c->pending_labels ? 1 : 0, s);
-    uint32_t launched = 3;  // k_commit, k_commit_fixup_min, k_commit_fixup
+                       c->pending_labels ? 1 : 0, c->bown, c->p_blocks, c->n_sm, s);
+    uint32_t launched = 4;  // k_claim, k_commit, k_commit_fixup_min, k_commit_fixup
     if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;

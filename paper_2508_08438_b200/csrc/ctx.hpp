@@ -201,7 +201,8 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    const uint32_t* exist, const uint8_t* label, const uint32_t* uidx, const uint8_t* owners,
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
-                   const uint64_t* users64, const MonCtx* mon, int pending_labels, cudaStream_t s);
+                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint8_t* own, uint64_t n_blocks,
+                   int n_sm, cudaStream_t s);
 void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                     const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,

@@ -300,12 +300,17 @@ __device__ __forceinline__ uint32_t exact_tokens(const uint8_t* __restrict__ tab
   return m;
 }
 
+#ifndef SKV_QCAP
+#define SKV_QCAP 64
+#endif
+constexpr uint32_t kQCap = SKV_QCAP;  // deferred tasks per warp (multiple of 32)
+
 __device__ __forceinline__ void flush_tasks(const SegTask* q, uint32_t qn, uint32_t lane, const uint8_t* tab,
                                             const uint8_t* cmap, const uint16_t* acc_tab, uint32_t inv,
                                             const HashScanArgs& a) {
   __syncwarp();
-  if (lane < qn) {
-    const SegTask t = q[lane];
+  for (uint32_t k = lane; k < qn; k += 32) {
+    const SegTask t = q[k];
     const uint32_t m = exact_tokens(tab, cmap, acc_tab, inv, a.tokens, t.tok, t.meta >> 16, t.meta & 0xffffu);
     if (m) {
       atomicOr(&a.mask_out[t.gb], m);
@@ -330,9 +335,24 @@ __device__ __forceinline__ uint32_t run_tokens(const uint8_t* __restrict__ tab, 
 }
 
 // FNV-1a step of a byte token: (h ^ t) * P^4 mod 2^64 in four 32-bit multiplies
+#ifndef SKV_FNV4
+#define SKV_FNV4 0
+#endif
 __device__ __forceinline__ uint64_t fnv_tok(uint64_t h, uint32_t t) {
   const uint32_t lo = static_cast<uint32_t>(h) ^ t, hi = static_cast<uint32_t>(h >> 32);
   uint32_t rlo, rhi;
+#if SKV_FNV4
+  // lo * P_lo as one wide multiply (no zeroed addend register), then the two cross terms
+  // into the high word: XOR + IMAD.WIDE + 2 IMAD per token
+  asm("{\n\t.reg .u64 w;\n\t.reg .u32 wh;\n\t"
+      "mul.wide.u32 w, %2, %4;\n\t"
+      "mov.b64 {%0, wh}, w;\n\t"
+      "mad.lo.u32 wh, %2, %5, wh;\n\t"
+      "mad.lo.u32 %1, %3, %4, wh;\n\t}"
+      : "=r"(rlo), "=r"(rhi)
+      : "r"(lo), "r"(hi), "r"(static_cast<uint32_t>(kFnvP4)), "r"(static_cast<uint32_t>(kFnvP4 >> 32)));
+  return (static_cast<uint64_t>(rhi) << 32) | rlo;
+#endif
   asm("{\n\t.reg .u32 c;\n\t"
       "mul.lo.u32 c, %2, %4;\n\t"
       "mad.lo.u32 c, %3, %5, c;\n\t"
@@ -363,13 +383,16 @@ __device__ __forceinline__ void ldg_tokens16(const uint32_t* p, uint32_t (&t)[16
 #ifndef SKV_HS_MINB
 #define SKV_HS_MINB 2
 #endif
+#ifndef SKV_HS_L1PF
+#define SKV_HS_L1PF 1
+#endif
 __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashScanArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   // row offsets index the DFA image [row_base, fast_bytes), which sits at sm[0..)
   const uint8_t* tab = sm - a.rules.row_base;
   uint16_t* acc_tab = reinterpret_cast<uint16_t*>(sm + a.off_list);
   __shared__ uint8_t cmap[256];
-  __shared__ SegTask s_q[kHSWarps][32];
+  __shared__ SegTask s_q[kHSWarps][kQCap];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   {  // DFA rows and accepting copies [row_base, fast_bytes) -> SMEM
     const uint32_t n = (a.rules.fast_bytes - a.rules.row_base + 15) / 16;
@@ -525,6 +548,15 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
       }
       if (out) a.d_out[gb] = dg;
     }
+#if SKV_HS_L1PF
+    // the next chunk's new token lines into L1 while this chunk computes: its windows
+    // start nout blocks on, so lane l touches block (nout + l) of the contiguous token
+    // stream (one 64-B segment per lane; exact within a prompt, harmless past its end)
+    {
+      const uint64_t nt = T0 + static_cast<uint64_t>(nout + lane) * B;
+      if (nt < a.n_tokens) asm volatile("prefetch.global.L1 [%0];" ::"l"(tokens + nt));
+    }
+#endif
     // ---- phase B: [ws+B, min(we, ws+B+W')), shared with window l+1 once the runs meet
     const uint32_t nZ = __shfl_down_sync(kFull, Z | ((amid & kAccRegion) << 1), 1);
     const uint32_t nSW = __shfl_down_sync(kFull, SW, 1);
@@ -567,36 +599,39 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
       if (me) atomicMin(&a.first_sens[p], b);
       f = ((A & kAccRegion) ? 1u : 0u) | (Cf ? 2u : 0u) | ((C2 & kAccRegion) ? 4u : 0u);
     }
-    // ---- exact rule masks of the flagged segments
+    // ---- exact rule masks of the flagged segments (segment s of a window: 0 = block,
+    // 1 = phase B, 2 = phase C).  Deferred: every flagged segment gets a queue slot
+    // (rank = exclusive prefix of the per-lane counts, one pass); the queue runs 32
+    // tasks per lane-pass once full.  In place: segments longer than 16 tokens, or a
+    // chunk with more flagged segments than the queue holds.
     if (__any_sync(kFull, f != 0)) {
-      __syncwarp();
-      for (uint32_t s = 0; s < 3; ++s) {
-        const uint32_t ms = __ballot_sync(kFull, (f >> s) & 1u);
-        if (!ms) continue;
-        const bool mine = (ms >> lane) & 1u;
+      const uint32_t cnt = __popc(f);
+      const uint32_t c0 = __ballot_sync(kFull, cnt & 1u), c1 = __ballot_sync(kFull, cnt >> 1);
+      const uint32_t tot = __popc(c0) + 2 * __popc(c1);
+      const bool queue = defer && tot <= kQCap;
+      if (queue && qn + tot > kQCap) {
+        flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
+        qn = 0;
+      }
+      const uint32_t lt = (1u << lane) - 1u;
+      uint32_t k = qn + __popc(c0 & lt) + 2 * __popc(c1 & lt);
+      for (uint32_t ff = f; ff; ff &= ff - 1) {
+        const uint32_t sg = __ffs(ff) - 1;
         uint32_t o, e, row;
-        if (s == 0) {
+        if (sg == 0) {
           o = ws, e = ws + B, row = start_row;
-        } else if (s == 1) {
+        } else if (sg == 1) {
           o = sb, e = eb, row = X;
         } else {
           o = sc, e = we, row = Y;
         }
-        if (defer) {  // queue: slot = qn + rank among this round's tasks; run 32 at a time
-          const uint32_t n = __popc(ms);
-          if (qn + n > 32) {
-            flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
-            qn = 0;
-          }
-          if (mine) {
-            SegTask t;
-            t.tok = T0 + o;
-            t.meta = row | ((e - o) << 16);
-            t.gb = gb, t.p = p, t.b = b, t.pad = 0;
-            q[qn + __popc(ms & ((1u << lane) - 1u))] = t;
-          }
-          qn += n;
-        } else if (mine) {  // in place (segments longer than 16 tokens)
+        if (queue) {
+          SegTask t;
+          t.tok = T0 + o;
+          t.meta = row | ((e - o) << 16);
+          t.gb = gb, t.p = p, t.b = b, t.pad = 0;
+          q[k++] = t;
+        } else {
           uint32_t m = 0;
           for (; o < e; ++o) {
             row = lds16(tab, row + cmap[tk0[o] & 0xffu]);
@@ -608,6 +643,7 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
           }
         }
       }
+      if (queue) qn += tot;
     }
     // ---- next chunk
     g += nout;
@@ -1064,6 +1100,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
       if (b < nj) {
         hk[bj + b] = th[j][lane];
         label[bj + b] = b >= fsj ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
+        slot_out[bj + b] = kNone;  // missing before the batch unless the probe below finds it
       }
     }
     uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
@@ -1145,6 +1182,97 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 // K6: commit (insert the new blocks of the batch).
 // ---------------------------------------------------------------------------------
 
+// Claims, flat over the batch's blocks (no prompt structure needed): every block the
+// probe did not find (slot = kNone) CASes its key into its home slot; kClaimQ blocks per
+// thread with their CASes in flight together (one asm block, so no result is waited for
+// before the last claim is issued); rare: the slot holds another key or the CAS lost
+// a race -> linear probing.  Output: the block's slot and whether this block's CAS
+// inserted the key (own = 1) or found it inserted by another prompt of the batch (0).
+constexpr int kClaimQ = 4;
+static_assert(kGroup == 1, "flat claims hash every key on its own");
+
+__device__ __forceinline__ void cas128_empty_x4(const uint64_t* sl, const bool* act, const uint64_t* h,
+                                                const uint64_t* d, Entry* e, unsigned long long* ol,
+                                                unsigned long long* oh) {
+  asm volatile(
+      "{\n\t.reg .pred q0, q1, q2, q3;\n\t.reg .b128 z, d0, d1, d2, d3, n0, n1, n2, n3;\n\t"
+      "setp.ne.u32 q0, %8, 0;\n\tsetp.ne.u32 q1, %9, 0;\n\tsetp.ne.u32 q2, %10, 0;\n\tsetp.ne.u32 q3, %11, 0;\n\t"
+      "mov.b128 z, {0, 0};\n\t"
+      "mov.b128 d0, {-1, -1};\n\tmov.b128 d1, {-1, -1};\n\tmov.b128 d2, {-1, -1};\n\tmov.b128 d3, {-1, -1};\n\t"
+      "mov.b128 n0, {%12, %13};\n\tmov.b128 n1, {%14, %15};\n\tmov.b128 n2, {%16, %17};\n\tmov.b128 n3, {%18, %19};\n\t"
+      "@q0 atom.global.cas.b128 d0, [%20], z, n0;\n\t"
+      "@q1 atom.global.cas.b128 d1, [%21], z, n1;\n\t"
+      "@q2 atom.global.cas.b128 d2, [%22], z, n2;\n\t"
+      "@q3 atom.global.cas.b128 d3, [%23], z, n3;\n\t"
+      "mov.b128 {%0, %1}, d0;\n\tmov.b128 {%2, %3}, d1;\n\tmov.b128 {%4, %5}, d2;\n\tmov.b128 {%6, %7}, d3;\n\t}"
+      : "=l"(ol[0]), "=l"(oh[0]), "=l"(ol[1]), "=l"(oh[1]), "=l"(ol[2]), "=l"(oh[2]), "=l"(ol[3]), "=l"(oh[3])
+      : "r"(static_cast<uint32_t>(act[0])), "r"(static_cast<uint32_t>(act[1])), "r"(static_cast<uint32_t>(act[2])),
+        "r"(static_cast<uint32_t>(act[3])), "l"(h[0]), "l"(d[0]), "l"(h[1]), "l"(d[1]), "l"(h[2]), "l"(d[2]),
+        "l"(h[3]), "l"(d[3]), "l"(&e[sl[0]].rec), "l"(&e[sl[1]].rec), "l"(&e[sl[2]].rec), "l"(&e[sl[3]].rec)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restrict__ hk,
+                                               const uint64_t* __restrict__ dk, uint32_t* __restrict__ slot_io,
+                                               uint8_t* __restrict__ own, const uint32_t* __restrict__ blk_off,
+                                               uint32_t n_prompts, uint32_t* err_flag) {
+  const uint64_t nb = blk_off[n_prompts];  // exact block count (the host may only hold a bound)
+  const uint64_t nthr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < nb;
+       i0 += nthr * kClaimQ) {
+    uint64_t h[kClaimQ], d[kClaimQ], sl[kClaimQ];
+    bool act[kClaimQ], pend[kClaimQ];
+    unsigned long long ol[kClaimQ], oh[kClaimQ];
+#pragma unroll
+    for (int q = 0; q < kClaimQ; ++q) {
+      const uint64_t i = i0 + q * nthr;
+      act[q] = i < nb && slot_io[i] == kNone;
+      h[q] = d[q] = 0;
+      sl[q] = 0;
+      if (act[q]) {
+        h[q] = hk[i];
+        d[q] = dk[i];
+        sl[q] = home_slot(ix, h[q], d[q], 0);
+      }
+    }
+    cas128_empty_x4(sl, act, h, d, ix.e, ol, oh);
+#pragma unroll
+    for (int q = 0; q < kClaimQ; ++q) pend[q] = act[q] && (ol[q] | oh[q]) != 0ull && !(ol[q] == h[q] && oh[q] == d[q]);
+    bool mine[kClaimQ];
+#pragma unroll
+    for (int q = 0; q < kClaimQ; ++q) mine[q] = act[q] && (ol[q] | oh[q]) == 0ull;
+    for (uint64_t k = 1;; ++k) {
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < kClaimQ; ++q) any |= pend[q];
+      if (!any) break;
+      if (k > ix.mask) {  // table full
+        atomicOr(err_flag, 2u);
+#pragma unroll
+        for (int q = 0; q < kClaimQ; ++q)
+          if (pend[q]) pend[q] = false, sl[q] = ~0ull;
+        break;
+      }
+#pragma unroll
+      for (int q = 0; q < kClaimQ; ++q)
+        if (pend[q]) {
+          sl[q] = (sl[q] + 1) & ix.mask;
+          mine[q] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[q]].rec), 0ull, 0ull, h[q], d[q], &ol[q],
+                           &oh[q]);
+          pend[q] = !mine[q] && !(ol[q] == h[q] && oh[q] == d[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kClaimQ; ++q) {
+      const uint64_t i = i0 + q * nthr;
+      if (!act[q]) continue;
+      slot_io[i] = sl[q] == ~0ull ? kNone : static_cast<uint32_t>(sl[q]);
+      own[i] = mine[q] ? 1 : 0;
+    }
+  }
+}
+
+
 // Commit (A.7).  Lanes of the warp of prompt p walk its new blocks b >= k_p (k_p = the
 // first block missing before the batch, from k_chain_probe):
 //   * CAS the key into its slot.  The inserting thread writes ITS payload (creator,
@@ -1163,9 +1291,15 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 #ifndef SKV_COMMIT_ROUNDS
 #define SKV_COMMIT_ROUNDS 2
 #endif
+#ifndef SKV_FLAT_CLAIM
+#define SKV_FLAT_CLAIM 0
+#endif
 constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 
-__global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __restrict__ hk,
+#ifndef SKV_COMMIT_MINB
+#define SKV_COMMIT_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SKV_COMMIT_MINB) k_commit(Index ix, const uint64_t* __restrict__ hk,
                                                 const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
                                                 const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
@@ -1174,7 +1308,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
                                                 uint32_t fix_cap, uint32_t* err_flag,
                                                 const uint32_t* __restrict__ matched,
                                                 const uint64_t* __restrict__ users, MonCtx M, int with_record,
-                                                int pending_labels) {
+                                                int pending_labels, const uint8_t* __restrict__ own) {
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
@@ -1220,6 +1354,7 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
     // together (one DRAM round trip; the CAS returns the resident key, so no separate
     // load is needed); rare: the slot holds another key or the CAS lost a race -> linear
     // probing with CAS, every pending round's next CAS again in flight together.
+#if !SKV_FLAT_CLAIM
     uint64_t sl[R];
     unsigned long long ol[R], oh[R];
     bool pend[R];
@@ -1233,7 +1368,12 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       sl[r] = home_slot(ix, hL, dL, base + 32 * r + lane);
       pend[r] = false;
     }
-    if constexpr (R == 2) {
+    if constexpr (R == kClaimQ) {
+      bool act[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) act[r] = base + 32 * r + lane < n;
+      cas128_empty_x4(sl, act, h, d, ix.e, ol, oh);
+    } else if constexpr (R == 2) {
       cas128_empty_x2(reinterpret_cast<unsigned long long*>(&ix.e[sl[0]].rec),
                       reinterpret_cast<unsigned long long*>(&ix.e[sl[1]].rec), base + lane < n, base + 32 + lane < n,
                       h[0], d[0], h[1], d[1], &ol[0], &oh[0], &ol[1], &oh[1]);
@@ -1291,6 +1431,23 @@ __global__ void __launch_bounds__(256) k_commit(Index ix, const uint64_t* __rest
       s32[r] = static_cast<uint32_t>(sl[r]);
       slot_out[bo + base + 32 * r + lane] = s32[r];
     }
+#else
+    // claims done by k_claim: this block's slot and whether its CAS inserted the key
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t b = base + 32 * r + lane;
+      if (b < n) {
+        s32[r] = slot_out[bo + b];
+        mine[r] = own[bo + b] != 0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
+#ifndef SKV_EXP_NOREC
+    if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+#endif
+#endif
     // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
     bool pmine[R];
@@ -1777,14 +1934,20 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    const uint32_t* exist, const uint8_t* label, const uint32_t* users, const uint8_t* owners,
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
-                   const uint64_t* users64, const MonCtx* mon, int pending_labels, cudaStream_t s) {
+                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint8_t* own, uint64_t n_blocks,
+                   int n_sm, cudaStream_t s) {
   const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
+#if SKV_FLAT_CLAIM
+  if (n_blocks)
+    k_claim<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n_blocks, 256 * kClaimQ), 8ull * n_sm)), 256, 0, s>>>(
+        ix, h, d, slot, own, blk_off, n, err_flag);
+#endif
   k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag,
                                                                     matched, users64, M, mon ? 1 : 0,
-                                                                    pending_labels);
+                                                                    pending_labels, own);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
                                           pending_labels);
