@@ -380,11 +380,39 @@ __device__ __forceinline__ void ldg_tokens16(const uint32_t* p, uint32_t (&t)[16
   }
 }
 
+#ifndef SKV_HS_PFCTX
+#define SKV_HS_PFCTX 0
+#endif
+#ifndef SKV_HS_PFDIST
+#define SKV_HS_PFDIST 1  // bit 0: next chunk, bit 1: the chunk after
+#endif
+// The next chunk's new token lines into L1 while this chunk computes: its windows start
+// nout blocks on, so lane l touches block (nout + l) of the contiguous token stream (one
+// 64-B segment per lane; exact within a prompt, harmless past its end); with
+// SKV_HS_PFCTX the right-context blocks past the chunk too.
+__device__ __forceinline__ void l1_prefetch_next(const uint32_t* tokens, uint64_t n_tokens, uint64_t T0,
+                                                 uint32_t nout, uint32_t lane, uint32_t B, uint32_t W) {
+#if SKV_HS_PFDIST & 1
+  const uint64_t nt = T0 + static_cast<uint64_t>(nout + lane) * B;
+  if (nt < n_tokens) asm volatile("prefetch.global.L1 [%0];" ::"l"(tokens + nt));
+#endif
+#if SKV_HS_PFDIST & 2
+  const uint64_t nt2 = T0 + static_cast<uint64_t>(2 * nout + lane) * B;
+  if (nt2 < n_tokens) asm volatile("prefetch.global.L1 [%0];" ::"l"(tokens + nt2));
+#endif
+#if SKV_HS_PFCTX
+  if (lane * B < W) {
+    const uint64_t ct = T0 + static_cast<uint64_t>(nout + 32 + lane) * B;
+    if (ct < n_tokens) asm volatile("prefetch.global.L1 [%0];" ::"l"(tokens + ct));
+  }
+#endif
+}
+
 #ifndef SKV_HS_MINB
 #define SKV_HS_MINB 2
 #endif
 #ifndef SKV_HS_L1PF
-#define SKV_HS_L1PF 1
+#define SKV_HS_L1PF 2  // 1: before phase B, 2: before phase A
 #endif
 __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashScanArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -394,35 +422,50 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
   __shared__ uint8_t cmap[256];
   __shared__ SegTask s_q[kHSWarps][kQCap];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
-  {  // DFA rows and accepting copies [row_base, fast_bytes) -> SMEM
-    const uint32_t n = (a.rules.fast_bytes - a.rules.row_base + 15) / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(a.rules.fast) + a.rules.row_base / 16;
-    uint4* dst = reinterpret_cast<uint4*>(sm);
-    for (uint32_t i = tid; i < n; i += blockDim.x) dst[i] = src[i];
-    if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
-    for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
+  // start-up: the DFA image loads, this warp's block range and the prompt search are
+  // all in flight before the first barrier
+  const uint32_t n_img = (a.rules.fast_bytes - a.rules.row_base + 15) / 16;
+  const uint4* img_src = reinterpret_cast<const uint4*>(a.rules.fast) + a.rules.row_base / 16;
+  uint4 img[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t i = tid + k * blockDim.x;
+    if (i < n_img) img[k] = img_src[i];
   }
-  __syncthreads();
-  SegTask* q = s_q[wid];
   const uint32_t* __restrict__ tokens = a.tokens;
   const uint32_t inv = a.rules.copy_inv;
   const uint32_t N = a.n_prompts;
   const uint32_t nb = a.blk_off[N];  // device-side block count (no host round trip)
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nwarps + wid, TW = static_cast<uint64_t>(gridDim.x) * nwarps;
   const uint32_t G0 = static_cast<uint32_t>(gw * nb / TW), G1 = static_cast<uint32_t>((gw + 1) * nb / TW);
-  if (G0 >= G1) return;
   uint32_t pp = 0;
-  {  // prompt containing G0
+  if (G0 < G1) {  // prompt containing G0 (the last with blk_off <= G0): 32-ary search, one
+                  // load per lane per round (4 dependent rounds for 65,536 prompts, not 16)
     uint32_t lo = 0, hi = N;
     while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (a.blk_off[mid] <= G0)
-        lo = mid;
-      else
-        hi = mid;
+      const uint32_t step = (hi - lo + 31) / 32;
+      const uint32_t m = lo + lane * step;
+      const uint32_t bal = __ballot_sync(kFull, m < hi && a.blk_off[m] <= G0);  // a prefix of the lanes
+      const uint32_t k = 31 - __clz(bal);
+      lo += k * step;
+      hi = min(hi, lo + step);
     }
     pp = lo;
   }
+  {  // DFA rows and accepting copies [row_base, fast_bytes) -> SMEM
+    uint4* dst = reinterpret_cast<uint4*>(sm);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = tid + k * blockDim.x;
+      if (i < n_img) dst[i] = img[k];
+    }
+    for (uint32_t i = tid + 4 * blockDim.x; i < n_img; i += blockDim.x) dst[i] = img_src[i];
+    if (tid < 64) reinterpret_cast<uint32_t*>(cmap)[tid] = reinterpret_cast<const uint32_t*>(a.rules.class2)[tid];
+    for (uint32_t i = tid; i < a.rules.n_copies; i += blockDim.x) acc_tab[i] = a.rules.copy_acc[i];
+  }
+  __syncthreads();
+  SegTask* q = s_q[wid];
+  if (G0 >= G1) return;
   uint32_t g = G0, qn = 0;
   const uint32_t B = a.B, W = a.W;
   const uint32_t Wp = min(W, B), kc = min(kConv, Wp);
@@ -485,6 +528,9 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
     const uint32_t we = min(r_i1, ws + B + W);
     const bool act = lane < nw, out = lane < nout;
     const bool nbr = lane + 1 < nw && !((bm >> (lane + 1)) & 1u);  // block b+1: same prompt, this chunk
+#if SKV_HS_L1PF == 2
+    l1_prefetch_next(tokens, a.n_tokens, T0, nout, lane, B, W);
+#endif
     // ---- phase A: the block's tokens, digest, DFA over the block from the start state
     uint32_t A = 0, X = 0, Z = 0, SW = 0, amid = 0, cw0 = 0;
     if (act) {
@@ -548,14 +594,8 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
       }
       if (out) a.d_out[gb] = dg;
     }
-#if SKV_HS_L1PF
-    // the next chunk's new token lines into L1 while this chunk computes: its windows
-    // start nout blocks on, so lane l touches block (nout + l) of the contiguous token
-    // stream (one 64-B segment per lane; exact within a prompt, harmless past its end)
-    {
-      const uint64_t nt = T0 + static_cast<uint64_t>(nout + lane) * B;
-      if (nt < a.n_tokens) asm volatile("prefetch.global.L1 [%0];" ::"l"(tokens + nt));
-    }
+#if SKV_HS_L1PF == 1
+    l1_prefetch_next(tokens, a.n_tokens, T0, nout, lane, B, W);
 #endif
     // ---- phase B: [ws+B, min(we, ws+B+W')), shared with window l+1 once the runs meet
     const uint32_t nZ = __shfl_down_sync(kFull, Z | ((amid & kAccRegion) << 1), 1);
