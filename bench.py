@@ -36,6 +36,7 @@ CFG2 = dict(n_prompts=65536, prompt_tokens=2048, block_tokens=16, window_tokens=
             pool_size=256, pool_tokens=640, pii_per_kib=1.0, seed=1)
 METRIC = "KV blocks admitted/sec (hash+scan+lookup+monitor) and % HBM roofline, 1/2/4/8 B200"
 UNIT = "blocks/s"
+CPU_STEPS = 6
 
 
 def peaks():
@@ -339,11 +340,14 @@ def run_ours(args):
             traffic = None
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        r = cpu_reference_run(steps=1, warmup=0, sample_prompts=args.cpu_sample, threads=os.cpu_count() or 1)
+        # a bounded sample (~10 s of CPU work): CPU_STEPS timed batches of --cpu-sample
+        # prompts after one warm-up batch, same generator, pool pre-inserted
+        r = cpu_reference_run(steps=CPU_STEPS, warmup=1, sample_prompts=args.cpu_sample,
+                              threads=os.cpu_count() or 1)
         if r is not None:
             cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"{args.cpu_sample} prompts of config 2 (pool pre-inserted), 1 batch: "
-                             f"{r['seconds']:.1f} s"}
+                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of config 2 after 1 warm-up batch "
+                             f"(pool pre-inserted): {r['blocks']} blocks in {r['seconds']:.1f} s"}
     # where the rest of the step goes: the commit is bound by random 128-bit CAS into the
     # index (one claim per new block), measured against the randmem ceiling
     cas_ceiling = None
@@ -410,7 +414,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
-    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")

@@ -336,7 +336,7 @@ __device__ __forceinline__ uint32_t run_tokens(const uint8_t* __restrict__ tab, 
 
 // FNV-1a step of a byte token: (h ^ t) * P^4 mod 2^64 in four 32-bit multiplies
 #ifndef SKV_FNV4
-#define SKV_FNV4 0
+#define SKV_FNV4 1
 #endif
 __device__ __forceinline__ uint64_t fnv_tok(uint64_t h, uint32_t t) {
   const uint32_t lo = static_cast<uint32_t>(h) ^ t, hi = static_cast<uint32_t>(h >> 32);
