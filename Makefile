@@ -49,6 +49,7 @@ clean:
 variant: $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o
 	mkdir -p variants/$(V)
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/kernels.cu -o variants/$(V)/kernels.o 2> variants/$(V)/ptxas.log || (cat variants/$(V)/ptxas.log; exit 1)
-	$(NVCC) $(ARCH) -shared -o variants/$(V)/libsafekv_b200.so variants/$(V)/kernels.o $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o -lcudart_static -lpthread -ldl -lrt
+	g++ $(CXXFLAGS) $(VFLAGS) -c $(SRC)/capi.cpp -o variants/$(V)/capi.o
+	$(NVCC) $(ARCH) -shared -o variants/$(V)/libsafekv_b200.so variants/$(V)/kernels.o variants/$(V)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o -lcudart_static -lpthread -ldl -lrt
 
 .PHONY: variant

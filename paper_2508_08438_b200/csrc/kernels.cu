@@ -1339,7 +1339,11 @@ constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 #ifndef SKV_COMMIT_MINB
 #define SKV_COMMIT_MINB 1
 #endif
-__global__ void __launch_bounds__(256, SKV_COMMIT_MINB) k_commit(Index ix, const uint64_t* __restrict__ hk,
+#ifndef SKV_COMMIT_MINB_NOREC
+#define SKV_COMMIT_MINB_NOREC 1
+#endif
+template <bool kRec>  // kRec: the batch's monitor records ride along (else k_record runs beside it)
+__global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_NOREC) k_commit(Index ix, const uint64_t* __restrict__ hk,
                                                 const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
                                                 const uint32_t* __restrict__ exist, const uint8_t* __restrict__ label,
                                                 const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
@@ -1355,9 +1359,8 @@ __global__ void __launch_bounds__(256, SKV_COMMIT_MINB) k_commit(Index ix, const
   const uint32_t lane = lane_id();
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) {
-#ifndef SKV_EXP_NOREC
-    if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
-#endif
+    if constexpr (kRec)
+      if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
     return;
   }
   const uint32_t creator = uidx[p];
@@ -1433,9 +1436,8 @@ __global__ void __launch_bounds__(256, SKV_COMMIT_MINB) k_commit(Index ix, const
     // the batch's monitor records (AccessStats::record of the matched blocks, which
     // precede block k0) run while the first claims are in flight: L2 atomics overlap the
     // claims' DRAM round trips (record and commit touch disjoint fields)
-#ifndef SKV_EXP_NOREC
-    if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
-#endif
+    if constexpr (kRec)
+      if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
@@ -1484,9 +1486,8 @@ __global__ void __launch_bounds__(256, SKV_COMMIT_MINB) k_commit(Index ix, const
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
-#ifndef SKV_EXP_NOREC
-    if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
-#endif
+    if constexpr (kRec)
+      if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
 #endif
     // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
@@ -1983,7 +1984,8 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
     k_claim<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n_blocks, 256 * kClaimQ), 8ull * n_sm)), 256, 0, s>>>(
         ix, h, d, slot, own, blk_off, n, err_flag);
 #endif
-  k_commit<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
+  auto* kern = mon ? k_commit<true> : k_commit<false>;
+  kern<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag,
                                                                     matched, users64, M, mon ? 1 : 0,
