@@ -20,9 +20,6 @@ struct skv_rules {
   skv::DfaTables dfa;
 };
 
-#ifndef SKV_FLAT_CLAIM
-#define SKV_FLAT_CLAIM 0
-#endif
 #ifndef SKV_REC_BESIDE
 #define SKV_REC_BESIDE 0  // measured: 0.82 ms beside vs 0.72 fused (DESIGN 5.3)
 #endif
@@ -134,7 +131,8 @@ struct skv_ctx {
   uint64_t* bd = nullptr;
   uint32_t* bmask = nullptr;
   uint8_t* blabel = nullptr;
-  uint8_t* bown = nullptr;  // commit: 1 iff this block's claim inserted its key
+  uint32_t* bprompt = nullptr;  // block -> prompt (written by the probe, read by the flat commit)
+  uint32_t* late = nullptr;     // commit: (child slot, parent block) links applied after the claims
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
   uint8_t* bmeta = nullptr;    // per matched block: tier | creator == user << 2 (TTFT epilogue)
@@ -554,7 +552,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->alt_bd = dalloc<uint64_t>(NB, c->owned);
     c->alt_bmask = dalloc<uint32_t>(NB, c->owned);
     c->blabel = dalloc<uint8_t>(NB, c->owned);
-    c->bown = dalloc<uint8_t>(NB, c->owned);
+    c->bprompt = dalloc<uint32_t>(NB, c->owned);
+    c->late = dalloc<uint32_t>(2 * NB, c->owned);
     c->bdecision = dalloc<uint8_t>(NB, c->owned);
     c->bslot = dalloc<uint32_t>(NB, c->owned);
     c->bmeta = dalloc<uint8_t>(NB, c->owned);
@@ -797,7 +796,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
     skv::launch_intern_users(c->users_tab, users, N, c->uidx, c->counters + 5, s);
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
-                            c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, s);
+                            c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt, s);
     CK(cudaEventRecord(c->ev[3], s));
     // stage 4: the monitor records (AccessStats::record of every matched block, in
     // prompt order) run inside the commit kernel, overlapping the claims' DRAM round
@@ -1000,7 +999,8 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       throw CapacityError("index capacity exhausted (eviction is not part of this path)");
     CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
-    CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));  // intra-batch duplicate fix-up count
+    CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
+    CK(cudaMemsetAsync(c->counters + 11, 0, 4, s));  // late child links
     ++c->batch_id;
     const bool rec = c->rec_pending;  // the batch's monitor records (see skv_admit)
     // The records (sector 1 of the matched entries, the window user sets) and the inserts
@@ -1016,10 +1016,10 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users,
-                       rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->bown,
-                       c->p_blocks, c->n_sm, s);
+                       rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
+                       c->n_sm, c->bprompt, c->late, c->counters + 11, s);
     if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
-    uint32_t launched = 3 + (SKV_FLAT_CLAIM ? 1 : 0) + (rec && kRecordBeside ? 1 : 0);
+    uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
     if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;

@@ -183,7 +183,7 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, cudaStream_t s);
+                        const MonCtx& mon, uint32_t* bprompt, cudaStream_t s);
 void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
                    const uint32_t* matched, const uint64_t* users, uint32_t n_prompts, cudaStream_t s);
 void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,
@@ -201,8 +201,8 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    const uint32_t* exist, const uint8_t* label, const uint32_t* uidx, const uint8_t* owners,
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
-                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint8_t* own, uint64_t n_blocks,
-                   int n_sm, cudaStream_t s);
+                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, cudaStream_t s);
 void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                     const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,

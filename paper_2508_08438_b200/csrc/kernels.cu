@@ -7,7 +7,7 @@
 //   k_probe       RadixCacheIndex::match_prefix / visible / lowest_tier
 //                 (cache_index.hpp:213-237, 483-485) over the flat index (A.5)
 //   k_record      AccessStats::record (access_stats.hpp:27-37) -- exact, order-preserving
-//   k_claim/k_commit  RadixCacheIndex::insert first-creator-wins + resolve_block (A.7)
+//   k_commit          RadixCacheIndex::insert first-creator-wins + resolve_block (A.7)
 //   k_epoch_*     EntropyMonitor::epoch_pass / check_anomaly (monitor.hpp:56-99),
 //                 set_label propagation (cache_index.hpp:654-685), AccessStats::roll
 // No tensor cores: nothing here is a contraction.  Everything is integer/byte work
@@ -65,6 +65,9 @@ __device__ __forceinline__ uint64_t slot_hash(uint64_t h, uint64_t d) {
 // config 2: kGroup 1/2/4/8 -> commit 0.88/0.93/1.22/1.54 ms, probe 0.238/0.216/0.237/
 // 0.254 ms), although isolated grouped CAS streams are ~1.9x faster
 // (profiles/r01_randmem_microbench.jsonl).
+#ifndef SKV_COMMIT_FLAT
+#define SKV_COMMIT_FLAT 0  // measured slower (DESIGN 5.3); kept as the documented alternative
+#endif
 #ifndef SKV_GROUP
 #define SKV_GROUP 1
 #endif
@@ -1100,7 +1103,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
     const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
-    uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon) {
+    uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon, uint32_t* __restrict__ bprompt) {
   __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
   __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -1141,6 +1144,9 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
         hk[bj + b] = th[j][lane];
         label[bj + b] = b >= fsj ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
         slot_out[bj + b] = kNone;  // missing before the batch unless the probe below finds it
+#if SKV_COMMIT_FLAT
+        bprompt[bj + b] = p0 + j;  // block -> prompt, for the flat commit
+#endif
       }
     }
     uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
@@ -1222,14 +1228,10 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
 // K6: commit (insert the new blocks of the batch).
 // ---------------------------------------------------------------------------------
 
-// Claims, flat over the batch's blocks (no prompt structure needed): every block the
-// probe did not find (slot = kNone) CASes its key into its home slot; kClaimQ blocks per
-// thread with their CASes in flight together (one asm block, so no result is waited for
-// before the last claim is issued); rare: the slot holds another key or the CAS lost
-// a race -> linear probing.  Output: the block's slot and whether this block's CAS
-// inserted the key (own = 1) or found it inserted by another prompt of the batch (0).
+// Four independent 128-bit claims (compare with empty = 0) in one asm block, for 4
+// rounds of claims in flight (SKV_COMMIT_ROUNDS=4); see cas128_empty_x2.
 constexpr int kClaimQ = 4;
-static_assert(kGroup == 1, "flat claims hash every key on its own");
+static_assert(kGroup == 1 || !SKV_COMMIT_FLAT, "the flat commit hashes every key on its own");
 
 __device__ __forceinline__ void cas128_empty_x4(const uint64_t* sl, const bool* act, const uint64_t* h,
                                                 const uint64_t* d, Entry* e, unsigned long long* ol,
@@ -1252,65 +1254,6 @@ __device__ __forceinline__ void cas128_empty_x4(const uint64_t* sl, const bool* 
       : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restrict__ hk,
-                                               const uint64_t* __restrict__ dk, uint32_t* __restrict__ slot_io,
-                                               uint8_t* __restrict__ own, const uint32_t* __restrict__ blk_off,
-                                               uint32_t n_prompts, uint32_t* err_flag) {
-  const uint64_t nb = blk_off[n_prompts];  // exact block count (the host may only hold a bound)
-  const uint64_t nthr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < nb;
-       i0 += nthr * kClaimQ) {
-    uint64_t h[kClaimQ], d[kClaimQ], sl[kClaimQ];
-    bool act[kClaimQ], pend[kClaimQ];
-    unsigned long long ol[kClaimQ], oh[kClaimQ];
-#pragma unroll
-    for (int q = 0; q < kClaimQ; ++q) {
-      const uint64_t i = i0 + q * nthr;
-      act[q] = i < nb && slot_io[i] == kNone;
-      h[q] = d[q] = 0;
-      sl[q] = 0;
-      if (act[q]) {
-        h[q] = hk[i];
-        d[q] = dk[i];
-        sl[q] = home_slot(ix, h[q], d[q], 0);
-      }
-    }
-    cas128_empty_x4(sl, act, h, d, ix.e, ol, oh);
-#pragma unroll
-    for (int q = 0; q < kClaimQ; ++q) pend[q] = act[q] && (ol[q] | oh[q]) != 0ull && !(ol[q] == h[q] && oh[q] == d[q]);
-    bool mine[kClaimQ];
-#pragma unroll
-    for (int q = 0; q < kClaimQ; ++q) mine[q] = act[q] && (ol[q] | oh[q]) == 0ull;
-    for (uint64_t k = 1;; ++k) {
-      bool any = false;
-#pragma unroll
-      for (int q = 0; q < kClaimQ; ++q) any |= pend[q];
-      if (!any) break;
-      if (k > ix.mask) {  // table full
-        atomicOr(err_flag, 2u);
-#pragma unroll
-        for (int q = 0; q < kClaimQ; ++q)
-          if (pend[q]) pend[q] = false, sl[q] = ~0ull;
-        break;
-      }
-#pragma unroll
-      for (int q = 0; q < kClaimQ; ++q)
-        if (pend[q]) {
-          sl[q] = (sl[q] + 1) & ix.mask;
-          mine[q] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[q]].rec), 0ull, 0ull, h[q], d[q], &ol[q],
-                           &oh[q]);
-          pend[q] = !mine[q] && !(ol[q] == h[q] && oh[q] == d[q]);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < kClaimQ; ++q) {
-      const uint64_t i = i0 + q * nthr;
-      if (!act[q]) continue;
-      slot_io[i] = sl[q] == ~0ull ? kNone : static_cast<uint32_t>(sl[q]);
-      own[i] = mine[q] ? 1 : 0;
-    }
-  }
-}
 
 
 // Commit (A.7).  Lanes of the warp of prompt p walk its new blocks b >= k_p (k_p = the
@@ -1331,9 +1274,6 @@ __global__ void __launch_bounds__(256) k_claim(Index ix, const uint64_t* __restr
 #ifndef SKV_COMMIT_ROUNDS
 #define SKV_COMMIT_ROUNDS 2
 #endif
-#ifndef SKV_FLAT_CLAIM
-#define SKV_FLAT_CLAIM 0
-#endif
 constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 
 #ifndef SKV_COMMIT_MINB
@@ -1352,7 +1292,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
                                                 uint32_t fix_cap, uint32_t* err_flag,
                                                 const uint32_t* __restrict__ matched,
                                                 const uint64_t* __restrict__ users, MonCtx M, int with_record,
-                                                int pending_labels, const uint8_t* __restrict__ own) {
+                                                int pending_labels) {
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
@@ -1397,7 +1337,6 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
     // together (one DRAM round trip; the CAS returns the resident key, so no separate
     // load is needed); rare: the slot holds another key or the CAS lost a race -> linear
     // probing with CAS, every pending round's next CAS again in flight together.
-#if !SKV_FLAT_CLAIM
     uint64_t sl[R];
     unsigned long long ol[R], oh[R];
     bool pend[R];
@@ -1473,22 +1412,6 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
       s32[r] = static_cast<uint32_t>(sl[r]);
       slot_out[bo + base + 32 * r + lane] = s32[r];
     }
-#else
-    // claims done by k_claim: this block's slot and whether its CAS inserted the key
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t b = base + 32 * r + lane;
-      if (b < n) {
-        s32[r] = slot_out[bo + b];
-        mine[r] = own[bo + b] != 0;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
-    if constexpr (kRec)
-      if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
-#endif
     // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
     bool pmine[R];
@@ -1580,6 +1503,213 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
     if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
+}
+
+// Flat commit (default): warp = 32 x R CONSECUTIVE blocks of the batch (prompt
+// boundaries anywhere), grid-stride over such groups -- every warp is busy with claims
+// from its first instruction (no per-prompt prologue), which keeps ~2x more claims in
+// flight than a warp per prompt.  Lane = block i of prompt p = bprompt[i]:
+//   * matched block (b < matched[p]): its monitor record (AccessStats::record), issued
+//     while the group's claims are in flight;
+//   * new block (the probe left slot = kNone): 128-bit CAS on its home slot (linear
+//     probing on a foreign key); the CAS winner writes creator, meta, parent slot and its
+//     own child's slot (block i+1, when the same lane group claimed it) in one 16-B store
+//     into sector 0 while the line is in L2; a claimant that found its key inserted by
+//     another prompt of the batch appends a duplicate fix-up entry;
+//   * child links not covered by a parent's own store -- parent existed before the batch,
+//     parent claimed by another prompt, or parent in the previous lane group (its slot
+//     may not be written yet) -- go to the late list as (child slot, parent block) and
+//     are exchanged into the parent's first-child list by k_commit_links after the
+//     kernel, once every slot is known.
+template <bool kRec>
+__global__ void __launch_bounds__(256) k_commit_flat(
+    Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
+    const uint32_t* __restrict__ bprompt, const uint8_t* __restrict__ label, const uint32_t* __restrict__ uidx,
+    const uint8_t* __restrict__ owners, uint32_t n_prompts, uint32_t* slot_io, unsigned long long* n_new,
+    uint32_t* fix_list, uint32_t* n_fix, uint32_t fix_cap, uint32_t* late, uint32_t* n_late, uint32_t* err_flag,
+    const uint32_t* __restrict__ matched, const uint64_t* __restrict__ users, MonCtx M, int pending_labels) {
+  constexpr int R = kCommitRounds;
+  constexpr uint32_t G = 32 * R;
+  const uint32_t lane = lane_id();
+  const uint32_t nb = blk_off[n_prompts];
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint32_t inserted = 0;
+  for (uint64_t g0 = ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * G; g0 < nb;
+       g0 += nw * G) {
+    uint32_t s32[R], pr[R], bb[R], pend_n[R], lab[R];
+    uint64_t h[R], d[R], sl[R];
+    bool nw_[R], mine[R], act[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint64_t i = g0 + 32 * r + lane;
+      act[r] = i < nb;
+      s32[r] = act[r] ? slot_io[i] : kNone;
+      nw_[r] = act[r] && s32[r] == kNone;
+      pr[r] = act[r] ? bprompt[i] : 0;
+      h[r] = d[r] = 0;
+      lab[r] = 0;
+      if (nw_[r]) {
+        h[r] = hk[i];
+        d[r] = dk[i];
+        lab[r] = label[i];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t o = act[r] ? blk_off[pr[r]] : 0;
+      bb[r] = static_cast<uint32_t>(g0 + 32 * r + lane - o);
+      pend_n[r] = act[r] ? blk_off[pr[r] + 1] - o : 0;  // blocks of the prompt
+      sl[r] = home_slot(ix, h[r], d[r], 0);
+    }
+    unsigned long long ol[R], oh[R];
+    if constexpr (R == kClaimQ) {
+      cas128_empty_x4(sl, nw_, h, d, ix.e, ol, oh);
+    } else if constexpr (R == 2) {
+      cas128_empty_x2(reinterpret_cast<unsigned long long*>(&ix.e[sl[0]].rec),
+                      reinterpret_cast<unsigned long long*>(&ix.e[sl[1]].rec), nw_[0], nw_[1], h[0], d[0], h[1],
+                      d[1], &ol[0], &oh[0], &ol[1], &oh[1]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ol[r] = oh[r] = ~0ull;
+        if (nw_[r])
+          cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r], &oh[r]);
+      }
+    }
+    // the monitor records of the group's matched blocks while the claims are in flight
+    if constexpr (kRec) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r] && !nw_[r] && bb[r] < matched[pr[r]]) {
+          const uint64_t u = users[pr[r]];
+          Entry& e = ix.e[s32[r]];
+          atomicAdd(&e.stats.hit_cur, 1u);
+          const uint32_t si = *reinterpret_cast<volatile uint32_t*>(&e.aux.set_idx);
+          bool fast = false;
+          if (si < kPendingSet) {
+            const ulonglong2 v = ld_relaxed128(&M.tab[static_cast<uint64_t>(si) * kSetSlots + (mix32(u) & (kSetSlots - 1))]);
+            fast = v.x == u && v.y >= M.wstart;
+          }
+          if (!fast) record_user(ix, M, s32[r], u);
+        }
+    }
+    bool pend[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      mine[r] = nw_[r] && (ol[r] | oh[r]) == 0ull;
+      pend[r] = nw_[r] && !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
+    }
+    for (uint64_t k = 1;; ++k) {
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) any |= pend[r];
+      if (!any) break;
+      if (k > ix.mask) {  // table full
+        atomicOr(err_flag, 2u);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (pend[r]) pend[r] = false, sl[r] = ~0ull;
+        break;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (pend[r]) {
+          sl[r] = (sl[r] + 1) & ix.mask;
+          mine[r] = cas128(reinterpret_cast<unsigned long long*>(&ix.e[sl[r]].rec), 0ull, 0ull, h[r], d[r], &ol[r],
+                           &oh[r]);
+          pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (nw_[r]) {
+        s32[r] = sl[r] == ~0ull ? kNone : static_cast<uint32_t>(sl[r]);
+        slot_io[g0 + 32 * r + lane] = s32[r];
+      }
+    // neighbours inside the group: block i-1 (parent) and i+1 (own child)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t ps = __shfl_up_sync(kFull, s32[r], 1);
+      bool pm = __shfl_up_sync(kFull, mine[r], 1);
+      uint32_t cs = __shfl_down_sync(kFull, s32[r], 1);
+      bool cm = __shfl_down_sync(kFull, mine[r], 1);
+      const uint32_t ps_prev = __shfl_sync(kFull, s32[r > 0 ? r - 1 : 0], 31);
+      const bool pm_prev = __shfl_sync(kFull, mine[r > 0 ? r - 1 : 0], 31);
+      const uint32_t cs_next = __shfl_sync(kFull, s32[r + 1 < R ? r + 1 : r], 0);
+      const bool cm_next = __shfl_sync(kFull, mine[r + 1 < R ? r + 1 : r], 0);
+      bool p_in = true;  // the parent block belongs to this lane group
+      if (lane == 0) {
+        if (r > 0) {
+          ps = ps_prev, pm = pm_prev;
+        } else {
+          p_in = false;
+        }
+      }
+      bool c_in = true;
+      if (lane == 31) {
+        if (r + 1 < R) {
+          cs = cs_next, cm = cm_next;
+        } else {
+          c_in = false;
+        }
+      }
+      if (!nw_[r] || s32[r] == kNone) continue;
+      const uint32_t b = bb[r], p = pr[r];
+      if (mine[r]) {
+        uint32_t parent = kNone;
+        bool late_link = false, need_parent = false;
+        if (b > 0) {
+          if (p_in) {
+            parent = ps;
+            late_link = !pm;
+          } else {  // previous lane group: its slot may not be written yet
+            parent = *reinterpret_cast<volatile uint32_t*>(&slot_io[g0 + 32 * r + lane - 1]);
+            late_link = true;
+            need_parent = parent == kNone;
+          }
+        }
+        const uint32_t child = (b + 1 < pend_n[r] && c_in && cm) ? cs : kNone;
+        const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owners ? owners[p] : 0u,
+                                        SKV_TIER_HBM, p);
+        *reinterpret_cast<uint4*>(&ix.e[s32[r]].rec.creator) = make_uint4(uidx[p], meta, parent, child);
+        if (late_link) {
+          const uint32_t f = atomicAdd(n_late, 1u);
+          if (f < fix_cap) {
+            late[2 * f] = s32[r];
+            late[2 * f + 1] = static_cast<uint32_t>(g0 + 32 * r + lane - 1) | (need_parent ? 0x80000000u : 0u);
+          } else {
+            atomicOr(err_flag, 4u);
+          }
+        }
+        ++inserted;
+      } else {
+        const uint32_t f = atomicAdd(n_fix, 1u);
+        if (f < fix_cap) {
+          fix_list[f] = s32[r];
+          fix_list[fix_cap + f] = b;  // block depth of this key
+          fix_list[2 * fix_cap + f] = p;
+          fix_list[3 * fix_cap + f] = kNone;
+        } else {
+          atomicOr(err_flag, 4u);
+        }
+      }
+    }
+  }
+  inserted = __reduce_add_sync(kFull, inserted);
+  if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
+}
+
+// Late child links of the flat commit: every slot is known now.
+__global__ void k_commit_links(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ late,
+                               const uint32_t* __restrict__ n_late, uint32_t cap) {
+  const uint32_t n = min(*n_late, cap);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t c = late[2 * k], pb = late[2 * k + 1];
+    const uint32_t ps = slot[pb & 0x7fffffffu];
+    if (pb >> 31) ix.e[c].rec.parent = ps;
+    const uint32_t sib = atomicExch(&ix.e[ps].rec.first_child, c);
+    if (sib != kNone) ix.e[c].aux.next_sibling = sib;
+  }
 }
 
 // Intra-batch duplicates, pass 1: lowest claiming prompt (all claims are complete).
@@ -1922,10 +2052,11 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, cudaStream_t s) {
+                        const MonCtx& mon, uint32_t* bprompt, cudaStream_t s) {
   if (n)
     k_chain_probe<<<cdiv(n, kCPPrompts * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
-                                                                   decision, slot, matched, exist, tier, bmeta, mon);
+                                                                   decision, slot, matched, exist, tier, bmeta, mon,
+                                                                   bprompt);
 }
 
 uint32_t record_grid(int device) {
@@ -1975,21 +2106,30 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    const uint32_t* exist, const uint8_t* label, const uint32_t* users, const uint8_t* owners,
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
-                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint8_t* own, uint64_t n_blocks,
-                   int n_sm, cudaStream_t s) {
+                   const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, cudaStream_t s) {
   const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
-#if SKV_FLAT_CLAIM
-  if (n_blocks)
-    k_claim<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n_blocks, 256 * kClaimQ), 8ull * n_sm)), 256, 0, s>>>(
-        ix, h, d, slot, own, blk_off, n, err_flag);
+#if SKV_COMMIT_FLAT
+  {
+    auto* kern = mon ? k_commit_flat<true> : k_commit_flat<false>;
+    kern<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(std::max<uint64_t>(n_blocks, 1), 32ull * kCommitRounds * 8),
+                                                    8ull * n_sm)),
+           256, 0, s>>>(ix, h, d, blk_off, bprompt, label, users, owners, n, slot, n_new, fix_list, n_fix, fix_cap,
+                        late, n_late, err_flag, matched, users64, M, pending_labels);
+    k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
+    k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
+                                            pending_labels);
+    k_commit_links<<<fix_grid, 256, 0, s>>>(ix, slot, late, n_late, fix_cap);
+    return;
+  }
 #endif
   auto* kern = mon ? k_commit<true> : k_commit<false>;
   kern<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag,
                                                                     matched, users64, M, mon ? 1 : 0,
-                                                                    pending_labels, own);
+                                                                    pending_labels);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
                                           pending_labels);
