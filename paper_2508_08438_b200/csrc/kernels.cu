@@ -26,7 +26,21 @@ constexpr uint64_t kFnvOff = 0xcbf29ce484222325ULL;
 constexpr uint64_t kFnvP = 0x100000001b3ULL;
 constexpr uint64_t kFnvP4 = kFnvP * kFnvP * kFnvP * kFnvP;  // (h^t)*P^4 == update_u32(t) for t < 256
 
-__device__ __forceinline__ uint64_t fnv_byte(uint64_t h, uint32_t b) { return (h ^ b) * kFnvP; }
+// (h ^ b) * P with P = 2^40 + 0x1b3: lo * 0x1b3 as one wide multiply, then the high word
+// gains hi * 0x1b3 and (lo << 8) -- three IMADs instead of a generic 64-bit multiply
+// (chained keys in k_chain_probe: 0.229 -> 0.222 ms per config-2 batch)
+__device__ __forceinline__ uint64_t fnv_byte(uint64_t h, uint32_t b) {
+  const uint32_t lo = static_cast<uint32_t>(h) ^ b, hi = static_cast<uint32_t>(h >> 32);
+  uint32_t rlo, rhi;
+  asm("{\n\t.reg .u64 w;\n\t.reg .u32 wh;\n\t"
+      "mul.wide.u32 w, %2, 0x1b3;\n\t"
+      "mov.b64 {%0, wh}, w;\n\t"
+      "mad.lo.u32 wh, %3, 0x1b3, wh;\n\t"
+      "mad.lo.u32 %1, %2, 256, wh;\n\t}"
+      : "=r"(rlo), "=r"(rhi)
+      : "r"(lo), "r"(hi));
+  return (static_cast<uint64_t>(rhi) << 32) | rlo;
+}
 __device__ __forceinline__ uint64_t fnv_u32(uint64_t h, uint32_t v) {
   h = fnv_byte(h, v & 0xff);
   h = fnv_byte(h, (v >> 8) & 0xff);
