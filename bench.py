@@ -33,7 +33,12 @@ ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CFG2 = dict(n_prompts=65536, prompt_tokens=2048, block_tokens=16, window_tokens=32, n_users=64,
-            pool_size=256, pool_tokens=640, pii_per_kib=1.0, seed=1)
+            pool_size=256, pool_tokens=640, pii_per_kib=1.0, pii_mix=0, seed=1, name="config 2")
+# BASELINE.json configs[2] per GPU (--workload 3): a 131,072-prompt shard of the 1M x 4k batch,
+# 256 users, mixed PII density (60% none / 30% one per 2 KiB / 10% one per 256 B)
+CFG3 = dict(n_prompts=131072, prompt_tokens=4096, block_tokens=16, window_tokens=32, n_users=256,
+            pool_size=256, pool_tokens=640, pii_per_kib=0.0, pii_mix=1, seed=3, name="config 3")
+CONFIGS = {2: CFG2, 3: CFG3}
 METRIC = "KV blocks admitted/sec (hash+scan+lookup+monitor) and % HBM roofline, 1/2/4/8 B200"
 UNIT = "blocks/s"
 CPU_STEPS = 6
@@ -106,7 +111,7 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- reference arm
-def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int, verbose=False):
+def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int, verbose=False, c=CFG2):
     """Reference CPU implementation of the path (oracle/_ref: the unmodified reference
     headers driven by the Appendix-A contract): std::regex Tier-1 scan on a thread pool,
     RadixCacheIndex / EntropyMonitor single-threaded behind their mutex."""
@@ -116,10 +121,9 @@ def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int
     L = load_ref()
     if L is None:
         return None
-    c = CFG2
     spec = GenSpec(n_prompts=sample_prompts, prompt_tokens=c["prompt_tokens"], n_users=c["n_users"],
                    pool_size=c["pool_size"], pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"],
-                   seed=c["seed"])
+                   pii_mix=c["pii_mix"], seed=c["seed"])
     eng = RefEngine(L, RefRules(L), B=c["block_tokens"], W=c["window_tokens"], threads=threads)
     pool = generate_pool(spec)
     eng.admit(*pool)
@@ -148,7 +152,8 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     sample = args.cpu_sample
-    r = cpu_reference_run(args.steps, args.warmup, sample, threads)
+    c = CONFIGS[args.workload]
+    r = cpu_reference_run(args.steps, args.warmup, sample, threads, c=c)
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsafekv_ref.so not built"}))
         return
@@ -156,11 +161,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/u64 integer; f64 entropy",
-        "data": "synthetic (deterministic generator, SURVEY 8(d) config 2 shape)",
-        "config": {"workload": f"config 2 sample: {sample} prompts/step x 2048 tokens, B=16, W=32, 64 users, "
-                               "256x640-token shared pool pre-inserted", "sample_prompts_per_step": sample},
+        "data": f"synthetic (deterministic generator, SURVEY 8(d) {c['name']} shape)",
+        "config": {"workload": f"{c['name']} sample: {sample} prompts/step x {c['prompt_tokens']} tokens, B=16, W=32, "
+                               f"{c['n_users']} users, 256x640-token shared pool pre-inserted",
+                   "sample_prompts_per_step": sample},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} steps x {sample} prompts of config 2"},
+                         "sample": f"{args.steps} steps x {sample} prompts of {c['name']}"},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -186,7 +192,7 @@ def run_ours(args):
     gpu = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
-    c = dict(CFG2)
+    c = dict(CONFIGS[args.workload])
     if args.prompts:
         c["n_prompts"] = args.prompts
     n_local = c["n_prompts"]  # weak scaling: every rank admits a full config-2 batch per step
@@ -213,7 +219,7 @@ def run_ours(args):
     # the global sequence that skv_route assigns to it (disjoint index forests, no
     # data-path collective)
     spec = GenSpec(n_prompts=n_local, prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
-                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"],
+                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
                    route_world=world, route_rank=rank, route_block_tokens=B)
     host, devb = [], []
     for k in range(n_batches):
@@ -343,10 +349,10 @@ def run_ours(args):
         # a bounded sample (~10 s of CPU work): CPU_STEPS timed batches of --cpu-sample
         # prompts after one warm-up batch, same generator, pool pre-inserted
         r = cpu_reference_run(steps=CPU_STEPS, warmup=1, sample_prompts=args.cpu_sample,
-                              threads=os.cpu_count() or 1)
+                              threads=os.cpu_count() or 1, c=c)
         if r is not None:
             cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of config 2 after 1 warm-up batch "
+                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of {c['name']} after 1 warm-up batch "
                              f"(pool pre-inserted): {r['blocks']} blocks in {r['seconds']:.1f} s"}
     # where the rest of the step goes: the commit is bound by random 128-bit CAS into the
     # index (one claim per new block), measured against the randmem ceiling
@@ -377,7 +383,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": ms_dev / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32 tokens / u64 keys (integer), f64 entropy", "data": "synthetic (deterministic generator)",
-        "config": {"workload": f"config 2: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
+        "config": {"workload": f"{c['name']}: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
                                f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
                    "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
                    "step": "admit + commit + epoch",
@@ -416,6 +422,8 @@ def main():
     ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
     ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (2 = the headline, default; 3 = the per-GPU shard of config 3)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
     args = ap.parse_args()
