@@ -205,6 +205,18 @@ typedef struct {
 int skv_export(skv_ctx* ctx, skv_entry* out, size_t cap, size_t* n);
 uint64_t skv_entry_count(skv_ctx* ctx);
 
+/* Eviction (RadixCacheIndex::evict, cache_index.hpp:281-292,697-807; untiered mode).
+ * skv_enable_eviction must precede the first admit: it allocates the per-entry access
+ * epoch / node id bookkeeping.  skv_evict frees needed_blocks entries, one block each,
+ * in the reference's victim order (unpinned HBM leaves, oldest access epoch first, then
+ * Public before non-Public, then the smallest node id, repeatedly), leaving tombstones
+ * that lookups treat as missing and a later insert of the same key revives as a fresh
+ * entry.  Writes the victims' keys (up to cap) and returns SKV_ERR_CAPACITY, after
+ * freeing every candidate, when fewer than needed_blocks could be freed. */
+int skv_enable_eviction(skv_ctx* ctx);
+int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
+              uint64_t* victims_d, size_t cap);
+
 /* Per-stage device times of the last skv_admit / skv_commit (CUDA events, ms). */
 typedef struct {
   float hash_scan_ms, chain_probe_ms, record_ms, admit_total_ms, commit_ms, epoch_ms;

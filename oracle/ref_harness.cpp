@@ -431,6 +431,29 @@ int ref_engine_commit(void* ev) {
 
 // Set tier tags on existing entries: tiers[k] (0 HBM, 1 DRAM, 2 SSD) for every full
 // block of every prompt, applied with RadixCacheIndex::demote (cache_index.hpp:362-381).
+// RadixCacheIndex::evict(needed, epoch) (cache_index.hpp:281-292) on the reference index;
+// *n_out = nodes freed.  Returns 1 when the reference ran out of candidates
+// (CapacityExhausted) after freeing what it could.
+int ref_engine_evict(void* ev, uint64_t needed, uint64_t epoch, uint64_t* n_out) {
+  auto* e = static_cast<RefEngine*>(ev);
+  auto count = [&] {
+    uint64_t n = 0;
+    e->idx->for_each_node([&](const CacheNode*) { ++n; });
+    return n;
+  };
+  const uint64_t before = count();
+  int rc = 0;
+  try {
+    e->idx->evict(needed, epoch);
+  } catch (const CapacityExhausted&) {
+    rc = 1;
+  }
+  *n_out = before - count();
+  return rc;
+}
+
+uint64_t ref_engine_current_epoch(void* ev) { return static_cast<RefEngine*>(ev)->idx->current_epoch(); }
+
 int ref_engine_set_tiers(void* ev, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts,
                          const uint8_t* tiers) {
   auto* e = static_cast<RefEngine*>(ev);

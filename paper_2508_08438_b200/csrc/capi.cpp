@@ -132,6 +132,17 @@ struct skv_ctx {
   uint32_t* bmask = nullptr;
   uint8_t* blabel = nullptr;
   uint32_t* bprompt = nullptr;  // block -> prompt (written by the probe, read by the flat commit)
+  // eviction (skv_enable_eviction): bookkeeping array + lazily allocated work buffers
+  bool evict_on = false;
+  uint64_t tombstones = 0;  // evicted slots not re-inserted (they keep their slot)
+  uint32_t* ev_counts = nullptr;
+  uint32_t* ev_incl = nullptr;
+  unsigned long long* ev_next_id = nullptr;
+  void* ev_temp = nullptr;
+  size_t ev_temp_bytes = 0;
+  unsigned long long *ev_eff = nullptr, *ev_keys_a = nullptr, *ev_keys_b = nullptr;
+  uint32_t *ev_vals_a = nullptr, *ev_vals_b = nullptr, *ev_n = nullptr;
+  uint64_t *ev_vh = nullptr, *ev_vd = nullptr;
   uint32_t* late = nullptr;     // commit: (child slot, parent block) links applied after the claims
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
@@ -797,6 +808,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_intern_users(c->users_tab, users, N, c->uidx, c->counters + 5, s);
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
                             c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt, s);
+    if (c->evict_on)  // match_prefix refreshes the access epoch of every visible matched node
+      skv::launch_touch_matched(c->ix, c->bslot, c->blk_off, c->matched, N, static_cast<uint32_t>(c->epoch), s);
     CK(cudaEventRecord(c->ev[3], s));
     // stage 4: the monitor records (AccessStats::record of every matched block, in
     // prompt order) run inside the commit kernel, overlapping the claims' DRAM round
@@ -995,12 +1008,12 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       if (new_entries) *new_entries = 0;
       return SKV_OK;
     }
-    if (c->entries + c->p_blocks > c->ix.cap - c->ix.cap / 8)
+    if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
       throw CapacityError("index capacity exhausted (eviction is not part of this path)");
     CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
-    CK(cudaMemsetAsync(c->counters + 11, 0, 4, s));  // late child links
+    CK(cudaMemsetAsync(c->counters + 11, 0, 8, s));  // late child links, re-inserted tombstones
     ++c->batch_id;
     const bool rec = c->rec_pending;  // the batch's monitor records (see skv_admit)
     // The records (sector 1 of the matched entries, the window user sets) and the inserts
@@ -1017,21 +1030,30 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users,
                        rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
-                       c->n_sm, c->bprompt, c->late, c->counters + 11, s);
+                       c->n_sm, c->bprompt, c->late, c->counters + 11, c->counters + 12, s);
     if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
     uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
+    if (c->evict_on) {  // insert walk epochs + node ids of the created blocks
+      skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off, c->p_n, static_cast<uint32_t>(c->epoch), c->ev_counts,
+                               c->ev_incl, c->ev_next_id, c->ev_temp, c->ev_temp_bytes, s);
+      launched += 4;
+    }
     if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
     CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
     if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
     std::memcpy(&nn, c->host_small, 8);
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     if (rec) launched += replay_record(c, s, c->host_small[5], c->host_small[4]);
-    c->entries += nn;
+    const uint32_t revived = c->host_small[6];
+    c->entries += nn + revived;
+    c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
+    nn += revived;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
     c->times.kernels_launched += launched;
     c->times.new_blocks = nn;
@@ -1187,6 +1209,66 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
 }
 
 uint64_t skv_entry_count(skv_ctx* c) { return c ? c->entries : 0; }
+
+int skv_enable_eviction(skv_ctx* c) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (c->evict_on) return SKV_OK;
+    if (c->entries || c->batch_id) throw StateError("skv_enable_eviction must precede the first admit");
+    skv::EvictMeta* em = dalloc<skv::EvictMeta>(c->ix.cap, c->owned);
+    CK(cudaMemsetAsync(em, 0, c->ix.cap * sizeof(skv::EvictMeta), c->stream));
+    const uint64_t N = std::max<uint64_t>(c->max_prompts, 1);
+    c->ev_counts = dalloc<uint32_t>(N, c->owned);
+    c->ev_incl = dalloc<uint32_t>(N, c->owned);
+    c->ev_next_id = dalloc<unsigned long long>(1, c->owned);
+    const unsigned long long one = 1;  // next_node_id_ (cache_index.hpp:832); the root is node 0
+    CK(cudaMemcpyAsync(c->ev_next_id, &one, 8, cudaMemcpyHostToDevice, c->stream));
+    c->ev_temp_bytes = skv::evict_temp_bytes(static_cast<uint32_t>(N), c->ix.cap);
+    c->ev_temp = dalloc<uint8_t>(c->ev_temp_bytes, c->owned);
+    sync_check(c->stream);
+    c->ix.em = em;
+    c->evict_on = true;
+    return SKV_OK;
+  });
+}
+
+int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
+              uint64_t* victims_d, size_t cap) {
+  (void)epoch;  // the victim order only compares access epochs (epoch - access_epoch, cache_index.hpp:709)
+  if (!c || !n_evicted) return SKV_ERR_ARG;
+  *n_evicted = 0;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (!c->evict_on) throw StateError("eviction is not enabled (skv_enable_eviction before the first admit)");
+    if (needed_blocks == 0) throw ArgError("evict: needed must be positive");
+    ensure_admit_resolved(c);
+    flush_record(c);
+    cudaStream_t s = c->stream;
+    if (!c->ev_eff) {  // work buffers, sized by the index capacity, on first use
+      c->ev_eff = dalloc<unsigned long long>(c->ix.cap, c->owned);
+      c->ev_keys_a = dalloc<unsigned long long>(c->ix.cap, c->owned);
+      c->ev_keys_b = dalloc<unsigned long long>(c->ix.cap, c->owned);
+      c->ev_vals_a = dalloc<uint32_t>(c->ix.cap, c->owned);
+      c->ev_vals_b = dalloc<uint32_t>(c->ix.cap, c->owned);
+      c->ev_vh = dalloc<uint64_t>(c->ix.cap, c->owned);
+      c->ev_vd = dalloc<uint64_t>(c->ix.cap, c->owned);
+      c->ev_n = dalloc<uint32_t>(1, c->owned);
+    }
+    const uint32_t v = skv::launch_evict(c->ix, needed_blocks, c->ev_eff, c->ev_keys_a, c->ev_keys_b, c->ev_vals_a,
+                                         c->ev_vals_b, c->ev_n, c->ev_temp, c->ev_temp_bytes, c->ev_vh, c->ev_vd,
+                                         c->host_small, s);
+    const size_t k = std::min<size_t>(v, cap);
+    if (victims_h && k) CK(cudaMemcpyAsync(victims_h, c->ev_vh, k * 8, cudaMemcpyDeviceToHost, s));
+    if (victims_d && k) CK(cudaMemcpyAsync(victims_d, c->ev_vd, k * 8, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    c->entries -= v;
+    c->tombstones += v;
+    *n_evicted = v;
+    if (v < needed_blocks) throw CapacityError("evict: no unpinned candidate leaf");
+    return SKV_OK;
+  });
+}
 
 int skv_last_times(skv_ctx* c, skv_stage_times* out) {
   if (!c || !out) return SKV_ERR_ARG;

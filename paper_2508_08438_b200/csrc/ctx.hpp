@@ -34,6 +34,17 @@ __host__ __device__ inline uint32_t make_meta(uint32_t label, uint32_t owner, ui
   return (label & 3u) | ((owner & 1u) << 2) | ((tier & 3u) << 3) | (1u << 5) | (prompt << 8);
 }
 constexpr uint32_t kMaxBatchPrompts = 1u << 24;  // the claiming-prompt field of Rec::meta
+__host__ __device__ inline bool meta_live(uint32_t m) { return (m >> 5) & 1u; }
+
+// Eviction bookkeeping (skv_enable_eviction), a parallel array beside the entries so the
+// admission path's two-sector entry is unchanged: the fields the reference's victim
+// order reads (cache_index.hpp:697-728) plus the tombstone flag.
+struct __align__(16) EvictMeta {
+  uint32_t access_epoch;  // CacheNode::access_epoch: epoch of the last match / insert walk
+  uint32_t node_id;       // CacheNode::node_id as the reference assigns it; kNone = assign at this commit
+  uint32_t depth;         // block index (children before parents on equal effective keys)
+  uint32_t dead;          // 1 = evicted: the key stays as a tombstone until re-inserted
+};
 
 struct __align__(16) Stats {
   uint32_t hit_cur, u_cnt, hit_pre, u_pre;
@@ -125,6 +136,7 @@ struct HSLayout {
 struct Index {
   Entry* e = nullptr;
   uint64_t cap = 0, mask = 0;
+  EvictMeta* em = nullptr;  // null unless eviction is enabled
 };
 
 // Monitor user sets (AccessStats::user_set, access_stats.hpp:21-37), one per entry touched
@@ -165,6 +177,17 @@ struct CostModelDev {
 };
 
 void launch_init_entries(const Index& ix, cudaStream_t s);
+// eviction (kernels.cu): access epochs of matched blocks at admit; node ids + access epochs
+// of every committed block at commit; evict(needed) = effective keys, sort, tombstones
+void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
+                          uint32_t n, uint32_t epoch, cudaStream_t s);
+void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, uint32_t n, uint32_t epoch,
+                         uint32_t* counts, uint32_t* base, unsigned long long* next_id, void* temp, size_t temp_bytes,
+                         cudaStream_t s);
+size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap);
+uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
+                      unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
+                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, cudaStream_t s);
 void launch_intern_users(const UserTable& t, const uint64_t* users, uint32_t n, uint32_t* uidx, uint32_t* err,
                          cudaStream_t s);
 void launch_ttft(const uint32_t* blk_off, const uint32_t* matched, const uint32_t* plen, const uint8_t* bmeta,
@@ -202,7 +225,7 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
                    const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
-                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, cudaStream_t s);
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived, cudaStream_t s);
 void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                     const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,

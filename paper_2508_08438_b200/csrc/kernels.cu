@@ -722,7 +722,7 @@ __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint6
     ulonglong2 k = rp[0];
     if (k.x == h && k.y == d) {
       *out = ix.e[s].rec;
-      return static_cast<uint32_t>(s);
+      return meta_live(out->meta) ? static_cast<uint32_t>(s) : kNone;  // a tombstone is missing
     }
     if (k.x == 0 && k.y == 0) return kNone;
     s = (s + 1) & ix.mask;
@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
         const bool act = b < nj;
         Probe pr{kNone, 0, 0};
         if (act) pr = probe_resolve(ix, th[j][lane], td[j][lane], ss[q], kk[q], mm[q]);
-        const bool found = pr.slot != kNone;
+        const bool found = pr.slot != kNone && meta_live(pr.meta);  // a tombstone is missing
         const uint32_t lab = meta_label(pr.meta);
         const bool vis = found && (lab == SKV_LABEL_PUBLIC || pr.creator == uj);
         const uint32_t nf = __ballot_sync(kFull, act && !found);
@@ -1470,6 +1470,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
         // linked by the fix-up pass)
         const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owner, SKV_TIER_HBM, p);
         *reinterpret_cast<uint4*>(&e.rec.creator) = make_uint4(creator, meta, par[r], own_child[r]);
+        if (ix.em) ix.em[s32[r]] = EvictMeta{0u, kNone, base + 32 * r + lane, 0u};
         // the parent link: under a parent that existed before the batch children race ->
         // exchange; under a parent this prompt claimed, the parent's own 16-B store wrote
         // the link, except across iterations (plain store); under a parent another
@@ -1686,6 +1687,7 @@ __global__ void __launch_bounds__(256) k_commit_flat(
         const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owners ? owners[p] : 0u,
                                         SKV_TIER_HBM, p);
         *reinterpret_cast<uint4*>(&ix.e[s32[r]].rec.creator) = make_uint4(uidx[p], meta, parent, child);
+        if (ix.em) ix.em[s32[r]] = EvictMeta{0u, kNone, b, 0u};
         if (late_link) {
           const uint32_t f = atomicAdd(n_late, 1u);
           if (f < fix_cap) {
@@ -1738,7 +1740,7 @@ __global__ void k_commit_fixup_min(Index ix, const uint32_t* __restrict__ fix_li
 __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
                                const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
-                               uint32_t fix_cap, int pending_labels) {
+                               uint32_t fix_cap, int pending_labels, uint32_t* n_revived) {
   const uint32_t nf = min(*n_fix, fix_cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
@@ -1747,6 +1749,16 @@ __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, c
     const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : label[blk_off[pw] + b],
                                     owners ? owners[pw] : 0u, SKV_TIER_HBM, pw);
     *reinterpret_cast<uint2*>(&r.creator) = make_uint2(uidx[pw], meta);
+    // a re-inserted tombstone is a fresh node (cache_index.hpp:192-201); its first claimant
+    // resets it, and it is still in its parent's child list
+    if (ix.em && ix.em[s].dead && atomicExch(&ix.em[s].dead, 0u)) {
+      ix.e[s].stats = Stats{0u, 0u, 0u, 0u};
+      ix.e[s].aux.set_idx = kNone;
+      ix.e[s].aux.mark = 0;
+      ix.em[s].node_id = kNone;
+      ix.em[s].depth = b;
+      atomicAdd(n_revived, 1u);
+    }
     // the duplicate claimant's own child under this entry (k_commit left it unlinked)
     const uint32_t c = fix_list[3 * fix_cap + i];
     if (c != kNone) {
@@ -1777,7 +1789,7 @@ __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, 
   if (i >= *n_list) return;
   uint32_t s = list[i];
   if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
-  if (meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
+  if (!meta_live(ix.e[s].rec.meta) || meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
   Stats st = ix.e[s].stats;
   if (st.hit_pre == 0) return;
   double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
@@ -1962,7 +1974,7 @@ __global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_en
   uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s > ix.mask) return;
   const Rec& r = ix.e[s].rec;
-  if (r.h == 0 && r.d == 0) return;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta)) return;
   Stats st = ix.e[s].stats;
   skv_entry e;
   e.h = r.h;
@@ -2110,6 +2122,168 @@ void launch_sort_keys(void* temp, size_t temp_bytes, const unsigned long long* i
   cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, n, 0, end_bit, s);
 }
 
+// ---------------------------------------------------------------------------------
+// Eviction (RadixCacheIndex::evict / select_victim, cache_index.hpp:281-292,697-728).
+//
+// The reference frees, one at a time, the unpinned HBM leaf with the oldest access epoch,
+// Public before non-Public, then the smallest node id; freeing a leaf can expose its
+// parent.  A parent's access epoch is never below a child's (every match or insert walk
+// that refreshes a node refreshes its whole root path), so this greedy order is the
+// order of eff(X) = max(key(X), eff(children)) with children before parents on equal
+// eff (a parent that inherits its deepest descendant's key goes right after it); a node
+// off HBM never leaves, and blocks every ancestor (eff = +inf).  One evict(V) therefore
+// tombstones the V smallest (eff, depth desc) live entries: eff by upward atomicMax,
+// then two stable radix sorts (depth desc, then eff).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long evict_key(const Index& ix, uint64_t s) {
+  const uint32_t m = ix.e[s].rec.meta;
+  if (meta_tier(m) != SKV_TIER_HBM) return ~0ull;
+  const EvictMeta em = ix.em[s];
+  return (static_cast<unsigned long long>(em.access_epoch) << 32) |
+         (static_cast<unsigned long long>(meta_label(m) != SKV_LABEL_PUBLIC) << 31) | (em.node_id & 0x7fffffffu);
+}
+
+__global__ void k_touch_matched(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                                const uint32_t* __restrict__ matched, uint32_t n, uint32_t epoch) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const uint32_t bo = blk_off[p], m = matched[p];
+  for (uint32_t b = lane_id(); b < m; b += 32) ix.em[slot[bo + b]].access_epoch = epoch;
+}
+
+// pass 1: every block of the prompt was walked by its insert -> access epoch; count the
+// blocks this prompt created (node id still unassigned, claimed by this prompt)
+__global__ void k_nodes_count(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                              uint32_t n, uint32_t epoch, uint32_t* counts) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const uint32_t bo = blk_off[p], nb = blk_off[p + 1] - bo;
+  uint32_t f = 0;
+  for (uint32_t b = lane_id(); b < nb; b += 32) {
+    const uint32_t s = slot[bo + b];
+    if (s == kNone) continue;
+    ix.em[s].access_epoch = epoch;
+    f += (ix.em[s].node_id == kNone && meta_prompt(ix.e[s].rec.meta) == p) ? 1u : 0u;
+  }
+  f = __reduce_add_sync(kFull, f);
+  if (lane_id() == 0) counts[p] = f;
+}
+
+// pass 2: insert() allocates id X for the new suffix node, ensure_boundary then splits
+// off its top block f-1 times, each split's upper half taking the next id: block j of
+// the f created blocks gets X+1+j, the deepest keeps X (cache_index.hpp:193,537)
+__global__ void k_nodes_assign(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                               uint32_t n, const uint32_t* __restrict__ counts, const uint32_t* __restrict__ incl,
+                               const unsigned long long* next_id) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const uint32_t f = counts[p];
+  if (!f) return;
+  const uint32_t bo = blk_off[p], nb = blk_off[p + 1] - bo, k = nb - f;
+  const unsigned long long X = *next_id + incl[p] - f;
+  for (uint32_t j = lane_id(); j < f; j += 32)
+    ix.em[slot[bo + k + j]].node_id = static_cast<uint32_t>(j + 1 < f ? X + 1 + j : X);
+}
+
+__global__ void k_nodes_bump(unsigned long long* next_id, const uint32_t* incl, uint32_t n) {
+  if (n) *next_id += incl[n - 1];
+}
+
+__global__ void k_evict_init(Index ix, unsigned long long* eff) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  eff[s] = ((r.h == 0 && r.d == 0) || !meta_live(r.meta)) ? 0ull : evict_key(ix, s);
+}
+
+__global__ void k_evict_propagate(Index ix, unsigned long long* eff) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  unsigned long long v = eff[s];
+  if (!v) return;
+  for (uint32_t p = ix.e[s].rec.parent; p != kNone; p = ix.e[p].rec.parent) {
+    const unsigned long long old = atomicMax(&eff[p], v);
+    if (old >= v) break;
+  }
+}
+
+__global__ void k_evict_compact(Index ix, const unsigned long long* __restrict__ eff, unsigned long long* keys,
+                                uint32_t* vals, uint32_t* n_live) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const unsigned long long v = eff[s];
+  if (v == 0 || v == ~0ull) return;
+  const uint32_t i = atomicAdd(n_live, 1u);
+  keys[i] = ~static_cast<unsigned long long>(ix.em[s].depth) & 0xffffffffull;  // deeper first
+  vals[i] = static_cast<uint32_t>(s);
+}
+
+__global__ void k_evict_gather(const unsigned long long* __restrict__ eff, const uint32_t* __restrict__ vals,
+                               unsigned long long* keys, const uint32_t* n_live) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *n_live) keys[i] = eff[vals[i]];
+}
+
+// tombstones: the key stays (linear probing and re-insertion find it), live = 0, the
+// claiming-prompt field at its maximum so a re-insert's atomicMin picks its claimant
+__global__ void k_evict_mark(Index ix, const uint32_t* __restrict__ vals, uint32_t v, uint64_t* vh, uint64_t* vd) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v) return;
+  const uint32_t s = vals[i];
+  Rec& r = ix.e[s].rec;
+  r.meta = (r.meta & 0x1fu) | 0xffffff00u;  // label/owner/tier kept, live cleared
+  ix.em[s].dead = 1;
+  if (vh) vh[i] = r.h;
+  if (vd) vd[i] = r.d;
+}
+
+void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
+                          uint32_t n, uint32_t epoch, cudaStream_t s) {
+  if (n) k_touch_matched<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, slot, blk_off, matched, n, epoch);
+}
+
+void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, uint32_t n, uint32_t epoch,
+                         uint32_t* counts, uint32_t* incl, unsigned long long* next_id, void* temp, size_t temp_bytes,
+                         cudaStream_t s) {
+  if (!n) return;
+  const unsigned g = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n) * 32, 256));
+  k_nodes_count<<<g, 256, 0, s>>>(ix, slot, blk_off, n, epoch, counts);
+  cub::DeviceScan::InclusiveSum(temp, temp_bytes, counts, incl, n, s);
+  k_nodes_assign<<<g, 256, 0, s>>>(ix, slot, blk_off, n, counts, incl, next_id);
+  k_nodes_bump<<<1, 1, 0, s>>>(next_id, incl, n);
+}
+
+size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap) {
+  size_t a = 0, b = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, a, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                std::max<uint32_t>(n_prompts, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const unsigned long long*>(nullptr),
+                                  static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<int>(std::min<uint64_t>(cap, 1u << 31)));
+  return std::max(a, b);
+}
+
+uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
+                      unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
+                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(cdiv(ix.cap, 256));
+  cudaMemsetAsync(n_live, 0, 4, s);
+  k_evict_init<<<g, 256, 0, s>>>(ix, eff);
+  k_evict_propagate<<<g, 256, 0, s>>>(ix, eff);
+  k_evict_compact<<<g, 256, 0, s>>>(ix, eff, keys_a, vals_a, n_live);
+  cudaMemcpyAsync(host_n, n_live, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const uint32_t n = *host_n;
+  if (n) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b, vals_a, vals_b, static_cast<int>(n), 0, 32, s);
+    k_evict_gather<<<cdiv(n, 256), 256, 0, s>>>(eff, vals_b, keys_a, n_live);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b, vals_b, vals_a, static_cast<int>(n), 0, 64, s);
+  }
+  const uint32_t v = static_cast<uint32_t>(std::min<uint64_t>(needed, n));
+  if (v) k_evict_mark<<<cdiv(v, 256), 256, 0, s>>>(ix, vals_a, v, victims_h, victims_d);
+  return v;
+}
+
 void launch_record_replay(const Index& ix, const MonCtx& mon, const uint32_t* replay, const uint32_t* n_replay,
                           const unsigned long long* keys, uint32_t n_keys, const uint64_t* users, int grid,
                           cudaStream_t s) {
@@ -2121,7 +2295,7 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
                    const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
-                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, cudaStream_t s) {
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived, cudaStream_t s) {
   const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
 #if SKV_COMMIT_FLAT
@@ -2133,7 +2307,7 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                         late, n_late, err_flag, matched, users64, M, pending_labels);
     k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
     k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
-                                            pending_labels);
+                                            pending_labels, n_revived);
     k_commit_links<<<fix_grid, 256, 0, s>>>(ix, slot, late, n_late, fix_cap);
     return;
   }
@@ -2146,7 +2320,7 @@ ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     pending_labels);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
-                                          pending_labels);
+                                          pending_labels, n_revived);
 }
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,

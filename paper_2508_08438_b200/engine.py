@@ -340,6 +340,23 @@ class AdmissionEngine:
         arr.sort(order=["h", "d"])
         return arr
 
+    def enable_eviction(self) -> None:
+        """Per-entry access epochs and node ids for ``evict`` (before the first admit)."""
+        self._check(self._lib.skv_enable_eviction(self._h))
+
+    def evict(self, needed_blocks: int, epoch: int = 0):
+        """RadixCacheIndex::evict (cache_index.hpp:281-292): frees ``needed_blocks`` entries
+        in the reference's victim order; returns (n_evicted, victim h, victim d).  Raises
+        CapacityExhausted (after freeing every candidate) when fewer could be freed."""
+        n = C.c_uint64()
+        cap = max(int(needed_blocks), 1)
+        vh = np.zeros(cap, np.uint64)
+        vd = np.zeros(cap, np.uint64)
+        rc = self._lib.skv_evict(self._h, needed_blocks, epoch, C.byref(n), _ptr(vh), _ptr(vd), cap)
+        self._evicted = (int(n.value), vh[:n.value], vd[:n.value])
+        self._check(rc)
+        return self._evicted
+
     def entry_count(self) -> int:
         return int(self._lib.skv_entry_count(self._h))
 

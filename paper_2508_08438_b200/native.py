@@ -163,6 +163,9 @@ SIGNATURES = {
     "skv_set_tiers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_export": (C.c_int, [C.c_void_p, C.POINTER(Entry), C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_entry_count": (C.c_uint64, [C.c_void_p]),
+    "skv_enable_eviction": (C.c_int, [C.c_void_p]),
+    "skv_evict": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p,
+                            C.c_size_t]),
     "skv_last_times": (C.c_int, [C.c_void_p, C.POINTER(StageTimes)]),
     "skv_cost_model_default": (None, [C.POINTER(CostModel)]),
     "skv_set_cost_model": (C.c_int, [C.c_void_p, C.POINTER(CostModel)]),

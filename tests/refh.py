@@ -64,6 +64,8 @@ def load_ref():
         "ref_workload_owner": (C.c_uint8, [vp, sz]),
         "ref_workload_truth": (sz, [vp, sz, sz, vp, vp, vp]),
         "ref_rule_corpus": (sz, [sz, C.c_uint64, C.c_char_p, sz, vp]),
+        "ref_engine_evict": (C.c_int, [vp, C.c_uint64, C.c_uint64, u64p]),
+        "ref_engine_current_epoch": (C.c_uint64, [vp]),
     }
     for n, (r, a) in sig.items():
         f = getattr(L, n)
@@ -153,6 +155,13 @@ class RefEngine:
         offsets = np.ascontiguousarray(offsets, np.uint64)
         tiers = np.ascontiguousarray(tiers, np.uint8)
         assert self.L.ref_engine_set_tiers(self.h, _p(tokens), _p(offsets), len(offsets) - 1, _p(tiers)) == 0
+
+    def evict(self, needed):
+        """RadixCacheIndex::evict(needed, current epoch); (rc, nodes freed)."""
+        ep = self.L.ref_engine_current_epoch(self.h)
+        n = C.c_uint64()
+        rc = self.L.ref_engine_evict(self.h, needed, ep, C.byref(n))
+        return rc, int(n.value)
 
     def epoch(self, cap=1 << 16):
         ep = C.c_uint64()

@@ -1,0 +1,77 @@
+"""GPU parity of eviction (RadixCacheIndex::evict / select_victim, cache_index.hpp:281-292,
+697-728, untiered): after batches spread over several monitor epochs (distinct access
+epochs), tier demotions (off-HBM entries never leave and pin their ancestors) and label
+changes, evict(k) on the CUDA index and on the unmodified reference must free the same
+number of entries and leave the same live index; later batches re-insert evicted keys
+(tombstones revive as fresh nodes with new node ids) and every admit, event and index
+dump must still match, through further evictions and a final over-ask (capacity
+exhausted after freeing every candidate)."""
+import numpy as np
+import pytest
+
+from paper_2508_08438_b200 import AdmissionEngine, CapacityExhausted, EngineConfig
+from refh import RefEngine, RefRules
+from test_gpu_parity import check_admit, check_events, check_index
+from workloads import make_batch, make_trunks
+
+pytestmark = pytest.mark.gpu
+
+
+def _step(eng, re_, rs, batch, epoch=True):
+    got = eng.admit(*batch)
+    exp = re_.admit(*batch)
+    check_admit(rs, got, exp)
+    eng.commit()
+    re_.commit()
+    if epoch:
+        ep_g, ev_g = eng.epoch_pass()
+        ep_r, ev_r = re_.epoch(cap=1 << 16)
+        assert ep_g == ep_r
+        check_events(ev_g, ev_r)
+    check_index(eng, re_)
+    return got
+
+
+def _evict(eng, re_, k):
+    rc_r, n_r = re_.evict(k)
+    try:
+        n_g = eng.evict(k)[0]
+        rc_g = 0
+    except CapacityExhausted:
+        n_g, rc_g = eng._evicted[0], 1
+    assert (rc_g, n_g) == (rc_r, n_r)
+    check_index(eng, re_)
+    assert eng.entry_count() == len(re_.export()["h"])
+    return n_g
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_evict_parity(ref, gpu, seed):
+    rng = np.random.default_rng(seed)
+    trunks = make_trunks(rng, 8)
+    B, W = 4, 8
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=1024,
+                       max_tokens=1 << 18, max_window_entries=1 << 14, u_pre_max=3, entropy_jump=0.1)
+    with AdmissionEngine(cfg) as eng:
+        eng.enable_eviction()
+        re_ = RefEngine(ref, RefRules(ref), B=B, W=W, u_pre_max=3, jump=0.1)
+        try:
+            rs = eng.rules
+            for k in range(4):
+                batch = make_batch(rng, trunks, 60, 5)
+                got = _step(eng, re_, rs, batch)
+                if k == 1:  # demote a slice of the index off HBM (those never leave)
+                    tiers = (rng.integers(0, 10, got.n_blocks) >= 8).astype(np.uint8)
+                    eng.set_tiers(got.block_h, got.block_d, tiers, got.block_offsets)
+                    re_.set_tiers(batch[0], batch[1], tiers)
+                    check_index(eng, re_)
+            total = eng.entry_count()
+            assert _evict(eng, re_, total // 5) == total // 5
+            for k in range(3):  # revivals, more epochs
+                _step(eng, re_, rs, make_batch(rng, trunks, 60, 5), epoch=(k != 1))
+            _evict(eng, re_, eng.entry_count() // 3)
+            _step(eng, re_, rs, make_batch(rng, trunks, 40, 5))
+            _evict(eng, re_, 10 ** 6)  # over-ask: frees every candidate, then capacity exhausted
+            _step(eng, re_, rs, make_batch(rng, trunks, 40, 5))
+        finally:
+            re_.close()
