@@ -211,9 +211,12 @@ uint64_t skv_entry_count(skv_ctx* ctx);
  * in the reference's victim order (unpinned HBM leaves, oldest access epoch first, then
  * Public before non-Public, then the smallest node id, repeatedly), leaving tombstones
  * that lookups treat as missing and a later insert of the same key revives as a fresh
- * entry.  Writes the victims' keys (up to cap) and returns SKV_ERR_CAPACITY, after
- * freeing every candidate, when fewer than needed_blocks could be freed. */
-int skv_enable_eviction(skv_ctx* ctx);
+ * entry.  With tiered_demotion (RadixCacheIndex::Config::tiered_demotion, lower tiers
+ * unbounded) a victim is instead demoted HBM -> DRAM and stays a leaf, so the victims are
+ * the smallest-key HBM leaves.  Writes the victims' keys (up to cap) and returns
+ * SKV_ERR_CAPACITY, after freeing every candidate, when fewer than needed_blocks could
+ * be freed. */
+int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
 int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap);
 

@@ -225,6 +225,7 @@ struct RefEngine {
   void* rules_box;
   uint32_t B, W;
   std::unique_ptr<RadixCacheIndex> idx;
+  MonitorConfig mcfg;
   std::unique_ptr<EntropyMonitor> mon;
   std::map<std::vector<uint32_t>, uint32_t> intern;  // block content -> id (exact, hash-free)
   std::vector<uint64_t> id_digest;                     // id -> token_seq_digest(content)
@@ -260,11 +261,27 @@ void* ref_engine_create(void* rules, uint32_t B, uint32_t W, double jump, uint64
   MonitorConfig mc;
   mc.entropy_jump = jump;
   mc.u_pre_max = u_pre_max;
+  e->mcfg = mc;
   e->mon = std::make_unique<EntropyMonitor>(*e->idx, mc);
   return e;
 }
 
 void ref_engine_free(void* e) { delete static_cast<RefEngine*>(e); }
+
+// RadixCacheIndex::Config::tiered_demotion (before any insert): a fresh index and monitor
+// with the same (unbounded) budgets.
+int ref_engine_set_tiered(void* ev, int tiered) {
+  auto* e = static_cast<RefEngine*>(ev);
+  if (!e->pending.empty()) return -1;
+  MonitorConfig mc = e->mcfg;
+  e->mon.reset();
+  RadixCacheIndex::Config cfg;
+  cfg.budget = TierBudget::from_tokens(1ull << 50, 1ull << 50, 1ull << 50);
+  cfg.tiered_demotion = tiered != 0;
+  e->idx = std::make_unique<RadixCacheIndex>(cfg);
+  e->mon = std::make_unique<EntropyMonitor>(*e->idx, mc);
+  return 0;
+}
 
 void ref_engine_set_threads(void* e, int n) { static_cast<RefEngine*>(e)->nthreads = n; }
 
@@ -436,9 +453,16 @@ int ref_engine_commit(void* ev) {
 // (CapacityExhausted) after freeing what it could.
 int ref_engine_evict(void* ev, uint64_t needed, uint64_t epoch, uint64_t* n_out) {
   auto* e = static_cast<RefEngine*>(ev);
+  // nodes holding HBM handles: freeing or demoting a victim removes one
   auto count = [&] {
     uint64_t n = 0;
-    e->idx->for_each_node([&](const CacheNode*) { ++n; });
+    e->idx->for_each_node([&](const CacheNode* nd) {
+      for (const KvHandle& h : nd->kv_handles)
+        if (h.tier == MemTier::HBM) {
+          ++n;
+          break;
+        }
+    });
     return n;
   };
   const uint64_t before = count();

@@ -134,6 +134,7 @@ struct skv_ctx {
   uint32_t* bprompt = nullptr;  // block -> prompt (written by the probe, read by the flat commit)
   // eviction (skv_enable_eviction): bookkeeping array + lazily allocated work buffers
   bool evict_on = false;
+  bool evict_tiered = false;  // victims move HBM -> DRAM instead of leaving
   uint64_t tombstones = 0;  // evicted slots not re-inserted (they keep their slot)
   uint32_t* ev_counts = nullptr;
   uint32_t* ev_incl = nullptr;
@@ -1210,7 +1211,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
 
 uint64_t skv_entry_count(skv_ctx* c) { return c ? c->entries : 0; }
 
-int skv_enable_eviction(skv_ctx* c) {
+int skv_enable_eviction(skv_ctx* c, int tiered_demotion) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
@@ -1229,6 +1230,7 @@ int skv_enable_eviction(skv_ctx* c) {
     sync_check(c->stream);
     c->ix.em = em;
     c->evict_on = true;
+    c->evict_tiered = tiered_demotion != 0;
     return SKV_OK;
   });
 }
@@ -1257,13 +1259,15 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     }
     const uint32_t v = skv::launch_evict(c->ix, needed_blocks, c->ev_eff, c->ev_keys_a, c->ev_keys_b, c->ev_vals_a,
                                          c->ev_vals_b, c->ev_n, c->ev_temp, c->ev_temp_bytes, c->ev_vh, c->ev_vd,
-                                         c->host_small, s);
+                                         c->host_small, c->evict_tiered ? 1 : 0, s);
     const size_t k = std::min<size_t>(v, cap);
     if (victims_h && k) CK(cudaMemcpyAsync(victims_h, c->ev_vh, k * 8, cudaMemcpyDeviceToHost, s));
     if (victims_d && k) CK(cudaMemcpyAsync(victims_d, c->ev_vd, k * 8, cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    c->entries -= v;
-    c->tombstones += v;
+    if (!c->evict_tiered) {
+      c->entries -= v;
+      c->tombstones += v;
+    }
     *n_evicted = v;
     if (v < needed_blocks) throw CapacityError("evict: no unpinned candidate leaf");
     return SKV_OK;

@@ -187,7 +187,8 @@ void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* 
 size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap);
 uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
                       unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
-                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, cudaStream_t s);
+                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, int tiered,
+                      cudaStream_t s);
 void launch_intern_users(const UserTable& t, const uint64_t* users, uint32_t n, uint32_t* uidx, uint32_t* err,
                          cudaStream_t s);
 void launch_ttft(const uint32_t* blk_off, const uint32_t* matched, const uint32_t* plen, const uint8_t* bmeta,

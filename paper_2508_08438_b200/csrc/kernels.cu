@@ -2218,6 +2218,39 @@ __global__ void k_evict_compact(Index ix, const unsigned long long* __restrict__
   vals[i] = static_cast<uint32_t>(s);
 }
 
+// tiered demotion (RadixCacheIndex tiered_demotion, evict_or_demote :743-766, lower tiers
+// unbounded): a victim moves HBM -> DRAM and stays in the tree as a leaf, so no parent is
+// ever exposed and the victims are simply the smallest-key HBM leaves
+__global__ void k_evict_children(Index ix, unsigned long long* flag) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta)) return;
+  if (r.parent != kNone) flag[r.parent] = 1;
+}
+
+__global__ void k_evict_leaves(Index ix, const unsigned long long* __restrict__ flag, unsigned long long* keys,
+                               uint32_t* vals, uint32_t* n_live) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta) || flag[s]) return;
+  const unsigned long long k = evict_key(ix, s);
+  if (k == ~0ull) return;  // not in HBM
+  const uint32_t i = atomicAdd(n_live, 1u);
+  keys[i] = k;
+  vals[i] = static_cast<uint32_t>(s);
+}
+
+__global__ void k_evict_demote(Index ix, const uint32_t* __restrict__ vals, uint32_t v, uint64_t* vh, uint64_t* vd) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v) return;
+  Rec& r = ix.e[vals[i]].rec;
+  r.meta = (r.meta & ~(3u << 3)) | (static_cast<uint32_t>(SKV_TIER_DRAM) << 3);
+  if (vh) vh[i] = r.h;
+  if (vd) vd[i] = r.d;
+}
+
 __global__ void k_evict_gather(const unsigned long long* __restrict__ eff, const uint32_t* __restrict__ vals,
                                unsigned long long* keys, const uint32_t* n_live) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2265,9 +2298,22 @@ size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap) {
 
 uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
                       unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
-                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, cudaStream_t s) {
+                      size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, int tiered,
+                      cudaStream_t s) {
   const unsigned g = static_cast<unsigned>(cdiv(ix.cap, 256));
   cudaMemsetAsync(n_live, 0, 4, s);
+  if (tiered) {
+    cudaMemsetAsync(eff, 0, ix.cap * sizeof(unsigned long long), s);
+    k_evict_children<<<g, 256, 0, s>>>(ix, eff);
+    k_evict_leaves<<<g, 256, 0, s>>>(ix, eff, keys_a, vals_a, n_live);
+    cudaMemcpyAsync(host_n, n_live, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const uint32_t n = *host_n;
+    if (n) cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b, vals_a, vals_b, static_cast<int>(n), 0, 64, s);
+    const uint32_t v = static_cast<uint32_t>(std::min<uint64_t>(needed, n));
+    if (v) k_evict_demote<<<cdiv(v, 256), 256, 0, s>>>(ix, vals_b, v, victims_h, victims_d);
+    return v;
+  }
   k_evict_init<<<g, 256, 0, s>>>(ix, eff);
   k_evict_propagate<<<g, 256, 0, s>>>(ix, eff);
   k_evict_compact<<<g, 256, 0, s>>>(ix, eff, keys_a, vals_a, n_live);

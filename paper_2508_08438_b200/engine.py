@@ -340,9 +340,10 @@ class AdmissionEngine:
         arr.sort(order=["h", "d"])
         return arr
 
-    def enable_eviction(self) -> None:
-        """Per-entry access epochs and node ids for ``evict`` (before the first admit)."""
-        self._check(self._lib.skv_enable_eviction(self._h))
+    def enable_eviction(self, tiered_demotion: bool = False) -> None:
+        """Per-entry access epochs and node ids for ``evict`` (before the first admit);
+        with ``tiered_demotion`` victims move HBM -> DRAM instead of leaving."""
+        self._check(self._lib.skv_enable_eviction(self._h, 1 if tiered_demotion else 0))
 
     def evict(self, needed_blocks: int, epoch: int = 0):
         """RadixCacheIndex::evict (cache_index.hpp:281-292): frees ``needed_blocks`` entries

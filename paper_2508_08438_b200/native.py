@@ -163,7 +163,7 @@ SIGNATURES = {
     "skv_set_tiers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_export": (C.c_int, [C.c_void_p, C.POINTER(Entry), C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_entry_count": (C.c_uint64, [C.c_void_p]),
-    "skv_enable_eviction": (C.c_int, [C.c_void_p]),
+    "skv_enable_eviction": (C.c_int, [C.c_void_p, C.c_int]),
     "skv_evict": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p,
                             C.c_size_t]),
     "skv_last_times": (C.c_int, [C.c_void_p, C.POINTER(StageTimes)]),

@@ -66,6 +66,7 @@ def load_ref():
         "ref_rule_corpus": (sz, [sz, C.c_uint64, C.c_char_p, sz, vp]),
         "ref_engine_evict": (C.c_int, [vp, C.c_uint64, C.c_uint64, u64p]),
         "ref_engine_current_epoch": (C.c_uint64, [vp]),
+        "ref_engine_set_tiered": (C.c_int, [vp, C.c_int]),
     }
     for n, (r, a) in sig.items():
         f = getattr(L, n)
@@ -155,6 +156,9 @@ class RefEngine:
         offsets = np.ascontiguousarray(offsets, np.uint64)
         tiers = np.ascontiguousarray(tiers, np.uint8)
         assert self.L.ref_engine_set_tiers(self.h, _p(tokens), _p(offsets), len(offsets) - 1, _p(tiers)) == 0
+
+    def set_tiered(self, tiered=True):
+        assert self.L.ref_engine_set_tiered(self.h, 1 if tiered else 0) == 0
 
     def evict(self, needed):
         """RadixCacheIndex::evict(needed, current epoch); (rc, nodes freed)."""

@@ -45,16 +45,18 @@ def _evict(eng, re_, k):
     return n_g
 
 
-@pytest.mark.parametrize("seed", [11, 12])
-def test_evict_parity(ref, gpu, seed):
+@pytest.mark.parametrize("seed,tiered", [(11, False), (12, False), (13, True)])
+def test_evict_parity(ref, gpu, seed, tiered):
     rng = np.random.default_rng(seed)
     trunks = make_trunks(rng, 8)
     B, W = 4, 8
     cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=1024,
                        max_tokens=1 << 18, max_window_entries=1 << 14, u_pre_max=3, entropy_jump=0.1)
     with AdmissionEngine(cfg) as eng:
-        eng.enable_eviction()
+        eng.enable_eviction(tiered_demotion=tiered)
         re_ = RefEngine(ref, RefRules(ref), B=B, W=W, u_pre_max=3, jump=0.1)
+        if tiered:
+            re_.set_tiered()
         try:
             rs = eng.rules
             for k in range(4):
@@ -66,7 +68,10 @@ def test_evict_parity(ref, gpu, seed):
                     re_.set_tiers(batch[0], batch[1], tiers)
                     check_index(eng, re_)
             total = eng.entry_count()
-            assert _evict(eng, re_, total // 5) == total // 5
+            if tiered:  # only leaves move (to DRAM), so ask for fewer than there are leaves
+                assert _evict(eng, re_, 50) == 50
+            else:
+                assert _evict(eng, re_, total // 5) == total // 5
             for k in range(3):  # revivals, more epochs
                 _step(eng, re_, rs, make_batch(rng, trunks, 60, 5), epoch=(k != 1))
             _evict(eng, re_, eng.entry_count() // 3)
