@@ -68,7 +68,7 @@ class SecretPlan:
     victim: int                        # victim UserId
     victim_tokens: np.ndarray          # the victim's prompt (u32 tokens)
     known_prefix: np.ndarray           # what the attacker knows precedes the secret
-    candidates: list                   # per position: list of u32 token arrays
+    candidates: list                   # per position: u32 token arrays (a 2-D array when equal length)
     truth: list                        # per position: the true token array
     category: str = ""
 
@@ -175,6 +175,15 @@ class _Campaign:
         self.b, self.s, self.k = backend, settings, max(1, epoch_every)
         self.metrics = CampaignMetrics()
 
+    def run_batch_flat(self, tok, off, users, rids) -> np.ndarray:
+        self.b.admit(tok, off, np.asarray(users, np.uint64))
+        t = self.b.ttft(len(off) - 1, np.asarray(rids, np.uint64))
+        self.b.commit()
+        self.metrics.batches += 1
+        if self.metrics.batches % self.k == 0:
+            self.metrics.leakage_events += self.b.epoch()
+        return t
+
     def run_batch(self, seqs, users, rids=None) -> Optional[np.ndarray]:
         """One admission batch: admit, TTFT (when request ids are given), commit, and the
         monitor epoch every k batches."""
@@ -237,49 +246,59 @@ def run_campaign(backend: Backend, plans: Sequence[SecretPlan], settings: Attack
     active = [True] * n
     npos = max((len(p.candidates) for p in plans), default=0)
     for pos in range(npos):
-        seqs, users, rids, owner = [], [], [], []
+        # one batch: every active secret's candidates for this position, built per secret
+        # as a (candidates x tokens) block (known prefix + recovered blocks + candidate)
+        toks, lens, users, rids, spans = [], [], [], [], []
         for i, p in enumerate(plans):
             if not active[i] or pos >= len(p.candidates):
                 continue
-            base = np.concatenate([p.known_prefix] + [np.asarray(r, np.uint32) for r in res[i].recovered])
-            allowed = max(0, min(len(p.candidates[pos]), settings.max_probes - res[i].probes_used))
-            for j in range(allowed):
-                if settings.pollution == "fresh":
-                    uid = ids[i][rotation[i] % len(ids[i])]
-                    rotation[i] += 1
+            cand = p.candidates[pos]
+            a = max(0, min(len(cand), settings.max_probes - res[i].probes_used))
+            if a:
+                base = np.concatenate([p.known_prefix] + [np.asarray(r, np.uint32) for r in res[i].recovered])
+                if isinstance(cand, np.ndarray) and cand.ndim == 2:
+                    blk = np.hstack([np.broadcast_to(base, (a, len(base))), cand[:a]])
+                    toks.append(blk.ravel())
+                    lens.append(np.full(a, blk.shape[1], np.uint64))
                 else:
-                    uid = ids[i][0]
-                seqs.append(np.concatenate([base, np.asarray(p.candidates[pos][j], np.uint32)]))
-                users.append(uid)
-                rids.append(rid(i))
-                owner.append((i, j))
-            res[i].probes_used += allowed
-            if allowed < len(p.candidates[pos]):
+                    rows = [np.concatenate([base, np.asarray(cand[j], np.uint32)]) for j in range(a)]
+                    toks.append(np.concatenate(rows))
+                    lens.append(np.array([len(r) for r in rows], np.uint64))
+                nid = len(ids[i])
+                if settings.pollution == "fresh":
+                    users.append(np.asarray(ids[i], np.uint64)[(rotation[i] + np.arange(a)) % nid])
+                    rotation[i] += a
+                else:
+                    users.append(np.full(a, ids[i][0], np.uint64))
+                rids.append(10000000 + probe_seq[i] + np.arange(1, a + 1, dtype=np.uint64) + plans[i].secret_id * 100000)
+                probe_seq[i] += a
+                spans.append((i, a))
+            res[i].probes_used += a
+            if a < len(cand):
                 res[i].budget_exhausted = True
                 active[i] = False
-        if not seqs:
+        if not spans:
             break
-        t = cp.run_batch(seqs, users, rids)
-        per = {}
-        for k, (i, j) in enumerate(owner):
-            per.setdefault(i, []).append((j, float(t[k])))
-        for i, obs in per.items():
+        tok = np.concatenate(toks).astype(np.uint32)
+        off = np.zeros(sum(len(x) for x in lens) + 1, np.uint64)
+        np.cumsum(np.concatenate(lens), out=off[1:])
+        t = cp.run_batch_flat(tok, off, np.concatenate(users), np.concatenate(rids))
+        k0 = 0
+        for i, a in spans:
+            tt = np.asarray(t[k0:k0 + a], np.float64)
+            k0 += a
             if not active[i]:
                 continue  # budget ran out inside this position: no pick (reconstruct returns)
-            best_hit, best_hit_t = None, float("inf")
-            best_any, best_any_t = 0, float("inf")
-            any_hit = False
-            for j, tt in obs:
-                if tt < best_any_t:
-                    best_any_t, best_any = tt, j
-                if tt < thr[i]:
-                    any_hit = True
-                    if tt < best_hit_t:
-                        best_hit_t, best_hit = tt, j
+            best_any = int(np.argmin(tt))  # first minimum, as the strict '<' scan
+            hit = tt < thr[i]
+            any_hit = bool(hit.any())
             if not any_hit and had_hit[i]:
                 res[i].downgraded_mid_attack = True
                 res[i].stale_probes += len(plans[i].candidates[pos])
-            pick = best_hit if any_hit else best_any
+            if any_hit:
+                pick = int(np.flatnonzero(hit)[np.argmin(tt[hit])])
+            else:
+                pick = best_any
             res[i].low_confidence.append(not any_hit)
             res[i].recovered.append(np.asarray(plans[i].candidates[pos][pick], np.uint32))
             had_hit[i] = had_hit[i] or any_hit
@@ -351,7 +370,7 @@ def digit_secret_plans(n: int, block_tokens: int, digits: int = 8, seed: int = 1
                 while len(pool) < n_candidates:
                     pool.add(rng.next_below(10 ** k))
                 vals = sorted(pool)
-            cands.append([np.array([ord(c) for c in f"{v:0{k}d}"], np.uint32) for v in vals])
+            cands.append(np.array([[ord(c) for c in f"{v:0{k}d}"] for v in vals], np.uint32))
             truth.append(_text(secret[q * k:(q + 1) * k]))
         plans.append(SecretPlan(secret_id=sid, victim=first_victim + s, victim_tokens=victim, known_prefix=known,
                                 candidates=cands, truth=truth, category="account"))
