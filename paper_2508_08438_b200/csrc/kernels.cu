@@ -1112,7 +1112,10 @@ __device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint
   return Probe{kNone, 0, 0};
 }
 
-__global__ void __launch_bounds__(kCPWarps * 32) k_chain_probe(
+#ifndef SKV_KCP_MINB
+#define SKV_KCP_MINB 1
+#endif
+__global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
     Index ix, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
     const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
