@@ -141,9 +141,8 @@ struct skv_ctx {
   unsigned long long* ev_next_id = nullptr;
   void* ev_temp = nullptr;
   size_t ev_temp_bytes = 0;
-  unsigned long long *ev_eff = nullptr, *ev_keys_a = nullptr, *ev_keys_b = nullptr;
-  uint32_t *ev_vals_a = nullptr, *ev_vals_b = nullptr, *ev_n = nullptr;
-  uint64_t *ev_vh = nullptr, *ev_vd = nullptr;
+  unsigned long long* ev_eff = nullptr;
+  uint32_t* ev_n = nullptr;
   uint32_t* late = nullptr;     // commit: (child slot, parent block) links applied after the claims
   uint8_t* bdecision = nullptr;
   uint32_t* bslot = nullptr;
@@ -1247,23 +1246,27 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     ensure_admit_resolved(c);
     flush_record(c);
     cudaStream_t s = c->stream;
-    if (!c->ev_eff) {  // work buffers, sized by the index capacity, on first use
+    if (!c->ev_eff) {  // per-slot effective keys, on first use
       c->ev_eff = dalloc<unsigned long long>(c->ix.cap, c->owned);
-      c->ev_keys_a = dalloc<unsigned long long>(c->ix.cap, c->owned);
-      c->ev_keys_b = dalloc<unsigned long long>(c->ix.cap, c->owned);
-      c->ev_vals_a = dalloc<uint32_t>(c->ix.cap, c->owned);
-      c->ev_vals_b = dalloc<uint32_t>(c->ix.cap, c->owned);
-      c->ev_vh = dalloc<uint64_t>(c->ix.cap, c->owned);
-      c->ev_vd = dalloc<uint64_t>(c->ix.cap, c->owned);
       c->ev_n = dalloc<uint32_t>(1, c->owned);
     }
-    const uint32_t v = skv::launch_evict(c->ix, needed_blocks, c->ev_eff, c->ev_keys_a, c->ev_keys_b, c->ev_vals_a,
-                                         c->ev_vals_b, c->ev_n, c->ev_temp, c->ev_temp_bytes, c->ev_vh, c->ev_vd,
-                                         c->host_small, c->evict_tiered ? 1 : 0, s);
+    // candidate lists sized by the live entries of this call (40 B each), freed after
+    std::vector<void*> tmp;
+    const uint64_t L = std::max<uint64_t>(c->entries, 1);
+    auto* keys_a = dalloc<unsigned long long>(L, tmp);
+    auto* keys_b = dalloc<unsigned long long>(L, tmp);
+    auto* vals_a = dalloc<uint32_t>(L, tmp);
+    auto* vals_b = dalloc<uint32_t>(L, tmp);
+    auto* vh = dalloc<uint64_t>(L, tmp);
+    auto* vd = dalloc<uint64_t>(L, tmp);
+    const uint32_t v = skv::launch_evict(c->ix, needed_blocks, c->ev_eff, keys_a, keys_b, vals_a, vals_b, c->ev_n,
+                                         c->ev_temp, c->ev_temp_bytes, vh, vd, c->host_small,
+                                         c->evict_tiered ? 1 : 0, s);
     const size_t k = std::min<size_t>(v, cap);
-    if (victims_h && k) CK(cudaMemcpyAsync(victims_h, c->ev_vh, k * 8, cudaMemcpyDeviceToHost, s));
-    if (victims_d && k) CK(cudaMemcpyAsync(victims_d, c->ev_vd, k * 8, cudaMemcpyDeviceToHost, s));
+    if (victims_h && k) CK(cudaMemcpyAsync(victims_h, vh, k * 8, cudaMemcpyDeviceToHost, s));
+    if (victims_d && k) CK(cudaMemcpyAsync(victims_d, vd, k * 8, cudaMemcpyDeviceToHost, s));
     sync_check(s);
+    for (void* p : tmp) cudaFree(p);
     if (!c->evict_tiered) {
       c->entries -= v;
       c->tombstones += v;
