@@ -138,7 +138,7 @@ struct skv_ctx {
   uint64_t tombstones = 0;  // evicted slots not re-inserted (they keep their slot)
   uint32_t* ev_counts = nullptr;
   uint32_t* ev_incl = nullptr;
-  unsigned long long* ev_next_id = nullptr;
+  uint64_t node_next = 1;  // next_node_id_ (cache_index.hpp:832); the root is node 0
   void* ev_temp = nullptr;
   size_t ev_temp_bytes = 0;
   unsigned long long* ev_eff = nullptr;
@@ -1026,18 +1026,22 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, c->rec_stream);
       CK(cudaEventRecord(c->rec_done, c->rec_stream));
     }
-    skv::launch_commit(c->ix, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
+    skv::Index ixc = c->ix;
+    const uint32_t ep32 = static_cast<uint32_t>(c->epoch);
+    if (c->evict_on) {  // speculative node ids: prefix over prompts of the blocks each would create
+      skv::launch_node_bases(c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl, c->ev_temp, c->ev_temp_bytes, s);
+      ixc.em_base = c->ev_incl;
+      ixc.em_next = static_cast<uint32_t>(c->node_next);
+      ixc.em_epoch = ep32;
+    }
+    skv::launch_commit(ixc, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users,
                        rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
                        c->n_sm, c->bprompt, c->late, c->counters + 11, c->counters + 12, s);
     if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
     uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
-    if (c->evict_on) {  // insert walk epochs + node ids of the created blocks
-      skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off, c->p_n, static_cast<uint32_t>(c->epoch), c->ev_counts,
-                               c->ev_incl, c->ev_next_id, c->ev_temp, c->ev_temp_bytes, s);
-      launched += 4;
-    }
+    if (c->evict_on) launched += 2;
     if (rec) finish_record(c, s);
     CK(cudaEventRecord(c->ev[6], s));
     unsigned long long nn = 0;
@@ -1045,12 +1049,25 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 7, c->counters + 7, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
     if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
     std::memcpy(&nn, c->host_small, 8);
     if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
     if (rec) launched += replay_record(c, s, c->host_small[5], c->host_small[4]);
     const uint32_t revived = c->host_small[6];
+    if (c->evict_on) {
+      // the insert walk refreshes every pre-existing block's access epoch; node ids are exact
+      // already unless the batch had duplicate claims
+      skv::launch_path_epochs(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, ep32, s);
+      launched += 1;
+      if (c->host_small[7] || !skv::node_ids_speculative()) {
+        skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl,
+                                 c->node_next, c->ev_temp, c->ev_temp_bytes, s);
+        launched += 3;
+      }
+      c->node_next += nn + revived;
+    }
     c->entries += nn + revived;
     c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
     nn += revived;
@@ -1221,9 +1238,6 @@ int skv_enable_eviction(skv_ctx* c, int tiered_demotion) {
     const uint64_t N = std::max<uint64_t>(c->max_prompts, 1);
     c->ev_counts = dalloc<uint32_t>(N, c->owned);
     c->ev_incl = dalloc<uint32_t>(N, c->owned);
-    c->ev_next_id = dalloc<unsigned long long>(1, c->owned);
-    const unsigned long long one = 1;  // next_node_id_ (cache_index.hpp:832); the root is node 0
-    CK(cudaMemcpyAsync(c->ev_next_id, &one, 8, cudaMemcpyHostToDevice, c->stream));
     c->ev_temp_bytes = skv::evict_temp_bytes(static_cast<uint32_t>(N), c->ix.cap);
     c->ev_temp = dalloc<uint8_t>(c->ev_temp_bytes, c->owned);
     sync_check(c->stream);

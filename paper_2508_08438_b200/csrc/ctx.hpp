@@ -137,6 +137,10 @@ struct Index {
   Entry* e = nullptr;
   uint64_t cap = 0, mask = 0;
   EvictMeta* em = nullptr;  // null unless eviction is enabled
+  // per commit (eviction enabled): speculative node-id bases (exclusive prefix over prompts of
+  // the blocks each would create), the next node id and the insert epoch
+  const uint32_t* em_base = nullptr;
+  uint32_t em_next = 0, em_epoch = 0;
 };
 
 // Monitor user sets (AccessStats::user_set, access_stats.hpp:21-37), one per entry touched
@@ -181,9 +185,14 @@ void launch_init_entries(const Index& ix, cudaStream_t s);
 // of every committed block at commit; evict(needed) = effective keys, sort, tombstones
 void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,
                           uint32_t n, uint32_t epoch, cudaStream_t s);
-void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, uint32_t n, uint32_t epoch,
-                         uint32_t* counts, uint32_t* base, unsigned long long* next_id, void* temp, size_t temp_bytes,
-                         cudaStream_t s);
+bool node_ids_speculative();
+void launch_node_bases(const uint32_t* blk_off, const uint32_t* exist, uint32_t n, uint32_t* counts, uint32_t* base,
+                       void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_path_epochs(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist,
+                        uint32_t n, uint32_t epoch, cudaStream_t s);
+void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist,
+                         uint32_t n, uint32_t* counts, uint32_t* incl, uint64_t next_id, void* temp,
+                         size_t temp_bytes, cudaStream_t s);
 size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap);
 uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
                       unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,

@@ -1473,7 +1473,11 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
         // linked by the fix-up pass)
         const uint32_t meta = make_meta(pending_labels ? SKV_LABEL_PENDING : lab[r], owner, SKV_TIER_HBM, p);
         *reinterpret_cast<uint4*>(&e.rec.creator) = make_uint4(creator, meta, par[r], own_child[r]);
-        if (ix.em) ix.em[s32[r]] = EvictMeta{0u, kNone, base + 32 * r + lane, 0u};
+        if (ix.em) {  // speculative node id: exact unless this batch has duplicate claims
+          const uint32_t b = base + 32 * r + lane, f = n - k0, j = b - k0;
+          const uint32_t X = ix.em_next + ix.em_base[p];
+          ix.em[s32[r]] = EvictMeta{ix.em_epoch, j + 1 < f ? X + 1 + j : X, b, 0u};
+        }
         // the parent link: under a parent that existed before the batch children race ->
         // exchange; under a parent this prompt claimed, the parent's own 16-B store wrote
         // the link, except across iterations (plain store); under a parent another
@@ -1758,8 +1762,9 @@ __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, c
       ix.e[s].stats = Stats{0u, 0u, 0u, 0u};
       ix.e[s].aux.set_idx = kNone;
       ix.e[s].aux.mark = 0;
-      ix.em[s].node_id = kNone;
+      ix.em[s].node_id = kNone;  // assigned by the exact pass (duplicate claims exist)
       ix.em[s].depth = b;
+      ix.em[s].access_epoch = ix.em_epoch;
       atomicAdd(n_revived, 1u);
     }
     // the duplicate claimant's own child under this entry (k_commit left it unlinked)
@@ -2154,42 +2159,55 @@ __global__ void k_touch_matched(Index ix, const uint32_t* __restrict__ slot, con
   for (uint32_t b = lane_id(); b < m; b += 32) ix.em[slot[bo + b]].access_epoch = epoch;
 }
 
-// pass 1: every block of the prompt was walked by its insert -> access epoch; count the
-// blocks this prompt created (node id still unassigned, claimed by this prompt)
+// Node ids (cache_index.hpp:193,537): insert() allocates id X for a prompt's new suffix
+// node, ensure_boundary then splits off its top block f-1 times, each split's upper half
+// taking the next id -- block j of the f created blocks gets X+1+j, the deepest keeps X;
+// X runs over the prompts in order.  The commit writes these ids speculatively with
+// f = blocks missing before the batch; only a batch with duplicate claims (a lower prompt
+// creating a block first, or a tombstone re-inserted) needs the exact pass below.
+__global__ void k_nodes_spec(const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist, uint32_t n,
+                             uint32_t* counts) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) counts[p] = blk_off[p + 1] - blk_off[p] - exist[p];
+}
+
+// every block before the prompt's first new one was walked by its insert: access epoch
+__global__ void k_path_epochs(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                              const uint32_t* __restrict__ exist, uint32_t n, uint32_t epoch) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const uint32_t bo = blk_off[p], k0 = exist[p];
+  for (uint32_t b = lane_id(); b < k0; b += 32) ix.em[slot[bo + b]].access_epoch = epoch;
+}
+
+// exact pass, 1: blocks this prompt created = new blocks whose final claimant it is
 __global__ void k_nodes_count(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
-                              uint32_t n, uint32_t epoch, uint32_t* counts) {
+                              const uint32_t* __restrict__ exist, uint32_t n, uint32_t* counts) {
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n) return;
   const uint32_t bo = blk_off[p], nb = blk_off[p + 1] - bo;
   uint32_t f = 0;
-  for (uint32_t b = lane_id(); b < nb; b += 32) {
+  for (uint32_t b = exist[p] + lane_id(); b < nb; b += 32) {
     const uint32_t s = slot[bo + b];
-    if (s == kNone) continue;
-    ix.em[s].access_epoch = epoch;
-    f += (ix.em[s].node_id == kNone && meta_prompt(ix.e[s].rec.meta) == p) ? 1u : 0u;
+    f += (s != kNone && meta_prompt(ix.e[s].rec.meta) == p) ? 1u : 0u;
   }
   f = __reduce_add_sync(kFull, f);
   if (lane_id() == 0) counts[p] = f;
 }
 
-// pass 2: insert() allocates id X for the new suffix node, ensure_boundary then splits
-// off its top block f-1 times, each split's upper half taking the next id: block j of
-// the f created blocks gets X+1+j, the deepest keeps X (cache_index.hpp:193,537)
+// exact pass, 2: the created blocks are the prompt's last f (a lower prompt sharing block
+// b shares every block before it)
 __global__ void k_nodes_assign(Index ix, const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
                                uint32_t n, const uint32_t* __restrict__ counts, const uint32_t* __restrict__ incl,
-                               const unsigned long long* next_id) {
+                               uint64_t next_id) {
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n) return;
   const uint32_t f = counts[p];
   if (!f) return;
   const uint32_t bo = blk_off[p], nb = blk_off[p + 1] - bo, k = nb - f;
-  const unsigned long long X = *next_id + incl[p] - f;
+  const uint64_t X = next_id + incl[p] - f;
   for (uint32_t j = lane_id(); j < f; j += 32)
     ix.em[slot[bo + k + j]].node_id = static_cast<uint32_t>(j + 1 < f ? X + 1 + j : X);
-}
-
-__global__ void k_nodes_bump(unsigned long long* next_id, const uint32_t* incl, uint32_t n) {
-  if (n) *next_id += incl[n - 1];
 }
 
 __global__ void k_evict_init(Index ix, unsigned long long* eff) {
@@ -2278,15 +2296,28 @@ void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t*
   if (n) k_touch_matched<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, slot, blk_off, matched, n, epoch);
 }
 
-void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, uint32_t n, uint32_t epoch,
-                         uint32_t* counts, uint32_t* incl, unsigned long long* next_id, void* temp, size_t temp_bytes,
-                         cudaStream_t s) {
+bool node_ids_speculative() { return !SKV_COMMIT_FLAT; }  // the flat commit leaves them to the exact pass
+
+void launch_node_bases(const uint32_t* blk_off, const uint32_t* exist, uint32_t n, uint32_t* counts, uint32_t* base,
+                       void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (!n) return;
+  k_nodes_spec<<<cdiv(n, 256), 256, 0, s>>>(blk_off, exist, n, counts);
+  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, base, n, s);
+}
+
+void launch_path_epochs(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist,
+                        uint32_t n, uint32_t epoch, cudaStream_t s) {
+  if (n) k_path_epochs<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(ix, slot, blk_off, exist, n, epoch);
+}
+
+void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist,
+                         uint32_t n, uint32_t* counts, uint32_t* incl, uint64_t next_id, void* temp,
+                         size_t temp_bytes, cudaStream_t s) {
   if (!n) return;
   const unsigned g = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n) * 32, 256));
-  k_nodes_count<<<g, 256, 0, s>>>(ix, slot, blk_off, n, epoch, counts);
+  k_nodes_count<<<g, 256, 0, s>>>(ix, slot, blk_off, exist, n, counts);
   cub::DeviceScan::InclusiveSum(temp, temp_bytes, counts, incl, n, s);
   k_nodes_assign<<<g, 256, 0, s>>>(ix, slot, blk_off, n, counts, incl, next_id);
-  k_nodes_bump<<<1, 1, 0, s>>>(next_id, incl, n);
 }
 
 size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap) {

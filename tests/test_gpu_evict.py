@@ -80,3 +80,36 @@ def test_evict_parity(ref, gpu, seed, tiered):
             _step(eng, re_, rs, make_batch(rng, trunks, 40, 5))
         finally:
             re_.close()
+
+
+def test_evict_speculative_node_ids(ref, gpu):
+    """Batches without duplicate claims take the commit's speculative node ids (no exact
+    pass); eviction order among equal-epoch, equal-label leaves then rests on them."""
+    rng = np.random.default_rng(21)
+    B, W = 4, 8
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=1024,
+                       max_tokens=1 << 18, max_window_entries=1 << 14)
+
+    def unique_batch(n):
+        toks, off = [], [0]
+        for _ in range(n):
+            t = rng.integers(ord("a"), ord("z") + 1, int(rng.integers(8, 80))).astype(np.uint32)
+            if rng.random() < 0.3:  # some private tails
+                t = np.concatenate([t, np.frombuffer(b"ssn 123-45-6789 ok", np.uint8).astype(np.uint32)])
+            toks.append(t)
+            off.append(off[-1] + len(t))
+        return (np.concatenate(toks), np.array(off, np.uint64), rng.integers(1, 6, n).astype(np.uint64),
+                np.zeros(n, np.uint8))
+
+    with AdmissionEngine(cfg) as eng:
+        eng.enable_eviction()
+        re_ = RefEngine(ref, RefRules(ref), B=B, W=W)
+        try:
+            rs = eng.rules
+            for _ in range(3):
+                _step(eng, re_, rs, unique_batch(50), epoch=False)
+            _evict(eng, re_, eng.entry_count() // 3)
+            _step(eng, re_, rs, unique_batch(50))
+            _evict(eng, re_, eng.entry_count() // 2)
+        finally:
+            re_.close()
