@@ -1,12 +1,12 @@
 """B200-native SafeKV admission hot path (hash -> rule-tier scan -> privacy-aware index
 lookup -> entropy monitor) behind the C ABI of include/safekv_b200.h."""
-from .native import (CapacityExhausted, CompileError, ConfigError, CudaError, ParseError, SkvError, StateError,
-                     load_library)
+from .native import (ArgError, CapacityExhausted, CompileError, ConfigError, CudaError, ParseError, SkvError,
+                     StateError, load_library)
 from .engine import (AdmissionEngine, AdmitResult, AnomalyEvent, EngineConfig, GenSpec, RuleSet, generate,
                      generate_pool, route, split_batch)
 
 __all__ = [
     "AdmissionEngine", "AdmitResult", "AnomalyEvent", "EngineConfig", "GenSpec", "RuleSet", "generate",
-    "generate_pool", "route", "split_batch", "load_library", "SkvError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
+    "generate_pool", "route", "split_batch", "load_library", "SkvError", "ArgError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
     "CudaError", "StateError",
 ]
