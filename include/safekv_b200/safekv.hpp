@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <utility>
 #include <vector>
 
 #include "../safekv_b200.h"
@@ -300,6 +301,21 @@ class AdmissionIndex {
     ok(skv_admit_ttft(ctx_, request_ids ? request_ids->data() : nullptr, s.ttft_ms.data(), s.intra_tokens.data(),
                       s.inter_tokens.data(), 0));
     return s;
+  }
+
+  // RadixCacheIndex::evict (cache_index.hpp:281-292).  enable_eviction() must precede
+  // the first admit (RadixCacheIndex::Config::tiered_demotion selects demotion to DRAM
+  // instead of freeing).  Returns the victims' keys (h, d); throws CapacityExhausted, like
+  // the reference, when fewer than needed blocks could be freed.
+  void enable_eviction(bool tiered_demotion = false) { ok(skv_enable_eviction(ctx_, tiered_demotion ? 1 : 0)); }
+  std::vector<std::pair<uint64_t, uint64_t>> evict(uint64_t needed_blocks, uint64_t epoch = 0) {
+    std::vector<uint64_t> h(needed_blocks), d(needed_blocks);
+    uint64_t n = 0;
+    const int rc = skv_evict(ctx_, needed_blocks, epoch, &n, h.data(), d.data(), h.size());
+    std::vector<std::pair<uint64_t, uint64_t>> out;
+    for (uint64_t i = 0; i < n && i < h.size(); ++i) out.emplace_back(h[i], d[i]);
+    ok(rc);
+    return out;
   }
 
   uint64_t entry_count() { return skv_entry_count(ctx_); }

@@ -244,6 +244,26 @@ int main() {
     neg.tier_penalty_ms[2] = 0.5;
     CHECK(throws<ConfigError>([&] { ix.set_cost_model(neg); }));
   }
+  // eviction (cache_index.hpp:281-292): oldest access epoch first; an evicted key is gone
+  // for lookups until it is inserted again
+  {
+    skv_config cfg = small_cfg(4);
+    AdmissionIndex ix(&cfg);
+    ix.enable_eviction();
+    const std::string a = "aaaabbbbccccdddd", b = "eeeeffffgggghhhh";
+    TokenSeq sa(a.begin(), a.end()), sb(b.begin(), b.end());
+    CHECK(ix.insert(sa, UserId{1}, OwnerClass::Customer) == 4);
+    ix.epoch_pass();  // sa's blocks keep the older access epoch
+    CHECK(ix.insert(sb, UserId{2}, OwnerClass::Customer) == 4);
+    auto victims = ix.evict(4);
+    CHECK(victims.size() == 4);
+    CHECK(ix.entry_count() == 4);
+    CHECK(ix.match_prefix(sa, UserId{9}).matched_tokens == 0);   // evicted
+    CHECK(ix.match_prefix(sb, UserId{9}).matched_tokens == 16);  // kept
+    CHECK(ix.insert(sa, UserId{1}, OwnerClass::Customer) == 4);  // re-inserted as fresh entries
+    CHECK(ix.match_prefix(sa, UserId{9}).matched_tokens == 16);
+    CHECK(throws<CapacityExhausted>([&] { ix.evict(100); }));
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
