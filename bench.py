@@ -38,7 +38,25 @@ CFG2 = dict(n_prompts=65536, prompt_tokens=2048, block_tokens=16, window_tokens=
 # 256 users, mixed PII density (60% none / 30% one per 2 KiB / 10% one per 256 B)
 CFG3 = dict(n_prompts=131072, prompt_tokens=4096, block_tokens=16, window_tokens=32, n_users=256,
             pool_size=256, pool_tokens=640, pii_per_kib=0.0, pii_mix=1, seed=3, name="config 3")
-CONFIGS = {2: CFG2, 3: CFG3}
+# BASELINE.json configs[3] (--workload 4): 4,096 long-context queries x 32,768 tokens in 128-token
+# blocks per step, against a pre-built index of 39,063 stored sequences x 256 blocks (10.0 M entries)
+# whose tier tags are derive_seed(seed, entry) mod 10 -> 0-1 HBM, 2-4 DRAM, 5-9 SSD; each query is a
+# uniform-length prefix of a stored sequence + fresh text; stored text carries
+# ~0.65 PII phrases per sequence, so about half of the prefixes stay Public (long visible matches)
+CFG4 = dict(n_prompts=4096, prompt_tokens=32768, block_tokens=128, window_tokens=32, n_users=64,
+            pool_size=256, pool_tokens=640, pii_per_kib=0.02, pii_mix=0, seed=4, name="config 4",
+            stored=39063, stored_chunk=2048)
+CONFIGS = {2: CFG2, 3: CFG3, 4: CFG4}
+
+
+def derive_seed_np(root: int, tags: np.ndarray) -> np.ndarray:
+    """util.hpp derive_seed over an array of tags (SplitMix64 with uint64 wrap-around)."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(root) ^ (np.uint64(0x51A1C9E3B7D24F85) * (tags.astype(np.uint64) + np.uint64(1)))
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
 METRIC = "KV blocks admitted/sec (hash+scan+lookup+monitor) and % HBM roofline, 1/2/4/8 B200"
 UNIT = "blocks/s"
 CPU_STEPS = 6
@@ -203,7 +221,7 @@ def run_ours(args):
     # index sized for HBM: load factor <= ~1/6 after the run (34 GB at the default run
     # length), so linear probing almost never leaves the home slot; ranks sharing a device
     # split half of its memory, never below load 0.6
-    need = (n_batches + 1) * blocks_per_batch
+    need = (n_batches + 1) * blocks_per_batch + c.get("stored", 0) * (L // B)
     ranks_per_dev = -(-world // max(torch.cuda.device_count(), 1))
     budget = torch.cuda.get_device_properties(gpu).total_memory // 2 // ranks_per_dev // 64
     cap = 1 << max(20, min(int(np.ceil(np.log2(need * 6))), int(np.floor(np.log2(max(budget, 1))))),
@@ -211,7 +229,8 @@ def run_ours(args):
     if args.index_log2:
         cap = 1 << args.index_log2
     ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
-                        max_prompts=n_local, max_tokens=n_local * L, max_window_entries=1 << 18,
+                        max_prompts=n_local, max_tokens=n_local * L,
+                        max_window_entries=1 << (20 if args.workload == 4 else 18),  # entries touched per window
                         device=gpu)
 
     # ---- inputs: distinct batches, generated into pinned host memory, copied to HBM
@@ -222,11 +241,34 @@ def run_ours(args):
                    pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
                    route_world=world, route_rank=rank, route_block_tokens=B)
     host, devb = [], []
+    stored = None
+    if args.workload == 4:  # the stored sequences of the pre-built index (host, chunked)
+        sspec = GenSpec(n_prompts=c["stored_chunk"], prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
+                        pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"])
+        stored = []
+        for s0 in range(0, c["stored"], c["stored_chunk"]):
+            sspec.n_prompts = min(c["stored_chunk"], c["stored"] - s0)
+            sspec.prompt_id_base = s0
+            t, o, u, w = generate(sspec)
+            stored.append((t, o, u, w))
+        stored_tok = np.concatenate([t for t, _, _, _ in stored]).reshape(c["stored"], L)
     for k in range(n_batches):
         spec.prompt_id_base = (k + 1) * 100_000_000
         tok_pin = torch.empty(n_local * L, dtype=torch.int32, pin_memory=True)
         tok_np = tok_pin.numpy().view(np.uint32)
-        _, off, users, owners = generate(spec, tokens_out=tok_np)
+        if args.workload == 4:  # a uniform-length prefix of a stored sequence + fresh text
+            rng = np.random.default_rng(c["seed"] * 1000 + k)
+            picks = rng.integers(0, c["stored"], n_local)
+            cuts = rng.integers(0, L + 1, n_local)
+            q = tok_np.reshape(n_local, L)
+            q[:] = rng.integers(ord("a"), ord("z") + 1, (n_local, L), dtype=np.uint32)
+            for i in range(n_local):
+                q[i, :cuts[i]] = stored_tok[picks[i], :cuts[i]]
+            off = np.arange(n_local + 1, dtype=np.uint64) * np.uint64(L)
+            users = rng.integers(1, c["n_users"] + 1, n_local).astype(np.uint64)
+            owners = np.zeros(n_local, np.uint8)
+        else:
+            _, off, users, owners = generate(spec, tokens_out=tok_np)
         # every host input of the e2e arm lives in pinned memory (async H2D)
         pins = [torch.from_numpy(a.view(v)).pin_memory() for a, v in
                 ((off, np.int64), (users, np.int64), (owners, np.uint8))]
@@ -241,8 +283,19 @@ def run_ours(args):
 
     def fresh_engine():
         eng = AdmissionEngine(ecfg)
-        eng.admit(*pool)
-        eng.commit()
+        if stored is not None:  # the tiered 10 M-entry index
+            first = 0
+            for t, o, u, w in stored:
+                r = eng.admit(t, o, u, w)
+                eng.commit()
+                tiers = (derive_seed_np(c["seed"], np.arange(first, first + r.n_blocks, dtype=np.uint64))
+                         % np.uint64(10)).astype(np.uint8)
+                tiers = np.where(tiers < 2, 0, np.where(tiers < 5, 1, 2)).astype(np.uint8)
+                eng.set_tiers(r.block_h, r.block_d, tiers, r.block_offsets)
+                first += r.n_blocks
+        else:
+            eng.admit(*pool)
+            eng.commit()
         eng.epoch_pass()
         return eng
 
@@ -345,7 +398,7 @@ def run_ours(args):
         except Exception:
             traffic = None
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and args.workload != 4:
         # a bounded sample (~10 s of CPU work): CPU_STEPS timed batches of --cpu-sample
         # prompts after one warm-up batch, same generator, pool pre-inserted
         r = cpu_reference_run(steps=CPU_STEPS, warmup=1, sample_prompts=args.cpu_sample,
@@ -384,7 +437,10 @@ def run_ours(args):
         "ms_per_step": ms_dev / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32 tokens / u64 keys (integer), f64 entropy", "data": "synthetic (deterministic generator)",
         "config": {"workload": f"{c['name']}: {n_local} prompts x {L} tokens per GPU per step, B={B}, "
-                               f"W={c['window_tokens']}, {c['n_users']} users, 256x640-token pool pre-inserted",
+                               f"W={c['window_tokens']}, {c['n_users']} users, " +
+                               (f"{c['stored']} x {L}-token stored sequences pre-inserted with HBM/DRAM/SSD tier "
+                                "tags, queries = uniform prefixes of them + fresh text" if args.workload == 4
+                                else "256x640-token pool pre-inserted"),
                    "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
                    "step": "admit + commit + epoch",
                    "index": f"{cap} slots x 64 B ({cap * 64 / 2**30:.0f} GiB), load {need / cap:.2f} at run end",
@@ -423,7 +479,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", type=int, default=2, choices=sorted(CONFIGS),
-                    help="BASELINE.json config (2 = the headline, default; 3 = the per-GPU shard of config 3)")
+                    help="BASELINE.json config (2 = the headline, default; 3 = the per-GPU shard of config 3; "
+                         "4 = long context over a 10 M-entry tiered index)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
     args = ap.parse_args()

@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
   const uint32_t Wp = min(W, B), kc = min(kConv, Wp);
   const uint32_t start_row = a.rules.start_row, eos2 = a.rules.eos2;
   const bool b16 = B == 16 && W >= kConv;
+  const bool bseg = B > 16 && B % 16 == 0;  // long blocks: 16-token segments with 256-bit loads
   const bool defer = W <= 2 * B && B <= 16;  // every flagged segment fits one 16-token task
   // prompt metadata of prompts pbase .. pbase+32 held in lanes (so = first block, st = first
   // token); reloaded only when a chunk reaches past it
@@ -590,6 +591,52 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
         X = SW = row;
         A = alo | amid;
         cw0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+      } else if (bseg && (al & 3) == 0) {
+        // B = 16k: the block in 16-token segments (two 256-bit loads each), byte-token FNV
+        // steps; a segment with a token >= 256 switches the digest to update_u32 over the
+        // whole block (recomputed after the run)
+        uint64_t h = a.digest_init;
+        bool wide = false;
+        uint32_t row = start_row;
+        for (uint32_t k0 = 0; k0 < B; k0 += 16) {
+          uint32_t t[16];
+          ldg_tokens16(tk0 + ws + k0, t, ((al + k0) & 7) == 0);
+          uint32_t any = 0;
+#pragma unroll
+          for (uint32_t k = 0; k < 16; ++k) any |= t[k];
+          if (any >> 8) {
+            wide = true;
+#pragma unroll
+            for (uint32_t k = 0; k < 16; ++k) t[k] &= 0xffu;
+          }
+#pragma unroll
+          for (uint32_t k = 0; k < 16; ++k) {
+            const uint32_t gk = k0 + k;
+            if (!wide) h = fnv_tok(h, t[k]);
+            const uint32_t ck = cmap[t[k]];
+            row = lds16(tab, row + ck);
+            if (gk < kc) {
+              A |= row;
+            } else if (gk < Wp) {
+              amid |= row;
+            } else {
+              A |= row;
+            }
+            if (gk + 1 == kc) Z = row;
+            if (gk + 1 == Wp) SW = row;
+            if (gk < 4) cw0 |= ck << (8 * gk);
+          }
+        }
+        if (wide) {
+#pragma unroll 1
+          for (uint32_t k = 0; k < B; ++k) dg = fnv_u32(dg, tk0[ws + k]);
+        } else {
+          dg = h;
+        }
+        if (kc == 0) Z = start_row;
+        if (Wp == 0) SW = start_row;
+        X = row;
+        A |= amid;
       } else {  // generic shape / alignment: token by token
         uint32_t row = start_row;
         for (uint32_t k = 0; k < B; ++k) {
