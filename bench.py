@@ -46,7 +46,13 @@ CFG3 = dict(n_prompts=131072, prompt_tokens=4096, block_tokens=16, window_tokens
 CFG4 = dict(n_prompts=4096, prompt_tokens=32768, block_tokens=128, window_tokens=32, n_users=64,
             pool_size=256, pool_tokens=640, pii_per_kib=0.02, pii_mix=0, seed=4, name="config 4",
             stored=39063, stored_chunk=2048)
-CONFIGS = {2: CFG2, 3: CFG3, 4: CFG4}
+# BASELINE.json configs[4] (--workload 5): adversarial probing mix -- batches of 4,096 config-2-shaped
+# prompts in which every 10th prompt is an attacker probe (identities >= 1,000,000 rotated over 4,
+# adversary.hpp:30,88-90): a victim prompt of the batch cut after a random number of whole blocks plus
+# one candidate token (the known prefix + recovered + candidate shape of adversary.hpp:114-116); the
+# monitor epoch runs after every batch (K = 1)
+CFG5 = dict(CFG2, n_prompts=4096, seed=5, name="config 5")
+CONFIGS = {2: CFG2, 3: CFG3, 4: CFG4, 5: CFG5}
 
 
 def derive_seed_np(root: int, tags: np.ndarray) -> np.ndarray:
@@ -240,7 +246,7 @@ def run_ours(args):
     spec = GenSpec(n_prompts=n_local, prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
                    pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
                    route_world=world, route_rank=rank, route_block_tokens=B)
-    host, devb = [], []
+    host, devb, ntok, nblk = [], [], [], []
     stored = None
     if args.workload == 4:  # the stored sequences of the pre-built index (host, chunked)
         sspec = GenSpec(n_prompts=c["stored_chunk"], prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
@@ -269,6 +275,24 @@ def run_ours(args):
             owners = np.zeros(n_local, np.uint8)
         else:
             _, off, users, owners = generate(spec, tokens_out=tok_np)
+            if args.workload == 5:  # every 10th prompt becomes an attacker probe
+                rng = np.random.default_rng(c["seed"] * 1000 + k)
+                rows = tok_np.reshape(n_local, L)
+                lens = np.full(n_local, L, np.int64)
+                for i in range(0, n_local, 10):
+                    v = int(rng.integers(0, n_local))
+                    cut = int(rng.integers(1, L // B)) * B
+                    rows[i, :cut] = rows[v, :cut]
+                    rows[i, cut] = ord("0") + int(rng.integers(0, 10))
+                    lens[i] = cut + 1
+                    users[i] = 1_000_000 + (k * 4 + i // 10) % 4
+                # compact the variable-length prompts to the front of the pinned buffer
+                flat = np.concatenate([rows[i, :lens[i]] for i in range(n_local)])
+                tok_np[:len(flat)] = flat
+                off = np.zeros(n_local + 1, np.uint64)
+                np.cumsum(lens, out=off[1:])
+        ntok.append(int(off[-1]))
+        nblk.append(int(((off[1:] - off[:-1]) // np.uint64(B)).sum()))
         # every host input of the e2e arm lives in pinned memory (async H2D)
         pins = [torch.from_numpy(a.view(v)).pin_memory() for a, v in
                 ((off, np.int64), (users, np.int64), (owners, np.uint8))]
@@ -301,12 +325,12 @@ def run_ours(args):
 
     def dev_batch(k):
         t, o, u, w = devb[k]
-        return N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, n_local * L, 1)
+        return N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, ntok[k], 1)
 
     def host_batch(k):
         _, tok, off, users, owners, _ = host[k]
         return N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
-                       n_local * L, 0)
+                       ntok[k], 0)
 
     # one step = admit(k) [+ stage batch k+1's stages 1-2 (and, e2e, its H2D) on the side
     # stream, overlapping] + commit(k) + epoch; nxt is None at the edge of a timed region
@@ -381,13 +405,16 @@ def run_ours(args):
         # launch runs alone on the GPU (in the pipelined pass it shares HBM with k_commit)
         _, hs, _, _, _ = timed(step_device, pipe=False)
 
-    total_blocks = blocks_per_batch * steps * world
+    # blocks and tokens actually admitted in the timed steps (probes of config 5 are short)
+    timed_blocks = float(np.mean(nblk[warm:warm + steps]))
+    timed_tokens = float(np.mean(ntok[warm:warm + steps]))
+    total_blocks = timed_blocks * steps * world
     value = total_blocks / (ms_dev / 1e3)
     e2e_value = total_blocks / (ms_e2e / 1e3)
     # roofline of the dominant kernel (k_hash_scan): algorithmic bytes per launch =
     # 4 B/token read once + 8 B digest + 4 B rule mask written per block
     hs_avg = float(np.mean(hs))
-    alg_bytes = 4 * n_local * L + 12 * blocks_per_batch
+    alg_bytes = 4 * timed_tokens + 12 * timed_blocks
     achieved = alg_bytes / (hs_avg / 1e3) / 1e9
     peak, kind = peaks()
     traffic = None
@@ -405,7 +432,8 @@ def run_ours(args):
                               threads=os.cpu_count() or 1, c=c)
         if r is not None:
             cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of {c['name']} after 1 warm-up batch "
+                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of {c['name']}"
+                             f"{' (benign prompts only)' if args.workload == 5 else ''} after 1 warm-up batch "
                              f"(pool pre-inserted): {r['blocks']} blocks in {r['seconds']:.1f} s"}
     # where the rest of the step goes: the commit is bound by random 128-bit CAS into the
     # index (one claim per new block), measured against the randmem ceiling
@@ -430,8 +458,8 @@ def run_ours(args):
         "note": "commit_ms includes the batch's monitor records (run inside k_commit); hash/scan of the next "
                 "batch overlaps it on a side stream",
     }
-    h2d = n_local * L * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
-    d2h = blocks_per_batch + n_local * 4
+    h2d = int(timed_tokens) * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
+    d2h = int(timed_blocks) + n_local * 4
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": ms_dev / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
