@@ -1166,6 +1166,9 @@ __device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint
 #ifndef SKV_KCP_MINB
 #define SKV_KCP_MINB 1
 #endif
+#ifndef SKV_KCP_GRID_PER_SM
+#define SKV_KCP_GRID_PER_SM 0  // > 0: at most this many CTAs per SM; warps stride over prompt groups
+#endif
 __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
     Index ix, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
     const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
@@ -1175,8 +1178,9 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
   __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
   __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  const uint32_t p0 = (blockIdx.x * kCPWarps + wid) * kCPPrompts;
-  if (p0 >= n_prompts) return;
+  // warp = kCPPrompts prompts; a grid smaller than that strides over the prompt groups
+  for (uint32_t p0 = (blockIdx.x * kCPWarps + wid) * kCPPrompts; p0 < n_prompts;
+       p0 += gridDim.x * kCPWarps * kCPPrompts) {
   const uint32_t p = p0 + lane;
   const bool has = lane < kCPPrompts && p < n_prompts;
   const uint32_t bo = has ? blk_off[p] : 0, n = has ? blk_off[p + 1] - bo : 0;
@@ -1290,6 +1294,8 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
   }
   const uint32_t msum = __reduce_add_sync(kFull, has ? m : 0u);
   if (lane == 0 && msum) atomicAdd(mon.matched_total, msum);
+  __syncwarp();
+  }  // prompt groups
 }
 
 // ---------------------------------------------------------------------------------
@@ -1347,6 +1353,9 @@ constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 #ifndef SKV_COMMIT_MINB
 #define SKV_COMMIT_MINB 1
 #endif
+#ifndef SKV_COMMIT_PERSIST
+#define SKV_COMMIT_PERSIST 8  // CTAs per SM; each warp then strides over ~7 prompts (0.72 -> 0.60 ms, run 103)
+#endif
 #ifndef SKV_COMMIT_MINB_NOREC
 #define SKV_COMMIT_MINB_NOREC 1
 #endif
@@ -1362,21 +1371,22 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
                                                 const uint64_t* __restrict__ users, MonCtx M, int with_record,
                                                 int pending_labels) {
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
-  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_prompts) return;
   const uint32_t lane = lane_id();
+  uint32_t inserted = 0;
+  // warp = prompt; a grid smaller than one warp per prompt strides over them
+  const uint32_t stride = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n_prompts; p += stride) {
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) {
     if constexpr (kRec)
       if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
-    return;
+    continue;
   }
   const uint32_t creator = uidx[p];
   const uint32_t owner = owners ? owners[p] : 0u;
   uint32_t carry = k0 > 0 ? slot_out[bo + k0 - 1] : kNone;  // parent of the first new block
   bool carry_mine = false;     // previous block's key claimed by this prompt (first new block: old parent)
   uint32_t carry_fix = kNone;  // previous block's duplicate fix-up entry, if it was a duplicate
-  uint32_t inserted = 0;
   // sibling links of the previous round set, applied once the next set's claims are in
   // flight (the exchange results are not waited for on the critical path)
   uint32_t q_slot[R], q_sib[R];
@@ -1574,6 +1584,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (q_sib[r] != kNone) ix.e[q_slot[r]].aux.next_sibling = q_sib[r];
+  }  // prompts
   inserted = __reduce_add_sync(kFull, inserted);
   if (lane == 0 && inserted) atomicAdd(n_new, static_cast<unsigned long long>(inserted));
 }
@@ -2139,7 +2150,10 @@ void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
                         const MonCtx& mon, uint32_t* bprompt, cudaStream_t s) {
   if (n)
-    k_chain_probe<<<cdiv(n, kCPPrompts * kCPWarps), kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
+    k_chain_probe<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n, kCPPrompts * kCPWarps),
+                                                             SKV_KCP_GRID_PER_SM ? SKV_KCP_GRID_PER_SM * 148ull
+                                                                                 : ~0ull)),
+                    kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
                                                                    decision, slot, matched, exist, tier, bmeta, mon,
                                                                    bprompt);
 }
@@ -2444,7 +2458,13 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
   }
 #endif
   auto* kern = mon ? k_commit<true> : k_commit<false>;
-  kern<<<cdiv(static_cast<uint64_t>(n) * 32, 256), 256, 0, s>>>(
+#if SKV_COMMIT_PERSIST
+  const unsigned cgrid = static_cast<unsigned>(std::min<uint64_t>(cdiv(static_cast<uint64_t>(n) * 32, 256),
+                                                                   static_cast<uint64_t>(SKV_COMMIT_PERSIST) * n_sm));
+#else
+  const unsigned cgrid = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n) * 32, 256));
+#endif
+  kern<<<cgrid, 256, 0, s>>>(
 ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     slot, n_new, fix_list, n_fix, fix_cap, err_flag,
                                                                     matched, users64, M, mon ? 1 : 0,
