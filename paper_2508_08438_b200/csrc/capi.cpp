@@ -20,10 +20,17 @@ struct skv_rules {
   skv::DfaTables dfa;
 };
 
+#ifndef SKV_COMMIT_FLAT_HOST
+#define SKV_COMMIT_FLAT_HOST 0  // set with SKV_COMMIT_FLAT: the flat commit needs bprompt from the probe
+#endif
 #ifndef SKV_REC_BESIDE
 #define SKV_REC_BESIDE 0  // measured: 0.82 ms beside vs 0.72 fused (DESIGN 5.3)
 #endif
 constexpr bool kRecordBeside = SKV_REC_BESIDE != 0;
+#ifndef SKV_PF_CHAIN
+#define SKV_PF_CHAIN 1
+#endif
+constexpr bool kPrefetchChain = SKV_PF_CHAIN != 0 && !SKV_COMMIT_FLAT_HOST;
 
 namespace {
 
@@ -197,6 +204,10 @@ struct skv_ctx {
   cudaEvent_t rec_start = nullptr, rec_done = nullptr;
   cudaEvent_t pf_done = nullptr;
   uint32_t *alt_counts = nullptr, *alt_blk_off = nullptr, *alt_first_sens = nullptr, *alt_bmask = nullptr;
+  // the prefetched batch's chained keys, labels and slot init (k_chain on the side stream)
+  uint64_t* alt_bh = nullptr;
+  uint8_t* alt_blabel = nullptr;
+  uint32_t* alt_bslot = nullptr;
   uint64_t* alt_bd = nullptr;
   bool pf_valid = false;
   cudaEvent_t pf_ev[2] = {};  // bracket the last prefetched hash/scan (side stream)
@@ -561,6 +572,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->alt_blk_off = dalloc<uint32_t>(N + 1, c->owned);
     c->alt_first_sens = dalloc<uint32_t>(N, c->owned);
     c->alt_bd = dalloc<uint64_t>(NB, c->owned);
+    c->alt_bh = dalloc<uint64_t>(NB, c->owned);
+    c->alt_blabel = dalloc<uint8_t>(NB, c->owned);
+    c->alt_bslot = dalloc<uint32_t>(NB, c->owned);
     c->alt_bmask = dalloc<uint32_t>(NB, c->owned);
     c->blabel = dalloc<uint8_t>(NB, c->owned);
     c->bprompt = dalloc<uint32_t>(NB, c->owned);
@@ -780,6 +794,11 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       std::swap(c->first_sens, c->alt_first_sens);
       std::swap(c->bd, c->alt_bd);
       std::swap(c->bmask, c->alt_bmask);
+      if (kPrefetchChain) {
+        std::swap(c->bh, c->alt_bh);
+        std::swap(c->blabel, c->alt_blabel);
+        std::swap(c->bslot, c->alt_bslot);
+      }
     } else {
       skv::launch_block_counts(off, N, B, c->counts, c->plen, s);
       skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
@@ -807,7 +826,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
     skv::launch_intern_users(c->users_tab, users, N, c->uidx, c->counters + 5, s);
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
-                            c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt, s);
+                            c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt,
+                            use_pf && kPrefetchChain ? 1 : 0, s);
     if (c->evict_on)  // match_prefix refreshes the access epoch of every visible matched node
       skv::launch_touch_matched(c->ix, c->bslot, c->blk_off, c->matched, N, static_cast<uint32_t>(c->epoch), s);
     CK(cudaEventRecord(c->ev[3], s));
@@ -982,6 +1002,10 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     CK(cudaMemsetAsync(c->alt_first_sens, 0xff, N * 4ull, st));
     stage12(c, st, tokens, off, N, b->n_tokens, nb_hint, c->alt_blk_off, c->alt_first_sens, c->alt_bd,
             c->alt_bmask);
+    // the serial chained-key FNV too, overlapping the current batch's commit; its probe is
+    // then lookups only
+    if (kPrefetchChain)
+      skv::launch_chain(c->alt_bd, c->alt_blk_off, c->alt_first_sens, N, c->alt_bh, c->alt_blabel, c->alt_bslot, st);
     CK(cudaEventRecord(c->pf_done, st));
     CK(cudaEventRecord(c->pf_ev[1], st));
     CK(cudaGetLastError());

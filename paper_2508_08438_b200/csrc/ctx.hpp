@@ -216,7 +216,9 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, uint32_t* bprompt, cudaStream_t s);
+                        const MonCtx& mon, uint32_t* bprompt, int prechained, cudaStream_t s);
+void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n, uint64_t* h,
+                  uint8_t* label, uint32_t* slot, cudaStream_t s);
 void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
                    const uint32_t* matched, const uint64_t* users, uint32_t n_prompts, cudaStream_t s);
 void launch_record_finish(const Index& ix, const MonCtx& mon, uint32_t* replay, uint32_t* n_replay, int grid,

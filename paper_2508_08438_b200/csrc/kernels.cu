@@ -1169,6 +1169,60 @@ __device__ __forceinline__ Probe probe_resolve(const Index& ix, uint64_t h, uint
 #ifndef SKV_KCP_GRID_PER_SM
 #define SKV_KCP_GRID_PER_SM 0  // > 0: at most this many CTAs per SM; warps stride over prompt groups
 #endif
+// Chained keys (A.2) for a prefetched batch, on the side stream while the previous batch
+// commits: warp = 32 prompts, lane = prompt, its serial FNV chain (16 byte-steps per
+// block) with all 32 lanes busy; digest tiles in and key tiles out coalesced through an
+// SMEM transpose (the chain overwrites each digest cell with its key).  Also the labels
+// (prefix-OR from the first sensitive block) and the probe's slot initialisation, so the
+// probe of that batch (k_chain_probe<true>) is lookups only.
+constexpr int kCHWarps = 4;
+__global__ void __launch_bounds__(kCHWarps * 32) k_chain(const uint64_t* __restrict__ dk,
+                                                         const uint32_t* __restrict__ blk_off,
+                                                         const uint32_t* __restrict__ first_sens, uint32_t n_prompts,
+                                                         uint64_t* __restrict__ hk, uint8_t* __restrict__ label,
+                                                         uint32_t* __restrict__ slot_out) {
+  __shared__ uint64_t s_t[kCHWarps][32][kPitch];
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  const uint32_t p0 = (blockIdx.x * kCHWarps + wid) * 32;
+  if (p0 >= n_prompts) return;
+  const uint32_t p = p0 + lane;
+  const bool has = p < n_prompts;
+  const uint32_t bo = has ? blk_off[p] : 0, n = has ? blk_off[p + 1] - bo : 0;
+  const uint32_t fs = has ? first_sens[p] : 0;
+  uint64_t (*t)[kPitch] = s_t[wid];
+  uint64_t h = 0;
+  const uint32_t nmax = __reduce_max_sync(kFull, n);
+  for (uint32_t t0 = 0; t0 < nmax; t0 += 32) {
+    const uint32_t b = t0 + lane;
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
+      if (b < nj) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&t[j][lane]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(dk + bj + b) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    const uint32_t cnt = n > t0 ? min(32u, n - t0) : 0u;
+    for (uint32_t c = 0; c < cnt; ++c) {
+      h = chain_key(h, t[lane][c]);
+      t[lane][c] = h;
+    }
+    __syncwarp();
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
+      const uint32_t fsj = __shfl_sync(kFull, fs, j);
+      if (b < nj) {
+        hk[bj + b] = t[j][lane];
+        label[bj + b] = b >= fsj ? SKV_LABEL_PRIVATE : SKV_LABEL_PUBLIC;
+        slot_out[bj + b] = kNone;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <bool kPre>  // kPre: keys, labels and slot init come from k_chain (the prefetch stage)
 __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
     Index ix, const uint64_t* __restrict__ dk, const uint32_t* __restrict__ blk_off,
     const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
@@ -1199,10 +1253,15 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
       if (b < nj) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&td[j][lane]));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(dk + bj + b) : "memory");
+        if constexpr (kPre) {
+          const uint32_t dsth = static_cast<uint32_t>(__cvta_generic_to_shared(&th[j][lane]));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dsth), "l"(hk + bj + b) : "memory");
+        }
       }
     }
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
+    if constexpr (!kPre) {
     const uint32_t cnt = n > t0 ? min(32u, n - t0) : 0u;
     for (uint32_t c = 0; c < cnt; ++c) {
       h = chain_key(h, td[lane][c]);
@@ -1221,6 +1280,7 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
 #endif
       }
     }
+    }  // !kPre
     uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
     while (todo) {
       uint32_t js[kCPInFlight];
@@ -2148,9 +2208,10 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, uint32_t* bprompt, cudaStream_t s) {
+                        const MonCtx& mon, uint32_t* bprompt, int prechained, cudaStream_t s) {
+  auto* kern = prechained ? k_chain_probe<true> : k_chain_probe<false>;
   if (n)
-    k_chain_probe<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n, kCPPrompts * kCPWarps),
+    kern<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n, kCPPrompts * kCPWarps),
                                                              SKV_KCP_GRID_PER_SM ? SKV_KCP_GRID_PER_SM * 148ull
                                                                                  : ~0ull)),
                     kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
@@ -2362,6 +2423,11 @@ void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t*
 }
 
 bool node_ids_speculative() { return !SKV_COMMIT_FLAT; }  // the flat commit leaves them to the exact pass
+
+void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n, uint64_t* h,
+                  uint8_t* label, uint32_t* slot, cudaStream_t s) {
+  if (n) k_chain<<<cdiv(n, 32 * kCHWarps), 32 * kCHWarps, 0, s>>>(d, blk_off, first_sens, n, h, label, slot);
+}
 
 void launch_node_bases(const uint32_t* blk_off, const uint32_t* exist, uint32_t n, uint32_t* counts, uint32_t* base,
                        void* temp, size_t temp_bytes, cudaStream_t s) {
