@@ -27,6 +27,9 @@ struct skv_rules {
 #define SKV_REC_BESIDE 0  // measured: 0.82 ms beside vs 0.72 fused (DESIGN 5.3)
 #endif
 constexpr bool kRecordBeside = SKV_REC_BESIDE != 0;
+#ifndef SKV_STREAM_PRIO
+#define SKV_STREAM_PRIO 0
+#endif
 #ifndef SKV_PF_CHAIN
 #define SKV_PF_CHAIN 1
 #endif
@@ -521,8 +524,17 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     if (prop.major != 10)
       throw CudaError("device " + std::string(prop.name) + " is not sm_100 (built for sm_100a only)");
     c->n_sm = prop.multiProcessorCount;
+#if SKV_STREAM_PRIO
+    // the batch's own work (admit, commit, epoch) ahead of the next batch's prefetch when
+    // both have CTAs waiting
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+#else
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+#endif
     CK(cudaStreamCreateWithFlags(&c->rec_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->rec_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->rec_done, cudaEventDisableTiming));
