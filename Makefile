@@ -11,9 +11,10 @@ BUILD    := build
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -I/usr/local/cuda/include -I$(JSON_INC)
 
-OBJS := $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/route.o
+GENLIB := workload/libskv_gen.so
 
-all: $(LIB) oracle
+all: $(LIB) $(GENLIB) oracle
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -27,8 +28,12 @@ $(BUILD)/capi.o: $(SRC)/capi.cpp $(SRC)/ctx.hpp $(SRC)/rules.hpp include/safekv_
 $(BUILD)/rules.o: $(SRC)/rules.cpp $(SRC)/rules.hpp | $(BUILD)
 	g++ $(CXXFLAGS) -c $< -o $@
 
-$(BUILD)/workload.o: $(SRC)/workload.cpp include/safekv_b200.h | $(BUILD)
+$(BUILD)/route.o: $(SRC)/route.cpp $(SRC)/route.hpp include/safekv_b200.h | $(BUILD)
 	g++ $(CXXFLAGS) -c $< -o $@
+
+# bench / test workload generator (not product code; workload/skv_gen.h)
+$(GENLIB): workload/skv_gen.cpp workload/skv_gen.h $(SRC)/route.hpp
+	g++ -O2 -std=c++20 -fPIC -shared -Wall -Wextra -pthread -o $@ workload/skv_gen.cpp
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lpthread -ldl -lrt
@@ -41,15 +46,15 @@ sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(BUILD)/libsafekv_b200.sass
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(GENLIB)
 
 .PHONY: all oracle sass clean
 
 # A/B variants of the CUDA library (tools/ab.sh): make variant V=name VFLAGS="-DFOO=1"
-variant: $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o
+variant: $(BUILD)/capi.o $(BUILD)/rules.o $(BUILD)/route.o
 	mkdir -p variants/$(V)
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/kernels.cu -o variants/$(V)/kernels.o 2> variants/$(V)/ptxas.log || (cat variants/$(V)/ptxas.log; exit 1)
 	g++ $(CXXFLAGS) $(VFLAGS) -c $(SRC)/capi.cpp -o variants/$(V)/capi.o
-	$(NVCC) $(ARCH) -shared -o variants/$(V)/libsafekv_b200.so variants/$(V)/kernels.o variants/$(V)/capi.o $(BUILD)/rules.o $(BUILD)/workload.o -lcudart_static -lpthread -ldl -lrt
+	$(NVCC) $(ARCH) -shared -o variants/$(V)/libsafekv_b200.so variants/$(V)/kernels.o variants/$(V)/capi.o $(BUILD)/rules.o $(BUILD)/route.o -lcudart_static -lpthread -ldl -lrt
 
 .PHONY: variant

@@ -19,6 +19,7 @@ of the prompt stream against its own index replica (weak scaling; see DESIGN.md
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import pathlib
@@ -52,7 +53,19 @@ CFG4 = dict(n_prompts=4096, prompt_tokens=32768, block_tokens=128, window_tokens
 # one candidate token (the known prefix + recovered + candidate shape of adversary.hpp:114-116); the
 # monitor epoch runs after every batch (K = 1)
 CFG5 = dict(CFG2, n_prompts=4096, seed=5, name="config 5")
-CONFIGS = {2: CFG2, 3: CFG3, 4: CFG4, 5: CFG5}
+# BASELINE.json configs[0] (--workload 1): the smallest preset workload -- the reference's own
+# safekv::generate(single_request_pii, 4 users, 1000 requests, seed 2) (committed golden fixture,
+# tests/golden/cfg1_workload.npz, made by tests/golden/make_golden.py from the unmodified reference):
+# 1,000 x 112-token prompts, 7,000 blocks; every step re-admits it on a warm index (latency-bound)
+CFG1 = dict(n_prompts=1000, prompt_tokens=112, block_tokens=16, window_tokens=32, n_users=4, pool_size=0,
+            pool_tokens=0, pii_per_kib=0.0, pii_mix=0, seed=2, name="config 1")
+CONFIGS = {1: CFG1, 2: CFG2, 3: CFG3, 4: CFG4, 5: CFG5}
+# prompts per step of the CPU reference (a deterministic prefix of each step's batch: the first
+# n prompts of the same global ids the GPU arm admits; BASELINE.md section 3 asks >= 10k prompts)
+CPU_SAMPLE = {1: 1000, 2: 10240, 3: 10240, 4: 512, 5: 4096}
+# config 4 on the CPU: the reference's pointer tree at 10 M entries (~5 GB, minutes to build) is
+# replaced by a 500 k-entry stored set (1,953 sequences x 256 blocks); queries have the same shape
+CPU_STORED_W4 = 1953
 
 
 def derive_seed_np(root: int, tags: np.ndarray) -> np.ndarray:
@@ -65,7 +78,7 @@ def derive_seed_np(root: int, tags: np.ndarray) -> np.ndarray:
         return z ^ (z >> np.uint64(31))
 METRIC = "KV blocks admitted/sec (hash+scan+lookup+monitor) and % HBM roofline, 1/2/4/8 B200"
 UNIT = "blocks/s"
-CPU_STEPS = 6
+CPU_STEPS = 2
 
 
 def peaks():
@@ -134,40 +147,140 @@ def dist_env():
     return world, rank, local
 
 
+# --------------------------------------------------------------------------- inputs
+def gen_spec(c, n, world=1, rank=0):
+    from workload import GenSpec
+    return GenSpec(n_prompts=n, prompt_tokens=c["prompt_tokens"], n_users=c["n_users"], pool_size=c["pool_size"],
+                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
+                   route_world=world, route_rank=rank, route_block_tokens=c["block_tokens"])
+
+
+def batch_id_base(k):
+    return (k + 1) * 100_000_000
+
+
+def stored_sequences(c, n_stored):
+    """Config 4's stored sequences (host, chunked): the pre-built index's contents."""
+    from workload import generate
+    L = c["prompt_tokens"]
+    sspec = gen_spec(c, c["stored_chunk"])
+    chunks = []
+    for s0 in range(0, n_stored, c["stored_chunk"]):
+        sspec.n_prompts = min(c["stored_chunk"], n_stored - s0)
+        sspec.prompt_id_base = s0
+        chunks.append(generate(sspec))
+    return chunks
+
+
+def stored_tiers(c, first, n):
+    """Tier tags of stored entries [first, first + n): derive_seed(seed, entry) mod 10 -> 0-1 HBM,
+    2-4 DRAM, 5-9 SSD."""
+    t = (derive_seed_np(c["seed"], np.arange(first, first + n, dtype=np.uint64)) % np.uint64(10)).astype(np.uint8)
+    return np.where(t < 2, 0, np.where(t < 5, 1, 2)).astype(np.uint8)
+
+
+def build_batch(c, workload, k, n, spec=None, stored_tok=None, tok_out=None):
+    """Host inputs of step k (the same for both arms; the CPU arm takes a prefix of n prompts).
+    Returns tokens (uint32), offsets, users, owners."""
+    from workload import generate
+    L, B = c["prompt_tokens"], c["block_tokens"]
+    if workload == 1:
+        w = np.load(ROOT / "tests" / "golden" / "cfg1_workload.npz")
+        tok = w["tokens"].astype(np.uint32)
+        if tok_out is not None:
+            tok_out[:len(tok)] = tok
+            tok = tok_out[:len(tok)]
+        return tok, w["offsets"].astype(np.uint64), w["users"].astype(np.uint64), w["owners"].astype(np.uint8)
+    tok = tok_out if tok_out is not None else np.empty(n * L, np.uint32)
+    if workload == 4:  # a uniform-length prefix of a stored sequence + fresh text
+        rng = np.random.default_rng(c["seed"] * 1000 + k)
+        picks = rng.integers(0, len(stored_tok), n)
+        cuts = rng.integers(0, L + 1, n)
+        q = tok[:n * L].reshape(n, L)
+        q[:] = rng.integers(ord("a"), ord("z") + 1, (n, L), dtype=np.uint32)
+        for i in range(n):
+            q[i, :cuts[i]] = stored_tok[picks[i], :cuts[i]]
+        off = np.arange(n + 1, dtype=np.uint64) * np.uint64(L)
+        users = rng.integers(1, c["n_users"] + 1, n).astype(np.uint64)
+        return tok[:n * L], off, users, np.zeros(n, np.uint8)
+    spec = spec or gen_spec(c, n)
+    spec.n_prompts = n
+    spec.prompt_id_base = batch_id_base(k)
+    _, off, users, owners = generate(spec, tokens_out=tok[:n * L])
+    if workload == 5:  # every 10th prompt becomes an attacker probe
+        rng = np.random.default_rng(c["seed"] * 1000 + k)
+        rows = tok[:n * L].reshape(n, L)
+        lens = np.full(n, L, np.int64)
+        for i in range(0, n, 10):
+            v = int(rng.integers(0, n))
+            cut = int(rng.integers(1, L // B)) * B
+            rows[i, :cut] = rows[v, :cut]
+            rows[i, cut] = ord("0") + int(rng.integers(0, 10))
+            lens[i] = cut + 1
+            users[i] = 1_000_000 + (k * 4 + i // 10) % 4
+        # compact the variable-length prompts to the front of the buffer
+        flat = np.concatenate([rows[i, :lens[i]] for i in range(n)])
+        tok[:len(flat)] = flat
+        off = np.zeros(n + 1, np.uint64)
+        np.cumsum(lens, out=off[1:])
+        return tok[:len(flat)], off, users, owners
+    return tok[:n * L], off, users, owners
+
+
 # --------------------------------------------------------------------------- reference arm
-def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int, verbose=False, c=CFG2):
-    """Reference CPU implementation of the path (oracle/_ref: the unmodified reference
-    headers driven by the Appendix-A contract): std::regex Tier-1 scan on a thread pool,
-    RadixCacheIndex / EntropyMonitor single-threaded behind their mutex."""
+def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int, c=CFG2, workload=2):
+    """The reference CPU implementation of the path: the UNMODIFIED reference headers
+    (oracle/_ref/libsafekv_ref.so) driven by the Appendix-A contract -- one stock
+    CompiledRuleSet::scan per window (detection.hpp:148-170) and the key hashing on a
+    thread pool, RadixCacheIndex / EntropyMonitor single-threaded behind their mutex
+    (cache_index.hpp:827).  Step k admits the first `sample_prompts` prompts of the SAME
+    batch (global prompt ids) the GPU arm admits at step k, after the same pool.  Only
+    oracle/_ref is loaded: the generator is bound from libsafekv_ref.so, which links the
+    same generator source as workload/libskv_gen.so."""
     sys.path.insert(0, str(ROOT / "tests"))
-    from refh import RefEngine, RefRules, load_ref
-    from paper_2508_08438_b200 import GenSpec, generate, generate_pool
+    from refh import REF_SO, RefEngine, RefRules, load_ref
     L = load_ref()
     if L is None:
         return None
-    spec = GenSpec(n_prompts=sample_prompts, prompt_tokens=c["prompt_tokens"], n_users=c["n_users"],
-                   pool_size=c["pool_size"], pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"],
-                   pii_mix=c["pii_mix"], seed=c["seed"])
+    import workload as W
+    W.use_library(REF_SO)
+    L.ref_engine_set_stock_scan.restype = None
+    L.ref_engine_set_stock_scan.argtypes = [ctypes.c_void_p, ctypes.c_int]
     eng = RefEngine(L, RefRules(L), B=c["block_tokens"], W=c["window_tokens"], threads=threads)
-    pool = generate_pool(spec)
-    eng.admit(*pool)
-    eng.commit()
+    L.ref_engine_set_stock_scan(eng.h, 1)
+    stored_tok = None
+    if workload == 4:  # reduced stored set (CPU_STORED_W4 sequences), tier tags as on the GPU
+        first = 0
+        chunks = stored_sequences(c, CPU_STORED_W4)
+        for t, o, u, w in chunks:
+            eng.admit(t, o, u, w)
+            eng.commit()
+            nb = int(((o[1:] - o[:-1]) // np.uint64(c["block_tokens"])).sum())
+            eng.set_tiers(t, o, stored_tiers(c, first, nb))
+            first += nb
+        stored_tok = np.concatenate([t for t, _, _, _ in chunks]).reshape(-1, c["prompt_tokens"])
+    elif workload != 1:
+        eng.admit(*W.generate_pool(gen_spec(c, sample_prompts)))
+        eng.commit()
     eng.epoch()
-    times, blocks = [], 0
+    spec = gen_spec(c, sample_prompts)
+    times, blocks, per_stage = [], 0, []
     for k in range(warmup + steps):
-        spec.prompt_id_base = (k + 1) * 10_000_000
-        batch = generate(spec)
+        batch = build_batch(c, workload, k, sample_prompts, spec=spec, stored_tok=stored_tok)
         t0 = time.perf_counter()
         o = eng.admit(*batch)
+        t1 = time.perf_counter()
         eng.commit()
         eng.epoch()
-        dt = time.perf_counter() - t0
+        t2 = time.perf_counter()
         if k >= warmup:
-            times.append(dt)
+            times.append(t2 - t0)
+            per_stage.append((t1 - t0, t2 - t1))
             blocks += len(o["block_h"])
     eng.close()
     tot = sum(times)
-    return {"value": blocks / tot, "seconds": tot, "blocks": blocks, "steps": steps}
+    return {"value": blocks / tot, "seconds": tot, "blocks": blocks, "steps": steps,
+            "admit_s": float(sum(a for a, _ in per_stage)), "commit_epoch_s": float(sum(b for _, b in per_stage))}
 
 
 def run_reference(args):
@@ -175,22 +288,29 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample
     c = CONFIGS[args.workload]
-    r = cpu_reference_run(args.steps, args.warmup, sample, threads, c=c)
+    sample = args.cpu_sample or CPU_SAMPLE[args.workload]
+    r = cpu_reference_run(args.steps, args.warmup, sample, threads, c=c, workload=args.workload)
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsafekv_ref.so not built"}))
         return
+    desc = (f"{c['name']} sample: the first {sample} prompts of each step's batch (same global prompt ids as "
+            f"the GPU arm) x {c['prompt_tokens']} tokens, B={c['block_tokens']}, W={c['window_tokens']}, "
+            f"{c['n_users']} users")
+    if args.workload == 4:
+        desc += f", stored index reduced to {CPU_STORED_W4} x {c['prompt_tokens']}-token sequences"
+    elif args.workload != 1:
+        desc += f", {c['pool_size']}x{c['pool_tokens']}-token shared pool pre-inserted"
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/u64 integer; f64 entropy",
         "data": f"synthetic (deterministic generator, SURVEY 8(d) {c['name']} shape)",
-        "config": {"workload": f"{c['name']} sample: {sample} prompts/step x {c['prompt_tokens']} tokens, B=16, W=32, "
-                               f"{c['n_users']} users, 256x640-token shared pool pre-inserted",
-                   "sample_prompts_per_step": sample},
+        "config": {"workload": desc, "sample_prompts_per_step": sample,
+                   "scan": "one stock CompiledRuleSet::scan per window on all host threads"},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} steps x {sample} prompts of {c['name']}"},
+                         "sample": f"{args.steps} steps x {sample} prompts of {c['name']}",
+                         "admit_s": r["admit_s"], "commit_epoch_s": r["commit_epoch_s"]},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -200,7 +320,7 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import ctypes as C
-    from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, GenSpec, generate, generate_pool
+    from paper_2508_08438_b200 import AdmissionEngine, EngineConfig
     from paper_2508_08438_b200 import native as N
 
     world, rank, local = dist_env()
@@ -217,7 +337,7 @@ def run_ours(args):
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
     c = dict(CONFIGS[args.workload])
-    if args.prompts:
+    if args.prompts and args.workload != 1:
         c["n_prompts"] = args.prompts
     n_local = c["n_prompts"]  # weak scaling: every rank admits a full config-2 batch per step
     L, B = c["prompt_tokens"], c["block_tokens"]
@@ -243,58 +363,22 @@ def run_ours(args):
     # N > 1: prefix-forest partitioning -- every rank admits the first n_local prompts of
     # the global sequence that skv_route assigns to it (disjoint index forests, no
     # data-path collective)
-    spec = GenSpec(n_prompts=n_local, prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
-                   pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
-                   route_world=world, route_rank=rank, route_block_tokens=B)
+    from workload import generate_pool
+    spec = gen_spec(c, n_local, world, rank)
     host, devb, ntok, nblk = [], [], [], []
-    stored = None
+    stored = stored_tok = None
     if args.workload == 4:  # the stored sequences of the pre-built index (host, chunked)
-        sspec = GenSpec(n_prompts=c["stored_chunk"], prompt_tokens=L, n_users=c["n_users"], pool_size=c["pool_size"],
-                        pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], seed=c["seed"])
-        stored = []
-        for s0 in range(0, c["stored"], c["stored_chunk"]):
-            sspec.n_prompts = min(c["stored_chunk"], c["stored"] - s0)
-            sspec.prompt_id_base = s0
-            t, o, u, w = generate(sspec)
-            stored.append((t, o, u, w))
+        stored = stored_sequences(c, c["stored"])
         stored_tok = np.concatenate([t for t, _, _, _ in stored]).reshape(c["stored"], L)
     for k in range(n_batches):
-        spec.prompt_id_base = (k + 1) * 100_000_000
-        tok_pin = torch.empty(n_local * L, dtype=torch.int32, pin_memory=True)
+        tok_pin = torch.empty(max(n_local * L, 1), dtype=torch.int32, pin_memory=True)
         tok_np = tok_pin.numpy().view(np.uint32)
-        if args.workload == 4:  # a uniform-length prefix of a stored sequence + fresh text
-            rng = np.random.default_rng(c["seed"] * 1000 + k)
-            picks = rng.integers(0, c["stored"], n_local)
-            cuts = rng.integers(0, L + 1, n_local)
-            q = tok_np.reshape(n_local, L)
-            q[:] = rng.integers(ord("a"), ord("z") + 1, (n_local, L), dtype=np.uint32)
-            for i in range(n_local):
-                q[i, :cuts[i]] = stored_tok[picks[i], :cuts[i]]
-            off = np.arange(n_local + 1, dtype=np.uint64) * np.uint64(L)
-            users = rng.integers(1, c["n_users"] + 1, n_local).astype(np.uint64)
-            owners = np.zeros(n_local, np.uint8)
-        else:
-            _, off, users, owners = generate(spec, tokens_out=tok_np)
-            if args.workload == 5:  # every 10th prompt becomes an attacker probe
-                rng = np.random.default_rng(c["seed"] * 1000 + k)
-                rows = tok_np.reshape(n_local, L)
-                lens = np.full(n_local, L, np.int64)
-                for i in range(0, n_local, 10):
-                    v = int(rng.integers(0, n_local))
-                    cut = int(rng.integers(1, L // B)) * B
-                    rows[i, :cut] = rows[v, :cut]
-                    rows[i, cut] = ord("0") + int(rng.integers(0, 10))
-                    lens[i] = cut + 1
-                    users[i] = 1_000_000 + (k * 4 + i // 10) % 4
-                # compact the variable-length prompts to the front of the pinned buffer
-                flat = np.concatenate([rows[i, :lens[i]] for i in range(n_local)])
-                tok_np[:len(flat)] = flat
-                off = np.zeros(n_local + 1, np.uint64)
-                np.cumsum(lens, out=off[1:])
+        tok, off, users, owners = build_batch(c, args.workload, k, n_local, spec=spec, stored_tok=stored_tok,
+                                              tok_out=tok_np)
         ntok.append(int(off[-1]))
         nblk.append(int(((off[1:] - off[:-1]) // np.uint64(B)).sum()))
         # every host input of the e2e arm lives in pinned memory (async H2D)
-        pins = [torch.from_numpy(a.view(v)).pin_memory() for a, v in
+        pins = [torch.from_numpy(np.ascontiguousarray(a).view(v)).pin_memory() for a, v in
                 ((off, np.int64), (users, np.int64), (owners, np.uint8))]
         off_p, users_p, owners_p = (t.numpy() for t in pins)
         host.append((tok_pin, tok_np, off_p.view(np.uint64), users_p.view(np.uint64), owners_p, pins))
@@ -302,7 +386,7 @@ def run_ours(args):
         devb.append((tok_pin.to(dev, non_blocking=True), torch.from_numpy(off.view(np.int64)).to(dev),
                      torch.from_numpy(users.view(np.int64)).to(dev), torch.from_numpy(owners).to(dev)))
     torch.cuda.synchronize()
-    pool = generate_pool(spec, rank)  # this rank's share of the pre-inserted pool
+    pool = generate_pool(spec, rank) if args.workload not in (1, 4) else None  # this rank's share
     pipeline = not args.no_pipeline
 
     def fresh_engine():
@@ -312,12 +396,9 @@ def run_ours(args):
             for t, o, u, w in stored:
                 r = eng.admit(t, o, u, w)
                 eng.commit()
-                tiers = (derive_seed_np(c["seed"], np.arange(first, first + r.n_blocks, dtype=np.uint64))
-                         % np.uint64(10)).astype(np.uint8)
-                tiers = np.where(tiers < 2, 0, np.where(tiers < 5, 1, 2)).astype(np.uint8)
-                eng.set_tiers(r.block_h, r.block_d, tiers, r.block_offsets)
+                eng.set_tiers(r.block_h, r.block_d, stored_tiers(c, first, r.n_blocks), r.block_offsets)
                 first += r.n_blocks
-        else:
+        elif pool is not None:
             eng.admit(*pool)
             eng.commit()
         eng.epoch_pass()
@@ -341,12 +422,16 @@ def run_ours(args):
         eng.commit()
         eng.epoch_pass()
 
-    # outputs returned to the host in the e2e arm: labels per block + match length per prompt
-    out_label = torch.empty(blocks_per_batch, dtype=torch.uint8, pin_memory=True)
+    # outputs returned to the host in the e2e arm: label + decision per block, match length +
+    # lowest tier per prompt (the admission decision a serving engine acts on)
+    out_label = torch.empty(max(blocks_per_batch, 1), dtype=torch.uint8, pin_memory=True)
+    out_dec = torch.empty(max(blocks_per_batch, 1), dtype=torch.uint8, pin_memory=True)
     out_match = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+    out_tier = torch.empty(n_local, dtype=torch.uint8, pin_memory=True)
 
     def step_host(eng, k, nxt):
-        o = N.AdmitOut(None, None, out_label.data_ptr(), None, None, out_match.data_ptr(), None, None, 0, 0, 0)
+        o = N.AdmitOut(None, None, out_label.data_ptr(), None, out_dec.data_ptr(), out_match.data_ptr(),
+                       out_tier.data_ptr(), None, 0, 0, 0)
         eng.admit_raw(host_batch(k), o)
         if nxt is not None:
             eng.prefetch_raw(host_batch(nxt))
@@ -425,16 +510,17 @@ def run_ours(args):
         except Exception:
             traffic = None
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline and args.workload != 4:
-        # a bounded sample (~10 s of CPU work): CPU_STEPS timed batches of --cpu-sample
-        # prompts after one warm-up batch, same generator, pool pre-inserted
-        r = cpu_reference_run(steps=CPU_STEPS, warmup=1, sample_prompts=args.cpu_sample,
-                              threads=os.cpu_count() or 1, c=c)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # a bounded sample (~10-30 s of CPU work): CPU_STEPS timed steps of the first
+        # CPU_SAMPLE prompts of the same batches, after one warm-up step
+        sample = args.cpu_sample or CPU_SAMPLE[args.workload]
+        r = cpu_reference_run(steps=CPU_STEPS, warmup=1, sample_prompts=sample, threads=os.cpu_count() or 1,
+                              c=c, workload=args.workload)
         if r is not None:
             cpu = {"value": r["value"], "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"{CPU_STEPS} batches x {args.cpu_sample} prompts of {c['name']}"
-                             f"{' (benign prompts only)' if args.workload == 5 else ''} after 1 warm-up batch "
-                             f"(pool pre-inserted): {r['blocks']} blocks in {r['seconds']:.1f} s"}
+                   "sample": f"{CPU_STEPS} steps x the first {sample} prompts of {c['name']}'s batches after 1 "
+                             f"warm-up step: {r['blocks']} blocks in {r['seconds']:.1f} s (stock "
+                             f"CompiledRuleSet::scan per window on all threads; index single-threaded)"}
     # where the rest of the step goes: the commit is bound by random 128-bit CAS into the
     # index (one claim per new block), measured against the randmem ceiling
     cas_ceiling = None
@@ -459,7 +545,7 @@ def run_ours(args):
                 "batch overlaps it on a side stream",
     }
     h2d = int(timed_tokens) * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
-    d2h = int(timed_blocks) + n_local * 4
+    d2h = 2 * int(timed_blocks) + n_local * 5
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": ms_dev / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -468,6 +554,8 @@ def run_ours(args):
                                f"W={c['window_tokens']}, {c['n_users']} users, " +
                                (f"{c['stored']} x {L}-token stored sequences pre-inserted with HBM/DRAM/SSD tier "
                                 "tags, queries = uniform prefixes of them + fresh text" if args.workload == 4
+                                else "the reference's generate() preset workload (golden fixture), re-admitted every "
+                                "step on a warm index" if args.workload == 1
                                 else "256x640-token pool pre-inserted"),
                    "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
                    "step": "admit + commit + epoch",
@@ -504,11 +592,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--prompts", type=int, default=0, help="override prompts per batch (debug)")
-    ap.add_argument("--cpu-sample", type=int, default=4096)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="CPU reference prompts per step (0 = CPU_SAMPLE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", type=int, default=2, choices=sorted(CONFIGS),
-                    help="BASELINE.json config (2 = the headline, default; 3 = the per-GPU shard of config 3; "
-                         "4 = long context over a 10 M-entry tiered index)")
+                    help="BASELINE.json config (2 = the headline, default; 1 = the smallest preset; 3 = the per-GPU "
+                         "shard of config 3; 4 = long context over a 10 M-entry tiered index; 5 = adversarial mix)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
     args = ap.parse_args()

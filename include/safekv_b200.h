@@ -154,13 +154,19 @@ int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
  * rule masks (stages 1-2, which read no index state) on a side stream, so they overlap
  * the pending batch's commit/epoch.  The next skv_admit with the same tokens/offsets
  * pointers and sizes consumes them; any other admit, or skv_set_rules, drops them.
- * The caller must keep the batch's device buffers unchanged until that admit.  Host
- * batches and unaligned tokens are accepted and ignored (admitted inline).  Results
- * are identical with or without prefetch; there is no reference counterpart (the
- * reference admits one prompt at a time). */
+ * A host batch is copied to the device asynchronously on the side stream, so the caller
+ * must keep its host buffers (tokens, offsets, users, owners) alive and unchanged until the
+ * consuming admit returns (a rewritten buffer would be admitted with stale stages 1-2).
+ * Device batches must likewise stay unchanged until that admit; device batches whose tokens
+ * are not 16-B aligned are ignored (admitted inline).  Results are identical with or
+ * without prefetch; there is no reference counterpart (the reference admits one prompt at
+ * a time). */
 int skv_prefetch(skv_ctx* ctx, const skv_batch* next);
 /* Insert the new blocks of the last admitted batch (first creator wins; intra-batch
- * duplicates are won by the lowest prompt index).  new_entries may be NULL. */
+ * duplicates are won by the lowest prompt index).  new_entries may be NULL.  A capacity
+ * failure detected after the kernels ran (probe sequence or monitor set pool exhausted)
+ * returns SKV_ERR_CAPACITY and leaves the context unusable for further batches (every
+ * later batch call returns SKV_ERR_STATE naming the cause; skv_export still works). */
 int skv_commit(skv_ctx* ctx, uint64_t* new_entries);
 
 typedef struct {
@@ -172,8 +178,12 @@ typedef struct {
   uint64_t epoch;
 } skv_event;
 
-/* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d). */
+/* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d).  *n_events is the total
+ * number of events; when it exceeds cap only the first cap are written and the whole list
+ * stays retrievable with skv_last_events (nothing is lost: the epoch has been applied). */
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
+/* The events of the last skv_epoch (sorted by (h, d)); *n_events = their total count. */
+int skv_last_events(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events);
 
 /* Label landing.  With pending != 0, skv_commit stores new entries
  * as PendingPrivate (visible to their creator only, like the reference's freshly inserted
@@ -219,6 +229,8 @@ uint64_t skv_entry_count(skv_ctx* ctx);
 int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
 int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap);
+/* (skv_evict returns SKV_ERR_STATE between skv_admit and skv_commit: the pending batch's
+ * matched path is pinned, like a request's path around insert in the reference.) */
 
 /* Per-stage device times of the last skv_admit / skv_commit (CUDA events, ms). */
 typedef struct {
@@ -259,37 +271,22 @@ int skv_tier1_scan(skv_ctx* ctx, const char* text, size_t len, uint32_t* rule_ma
 int skv_token_seq_digest(skv_ctx* ctx, const uint32_t* tokens, size_t n, uint64_t* digest);
 
 /* ------------------------------------------------------------------------------
- * Synthetic workload generator (host), deterministic, built from the reference's
- * generator primitives (workload.hpp:155-266; util.hpp:14-55).  See DESIGN.md.
+ * Multi-GPU request router (host).  Entries at depth < depth (the
+ * first `depth` blocks of every prompt) are replicated on every rank; an entry at depth
+ * >= depth belongs to the rank of the key h_depth of its depth-`depth` ancestor.  A prompt
+ * with more than `depth` full blocks is therefore routed by h_depth (a hash of the key of
+ * its block `depth`), so every entry it can probe, record, insert or relabel below the
+ * replicated layer lives on its rank; a prompt with at most `depth` blocks touches
+ * replicated entries only and goes to prompt_id % world (prompt_ids may be NULL: index p).
+ * depth = 0 is pure prefix-forest partitioning (route by the root block).  There is no
+ * reference counterpart: the reference is single-process.
+ * The synthetic workload generator of the bench and tests (workload/skv_gen.h) is NOT
+ * part of this library.
  * ------------------------------------------------------------------------------ */
-typedef struct {
-  uint64_t n_prompts, prompt_tokens;  /* prompt length (all prompts equal) */
-  uint64_t n_users;                   /* user = first_user + p % n_users   */
-  uint64_t first_user;
-  uint64_t pool_size, pool_tokens;    /* shared-prefix pool                */
-  double shared_fraction;             /* fraction of prompts that start with a pool prefix */
-  double pii_per_kib;                 /* PII phrases per KiB of unique body */
-  uint32_t pii_mix;                   /* 1: config-3 mix (60% none, 30% one per 2 KiB, 10% one per 256 B) */
-  uint64_t seed;
-  uint64_t prompt_id_base;            /* global id of prompt 0 (sharding)  */
-  /* prefix-forest partitioning: with route_world > 1 the batch is the first n_prompts
-   * global ids >= prompt_id_base whose prompt skv_route()s to route_rank */
-  uint32_t route_world, route_rank, route_block_tokens, pad_;
-  uint64_t* prompt_ids_out;           /* optional: global id of each generated prompt */
-} skv_gen_spec;
-/* Writes n_prompts*prompt_tokens tokens and n_prompts+1 offsets; users/owners may be NULL. */
-int skv_generate(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
-                 uint8_t* owners, int nthreads);
-/* Multi-GPU router (host): rank of each prompt = a hash of the key h_0 of its first full
- * block, i.e. of the root of its path in the prefix forest.  Every index entry a prompt
- * can touch lies in that root's tree, so ranks own disjoint forests and admit/commit/
- * monitor/epoch need no cross-rank exchange.  Prompts without a
- * full block go to prompt_id % world (prompt_ids may be NULL: index p). */
 int skv_route(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
               const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out);
-/* The pool prefixes themselves (pool_size prompts of pool_tokens). */
-int skv_generate_pool(const skv_gen_spec* spec, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
-                      uint8_t* owners);
+int skv_route_depth(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
+                    uint32_t depth, const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out);
 
 #ifdef __cplusplus
 }

@@ -58,6 +58,10 @@ struct RuleMasks {
   std::vector<std::shared_ptr<const CompiledRuleSet>> single;  // one snapshot per rule
 };
 
+std::string content_key(const uint32_t* t, uint32_t n) {
+  return std::string(reinterpret_cast<const char*>(t), static_cast<size_t>(n) * 4);
+}
+
 uint64_t block_digest(const uint32_t* t, uint32_t n) {
   TokenSeq s(t, t + n);
   return token_seq_digest(s);
@@ -167,8 +171,24 @@ uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
 // Windows are scanned with a std::thread pool (scans are reentrant on an immutable
 // snapshot, detection.hpp:116-117).  out_mask is indexed by the flat block index
 // (prompt-major).  Returns the number of blocks.
+// stock = 1: ONE CompiledRuleSet::scan per window, exactly as RuleEngine::tier1_scan runs it
+// (detection.hpp:148-170, 217); the mask is then 1 for a sensitive window (the label input),
+// not the per-rule attribution.  This is the timed reference arm of bench.py.
+static uint64_t scan_windows(void* r, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts, uint32_t B,
+                             uint32_t W, uint64_t* out_mask, int nthreads, int stock, uint64_t* out_h = nullptr,
+                             uint64_t* out_d = nullptr);
+
 uint64_t ref_scan_windows(void* r, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts,
                           uint32_t B, uint32_t W, uint64_t* out_mask, int nthreads) {
+  return scan_windows(r, tok, off, n_prompts, B, W, out_mask, nthreads, 0);
+}
+
+// With out_h/out_d the same worker threads also compute every block's key (A.2: stages 1-2
+// of a prompt run on one pool thread; hashing is reentrant).
+static uint64_t scan_windows(void* r, const uint32_t* tok, const uint64_t* off, uint32_t n_prompts, uint32_t B,
+                             uint32_t W, uint64_t* out_mask, int nthreads, int stock, uint64_t* out_h,
+                             uint64_t* out_d) {
+  const CompiledRuleSet& set = *static_cast<RulesBox*>(r)->set;
   std::vector<uint64_t> boff(n_prompts + 1, 0);
   for (uint32_t p = 0; p < n_prompts; ++p) boff[p + 1] = boff[p] + (off[p + 1] - off[p]) / B;
   if (nthreads <= 0) nthreads = static_cast<int>(std::thread::hardware_concurrency());
@@ -179,11 +199,18 @@ uint64_t ref_scan_windows(void* r, const uint32_t* tok, const uint64_t* off, uin
       if (p >= n_prompts) break;
       uint64_t L = off[p + 1] - off[p];
       uint64_t n = L / B;
+      if (out_h)
+        for (uint64_t b = 0, h = 0; b < n; ++b) {
+          uint64_t d = block_digest(tok + off[p] + b * B, B);
+          h = chain_key(b ? h : 0, d);
+          out_h[boff[p] + b] = h;
+          out_d[boff[p] + b] = d;
+        }
       for (uint64_t b = 0; b < n; ++b) {
         uint64_t s = off[p] + b * B, e = off[p] + std::min<uint64_t>(L, (b + 1) * B + W);
         TokenSeq win(tok + s, tok + e);
         std::string text = detokenize_bytes(win);
-        out_mask[boff[p] + b] = ref_rules_mask(r, text.data(), text.size());
+        out_mask[boff[p] + b] = stock ? (set.scan(text).sensitive ? 1u : 0u) : ref_rules_mask(r, text.data(), text.size());
       }
     }
   };
@@ -227,7 +254,7 @@ struct RefEngine {
   std::unique_ptr<RadixCacheIndex> idx;
   MonitorConfig mcfg;
   std::unique_ptr<EntropyMonitor> mon;
-  std::map<std::vector<uint32_t>, uint32_t> intern;  // block content -> id (exact, hash-free)
+  std::unordered_map<std::string, uint32_t> intern;  // block content (raw token bytes) -> id (exact)
   std::vector<uint64_t> id_digest;                     // id -> token_seq_digest(content)
   struct Pending {
     TokenSeq ids;
@@ -245,6 +272,7 @@ struct RefEngine {
   };
   std::vector<Served> served;
   int nthreads = 1;
+  int stock_scan = 0;  // 1: one CompiledRuleSet::scan per window (bench reference arm)
   bool pending_labels = false;  // commit leaves new nodes PendingPrivate (insert's label)
 };
 
@@ -284,6 +312,7 @@ int ref_engine_set_tiered(void* ev, int tiered) {
 }
 
 void ref_engine_set_threads(void* e, int n) { static_cast<RefEngine*>(e)->nthreads = n; }
+void ref_engine_set_stock_scan(void* e, int on) { static_cast<RefEngine*>(e)->stock_scan = on; }
 
 // Phase L of Appendix A.1 for one batch: hashes, window verdicts, labels, lookups and
 // monitor records (in prompt order).  Per-block outputs are prompt-major flat arrays.
@@ -298,8 +327,7 @@ int ref_engine_admit(void* ev, const uint32_t* tok, const uint64_t* off, const u
   for (uint32_t p = 0; p < n_prompts; ++p) boff[p + 1] = boff[p] + (off[p + 1] - off[p]) / B;
   uint64_t nblk = boff[n_prompts];
   std::vector<uint64_t> mask(nblk);
-  ref_scan_windows(e->rules_box, tok, off, n_prompts, B, e->W, mask.data(), e->nthreads);
-  ref_block_keys(tok, off, n_prompts, B, out_h, out_d);
+  scan_windows(e->rules_box, tok, off, n_prompts, B, e->W, mask.data(), e->nthreads, e->stock_scan, out_h, out_d);
   e->pending.clear();
   e->served.assign(n_prompts, {});
   for (uint32_t p = 0; p < n_prompts; ++p) {
@@ -316,7 +344,7 @@ int ref_engine_admit(void* ev, const uint32_t* tok, const uint64_t* off, const u
                          : static_cast<uint8_t>(SensitivityLabel::Public);
       out_label[k] = lbl;
       pd.labels.push_back(lbl);
-      std::vector<uint32_t> content(tok + off[p] + b * B, tok + off[p] + (b + 1) * B);
+      std::string content = content_key(tok + off[p] + b * B, B);
       auto it = e->intern.find(content);
       uint32_t id;
       if (it == e->intern.end()) {
@@ -405,7 +433,7 @@ int ref_engine_resolve(void* ev, const uint32_t* tok, const uint64_t* off, uint3
       if (first[p] >= n) continue;
       TokenSeq ids;
       for (uint64_t b = 0; b < n; ++b) {
-        std::vector<uint32_t> content(tok + off[p] + b * B, tok + off[p] + (b + 1) * B);
+        std::string content = content_key(tok + off[p] + b * B, B);
         auto it = e->intern.find(content);
         if (it == e->intern.end()) return -1;
         ids.push_back(it->second);
@@ -486,7 +514,7 @@ int ref_engine_set_tiers(void* ev, const uint32_t* tok, const uint64_t* off, uin
     uint64_t n = (off[p + 1] - off[p]) / e->B;
     TokenSeq ids;
     for (uint64_t b = 0; b < n; ++b, ++k) {
-      std::vector<uint32_t> content(tok + off[p] + b * e->B, tok + off[p] + (b + 1) * e->B);
+      std::string content = content_key(tok + off[p] + b * e->B, e->B);
       auto it = e->intern.find(content);
       if (it == e->intern.end()) return -1;
       ids.push_back(it->second);

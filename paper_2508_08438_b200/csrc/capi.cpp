@@ -179,6 +179,10 @@ struct skv_ctx {
   skv::HSLayout hs_layout{};
   uint32_t rec_grid = 0;
 
+  // set when a failed call left device state that no longer follows the reference (every
+  // later batch call raises StateError with this reason; export still works)
+  std::string poisoned;
+  std::vector<skv_event> last_events;  // every event of the last skv_epoch, sorted by key
   // pending batch (between admit and commit)
   bool pending = false;
   // monitor records of the last admit, executed inside the commit kernel (overlapping
@@ -213,7 +217,11 @@ struct skv_ctx {
   uint32_t* alt_bslot = nullptr;
   uint64_t* alt_bd = nullptr;
   bool pf_valid = false;
-  cudaEvent_t pf_ev[2] = {};  // bracket the last prefetched hash/scan (side stream)
+  // bracket a prefetched hash/scan (side stream); two pairs, alternating, so that the admit
+  // consuming prefetch k still reads its own pair after prefetch k+1 has been enqueued
+  cudaEvent_t pf_ev[2][2] = {};
+  int pf_pair = 0;      // pair of the staged prefetch
+  int adm_pf_pair = 0;  // pair of the prefetch the last admit consumed
   void* side_temp = nullptr;
   size_t side_temp_bytes = 0;
   bool pf_on_device = false;
@@ -403,10 +411,19 @@ uint64_t host_block_count(const skv_batch* b, uint32_t B) {
   return n_blocks;
 }
 
+// CUDA-event interval; a failed query (an event never recorded, or recorded on another
+// device) is reported as -1 rather than a stale or zero time
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return -1.0f;
+  }
   return ms;
+}
+
+void check_usable(const skv_ctx* c) {
+  if (!c->poisoned.empty()) throw StateError("context unusable after an earlier failure: " + c->poisoned);
 }
 
 }  // namespace
@@ -539,7 +556,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     CK(cudaEventCreateWithFlags(&c->rec_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->rec_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->pf_done, cudaEventDisableTiming));
-    for (auto& ev : c->pf_ev) CK(cudaEventCreate(&ev));
+    for (auto& pr : c->pf_ev)
+      for (auto& ev : pr) CK(cudaEventCreate(&ev));
     for (auto& ev : c->ev) CK(cudaEventCreate(&ev));
     // index
     uint64_t cap = next_pow2(std::max<uint64_t>(cfg->index_capacity, 1024));
@@ -665,8 +683,9 @@ int skv_destroy(skv_ctx* c) {
   if (c->rec_start) cudaEventDestroy(c->rec_start);
   if (c->rec_done) cudaEventDestroy(c->rec_done);
   if (c->pf_done) cudaEventDestroy(c->pf_done);
-  for (auto ev : c->pf_ev)
-    if (ev) cudaEventDestroy(ev);
+  for (auto& pr : c->pf_ev)
+    for (auto ev : pr)
+      if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return SKV_OK;
@@ -742,6 +761,7 @@ void ensure_admit_resolved(skv_ctx* c) {
 int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
+    check_usable(c);
     CK(cudaSetDevice(c->device));
     const uint32_t N = b->n_prompts;
     const uint32_t B = c->cfg.block_tokens;
@@ -872,6 +892,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     if (!nb_known && !out) CK(cudaMemcpyAsync(c->host_small + 20, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
     c->adm_lazy = !out && b->on_device;
     c->adm_use_pf = use_pf;
+    c->adm_pf_pair = c->pf_pair;
     c->adm_launched = launched;
     c->pending = true;
     c->p_n = N;
@@ -901,7 +922,8 @@ void resolve_admit(skv_ctx* c) {
   const bool use_pf = c->adm_use_pf;
   const uint32_t launched = c->adm_launched;
   {
-    c->times.hash_scan_ms = use_pf ? elapsed(c->pf_ev[0], c->pf_ev[1]) : elapsed(c->ev[1], c->ev[2]);
+    c->times.hash_scan_ms =
+        use_pf ? elapsed(c->pf_ev[c->adm_pf_pair][0], c->pf_ev[c->adm_pf_pair][1]) : elapsed(c->ev[1], c->ev[2]);
     c->times.prefetched = use_pf ? 1 : 0;
     c->times.chain_probe_ms = elapsed(c->ev[2], c->ev[3]);
     c->times.record_ms = elapsed(c->ev[3], c->ev[4]);
@@ -1008,7 +1030,8 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     } else if (reinterpret_cast<uintptr_t>(b->tokens) % 16) {
       return SKV_OK;
     }
-    CK(cudaEventRecord(c->pf_ev[0], st));
+    c->pf_pair ^= 1;
+    CK(cudaEventRecord(c->pf_ev[c->pf_pair][0], st));
     skv::launch_block_counts(off, N, c->cfg.block_tokens, c->alt_counts, c->alt_plen, st);
     skv::launch_exclusive_scan(c->side_temp, c->side_temp_bytes, c->alt_counts, c->alt_blk_off, N + 1, st);
     CK(cudaMemsetAsync(c->alt_first_sens, 0xff, N * 4ull, st));
@@ -1019,7 +1042,7 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     if (kPrefetchChain)
       skv::launch_chain(c->alt_bd, c->alt_blk_off, c->alt_first_sens, N, c->alt_bh, c->alt_blabel, c->alt_bslot, st);
     CK(cudaEventRecord(c->pf_done, st));
-    CK(cudaEventRecord(c->pf_ev[1], st));
+    CK(cudaEventRecord(c->pf_ev[c->pf_pair][1], st));
     CK(cudaGetLastError());
     c->pf_valid = true;
     c->pf_on_device = b->on_device != 0;
@@ -1036,6 +1059,7 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
 int skv_commit(skv_ctx* c, uint64_t* new_entries) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
+    check_usable(c);
     if (!c->pending) throw StateError("skv_commit without a preceding skv_admit");
     CK(cudaSetDevice(c->device));
     cudaStream_t s = c->stream;
@@ -1064,6 +1088,9 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     }
     skv::Index ixc = c->ix;
     const uint32_t ep32 = static_cast<uint32_t>(c->epoch);
+    // node ids are u32 on the device (the victim order's tie-break); refuse before they wrap
+    if (c->evict_on && c->node_next + c->p_blocks >= (1ull << 31))
+      throw CapacityError("eviction node-id space exhausted (2^31 nodes created)");
     if (c->evict_on) {  // speculative node ids: prefix over prompts of the blocks each would create
       skv::launch_node_bases(c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl, c->ev_temp, c->ev_temp_bytes, s);
       ixc.em_base = c->ev_incl;
@@ -1074,7 +1101,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users,
                        rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
-                       c->n_sm, c->bprompt, c->late, c->counters + 11, c->counters + 12, s);
+                       c->n_sm, c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
     if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
     uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
     if (c->evict_on) launched += 2;
@@ -1087,11 +1114,28 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 7, c->counters + 7, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
-    if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
     std::memcpy(&nn, c->host_small, 8);
-    if (c->host_small[4] & 2u) throw CapacityError("index probe sequence exhausted");
-    if (rec) launched += replay_record(c, s, c->host_small[5], c->host_small[4]);
+    const uint32_t err = c->host_small[4];
     const uint32_t revived = c->host_small[6];
+    if (err) {
+      // the kernels have run: the host counters follow the device state before anything is
+      // raised (skv_export sizes its buffer by them), and the context refuses further batches
+      // (its index or monitor state no longer equals the reference's)
+      c->entries += nn + revived;
+      c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
+      c->node_next += nn + revived;
+      c->pending = false;
+      c->rec_pending = false;
+      if (c->adm_lazy) c->adm_lazy = false, c->p_blocks = c->host_small[20];
+      const char* why = (err & 8u)   ? "user table exhausted (raise max_users); the batch was not inserted"
+                        : (err & 2u) ? "index probe sequence exhausted"
+                        : (err & 1u) ? "monitor window user-set pool exhausted (raise max_window_entries)"
+                                     : "commit fix-up list overflow";
+      if (!(err & 8u)) c->poisoned = why;  // a user-table overflow inserts nothing: still consistent
+      throw CapacityError(why);
+    }
+    if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
+    if (rec) launched += replay_record(c, s, c->host_small[5], err);
     if (c->evict_on) {
       // the insert walk refreshes every pre-existing block's access epoch; node ids are exact
       // already unless the batch had duplicate claims
@@ -1119,6 +1163,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
 int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch_out) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
+    check_usable(c);
     CK(cudaSetDevice(c->device));
     ensure_admit_resolved(c);
     flush_record(c);
@@ -1164,9 +1209,17 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     if (events)
       for (size_t i = 0; i < ev.size() && i < cap; ++i) events[i] = ev[i];
     if (n_events) *n_events = ev.size();
+    c->last_events = std::move(ev);  // the whole list stays retrievable (skv_last_events)
     if (epoch_out) *epoch_out = epoch;
     return SKV_OK;
   });
+}
+
+int skv_last_events(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events) {
+  if (!c || (cap && !events)) return SKV_ERR_ARG;
+  for (size_t i = 0; i < c->last_events.size() && i < cap; ++i) events[i] = c->last_events[i];
+  if (n_events) *n_events = c->last_events.size();
+  return SKV_OK;
 }
 
 int skv_set_label_policy(skv_ctx* c, int pending) {
@@ -1246,14 +1299,20 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
     ensure_admit_resolved(c);
     flush_record(c);
     std::vector<void*> tmp;
-    skv_entry* dout = dalloc<skv_entry>(std::max<uint64_t>(c->entries, 1), tmp);
-    uint32_t* dn = dalloc<uint32_t>(1, tmp);
     cudaStream_t s = c->stream;
-    CK(cudaMemsetAsync(dn, 0, 4, s));
-    skv::launch_export(c->ix, c->users_tab.rev, dout, dn, s);
+    uint32_t* dn = dalloc<uint32_t>(1, tmp);
+    uint64_t room = std::max<uint64_t>(c->entries, 1);
+    skv_entry* dout = nullptr;
     uint32_t cnt = 0;
-    CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
-    sync_check(s);
+    for (int attempt = 0; attempt < 2; ++attempt) {  // the device count is exact even past the buffer
+      dout = dalloc<skv_entry>(room, tmp);
+      CK(cudaMemsetAsync(dn, 0, 4, s));
+      skv::launch_export(c->ix, c->users_tab.rev, dout, dn, static_cast<uint32_t>(room), s);
+      CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
+      sync_check(s);
+      if (cnt <= room) break;
+      room = cnt;
+    }
     if (out && cnt) CK(cudaMemcpy(out, dout, std::min<size_t>(cnt, cap) * sizeof(skv_entry), cudaMemcpyDeviceToHost));
     for (void* p : tmp) cudaFree(p);
     if (n) *n = cnt;
@@ -1293,6 +1352,11 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     CK(cudaSetDevice(c->device));
     if (!c->evict_on) throw StateError("eviction is not enabled (skv_enable_eviction before the first admit)");
     if (needed_blocks == 0) throw ArgError("evict: needed must be positive");
+    check_usable(c);
+    // the pending batch's matched path is pinned until its commit (the reference pins a
+    // request's path around insert, cache_index.hpp:347-356, serving_sim.hpp:196,215): its
+    // lookup results would otherwise point at tombstones
+    if (c->pending && c->p_n) throw StateError("skv_evict between skv_admit and skv_commit (commit first)");
     ensure_admit_resolved(c);
     flush_record(c);
     cudaStream_t s = c->stream;

@@ -237,7 +237,8 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    uint32_t n_prompts, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
                    const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
-                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived, cudaStream_t s);
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived,
+                   const MonCtx& pool, cudaStream_t s);
 void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                     const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
@@ -253,7 +254,8 @@ void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                       const uint8_t* tiers, uint32_t n,
                       cudaStream_t s);
-void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s);
+void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, uint32_t cap,
+                   cudaStream_t s);
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);

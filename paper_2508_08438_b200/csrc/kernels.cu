@@ -1433,6 +1433,9 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t lane = lane_id();
   uint32_t inserted = 0;
+  // the admit of this batch overflowed the user table (k_intern_users, err bit 8): its creator
+  // indices are invalid, so nothing is inserted or recorded (the host raises CapacityExhausted)
+  if (*reinterpret_cast<volatile uint32_t*>(err_flag) & 8u) return;
   // warp = prompt; a grid smaller than one warp per prompt strides over them
   const uint32_t stride = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n_prompts; p += stride) {
@@ -1869,7 +1872,7 @@ __global__ void k_commit_fixup_min(Index ix, const uint32_t* __restrict__ fix_li
 __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
                                const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
-                               uint32_t fix_cap, int pending_labels, uint32_t* n_revived) {
+                               uint32_t fix_cap, int pending_labels, uint32_t* n_revived, MonCtx P) {
   const uint32_t nf = min(*n_fix, fix_cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
@@ -1882,7 +1885,18 @@ __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, c
     // resets it, and it is still in its parent's child list
     if (ix.em && ix.em[s].dead && atomicExch(&ix.em[s].dead, 0u)) {
       ix.e[s].stats = Stats{0u, 0u, 0u, 0u};
-      ix.e[s].aux.set_idx = kNone;
+      // an entry already listed in the current window (set_idx set) keeps its place in the list
+      // (acquire_set must not append it twice) but gets a fresh, empty user set: a set allocated
+      // in this window has no live member (pool sets are only reused across windows)
+      if (ix.e[s].aux.set_idx != kNone && P.hdr) {
+        const uint32_t si = atomicAdd(P.pool_count, 1u);
+        if (si >= P.pool_cap) {
+          atomicOr(P.err, 1u);
+        } else {
+          P.hdr[si] = SetHdr{0u, 0u, 0u, 0u, 0ull};
+          ix.e[s].aux.set_idx = si;
+        }
+      }
       ix.e[s].aux.mark = 0;
       ix.em[s].node_id = kNone;  // assigned by the exact pass (duplicate claims exist)
       ix.em[s].depth = b;
@@ -2100,7 +2114,8 @@ __global__ void k_set_tiers(Index ix, const uint64_t* h, const uint64_t* d, cons
   }
 }
 
-__global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_entry* out, uint32_t* n_out) {
+__global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_entry* out, uint32_t* n_out,
+                         uint32_t cap) {
   uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s > ix.mask) return;
   const Rec& r = ix.e[s].rec;
@@ -2117,7 +2132,8 @@ __global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_en
   e.u_cnt = st.u_cnt;
   e.hit_pre = st.hit_pre;
   e.u_pre = st.u_pre;
-  out[atomicAdd(n_out, 1u)] = e;
+  const uint32_t k = atomicAdd(n_out, 1u);
+  if (k < cap) out[k] = e;  // the count is exact even past cap (the host re-sizes and retries)
 }
 
 __global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask) {
@@ -2506,7 +2522,8 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                    uint32_t n, uint32_t* slot, unsigned long long* n_new, uint32_t* fix_list, uint32_t* n_fix,
                    uint32_t fix_cap, uint32_t* err_flag, int fix_grid, const uint32_t* matched,
                    const uint64_t* users64, const MonCtx* mon, int pending_labels, uint64_t n_blocks, int n_sm,
-                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived, cudaStream_t s) {
+                   const uint32_t* bprompt, uint32_t* late, uint32_t* n_late, uint32_t* n_revived,
+                   const MonCtx& pool, cudaStream_t s) {
   const MonCtx M = mon ? *mon : MonCtx{};
   if (!n) return;
 #if SKV_COMMIT_FLAT
@@ -2518,7 +2535,7 @@ void launch_commit(const Index& ix, const uint64_t* h, const uint64_t* d, const 
                         late, n_late, err_flag, matched, users64, M, pending_labels);
     k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
     k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
-                                            pending_labels, n_revived);
+                                            pending_labels, n_revived, pool);
     k_commit_links<<<fix_grid, 256, 0, s>>>(ix, slot, late, n_late, fix_cap);
     return;
   }
@@ -2537,7 +2554,7 @@ ix, h, d, blk_off, exist, label, users, owners, n,
                                                                     pending_labels);
   k_commit_fixup_min<<<fix_grid, 256, 0, s>>>(ix, fix_list, n_fix, fix_cap);
   k_commit_fixup<<<fix_grid, 256, 0, s>>>(ix, blk_off, label, users, owners, fix_list, n_fix, fix_cap,
-                                          pending_labels, n_revived);
+                                          pending_labels, n_revived, pool);
 }
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
@@ -2582,8 +2599,9 @@ void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, con
   if (n) k_set_tiers<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, boff, n_prompts, tiers, n);
 }
 
-void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, cudaStream_t s) {
-  k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, user_rev, static_cast<skv_entry*>(out), n_out);
+void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, uint32_t cap,
+                   cudaStream_t s) {
+  k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, user_rev, static_cast<skv_entry*>(out), n_out, cap);
 }
 
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s) {
@@ -2627,18 +2645,18 @@ __global__ void k_intern_users(UserTable t, const uint64_t* __restrict__ users, 
     if (k == kNoUser) k = atomicCAS(&t.keys[s], kNoUser, u);
     if (k == kNoUser) {  // inserted: allocate (index 0 is reserved)
       const uint32_t id = atomicAdd(t.count, 1u) + 1;
-      if (id >= t.cap) atomicOr(err, 8u);
+      if (id >= t.cap) atomicOr(err, 8u);  // k_commit then inserts nothing (no creator past the table)
       if (id < t.cap) t.rev[id] = u;
       __threadfence();
       atomicExch(&t.idx[s], id + 1);
-      uidx[p] = id;
+      uidx[p] = id < t.cap ? id : 0u;
       return;
     }
     if (k == u) {
       uint32_t v;
       while ((v = *reinterpret_cast<volatile uint32_t*>(&t.idx[s])) == 0) {
       }
-      uidx[p] = v - 1;
+      uidx[p] = v - 1 < t.cap ? v - 1 : 0u;
       return;
     }
   }

@@ -274,10 +274,11 @@ class AdmissionEngine:
         n = C.c_size_t()
         ep = C.c_uint64()
         self._check(self._lib.skv_epoch(self._h, buf, cap, C.byref(n), C.byref(ep)))
+        if n.value > cap:  # the epoch is applied; fetch the whole list (skv_last_events)
+            buf = self._evbuf = (N.Event * n.value)()
+            self._check(self._lib.skv_last_events(self._h, buf, n.value, C.byref(n)))
         evs = [AnomalyEvent(e.h, e.d, e.action, e.owner, e.entropy_now, e.entropy_prev, e.u_pre, e.epoch)
-               for e in buf[:min(cap, n.value)]]
-        if n.value > cap:
-            raise N.CapacityExhausted(f"{n.value} events > buffer {cap}")
+               for e in buf[:n.value]]
         return int(ep.value), evs
 
     # --------------------------------------------------------------- misc
@@ -383,58 +384,18 @@ class AdmissionEngine:
         return int(d.value)
 
 
-@dataclass
-class GenSpec:
-    n_prompts: int
-    prompt_tokens: int
-    n_users: int = 64
-    first_user: int = 1
-    pool_size: int = 256
-    pool_tokens: int = 640
-    shared_fraction: float = 1.0
-    pii_per_kib: float = 1.0
-    pii_mix: int = 0
-    seed: int = 1
-    prompt_id_base: int = 0
-    # prefix-forest partitioning: emit the first n_prompts ids routed to route_rank
-    route_world: int = 1
-    route_rank: int = 0
-    route_block_tokens: int = 16
-
-    def native(self, ids_out: Optional[np.ndarray] = None) -> N.GenSpec:
-        return N.GenSpec(self.n_prompts, self.prompt_tokens, self.n_users, self.first_user, self.pool_size,
-                         self.pool_tokens, self.shared_fraction, self.pii_per_kib, self.pii_mix, self.seed,
-                         self.prompt_id_base, self.route_world, self.route_rank, self.route_block_tokens, 0,
-                         _ptr(ids_out))
-
-
-def generate(spec: GenSpec, nthreads: int = 0, tokens_out: Optional[np.ndarray] = None,
-             return_ids: bool = False):
-    """Deterministic synthetic batch (host).  Returns tokens, offsets, users, owners
-    (+ the global prompt ids with ``return_ids``)."""
-    lib = N.load_library()
-    n, L = spec.n_prompts, spec.prompt_tokens
-    tokens = tokens_out if tokens_out is not None else np.empty(n * L, np.uint32)
-    offsets = np.empty(n + 1, np.uint64)
-    users = np.empty(n, np.uint64)
-    owners = np.empty(n, np.uint8)
-    ids = np.empty(n, np.uint64)
-    s = spec.native(ids)
-    N.raise_for(lib.skv_generate(C.byref(s), _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), nthreads),
-                "generate")
-    return (tokens, offsets, users, owners, ids) if return_ids else (tokens, offsets, users, owners)
-
-
 def route(tokens: np.ndarray, offsets: np.ndarray, world: int, block_tokens: int,
-          prompt_ids: Optional[np.ndarray] = None) -> np.ndarray:
-    """skv_route: owning rank of every prompt under prefix-forest partitioning (host)."""
+          prompt_ids: Optional[np.ndarray] = None, depth: int = 0) -> np.ndarray:
+    """skv_route_depth: owning rank of every prompt (host).  Entries at depth < ``depth`` are
+    replicated; deeper ones belong to the rank of their depth-``depth`` ancestor's key."""
     lib = N.load_library()
     tokens = np.ascontiguousarray(tokens, np.uint32)
     offsets = np.ascontiguousarray(offsets, np.uint64)
     n = len(offsets) - 1
     ids = None if prompt_ids is None else np.ascontiguousarray(prompt_ids, np.uint64)
     out = np.empty(n, np.uint32)
-    N.raise_for(lib.skv_route(_ptr(tokens), _ptr(offsets), n, block_tokens, _ptr(ids), world, _ptr(out)), "route")
+    N.raise_for(lib.skv_route_depth(_ptr(tokens), _ptr(offsets), n, block_tokens, depth, _ptr(ids), world, _ptr(out)),
+                "route")
     return out
 
 
@@ -450,26 +411,3 @@ def split_batch(tokens, offsets, users, owners, ranks: np.ndarray, rank: int):
     tok = np.concatenate(parts).astype(np.uint32) if parts else np.zeros(0, np.uint32)
     own = None if owners is None else np.asarray(owners, np.uint8)[sel]
     return tok, off, np.asarray(users, np.uint64)[sel], own
-
-
-def generate_pool(spec: GenSpec, rank: Optional[int] = None):
-    """The shared-prefix pool; with ``rank`` (and spec.route_world > 1) only the
-    prefixes whose prefix-forest root is owned by that rank."""
-    toks, off, users, owners = _generate_pool(spec)
-    if rank is None or spec.route_world <= 1:
-        return toks, off, users, owners
-    ranks = route(toks, off, spec.route_world, spec.route_block_tokens)
-    return split_batch(toks, off, users, owners, ranks, rank)
-
-
-def _generate_pool(spec: GenSpec):
-    lib = N.load_library()
-    n, L = spec.pool_size, spec.pool_tokens
-    tokens = np.empty(n * L, np.uint32)
-    offsets = np.empty(n + 1, np.uint64)
-    users = np.empty(n, np.uint64)
-    owners = np.empty(n, np.uint8)
-    s = spec.native()
-    N.raise_for(lib.skv_generate_pool(C.byref(s), _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners)),
-                "generate_pool")
-    return tokens, offsets, users, owners

@@ -123,15 +123,6 @@ class CostModel(C.Structure):
                 ("noise_sigma_ms", C.c_double), ("seed", C.c_uint64)]
 
 
-class GenSpec(C.Structure):
-    _fields_ = [("n_prompts", C.c_uint64), ("prompt_tokens", C.c_uint64), ("n_users", C.c_uint64),
-                ("first_user", C.c_uint64), ("pool_size", C.c_uint64), ("pool_tokens", C.c_uint64),
-                ("shared_fraction", C.c_double), ("pii_per_kib", C.c_double), ("pii_mix", C.c_uint32),
-                ("seed", C.c_uint64), ("prompt_id_base", C.c_uint64), ("route_world", C.c_uint32),
-                ("route_rank", C.c_uint32), ("route_block_tokens", C.c_uint32), ("pad_", C.c_uint32),
-                ("prompt_ids_out", C.c_void_p)]
-
-
 # name -> (restype, argtypes); this table is also the export list checked by the CPU tests
 SIGNATURES = {
     "skv_rules_default": (C.c_int, [C.POINTER(C.c_void_p)]),
@@ -157,6 +148,7 @@ SIGNATURES = {
     "skv_commit": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "skv_epoch": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t),
                             C.POINTER(C.c_uint64)]),
+    "skv_last_events": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_set_label_policy": (C.c_int, [C.c_void_p, C.c_int]),
     "skv_resolve_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
                                      C.c_void_p]),
@@ -172,9 +164,9 @@ SIGNATURES = {
     "skv_admit_ttft": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
-    "skv_generate": (C.c_int, [C.POINTER(GenSpec), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "skv_route": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]),
-    "skv_generate_pool": (C.c_int, [C.POINTER(GenSpec), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "skv_route_depth": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                  C.c_uint32, C.c_void_p]),
 }
 
 _lib = None

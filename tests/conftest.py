@@ -18,6 +18,9 @@ def _ensure_built():
     lib = ROOT / "paper_2508_08438_b200" / "libsafekv_b200.so"
     orc = ROOT / "oracle" / "_ref" / "liboracle.so"
     ref = ROOT / "oracle" / "_ref" / "libsafekv_ref.so"
+    gen = ROOT / "workload" / "libskv_gen.so"
+    if not gen.exists():
+        subprocess.run(["make", "-C", str(ROOT), "workload/libskv_gen.so"], check=True, capture_output=True)
     if not lib.exists():
         subprocess.run(["make", "-C", str(ROOT), "-j8", "paper_2508_08438_b200/libsafekv_b200.so"], check=True,
                        capture_output=True)

@@ -10,7 +10,8 @@ import pytest
 
 from conftest import gpu_available
 from paper_2508_08438_b200 import native as N
-from paper_2508_08438_b200 import AdmissionEngine, CudaError, GenSpec, generate, generate_pool
+from paper_2508_08438_b200 import AdmissionEngine, CudaError
+from workload import GenSpec, generate, generate_pool
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 
@@ -34,7 +35,7 @@ def test_struct_layouts_match_header(tmp_path):
     """Every ctypes mirror has the size and field offsets the C compiler gives the header."""
     import subprocess
     pairs = {"skv_event": N.Event, "skv_entry": N.Entry, "skv_config": N.Config, "skv_batch": N.Batch,
-             "skv_admit_out": N.AdmitOut, "skv_stage_times": N.StageTimes, "skv_gen_spec": N.GenSpec,
+             "skv_admit_out": N.AdmitOut, "skv_stage_times": N.StageTimes,
              "skv_dfa_view": N.DfaView, "skv_cost_model": N.CostModel}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "safekv_b200.h"', "int main(void){"]
     for cname, cls in pairs.items():
@@ -54,6 +55,52 @@ def test_struct_layouts_match_header(tmp_path):
         for f, _ in cls._fields_:
             if f != "pad":
                 assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, f"{cname}.{f}"
+
+
+def test_generator_struct_layout(tmp_path):
+    """workload/skv_gen.h's spec struct matches its ctypes mirror."""
+    import subprocess
+    import workload as W
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "skv_gen.h"', "int main(void){",
+             'printf("size %zu\\n", sizeof(skvgen_spec));']
+    for f, _ in W._Spec._fields_:
+        lines.append(f'printf("{f} %zu\\n", offsetof(skvgen_spec, {f}));')
+    lines.append("return 0;}")
+    src = tmp_path / "gl.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "gl"
+    subprocess.run(["gcc", "-I", str(ROOT / "workload"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert int(got["size"]) == C.sizeof(W._Spec)
+    for f, _ in W._Spec._fields_:
+        assert int(got[f]) == getattr(W._Spec, f).offset, f
+
+
+def test_generator_is_not_in_the_product_library():
+    """The bench/test generator lives in workload/ (and oracle/_ref for the reference arm),
+    never in the product library."""
+    lib = N.load_library()
+    for name in ("skvgen_generate", "skv_generate", "skv_generate_pool"):
+        assert not hasattr(lib, name), name
+
+
+def test_reference_arm_generator_is_identical(ref):
+    """The reference arm binds the generator from oracle/_ref/libsafekv_ref.so (compiled from
+    the same source): both produce the same bytes."""
+    import importlib
+    import workload as W
+    spec = GenSpec(n_prompts=40, prompt_tokens=2048, seed=7, prompt_id_base=123456)
+    a = generate(spec)
+    try:
+        W.use_library(ROOT / "oracle" / "_ref" / "libsafekv_ref.so")
+        b = generate(spec)
+        pa = generate_pool(spec)
+    finally:
+        W.use_library()
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    for x, y in zip(pa, generate_pool(spec)):
+        np.testing.assert_array_equal(x, y)
 
 
 def test_no_cpu_fallback_without_gpu():

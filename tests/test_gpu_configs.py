@@ -21,7 +21,8 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, GenSpec, generate, generate_pool
+from paper_2508_08438_b200 import AdmissionEngine, EngineConfig
+from workload import GenSpec, generate, generate_pool
 from refh import RefEngine, RefRules
 from test_gpu_parity import check_admit, check_events, check_index
 

@@ -4,7 +4,7 @@ empty index -- each with the reference's behaviour where the reference has one."
 import numpy as np
 import pytest
 
-from paper_2508_08438_b200 import (AdmissionEngine, ArgError, CapacityExhausted, EngineConfig, StateError)
+from paper_2508_08438_b200 import AdmissionEngine, ArgError, CapacityExhausted, EngineConfig, StateError
 from refh import RefEngine, RefRules
 from test_gpu_parity import check_admit, check_index
 

@@ -113,3 +113,54 @@ def test_evict_speculative_node_ids(ref, gpu):
             _evict(eng, re_, eng.entry_count() // 2)
         finally:
             re_.close()
+
+
+def test_evict_revive_rematch_in_one_window(ref, gpu):
+    """Entries touched in the current monitor window are evicted, re-inserted (revived as
+    fresh nodes with empty windows) and matched again, all before the window's epoch: the
+    revived entry's user set starts empty and its window is rolled once."""
+    rng = np.random.default_rng(31)
+    trunks = make_trunks(rng, 5)
+    B, W = 4, 8
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=1024,
+                       max_tokens=1 << 18, max_window_entries=1 << 14, u_pre_max=3, entropy_jump=0.1)
+    with AdmissionEngine(cfg) as eng:
+        eng.enable_eviction()
+        re_ = RefEngine(ref, RefRules(ref), B=B, W=W, u_pre_max=3, jump=0.1)
+        try:
+            rs = eng.rules
+            batches = [make_batch(rng, trunks, 60, 7) for _ in range(3)]
+            _step(eng, re_, rs, batches[0])                 # window 1 closes
+            _step(eng, re_, rs, batches[1], epoch=False)    # window 2: touches entries
+            _evict(eng, re_, eng.entry_count() // 2)        # ... evicts some of them
+            _step(eng, re_, rs, batches[1], epoch=False)    # ... re-inserts (revives) them
+            _step(eng, re_, rs, batches[1], epoch=False)    # ... and matches them again
+            _step(eng, re_, rs, batches[2])                 # window 2 closes: events, roll
+            _step(eng, re_, rs, batches[1])
+        finally:
+            re_.close()
+
+
+def test_evict_refused_while_batch_pending(ref, gpu):
+    """An admitted batch's matched path is pinned until its commit: evict in between is a
+    state error, and the context stays consistent."""
+    from paper_2508_08438_b200 import StateError
+    rng = np.random.default_rng(32)
+    trunks = make_trunks(rng, 5)
+    cfg = EngineConfig(block_tokens=4, window_tokens=8, index_capacity=1 << 14, max_prompts=256,
+                       max_tokens=1 << 16, max_window_entries=1 << 12)
+    with AdmissionEngine(cfg) as eng:
+        eng.enable_eviction()
+        re_ = RefEngine(ref, RefRules(ref), B=4, W=8)
+        try:
+            _step(eng, re_, eng.rules, make_batch(rng, trunks, 40, 4))
+            batch = make_batch(rng, trunks, 40, 4)
+            check_admit(eng.rules, eng.admit(*batch), re_.admit(*batch))
+            with pytest.raises(StateError):
+                eng.evict(5)
+            eng.commit()
+            re_.commit()
+            check_index(eng, re_)
+            _evict(eng, re_, 5)
+        finally:
+            re_.close()

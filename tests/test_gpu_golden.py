@@ -124,7 +124,7 @@ def test_large_batch_properties(gpu):
     matches exactly its 40-block pool prefix (pool pre-inserted, Public), labels are a
     prefix-OR of the window masks, keys of identical pool prefixes coincide, and a
     sample of prompts agrees with the C oracle."""
-    from paper_2508_08438_b200 import GenSpec, generate, generate_pool
+    from workload import GenSpec, generate, generate_pool
     spec = GenSpec(n_prompts=65536, prompt_tokens=2048, seed=1)
     tok, off, users, owners = generate(spec)
     ptok, poff, pusers, powners = generate_pool(spec)

@@ -51,7 +51,7 @@ def check_index(eng, ref_eng):
 
 
 def run_scenario(ref, seed, B, W, n_batches, n_prompts, n_users, jump=0.3, u_pre_max=1, epoch_every=1,
-                 wide_p=0.0, rules_json=None):
+                 wide_p=0.0, rules_json=None, ev_cap=1 << 16):
     rng = np.random.default_rng(seed)
     trunks = make_trunks(rng, 12)
     cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 18, max_prompts=4096,
@@ -72,7 +72,7 @@ def run_scenario(ref, seed, B, W, n_batches, n_prompts, n_users, jump=0.3, u_pre
                 eng.commit()
                 re_.commit()
                 if (k + 1) % epoch_every == 0:
-                    ep_g, ev_g = eng.epoch_pass()
+                    ep_g, ev_g = eng.epoch_pass(cap=ev_cap)
                     ep_r, ev_r = re_.epoch(cap=1 << 16)
                     assert ep_g == ep_r
                     check_events(ev_g, ev_r)
@@ -88,10 +88,11 @@ def test_parity_b16_w32(ref, gpu, seed):
     run_scenario(ref, seed, B=16, W=32, n_batches=6, n_prompts=160, n_users=4)
 
 
-@pytest.mark.parametrize("seed", [11, 12])
-def test_parity_small_blocks_many_events(ref, gpu, seed):
-    # B=4 makes deep trees, many shared entries and frequent monitor events
-    fired = run_scenario(ref, seed, B=4, W=8, n_batches=8, n_prompts=120, n_users=3)
+@pytest.mark.parametrize("seed,ev_cap", [(11, 1 << 16), (12, 1)])
+def test_parity_small_blocks_many_events(ref, gpu, seed, ev_cap):
+    # B=4 makes deep trees, many shared entries and frequent monitor events; ev_cap=1: every
+    # epoch overflows the caller's event buffer and the rest comes from skv_last_events
+    fired = run_scenario(ref, seed, B=4, W=8, n_batches=8, n_prompts=120, n_users=3, ev_cap=ev_cap)
     assert fired > 0
 
 

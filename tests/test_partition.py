@@ -16,7 +16,8 @@ import numpy as np
 import pytest
 
 from oracle_c import OracleEngine, lib as orc_lib
-from paper_2508_08438_b200 import GenSpec, generate, route, split_batch
+from paper_2508_08438_b200 import route, split_batch
+from workload import GenSpec, generate
 from workloads import make_batch, make_trunks
 
 WORLD = 2

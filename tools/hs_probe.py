@@ -5,7 +5,8 @@ import numpy as np
 import torch
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, GenSpec, generate, generate_pool
+from paper_2508_08438_b200 import AdmissionEngine, EngineConfig
+from workload import GenSpec, generate, generate_pool
 from paper_2508_08438_b200 import native as N
 
 n = 65536

@@ -1,5 +1,5 @@
-// workload.cpp -- deterministic synthetic prompt batches for the bench configs
-// (SURVEY.md section 8(d)).  Built from the reference's generator primitives, restated:
+// skv_gen.cpp -- deterministic synthetic prompt batches for the bench configs and tests
+// (SURVEY.md section 8(d)).  BENCH / TEST INFRASTRUCTURE, not product code (see skv_gen.h).  Built from the reference's generator primitives, restated:
 //   SplitMix64 / derive_seed      (util.hpp:14-55)
 //   detail::filler, base36        (workload.hpp:243-266)  letters-only, unique prefix
 //   detail::make_secret           (workload.hpp:182-241)  8 PII template families
@@ -11,7 +11,8 @@
 #include <thread>
 #include <vector>
 
-#include "../../include/safekv_b200.h"
+#include "skv_gen.h"
+#include "../paper_2508_08438_b200/csrc/route.hpp"
 
 namespace {
 
@@ -100,48 +101,17 @@ std::string make_secret(size_t family, SplitMix64& rng) {
   }
 }
 
-// ---- prefix-forest routing (multi-GPU partitioning)
-constexpr uint64_t kFnvOff = 0xcbf29ce484222325ULL, kFnvP = 0x100000001b3ULL;
-
-uint64_t fnv_u32(uint64_t h, uint32_t v) {
-  for (int i = 0; i < 4; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * kFnvP;
-  return h;
-}
-uint64_t fnv_u64(uint64_t h, uint64_t v) { return fnv_u32(fnv_u32(h, static_cast<uint32_t>(v)), v >> 32); }
-
-// key h_0 of a prompt's first full block: FNV(u64 0 || u64 d_0), d_0 = token_seq_digest
-// (core.hpp:68-73) of tokens [0, B) -- the root of the prompt's path in the prefix forest
-uint64_t root_key(const uint32_t* t, uint32_t B) {
-  uint64_t d = fnv_u32(kFnvOff, B);
-  for (uint32_t i = 0; i < B; ++i) d = fnv_u32(d, t[i]);
-  return fnv_u64(fnv_u64(kFnvOff, 0), d);
-}
-
-uint32_t rank_of_root(uint64_t h0, uint32_t world) {
-  uint64_t z = h0 + 0x9e3779b97f4a7c15ULL;  // SplitMix64 finalizer, then multiply-high range map
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  z ^= z >> 31;
-  return static_cast<uint32_t>((static_cast<unsigned __int128>(z) * world) >> 64);
-}
-
-uint32_t route_one(const uint32_t* t, uint64_t len, uint32_t B, uint64_t prompt_id, uint32_t world) {
-  if (world <= 1) return 0;
-  if (len < B) return static_cast<uint32_t>(prompt_id % world);  // no index interaction
-  return rank_of_root(root_key(t, B), world);
-}
-
 constexpr uint64_t kPoolTag = 0x706f6f6c00000000ULL;   // "pool"
 constexpr uint64_t kPoolUniq = 0x10000000000ULL;       // filler counters of pool prefixes
 constexpr uint64_t kBodyUniq = 0x20000000000ULL;       // filler counters of prompt bodies
 
-std::string pool_prefix(const skv_gen_spec& s, uint64_t i) {
+std::string pool_prefix(const skvgen_spec& s, uint64_t i) {
   SplitMix64 rng(derive_seed(s.seed, kPoolTag + i));
   return filler(kPoolUniq + i, s.pool_tokens, rng);
 }
 
 // Unique body of `n` bytes with PII phrases planted at the configured density.
-std::string body(const skv_gen_spec& s, uint64_t gid, size_t n, SplitMix64& rng) {
+std::string body(const skvgen_spec& s, uint64_t gid, size_t n, SplitMix64& rng) {
   std::string b = filler(kBodyUniq + gid, n, rng);
   double rate = s.pii_per_kib;  // phrases per KiB
   if (s.pii_mix) {
@@ -168,9 +138,9 @@ std::string body(const skv_gen_spec& s, uint64_t gid, size_t n, SplitMix64& rng)
 
 extern "C" {
 
-int skv_generate_pool(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
+int skvgen_generate_pool(const skvgen_spec* s, uint32_t* tokens, uint64_t* offsets, uint64_t* users,
                       uint8_t* owners) {
-  if (!s || !tokens || !offsets) return SKV_ERR_ARG;
+  if (!s || !tokens || !offsets) return 1;
   for (uint64_t i = 0; i < s->pool_size; ++i) {
     std::string t = pool_prefix(*s, i);
     offsets[i] = i * s->pool_tokens;
@@ -179,26 +149,26 @@ int skv_generate_pool(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets
     if (owners) owners[i] = 0;
   }
   offsets[s->pool_size] = s->pool_size * s->pool_tokens;
-  return SKV_OK;
+  return 0;
 }
 
-int skv_route(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
-              const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out) {
-  if (!offsets || !rank_out || (n_prompts && !tokens) || block_tokens == 0 || world == 0) return SKV_ERR_ARG;
+int skvgen_route(const uint32_t* tokens, const uint64_t* offsets, uint32_t n_prompts, uint32_t block_tokens,
+                 uint32_t depth, const uint64_t* prompt_ids, uint32_t world, uint32_t* rank_out) {
+  if (!offsets || !rank_out || (n_prompts && !tokens) || block_tokens == 0 || world == 0) return 1;
   for (uint32_t p = 0; p < n_prompts; ++p) {
-    if (offsets[p + 1] < offsets[p]) return SKV_ERR_ARG;
-    rank_out[p] = route_one(tokens + offsets[p], offsets[p + 1] - offsets[p], block_tokens,
-                            prompt_ids ? prompt_ids[p] : p, world);
+    if (offsets[p + 1] < offsets[p]) return 1;
+    rank_out[p] = skvroute::route_one(tokens + offsets[p], offsets[p + 1] - offsets[p], block_tokens, depth,
+                                       prompt_ids ? prompt_ids[p] : p, world);
   }
-  return SKV_OK;
+  return 0;
 }
 
-int skv_generate(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets, uint64_t* users, uint8_t* owners,
+int skvgen_generate(const skvgen_spec* s, uint32_t* tokens, uint64_t* offsets, uint64_t* users, uint8_t* owners,
                  int nthreads) {
-  if (!s || !tokens || !offsets) return SKV_ERR_ARG;
-  if (s->n_users == 0 || s->prompt_tokens == 0) return SKV_ERR_CONFIG;
-  if (s->shared_fraction > 0 && (s->pool_size == 0 || s->pool_tokens >= s->prompt_tokens)) return SKV_ERR_CONFIG;
-  if (s->route_world > 1 && (s->route_rank >= s->route_world || s->route_block_tokens == 0)) return SKV_ERR_CONFIG;
+  if (!s || !tokens || !offsets) return 1;
+  if (s->n_users == 0 || s->prompt_tokens == 0) return 4;
+  if (s->shared_fraction > 0 && (s->pool_size == 0 || s->pool_tokens >= s->prompt_tokens)) return 4;
+  if (s->route_world > 1 && (s->route_rank >= s->route_world || s->route_block_tokens == 0)) return 4;
   const uint64_t N = s->n_prompts, L = s->prompt_tokens;
   std::vector<std::string> pool;
   if (s->shared_fraction > 0)
@@ -216,19 +186,20 @@ int skv_generate(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets, uin
   if (s->route_world <= 1) {
     for (uint64_t p = 0; p < N; ++p) gids[p] = s->prompt_id_base + p;
   } else {
-    const uint32_t B = s->route_block_tokens, G = s->route_world;
+    const uint32_t B = s->route_block_tokens, G = s->route_world, D = s->route_depth;
+    const uint64_t need = static_cast<uint64_t>(D + 1) * B;  // tokens that decide the rank
     std::vector<int> pool_rank(pool.size(), -1);
-    std::vector<uint32_t> tb(B);
+    std::vector<uint32_t> tb(need);
     auto tok_rank = [&](const std::string& t, uint64_t gid) {
-      if (t.size() < B) return static_cast<uint32_t>(gid % G);
-      for (uint32_t i = 0; i < B; ++i) tb[i] = static_cast<unsigned char>(t[i]);
-      return route_one(tb.data(), t.size(), B, gid, G);
+      if (L < need) return static_cast<uint32_t>(gid % G);
+      for (uint64_t i = 0; i < need; ++i) tb[i] = static_cast<unsigned char>(t[i]);
+      return skvroute::route_one(tb.data(), L, B, D, gid, G);
     };
     for (uint64_t gid = s->prompt_id_base, p = 0; p < N; ++gid) {
       SplitMix64 rng(derive_seed(s->seed, gid));
       uint32_t r;
-      if (s->shared_fraction > 0 && rng.next_double() < s->shared_fraction && s->pool_tokens >= B) {
-        const uint64_t i = rng.next_below(s->pool_size);  // the first B tokens are the pool prefix's
+      if (s->shared_fraction > 0 && rng.next_double() < s->shared_fraction && s->pool_tokens >= need) {
+        const uint64_t i = rng.next_below(s->pool_size);  // the deciding tokens are the pool prefix's
         if (pool_rank[i] < 0) pool_rank[i] = static_cast<int>(tok_rank(pool[i], gid));
         r = static_cast<uint32_t>(pool_rank[i]);
       } else {
@@ -258,7 +229,7 @@ int skv_generate(const skv_gen_spec* s, uint32_t* tokens, uint64_t* offsets, uin
   }
   for (auto& t : th) t.join();
   offsets[N] = N * L;
-  return SKV_OK;
+  return 0;
 }
 
 }  // extern "C"
