@@ -229,8 +229,9 @@ uint64_t skv_entry_count(skv_ctx* ctx);
 int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
 int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap);
-/* (skv_evict returns SKV_ERR_STATE between skv_admit and skv_commit: the pending batch's
- * matched path is pinned, like a request's path around insert in the reference.) */
+/* An admitted but uncommitted batch is dropped by skv_evict (its lookups and monitor records
+ * stand; its commit would attach blocks to entries the eviction may free -- the reference pins
+ * a request's path around insert), so a following skv_commit returns SKV_ERR_STATE. */
 
 /* Per-stage device times of the last skv_admit / skv_commit (CUDA events, ms). */
 typedef struct {

@@ -185,6 +185,7 @@ struct skv_ctx {
   std::vector<skv_event> last_events;  // every event of the last skv_epoch, sorted by key
   // pending batch (between admit and commit)
   bool pending = false;
+  bool dropped_by_evict = false;  // the last admitted batch was dropped by skv_evict
   // monitor records of the last admit, executed inside the commit kernel (overlapping
   // the claims), or on their own when the batch is not committed
   bool rec_pending = false;
@@ -769,6 +770,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
     ensure_admit_resolved(c);
     flush_record(c);  // the previous batch was admitted but not committed
+    c->dropped_by_evict = false;
     if (N == 0) {
       if (out) out->n_blocks = 0, out->matched_total = 0;
       c->pending = true;
@@ -1060,7 +1062,9 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     check_usable(c);
-    if (!c->pending) throw StateError("skv_commit without a preceding skv_admit");
+    if (!c->pending)
+      throw StateError(c->dropped_by_evict ? "skv_commit: the admitted batch was dropped by skv_evict (admit it again)"
+                                           : "skv_commit without a preceding skv_admit");
     CK(cudaSetDevice(c->device));
     cudaStream_t s = c->stream;
     if (c->p_n == 0) {
@@ -1353,10 +1357,12 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     if (!c->evict_on) throw StateError("eviction is not enabled (skv_enable_eviction before the first admit)");
     if (needed_blocks == 0) throw ArgError("evict: needed must be positive");
     check_usable(c);
-    // the pending batch's matched path is pinned until its commit (the reference pins a
-    // request's path around insert, cache_index.hpp:347-356, serving_sim.hpp:196,215): its
-    // lookup results would otherwise point at tombstones
-    if (c->pending && c->p_n) throw StateError("skv_evict between skv_admit and skv_commit (commit first)");
+    // an admitted, uncommitted batch is dropped: its lookups ran (and its monitor records were
+    // applied by flush_record), but its commit would attach new blocks to entries this call may
+    // tombstone (the reference pins a request's path around insert, cache_index.hpp:347-356,
+    // serving_sim.hpp:196,215), so a later skv_commit raises SKV_ERR_STATE
+    if (c->pending && c->p_n) c->dropped_by_evict = true;
+    c->pending = false;
     ensure_admit_resolved(c);
     flush_record(c);
     cudaStream_t s = c->stream;

@@ -141,9 +141,10 @@ def test_evict_revive_rematch_in_one_window(ref, gpu):
             re_.close()
 
 
-def test_evict_refused_while_batch_pending(ref, gpu):
-    """An admitted batch's matched path is pinned until its commit: evict in between is a
-    state error, and the context stays consistent."""
+def test_evict_drops_pending_batch(ref, gpu):
+    """An evict between admit and commit drops the admitted batch: its commit (which would
+    attach new blocks under entries the eviction may have freed) is a state error, the
+    context stays consistent, and the batch can be admitted again."""
     from paper_2508_08438_b200 import StateError
     rng = np.random.default_rng(32)
     trunks = make_trunks(rng, 5)
@@ -156,11 +157,9 @@ def test_evict_refused_while_batch_pending(ref, gpu):
             _step(eng, re_, eng.rules, make_batch(rng, trunks, 40, 4))
             batch = make_batch(rng, trunks, 40, 4)
             check_admit(eng.rules, eng.admit(*batch), re_.admit(*batch))
+            _evict(eng, re_, 5)  # the reference evicts between two submits (records applied)
             with pytest.raises(StateError):
-                eng.evict(5)
-            eng.commit()
-            re_.commit()
-            check_index(eng, re_)
-            _evict(eng, re_, 5)
+                eng.commit()
+            _step(eng, re_, eng.rules, batch)  # admitted again, committed on both sides
         finally:
             re_.close()
