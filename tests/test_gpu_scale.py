@@ -112,7 +112,7 @@ def test_scale_config4_long_context_tiered(ref, gpu):
             matched += int(got.matched_blocks.sum())
             # the slowest tier of a match (MatchResult::lowest_tier): SSD once it spans many blocks
             assert set(got.lowest_tier[got.matched_blocks > 8].tolist()) <= {2}
-        assert matched > 256 * 64  # long visible matches (uniform prefix lengths, half the prefixes Public)
+        assert matched > 2 * 256 * 16  # long visible matches (uniform prefix lengths, half the prefixes Public)
     finally:
         eng.close()
         re_.close()
