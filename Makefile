@@ -19,7 +19,7 @@ all: $(LIB) $(GENLIB) oracle
 $(BUILD):
 	mkdir -p $(BUILD)
 
-$(BUILD)/kernels.o: $(SRC)/kernels.cu $(SRC)/ctx.hpp include/safekv_b200.h | $(BUILD)
+$(BUILD)/kernels.o: $(SRC)/kernels.cu $(SRC)/hash_scan16.cuh $(SRC)/ctx.hpp include/safekv_b200.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; exit 1)
 
 $(BUILD)/capi.o: $(SRC)/capi.cpp $(SRC)/ctx.hpp $(SRC)/rules.hpp include/safekv_b200.h | $(BUILD)

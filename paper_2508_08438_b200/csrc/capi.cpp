@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -83,6 +84,11 @@ int log2u(uint64_t x) {
   return b;
 }
 
+bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && *v != '0';
+}
+
 uint64_t fnv_u32_host(uint64_t h, uint32_t v) {
   for (int i = 0; i < 4; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * 0x100000001b3ULL;
   return h;
@@ -100,6 +106,7 @@ struct skv_ctx {
   // rules
   skv_rules rules_host;
   skv::DevRules rules_dev;
+  skv::DevRules16 rules16;  // k_hash_scan16's automaton (B = 16, W = 32)
   void* rules_buf = nullptr;
   bool rules_loaded = false;
 
@@ -271,6 +278,8 @@ int guard(skv_ctx* c, F&& f) {
   }
 }
 
+void build_rules16(skv_ctx* c, const skv_rules& r);
+
 // Device form of the DFA (see ctx.hpp DevRules).  The 16-bit row offsets and the
 // 16-bit in-entry rule mask bound the device automaton; larger rule sets are rejected
 // here with CompileError (documented in DESIGN.md).
@@ -356,6 +365,61 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
     throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB (block_tokens too large)");
   c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem, 32 * c->hs_layout.warps);
   if (c->hs_grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
+  build_rules16(c, r);
+}
+
+// The B = 16 / W = 32 automaton of k_hash_scan16 (ctx.hpp DevRules16, hash_scan16.cuh): column t
+// < 128 of the image holds, for every state index (S base states, then their S shadow copies),
+// v(next) = 2 * index of the next state -- the shadow copy when the transition accepts a rule
+// or the state is a shadow already; column 128 holds the end-of-text rule mask.  Not built
+// (the general kernel runs) for other shapes or when the image does not fit SMEM beside the
+// per-warp task queues.
+void build_rules16(skv_ctx* c, const skv_rules& r) {
+  skv::DevRules16& R = c->rules16;
+  for (void* p : {static_cast<void*>(R.img), static_cast<void*>(R.hi), static_cast<void*>(R.full)})
+    if (p) CK(cudaFree(p));
+  R = skv::DevRules16{};
+  const auto& d = r.dfa;
+  const uint32_t S = d.n_states, C = d.n_classes;
+  if (c->cfg.block_tokens != 16 || c->cfg.window_tokens != 32 || 4ull * S >= 65536) return;
+  const uint32_t S2 = 2 * S, colbytes = 4 * S;
+  const uint32_t img_bytes = 129 * colbytes;
+  uint32_t q_cap = 256;  // deferred tasks per warp: shrink to fit, at least 3 segments x 32 lanes
+  while (q_cap > 96 && skv::hash_scan16_smem(img_bytes, q_cap) > 227 * 1024) q_cap -= 32;
+  if (skv::hash_scan16_smem(img_bytes, q_cap) > 227 * 1024) return;
+  std::vector<uint16_t> img(129ull * S2 + 8, 0), hi(128ull * S2, 0);
+  std::vector<uint32_t> full(256ull * S, 0);
+  for (uint32_t b = 0; b < 256; ++b) {
+    const uint32_t k = d.class_map[b];
+    uint16_t* col = b < 128 ? &img[static_cast<size_t>(b) * S2] : &hi[static_cast<size_t>(b - 128) * S2];
+    for (uint32_t s = 0; s < S; ++s) {
+      const uint32_t t = d.next[s * C + k], acc = d.acc[s * (C + 1) + k];
+      col[s] = static_cast<uint16_t>(2 * (t + (acc ? S : 0)));
+      col[S + s] = static_cast<uint16_t>(2 * (t + S));
+      full[static_cast<size_t>(b) * S + s] = (acc << 16) | (2 * t);
+    }
+  }
+  for (uint32_t s = 0; s < S; ++s)
+    img[128ull * S2 + s] = img[128ull * S2 + S + s] = static_cast<uint16_t>(d.acc[s * (C + 1) + C]);
+  const uint32_t smem = skv::hash_scan16_smem(img_bytes, q_cap);
+  const int grid = skv::hash_scan16_grid(c->device, smem);
+  if (grid <= 0) return;
+  const size_t img_al = (img_bytes + 15) & ~size_t(15);
+  CK(cudaMalloc(&R.img, img_al));
+  CK(cudaMalloc(&R.hi, hi.size() * 2));
+  CK(cudaMalloc(&R.full, full.size() * 4));
+  CK(cudaMemcpyAsync(R.img, img.data(), img_al, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(R.hi, hi.data(), hi.size() * 2, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(R.full, full.data(), full.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  sync_check(c->stream);
+  R.img_bytes = img_bytes;
+  R.colbytes = colbytes;
+  R.s2 = S2;
+  R.v_start = 2 * d.start;
+  R.q_cap = q_cap;
+  R.smem = smem;
+  R.grid = grid;
+  R.ok = true;
 }
 
 skv::MonCtx monitor_ctx(skv_ctx* c) {
@@ -377,7 +441,41 @@ skv::MonCtx monitor_ctx(skv_ctx* c) {
 // batch whose block offsets are already in blk_off (the kernel reads the block count
 // from blk_off[N], so no host round trip is needed).
 void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t* off, uint32_t N, uint64_t n_tokens,
-             uint64_t nb_hint, uint32_t* blk_off, uint32_t* first_sens, uint64_t* bd, uint32_t* bmask) {
+             uint64_t nb_hint, uint32_t* blk_off, uint32_t* first_sens, uint64_t* bd, uint32_t* bmask,
+             bool overlapped = false) {
+  static const bool force_general = getenv_flag("SKV_HS_GENERAL");
+  static const bool pf_general = getenv_flag("SKV_PF_GENERAL");
+  // a prefetch (stages 1-2 of the next batch beside the current commit) runs on a quarter of the
+  // SMs: the one-CTA-per-SM kernel would otherwise hold every SM until it ends and serialise the
+  // commit behind it (measured: 1.13 ms per config-2 step at full grid, 0.97 at a quarter)
+  static const int pf_frac = getenv("SKV_H16_PF_FRAC") ? atoi(getenv("SKV_H16_PF_FRAC")) : 4;
+  if (c->rules16.ok && !force_general && !(overlapped && pf_general)) {
+    const skv::DevRules16& R = c->rules16;
+    skv::HS16Args h;
+    h.tokens = tokens;
+    h.tok_off = off;
+    h.blk_off = blk_off;
+    h.n_prompts = N;
+    h.n_tokens = n_tokens;
+    h.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, 16);
+    h.img = R.img;
+    h.img_bytes = R.img_bytes;
+    h.hi = R.hi;
+    h.full = R.full;
+    h.colbytes = R.colbytes;
+    h.s2 = R.s2;
+    h.v_start = R.v_start;
+    h.q_cap = R.q_cap;
+    h.d_out = bd;
+    h.mask_out = bmask;
+    h.first_sens = first_sens;
+    // a small batch needs fewer CTAs (one 32-warp CTA per SM otherwise)
+    const uint64_t want = nb_hint ? (nb_hint + 32 * 32 - 1) / (32 * 32) : static_cast<uint64_t>(R.grid);
+    uint64_t grid = std::min<uint64_t>(R.grid, std::max<uint64_t>(want, 1));
+    if (overlapped && pf_frac > 1) grid = std::max<uint64_t>(1, grid / pf_frac);
+    skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st);
+    return;
+  }
   skv::HashScanArgs a;
   a.tokens = tokens;
   a.tok_off = off;
@@ -673,6 +771,9 @@ int skv_destroy(skv_ctx* c) {
   if (c->rec_stream) cudaStreamSynchronize(c->rec_stream);
   for (void* p : c->owned) cudaFree(p);
   if (c->rules_buf) cudaFree(c->rules_buf);
+  for (void* p : {static_cast<void*>(c->rules16.img), static_cast<void*>(c->rules16.hi),
+                  static_cast<void*>(c->rules16.full)})
+    if (p) cudaFree(p);
   if (c->host_small) cudaFreeHost(c->host_small);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -1038,7 +1139,7 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     skv::launch_exclusive_scan(c->side_temp, c->side_temp_bytes, c->alt_counts, c->alt_blk_off, N + 1, st);
     CK(cudaMemsetAsync(c->alt_first_sens, 0xff, N * 4ull, st));
     stage12(c, st, tokens, off, N, b->n_tokens, nb_hint, c->alt_blk_off, c->alt_first_sens, c->alt_bd,
-            c->alt_bmask);
+            c->alt_bmask, true);
     // the serial chained-key FNV too, overlapping the current batch's commit; its probe is
     // then lookups only
     if (kPrefetchChain)

@@ -112,6 +112,39 @@ struct DevRules {
   uint32_t copy_inv = 0;  // ceil(2^32 / row_bytes): j = umulhi(offset - kAccRegion, copy_inv)
 };
 
+// The B = 16 / W = 32 automaton of k_hash_scan16 (hash_scan16.cuh): byte-indexed
+// columns (entry (byte t, state) at t * colbytes + v, v = 2 * state index), every state with a
+// shadow copy (index + S) that accepting transitions enter and never leave.
+struct DevRules16 {
+  bool ok = false;       // built (B == 16, W == 32 and the image fits SMEM beside the task queues)
+  uint16_t* img = nullptr;   // 129 columns (bytes 0..127, then EOS rule masks) x 2S, SMEM image
+  uint32_t img_bytes = 0;
+  uint16_t* hi = nullptr;    // bytes 128..255 (global)
+  uint32_t* full = nullptr;  // [256][S]: (rule mask << 16) | v(next), base states (exact masks)
+  uint32_t colbytes = 0, s2 = 0, v_start = 0, q_cap = 0, smem = 0;
+  int grid = 0;
+};
+
+struct HS16Args {
+  const uint32_t* tokens;
+  const uint64_t* tok_off;
+  const uint32_t* blk_off;
+  uint32_t n_prompts;
+  uint64_t n_tokens;
+  uint64_t digest_init;
+  const uint16_t* img;
+  uint32_t img_bytes;
+  const uint16_t* hi;
+  const uint32_t* full;
+  uint32_t colbytes;  // 4S
+  uint32_t s2;        // 2S: v >= s2 <=> shadow (accepted) state
+  uint32_t v_start;
+  uint32_t q_cap;  // deferred exact tasks per warp (>= 96)
+  uint64_t* d_out;
+  uint32_t* mask_out;
+  uint32_t* first_sens;
+};
+
 struct HashScanArgs {
   const uint32_t* tokens;
   const uint64_t* tok_off;
@@ -213,6 +246,11 @@ void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, ui
 int hash_scan_grid(int device, uint32_t smem_bytes, uint32_t threads);
 HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s);
+// k_hash_scan16: fixed task-queue / slot layout; returns the dynamic SMEM bytes for an image and
+// queue capacity, and the persistent grid (-1 on failure)
+uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap);
+int hash_scan16_grid(int device, uint32_t smem);
+void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,

@@ -764,6 +764,8 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
   flush_tasks(q, qn, lane, tab, cmap, acc_tab, inv, a);
 }
 
+#include "hash_scan16.cuh"
+
 // find_slot: used by set_tiers (point lookups of block b, group leader key (hL, dL))
 __device__ __forceinline__ uint32_t find_slot(const Index& ix, uint64_t h, uint64_t d, uint64_t hL, uint64_t dL,
                                               uint32_t b, Rec* out) {
@@ -2219,6 +2221,29 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
   const uint32_t g = a.n_blocks ? std::min<uint32_t>(grid, (a.n_blocks + wpc - 1) / wpc) : static_cast<uint32_t>(grid);
   if (a.n_prompts == 0 || g == 0) return;
   k_hash_scan<<<g, threads, smem, s>>>(a);
+}
+
+uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap) {
+  return round16(img_bytes) + 4 * kH16Warps * static_cast<uint32_t>(sizeof(Slot16)) +
+         kH16Warps * q_cap * static_cast<uint32_t>(sizeof(H16Task));
+}
+
+int hash_scan16_grid(int device, uint32_t smem) {
+  if (cudaFuncSetAttribute(k_hash_scan16, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+      cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan16, kH16Warps * 32, smem) != cudaSuccess ||
+      per_sm < 1)
+    return -1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return per_sm * sms;
+}
+
+void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s) {
+  if (a.n_prompts == 0 || grid <= 0) return;
+  k_hash_scan16<<<grid, kH16Warps * 32, smem, s>>>(a);
 }
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
