@@ -25,6 +25,13 @@ KEYS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "SMEM wavefronts", 1.0),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "SMEM bank conflicts", 1.0),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate (%)", 1.0),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 sectors read", 1.0),
+    ("lts__t_sectors_srcunit_tex_op_write.sum", "L2 sectors written", 1.0),
+    ("lts__t_sectors_srcunit_tex_op_atom.sum", "L2 sectors atomic", 1.0),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 sectors reduction", 1.0),
+    ("lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "L2 read sectors hit", 1.0),
+    ("dram__sectors_read.sum", "DRAM sectors read", 1.0),
+    ("dram__sectors_write.sum", "DRAM sectors written", 1.0),
     ("launch__registers_per_thread", "registers/thread", 1.0),
     ("launch__grid_size", "grid", 1.0),
 ]
@@ -72,6 +79,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--title", default="ncu summary")
     ap.add_argument("--traffic-json")
+    ap.add_argument("--units", action="append", default=[],
+                    help="kernel=count[:name]: also print DRAM / L2 sectors per unit (e.g. k_commit=5767168:new block)")
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
     if a.launches:
@@ -85,8 +94,20 @@ def main():
         for name, vals, stalls in rep_metrics(rep):
             lines += [f"### {name}", "", "| metric | value |", "|---|---|"]
             lines += [f"| {k} | {v:,.2f} |" for k, v in vals.items()]
-            lines += [f"| top stalls (per issue) | {', '.join(f'{s}={x:.2f}' for s, x in stalls)} |", ""]
-            if a.traffic_json and name == "k_hash_scan":
+            lines += [f"| top stalls (per issue) | {', '.join(f'{s}={x:.2f}' for s, x in stalls)} |"]
+            for u in a.units:
+                k, rest = u.split("=", 1)
+                cnt, _, uname = rest.partition(":")
+                if name.startswith(k) and float(cnt) > 0:
+                    n = float(cnt)
+                    for lab in ("DRAM sectors read", "DRAM sectors written", "L2 sectors read", "L2 sectors atomic",
+                                "L2 sectors written"):
+                        if lab in vals:
+                            lines.append(f"| {lab} per {uname or 'unit'} | {vals[lab] / n:.2f} |")
+                    mb = vals.get("DRAM read (MB)", 0) + vals.get("DRAM write (MB)", 0)
+                    lines.append(f"| DRAM bytes per {uname or 'unit'} | {mb * 1e6 / n:.1f} |")
+            lines.append("")
+            if a.traffic_json and name.startswith("k_hash_scan"):
                 mb = vals.get("DRAM read (MB)", 0) + vals.get("DRAM write (MB)", 0)
                 json.dump({"kernel": name, "dram_bytes_per_launch": mb * 1e6, "source": rep},
                           open(a.traffic_json, "w"), indent=1)
