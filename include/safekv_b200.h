@@ -272,6 +272,48 @@ int skv_tier1_scan(skv_ctx* ctx, const char* text, size_t len, uint32_t* rule_ma
 int skv_token_seq_digest(skv_ctx* ctx, const uint32_t* tokens, size_t n, uint64_t* digest);
 
 /* ------------------------------------------------------------------------------
+ * Replicated layer (multi-GPU; north star: "each GPU holds a replica
+ * of the index, and new-entry inserts and entropy counters are merged across GPUs").  Entries
+ * at depth < depth (the first `depth` blocks of every prompt: system prompts, shared roots)
+ * are replicated on every rank; deeper entries live on the rank skv_route_depth sends their
+ * prompts to.  Per batch every rank runs admit -> commit -> skv_replica_export; the caller
+ * all-gathers the exports (NCCL over NVLink; the accesses can stay in device memory) and every
+ * rank runs skv_replica_apply on the same data: the entries merged to the lowest global prompt
+ * id per key (first creator wins), the accesses as the raw concatenation of all ranks' exports,
+ * merged on the device (per (entry, user) the lowest first prompt id and the summed count, then
+ * replayed per entry in global prompt order).  The replicated entries therefore stay identical
+ * everywhere and their AccessStats equal a single engine's, the order-dependent 64-user
+ * saturation included.  The Python mirror is paper_2508_08438_b200.ReplicaGroup.  No reference
+ * counterpart (the reference is single-process).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t h, d;     /* entry key                                      */
+  uint64_t ph, pd;   /* parent key, (0, 0) for a root                  */
+  uint64_t creator;  /* UserId of the creating prompt                  */
+  uint64_t gid;      /* global id of the creating prompt               */
+  uint8_t label, owner, pad[6];
+} skv_rep_entry;     /* 56 B */
+typedef struct {
+  uint64_t h, d;     /* entry key                                      */
+  uint64_t user;     /* UserId                                         */
+  uint64_t gid;      /* global id of the user's first accessing prompt */
+  uint64_t count;    /* accesses                                       */
+} skv_rep_access;    /* 40 B */
+/* Before the first admit; not combinable with eviction. */
+int skv_set_replicated_depth(skv_ctx* ctx, uint32_t depth);
+/* After skv_commit: the replicated-layer entries the commit created (host) and the batch's
+ * replicated-layer accesses aggregated per (entry, user) (device memory when accs_on_device).
+ * prompt_gids[p] = global id of the last batch's prompt p (host).  When ecap / acap are too
+ * small, returns SKV_ERR_CAPACITY with *n_ents / *n_accs set (call again: the export is
+ * repeatable until skv_replica_apply). */
+int skv_replica_export(skv_ctx* ctx, const uint64_t* prompt_gids, skv_rep_entry* ents, size_t ecap, size_t* n_ents,
+                       skv_rep_access* accs, size_t acap, size_t* n_accs, int accs_on_device);
+/* Apply every rank's export: ents = the merged entries (host), accs = all ranks' access exports
+ * concatenated, unmerged (device memory when accs_on_device).  Ends the batch's sync. */
+int skv_replica_apply(skv_ctx* ctx, const skv_rep_entry* ents, size_t n_ents, const skv_rep_access* accs,
+                      size_t n_accs, int accs_on_device);
+
+/* ------------------------------------------------------------------------------
  * Multi-GPU request router (host).  Entries at depth < depth (the
  * first `depth` blocks of every prompt) are replicated on every rank; an entry at depth
  * >= depth belongs to the rank of the key h_depth of its depth-`depth` ancestor.  A prompt

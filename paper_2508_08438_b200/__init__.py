@@ -2,9 +2,12 @@
 lookup -> entropy monitor) behind the C ABI of include/safekv_b200.h."""
 from .native import (ArgError, CapacityExhausted, CompileError, ConfigError, CudaError, ParseError, SkvError,
                      StateError, load_library)
-from .engine import AdmissionEngine, AdmitResult, AnomalyEvent, EngineConfig, RuleSet, route, split_batch
+from .engine import (REP_ACCESS, REP_ENTRY, AdmissionEngine, AdmitResult, AnomalyEvent, EngineConfig, ReplicaGroup,
+                     RuleSet, merge_entries, merge_events, merge_replica, route, split_batch, torch_allgather,
+                     torch_allgather_device)
 
 __all__ = [
-    "AdmissionEngine", "AdmitResult", "AnomalyEvent", "EngineConfig", "RuleSet", "route", "split_batch", "load_library", "SkvError", "ArgError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
+    "AdmissionEngine", "AdmitResult", "AnomalyEvent", "EngineConfig", "RuleSet", "route", "split_batch",
+    "ReplicaGroup", "merge_replica", "merge_entries", "merge_events", "torch_allgather", "torch_allgather_device", "REP_ENTRY", "REP_ACCESS", "load_library", "SkvError", "ArgError", "ParseError", "CompileError", "ConfigError", "CapacityExhausted",
     "CudaError", "StateError",
 ]

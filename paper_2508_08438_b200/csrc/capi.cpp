@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -190,6 +191,17 @@ struct skv_ctx {
   // later batch call raises StateError with this reason; export still works)
   std::string poisoned;
   std::vector<skv_event> last_events;  // every event of the last skv_epoch, sorted by key
+  // replicated layer (skv_set_replicated_depth): device scratch of the export / apply
+  bool rep_sync_due = false;  // a committed batch waits for skv_replica_export / apply
+  skv_rep_entry* rep_ents = nullptr;   // export scratch (new_cap)
+  skv_rep_access* rep_accs = nullptr;  // export scratch (pair capacity)
+  uint64_t* rep_gids = nullptr;        // per prompt of the last batch
+  void* rep_in = nullptr;              // apply input (grown on demand)
+  size_t rep_in_bytes = 0;
+  uint32_t* rep_slots = nullptr;
+  uint32_t* rep_uidx = nullptr;
+  skv::RepScratch rep_w;  // device merge of the ranks' access exports
+  size_t rep_in_ents = 0;
   // pending batch (between admit and commit)
   bool pending = false;
   bool dropped_by_evict = false;  // the last admitted batch was dropped by skv_evict
@@ -771,6 +783,8 @@ int skv_destroy(skv_ctx* c) {
   if (c->rec_stream) cudaStreamSynchronize(c->rec_stream);
   for (void* p : c->owned) cudaFree(p);
   if (c->rules_buf) cudaFree(c->rules_buf);
+  for (void* p : {c->rep_in, static_cast<void*>(c->rep_slots), static_cast<void*>(c->rep_uidx)})
+    if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->rules16.img), static_cast<void*>(c->rules16.hi),
                   static_cast<void*>(c->rules16.full)})
     if (p) cudaFree(p);
@@ -841,6 +855,9 @@ uint32_t replay_record(skv_ctx* c, cudaStream_t s, uint32_t n_replay, uint32_t e
 // records of a batch that is not committed (next admit, epoch or export first)
 void flush_record(skv_ctx* c) {
   if (!c->rec_pending) return;
+  // a replicated layer aggregates the batch's accesses for the cross-rank merge, which follows
+  // the batch's commit: an uncommitted batch cannot be merged
+  if (c->ix.rep.depth) throw StateError("replicated layer: commit the admitted batch first");
   cudaStream_t s = c->stream;
   skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, s);
   finish_record(c, s);
@@ -869,6 +886,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const uint32_t B = c->cfg.block_tokens;
     if (N > c->max_prompts) throw ArgError("n_prompts exceeds max_prompts");
     if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
+    if (c->rep_sync_due) throw StateError("replicated layer: skv_replica_export / skv_replica_apply of the last batch first");
     ensure_admit_resolved(c);
     flush_record(c);  // the previous batch was admitted but not committed
     c->dropped_by_evict = false;
@@ -1179,6 +1197,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
     CK(cudaMemsetAsync(c->counters + 11, 0, 8, s));  // late child links, re-inserted tombstones
+    if (c->ix.rep.depth) CK(cudaMemsetAsync(c->ix.rep.new_n, 0, 4, s));
     ++c->batch_id;
     const bool rec = c->rec_pending;  // the batch's monitor records (see skv_admit)
     // The records (sector 1 of the matched entries, the window user sets) and the inserts
@@ -1260,6 +1279,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     c->times.kernels_launched += launched;
     c->times.new_blocks = nn;
     c->pending = false;
+    c->rep_sync_due = c->ix.rep.depth != 0;
     if (new_entries) *new_entries = nn;
     return SKV_OK;
   });
@@ -1433,6 +1453,7 @@ int skv_enable_eviction(skv_ctx* c, int tiered_demotion) {
     CK(cudaSetDevice(c->device));
     if (c->evict_on) return SKV_OK;
     if (c->entries || c->batch_id) throw StateError("skv_enable_eviction must precede the first admit");
+    if (c->ix.rep.depth) throw StateError("the replicated layer and eviction cannot be combined");
     skv::EvictMeta* em = dalloc<skv::EvictMeta>(c->ix.cap, c->owned);
     CK(cudaMemsetAsync(em, 0, c->ix.cap * sizeof(skv::EvictMeta), c->stream));
     const uint64_t N = std::max<uint64_t>(c->max_prompts, 1);
@@ -1494,6 +1515,157 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     }
     *n_evicted = v;
     if (v < needed_blocks) throw CapacityError("evict: no unpinned candidate leaf");
+    return SKV_OK;
+  });
+}
+
+// ------------------------------------------------------------------ replicated layer
+int skv_set_replicated_depth(skv_ctx* c, uint32_t depth) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (c->entries || c->batch_id || c->pending) throw StateError("skv_set_replicated_depth must precede the first admit");
+    if (c->evict_on) throw StateError("the replicated layer and eviction cannot be combined");
+    if (depth == 0 || c->ix.rep.depth) {
+      if (depth != c->ix.rep.depth && c->ix.rep.depth) throw StateError("replicated depth already set");
+      return SKV_OK;
+    }
+    skv::RepLayer& R = c->ix.rep;
+    uint32_t pairs = 1u << 16;
+    while (pairs < 4 * c->cfg.max_window_entries && pairs < (1u << 24)) pairs <<= 1;
+    R.pair_key = dalloc<ulonglong2>(pairs, c->owned);
+    R.pair_first = dalloc<uint32_t>(pairs, c->owned);
+    R.pair_gid = dalloc<unsigned long long>(pairs, c->owned);
+    skv::RepScratch& W = c->rep_w;
+    W.gid_a = dalloc<unsigned long long>(pairs, c->owned);
+    W.gid_b = dalloc<unsigned long long>(pairs, c->owned);
+    W.val_a = dalloc<uint32_t>(pairs, c->owned);
+    W.val_b = dalloc<uint32_t>(pairs, c->owned);
+    W.slot_a = dalloc<uint32_t>(pairs, c->owned);
+    W.slot_b = dalloc<uint32_t>(pairs, c->owned);
+    W.n = dalloc<uint32_t>(1, c->owned);
+    W.host_n = c->host_small + 40;
+    W.temp_bytes = skv::rep_sort_temp_bytes(pairs);
+    W.temp = dalloc<uint8_t>(W.temp_bytes, c->owned);
+    R.pair_cnt = dalloc<uint32_t>(pairs, c->owned);
+    R.pair_mask = pairs - 1;
+    R.new_cap = static_cast<uint32_t>(std::min<uint64_t>(c->max_blocks, 1ull << 26));
+    R.new_list = dalloc<uint32_t>(R.new_cap, c->owned);
+    R.new_n = dalloc<uint32_t>(1, c->owned);
+    R.err = dalloc<uint32_t>(1, c->owned);
+    c->rep_ents = dalloc<skv_rep_entry>(R.new_cap, c->owned);
+    c->rep_accs = dalloc<skv_rep_access>(pairs, c->owned);
+    c->rep_gids = dalloc<uint64_t>(c->max_prompts, c->owned);
+    CK(cudaMemsetAsync(R.new_n, 0, 4, c->stream));
+    CK(cudaMemsetAsync(R.err, 0, 4, c->stream));
+    R.depth = depth;
+    skv::launch_rep_clear(c->ix, c->stream);
+    sync_check(c->stream);
+    return SKV_OK;
+  });
+}
+
+int skv_replica_export(skv_ctx* c, const uint64_t* gids, skv_rep_entry* ents, size_t ecap, size_t* n_ents,
+                       skv_rep_access* accs, size_t acap, size_t* n_accs, int accs_on_device) {
+  if (!c || !n_ents || !n_accs) return SKV_ERR_ARG;
+  *n_ents = *n_accs = 0;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (!c->ix.rep.depth) throw StateError("no replicated layer (skv_set_replicated_depth)");
+    if (!c->rep_sync_due) throw StateError("skv_replica_export: no committed batch to export");
+    if (c->p_n && !gids) throw ArgError("prompt_gids required");
+    cudaStream_t s = c->stream;
+    if (c->p_n) CK(cudaMemcpyAsync(c->rep_gids, gids, c->p_n * 8ull, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->host_small + 32, c->ix.rep.new_n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 33, c->ix.rep.err, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    if (c->host_small[33]) throw CapacityError("replicated layer: pair table or new-entry list full");
+    const uint32_t nn = std::min(c->host_small[32], c->ix.rep.new_cap);
+    CK(cudaMemsetAsync(c->counters + 13, 0, 4, s));
+    skv::launch_rep_export(c->ix, c->users_tab.rev, c->rep_gids, nn, c->rep_ents, c->rep_accs, c->counters + 13,
+                           c->ix.rep.pair_mask + 1, s);
+    CK(cudaMemcpyAsync(c->host_small + 34, c->counters + 13, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    const uint32_t na = c->host_small[34];
+    *n_ents = nn;
+    *n_accs = na;
+    if (nn > ecap || na > acap || (nn && !ents) || (na && !accs))
+      throw CapacityError("skv_replica_export: buffers too small (sizes returned)");
+    if (nn) CK(cudaMemcpyAsync(ents, c->rep_ents, nn * sizeof(skv_rep_entry), cudaMemcpyDeviceToHost, s));
+    if (na)
+      CK(cudaMemcpyAsync(accs, c->rep_accs, na * sizeof(skv_rep_access),
+                         accs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    return SKV_OK;
+  });
+}
+
+int skv_replica_apply(skv_ctx* c, const skv_rep_entry* ents, size_t n_ents, const skv_rep_access* accs,
+                      size_t n_accs, int accs_on_device) {
+  if (!c || (n_ents && !ents) || (n_accs && !accs)) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (!c->ix.rep.depth) throw StateError("no replicated layer (skv_set_replicated_depth)");
+    if (!c->rep_sync_due) throw StateError("skv_replica_apply: no committed batch to apply to");
+    cudaStream_t s = c->stream;
+    const size_t off_a = (n_ents * sizeof(skv_rep_entry) + 15) & ~size_t(15);
+    const size_t off_c = (off_a + n_accs * sizeof(skv_rep_access) + 15) & ~size_t(15);
+    const size_t need = off_c + n_ents * 8 + 64;
+    if (need > c->rep_in_bytes) {
+      if (c->rep_in) CK(cudaFree(c->rep_in));
+      c->rep_in_bytes = need * 2;
+      CK(cudaMalloc(&c->rep_in, c->rep_in_bytes));
+    }
+    if (n_ents > c->rep_in_ents) {
+      if (c->rep_slots) CK(cudaFree(c->rep_slots));
+      if (c->rep_uidx) CK(cudaFree(c->rep_uidx));
+      c->rep_in_ents = n_ents * 2;
+      CK(cudaMalloc(&c->rep_slots, c->rep_in_ents * 4));
+      CK(cudaMalloc(&c->rep_uidx, c->rep_in_ents * 4));
+    }
+    auto* dents = static_cast<skv_rep_entry*>(c->rep_in);
+    auto* daccs = reinterpret_cast<skv_rep_access*>(static_cast<uint8_t*>(c->rep_in) + off_a);
+    auto* dcr = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(c->rep_in) + off_c);
+    if (n_ents) CK(cudaMemcpyAsync(dents, ents, n_ents * sizeof(skv_rep_entry), cudaMemcpyHostToDevice, s));
+    if (n_accs && !accs_on_device)
+      CK(cudaMemcpyAsync(daccs, accs, n_accs * sizeof(skv_rep_access), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(c->counters + 14, 0, 4, s));  // entries claimed here
+    CK(cudaMemsetAsync(c->ix.rep.err, 0, 4, s));
+    if (n_ents) {  // creators: interned like an admitted prompt's user
+      static_assert(offsetof(skv_rep_entry, creator) % 8 == 0, "");
+      std::vector<uint64_t> cr(n_ents);
+      for (size_t i = 0; i < n_ents; ++i) cr[i] = ents[i].creator;
+      CK(cudaMemcpyAsync(dcr, cr.data(), n_ents * 8, cudaMemcpyHostToDevice, s));
+      skv::launch_intern_users(c->users_tab, dcr, static_cast<uint32_t>(n_ents), c->rep_uidx, c->counters + 5, s);
+    }
+    skv::MonCtx m;
+    m.hdr = c->set_hdr;
+    m.tab = c->set_tab;
+    m.pool_cap = c->pool_cap;
+    m.pool_count = c->counters + 0;
+    m.touched = c->touched[c->cur];
+    m.n_touched = c->counters + 1 + c->cur;
+    m.batch = c->rec_batch;  // the batch whose accesses these are
+    m.wstart = c->wstart;
+    m.err = c->counters + 5;
+    m.matched_total = c->counters + 10;
+    if (n_accs > c->ix.rep.pair_mask + 1ull) throw CapacityError("skv_replica_apply: more accesses than the pair table");
+    skv::launch_rep_clear(c->ix, s);  // the local aggregation was exported: the table merges now
+    skv::launch_rep_apply(c->ix, m, dents, c->rep_uidx, static_cast<uint32_t>(n_ents), c->rep_slots, c->counters + 14,
+                          accs_on_device ? static_cast<const void*>(accs) : daccs, static_cast<uint32_t>(n_accs),
+                          c->rep_w, c->ix.rep.err, s);
+    skv::launch_rep_clear(c->ix, s);
+    CK(cudaMemsetAsync(c->ix.rep.new_n, 0, 4, s));
+    CK(cudaMemcpyAsync(c->host_small + 35, c->counters + 14, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 36, c->ix.rep.err, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 37, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    c->entries += c->host_small[35];
+    c->rep_sync_due = false;
+    if (c->host_small[36] || (c->host_small[37] & 9u)) {
+      c->poisoned = "replicated-layer apply failed (an entry, a parent or an accessed key is missing, or a pool is full)";
+      throw CapacityError(c->poisoned);
+    }
     return SKV_OK;
   });
 }

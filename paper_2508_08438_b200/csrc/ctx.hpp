@@ -166,9 +166,28 @@ struct HSLayout {
   uint32_t stage, off_list, buf_gap, n_gap, buf_tail, warps, total;
 };
 
+// Replicated layer (multi-GPU, skv_set_replicated_depth): entries at depth < depth exist on every
+// rank.  Their accesses are not recorded locally but aggregated per (entry, user) -- first prompt of
+// the batch, access count -- into an open-addressed pair table (key {user, slot + 1}, empty = 0), and
+// the commit lists the replicated-layer entries it creates; both are exported, merged over the ranks
+// and applied identically everywhere (skv_replica_export / skv_replica_apply).
+struct RepLayer {
+  uint32_t depth = 0;           // 0: nothing replicated
+  ulonglong2* pair_key = nullptr;
+  uint32_t* pair_first = nullptr;  // lowest local prompt index (init ~0)
+  unsigned long long* pair_gid = nullptr;  // apply: lowest global prompt id (init ~0)
+  uint32_t* pair_cnt = nullptr;
+  uint32_t pair_mask = 0;
+  uint32_t* new_list = nullptr;  // slots the commit created at depth < depth
+  uint32_t* new_n = nullptr;
+  uint32_t new_cap = 0;
+  uint32_t* err = nullptr;       // bit 0: pair table full, bit 1: new list full
+};
+
 struct Index {
   Entry* e = nullptr;
   uint64_t cap = 0, mask = 0;
+  RepLayer rep;
   EvictMeta* em = nullptr;  // null unless eviction is enabled
   // per commit (eviction enabled): speculative node-id bases (exclusive prefix over prompts of
   // the blocks each would create), the next node id and the insert epoch
@@ -297,5 +316,21 @@ void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);
+// replicated layer (multi-GPU): export / clear / apply (kernels.cu)
+void launch_rep_export(const Index& ix, const uint64_t* user_rev, const uint64_t* gids, uint32_t n_new, void* ents,
+                       void* accs, uint32_t* n_accs, uint32_t acc_cap, cudaStream_t s);
+void launch_rep_clear(const Index& ix, cudaStream_t s);
+// device merge scratch of skv_replica_apply (pair capacity each)
+struct RepScratch {
+  unsigned long long *gid_a = nullptr, *gid_b = nullptr;
+  uint32_t *val_a = nullptr, *val_b = nullptr, *slot_a = nullptr, *slot_b = nullptr, *n = nullptr;
+  uint32_t* host_n = nullptr;  // pinned
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+};
+size_t rep_sort_temp_bytes(uint32_t n);
+void launch_rep_apply(const Index& ix, const MonCtx& M, const void* ents, const uint32_t* uidx, uint32_t n_ents,
+                      uint32_t* slots, uint32_t* n_claimed, const void* accs, uint32_t n_accs, const RepScratch& W,
+                      uint32_t* err, cudaStream_t s);
 
 }  // namespace skv

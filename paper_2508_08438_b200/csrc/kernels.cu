@@ -953,9 +953,34 @@ __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* 
 #endif
 constexpr int kRecRounds = SKV_KRECROUNDS;
 
+// replicated layer: an access to an entry at depth < rep.depth is aggregated per (entry, user)
+// -- lowest prompt of the batch and count -- for the cross-rank merge instead of being recorded
+__device__ void rep_pair_add(const RepLayer& R, uint32_t slot, uint64_t user, uint32_t p) {
+  const ulonglong2 key = make_ulonglong2(user, static_cast<unsigned long long>(slot) + 1);
+  uint32_t h = (mix32(user ^ (static_cast<uint64_t>(slot) << 32)) ^ slot * 0x9e3779b9u) & R.pair_mask;
+  for (uint32_t i = 0; i <= R.pair_mask; ++i, h = (h + 1) & R.pair_mask) {
+    ulonglong2 cur = ld_relaxed128(&R.pair_key[h]);
+    if (cur.x == 0 && cur.y == 0) {
+      ulonglong2 old;
+      cas128_dev(&R.pair_key[h], make_ulonglong2(0, 0), key, &old);
+      cur = old.x == 0 && old.y == 0 ? key : old;
+    }
+    if (cur.x == key.x && cur.y == key.y) {
+      atomicMin(&R.pair_first[h], p);
+      atomicAdd(&R.pair_cnt[h], 1u);
+      return;
+    }
+  }
+  atomicOr(R.err, 1u);
+}
+
 __device__ __forceinline__ void record_prompt(const Index& ix, const MonCtx& M, const uint32_t* __restrict__ slot_in,
-                                              uint32_t bo, uint32_t m, uint64_t u, uint32_t lane) {
+                                              uint32_t bo, uint32_t m, uint64_t u, uint32_t lane, uint32_t p) {
   const uint32_t pos = mix32(u) & (kSetSlots - 1);
+  const uint32_t rd = min(ix.rep.depth, m);
+  for (uint32_t b = lane; b < rd; b += 32) rep_pair_add(ix.rep, slot_in[bo + b], u, p);
+  bo += rd;
+  m -= rd;
   for (uint32_t base = 0; base < m; base += 32 * kRecRounds) {
     uint32_t sl[kRecRounds], si[kRecRounds];
 #pragma unroll
@@ -988,7 +1013,7 @@ __global__ void __launch_bounds__(256) k_record(Index ix, MonCtx M, const uint32
                                                 const uint64_t* __restrict__ users, uint32_t n_prompts) {
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
-  record_prompt(ix, M, slot_in, blk_off[p], matched[p], users[p], lane_id());
+  record_prompt(ix, M, slot_in, blk_off[p], matched[p], users[p], lane_id(), p);
 }
 
 // accesses (slot << 32 | prompt) of the entries that need an ordered replay
@@ -998,7 +1023,7 @@ __global__ void k_replay_emit(Index ix, MonCtx M, const uint32_t* __restrict__ s
   const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_prompts) return;
   const uint32_t bo = blk_off[p], m = matched[p];
-  for (uint32_t b = lane_id(); b < m; b += 32) {
+  for (uint32_t b = ix.rep.depth + lane_id(); b < m; b += 32) {  // replicated entries: merged, not recorded
     const uint32_t s = slot_in[bo + b];
     if (M.hdr[ix.e[s].aux.set_idx].ovf == M.batch)
       keys[atomicAdd(n_keys, 1u)] = (static_cast<unsigned long long>(s) << 32) | p;
@@ -1444,7 +1469,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
   const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo, k0 = exist[p];
   if (k0 >= n) {
     if constexpr (kRec)
-      if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+      if (with_record) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane, p);
     continue;
   }
   const uint32_t creator = uidx[p];
@@ -1519,7 +1544,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
     // precede block k0) run while the first claims are in flight: L2 atomics overlap the
     // claims' DRAM round trips (record and commit touch disjoint fields)
     if constexpr (kRec)
-      if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane);
+      if (with_record && base == k0) record_prompt(ix, M, slot_out, bo, matched[p], users[p], lane, p);
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (base + 32 * r + lane < n) pend[r] = !mine[r] && !(ol[r] == h[r] && oh[r] == d[r]);
@@ -1554,6 +1579,13 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
       if (base + 32 * r + lane >= n || sl[r] == ~0ull) continue;
       s32[r] = static_cast<uint32_t>(sl[r]);
       slot_out[bo + base + 32 * r + lane] = s32[r];
+      if (mine[r] && base + 32 * r + lane < ix.rep.depth) {  // a replicated-layer entry this batch created
+        const uint32_t k = atomicAdd(ix.rep.new_n, 1u);
+        if (k < ix.rep.new_cap)
+          ix.rep.new_list[k] = s32[r];
+        else
+          atomicOr(ix.rep.err, 2u);
+      }
     }
     // payloads and parent links (parent = previous block's slot); sector 0 only
     uint32_t par[R];
@@ -2695,5 +2727,269 @@ void launch_intern_users(const UserTable& t, const uint64_t* users, uint32_t n, 
 
 void launch_init_entries(const Index& ix, cudaStream_t s) {
   k_init_entries<<<static_cast<uint32_t>((ix.cap + 255) / 256), 256, 0, s>>>(ix);
+}
+
+// ---------------------------------------------------------------------------------
+// Replicated layer (multi-GPU): export of a rank's new replicated-layer
+// entries and aggregated accesses, application of the merge of all ranks' exports.
+// ---------------------------------------------------------------------------------
+namespace {
+static_assert(sizeof(skv_rep_entry) == 56 && sizeof(skv_rep_access) == 40, "replica record layouts");
+
+__global__ void k_rep_export_new(Index ix, const uint64_t* __restrict__ user_rev, const uint64_t* __restrict__ gids,
+                                 skv_rep_entry* out, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Rec r = ix.e[ix.rep.new_list[i]].rec;
+  skv_rep_entry o;
+  o.h = r.h;
+  o.d = r.d;
+  o.ph = o.pd = 0;
+  if (r.parent != kNone) {
+    o.ph = ix.e[r.parent].rec.h;
+    o.pd = ix.e[r.parent].rec.d;
+  }
+  o.creator = user_rev[r.creator];
+  o.gid = gids[meta_prompt(r.meta)];
+  o.label = static_cast<uint8_t>(meta_label(r.meta));
+  o.owner = static_cast<uint8_t>(meta_owner(r.meta));
+  for (int k = 0; k < 6; ++k) o.pad[k] = 0;
+  out[i] = o;
+}
+
+__global__ void k_rep_export_acc(Index ix, const uint64_t* __restrict__ gids, skv_rep_access* out, uint32_t* n_out,
+                                 uint32_t cap) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h > ix.rep.pair_mask) return;
+  const ulonglong2 key = ix.rep.pair_key[h];
+  if (key.y == 0) return;
+  const uint32_t slot = static_cast<uint32_t>(key.y - 1);
+  const uint32_t k = atomicAdd(n_out, 1u);
+  if (k >= cap) return;
+  skv_rep_access o;
+  o.h = ix.e[slot].rec.h;
+  o.d = ix.e[slot].rec.d;
+  o.user = key.x;
+  o.gid = gids[ix.rep.pair_first[h]];
+  o.count = ix.rep.pair_cnt[h];
+  out[k] = o;
+}
+
+__global__ void k_rep_clear(RepLayer R) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h > R.pair_mask) return;
+  R.pair_key[h] = make_ulonglong2(0ull, 0ull);
+  R.pair_first[h] = 0xffffffffu;
+  R.pair_gid[h] = ~0ull;
+  R.pair_cnt[h] = 0;
+}
+
+// slot of an existing key (the replicated layer is identical on every rank), kNone if absent
+__device__ uint32_t rep_find(const Index& ix, uint64_t h, uint64_t d) {
+  uint64_t s = home_slot(ix, h, d, 0);
+  for (uint64_t i = 0; i <= ix.mask; ++i, s = (s + 1) & ix.mask) {
+    const ulonglong2 k = *reinterpret_cast<const ulonglong2*>(&ix.e[s].rec);
+    if (k.x == h && k.y == d) return static_cast<uint32_t>(s);
+    if (k.x == 0 && k.y == 0) return kNone;
+  }
+  return kNone;
+}
+
+// merged entries (one per key, the global first creator's payload): claim absent keys, write the
+// winner's creator / label / owner into every copy
+__global__ void k_rep_apply_claim(Index ix, const skv_rep_entry* __restrict__ ents, const uint32_t* __restrict__ uidx,
+                                  uint32_t n, uint32_t* slot_out, uint32_t* n_claimed, uint32_t* err) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const skv_rep_entry r = ents[i];
+  uint64_t s = home_slot(ix, r.h, r.d, 0);
+  bool claimed = false, ok = false;
+  for (uint64_t k = 0; k <= ix.mask; ++k, s = (s + 1) & ix.mask) {
+    unsigned long long ol, oh;
+    if (cas128(reinterpret_cast<unsigned long long*>(&ix.e[s].rec), 0ull, 0ull, r.h, r.d, &ol, &oh)) {
+      claimed = ok = true;
+      break;
+    }
+    if (ol == r.h && oh == r.d) {
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) {
+    atomicOr(err, 2u);
+    slot_out[i] = kNone;
+    return;
+  }
+  Rec& e = ix.e[s].rec;
+  const uint32_t old = claimed ? 0u : e.meta;
+  *reinterpret_cast<uint2*>(&e.creator) =
+      make_uint2(uidx[i], make_meta(r.label, r.owner, claimed ? SKV_TIER_HBM : meta_tier(old), meta_prompt(old)));
+  slot_out[i] = claimed ? (static_cast<uint32_t>(s) | 0x80000000u) : static_cast<uint32_t>(s);
+  if (claimed) atomicAdd(n_claimed, 1u);
+}
+
+// parent links of the entries the claim pass created (their parents exist now)
+__global__ void k_rep_apply_link(Index ix, const skv_rep_entry* __restrict__ ents, const uint32_t* __restrict__ slots,
+                                 uint32_t n, uint32_t* err) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || slots[i] == kNone || !(slots[i] & 0x80000000u)) return;
+  const uint32_t s = slots[i] & 0x7fffffffu;
+  const skv_rep_entry r = ents[i];
+  if (r.ph == 0 && r.pd == 0) return;  // a root
+  const uint32_t ps = rep_find(ix, r.ph, r.pd);
+  if (ps == kNone) {
+    atomicOr(err, 4u);
+    return;
+  }
+  ix.e[s].rec.parent = ps;
+  const uint32_t sib = atomicExch(&ix.e[ps].rec.first_child, s);
+  if (sib != kNone) ix.e[s].aux.next_sibling = sib;
+}
+
+// Device merge of the ranks' raw access exports (all ranks' records, any order): per (entry, user)
+// the lowest first prompt id and the summed count (pair table keyed {user, slot + 1}) ...
+__global__ void k_rep_merge_insert(Index ix, const skv_rep_access* __restrict__ accs, uint32_t n, uint32_t* err) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const skv_rep_access a = accs[i];
+  const uint32_t slot = rep_find(ix, a.h, a.d);
+  if (slot == kNone) {
+    atomicOr(err, 8u);
+    return;
+  }
+  const RepLayer& R = ix.rep;
+  const ulonglong2 key = make_ulonglong2(a.user, static_cast<unsigned long long>(slot) + 1);
+  uint32_t h = (mix32(a.user ^ (static_cast<uint64_t>(slot) << 32)) ^ slot * 0x9e3779b9u) & R.pair_mask;
+  for (uint32_t t = 0; t <= R.pair_mask; ++t, h = (h + 1) & R.pair_mask) {
+    ulonglong2 cur = ld_relaxed128(&R.pair_key[h]);
+    if (cur.x == 0 && cur.y == 0) {
+      ulonglong2 old;
+      cas128_dev(&R.pair_key[h], make_ulonglong2(0, 0), key, &old);
+      cur = old.x == 0 && old.y == 0 ? key : old;
+    }
+    if (cur.x == key.x && cur.y == key.y) {
+      atomicMin(&R.pair_gid[h], static_cast<unsigned long long>(a.gid));
+      atomicAdd(&R.pair_cnt[h], static_cast<uint32_t>(a.count));
+      return;
+    }
+  }
+  atomicOr(err, 1u);
+}
+
+// ... compacted as (first gid -> pair) for a sort by gid, then a stable sort by entry slot ...
+__global__ void k_rep_merge_compact(RepLayer R, unsigned long long* gid_keys, uint32_t* vals, uint32_t* n_out) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h > R.pair_mask || R.pair_key[h].y == 0) return;
+  const uint32_t k = atomicAdd(n_out, 1u);
+  gid_keys[k] = R.pair_gid[h];
+  vals[k] = h;
+}
+
+__global__ void k_rep_merge_slotkeys(RepLayer R, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ n,
+                                     uint32_t* slot_keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n) return;
+  slot_keys[i] = static_cast<uint32_t>(R.pair_key[vals[i]].y - 1);
+}
+
+// ... and each entry's merged accesses replayed, one thread per entry, in global order against its
+// window set (AccessStats::record, access_stats.hpp:27-37, with a user's repeats folded into its
+// count: once admitted a user's later accesses add 0; a user not admitted on its first access
+// never is, so each of its accesses adds 1)
+__global__ void k_rep_apply_acc(Index ix, MonCtx M, const uint32_t* __restrict__ slot_keys,
+                                const uint32_t* __restrict__ vals, const uint32_t* __restrict__ n_ptr) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t n = *n_ptr;
+  if (i >= n || (i > 0 && slot_keys[i - 1] == slot_keys[i])) return;  // not the entry's first
+  const RepLayer& R = ix.rep;
+  const uint32_t s = slot_keys[i];
+  Entry& e = ix.e[s];
+  const uint32_t si = acquire_set(e, s, M);
+  if (si == kNone) return;  // pool exhausted (M.err)
+  SetHdr& hd = M.hdr[si];
+  ulonglong2* tab = M.tab + static_cast<uint64_t>(si) * kSetSlots;
+  uint32_t size = hd.size, hits = 0, ucnt = 0;
+  for (uint32_t j = i; j < n && slot_keys[j] == s; ++j) {
+    const uint32_t v = vals[j];
+    const uint64_t u = R.pair_key[v].x;
+    const uint32_t c = R.pair_cnt[v];
+    hits += c;
+    uint32_t pos = mix32(u) & (kSetSlots - 1), free_pos = kNone;
+    bool member = false;
+    for (uint32_t t = 0; t < kSetSlots; ++t, pos = (pos + 1) & (kSetSlots - 1)) {
+      const ulonglong2 x = tab[pos];
+      if (x.y < M.wstart) {
+        free_pos = pos;
+        break;
+      }
+      if (x.x == u) {
+        member = true;
+        break;
+      }
+    }
+    if (member) continue;
+    if (size < kMaxSetUsers && free_pos != kNone) {
+      tab[free_pos] = make_ulonglong2(u, M.batch);
+      ++size;
+      ucnt += 1;
+    } else {
+      ucnt += c;  // saturated: every access of an untracked user counts as new (access_stats.hpp:33)
+    }
+  }
+  e.stats.hit_cur += hits;
+  e.stats.u_cnt += ucnt;
+  hd.size = size;
+}
+}  // namespace
+
+void launch_rep_export(const Index& ix, const uint64_t* user_rev, const uint64_t* gids, uint32_t n_new,
+                       void* ents, void* accs, uint32_t* n_accs, uint32_t acc_cap, cudaStream_t s) {
+  if (n_new) k_rep_export_new<<<cdiv(n_new, 256), 256, 0, s>>>(ix, user_rev, gids, static_cast<skv_rep_entry*>(ents),
+                                                               n_new);
+  k_rep_export_acc<<<cdiv(ix.rep.pair_mask + 1ull, 256), 256, 0, s>>>(ix, gids, static_cast<skv_rep_access*>(accs),
+                                                                       n_accs, acc_cap);
+}
+
+void launch_rep_clear(const Index& ix, cudaStream_t s) {
+  k_rep_clear<<<cdiv(ix.rep.pair_mask + 1ull, 256), 256, 0, s>>>(ix.rep);
+}
+
+size_t rep_sort_temp_bytes(uint32_t n) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const unsigned long long*>(nullptr),
+                                  static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), n);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), n);
+  return std::max(a, b);
+}
+
+void launch_rep_apply(const Index& ix, const MonCtx& M, const void* ents, const uint32_t* uidx, uint32_t n_ents,
+                      uint32_t* slots, uint32_t* n_claimed, const void* accs, uint32_t n_accs, const RepScratch& W,
+                      uint32_t* err, cudaStream_t s) {
+  const auto* E = static_cast<const skv_rep_entry*>(ents);
+  if (n_ents) {
+    k_rep_apply_claim<<<cdiv(n_ents, 256), 256, 0, s>>>(ix, E, uidx, n_ents, slots, n_claimed, err);
+    k_rep_apply_link<<<cdiv(n_ents, 256), 256, 0, s>>>(ix, E, slots, n_ents, err);
+  }
+  if (!n_accs) return;
+  const uint32_t cap = ix.rep.pair_mask + 1;
+  k_rep_merge_insert<<<cdiv(n_accs, 256), 256, 0, s>>>(ix, static_cast<const skv_rep_access*>(accs), n_accs, err);
+  cudaMemsetAsync(W.n, 0, 4, s);
+  k_rep_merge_compact<<<cdiv(cap, 256), 256, 0, s>>>(ix.rep, W.gid_a, W.val_a, W.n);
+  // the pair count bounds the sorts: read it (one small copy) so they sort only the used pairs
+  uint32_t np = 0;
+  cudaMemcpyAsync(W.host_n, W.n, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  np = *W.host_n;
+  if (!np) return;
+  size_t tb = W.temp_bytes;
+  cub::DeviceRadixSort::SortPairs(W.temp, tb, W.gid_a, W.gid_b, W.val_a, W.val_b, np, 0, 64, s);
+  k_rep_merge_slotkeys<<<cdiv(np, 256), 256, 0, s>>>(ix.rep, W.val_b, W.n, W.slot_a);
+  int bits = 1;
+  while ((1ull << bits) <= ix.mask) ++bits;
+  tb = W.temp_bytes;
+  cub::DeviceRadixSort::SortPairs(W.temp, tb, W.slot_a, W.slot_b, W.val_b, W.val_a, np, 0, bits, s);
+  k_rep_apply_acc<<<cdiv(np, 256), 256, 0, s>>>(ix, M, W.slot_b, W.val_a, W.n);
 }
 }  // namespace skv

@@ -359,6 +359,51 @@ class AdmissionEngine:
         self._check(rc)
         return self._evicted
 
+    # --------------------------------------------------------------- replicated layer (multi-GPU)
+    def set_replicated_depth(self, depth: int) -> None:
+        """Entries at depth < ``depth`` are replicated on every rank (before the first admit);
+        see ReplicaGroup."""
+        self._check(self._lib.skv_set_replicated_depth(self._h, depth))
+
+    def replica_export(self, prompt_gids: np.ndarray, device: bool = False):
+        """After ``commit``: (new replicated-layer entries as a REP_ENTRY array, the batch's
+        replicated-layer accesses aggregated per (entry, user) as a REP_ACCESS array -- or, with
+        ``device``, as a uint8 torch tensor in device memory); ``prompt_gids`` = global ids of the
+        batch's prompts."""
+        gids = np.ascontiguousarray(prompt_gids, np.uint64)
+        ne, na = C.c_size_t(), C.c_size_t()
+        ecap, acap = 1 << 12, 1 << 14
+        while True:
+            ents = np.zeros(ecap, REP_ENTRY)
+            if device:
+                import torch
+                accs = torch.empty(acap * REP_ACCESS.itemsize, dtype=torch.uint8,
+                                   device=torch.device("cuda", self.cfg.device))
+                aptr = accs.data_ptr()
+            else:
+                accs = np.zeros(acap, REP_ACCESS)
+                aptr = _ptr(accs)
+            rc = self._lib.skv_replica_export(self._h, _ptr(gids), _ptr(ents), ecap, C.byref(ne), aptr, acap,
+                                              C.byref(na), 1 if device else 0)
+            if rc == N.SKV_ERR_CAPACITY and (ne.value > ecap or na.value > acap):
+                ecap, acap = max(ecap, ne.value), max(acap, na.value)
+                continue
+            self._check(rc)
+            return ents[:ne.value], accs[:na.value * (REP_ACCESS.itemsize if device else 1)]
+
+    def replica_apply(self, ents: np.ndarray, accs) -> None:
+        """Apply every rank's export: ``ents`` merged (``merge_replica``), ``accs`` the ranks'
+        access exports concatenated (a REP_ACCESS array, or a uint8 torch tensor in device
+        memory); the accesses are merged on the device."""
+        ents = np.ascontiguousarray(ents, REP_ENTRY)
+        if isinstance(accs, np.ndarray):
+            accs = np.ascontiguousarray(accs, REP_ACCESS)
+            rc = self._lib.skv_replica_apply(self._h, _ptr(ents), len(ents), _ptr(accs), len(accs), 0)
+        else:  # a device tensor of raw REP_ACCESS records
+            n = accs.numel() // REP_ACCESS.itemsize
+            rc = self._lib.skv_replica_apply(self._h, _ptr(ents), len(ents), accs.data_ptr() if n else None, n, 1)
+        self._check(rc)
+
     def entry_count(self) -> int:
         return int(self._lib.skv_entry_count(self._h))
 
@@ -382,6 +427,129 @@ class AdmissionEngine:
         d = C.c_uint64()
         self._check(self._lib.skv_token_seq_digest(self._h, _ptr(t), len(t), C.byref(d)))
         return int(d.value)
+
+
+# skv_rep_entry / skv_rep_access (include/safekv_b200.h)
+REP_ENTRY = np.dtype([("h", "<u8"), ("d", "<u8"), ("ph", "<u8"), ("pd", "<u8"), ("creator", "<u8"), ("gid", "<u8"),
+                      ("label", "u1"), ("owner", "u1"), ("pad", "u1", (6,))])
+REP_ACCESS = np.dtype([("h", "<u8"), ("d", "<u8"), ("user", "<u8"), ("gid", "<u8"), ("count", "<u8")])
+assert REP_ENTRY.itemsize == 56 and REP_ACCESS.itemsize == 40
+
+
+def merge_replica(ents_list, accs_list):
+    """The merge every rank applies (host, identical everywhere): of all ranks' new
+    replicated-layer entries, the one per key with the lowest global prompt id (first creator
+    wins, cache_index.hpp:164-168); of all accesses, per (key, user) the lowest first prompt id
+    and the summed count, sorted by key then first prompt id (the global access order the
+    entry's AccessStats replays)."""
+    E = np.concatenate([np.asarray(e, REP_ENTRY) for e in ents_list]) if ents_list else np.zeros(0, REP_ENTRY)
+    if len(E):
+        E = E[np.lexsort((E["gid"], E["d"], E["h"]))]
+        keep = np.ones(len(E), bool)
+        keep[1:] = (E["h"][1:] != E["h"][:-1]) | (E["d"][1:] != E["d"][:-1])
+        E = E[keep]
+    A = np.concatenate([np.asarray(a, REP_ACCESS) for a in accs_list]) if accs_list else np.zeros(0, REP_ACCESS)
+    if len(A):
+        A = A[np.lexsort((A["gid"], A["user"], A["d"], A["h"]))]
+        head = np.ones(len(A), bool)
+        head[1:] = (A["h"][1:] != A["h"][:-1]) | (A["d"][1:] != A["d"][:-1]) | (A["user"][1:] != A["user"][:-1])
+        starts = np.flatnonzero(head)
+        counts = np.add.reduceat(A["count"], starts)
+        A = A[starts].copy()  # the first row of a (key, user) group carries its lowest gid
+        A["count"] = counts
+        A = A[np.lexsort((A["gid"], A["d"], A["h"]))]
+    return E, A
+
+
+def merge_entries(ents_list):
+    """The first-creator merge of all ranks' new replicated-layer entries: one per key, the
+    lowest global prompt id (cache_index.hpp:164-168)."""
+    return merge_replica(ents_list, [])[0]
+
+
+def torch_allgather(group=None):
+    """An allgather of numpy records over torch.distributed (NCCL: device tensors over NVLink;
+    gloo: host tensors): returns every rank's array, in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+    def ag(arr: np.ndarray):
+        raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+        n = torch.tensor([raw.size], dtype=torch.int64, device=dev)
+        sizes = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n, group=group)
+        sizes = [int(x.item()) for x in sizes]
+        mx = max(max(sizes), 1)
+        buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
+        if raw.size:
+            buf[:raw.size] = torch.from_numpy(raw.copy()).to(dev)
+        outs = [torch.empty(mx, dtype=torch.uint8, device=dev) for _ in range(world)]
+        dist.all_gather(outs, buf, group=group)
+        return [o[:sz].cpu().numpy().view(arr.dtype) for o, sz in zip(outs, sizes)]
+    return ag
+
+
+def torch_allgather_device(group=None):
+    """NCCL allgather of a uint8 device tensor of records: every rank's records concatenated, in
+    rank order, staying in device memory (NVLink; no host round trip of the data)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+
+    def ag(t):
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        sizes = torch.empty(world, dtype=torch.int64, device=t.device)
+        dist.all_gather_into_tensor(sizes, n, group=group)
+        sizes = sizes.tolist()
+        mx = max(max(sizes), 1)
+        buf = torch.zeros(mx, dtype=torch.uint8, device=t.device)
+        buf[:t.numel()] = t
+        out = torch.empty(world * mx, dtype=torch.uint8, device=t.device)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        return torch.cat([out[i * mx:i * mx + sz] for i, sz in enumerate(sizes)])
+    return ag
+
+
+class ReplicaGroup:
+    """Cross-rank merge of the replicated layer (north star: "each GPU holds a replica of the
+    index, and new-entry inserts and entropy counters are merged across GPUs with NCCL").
+    Per batch: ``engine.commit()`` then ``sync(prompt_gids)``; every rank applies the same merge,
+    so replicated entries and their window statistics are identical on all ranks and equal one
+    engine's over the whole batch.  With ``allgather_device`` (NCCL) the access records stay
+    in device memory from the export through the all-gather to the device-side merge."""
+
+    def __init__(self, engine: "AdmissionEngine", depth: int, allgather, allgather_device=None):
+        self.engine, self.depth = engine, depth
+        self.allgather, self.allgather_device = allgather, allgather_device
+        engine.set_replicated_depth(depth)
+
+    def sync(self, prompt_gids: np.ndarray):
+        if self.allgather_device is not None:
+            e, a = self.engine.replica_export(prompt_gids, device=True)
+            E = merge_entries(self.allgather(e))
+            A = self.allgather_device(a)
+            self.engine.replica_apply(E, A)
+            return len(E), A.numel() // REP_ACCESS.itemsize
+        e, a = self.engine.replica_export(prompt_gids)
+        E = merge_entries(self.allgather(e))
+        A = self.allgather(a)
+        A = np.concatenate(A) if A else np.zeros(0, REP_ACCESS)
+        self.engine.replica_apply(E, A)
+        return len(E), len(A)
+
+
+def merge_events(events_per_rank):
+    """Union of the ranks' epoch events (a replicated entry fires identically on every rank),
+    sorted by key."""
+    seen, out = set(), []
+    for evs in events_per_rank:
+        for e in evs:
+            if (e.h, e.d) not in seen:
+                seen.add((e.h, e.d))
+                out.append(e)
+    return sorted(out, key=lambda e: (e.h, e.d))
 
 
 def route(tokens: np.ndarray, offsets: np.ndarray, world: int, block_tokens: int,

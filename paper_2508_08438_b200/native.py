@@ -123,6 +123,16 @@ class CostModel(C.Structure):
                 ("noise_sigma_ms", C.c_double), ("seed", C.c_uint64)]
 
 
+class RepEntry(C.Structure):
+    _fields_ = [("h", C.c_uint64), ("d", C.c_uint64), ("ph", C.c_uint64), ("pd", C.c_uint64), ("creator", C.c_uint64),
+                ("gid", C.c_uint64), ("label", C.c_uint8), ("owner", C.c_uint8), ("pad", C.c_uint8 * 6)]
+
+
+class RepAccess(C.Structure):
+    _fields_ = [("h", C.c_uint64), ("d", C.c_uint64), ("user", C.c_uint64), ("gid", C.c_uint64),
+                ("count", C.c_uint64)]
+
+
 # name -> (restype, argtypes); this table is also the export list checked by the CPU tests
 SIGNATURES = {
     "skv_rules_default": (C.c_int, [C.POINTER(C.c_void_p)]),
@@ -164,6 +174,10 @@ SIGNATURES = {
     "skv_admit_ttft": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
+    "skv_set_replicated_depth": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "skv_replica_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t),
+                                     C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.c_int]),
+    "skv_replica_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int]),
     "skv_route": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_route_depth": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                   C.c_uint32, C.c_void_p]),

@@ -36,7 +36,8 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     pairs = {"skv_event": N.Event, "skv_entry": N.Entry, "skv_config": N.Config, "skv_batch": N.Batch,
              "skv_admit_out": N.AdmitOut, "skv_stage_times": N.StageTimes,
-             "skv_dfa_view": N.DfaView, "skv_cost_model": N.CostModel}
+             "skv_dfa_view": N.DfaView, "skv_cost_model": N.CostModel, "skv_rep_entry": N.RepEntry,
+             "skv_rep_access": N.RepAccess}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "safekv_b200.h"', "int main(void){"]
     for cname, cls in pairs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
