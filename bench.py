@@ -59,10 +59,17 @@ CFG5 = dict(CFG2, n_prompts=4096, seed=5, name="config 5")
 # 1,000 x 112-token prompts, 7,000 blocks; every step re-admits it on a warm index (latency-bound)
 CFG1 = dict(n_prompts=1000, prompt_tokens=112, block_tokens=16, window_tokens=32, n_users=4, pool_size=0,
             pool_tokens=0, pii_per_kib=0.0, pii_mix=0, seed=2, name="config 1")
-CONFIGS = {1: CFG1, 2: CFG2, 3: CFG3, 4: CFG4, 5: CFG5}
+# --workload 6: the reference's presets/system_prompt.json shape at bench scale -- ONE 8,192-token
+# system prompt shared by every prompt (512 blocks) + a unique 2,048-token body, 16,384 prompts per
+# GPU per step.  Prefix-forest routing would send every prompt to one rank; with N > 1 the system
+# prompt's 512 blocks form the replicated layer (rep_depth) and prompts route by their first body
+# block, the replicated entries' inserts and window statistics merged over NCCL every step
+CFG6 = dict(n_prompts=16384, prompt_tokens=10240, block_tokens=16, window_tokens=32, n_users=64, pool_size=1,
+            pool_tokens=8192, pii_per_kib=1.0, pii_mix=0, seed=6, name="config 6 (system prompt)", rep_depth=512)
+CONFIGS = {1: CFG1, 2: CFG2, 3: CFG3, 4: CFG4, 5: CFG5, 6: CFG6}
 # prompts per step of the CPU reference (a deterministic prefix of each step's batch: the first
 # n prompts of the same global ids the GPU arm admits; BASELINE.md section 3 asks >= 10k prompts)
-CPU_SAMPLE = {1: 1000, 2: 10240, 3: 10240, 4: 512, 5: 4096}
+CPU_SAMPLE = {1: 1000, 2: 10240, 3: 10240, 4: 512, 5: 4096, 6: 1024}
 # config 4 on the CPU: the reference's pointer tree at 10 M entries (~5 GB, minutes to build) is
 # replaced by a 500 k-entry stored set (1,953 sequences x 256 blocks); queries have the same shape
 CPU_STORED_W4 = 1953
@@ -148,11 +155,11 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- inputs
-def gen_spec(c, n, world=1, rank=0):
+def gen_spec(c, n, world=1, rank=0, rep_depth=0):
     from workload import GenSpec
     return GenSpec(n_prompts=n, prompt_tokens=c["prompt_tokens"], n_users=c["n_users"], pool_size=c["pool_size"],
                    pool_tokens=c["pool_tokens"], pii_per_kib=c["pii_per_kib"], pii_mix=c["pii_mix"], seed=c["seed"],
-                   route_world=world, route_rank=rank, route_block_tokens=c["block_tokens"])
+                   route_world=world, route_rank=rank, route_block_tokens=c["block_tokens"], route_depth=rep_depth)
 
 
 def batch_id_base(k):
@@ -181,7 +188,7 @@ def stored_tiers(c, first, n):
 
 def build_batch(c, workload, k, n, spec=None, stored_tok=None, tok_out=None):
     """Host inputs of step k (the same for both arms; the CPU arm takes a prefix of n prompts).
-    Returns tokens (uint32), offsets, users, owners."""
+    Returns tokens (uint32), offsets, users, owners, global prompt ids (None for workloads 1 and 4)."""
     from workload import generate
     L, B = c["prompt_tokens"], c["block_tokens"]
     if workload == 1:
@@ -190,7 +197,7 @@ def build_batch(c, workload, k, n, spec=None, stored_tok=None, tok_out=None):
         if tok_out is not None:
             tok_out[:len(tok)] = tok
             tok = tok_out[:len(tok)]
-        return tok, w["offsets"].astype(np.uint64), w["users"].astype(np.uint64), w["owners"].astype(np.uint8)
+        return tok, w["offsets"].astype(np.uint64), w["users"].astype(np.uint64), w["owners"].astype(np.uint8), None
     tok = tok_out if tok_out is not None else np.empty(n * L, np.uint32)
     if workload == 4:  # a uniform-length prefix of a stored sequence + fresh text
         rng = np.random.default_rng(c["seed"] * 1000 + k)
@@ -202,11 +209,11 @@ def build_batch(c, workload, k, n, spec=None, stored_tok=None, tok_out=None):
             q[i, :cuts[i]] = stored_tok[picks[i], :cuts[i]]
         off = np.arange(n + 1, dtype=np.uint64) * np.uint64(L)
         users = rng.integers(1, c["n_users"] + 1, n).astype(np.uint64)
-        return tok[:n * L], off, users, np.zeros(n, np.uint8)
+        return tok[:n * L], off, users, np.zeros(n, np.uint8), None
     spec = spec or gen_spec(c, n)
     spec.n_prompts = n
     spec.prompt_id_base = batch_id_base(k)
-    _, off, users, owners = generate(spec, tokens_out=tok[:n * L])
+    _, off, users, owners, gids = generate(spec, tokens_out=tok[:n * L], return_ids=True)
     if workload == 5:  # every 10th prompt becomes an attacker probe
         rng = np.random.default_rng(c["seed"] * 1000 + k)
         rows = tok[:n * L].reshape(n, L)
@@ -223,8 +230,8 @@ def build_batch(c, workload, k, n, spec=None, stored_tok=None, tok_out=None):
         tok[:len(flat)] = flat
         off = np.zeros(n + 1, np.uint64)
         np.cumsum(lens, out=off[1:])
-        return tok[:len(flat)], off, users, owners
-    return tok[:n * L], off, users, owners
+        return tok[:len(flat)], off, users, owners, gids
+    return tok[:n * L], off, users, owners, gids
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -266,7 +273,7 @@ def cpu_reference_run(steps: int, warmup: int, sample_prompts: int, threads: int
     spec = gen_spec(c, sample_prompts)
     times, blocks, per_stage = [], 0, []
     for k in range(warmup + steps):
-        batch = build_batch(c, workload, k, sample_prompts, spec=spec, stored_tok=stored_tok)
+        batch = build_batch(c, workload, k, sample_prompts, spec=spec, stored_tok=stored_tok)[:4]
         t0 = time.perf_counter()
         o = eng.admit(*batch)
         t1 = time.perf_counter()
@@ -364,8 +371,13 @@ def run_ours(args):
     # the global sequence that skv_route assigns to it (disjoint index forests, no
     # data-path collective)
     from workload import generate_pool
-    spec = gen_spec(c, n_local, world, rank)
-    host, devb, ntok, nblk = [], [], [], []
+    from workload import route as gen_route
+    # replicated layer: entries at depth < rep_depth on every rank, prompts
+    # routed by their block rep_depth; 0 = prefix-forest partitioning (configs 2/3: their 256 pool
+    # roots already balance the ranks, the replicated layer would be empty)
+    rep_depth = (args.rep_depth if args.rep_depth >= 0 else c.get("rep_depth", 0)) if world > 1 else 0
+    spec = gen_spec(c, n_local, world, rank, rep_depth)
+    host, devb, ntok, nblk, batch_gids = [], [], [], [], []
     stored = stored_tok = None
     if args.workload == 4:  # the stored sequences of the pre-built index (host, chunked)
         stored = stored_sequences(c, c["stored"])
@@ -373,8 +385,9 @@ def run_ours(args):
     for k in range(n_batches):
         tok_pin = torch.empty(max(n_local * L, 1), dtype=torch.int32, pin_memory=True)
         tok_np = tok_pin.numpy().view(np.uint32)
-        tok, off, users, owners = build_batch(c, args.workload, k, n_local, spec=spec, stored_tok=stored_tok,
-                                              tok_out=tok_np)
+        tok, off, users, owners, gids = build_batch(c, args.workload, k, n_local, spec=spec, stored_tok=stored_tok,
+                                                    tok_out=tok_np)
+        batch_gids.append(gids)
         ntok.append(int(off[-1]))
         nblk.append(int(((off[1:] - off[:-1]) // np.uint64(B)).sum()))
         # every host input of the e2e arm lives in pinned memory (async H2D)
@@ -386,11 +399,24 @@ def run_ours(args):
         devb.append((tok_pin.to(dev, non_blocking=True), torch.from_numpy(off.view(np.int64)).to(dev),
                      torch.from_numpy(users.view(np.int64)).to(dev), torch.from_numpy(owners).to(dev)))
     torch.cuda.synchronize()
-    pool = generate_pool(spec, rank) if args.workload not in (1, 4) else None  # this rank's share
+    pool = pool_gids = None
+    if args.workload not in (1, 4):  # this rank's share of the pool (and the pool prompts' global ids)
+        pt, po, pu, pw = generate_pool(spec)
+        pr = gen_route(pt, po, world, B, depth=rep_depth) if world > 1 else np.zeros(len(po) - 1, np.uint32)
+        from paper_2508_08438_b200 import split_batch
+        pool = split_batch(pt, po, pu, pw, pr, rank)
+        pool_gids = np.flatnonzero(pr == rank).astype(np.uint64)
     pipeline = not args.no_pipeline
+    replica = {}
 
     def fresh_engine():
         eng = AdmissionEngine(ecfg)
+        replica.clear()
+        if rep_depth:
+            import torch.distributed as dist
+            from paper_2508_08438_b200 import ReplicaGroup, torch_allgather, torch_allgather_device
+            nccl = dist.get_backend() == "nccl"
+            replica["g"] = ReplicaGroup(eng, rep_depth, torch_allgather(), torch_allgather_device() if nccl else None)
         if stored is not None:  # the tiered 10 M-entry index
             first = 0
             for t, o, u, w in stored:
@@ -401,6 +427,8 @@ def run_ours(args):
         elif pool is not None:
             eng.admit(*pool)
             eng.commit()
+            if replica:
+                replica["g"].sync(pool_gids)
         eng.epoch_pass()
         return eng
 
@@ -420,6 +448,10 @@ def run_ours(args):
         if nxt is not None:
             eng.prefetch_raw(dev_batch(nxt))
         eng.commit()
+        if replica:  # the replicated layer's inserts and window statistics, merged over the ranks
+            t0 = time.perf_counter()
+            replica["g"].sync(batch_gids[k])
+            replica.setdefault("ms", []).append(1e3 * (time.perf_counter() - t0))
         eng.epoch_pass()
 
     # outputs returned to the host in the e2e arm: label + decision per block, match length +
@@ -436,6 +468,8 @@ def run_ours(args):
         if nxt is not None:
             eng.prefetch_raw(host_batch(nxt))
         eng.commit()
+        if replica:
+            replica["g"].sync(batch_gids[k])
         eng.epoch_pass()
 
     def barrier():
@@ -560,7 +594,10 @@ def run_ours(args):
                    "global_batch_prompts": n_local * world, "l2": f"inputs {n_local * L * 4 / 2**20:.0f} MiB/step per GPU (L2 126 MB), distinct batch per step",
                    "step": "admit + commit + epoch",
                    "index": f"{cap} slots x 64 B ({cap * 64 / 2**30:.0f} GiB), load {need / cap:.2f} at run end",
-                   "parallelism": (f"prefix-forest partitioned x{world} (skv_route; no data-path collective)"
+                   "parallelism": ((f"x{world} ranks: depth < {rep_depth} replicated on every rank (new entries + "
+                                    f"window statistics merged per step over {'NCCL' if world > 1 else ''} all-gather), "
+                                    f"prompts routed by block {rep_depth}" if rep_depth else
+                                    f"prefix-forest partitioned x{world} (skv_route; no data-path collective)")
                                    if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
                                 f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
@@ -574,7 +611,8 @@ def run_ours(args):
                      "avg_launch_ms_overlapped": hs_overlapped},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "step_breakdown": breakdown,
+        "step_breakdown": dict(breakdown, **({"replica_sync_ms_median": float(np.median(replica["ms"]))}
+                                             if replica.get("ms") else {})),
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -596,9 +634,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", type=int, default=2, choices=sorted(CONFIGS),
                     help="BASELINE.json config (2 = the headline, default; 1 = the smallest preset; 3 = the per-GPU "
-                         "shard of config 3; 4 = long context over a 10 M-entry tiered index; 5 = adversarial mix)")
+                         "shard of config 3; 4 = long context over a 10 M-entry tiered index; 5 = adversarial mix; "
+                         "6 = one shared 8,192-token system prompt)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
+    ap.add_argument("--rep-depth", type=int, default=-1,
+                    help="N > 1: replicated-layer depth (-1 = the workload's default: 512 for 6, else 0)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

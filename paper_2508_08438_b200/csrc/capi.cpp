@@ -1188,6 +1188,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     cudaStream_t s = c->stream;
     if (c->p_n == 0) {
       c->pending = false;
+      c->rep_sync_due = c->ix.rep.depth != 0;  // an empty share still takes part in the merge
       if (new_entries) *new_entries = 0;
       return SKV_OK;
     }
