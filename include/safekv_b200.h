@@ -92,7 +92,7 @@ typedef struct skv_ctx skv_ctx;
 
 typedef struct {
   int device;                  /* CUDA device ordinal                                 */
-  uint32_t block_tokens;       /* B: tokens per KV block (multiple of 4, 4..4096)     */
+  uint32_t block_tokens;       /* B: tokens per KV block (1..4096; the facade uses 1)  */
   uint32_t window_tokens;      /* W: right-context tokens of a block's scan window    */
   uint64_t index_capacity;     /* entry slots (rounded up to a power of two)          */
   uint64_t max_prompts;        /* per batch (<= 2^24)                                 */
@@ -265,6 +265,31 @@ int skv_set_cost_model(skv_ctx* ctx, const skv_cost_model* m);
  * NULL; on_device applies to request_ids and the outputs.  Valid until the next admit. */
 int skv_admit_ttft(skv_ctx* ctx, const uint64_t* request_ids, double* ttft_ms, uint32_t* intra_tokens,
                    uint32_t* inter_tokens, int on_device);
+
+/* ------------------------------------------------------------------------------
+ * Per-call entry points of the reference-API facade (include/safekv/): the reference's
+ * per-node operations on the device index, entries named by their keys (a facade NodeRef is
+ * the key list of one insert's blocks).
+ * ------------------------------------------------------------------------------ */
+/* RadixCacheIndex::match_prefix (cache_index.hpp:213-237): an admit that records no accesses
+ * (the reference's match only stamps access epochs) and leaves nothing to commit. */
+int skv_lookup(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
+/* RadixCacheIndex::insert (cache_index.hpp:152-205): admit without access records + commit. */
+int skv_insert(skv_ctx* ctx, const skv_batch* batch, uint64_t* new_entries);
+/* Entries by key (found[i] = 0 for a missing key; found may be NULL). */
+int skv_get_entries(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, size_t n, skv_entry* out, uint8_t* found);
+/* set_label (cache_index.hpp:312-315, 654-685) on entries given root-first; with propagate a
+ * Private / Restricted label also goes to every descendant of the last one (promotion to
+ * Public never propagates).  *changed = entries whose label changed. */
+int skv_label_entries(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, size_t n, uint8_t label, int propagate,
+                      size_t* changed);
+/* record_access (cache_index.hpp:385-388, AccessStats::record) of (entry, user) pairs in order. */
+int skv_record_accesses(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, const uint64_t* users, size_t n);
+/* roll_window (cache_index.hpp:390-393, AccessStats::roll) of the given entries. */
+int skv_roll_entries(skv_ctx* ctx, const uint64_t* h, const uint64_t* d, size_t n);
+/* EntropyMonitor::check_anomaly (monitor.hpp:56-81) on one entry: *ev gets the event values,
+ * *fired = 1 (and the entry and its subtree are relabeled) when the predicate holds. */
+int skv_check_anomaly(skv_ctx* ctx, uint64_t h, uint64_t d, uint64_t epoch, skv_event* ev, int* fired);
 
 /* Per-call wrappers (batch of one, still on the device) for the facade:
  * RuleEngine::tier1_scan (detection.hpp:217) and token_seq_digest (core.hpp:68). */

@@ -205,6 +205,7 @@ struct skv_ctx {
   // pending batch (between admit and commit)
   bool pending = false;
   bool dropped_by_evict = false;  // the last admitted batch was dropped by skv_evict
+  bool no_record = false;         // skv_lookup / skv_insert: the admit records no accesses
   // monitor records of the last admit, executed inside the commit kernel (overlapping
   // the claims), or on their own when the batch is not committed
   bool rec_pending = false;
@@ -632,7 +633,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   int rc = guard(c.get(), [&] {
     c->cfg = *cfg;
     const uint32_t B = cfg->block_tokens;
-    if (B < 4 || B > 4096 || B % 4) throw skv::ConfigError("block_tokens must be a multiple of 4 in [4, 4096]");
+    if (B < 1 || B > 4096) throw skv::ConfigError("block_tokens must be in [1, 4096]");
     if (cfg->window_tokens > 4096) throw skv::ConfigError("window_tokens must be <= 4096");
     if (cfg->max_prompts == 0 || cfg->max_prompts > skv::kMaxBatchPrompts)
       throw skv::ConfigError("max_prompts must be in [1, 2^24]");
@@ -987,7 +988,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // stage 4: the monitor records (AccessStats::record of every matched block, in
     // prompt order) run inside the commit kernel, overlapping the claims' DRAM round
     // trips; a batch that is not committed gets them from flush_record
-    c->rec_pending = true;
+    c->rec_pending = !c->no_record;
     c->rec_mon = mon;
     c->rec_users = users;
     c->rec_n = N;
@@ -1667,6 +1668,189 @@ int skv_replica_apply(skv_ctx* c, const skv_rep_entry* ents, size_t n_ents, cons
       c->poisoned = "replicated-layer apply failed (an entry, a parent or an accessed key is missing, or a pool is full)";
       throw CapacityError(c->poisoned);
     }
+    return SKV_OK;
+  });
+}
+
+// ------------------------------------------------------------------ per-call facade entry points
+int skv_lookup(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
+  if (!c || !b) return SKV_ERR_ARG;
+  if (c->ix.rep.depth) return fail(c, SKV_ERR_STATE, "skv_lookup: not with a replicated layer");
+  c->no_record = true;
+  const int rc = skv_admit(c, b, out);
+  c->no_record = false;
+  if (rc == SKV_OK) c->pending = false;  // nothing to commit, nothing recorded
+  return rc;
+}
+
+int skv_insert(skv_ctx* c, const skv_batch* b, uint64_t* new_entries) {
+  if (!c || !b) return SKV_ERR_ARG;
+  if (c->ix.rep.depth) return fail(c, SKV_ERR_STATE, "skv_insert: not with a replicated layer");
+  c->no_record = true;
+  int rc = skv_admit(c, b, nullptr);
+  c->no_record = false;
+  if (rc != SKV_OK) return rc;
+  return skv_commit(c, new_entries);
+}
+
+namespace {
+// device slots of host keys (SKV_ERR_ARG when one is not a live entry)
+std::vector<void*> find_slots(skv_ctx* c, const uint64_t* h, const uint64_t* d, size_t n, uint32_t** slots) {
+  std::vector<void*> tmp;
+  uint64_t* dh = dalloc<uint64_t>(n, tmp);
+  uint64_t* dd = dalloc<uint64_t>(n, tmp);
+  *slots = dalloc<uint32_t>(n, tmp);
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(dh, h, n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
+  skv::launch_find_entries(c->ix, dh, dd, static_cast<uint32_t>(n), *slots, s);
+  std::vector<uint32_t> hs(n);
+  CK(cudaMemcpyAsync(hs.data(), *slots, n * 4, cudaMemcpyDeviceToHost, s));
+  sync_check(s);
+  for (uint32_t v : hs)
+    if (v == skv::kNone) {
+      for (void* q : tmp) cudaFree(q);
+      throw ArgError("no such entry");
+    }
+  return tmp;
+}
+
+skv::MonCtx current_window(skv_ctx* c) {
+  skv::MonCtx m;
+  m.hdr = c->set_hdr;
+  m.tab = c->set_tab;
+  m.pool_cap = c->pool_cap;
+  m.pool_count = c->counters + 0;
+  m.touched = c->touched[c->cur];
+  m.n_touched = c->counters + 1 + c->cur;
+  m.batch = c->rec_batch;
+  m.wstart = c->wstart;
+  m.err = c->counters + 5;
+  m.matched_total = c->counters + 10;
+  return m;
+}
+}  // namespace
+
+int skv_get_entries(skv_ctx* c, const uint64_t* h, const uint64_t* d, size_t n, skv_entry* out, uint8_t* found) {
+  if (!c || (n && (!h || !d || !out))) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    flush_record(c);
+    if (!n) return SKV_OK;
+    std::vector<void*> tmp;
+    uint64_t* dh = dalloc<uint64_t>(n, tmp);
+    uint64_t* dd = dalloc<uint64_t>(n, tmp);
+    uint32_t* sl = dalloc<uint32_t>(n, tmp);
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(dh, h, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dd, d, n * 8, cudaMemcpyHostToDevice, s));
+    skv::launch_find_entries(c->ix, dh, dd, static_cast<uint32_t>(n), sl, s);
+    std::vector<uint32_t> hs(n);
+    CK(cudaMemcpyAsync(hs.data(), sl, n * 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    std::vector<uint64_t> rev(1);
+    for (size_t i = 0; i < n; ++i) {
+      if (found) found[i] = hs[i] != skv::kNone;
+      out[i] = skv_entry{};
+      if (hs[i] == skv::kNone) continue;
+      skv::Entry e;
+      CK(cudaMemcpy(&e, c->ix.e + hs[i], sizeof(e), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(rev.data(), c->users_tab.rev + e.rec.creator, 8, cudaMemcpyDeviceToHost));
+      out[i].h = e.rec.h;
+      out[i].d = e.rec.d;
+      out[i].creator = rev[0];
+      out[i].label = static_cast<uint8_t>(skv::meta_label(e.rec.meta));
+      out[i].owner = static_cast<uint8_t>(skv::meta_owner(e.rec.meta));
+      out[i].tier = static_cast<uint8_t>(skv::meta_tier(e.rec.meta));
+      out[i].hit_cur = e.stats.hit_cur;
+      out[i].u_cnt = e.stats.u_cnt;
+      out[i].hit_pre = e.stats.hit_pre;
+      out[i].u_pre = e.stats.u_pre;
+    }
+    for (void* q : tmp) cudaFree(q);
+    return SKV_OK;
+  });
+}
+
+int skv_label_entries(skv_ctx* c, const uint64_t* h, const uint64_t* d, size_t n, uint8_t label, int propagate,
+                      size_t* changed) {
+  if (!c || !n || !h || !d || label > SKV_LABEL_RESTRICTED) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    uint32_t* sl = nullptr;
+    std::vector<void*> tmp = find_slots(c, h, d, n, &sl);
+    unsigned long long* ch = dalloc<unsigned long long>(1, tmp);
+    // promotion to Public never propagates (cache_index.hpp:658-662)
+    const int prop = propagate && (label == SKV_LABEL_PRIVATE || label == SKV_LABEL_RESTRICTED);
+    skv::launch_label_entries(c->ix, sl, static_cast<uint32_t>(n), label, prop, ch, c->stream);
+    unsigned long long hc = 0;
+    CK(cudaMemcpyAsync(c->host_small + 44, ch, 8, cudaMemcpyDeviceToHost, c->stream));
+    sync_check(c->stream);
+    std::memcpy(&hc, c->host_small + 44, 8);
+    for (void* q : tmp) cudaFree(q);
+    if (changed) *changed = hc;
+    return SKV_OK;
+  });
+}
+
+int skv_record_accesses(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint64_t* users, size_t n) {
+  if (!c || (n && (!h || !d || !users))) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    check_usable(c);
+    ensure_admit_resolved(c);
+    flush_record(c);
+    if (!n) return SKV_OK;
+    uint32_t* sl = nullptr;
+    std::vector<void*> tmp = find_slots(c, h, d, n, &sl);
+    uint64_t* du = dalloc<uint64_t>(n, tmp);
+    CK(cudaMemcpyAsync(du, users, n * 8, cudaMemcpyHostToDevice, c->stream));
+    skv::launch_record_list(c->ix, current_window(c), sl, du, static_cast<uint32_t>(n), c->stream);
+    CK(cudaMemcpyAsync(c->host_small + 46, c->counters + 5, 4, cudaMemcpyDeviceToHost, c->stream));
+    sync_check(c->stream);
+    for (void* q : tmp) cudaFree(q);
+    if (c->host_small[46] & 1u) throw CapacityError("monitor window user-set pool exhausted (raise max_window_entries)");
+    return SKV_OK;
+  });
+}
+
+int skv_roll_entries(skv_ctx* c, const uint64_t* h, const uint64_t* d, size_t n) {
+  if (!c || (n && (!h || !d))) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    check_usable(c);
+    ensure_admit_resolved(c);
+    flush_record(c);
+    if (!n) return SKV_OK;
+    uint32_t* sl = nullptr;
+    std::vector<void*> tmp = find_slots(c, h, d, n, &sl);
+    skv::launch_roll_list(c->ix, current_window(c), sl, static_cast<uint32_t>(n), c->stream);
+    sync_check(c->stream);
+    for (void* q : tmp) cudaFree(q);
+    return SKV_OK;
+  });
+}
+
+int skv_check_anomaly(skv_ctx* c, uint64_t h, uint64_t d, uint64_t epoch, skv_event* ev, int* fired) {
+  if (!c || !ev || !fired) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    check_usable(c);
+    ensure_admit_resolved(c);
+    flush_record(c);
+    uint32_t* sl = nullptr;
+    std::vector<void*> tmp = find_slots(c, &h, &d, 1, &sl);
+    uint32_t slot = 0;
+    CK(cudaMemcpy(&slot, sl, 4, cudaMemcpyDeviceToHost));
+    skv_event* dev = dalloc<skv_event>(1, tmp);
+    int* df = dalloc<int>(1, tmp);
+    skv::launch_check_one(c->ix, slot, c->cfg.entropy_jump, c->cfg.u_pre_max, epoch, dev, df, c->stream);
+    CK(cudaMemcpyAsync(ev, dev, sizeof(skv_event), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(fired, df, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync_check(c->stream);
+    for (void* q : tmp) cudaFree(q);
     return SKV_OK;
   });
 }

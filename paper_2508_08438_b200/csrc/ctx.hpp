@@ -316,6 +316,16 @@ void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);
+// per-entry calls of the reference-API facade (kernels.cu)
+void launch_find_entries(const Index& ix, const uint64_t* h, const uint64_t* d, uint32_t n, uint32_t* slots,
+                         cudaStream_t s);
+void launch_label_entries(const Index& ix, const uint32_t* slots, uint32_t n, uint32_t label, int propagate,
+                          unsigned long long* changed, cudaStream_t s);
+void launch_record_list(const Index& ix, const MonCtx& M, const uint32_t* slots, const uint64_t* users, uint32_t n,
+                        cudaStream_t s);
+void launch_roll_list(const Index& ix, const MonCtx& M, const uint32_t* slots, uint32_t n, cudaStream_t s);
+void launch_check_one(const Index& ix, uint32_t slot, double jump, uint64_t u_pre_max, uint64_t epoch, void* ev,
+                      int* fired, cudaStream_t s);
 // replicated layer (multi-GPU): export / clear / apply (kernels.cu)
 void launch_rep_export(const Index& ix, const uint64_t* user_rev, const uint64_t* gids, uint32_t n_new, void* ents,
                        void* accs, uint32_t* n_accs, uint32_t acc_cap, cudaStream_t s);

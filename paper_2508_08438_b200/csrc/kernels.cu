@@ -2992,4 +2992,158 @@ void launch_rep_apply(const Index& ix, const MonCtx& M, const void* ents, const 
   cub::DeviceRadixSort::SortPairs(W.temp, tb, W.slot_a, W.slot_b, W.val_b, W.val_a, np, 0, bits, s);
   k_rep_apply_acc<<<cdiv(np, 256), 256, 0, s>>>(ix, M, W.slot_b, W.val_a, W.n);
 }
+
+// ---------------------------------------------------------------------------------
+// Per-entry calls of the reference-API facade (include/safekv/): set_label / record_access /
+// roll_window / check_anomaly on given entries, in call order (one thread: these are the
+// reference's per-call operations, cache_index.hpp:312-315,385-393, monitor.hpp:56-81)
+// ---------------------------------------------------------------------------------
+namespace {
+__global__ void k_find_entries(Index ix, const uint64_t* __restrict__ h, const uint64_t* __restrict__ d, uint32_t n,
+                               uint32_t* slots) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t s = rep_find(ix, h[i], d[i]);
+  slots[i] = (s != kNone && meta_live(ix.e[s].rec.meta)) ? s : kNone;
+}
+
+__device__ uint32_t label_subtree(const Index& ix, uint32_t root, uint32_t lab) {
+  uint32_t changed = 0;
+  uint32_t cur = ix.e[root].rec.first_child;
+  while (cur != kNone) {
+    const uint32_t m = ix.e[cur].rec.meta;
+    if (meta_label(m) != lab) {
+      ix.e[cur].rec.meta = (m & ~3u) | lab;
+      ++changed;
+    }
+    const uint32_t c = ix.e[cur].rec.first_child;
+    if (c != kNone) {
+      cur = c;
+      continue;
+    }
+    while (cur != root && ix.e[cur].aux.next_sibling == kNone) cur = ix.e[cur].rec.parent;
+    if (cur == root) break;
+    cur = ix.e[cur].aux.next_sibling;
+  }
+  return changed;
+}
+
+// label the entries (a facade node's blocks, root-first); with propagate, also every descendant
+// of the last one (apply_label_subtree, cache_index.hpp:672-685)
+__global__ void k_label_entries(Index ix, const uint32_t* __restrict__ slots, uint32_t n, uint32_t lab, int propagate,
+                                unsigned long long* changed) {
+  uint32_t ch = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t s = slots[i];
+    const uint32_t m = ix.e[s].rec.meta;
+    if (meta_label(m) != lab) {
+      ix.e[s].rec.meta = (m & ~3u) | lab;
+      ++ch;
+    }
+    if (propagate && i + 1 == n) ch += label_subtree(ix, s, lab);
+  }
+  *changed = ch;
+}
+
+// AccessStats::record of (entry, user) pairs in order, against the entries' window sets
+__global__ void k_record_list(Index ix, MonCtx M, const uint32_t* __restrict__ slots,
+                              const uint64_t* __restrict__ users, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t s = slots[i];
+    Entry& e = ix.e[s];
+    const uint32_t si = acquire_set(e, s, M);
+    if (si == kNone) return;
+    SetHdr& hd = M.hdr[si];
+    ulonglong2* tab = M.tab + static_cast<uint64_t>(si) * kSetSlots;
+    const uint64_t u = users[i];
+    e.stats.hit_cur += 1;
+    uint32_t pos = mix32(u) & (kSetSlots - 1), free_pos = kNone;
+    bool member = false;
+    for (uint32_t t = 0; t < kSetSlots; ++t, pos = (pos + 1) & (kSetSlots - 1)) {
+      const ulonglong2 x = tab[pos];
+      if (x.y < M.wstart) {
+        free_pos = pos;
+        break;
+      }
+      if (x.x == u) {
+        member = true;
+        break;
+      }
+    }
+    if (member) continue;
+    if (hd.size < kMaxSetUsers && free_pos != kNone) {
+      tab[free_pos] = make_ulonglong2(u, M.batch);
+      hd.size += 1;
+    }
+    e.stats.u_cnt += 1;  // a new member, or saturated: counted as new (access_stats.hpp:30-36)
+  }
+}
+
+// AccessStats::roll (access_stats.hpp:39-45) of given entries outside the epoch pass: the entry
+// keeps (or gets) its place in the current window list, with a fresh empty set
+__global__ void k_roll_list(Index ix, MonCtx M, const uint32_t* __restrict__ slots, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t s = slots[i];
+    Entry& e = ix.e[s];
+    if (acquire_set(e, s, M) == kNone) return;  // listed in the current window from now on
+    const uint32_t si = atomicAdd(M.pool_count, 1u);
+    if (si >= M.pool_cap) {
+      atomicOr(M.err, 1u);
+      return;
+    }
+    M.hdr[si] = SetHdr{0u, 0u, 0u, 0u, 0ull};
+    e.aux.set_idx = si;
+    const Stats st = e.stats;
+    e.stats = Stats{0u, 0u, st.hit_cur, st.u_cnt};
+  }
+}
+
+// EntropyMonitor::check_anomaly (monitor.hpp:56-81) on one entry: the event's values always, the
+// downgrade / restrict with subtree propagation when the predicate holds on a Public entry
+__global__ void k_check_one(Index ix, uint32_t s, double jump, uint64_t u_pre_max, uint64_t epoch, DevEvent* ev,
+                            int* fired) {
+  const Rec& r = ix.e[s].rec;
+  const Stats st = ix.e[s].stats;
+  DevEvent o;
+  o.h = r.h;
+  o.d = r.d;
+  o.owner = static_cast<uint8_t>(meta_owner(r.meta));
+  for (int k = 0; k < 6; ++k) o.pad[k] = 0;
+  o.now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
+  o.prev = st.hit_pre ? static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre) : 0.0;
+  o.u_pre = st.u_pre;
+  o.epoch = epoch;
+  o.action = SKV_ACTION_NONE;
+  *fired = 0;
+  if (meta_label(r.meta) == SKV_LABEL_PUBLIC && st.hit_pre > 0 && (o.now - o.prev) >= jump &&
+      static_cast<uint64_t>(st.u_pre) <= u_pre_max) {
+    const uint32_t lab = o.owner == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+    o.action = o.owner == 0 ? SKV_ACTION_DOWNGRADE : SKV_ACTION_RESTRICT;
+    ix.e[s].rec.meta = (r.meta & ~3u) | lab;
+    label_subtree(ix, s, lab);
+    *fired = 1;
+  }
+  *ev = o;
+}
+}  // namespace
+
+void launch_find_entries(const Index& ix, const uint64_t* h, const uint64_t* d, uint32_t n, uint32_t* slots,
+                         cudaStream_t s) {
+  if (n) k_find_entries<<<cdiv(n, 256), 256, 0, s>>>(ix, h, d, n, slots);
+}
+void launch_label_entries(const Index& ix, const uint32_t* slots, uint32_t n, uint32_t label, int propagate,
+                          unsigned long long* changed, cudaStream_t s) {
+  k_label_entries<<<1, 1, 0, s>>>(ix, slots, n, label, propagate, changed);
+}
+void launch_record_list(const Index& ix, const MonCtx& M, const uint32_t* slots, const uint64_t* users, uint32_t n,
+                        cudaStream_t s) {
+  if (n) k_record_list<<<1, 1, 0, s>>>(ix, M, slots, users, n);
+}
+void launch_roll_list(const Index& ix, const MonCtx& M, const uint32_t* slots, uint32_t n, cudaStream_t s) {
+  if (n) k_roll_list<<<1, 1, 0, s>>>(ix, M, slots, n);
+}
+void launch_check_one(const Index& ix, uint32_t slot, double jump, uint64_t u_pre_max, uint64_t epoch, void* ev,
+                      int* fired, cudaStream_t s) {
+  k_check_one<<<1, 1, 0, s>>>(ix, slot, jump, u_pre_max, epoch, static_cast<DevEvent*>(ev), fired);
+}
 }  // namespace skv

@@ -172,6 +172,15 @@ SIGNATURES = {
     "skv_cost_model_default": (None, [C.POINTER(CostModel)]),
     "skv_set_cost_model": (C.c_int, [C.c_void_p, C.POINTER(CostModel)]),
     "skv_admit_ttft": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    "skv_lookup": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(AdmitOut)]),
+    "skv_insert": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(C.c_uint64)]),
+    "skv_get_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Entry), C.c_void_p]),
+    "skv_label_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint8, C.c_int,
+                                    C.POINTER(C.c_size_t)]),
+    "skv_record_accesses": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    "skv_roll_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    "skv_check_anomaly": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Event),
+                                    C.POINTER(C.c_int)]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "skv_set_replicated_depth": (C.c_int, [C.c_void_p, C.c_uint32]),

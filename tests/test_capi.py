@@ -114,7 +114,7 @@ def test_no_cpu_fallback_without_gpu():
 def test_config_validation_precedes_device():
     from paper_2508_08438_b200 import ConfigError
     with pytest.raises(ConfigError):
-        AdmissionEngine(block_tokens=6)
+        AdmissionEngine(block_tokens=0)
 
 
 def test_generator_is_deterministic_and_shardable():
