@@ -178,6 +178,8 @@ typedef struct {
   uint64_t epoch;
 } skv_event;
 
+/* MonitorConfig (monitor.hpp:12-15) of the context's entropy monitor. */
+int skv_set_monitor_config(skv_ctx* ctx, double entropy_jump, uint64_t u_pre_max);
 /* advance_epoch + epoch_pass + roll.  Events are sorted by (h, d).  *n_events is the total
  * number of events; when it exceeds cap only the first cap are written and the whole list
  * stays retrievable with skv_last_events (nothing is lost: the epoch has been applied). */

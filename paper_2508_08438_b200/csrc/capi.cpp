@@ -1349,6 +1349,13 @@ int skv_last_events(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events)
   return SKV_OK;
 }
 
+int skv_set_monitor_config(skv_ctx* c, double entropy_jump, uint64_t u_pre_max) {
+  if (!c) return SKV_ERR_ARG;
+  c->cfg.entropy_jump = entropy_jump;
+  c->cfg.u_pre_max = u_pre_max;
+  return SKV_OK;
+}
+
 int skv_set_label_policy(skv_ctx* c, int pending) {
   if (!c) return SKV_ERR_ARG;
   c->pending_labels = pending != 0;

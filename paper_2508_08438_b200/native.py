@@ -159,6 +159,7 @@ SIGNATURES = {
     "skv_epoch": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t),
                             C.POINTER(C.c_uint64)]),
     "skv_last_events": (C.c_int, [C.c_void_p, C.POINTER(Event), C.c_size_t, C.POINTER(C.c_size_t)]),
+    "skv_set_monitor_config": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64]),
     "skv_set_label_policy": (C.c_int, [C.c_void_p, C.c_int]),
     "skv_resolve_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
                                      C.c_void_p]),
