@@ -235,6 +235,14 @@ int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_
  * stand; its commit would attach blocks to entries the eviction may free -- the reference pins
  * a request's path around insert), so a following skv_commit returns SKV_ERR_STATE. */
 
+/* SURVEY A.8 evaluation leak flag of the last admitted batch (serving_sim.hpp:379-392 with
+ * block_truth, workload.hpp:137-147): block b of prompt p leaks iff its label is Public and it
+ * overlaps a planted span of p that is sensitive on its own (SpanSensitivity::Always).  The
+ * caller passes only those spans: prompt p's are [span_off[p], span_off[p+1]) of span_begin /
+ * span_end (token offsets within the prompt, end exclusive).  flags (per block, may be NULL). */
+int skv_leak_flags(skv_ctx* ctx, const uint32_t* span_off, const uint64_t* span_begin, const uint64_t* span_end,
+                   uint8_t* flags, uint64_t* n_leaks);
+
 /* Per-stage device times of the last skv_admit / skv_commit (CUDA events, ms). */
 typedef struct {
   float hash_scan_ms, chain_probe_ms, record_ms, admit_total_ms, commit_ms, epoch_ms;

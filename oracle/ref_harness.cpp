@@ -639,6 +639,13 @@ size_t ref_workload_truth(void* w, size_t i, size_t cap, uint64_t* begin, uint64
   return tr.size();
 }
 
+// safekv::block_truth (workload.hpp:137-147) of request i's byte range [begin, end).
+void ref_workload_block_truth(void* w, size_t i, size_t begin, size_t end, int* alone, int* with_ctx) {
+  BlockTruth t = block_truth(static_cast<WlBox*>(w)->wl.requests[i], begin, end);
+  *alone = t.sensitive_alone ? 1 : 0;
+  *with_ctx = t.sensitive_with_context ? 1 : 0;
+}
+
 // Generator primitives (workload.hpp:155-266), exposed so tests can pin the
 // product-side synthetic generator against the reference byte for byte.
 size_t ref_filler(uint64_t uniq, size_t n, uint64_t* rng_state, char* out) {

@@ -1862,6 +1862,39 @@ int skv_check_anomaly(skv_ctx* c, uint64_t h, uint64_t d, uint64_t epoch, skv_ev
   });
 }
 
+int skv_leak_flags(skv_ctx* c, const uint32_t* span_off, const uint64_t* span_begin, const uint64_t* span_end,
+                   uint8_t* flags, uint64_t* n_leaks) {
+  if (!c || !span_off) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    const uint32_t N = c->last_n;
+    if (span_off[0] != 0) throw ArgError("span offsets must start at 0");
+    const size_t ns = span_off[N];
+    if (ns && (!span_begin || !span_end)) throw ArgError("null span arrays");
+    std::vector<void*> tmp;
+    uint32_t* doff = dalloc<uint32_t>(N + 1ull, tmp);
+    uint64_t* db = dalloc<uint64_t>(std::max<size_t>(ns, 1), tmp);
+    uint64_t* de = dalloc<uint64_t>(std::max<size_t>(ns, 1), tmp);
+    unsigned long long* dn = dalloc<unsigned long long>(1, tmp);
+    uint8_t* df = flags ? dalloc<uint8_t>(std::max<uint64_t>(c->p_blocks, 1), tmp) : nullptr;
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(doff, span_off, (N + 1ull) * 4, cudaMemcpyHostToDevice, s));
+    if (ns) CK(cudaMemcpyAsync(db, span_begin, ns * 8, cudaMemcpyHostToDevice, s));
+    if (ns) CK(cudaMemcpyAsync(de, span_end, ns * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(dn, 0, 8, s));
+    skv::launch_leak_flags(c->blk_off, c->blabel, doff, db, de, N, c->cfg.block_tokens, df, dn, s);
+    unsigned long long hn = 0;
+    CK(cudaMemcpyAsync(c->host_small + 48, dn, 8, cudaMemcpyDeviceToHost, s));
+    if (flags && c->p_blocks) CK(cudaMemcpyAsync(flags, df, c->p_blocks, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    std::memcpy(&hn, c->host_small + 48, 8);
+    for (void* q : tmp) cudaFree(q);
+    if (n_leaks) *n_leaks = hn;
+    return SKV_OK;
+  });
+}
+
 int skv_last_times(skv_ctx* c, skv_stage_times* out) {
   if (!c || !out) return SKV_ERR_ARG;
   return guard(c, [&] {

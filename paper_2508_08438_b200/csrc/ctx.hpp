@@ -316,6 +316,9 @@ void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);
+void launch_leak_flags(const uint32_t* blk_off, const uint8_t* label, const uint32_t* span_off, const uint64_t* sb,
+                       const uint64_t* se, uint32_t n_prompts, uint32_t B, uint8_t* flags,
+                       unsigned long long* n_leaks, cudaStream_t s);
 // per-entry calls of the reference-API facade (kernels.cu)
 void launch_find_entries(const Index& ix, const uint64_t* h, const uint64_t* d, uint32_t n, uint32_t* slots,
                          cudaStream_t s);

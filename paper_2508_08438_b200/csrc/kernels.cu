@@ -3146,4 +3146,36 @@ void launch_check_one(const Index& ix, uint32_t slot, double jump, uint64_t u_pr
                       int* fired, cudaStream_t s) {
   k_check_one<<<1, 1, 0, s>>>(ix, slot, jump, u_pre_max, epoch, static_cast<DevEvent*>(ev), fired);
 }
+
+// ---------------------------------------------------------------------------------
+// A.8 evaluation leak flag (serving_sim.hpp:379-392 with block_truth, workload.hpp:137-147): a
+// block of the last admitted batch is a leak iff it is labeled Public and overlaps a planted span
+// that is sensitive on its own (SpanSensitivity::Always).  One thread per block.
+// ---------------------------------------------------------------------------------
+namespace {
+__global__ void k_leak_flags(const uint32_t* __restrict__ blk_off, const uint8_t* __restrict__ label,
+                             const uint32_t* __restrict__ span_off, const uint64_t* __restrict__ sb,
+                             const uint64_t* __restrict__ se, uint32_t n_prompts, uint32_t B, uint8_t* flags,
+                             unsigned long long* n_leaks) {
+  const uint32_t p = blockIdx.x;
+  if (p >= n_prompts) return;
+  const uint32_t b0 = blk_off[p], nb = blk_off[p + 1] - b0, s0 = span_off[p], s1 = span_off[p + 1];
+  uint32_t leaks = 0;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    const uint64_t lo = static_cast<uint64_t>(b) * B, hi = lo + B;
+    bool hit = false;
+    for (uint32_t k = s0; k < s1 && !hit; ++k) hit = !(se[k] <= lo || sb[k] >= hi);
+    const bool leak = hit && label[b0 + b] == SKV_LABEL_PUBLIC;
+    if (flags) flags[b0 + b] = leak ? 1 : 0;
+    leaks += leak;
+  }
+  if (leaks) atomicAdd(n_leaks, static_cast<unsigned long long>(leaks));
+}
+}  // namespace
+
+void launch_leak_flags(const uint32_t* blk_off, const uint8_t* label, const uint32_t* span_off, const uint64_t* sb,
+                       const uint64_t* se, uint32_t n_prompts, uint32_t B, uint8_t* flags,
+                       unsigned long long* n_leaks, cudaStream_t s) {
+  if (n_prompts) k_leak_flags<<<n_prompts, 128, 0, s>>>(blk_off, label, span_off, sb, se, n_prompts, B, flags, n_leaks);
+}
 }  // namespace skv

@@ -233,6 +233,7 @@ class AdmissionEngine:
                        _ptr(res.block_offsets), 0, 0, 0)
         self._check(self._lib.skv_admit(self._h, C.byref(b), C.byref(o)))
         res.n_blocks, res.matched_total = int(o.n_blocks), int(o.matched_total)
+        self._last_blocks = res.n_blocks
         return res
 
     def admit_raw(self, batch: N.Batch, out: Optional[N.AdmitOut] = None) -> None:
@@ -403,6 +404,18 @@ class AdmissionEngine:
             n = accs.numel() // REP_ACCESS.itemsize
             rc = self._lib.skv_replica_apply(self._h, _ptr(ents), len(ents), accs.data_ptr() if n else None, n, 1)
         self._check(rc)
+
+    def leak_flags(self, span_off: np.ndarray, span_begin: np.ndarray, span_end: np.ndarray):
+        """SURVEY A.8 leak flags of the last admit: (per-block flags, count).  Spans: the planted
+        spans that are sensitive on their own, per prompt [span_off[p], span_off[p+1])."""
+        so = np.ascontiguousarray(span_off, np.uint32)
+        sb = np.ascontiguousarray(span_begin, np.uint64)
+        se = np.ascontiguousarray(span_end, np.uint64)
+        nb = getattr(self, "_last_blocks", None)
+        flags = np.zeros(max(int(nb or 0), 1), np.uint8)
+        n = C.c_uint64()
+        self._check(self._lib.skv_leak_flags(self._h, _ptr(so), _ptr(sb), _ptr(se), _ptr(flags), C.byref(n)))
+        return flags[:int(nb or 0)], int(n.value)
 
     def entry_count(self) -> int:
         return int(self._lib.skv_entry_count(self._h))

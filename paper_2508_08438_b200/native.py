@@ -182,6 +182,8 @@ SIGNATURES = {
     "skv_roll_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "skv_check_anomaly": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Event),
                                     C.POINTER(C.c_int)]),
+    "skv_leak_flags": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.POINTER(C.c_uint64)]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "skv_set_replicated_depth": (C.c_int, [C.c_void_p, C.c_uint32]),

@@ -153,3 +153,48 @@ def test_large_batch_properties(gpu):
     np.testing.assert_array_equal(eng.rules.to_rule_mask_array(got.rule_mask[sel]), exp["mask"])
     np.testing.assert_array_equal(got.label[sel], exp["label"])
     orc.close()
+
+
+def _always_spans(w):
+    cnt = w["truth_count"].astype(np.int64)
+    keep = w["truth_sens"] == 0  # SpanSensitivity::Always
+    so = np.zeros(len(cnt) + 1, np.uint32)
+    owner = np.repeat(np.arange(len(cnt)), cnt)[keep]
+    np.add.at(so, owner + 1, 1)
+    return np.cumsum(so).astype(np.uint32), w["truth_begin"][keep], w["truth_end"][keep]
+
+
+def test_leak_flags_config1(ref, gpu):
+    """SURVEY A.8 leak flags on the device (skv_leak_flags) for config 1: with the default rules
+    against the reference's golden (no planted secret leaks); with a rule set that knows only the
+    SSN and e-mail templates, Public blocks over planted secrets do leak, and the device flags
+    equal Public (reference labels under the same rules) AND block_truth.sensitive_alone."""
+    from paper_2508_08438_b200 import RuleSet
+    from refh import RefEngine, RefRules
+    w = np.load(GOLD / "cfg1_workload.npz")
+    lk = np.load(GOLD / "cfg1_leak.npz")
+    tok = w["tokens"].astype(np.uint32)
+    so, sb, se = _always_spans(w)
+    with AdmissionEngine(cfg()) as eng:
+        eng.admit(tok, w["offsets"], w["users"], w["owners"])
+        flags, n = eng.leak_flags(so, sb, se)
+        np.testing.assert_array_equal(flags, lk["r1_leak"])
+        assert n == int(lk["r1_leak"].sum())
+    rules = ('{"version": 3, "rules": ['
+             '{"rule_id": "ssn", "category": "Identity Information", "kind": "regex", '
+             '"pattern": "\\\\b\\\\d{3}-\\\\d{2}-\\\\d{4}\\\\b"},'
+             '{"rule_id": "mail", "category": "Basic Information", "kind": "regex", '
+             '"pattern": "[A-Za-z0-9._%+-]+@[A-Za-z0-9.-]+\\\\.[A-Za-z]{2,}"}]}')
+    with AdmissionEngine(cfg()) as eng:
+        eng.set_rules(RuleSet.from_json(rules))
+        got = eng.admit(tok, w["offsets"], w["users"], w["owners"])
+        re_ = RefEngine(ref, RefRules(ref, rules), B=16, W=32)
+        try:
+            exp = re_.admit(tok, w["offsets"], w["users"], w["owners"])
+        finally:
+            re_.close()
+        np.testing.assert_array_equal(got.label, exp["label"])
+        flags, n = eng.leak_flags(so, sb, se)
+        want = ((exp["label"] == 1) & (lk["sensitive_alone"] == 1)).astype(np.uint8)
+        np.testing.assert_array_equal(flags, want)
+        assert n == int(want.sum()) > 0

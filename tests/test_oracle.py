@@ -221,3 +221,25 @@ def test_monitor_saturation():
     x = oe.export()
     assert x["hit_cur"][0] == 66 and x["u_cnt"][0] == 66
     oe.close()
+
+
+def test_leak_golden_matches_truth_spans():
+    """the golden sensitive_alone flags (reference block_truth, tests/golden/
+    make_leak_golden.py) are exactly 'the block overlaps a planted span of sensitivity Always'
+    -- the span convention skv_leak_flags takes."""
+    import numpy as np
+    g = pathlib.Path(__file__).resolve().parent / "golden"
+    w = np.load(g / "cfg1_workload.npz")
+    lk = np.load(g / "cfg1_leak.npz")
+    off = w["offsets"].astype(np.int64)
+    cnt = w["truth_count"].astype(np.int64)
+    so = np.concatenate([[0], np.cumsum(cnt)])
+    mine = []
+    for i in range(len(off) - 1):
+        spans = [(int(w["truth_begin"][k]), int(w["truth_end"][k])) for k in range(so[i], so[i + 1])
+                 if w["truth_sens"][k] == 0]
+        for b in range((off[i + 1] - off[i]) // 16):
+            lo, hi = 16 * b, 16 * (b + 1)
+            mine.append(int(any(not (e <= lo or s >= hi) for s, e in spans)))
+    assert np.array_equal(np.array(mine, np.uint8), lk["sensitive_alone"])
+    assert lk["sensitive_alone"].sum() > 0

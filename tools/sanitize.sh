@@ -1,0 +1,13 @@
+#!/bin/bash
+# compute-sanitizer over small configurations of the CUDA path (memcheck / racecheck /
+# synccheck / initcheck).  Logs -> gpurun_out/sanitize_<tool>.log; summary lines to stdout.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+T="tests/test_gpu_parity.py::test_parity_b16_w32 tests/test_gpu_parity.py::test_parity_small_blocks_many_events tests/test_gpu_evict.py::test_evict_parity tests/test_gpu_replica.py::test_replicated_layer_in_process tests/test_gpu_labels.py tests/test_gpu_golden.py::test_config1_golden"
+for tool in memcheck racecheck synccheck initcheck; do
+  extra=""
+  [ "$tool" = "memcheck" ] && extra="--leak-check no"
+  timeout 1500 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 50 \
+      python -m pytest $T -x -q -p no:cacheprovider > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/sanitize_$tool.log | tail -2 | tr '\n' ' ')"
+done
