@@ -69,6 +69,10 @@ int skv_rules_info(const skv_rules* r, uint32_t i, const char** rule_id, const c
                    int* enabled);
 size_t skv_rules_warning_count(const skv_rules* r);
 const char* skv_rules_warning(const skv_rules* r, size_t i);
+/* The device runs a rule set as consecutive groups of <= 16 enabled rules whose automata fit its
+ * tables (one scan pass per group; window masks keep bit j = j-th enabled rule across groups),
+ * so rule sets of up to 32 enabled rules load whatever their automaton size. */
+uint32_t skv_rules_group_count(const skv_rules* r);
 /* Device rule masks use bit j = j-th ENABLED rule; this maps j -> rule list index. */
 uint32_t skv_rules_enabled_count(const skv_rules* r);
 uint32_t skv_rules_enabled_rule(const skv_rules* r, uint32_t j);

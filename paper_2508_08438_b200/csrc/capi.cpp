@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -19,7 +20,8 @@
 
 struct skv_rules {
   skv::RuleSetSpec spec;
-  skv::DfaTables dfa;
+  skv::DfaTables dfa;       // the whole rule set's automaton (skv_rules_dfa; the rule order)
+  skv::RuleGroups groups;   // the device's automata: consecutive groups of <= 16 enabled rules
 };
 
 #ifndef SKV_COMMIT_FLAT_HOST
@@ -106,9 +108,17 @@ struct skv_ctx {
 
   // rules
   skv_rules rules_host;
-  skv::DevRules rules_dev;
-  skv::DevRules16 rules16;  // k_hash_scan16's automaton (B = 16, W = 32)
-  void* rules_buf = nullptr;
+  // one device automaton per rule group (skv_rules::groups): the general kernel's tables and,
+  // for B = 16 / W = 32, k_hash_scan16's
+  struct DevGroup {
+    skv::DevRules dev{};
+    void* buf = nullptr;
+    skv::DevRules16 r16{};
+    skv::HSLayout layout{};
+    uint32_t smem = 0, shift = 0;
+    int grid = 0;
+  };
+  std::vector<DevGroup> groups;
   bool rules_loaded = false;
 
   // index
@@ -181,10 +191,7 @@ struct skv_ctx {
   void* temp = nullptr;
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
-  int hs_grid = 0;
   int n_sm = 148;
-  uint32_t hs_smem = 0;
-  skv::HSLayout hs_layout{};
   uint32_t rec_grid = 0;
 
   // set when a failed call left device state that no longer follows the reference (every
@@ -291,20 +298,31 @@ int guard(skv_ctx* c, F&& f) {
   }
 }
 
-void build_rules16(skv_ctx* c, const skv_rules& r);
+// Whether a group automaton fits the general kernel's device tables (u16 row offsets below the
+// 32 KB copy region, <= 63 byte classes, u16 copy-row rule masks: <= 16 rules per group).
+bool fits_device(const skv::DfaTables& d) {
+  const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 2;
+  if (C + 1 > 64 || d.rule_index.size() > 16) return false;
+  if (((S * row + 15) & ~15u) > skv::kAccRegion) return false;
+  std::set<std::pair<uint32_t, uint32_t>> copies;
+  for (uint32_t s = 0; s < S; ++s)
+    for (uint32_t k = 0; k <= C; ++k)
+      if (d.acc[s * (C + 1) + k]) copies.emplace(k < C ? d.next[s * C + k] : UINT32_MAX, d.acc[s * (C + 1) + k]);
+  return skv::kAccRegion + copies.size() * row <= 65535;
+}
 
-// Device form of the DFA (see ctx.hpp DevRules).  The 16-bit row offsets and the
-// 16-bit in-entry rule mask bound the device automaton; larger rule sets are rejected
-// here with CompileError (documented in DESIGN.md).
-void upload_rules(skv_ctx* c, const skv_rules& r) {
-  const auto& d = r.dfa;
+void free_group(skv_ctx::DevGroup& g) {
+  for (void* p : {g.buf, static_cast<void*>(g.r16.img), static_cast<void*>(g.r16.hi), static_cast<void*>(g.r16.full)})
+    if (p) cudaFree(p);
+  g = skv_ctx::DevGroup{};
+}
+
+// Device form of one group's DFA (see ctx.hpp DevRules): rows at the top of the 32 KB region,
+// accepting transitions pointing at copies of their target row above it.
+void build_group(skv_ctx* c, const skv::DfaTables& d, skv_ctx::DevGroup& g) {
   const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 2;
   const uint32_t norm = S * row;
-  if (C + 1 > 64) throw skv::CompileError("device DFA: more than 63 byte classes");
-  if (norm > skv::kAccRegion)
-    throw skv::CompileError("device DFA: " + std::to_string(S) + " states x " + std::to_string(C + 1) +
-                            " columns exceed the 32 KB row region");
-  if (d.rule_index.size() > 16) throw skv::CompileError("device DFA: more than 16 enabled rules");
+  if (!fits_device(d)) throw skv::CompileError("device DFA: a rule group exceeds the device tables");
   // accepting transitions -> copies of the target row in the region above 32 KB
   std::map<std::pair<uint32_t, uint32_t>, uint32_t> copy_of;  // (target, acc) -> copy index
   std::vector<std::pair<uint32_t, uint32_t>> copies;
@@ -329,7 +347,6 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
     }
   }
   const uint32_t fast_bytes = skv::kAccRegion + static_cast<uint32_t>(copies.size()) * row;
-  if (fast_bytes > 65535) throw skv::CompileError("device DFA: too many accepting transitions");
   std::vector<uint8_t> fast(fast_bytes, 0);
   std::memcpy(fast.data() + row_base, entry.data(), entry.size() * 2);
   for (size_t j = 0; j < copies.size(); ++j)
@@ -346,39 +363,33 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
   const size_t fast_al = (fast_bytes + 15) & ~size_t(15);
   const size_t full_bytes = full.size() * 4;
   const size_t acc_bytes = copy_acc.size() * 2;
-  void* buf = nullptr;
-  CK(cudaMalloc(&buf, fast_al + full_bytes + 256 + acc_bytes + 64));
-  uint8_t* base = static_cast<uint8_t*>(buf);
+  CK(cudaMalloc(&g.buf, fast_al + full_bytes + 256 + acc_bytes + 64));
+  uint8_t* base = static_cast<uint8_t*>(g.buf);
   CK(cudaMemcpyAsync(base, fast.data(), fast_bytes, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(base + fast_al, full.data(), full_bytes, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(base + fast_al + full_bytes, class2, 256, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(base + fast_al + full_bytes + 256, copy_acc.data(), acc_bytes, cudaMemcpyHostToDevice,
                      c->stream));
-  c->rules_dev.copy_acc = reinterpret_cast<uint16_t*>(base + fast_al + full_bytes + 256);
-  c->rules_dev.n_copies = static_cast<uint32_t>(copies.size());
-  c->rules_dev.copy_inv = inv;
-  sync_check(c->stream);
-  if (c->rules_buf) CK(cudaFree(c->rules_buf));
-  c->rules_buf = buf;
-  c->rules_dev.fast = reinterpret_cast<uint16_t*>(base);
-  c->rules_dev.full = reinterpret_cast<uint32_t*>(base + fast_al);
-  c->rules_dev.class2 = base + fast_al + full_bytes;
-  c->rules_dev.fast_bytes = fast_bytes;
-  c->rules_dev.norm_bytes = norm;
-  c->rules_dev.row_bytes = row;
-  c->rules_dev.start_row = row_base + d.start * row;
-  c->rules_dev.row_base = row_base;
-  c->rules_dev.eos2 = C * 2;
-  c->rules_dev.n_enabled = static_cast<uint32_t>(d.rule_index.size());
-  c->rules_host = r;
-  c->rules_loaded = true;
-  c->hs_layout = skv::hash_scan_layout(c->rules_dev, c->cfg.block_tokens, c->cfg.window_tokens);
-  c->hs_smem = c->hs_layout.total;
-  if (c->hs_layout.warps == 0 || c->hs_smem > 227 * 1024)
+  skv::DevRules& R = g.dev;
+  R.copy_acc = reinterpret_cast<uint16_t*>(base + fast_al + full_bytes + 256);
+  R.n_copies = static_cast<uint32_t>(copies.size());
+  R.copy_inv = inv;
+  R.fast = reinterpret_cast<uint16_t*>(base);
+  R.full = reinterpret_cast<uint32_t*>(base + fast_al);
+  R.class2 = base + fast_al + full_bytes;
+  R.fast_bytes = fast_bytes;
+  R.norm_bytes = norm;
+  R.row_bytes = row;
+  R.start_row = row_base + d.start * row;
+  R.row_base = row_base;
+  R.eos2 = C * 2;
+  R.n_enabled = static_cast<uint32_t>(d.rule_index.size());
+  g.layout = skv::hash_scan_layout(R, c->cfg.block_tokens, c->cfg.window_tokens);
+  g.smem = g.layout.total;
+  if (g.layout.warps == 0 || g.smem > 227 * 1024)
     throw skv::ConfigError("hash/scan shared-memory footprint exceeds 227 KB (block_tokens too large)");
-  c->hs_grid = skv::hash_scan_grid(c->device, c->hs_smem, 32 * c->hs_layout.warps);
-  if (c->hs_grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
-  build_rules16(c, r);
+  g.grid = skv::hash_scan_grid(c->device, g.smem, 32 * g.layout.warps);
+  if (g.grid <= 0) throw CudaError("k_hash_scan: shared-memory opt-in / occupancy query failed");
 }
 
 // The B = 16 / W = 32 automaton of k_hash_scan16 (ctx.hpp DevRules16, hash_scan16.cuh): column t
@@ -387,12 +398,8 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
 // or the state is a shadow already; column 128 holds the end-of-text rule mask.  Not built
 // (the general kernel runs) for other shapes or when the image does not fit SMEM beside the
 // per-warp task queues.
-void build_rules16(skv_ctx* c, const skv_rules& r) {
-  skv::DevRules16& R = c->rules16;
-  for (void* p : {static_cast<void*>(R.img), static_cast<void*>(R.hi), static_cast<void*>(R.full)})
-    if (p) CK(cudaFree(p));
-  R = skv::DevRules16{};
-  const auto& d = r.dfa;
+void build_group16(skv_ctx* c, const skv::DfaTables& d, skv_ctx::DevGroup& g) {
+  skv::DevRules16& R = g.r16;
   const uint32_t S = d.n_states, C = d.n_classes;
   if (c->cfg.block_tokens != 16 || c->cfg.window_tokens != 32 || 4ull * S >= 65536) return;
   const uint32_t S2 = 2 * S, colbytes = 4 * S;
@@ -424,7 +431,6 @@ void build_rules16(skv_ctx* c, const skv_rules& r) {
   CK(cudaMemcpyAsync(R.img, img.data(), img_al, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(R.hi, hi.data(), hi.size() * 2, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(R.full, full.data(), full.size() * 4, cudaMemcpyHostToDevice, c->stream));
-  sync_check(c->stream);
   R.img_bytes = img_bytes;
   R.colbytes = colbytes;
   R.s2 = S2;
@@ -433,6 +439,27 @@ void build_rules16(skv_ctx* c, const skv_rules& r) {
   R.smem = smem;
   R.grid = grid;
   R.ok = true;
+}
+
+// The rule set's device automata (one per rule group); replaces the previous set atomically
+// (RuleEngine::load_rules swap, detection.hpp:238-241) once every table is on the device.
+void upload_rules(skv_ctx* c, const skv_rules& r) {
+  std::vector<skv_ctx::DevGroup> gs(r.groups.groups.size());
+  try {
+    for (size_t i = 0; i < gs.size(); ++i) {
+      build_group(c, r.groups.groups[i], gs[i]);
+      build_group16(c, r.groups.groups[i], gs[i]);
+      gs[i].shift = r.groups.first_bit[i];
+    }
+    sync_check(c->stream);
+  } catch (...) {
+    for (auto& g : gs) free_group(g);
+    throw;
+  }
+  for (auto& g : c->groups) free_group(g);
+  c->groups = std::move(gs);
+  c->rules_host = r;
+  c->rules_loaded = true;
 }
 
 skv::MonCtx monitor_ctx(skv_ctx* c) {
@@ -462,53 +489,62 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
   // SMs: the one-CTA-per-SM kernel would otherwise hold every SM until it ends and serialise the
   // commit behind it (measured: 1.13 ms per config-2 step at full grid, 0.97 at a quarter)
   static const int pf_frac = getenv("SKV_H16_PF_FRAC") ? atoi(getenv("SKV_H16_PF_FRAC")) : 4;
-  if (c->rules16.ok && !force_general && !(overlapped && pf_general)) {
-    const skv::DevRules16& R = c->rules16;
-    skv::HS16Args h;
-    h.tokens = tokens;
-    h.tok_off = off;
-    h.blk_off = blk_off;
-    h.n_prompts = N;
-    h.n_tokens = n_tokens;
-    h.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, 16);
-    h.img = R.img;
-    h.img_bytes = R.img_bytes;
-    h.hi = R.hi;
-    h.full = R.full;
-    h.colbytes = R.colbytes;
-    h.s2 = R.s2;
-    h.v_start = R.v_start;
-    h.q_cap = R.q_cap;
-    h.d_out = bd;
-    h.mask_out = bmask;
-    h.first_sens = first_sens;
-    // a small batch needs fewer CTAs (one 32-warp CTA per SM otherwise)
-    const uint64_t want = nb_hint ? (nb_hint + 32 * 32 - 1) / (32 * 32) : static_cast<uint64_t>(R.grid);
-    uint64_t grid = std::min<uint64_t>(R.grid, std::max<uint64_t>(want, 1));
-    if (overlapped && pf_frac > 1) grid = std::max<uint64_t>(1, grid / pf_frac);
-    skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st);
-    return;
+  // one pass per rule group: the first stores the digests and the window masks, the others OR
+  // their masks in at their rules' bits (a rule set larger than one device automaton)
+  for (size_t gi = 0; gi < c->groups.size(); ++gi) {
+    const skv_ctx::DevGroup& g = c->groups[gi];
+    if (g.r16.ok && !force_general && !(overlapped && pf_general)) {
+      const skv::DevRules16& R = g.r16;
+      skv::HS16Args h;
+      h.tokens = tokens;
+      h.tok_off = off;
+      h.blk_off = blk_off;
+      h.n_prompts = N;
+      h.n_tokens = n_tokens;
+      h.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, 16);
+      h.img = R.img;
+      h.img_bytes = R.img_bytes;
+      h.hi = R.hi;
+      h.full = R.full;
+      h.colbytes = R.colbytes;
+      h.s2 = R.s2;
+      h.v_start = R.v_start;
+      h.q_cap = R.q_cap;
+      h.mask_shift = g.shift;
+      h.first = gi == 0;
+      h.d_out = bd;
+      h.mask_out = bmask;
+      h.first_sens = first_sens;
+      // a small batch needs fewer CTAs (one 32-warp CTA per SM otherwise)
+      const uint64_t want = nb_hint ? (nb_hint + 32 * 32 - 1) / (32 * 32) : static_cast<uint64_t>(R.grid);
+      uint64_t grid = std::min<uint64_t>(R.grid, std::max<uint64_t>(want, 1));
+      if (overlapped && pf_frac > 1) grid = std::max<uint64_t>(1, grid / pf_frac);
+      skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st);
+      continue;
+    }
+    skv::HashScanArgs a;
+    a.tokens = tokens;
+    a.tok_off = off;
+    a.blk_off = blk_off;
+    a.n_prompts = N;
+    a.n_tokens = n_tokens;
+    a.n_blocks = static_cast<uint32_t>(nb_hint);  // grid-size hint only; 0 = unknown
+    a.B = c->cfg.block_tokens;
+    a.W = c->cfg.window_tokens;
+    a.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, a.B);
+    a.rules = g.dev;
+    a.mask_shift = g.shift;
+    a.first = gi == 0;
+    a.d_out = bd;
+    a.mask_out = bmask;
+    a.first_sens = first_sens;
+    a.off_list = g.layout.off_list;
+    a.stage = g.layout.stage;
+    a.buf_gap = g.layout.buf_gap;
+    a.n_gap = g.layout.n_gap;
+    a.buf_tail = g.layout.buf_tail;
+    skv::launch_hash_scan(a, g.grid, g.smem, 32 * g.layout.warps, st);
   }
-  skv::HashScanArgs a;
-  a.tokens = tokens;
-  a.tok_off = off;
-  a.blk_off = blk_off;
-  a.n_prompts = N;
-  a.n_tokens = n_tokens;
-  a.n_blocks = static_cast<uint32_t>(nb_hint);  // grid-size hint only; 0 = unknown
-  a.B = c->cfg.block_tokens;
-  a.W = c->cfg.window_tokens;
-  a.digest_init = fnv_u32_host(0xcbf29ce484222325ULL, a.B);
-  a.rules = c->rules_dev;
-  a.d_out = bd;
-  a.mask_out = bmask;
-  a.first_sens = first_sens;
-  a.off_list = c->hs_layout.off_list;
-  a.stage = c->hs_layout.stage;
-  a.buf_gap = c->hs_layout.buf_gap;
-  a.n_gap = c->hs_layout.n_gap;
-  a.buf_tail = c->hs_layout.buf_tail;
-  skv::launch_hash_scan(a, c->hs_grid, c->hs_smem, 32 * c->hs_layout.warps, st);
 }
 
 // Offsets of a host batch: [0, n_tokens], non-decreasing.  Returns the block count.
@@ -550,6 +586,7 @@ int skv_rules_default(skv_rules** out) {
     r->spec.version = 1;  // RuleEngine() default snapshot version (detection.hpp:210)
     r->spec.rules = skv::default_pattern_rules();
     r->dfa = skv::compile_rules(r->spec.rules);
+    r->groups = skv::compile_rule_groups(r->spec.rules, fits_device);
     *out = r.release();
     return SKV_OK;
   });
@@ -562,6 +599,7 @@ int skv_rules_from_json(const char* json, size_t len, skv_rules** out, char* err
     auto r = std::make_unique<skv_rules>();
     r->spec = skv::parse_rules_json(std::string(json, len));
     r->dfa = skv::compile_rules(r->spec.rules);
+    r->groups = skv::compile_rule_groups(r->spec.rules, fits_device);
     *out = r.release();
     return SKV_OK;
   });
@@ -592,6 +630,10 @@ size_t skv_rules_warning_count(const skv_rules* r) { return r ? r->spec.warnings
 const char* skv_rules_warning(const skv_rules* r, size_t i) {
   return (r && i < r->spec.warnings.size()) ? r->spec.warnings[i].c_str() : nullptr;
 }
+uint32_t skv_rules_group_count(const skv_rules* r) {
+  return r ? static_cast<uint32_t>(r->groups.groups.size()) : 0;
+}
+
 uint32_t skv_rules_enabled_count(const skv_rules* r) {
   return r ? static_cast<uint32_t>(r->dfa.rule_index.size()) : 0;
 }
@@ -783,11 +825,8 @@ int skv_destroy(skv_ctx* c) {
   if (c->side) cudaStreamSynchronize(c->side);
   if (c->rec_stream) cudaStreamSynchronize(c->rec_stream);
   for (void* p : c->owned) cudaFree(p);
-  if (c->rules_buf) cudaFree(c->rules_buf);
+  for (auto& g : c->groups) free_group(g);
   for (void* p : {c->rep_in, static_cast<void*>(c->rep_slots), static_cast<void*>(c->rep_uidx)})
-    if (p) cudaFree(p);
-  for (void* p : {static_cast<void*>(c->rules16.img), static_cast<void*>(c->rules16.hi),
-                  static_cast<void*>(c->rules16.full)})
     if (p) cudaFree(p);
   if (c->host_small) cudaFreeHost(c->host_small);
   for (auto& ev : c->ev)
@@ -1913,7 +1952,8 @@ int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {
     uint32_t* dm = dalloc<uint32_t>(1, tmp);
     cudaStream_t s = c->stream;
     if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
-    skv::launch_scan_text(dt, static_cast<uint32_t>(len), c->rules_dev, dm, s);
+    CK(cudaMemsetAsync(dm, 0, 4, s));
+    for (const auto& g : c->groups) skv::launch_scan_text(dt, static_cast<uint32_t>(len), g.dev, dm, g.shift, s);
     CK(cudaMemcpyAsync(c->host_small, dm, 4, cudaMemcpyDeviceToHost, s));
     sync_check(s);
     *mask = c->host_small[0];

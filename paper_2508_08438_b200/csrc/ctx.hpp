@@ -140,6 +140,8 @@ struct HS16Args {
   uint32_t s2;        // 2S: v >= s2 <=> shadow (accepted) state
   uint32_t v_start;
   uint32_t q_cap;  // deferred exact tasks per warp (>= 96)
+  uint32_t mask_shift;  // bit of this rule group's first rule in the window masks
+  uint32_t first;       // 1: the first group (stores digests and masks); else masks are OR-ed in
   uint64_t* d_out;
   uint32_t* mask_out;
   uint32_t* first_sens;
@@ -155,6 +157,8 @@ struct HashScanArgs {
   uint32_t B, W;
   uint64_t digest_init;  // FNV state after update_u32(B)
   DevRules rules;
+  uint32_t mask_shift;  // bit of this rule group's first rule in the window masks
+  uint32_t first;       // 1: the first group (stores digests and masks); else masks are OR-ed in
   uint64_t* d_out;
   uint32_t* mask_out;
   uint32_t* first_sens;
@@ -313,7 +317,7 @@ void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, con
                       cudaStream_t s);
 void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, uint32_t cap,
                    cudaStream_t s);
-void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s);
+void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, uint32_t shift, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);
 void launch_leak_flags(const uint32_t* blk_off, const uint8_t* label, const uint32_t* span_off, const uint64_t* sb,

@@ -131,7 +131,7 @@ __device__ __forceinline__ void h16_flush(H16Task* q, uint32_t qn, uint32_t lane
     const uint32_t m = h16_exact(a.full, S, a.tokens, t.tokv & 0xffffffffffull, (t.tokv >> 40) & 63u,
                                  static_cast<uint32_t>(t.tokv >> 46));
     if (m) {
-      atomicOr(&a.mask_out[t.gb], m);
+      atomicOr(&a.mask_out[t.gb], m << a.mask_shift);
       atomicMin(&a.first_sens[t.p], t.gb - a.blk_off[t.p]);
     }
   }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
       Xb = h16_base(v, s2);
       dg = h;
     }
-    if (own && k0 >= G0 && k0 < G1) a.d_out[k0] = dg;
+    if (a.first && own && k0 >= G0 && k0 < G1) a.d_out[k0] = dg;
     const uint32_t P = own ? (Xb | (faw << 16)) : 0u;
     // ---- phase B: window k0-1 over this block, from X(k0-1)
     const uint32_t Pd1 = __shfl_sync(kFull, lane == 31 ? Pprev : P, (lane + 31) & 31);
@@ -368,7 +368,10 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
         f = (fa ? 1u : 0u) | (C1w ? 2u : 0u);
       }
       const uint32_t me = *reinterpret_cast<const uint16_t*>(eos + fin);  // end-of-text transition (exact)
-      a.mask_out[w] = me;
+      if (a.first)
+        a.mask_out[w] = me;
+      else if (me)
+        atomicOr(&a.mask_out[w], me << a.mask_shift);  // a later rule group (bits shifted to its rules)
       if (fast && (me || f)) pw = slot_p[pw];
       if (me) atomicMin(&a.first_sens[pw], bw);
       sX = Xw;  // segment start states for the exact masks: block w+1 from X(w), block w+2 from Y(w)

@@ -330,7 +330,7 @@ __device__ __forceinline__ void flush_tasks(const SegTask* q, uint32_t qn, uint3
     const SegTask t = q[k];
     const uint32_t m = exact_tokens(tab, cmap, acc_tab, inv, a.tokens, t.tok, t.meta >> 16, t.meta & 0xffffu);
     if (m) {
-      atomicOr(&a.mask_out[t.gb], m);
+      atomicOr(&a.mask_out[t.gb], m << a.mask_shift);
       atomicMin(&a.first_sens[t.p], t.b);
     }
   }
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
         X = row;
         A |= amid;
       }
-      if (out) a.d_out[gb] = dg;
+      if (out && a.first) a.d_out[gb] = dg;
     }
 #if SKV_HS_L1PF == 1
     l1_prefetch_next(tokens, a.n_tokens, T0, nout, lane, B, W);
@@ -703,7 +703,10 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
         }
       }
       const uint32_t me = copy_mask(acc_tab, lds16(tab, fin + eos2), inv);  // end-of-window transition
-      a.mask_out[gb] = me;
+      if (a.first)
+        a.mask_out[gb] = me;
+      else if (me)
+        atomicOr(&a.mask_out[gb], me << a.mask_shift);  // a later rule group (bits shifted to its rules)
       if (me) atomicMin(&a.first_sens[p], b);
       f = ((A & kAccRegion) ? 1u : 0u) | (Cf ? 2u : 0u) | ((C2 & kAccRegion) ? 4u : 0u);
     }
@@ -746,7 +749,7 @@ __global__ void __launch_bounds__(kHSWarps * 32, SKV_HS_MINB) k_hash_scan(HashSc
             m |= copy_mask(acc_tab, row, inv);
           }
           if (m) {
-            atomicOr(&a.mask_out[gb], m);
+            atomicOr(&a.mask_out[gb], m << a.mask_shift);
             atomicMin(&a.first_sens[p], b);
           }
         }
@@ -2170,7 +2173,7 @@ __global__ void k_export(Index ix, const uint64_t* __restrict__ user_rev, skv_en
   if (k < cap) out[k] = e;  // the count is exact even past cap (the host re-sizes and retries)
 }
 
-__global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask) {
+__global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, uint32_t shift) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t row = r.start_row, acc = 0;
   for (uint32_t i = 0; i < len; ++i) {
@@ -2179,7 +2182,7 @@ __global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint3
     row = e & 0xffffu;
   }
   acc |= r.full[(row - r.row_base + r.eos2) >> 1];
-  *mask = acc >> 16;
+  *mask |= (acc >> 16) << shift;
 }
 
 __global__ void k_digest(const uint32_t* t, uint32_t n, uint64_t* out) {
@@ -2661,8 +2664,8 @@ void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_
   k_export<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, user_rev, static_cast<skv_entry*>(out), n_out, cap);
 }
 
-void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, cudaStream_t s) {
-  k_scan_text<<<1, 32, 0, s>>>(text, len, r, mask);
+void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, uint32_t shift, cudaStream_t s) {
+  k_scan_text<<<1, 32, 0, s>>>(text, len, r, mask, shift);
 }
 
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s) {

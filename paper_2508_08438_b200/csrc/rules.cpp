@@ -1068,4 +1068,44 @@ DfaTables compile_rules(const std::vector<PatternRule>& rules) {
   return out;
 }
 
+RuleGroups compile_rule_groups(const std::vector<PatternRule>& rules,
+                               const std::function<bool(const DfaTables&)>& fits, uint32_t max_group) {
+  std::vector<size_t> enabled;
+  for (size_t i = 0; i < rules.size(); ++i)
+    if (rules[i].enabled) enabled.push_back(i);
+  RuleGroups out;
+  auto compile_range = [&](size_t a, size_t b) {  // enabled[a, b) stay enabled
+    std::vector<PatternRule> sub = rules;
+    for (auto& r : sub) r.enabled = false;
+    for (size_t k = a; k < b; ++k) sub[enabled[k]].enabled = true;
+    return compile_rules(sub);
+  };
+  if (enabled.empty()) {
+    out.groups.push_back(compile_rules(rules));
+    out.first_bit.push_back(0);
+    return out;
+  }
+  for (size_t a = 0; a < enabled.size();) {
+    size_t b = std::min(enabled.size(), a + max_group);
+    DfaTables t = compile_range(a, b);
+    while (!fits(t)) {  // shrink until the group's automaton fits the device tables
+      if (b - a == 1)
+        throw CompileError("rule '" + rules[enabled[a]].rule_id + "': its automaton exceeds the device table limits");
+      b = a + (b - a) / 2;
+      t = compile_range(a, b);
+    }
+    // grow back one rule at a time while it still fits (halving may have overshot)
+    while (b < enabled.size() && b - a < max_group) {
+      DfaTables t2 = compile_range(a, b + 1);
+      if (!fits(t2)) break;
+      t = std::move(t2);
+      ++b;
+    }
+    out.first_bit.push_back(static_cast<uint32_t>(a));
+    out.groups.push_back(std::move(t));
+    a = b;
+  }
+  return out;
+}
+
 }  // namespace skv

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -73,5 +74,17 @@ struct DfaTables {
 // reference CompiledRuleSet::compile (detection.hpp:120-144): duplicate rule_id and
 // bad regex raise CompileError naming the rule.
 DfaTables compile_rules(const std::vector<PatternRule>& rules);
+
+// Device rule groups: the enabled rules, in order, cut into consecutive groups of at most
+// max_group rules whose automaton satisfies `fits` (the device table limits); each group is
+// compiled over the full list with the other rules disabled (so duplicate blacklist terms keep
+// the reference's last-writer semantics, detection.hpp:62,157-159).  Group g's mask bit k is the
+// (first_bit[g] + k)-th enabled rule.  CompileError if a single rule does not fit.
+struct RuleGroups {
+  std::vector<DfaTables> groups;
+  std::vector<uint32_t> first_bit;
+};
+RuleGroups compile_rule_groups(const std::vector<PatternRule>& rules, const std::function<bool(const DfaTables&)>& fits,
+                               uint32_t max_group = 16);
 
 }  // namespace skv

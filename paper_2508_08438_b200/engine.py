@@ -80,6 +80,10 @@ class RuleSet:
         n = self._lib.skv_rules_warning_count(self._h)
         return [self._lib.skv_rules_warning(self._h, i).decode() for i in range(n)]
 
+    def group_count(self) -> int:
+        """Device automata the rule set runs as (one scan pass each)."""
+        return int(self._lib.skv_rules_group_count(self._h))
+
     def enabled_rules(self) -> list[int]:
         n = self._lib.skv_rules_enabled_count(self._h)
         return [int(self._lib.skv_rules_enabled_rule(self._h, j)) for j in range(n)]

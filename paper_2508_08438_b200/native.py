@@ -144,6 +144,7 @@ SIGNATURES = {
                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "skv_rules_warning_count": (C.c_size_t, [C.c_void_p]),
     "skv_rules_warning": (C.c_char_p, [C.c_void_p, C.c_size_t]),
+    "skv_rules_group_count": (C.c_uint32, [C.c_void_p]),
     "skv_rules_enabled_count": (C.c_uint32, [C.c_void_p]),
     "skv_rules_enabled_rule": (C.c_uint32, [C.c_void_p, C.c_uint32]),
     "skv_rules_dfa": (C.c_int, [C.c_void_p, C.POINTER(DfaView)]),

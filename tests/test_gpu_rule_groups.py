@@ -1,0 +1,88 @@
+"""Rule sets larger than one device automaton: more than 16 enabled rules,
+and automata beyond the 32 KB row region, run as consecutive rule groups (one scan pass each,
+masks at their rules' bits).  Per-rule window masks, labels, matches, events and the index must
+equal the unmodified reference (std::regex per rule) -- on both the B=16/W=32 kernel and the
+general one (B=8)."""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2508_08438_b200 import AdmissionEngine, EngineConfig, RuleSet
+from refh import RefEngine, RefRules
+from test_gpu_parity import check_admit, check_events, check_index
+
+pytestmark = pytest.mark.gpu
+
+
+def rule_sets():
+    rng = np.random.default_rng(7)
+    words = ["alpha", "beta", "cache", "kv", "block", "prefix", "user", "mail", "account", "number", "imei", "card"]
+    many = []
+    for i in range(28):
+        w = words[i % len(words)]
+        if i % 4 == 0:
+            many.append({"rule_id": f"b{i}", "category": f"C{i % 5}", "kind": "blacklist", "pattern": f"{w.upper()}{i}"})
+        else:
+            many.append({"rule_id": f"r{i}", "category": f"C{i % 6}", "kind": "regex",
+                         "pattern": f"\\b{w}[0-9]{{{1 + i % 3}}}\\b|x{i}y+z", "enabled": i % 9 != 5})
+    lits = ["".join(rng.choice(list("abcdefgh"), 10)) for _ in range(300)]
+    big = [{"rule_id": f"g{i}", "category": f"Big{i % 3}", "kind": "regex", "pattern": "|".join(lits[25 * i:25 * i + 25])}
+           for i in range(12)]
+    return {"many": (json.dumps({"version": 11, "rules": many}), words), "big": (json.dumps({"version": 12, "rules": big}), lits)}
+
+
+def make_batch(rng, vocab, n_prompts, n_users):
+    toks, offs, users = [], [0], []
+    for _ in range(n_prompts):
+        parts = []
+        for _ in range(int(rng.integers(4, 40))):
+            r = rng.random()
+            w = vocab[rng.integers(len(vocab))]
+            if r < 0.3:
+                parts.append(w + str(int(rng.integers(0, 1000))))
+            elif r < 0.4:
+                parts.append(w.upper() + str(int(rng.integers(0, 30))))
+            elif r < 0.5:
+                parts.append(f"x{int(rng.integers(0, 30))}yyz")
+            else:
+                parts.append(w)
+        t = np.frombuffer(" ".join(parts).encode(), np.uint8).astype(np.uint32)
+        toks.append(t)
+        offs.append(offs[-1] + len(t))
+        users.append(1 + int(rng.integers(n_users)))
+    return (np.concatenate(toks), np.array(offs, np.uint64), np.array(users, np.uint64),
+            np.zeros(n_prompts, np.uint8))
+
+
+@pytest.mark.parametrize("which,B,W", [("many", 16, 32), ("many", 8, 16), ("big", 16, 32), ("big", 8, 16)])
+def test_rule_groups_parity(ref, gpu, which, B, W):
+    text, vocab = rule_sets()[which]
+    rs = RuleSet.from_json(text)
+    assert rs.group_count() >= 2
+    rng = np.random.default_rng(hash((which, B)) % 1000)
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=512, max_tokens=1 << 18,
+                       max_window_entries=1 << 14)
+    with AdmissionEngine(cfg) as eng:
+        eng.set_rules(rs)
+        re_ = RefEngine(ref, RefRules(ref, text), B=B, W=W)
+        try:
+            flagged = 0
+            for _ in range(3):
+                batch = make_batch(rng, vocab, 160, 5)
+                got = eng.admit(*batch)
+                exp = re_.admit(*batch)
+                check_admit(rs, got, exp)
+                flagged += int((got.rule_mask != 0).sum())
+                eng.commit()
+                re_.commit()
+                _, ev_g = eng.epoch_pass()
+                _, ev_r = re_.epoch()
+                check_events(ev_g, ev_r)
+                check_index(eng, re_)
+            assert flagged > 0
+            # per-call tier1_scan across the groups
+            for t in (b"alpha12 x3yyz", b"CARD11 kv", vocab[3].encode() + b" " + vocab[250 % len(vocab)].encode()):
+                assert rs.to_rule_mask(eng.tier1_scan(t)) == RefRules(ref, text).mask(t)
+        finally:
+            re_.close()
