@@ -436,8 +436,22 @@ def run_ours(args):
         t, o, u, w = devb[k]
         return N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, ntok[k], 1)
 
+    # e2e inputs: the prompts' byte tokens (the reference's ByteVocabulary, core.hpp:92-101 -- every
+    # workload token is a byte) in pinned host memory, a quarter of the TokenId copy; widened on
+    # the device (skv_batch::token_bytes).  --e2e-u32 sends the uint32 TokenIds instead.
+    byte_tokens = not args.e2e_u32 and all(int(h[1][:ntok[k]].max(initial=0)) < 256 for k, h in enumerate(host))
+    host8 = []
+    if byte_tokens:
+        for k, h in enumerate(host):
+            t8 = torch.empty(max(ntok[k], 1), dtype=torch.uint8, pin_memory=True)
+            t8.numpy()[:ntok[k]] = h[1][:ntok[k]]
+            host8.append(t8)
+
     def host_batch(k):
         _, tok, off, users, owners, _ = host[k]
+        if byte_tokens:
+            return N.Batch(None, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local, ntok[k], 0,
+                           host8[k].data_ptr())
         return N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
                        ntok[k], 0)
 
@@ -578,7 +592,7 @@ def run_ours(args):
         "note": "commit_ms includes the batch's monitor records (run inside k_commit); hash/scan of the next "
                 "batch overlaps it on a side stream",
     }
-    h2d = int(timed_tokens) * 4 + (n_local + 1) * 8 + n_local * 8 + n_local
+    h2d = int(timed_tokens) * (1 if byte_tokens else 4) + (n_local + 1) * 8 + n_local * 8 + n_local
     d2h = 2 * int(timed_blocks) + n_local * 5
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
@@ -610,7 +624,11 @@ def run_ours(args):
                      "timing": "CUDA events around each k_hash_scan launch on its stream, un-pipelined pass",
                      "avg_launch_ms_overlapped": hs_overlapped},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "inputs": ("byte tokens (ByteVocabulary) + offsets, users, owners from pinned host memory, widened "
+                           "on the device" if byte_tokens else "uint32 TokenIds + offsets, users, owners from pinned "
+                           "host memory"),
+                "outputs": "label + decision per block, matched blocks + lowest tier per prompt, to pinned host memory"},
         "step_breakdown": dict(breakdown, **({"replica_sync_ms_median": float(np.median(replica["ms"]))}
                                              if replica.get("ms") else {})),
         "gpu_launches": launches,
@@ -638,6 +656,7 @@ def main():
                          "6 = one shared 8,192-token system prompt)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
+    ap.add_argument("--e2e-u32", action="store_true", help="e2e arm: send uint32 TokenIds instead of byte tokens")
     ap.add_argument("--rep-depth", type=int, default=-1,
                     help="N > 1: replicated-layer depth (-1 = the workload's default: 512 for 6, else 0)")
     args = ap.parse_args()

@@ -134,6 +134,10 @@ typedef struct {
   uint32_t n_prompts;
   uint64_t n_tokens;
   int on_device;           /* 1: all pointers are device pointers (inputs resident in HBM) */
+  /* optional, instead of tokens: the prompts' tokens as bytes -- the reference's ByteVocabulary
+   * (core.hpp:92-101: TokenId = byte value), e.g. the prompt text itself.  A quarter of the
+   * tokens' host->device copy; widened to TokenIds on the device.  tokens is then ignored. */
+  const uint8_t* token_bytes;
 } skv_batch;
 
 typedef struct {

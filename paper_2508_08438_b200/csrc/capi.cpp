@@ -146,6 +146,7 @@ struct skv_ctx {
   // batch buffers
   uint64_t max_prompts = 0, max_tokens = 0, max_blocks = 0;
   uint32_t* d_tokens = nullptr;
+  uint8_t* d_tok8 = nullptr;  // byte-token staging (skv_batch::token_bytes)
   uint64_t* d_off = nullptr;
   uint64_t* d_users = nullptr;
   uint8_t* d_owners = nullptr;
@@ -259,6 +260,7 @@ struct skv_ctx {
   const void* pf_owners = nullptr;
   // host-batch staging set (skv_prefetch of a host batch copies into it on the side stream)
   uint32_t* alt_tokens = nullptr;
+  uint8_t* alt_tok8 = nullptr;  // byte-token staging (skv_batch::token_bytes)
   uint64_t* alt_off = nullptr;
   uint64_t* alt_users = nullptr;
   uint8_t* alt_owners = nullptr;
@@ -938,7 +940,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       c->last_n = 0;
       return SKV_OK;
     }
-    if (!b->tokens || !b->offsets || !b->users) throw ArgError("null batch pointer");
+    if ((!b->tokens && !b->token_bytes) || !b->offsets || !b->users) throw ArgError("null batch pointer");
+    const void* tok_id = b->token_bytes ? static_cast<const void*>(b->token_bytes) : b->tokens;
     cudaStream_t s = c->stream;
     const uint32_t* tokens;
     const uint64_t* off;
@@ -946,7 +949,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const uint8_t* owners;
     uint64_t n_blocks = 0;
     // stages 1+2 (and for host batches the H2D) were staged by skv_prefetch for exactly this batch?
-    const bool use_pf = c->pf_valid && c->pf_on_device == (b->on_device != 0) && c->pf_tokens == b->tokens &&
+    const bool use_pf = c->pf_valid && c->pf_on_device == (b->on_device != 0) && c->pf_tokens == tok_id &&
                         c->pf_offsets == b->offsets && c->pf_users == b->users && c->pf_owners == b->owners &&
                         c->pf_n == N && c->pf_ntok == b->n_tokens;
     if (c->pf_valid && !use_pf) CK(cudaStreamSynchronize(c->side));  // stale prefetch: drop it
@@ -960,7 +963,13 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
         std::swap(c->d_users, c->alt_users);
         std::swap(c->d_owners, c->alt_owners);
       } else {
-        CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, s));
+        if (b->token_bytes) {  // byte tokens: a quarter of the copy, widened on the device
+          if (!c->d_tok8) c->d_tok8 = dalloc<uint8_t>(c->max_tokens + 16, c->owned);
+          CK(cudaMemcpyAsync(c->d_tok8, b->token_bytes, b->n_tokens, cudaMemcpyHostToDevice, s));
+          skv::launch_widen(c->d_tok8, c->d_tokens, b->n_tokens, s);
+        } else {
+          CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, s));
+        }
         CK(cudaMemcpyAsync(c->d_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(c->d_users, b->users, N * 8ull, cudaMemcpyHostToDevice, s));
         if (b->owners) CK(cudaMemcpyAsync(c->d_owners, b->owners, N, cudaMemcpyHostToDevice, s));
@@ -969,6 +978,12 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       off = c->d_off;
       users = c->d_users;
       owners = b->owners ? c->d_owners : nullptr;
+    } else if (b->token_bytes) {
+      if (!use_pf) skv::launch_widen(b->token_bytes, c->d_tokens, b->n_tokens, s);  // else staged by the prefetch
+      tokens = c->d_tokens;
+      off = b->offsets;
+      users = b->users;
+      owners = b->owners;
     } else {
       tokens = b->tokens;
       if (reinterpret_cast<uintptr_t>(tokens) % 16) {
@@ -1163,7 +1178,8 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     const uint32_t N = b->n_prompts;
     // anything the pipeline cannot stage is admitted inline by skv_admit (which also
     // reports its argument errors)
-    if (N == 0 || N > c->max_prompts || b->n_tokens > c->max_tokens || !b->tokens || !b->offsets || !b->users)
+    if (N == 0 || N > c->max_prompts || b->n_tokens > c->max_tokens || (!b->tokens && !b->token_bytes) ||
+        !b->offsets || !b->users)
       return SKV_OK;
     cudaStream_t st = c->side;
     const uint32_t* tokens = b->tokens;
@@ -1182,12 +1198,27 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
         c->alt_users = dalloc<uint64_t>(c->max_prompts, c->owned);
         c->alt_owners = dalloc<uint8_t>(c->max_prompts, c->owned);
       }
-      CK(cudaMemcpyAsync(c->alt_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, st));
+      if (b->token_bytes) {
+        if (!c->alt_tok8) c->alt_tok8 = dalloc<uint8_t>(c->max_tokens + 16, c->owned);
+        CK(cudaMemcpyAsync(c->alt_tok8, b->token_bytes, b->n_tokens, cudaMemcpyHostToDevice, st));
+        skv::launch_widen(c->alt_tok8, c->alt_tokens, b->n_tokens, st);
+      } else {
+        CK(cudaMemcpyAsync(c->alt_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, st));
+      }
       CK(cudaMemcpyAsync(c->alt_off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(c->alt_users, b->users, N * 8ull, cudaMemcpyHostToDevice, st));
       if (b->owners) CK(cudaMemcpyAsync(c->alt_owners, b->owners, N, cudaMemcpyHostToDevice, st));
       tokens = c->alt_tokens;
       off = c->alt_off;
+    } else if (b->token_bytes) {  // device byte tokens: widened into the staging set
+      if (!c->alt_tokens) {
+        c->alt_tokens = dalloc<uint32_t>(c->max_tokens + 4, c->owned);
+        c->alt_off = dalloc<uint64_t>(c->max_prompts + 1, c->owned);
+        c->alt_users = dalloc<uint64_t>(c->max_prompts, c->owned);
+        c->alt_owners = dalloc<uint8_t>(c->max_prompts, c->owned);
+      }
+      skv::launch_widen(b->token_bytes, c->alt_tokens, b->n_tokens, st);
+      tokens = c->alt_tokens;
     } else if (reinterpret_cast<uintptr_t>(b->tokens) % 16) {
       return SKV_OK;
     }
@@ -1207,7 +1238,7 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     CK(cudaGetLastError());
     c->pf_valid = true;
     c->pf_on_device = b->on_device != 0;
-    c->pf_tokens = b->tokens;
+    c->pf_tokens = b->token_bytes ? static_cast<const void*>(b->token_bytes) : b->tokens;
     c->pf_offsets = b->offsets;
     c->pf_users = b->users;
     c->pf_owners = b->owners;

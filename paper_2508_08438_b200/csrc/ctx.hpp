@@ -237,6 +237,7 @@ struct CostModelDev {
 };
 
 void launch_init_entries(const Index& ix, cudaStream_t s);
+void launch_widen(const uint8_t* in, uint32_t* out, uint64_t n, cudaStream_t s);
 // eviction (kernels.cu): access epochs of matched blocks at admit; node ids + access epochs
 // of every committed block at commit; evict(needed) = effective keys, sort, tombstones
 void launch_touch_matched(const Index& ix, const uint32_t* slot, const uint32_t* blk_off, const uint32_t* matched,

@@ -3181,4 +3181,26 @@ void launch_leak_flags(const uint32_t* blk_off, const uint8_t* label, const uint
                        unsigned long long* n_leaks, cudaStream_t s) {
   if (n_prompts) k_leak_flags<<<n_prompts, 128, 0, s>>>(blk_off, label, span_off, sb, se, n_prompts, B, flags, n_leaks);
 }
+
+// byte tokens (ByteVocabulary) -> TokenIds: 16 bytes per thread in, 4 x 16 B out
+namespace {
+__global__ void k_widen(const uint8_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n) {
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16ull;
+  if (i >= n) return;
+  if (i + 16 <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    const uint4 v = *reinterpret_cast<const uint4*>(in + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint4* o = reinterpret_cast<uint4*>(out + i);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_uint4(w[q] & 0xffu, (w[q] >> 8) & 0xffu, (w[q] >> 16) & 0xffu, w[q] >> 24);
+  } else {
+    for (uint64_t k = i; k < n && k < i + 16; ++k) out[k] = in[k];
+  }
+}
+}  // namespace
+
+void launch_widen(const uint8_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+  if (n) k_widen<<<static_cast<uint32_t>((n + 16 * 256 - 1) / (16 * 256)), 256, 0, s>>>(in, out, n);
+}
 }  // namespace skv

@@ -218,7 +218,11 @@ class AdmissionEngine:
     # --------------------------------------------------------------- phase L
     def admit(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,
               owners: Optional[np.ndarray] = None) -> AdmitResult:
-        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        """Phase L of one batch.  ``tokens`` as uint32 TokenIds, or as uint8 byte tokens (the
+        reference's ByteVocabulary: a quarter of the host->device copy, skv_batch::token_bytes)."""
+        as_bytes = isinstance(tokens, (bytes, bytearray)) or np.asarray(tokens).dtype == np.uint8
+        tokens = np.ascontiguousarray(np.frombuffer(tokens, np.uint8) if isinstance(tokens, (bytes, bytearray))
+                                      else tokens, dtype=np.uint8 if as_bytes else np.uint32)
         offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
         users = np.ascontiguousarray(users, dtype=np.uint64)
         if owners is not None:
@@ -231,7 +235,8 @@ class AdmissionEngine:
             block_d=np.zeros(nb, np.uint64), label=np.zeros(nb, np.uint8), rule_mask=np.zeros(nb, np.uint32),
             decision=np.zeros(nb, np.uint8), matched_blocks=np.zeros(n, np.uint32),
             lowest_tier=np.zeros(n, np.uint8))
-        b = N.Batch(_ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), n, len(tokens), 0)
+        b = N.Batch(None if as_bytes else _ptr(tokens), _ptr(offsets), _ptr(users), _ptr(owners), n, len(tokens), 0,
+                    _ptr(tokens) if as_bytes else None)
         o = N.AdmitOut(_ptr(res.block_h), _ptr(res.block_d), _ptr(res.label), _ptr(res.rule_mask),
                        _ptr(res.decision), _ptr(res.matched_blocks), _ptr(res.lowest_tier),
                        _ptr(res.block_offsets), 0, 0, 0)

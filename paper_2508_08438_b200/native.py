@@ -88,7 +88,8 @@ class Config(C.Structure):
 
 class Batch(C.Structure):
     _fields_ = [("tokens", C.c_void_p), ("offsets", C.c_void_p), ("users", C.c_void_p), ("owners", C.c_void_p),
-                ("n_prompts", C.c_uint32), ("n_tokens", C.c_uint64), ("on_device", C.c_int)]
+                ("n_prompts", C.c_uint32), ("n_tokens", C.c_uint64), ("on_device", C.c_int),
+                ("token_bytes", C.c_void_p)]
 
 
 class AdmitOut(C.Structure):

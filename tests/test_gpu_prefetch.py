@@ -128,3 +128,45 @@ def test_prefetch_mismatch_is_dropped(gpu):
             rc = c_.admit(*b1)
             np.testing.assert_array_equal(got["rule_mask"][:o.n_blocks], rc.rule_mask)
             np.testing.assert_array_equal(got["label"][:o.n_blocks], rc.label)
+
+
+def test_byte_token_batches(ref, gpu):
+    """Byte tokens (skv_batch::token_bytes, the reference's ByteVocabulary) give exactly the
+    TokenId path's results -- host and device batches, inline and prefetched."""
+    import torch
+    from paper_2508_08438_b200 import native as N
+    from test_gpu_parity import check_admit, check_index
+    rng = np.random.default_rng(77)
+    trunks = make_trunks(rng, 8)
+    batches = [make_batch(rng, trunks, 120, 5) for _ in range(4)]
+    cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 16, max_prompts=1024,
+                       max_tokens=1 << 18, max_window_entries=1 << 14)
+    with AdmissionEngine(cfg) as a, AdmissionEngine(cfg) as b:
+        re_ = RefEngine(ref, RefRules(ref), B=16, W=32)
+        try:
+            for k, (tok, off, users, owners) in enumerate(batches):
+                t8 = tok.astype(np.uint8)
+                if k % 2 == 0:  # host byte batch
+                    got = a.admit(t8, off, users, owners)
+                else:           # device byte batch, prefetched then admitted
+                    dev = torch.device("cuda", 0)
+                    dt = torch.from_numpy(t8.copy()).to(dev)
+                    do = torch.from_numpy(off.view(np.int64)).to(dev)
+                    du = torch.from_numpy(users.view(np.int64)).to(dev)
+                    dw = torch.from_numpy(owners).to(dev)
+                    bat = N.Batch(None, do.data_ptr(), du.data_ptr(), dw.data_ptr(), len(off) - 1, len(tok), 1,
+                                  dt.data_ptr())
+                    a.prefetch_raw(bat)
+                    a.admit_raw(bat)
+                    got = None
+                exp_u32 = b.admit(tok, off, users, owners)
+                exp = re_.admit(tok, off, users, owners)
+                check_admit(b.rules, exp_u32, exp)
+                if got is not None:
+                    check_admit(a.rules, got, exp)
+                a.commit()
+                b.commit()
+                re_.commit()
+                check_index(a, re_)
+        finally:
+            re_.close()
