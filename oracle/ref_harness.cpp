@@ -312,6 +312,15 @@ int ref_engine_set_tiered(void* ev, int tiered) {
 }
 
 void ref_engine_set_threads(void* e, int n) { static_cast<RefEngine*>(e)->nthreads = n; }
+
+// Hot reload between batches: the next admit scans with the new snapshot (RuleEngine::load_rules
+// swaps the active set atomically, detection.hpp:238-241; in-flight scans keep the old one -- in
+// the batched contract a batch is one scan, so the swap lands at a batch boundary).
+void ref_engine_set_rules(void* ev, void* rules) {
+  auto* e = static_cast<RefEngine*>(ev);
+  e->rules_box = rules;
+  e->rules = static_cast<RulesBox*>(rules)->set;
+}
 void ref_engine_set_stock_scan(void* e, int on) { static_cast<RefEngine*>(e)->stock_scan = on; }
 
 // Phase L of Appendix A.1 for one batch: hashes, window verdicts, labels, lookups and

@@ -45,6 +45,7 @@ def load_ref():
         "ref_engine_create": (vp, [vp, C.c_uint32, C.c_uint32, C.c_double, C.c_uint64]),
         "ref_engine_free": (None, [vp]),
         "ref_engine_set_threads": (None, [vp, C.c_int]),
+        "ref_engine_set_rules": (None, [vp, vp]),
         "ref_engine_admit": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp, vp, vp, vp, vp, vp]),
         "ref_engine_commit": (C.c_int, [vp]),
         "ref_engine_set_tiers": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
@@ -109,6 +110,11 @@ class RefEngine:
         if self.h:
             self.L.ref_engine_free(self.h)
             self.h = None
+
+    def set_rules(self, rules: "RefRules"):
+        """Reload between batches (RuleEngine::load_rules swap, detection.hpp:238-241)."""
+        self.rules = rules
+        self.L.ref_engine_set_rules(self.h, rules.h)
 
     def admit(self, tokens, offsets, users, owners=None):
         tokens = np.ascontiguousarray(tokens, np.uint32)

@@ -86,3 +86,33 @@ def test_rule_groups_parity(ref, gpu, which, B, W):
                 assert rs.to_rule_mask(eng.tier1_scan(t)) == RefRules(ref, text).mask(t)
         finally:
             re_.close()
+
+
+def test_hot_reload_parity(ref, gpu):
+    """Rule hot reload at batch boundaries (RuleEngine::load_rules, detection.hpp:238-241, 651-662):
+    default -> 28-rule set -> large-automaton set -> default, the device (skv_set_rules) and the
+    reference engine swapping the same snapshots between the same batches; every batch, epoch and
+    index dump equal."""
+    sets = rule_sets()
+    vocab = sets["many"][1] + sets["big"][1][:40]
+    seq = [None, sets["many"][0], sets["big"][0], None]
+    rng = np.random.default_rng(99)
+    cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 16, max_prompts=512, max_tokens=1 << 18,
+                       max_window_entries=1 << 14)
+    with AdmissionEngine(cfg) as eng:
+        re_ = RefEngine(ref, RefRules(ref), B=16, W=32)
+        try:
+            for text in seq:
+                rs = RuleSet.default() if text is None else RuleSet.from_json(text)
+                eng.set_rules(rs)
+                re_.set_rules(RefRules(ref, text))
+                for _ in range(2):
+                    batch = make_batch(rng, vocab, 120, 4)
+                    check_admit(rs, eng.admit(*batch), re_.admit(*batch))
+                    eng.commit()
+                    re_.commit()
+                    _, ev_g = eng.epoch_pass()
+                    check_events(ev_g, re_.epoch()[1])
+                    check_index(eng, re_)
+        finally:
+            re_.close()
