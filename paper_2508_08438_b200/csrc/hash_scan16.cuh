@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
     const uint32_t w = k0 - 2;                 // the window this lane finalises
     const uint32_t lo = max(g, G0 + 2) - 2;    // lowest block whose geometry the chunk needs
     const uint32_t hi_b = min(g + 32, nb);     // one past the highest
-    const bool fast = lo >= prev_s && hi_b <= next_e;
+    const bool fast = __all_sync(kFull, lo >= prev_s && hi_b <= next_e);  // warp-uniform (a vote)
     unsigned long long tok0 = 0, tokw = 0;
     uint32_t ew = 0, pw = 0, bw = 0;
     if (fast) {
@@ -256,7 +256,9 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
     for (uint32_t k = 0; k < 16; ++k) any |= t[k];
     uint32_t Zb, Xb, faw;  // base states after kConv16 / 16 bytes; flags: bit 0 = [0,4) accepted, bit 1 = [4,16)
     uint64_t dg;
-    const bool slow_bytes = any >= 128u;  // a byte >= 128 (or a wide token): general steps
+    // a byte >= 128 (or a wide token) in any lane's block: the whole warp takes the general steps
+    // (warp-uniform, so the fast path carries no divergence bookkeeping)
+    const bool slow_bytes = __any_sync(kFull, any >= 128u);
     if (!slow_bytes) {
       uint64_t h = a.digest_init;
       uint32_t v = v_start;
@@ -305,10 +307,10 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
     }
     uint32_t C1 = V >= s2 ? 1u : 0u;
     const uint32_t Vb = h16_base(V, s2);
+    const bool met = Vb == Zb;  // the runs met: window k0-1's run over [4,16) is this block's own
     uint32_t Y1 = Xb;
-    if (Vb == Zb) {
-      C1 |= faw >> 1;  // the runs met: window k0-1's run over [4,16) is this block's own
-    } else {
+    C1 |= met ? faw >> 1 : 0u;
+    if (!__all_sync(kFull, met)) {  // a lane whose runs did not meet: the warp steps the rest (uniformly)
       uint32_t v = Vb;
       if (!slow_bytes) {
 #pragma unroll
@@ -316,8 +318,10 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
       } else {
         v = h16_run_global(tab, a.hi, colbytes, tokens, tok0 + kConv16, 16 - kConv16, v);
       }
-      C1 |= v >= s2 ? 1u : 0u;
-      Y1 = h16_base(v, s2);
+      if (!met) {
+        C1 |= v >= s2 ? 1u : 0u;
+        Y1 = h16_base(v, s2);
+      }
     }
     const uint32_t Q = Y1 | (C1 << 16);
     // ---- window w = k0 - 2: its block (lane l-2), its phase B (lane l-1), phase C here
