@@ -4,6 +4,7 @@
 // the device (token_seq_digest in core.hpp calls the CUDA library).
 #pragma once
 
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <string_view>
@@ -22,6 +23,13 @@ class SplitMix64 {
   }
   uint64_t next_below(uint64_t bound) { return bound ? next() % bound : 0; }
   double next_double() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  // util.hpp:33-39 (Box-Muller, the reference's explicit formula)
+  double next_normal() {
+    double u1 = next_double();
+    const double u2 = next_double();
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  }
 
  private:
   uint64_t state_;

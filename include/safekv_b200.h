@@ -312,6 +312,10 @@ int skv_check_anomaly(skv_ctx* ctx, uint64_t h, uint64_t d, uint64_t epoch, skv_
 /* Per-call wrappers (batch of one, still on the device) for the facade:
  * RuleEngine::tier1_scan (detection.hpp:217) and token_seq_digest (core.hpp:68). */
 int skv_tier1_scan(skv_ctx* ctx, const char* text, size_t len, uint32_t* rule_mask);
+/* Tier-1 scan of n independent texts text[offsets[i] : offsets[i+1]] in one launch (the
+ * DetectionPipeline drain's RuleEngine::tier1_scan per pending block, detection.hpp:547-552);
+ * rule_masks[i] = enabled-rule mask of text i, as skv_tier1_scan. */
+int skv_tier1_scan_batch(skv_ctx* ctx, const char* text, const uint64_t* offsets, uint32_t n, uint32_t* rule_masks);
 int skv_token_seq_digest(skv_ctx* ctx, const uint32_t* tokens, size_t n, uint64_t* digest);
 
 /* ------------------------------------------------------------------------------

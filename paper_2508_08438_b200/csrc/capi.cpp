@@ -1993,6 +1993,37 @@ int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {
   });
 }
 
+int skv_tier1_scan_batch(skv_ctx* c, const char* text, const uint64_t* offsets, uint32_t n, uint32_t* rule_masks) {
+  if (!c || !offsets || (n && !rule_masks)) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    if (offsets[0] != 0) throw ArgError("offsets[0] must be 0");
+    for (uint32_t i = 0; i < n; ++i)
+      if (offsets[i + 1] < offsets[i]) throw ArgError("offsets must be non-decreasing");
+    const uint64_t len = offsets[n];
+    if (len && !text) throw ArgError("null text");
+    if (n == 0) return SKV_OK;
+    CK(cudaSetDevice(c->device));
+    std::vector<void*> tmp;
+    uint8_t* dt = dalloc<uint8_t>(len + 1, tmp);
+    uint64_t* doff = dalloc<uint64_t>(n + 1ull, tmp);
+    uint32_t* dm = dalloc<uint32_t>(n, tmp);
+    cudaStream_t s = c->stream;
+    try {
+      if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(doff, offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(dm, 0, n * 4ull, s));
+      for (const auto& g : c->groups) skv::launch_scan_texts(dt, doff, n, g.dev, dm, g.shift, s);
+      CK(cudaMemcpyAsync(rule_masks, dm, n * 4ull, cudaMemcpyDeviceToHost, s));
+      sync_check(s);
+    } catch (...) {
+      for (void* p : tmp) cudaFree(p);
+      throw;
+    }
+    for (void* p : tmp) cudaFree(p);
+    return SKV_OK;
+  });
+}
+
 int skv_token_seq_digest(skv_ctx* c, const uint32_t* tokens, size_t n, uint64_t* digest) {
   if (!c || (!tokens && n) || !digest) return SKV_ERR_ARG;
   return guard(c, [&] {

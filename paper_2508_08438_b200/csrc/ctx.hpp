@@ -319,6 +319,8 @@ void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, con
 void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_t* n_out, uint32_t cap,
                    cudaStream_t s);
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, uint32_t shift, cudaStream_t s);
+void launch_scan_texts(const uint8_t* text, const uint64_t* off, uint32_t n, DevRules r, uint32_t* masks,
+                       uint32_t shift, cudaStream_t s);
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s);
 uint32_t record_grid(int device);
 void launch_leak_flags(const uint32_t* blk_off, const uint8_t* label, const uint32_t* span_off, const uint64_t* sb,

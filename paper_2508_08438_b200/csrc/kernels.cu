@@ -2185,6 +2185,23 @@ __global__ void k_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint3
   *mask |= (acc >> 16) << shift;
 }
 
+// A batch of independent texts (DetectionPipeline drains: CompiledRuleSet::scan per pending
+// block, detection.hpp:148-170, 547-552): one thread per text -- pipeline texts are a block plus
+// its context, a few dozen bytes, so a text is one thread's sequential walk of the search DFA.
+__global__ void k_scan_texts(const uint8_t* __restrict__ text, const uint64_t* __restrict__ off, uint32_t n,
+                             DevRules r, uint32_t* __restrict__ masks, uint32_t shift) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t row = r.start_row, acc = 0;
+  for (uint64_t k = off[i], e = off[i + 1]; k < e; ++k) {
+    const uint32_t v = r.full[(row - r.row_base + r.class2[text[k]]) >> 1];
+    acc |= v;
+    row = v & 0xffffu;
+  }
+  acc |= r.full[(row - r.row_base + r.eos2) >> 1];
+  masks[i] |= (acc >> 16) << shift;
+}
+
 __global__ void k_digest(const uint32_t* t, uint32_t n, uint64_t* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint64_t h = fnv_u32(kFnvOff, n);
@@ -2236,10 +2253,21 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W) {
   return L;
 }
 
+// The dynamic-SMEM opt-in is a per-function attribute shared by every context and rule group of
+// the process: set it to the device maximum (occupancy follows each launch's own smem), never to
+// one group's footprint -- a later, smaller group would otherwise make a larger one fail to launch.
+static bool optin_max_smem(const void* fn, int device) {
+  int optin = 0;
+  cudaFuncAttributes fa;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess ||
+      cudaFuncGetAttributes(&fa, fn) != cudaSuccess)
+    return false;
+  const int dyn = optin - static_cast<int>(fa.sharedSizeBytes);  // the opt-in covers static + dynamic
+  return dyn > 0 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) == cudaSuccess;
+}
+
 int hash_scan_grid(int device, uint32_t smem, uint32_t threads) {
-  if (cudaFuncSetAttribute(k_hash_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-      cudaSuccess)
-    return -1;
+  if (!optin_max_smem(reinterpret_cast<const void*>(k_hash_scan), device)) return -1;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan, static_cast<int>(threads), smem) !=
       cudaSuccess)
@@ -2264,9 +2292,7 @@ uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap) {
 }
 
 int hash_scan16_grid(int device, uint32_t smem) {
-  if (cudaFuncSetAttribute(k_hash_scan16, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-      cudaSuccess)
-    return -1;
+  if (!optin_max_smem(reinterpret_cast<const void*>(k_hash_scan16), device)) return -1;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_scan16, kH16Warps * 32, smem) != cudaSuccess ||
       per_sm < 1)
@@ -2666,6 +2692,11 @@ void launch_export(const Index& ix, const uint64_t* user_rev, void* out, uint32_
 
 void launch_scan_text(const uint8_t* text, uint32_t len, DevRules r, uint32_t* mask, uint32_t shift, cudaStream_t s) {
   k_scan_text<<<1, 32, 0, s>>>(text, len, r, mask, shift);
+}
+
+void launch_scan_texts(const uint8_t* text, const uint64_t* off, uint32_t n, DevRules r, uint32_t* masks,
+                       uint32_t shift, cudaStream_t s) {
+  if (n) k_scan_texts<<<cdiv(n, 128), 128, 0, s>>>(text, off, n, r, masks, shift);
 }
 
 void launch_digest(const uint32_t* tokens, uint32_t n, uint64_t* out, cudaStream_t s) {

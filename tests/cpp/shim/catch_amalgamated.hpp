@@ -62,13 +62,20 @@ namespace Catch {
 class Approx {
  public:
   explicit Approx(double v) : v_(v) {}
+  // Catch2: within the absolute margin, or within epsilon relative to the magnitude
+  Approx& margin(double m) {
+    margin_ = m;
+    return *this;
+  }
   friend bool operator==(double a, const Approx& b) {
-    return std::fabs(a - b.v_) <= 1.1920929e-7f * 100 * (1.0 + std::max(std::fabs(a), std::fabs(b.v_)));
+    return std::fabs(a - b.v_) <= b.margin_ ||
+           std::fabs(a - b.v_) <= 1.1920929e-7f * 100 * (1.0 + std::max(std::fabs(a), std::fabs(b.v_)));
   }
   friend bool operator==(const Approx& b, double a) { return a == b; }
 
  private:
   double v_;
+  double margin_ = 0.0;
 };
 namespace Matchers {
 struct ContainsSubstring {

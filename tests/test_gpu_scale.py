@@ -38,6 +38,7 @@ def _engines(ref, c, cap_log2, window_log2=18):
 
 
 def _step(eng, re_, batch, epoch=True, export=True):
+    batch = batch[:4]  # bench.build_batch also returns the global prompt ids
     got = eng.admit(*batch)
     exp = re_.admit(*batch)
     check_admit(eng.rules, got, exp)
