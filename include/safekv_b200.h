@@ -170,6 +170,15 @@ int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
  * without prefetch; there is no reference counterpart (the reference admits one prompt at
  * a time). */
 int skv_prefetch(skv_ctx* ctx, const skv_batch* next);
+/* Host-input staging (end-to-end pipelining): queue the host->device copy of a HOST batch
+ * (tokens or token bytes, offsets, users, owners) on a copy stream into one of two device
+ * slots, so the copy of batch k+1 or k+2 overlaps the admission of batch k.  A later
+ * skv_prefetch / skv_admit of the same batch (same pointers and sizes) reads the staged copy;
+ * the caller keeps the host buffers unchanged until that admit returns.  A slot is reused once
+ * the batch admitted from it is committed (or dropped); with both slots busy the call stages
+ * nothing and the batch is copied inline later.  Pinned host memory makes the copy
+ * asynchronous.  No reference counterpart (the reference has no device). */
+int skv_stage(skv_ctx* ctx, const skv_batch* batch);
 /* Insert the new blocks of the last admitted batch (first creator wins; intra-batch
  * duplicates are won by the lowest prompt index).  new_entries may be NULL.  A capacity
  * failure detected after the kernels ran (probe sequence or monitor set pool exhausted)

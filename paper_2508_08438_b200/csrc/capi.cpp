@@ -266,6 +266,33 @@ struct skv_ctx {
   uint8_t* alt_owners = nullptr;
   uint32_t pf_n = 0;
   uint64_t pf_ntok = 0;
+
+  // host-input staging ring (skv_stage): a host batch's H2D into one of two device slots on
+  // a copy stream, ahead of its prefetch / admit, so the copy of batch k+1 runs while batch k
+  // is admitted and committed (the PCIe copy is the end-to-end bottleneck).  A slot is FREE,
+  // STAGED (copy queued), PREFETCHED (stages 1-2 queued on it) or INUSE (its users / owners
+  // are read until the batch's commit); free_ev orders the next copy after the last reader.
+  enum SlotState { kSlotFree, kSlotStaged, kSlotPrefetched, kSlotInUse };
+  struct HostSlot {
+    uint32_t* tok = nullptr;
+    uint8_t* tok8 = nullptr;
+    uint64_t* off = nullptr;
+    uint64_t* users = nullptr;
+    uint8_t* owners = nullptr;
+    cudaEvent_t ready = nullptr, free_ev = nullptr;
+    SlotState state = kSlotFree;
+    const void* id_tok = nullptr;
+    const uint64_t* id_off = nullptr;
+    const uint64_t* id_users = nullptr;
+    const uint8_t* id_owners = nullptr;
+    uint32_t n = 0;
+    uint64_t ntok = 0;
+    bool bytes = false;
+  };
+  HostSlot hslot[2];
+  cudaStream_t copy = nullptr;
+  int pf_slot = -1;   // slot of the prefetched batch
+  int use_slot = -1;  // slot of the pending (admitted) batch
 };
 
 namespace {
@@ -697,17 +724,16 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     if (prop.major != 10)
       throw CudaError("device " + std::string(prop.name) + " is not sm_100 (built for sm_100a only)");
     c->n_sm = prop.multiProcessorCount;
-#if SKV_STREAM_PRIO
-    // the batch's own work (admit, commit, epoch) ahead of the next batch's prefetch when
-    // both have CTAs waiting
-    int prio_lo = 0, prio_hi = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
-    CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
-#else
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-#endif
+    {
+      // SKV_STREAM_PRIO (diagnostic): 1 = the batch's own work (admit, commit, epoch) ahead of the
+      // next batch's prefetch when both have CTAs waiting, 2 = the prefetch ahead
+      const char* pe = std::getenv("SKV_STREAM_PRIO");
+      const int mode = pe ? std::atoi(pe) : SKV_STREAM_PRIO;
+      int prio_lo = 0, prio_hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+      CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, mode == 1 ? prio_hi : prio_lo));
+      CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, mode == 2 ? prio_hi : prio_lo));
+    }
     CK(cudaStreamCreateWithFlags(&c->rec_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->rec_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->rec_done, cudaEventDisableTiming));
@@ -821,8 +847,59 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   return SKV_OK;
 }
 
+int find_staged(skv_ctx* c, const skv_batch* b);
+void unprefetch_slot(skv_ctx* c);
+
+int skv_stage(skv_ctx* c, const skv_batch* b) {
+  if (!c || !b) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (b->on_device) throw ArgError("skv_stage: host batches only");
+    const uint32_t N = b->n_prompts;
+    if (N > c->max_prompts) throw ArgError("n_prompts exceeds max_prompts");
+    if (b->n_tokens > c->max_tokens) throw ArgError("n_tokens exceeds max_tokens");
+    if (N == 0 || (!b->tokens && !b->token_bytes) || !b->offsets || !b->users) return SKV_OK;
+    if (find_staged(c, b) >= 0) return SKV_OK;
+    int si = -1;
+    for (int i = 0; i < 2 && si < 0; ++i)
+      if (c->hslot[i].state == skv_ctx::kSlotFree) si = i;
+    if (si < 0) return SKV_OK;  // both slots busy: the prefetch / admit copies it inline
+    auto& hs = c->hslot[si];
+    if (!c->copy) CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    if (!hs.tok) {
+      hs.tok = dalloc<uint32_t>(c->max_tokens + 4, c->owned);
+      hs.tok8 = dalloc<uint8_t>(c->max_tokens + 16, c->owned);
+      hs.off = dalloc<uint64_t>(c->max_prompts + 1, c->owned);
+      hs.users = dalloc<uint64_t>(c->max_prompts, c->owned);
+      hs.owners = dalloc<uint8_t>(c->max_prompts, c->owned);
+      CK(cudaEventCreateWithFlags(&hs.ready, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&hs.free_ev, cudaEventDisableTiming));
+    }
+    cudaStream_t cs = c->copy;
+    CK(cudaStreamWaitEvent(cs, hs.free_ev, 0));  // the slot's last reader (a previous batch's commit)
+    if (b->token_bytes)
+      CK(cudaMemcpyAsync(hs.tok8, b->token_bytes, b->n_tokens, cudaMemcpyHostToDevice, cs));
+    else
+      CK(cudaMemcpyAsync(hs.tok, b->tokens, b->n_tokens * 4, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(hs.off, b->offsets, (N + 1) * 8ull, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(hs.users, b->users, N * 8ull, cudaMemcpyHostToDevice, cs));
+    if (b->owners) CK(cudaMemcpyAsync(hs.owners, b->owners, N, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(hs.ready, cs));
+    hs.state = skv_ctx::kSlotStaged;
+    hs.id_tok = b->token_bytes ? static_cast<const void*>(b->token_bytes) : b->tokens;
+    hs.id_off = b->offsets;
+    hs.id_users = b->users;
+    hs.id_owners = b->owners;
+    hs.n = N;
+    hs.ntok = b->n_tokens;
+    hs.bytes = b->token_bytes != nullptr;
+    return SKV_OK;
+  });
+}
+
 int skv_destroy(skv_ctx* c) {
   if (!c) return SKV_ERR_ARG;
+  if (c->copy) cudaStreamSynchronize(c->copy);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->side) cudaStreamSynchronize(c->side);
   if (c->rec_stream) cudaStreamSynchronize(c->rec_stream);
@@ -845,6 +922,11 @@ int skv_destroy(skv_ctx* c) {
     for (auto ev : pr)
       if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
+  for (auto& h : c->hslot) {
+    if (h.ready) cudaEventDestroy(h.ready);
+    if (h.free_ev) cudaEventDestroy(h.free_ev);
+  }
+  if (c->copy) cudaStreamDestroy(c->copy);
   delete c;
   return SKV_OK;
 }
@@ -856,6 +938,7 @@ int skv_set_rules(skv_ctx* c, const skv_rules* r) {
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     if (c->pf_valid) CK(cudaStreamSynchronize(c->side));
+    if (c->pf_valid) unprefetch_slot(c);
     c->pf_valid = false;  // a staged scan used the previous rule snapshot
     upload_rules(c, *r);
     return SKV_OK;
@@ -919,6 +1002,34 @@ void ensure_admit_resolved(skv_ctx* c) {
   resolve_admit(c);
 }
 
+// ------------------------------------------------------------------ host staging ring
+int find_staged(skv_ctx* c, const skv_batch* b) {
+  const void* tok = b->token_bytes ? static_cast<const void*>(b->token_bytes) : b->tokens;
+  for (int i = 0; i < 2; ++i) {
+    const auto& h = c->hslot[i];
+    if (h.state == skv_ctx::kSlotStaged && h.id_tok == tok && h.id_off == b->offsets && h.id_users == b->users &&
+        h.id_owners == b->owners && h.n == b->n_prompts && h.ntok == b->n_tokens && h.bytes == (b->token_bytes != nullptr))
+      return i;
+  }
+  return -1;
+}
+
+// the pending batch no longer reads its slot once the kernels queued so far have run
+void release_slot(skv_ctx* c) {
+  if (c->use_slot < 0) return;
+  auto& h = c->hslot[c->use_slot];
+  CK(cudaEventRecord(h.free_ev, c->stream));
+  h.state = skv_ctx::kSlotFree;
+  c->use_slot = -1;
+}
+
+// a dropped prefetch leaves its staged copy usable
+void unprefetch_slot(skv_ctx* c) {
+  if (c->pf_slot >= 0 && c->hslot[c->pf_slot].state == skv_ctx::kSlotPrefetched)
+    c->hslot[c->pf_slot].state = skv_ctx::kSlotStaged;
+  c->pf_slot = -1;
+}
+
 int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
@@ -931,6 +1042,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     if (c->rep_sync_due) throw StateError("replicated layer: skv_replica_export / skv_replica_apply of the last batch first");
     ensure_admit_resolved(c);
     flush_record(c);  // the previous batch was admitted but not committed
+    release_slot(c);
     c->dropped_by_evict = false;
     if (N == 0) {
       if (out) out->n_blocks = 0, out->matched_total = 0;
@@ -952,10 +1064,35 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     const bool use_pf = c->pf_valid && c->pf_on_device == (b->on_device != 0) && c->pf_tokens == tok_id &&
                         c->pf_offsets == b->offsets && c->pf_users == b->users && c->pf_owners == b->owners &&
                         c->pf_n == N && c->pf_ntok == b->n_tokens;
-    if (c->pf_valid && !use_pf) CK(cudaStreamSynchronize(c->side));  // stale prefetch: drop it
+    if (c->pf_valid && !use_pf) {  // stale prefetch: drop it
+      CK(cudaStreamSynchronize(c->side));
+      unprefetch_slot(c);
+    }
     c->pf_valid = false;
     CK(cudaEventRecord(c->ev[0], s));
+    // the host batch's H2D already queued by skv_stage (and its stages 1-2 by skv_prefetch)?
+    int si = -1;
     if (!b->on_device) {
+      if (use_pf)
+        si = c->pf_slot;
+      else
+        si = find_staged(c, b);
+    }
+    c->pf_slot = -1;
+    if (si >= 0) {
+      n_blocks = host_block_count(b, B);
+      auto& hs = c->hslot[si];
+      if (!use_pf) {
+        CK(cudaStreamWaitEvent(s, hs.ready, 0));
+        if (hs.bytes) skv::launch_widen(hs.tok8, hs.tok, b->n_tokens, s);
+      }
+      tokens = hs.tok;
+      off = hs.off;
+      users = hs.users;
+      owners = b->owners ? hs.owners : nullptr;
+      hs.state = skv_ctx::kSlotInUse;
+      c->use_slot = si;
+    } else if (!b->on_device) {
       n_blocks = host_block_count(b, B);
       if (use_pf) {
         std::swap(c->d_tokens, c->alt_tokens);
@@ -1173,7 +1310,10 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    if (c->pf_valid) CK(cudaStreamSynchronize(c->side));
+    if (c->pf_valid) {
+      CK(cudaStreamSynchronize(c->side));
+      unprefetch_slot(c);
+    }
     c->pf_valid = false;
     const uint32_t N = b->n_prompts;
     // anything the pipeline cannot stage is admitted inline by skv_admit (which also
@@ -1185,7 +1325,21 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
     const uint32_t* tokens = b->tokens;
     const uint64_t* off = b->offsets;
     uint64_t nb_hint = 0;
-    if (!b->on_device) {
+    const int si = b->on_device ? -1 : find_staged(c, b);
+    if (si >= 0) {  // copied by skv_stage: stages 1-2 wait for the copy on the device
+      try {
+        nb_hint = host_block_count(b, c->cfg.block_tokens);
+      } catch (const ArgError&) {
+        return SKV_OK;
+      }
+      auto& hs = c->hslot[si];
+      CK(cudaStreamWaitEvent(st, hs.ready, 0));
+      if (hs.bytes) skv::launch_widen(hs.tok8, hs.tok, b->n_tokens, st);
+      tokens = hs.tok;
+      off = hs.off;
+      hs.state = skv_ctx::kSlotPrefetched;
+      c->pf_slot = si;
+    } else if (!b->on_device) {
       // host batch: H2D into the alternate staging set on the side stream
       try {
         nb_hint = host_block_count(b, c->cfg.block_tokens);
@@ -1248,6 +1402,13 @@ int skv_prefetch(skv_ctx* c, const skv_batch* b) {
   });
 }
 
+// SMs the persistent commit grid is sized for (SKV_COMMIT_SMS, diagnostic: leave SMs to a
+// prefetch running beside it)
+int commit_sms(const skv_ctx* c) {
+  static const int env = std::getenv("SKV_COMMIT_SMS") ? std::atoi(std::getenv("SKV_COMMIT_SMS")) : 0;
+  return env > 0 ? std::min(env, c->n_sm) : c->n_sm;
+}
+
 int skv_commit(skv_ctx* c, uint64_t* new_entries) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
@@ -1258,6 +1419,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     CK(cudaSetDevice(c->device));
     cudaStream_t s = c->stream;
     if (c->p_n == 0) {
+      release_slot(c);
       c->pending = false;
       c->rep_sync_due = c->ix.rep.depth != 0;  // an empty share still takes part in the merge
       if (new_entries) *new_entries = 0;
@@ -1297,7 +1459,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
                        c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
                        static_cast<int>(c->rec_grid), c->matched, c->rec_users,
                        rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
-                       c->n_sm, c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
+                       commit_sms(c), c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
     if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
     uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
     if (c->evict_on) launched += 2;
@@ -1320,6 +1482,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       c->entries += nn + revived;
       c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
       c->node_next += nn + revived;
+      release_slot(c);
       c->pending = false;
       c->rec_pending = false;
       if (c->adm_lazy) c->adm_lazy = false, c->p_blocks = c->host_small[20];
@@ -1350,6 +1513,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
     c->times.kernels_launched += launched;
     c->times.new_blocks = nn;
+    release_slot(c);
     c->pending = false;
     c->rep_sync_due = c->ix.rep.depth != 0;
     if (new_entries) *new_entries = nn;
@@ -1566,6 +1730,7 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     c->pending = false;
     ensure_admit_resolved(c);
     flush_record(c);
+    release_slot(c);
     cudaStream_t s = c->stream;
     if (!c->ev_eff) {  // per-slot effective keys, on first use
       c->ev_eff = dalloc<unsigned long long>(c->ix.cap, c->owned);

@@ -263,6 +263,10 @@ class AdmissionEngine:
         b = N.Batch(_ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), len(arrs[1]) - 1, len(arrs[0]), 0)
         self._check(self._lib.skv_prefetch(self._h, C.byref(b)))
 
+    def stage_raw(self, batch: N.Batch) -> None:
+        """skv_stage: queue the host->device copy of a host batch ahead of its prefetch / admit."""
+        self._check(self._lib.skv_stage(self._h, C.byref(batch)))
+
     def prefetch_raw(self, batch: N.Batch) -> None:
         """skv_prefetch with caller-owned (device or host) pointers."""
         self._check(self._lib.skv_prefetch(self._h, C.byref(batch)))

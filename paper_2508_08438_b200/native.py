@@ -187,6 +187,7 @@ SIGNATURES = {
     "skv_leak_flags": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.POINTER(C.c_uint64)]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
+    "skv_stage": (C.c_int, [C.c_void_p, C.c_void_p]),
     "skv_tier1_scan_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "skv_set_replicated_depth": (C.c_int, [C.c_void_p, C.c_uint32]),
