@@ -246,6 +246,18 @@ uint64_t skv_entry_count(skv_ctx* ctx);
  * SKV_ERR_CAPACITY, after freeing every candidate, when fewer than needed_blocks could
  * be freed. */
 int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
+/* TierBudget (cache_index.hpp:26-55) in blocks, with the reference's insert-time make_room
+ * (cache_index.hpp:183-190, 801-806) -- SURVEY Appendix A.9: every prompt's matched path stays
+ * pinned from its lookup until the batch's commit ends (ServingSimulator::submit pins,
+ * serving_sim.hpp:195-215); the commit inserts the prompts in order, each first evicting unpinned
+ * leaves in the reference's victim order until its new blocks fit the HBM budget; a prompt that
+ * cannot make room is dropped (nothing inserted, CapacityExhausted in the reference -- listed by
+ * skv_last_drops) and the commit continues.  Needs skv_enable_eviction (untiered); call before
+ * the first admit.  skv_tier_usage: used / capacity blocks per tier (HBM, DRAM, SSD). */
+int skv_set_tier_budget(skv_ctx* ctx, uint64_t hbm_blocks, uint64_t dram_blocks, uint64_t ssd_blocks);
+int skv_tier_usage(skv_ctx* ctx, uint64_t* used3, uint64_t* cap3);
+/* Prompts (indices into the last committed batch, ascending) whose insert could not make room. */
+int skv_last_drops(skv_ctx* ctx, uint32_t* prompts, size_t cap, size_t* n);
 int skv_evict(skv_ctx* ctx, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap);
 /* An admitted but uncommitted batch is dropped by skv_evict (its lookups and monitor records

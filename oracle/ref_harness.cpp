@@ -274,6 +274,8 @@ struct RefEngine {
   int nthreads = 1;
   int stock_scan = 0;  // 1: one CompiledRuleSet::scan per window (bench reference arm)
   bool pending_labels = false;  // commit leaves new nodes PendingPrivate (insert's label)
+  bool budgeted = false;        // A.9: a bounded HBM budget (insert-time make_room)
+  std::vector<uint32_t> dropped;  // prompts of the last commit whose insert raised CapacityExhausted
 };
 
 void* ref_engine_create(void* rules, uint32_t B, uint32_t W, double jump, uint64_t u_pre_max) {
@@ -309,6 +311,40 @@ int ref_engine_set_tiered(void* ev, int tiered) {
   e->idx = std::make_unique<RadixCacheIndex>(cfg);
   e->mon = std::make_unique<EntropyMonitor>(*e->idx, mc);
   return 0;
+}
+
+// A.9 (bounded budgets): RadixCacheIndex::Config::budget = TierBudget::from_tokens(hbm, dram, ssd)
+// in blocks (one interned token per block), before any insert.  The commit then runs the
+// serving contract of ServingSimulator::submit (serving_sim.hpp:195-215) for the batch: every
+// prompt's matched path stays pinned from its lookup until the batch's inserts are done, each
+// insert makes room for its new blocks (cache_index.hpp:183-190, 801-806: evicting unpinned
+// leaves), and an insert that cannot make room raises CapacityExhausted -- that prompt is dropped
+// (nothing inserted) and the next one is inserted.
+int ref_engine_set_budget(void* ev, uint64_t hbm, uint64_t dram, uint64_t ssd, int tiered) {
+  auto* e = static_cast<RefEngine*>(ev);
+  if (!e->pending.empty()) return -1;
+  MonitorConfig mc = e->mcfg;
+  e->mon.reset();
+  RadixCacheIndex::Config cfg;
+  cfg.budget = TierBudget::from_tokens(hbm, dram, ssd);
+  cfg.tiered_demotion = tiered != 0;
+  e->idx = std::make_unique<RadixCacheIndex>(cfg);
+  e->mon = std::make_unique<EntropyMonitor>(*e->idx, mc);
+  e->budgeted = true;
+  return 0;
+}
+
+// prompts dropped by the last commit (A.9), ascending
+size_t ref_engine_dropped(void* ev, uint32_t* out, size_t cap) {
+  auto* e = static_cast<RefEngine*>(ev);
+  for (size_t i = 0; i < e->dropped.size() && i < cap; ++i) out[i] = e->dropped[i];
+  return e->dropped.size();
+}
+
+// the index's used tokens (= blocks) per tier
+void ref_engine_budget_used(void* ev, uint64_t* used3) {
+  auto* e = static_cast<RefEngine*>(ev);
+  for (int t = 0; t < 3; ++t) used3[t] = e->idx->budget().used(static_cast<MemTier>(t));
 }
 
 void ref_engine_set_threads(void* e, int n) { static_cast<RefEngine*>(e)->nthreads = n; }
@@ -460,11 +496,31 @@ int ref_engine_resolve(void* ev, const uint32_t* tok, const uint64_t* off, uint3
 // Phase C (A.7): insert in prompt order, one node per block, labels applied per block.
 int ref_engine_commit(void* ev) {
   auto* e = static_cast<RefEngine*>(ev);
+  e->dropped.clear();
+  // A.9: the batch's matched paths stay pinned through its inserts (serving_sim.hpp:196,215)
+  std::vector<NodeRef> pins;
+  if (e->budgeted)
+    for (auto& sv : e->served)
+      for (NodeRef n : sv.m.path) {
+        e->idx->pin(n);
+        pins.push_back(n);
+      }
+  uint32_t pi = 0;
   for (auto& pd : e->pending) {
+    const uint32_t p = pi++;
     size_t n = pd.ids.size();
     if (n == 0) continue;
     uint32_t fresh = 0;
-    e->idx->insert(pd.ids, pd.user, pd.owner, e->idx->current_epoch(), &fresh);
+    if (e->budgeted) {
+      try {
+        e->idx->insert(pd.ids, pd.user, pd.owner, e->idx->current_epoch(), &fresh);
+      } catch (const CapacityExhausted&) {
+        e->dropped.push_back(p);
+        continue;
+      }
+    } else {
+      e->idx->insert(pd.ids, pd.user, pd.owner, e->idx->current_epoch(), &fresh);
+    }
     if (fresh == 0) continue;
     size_t k0 = n - fresh;
     for (size_t k = k0 + 1; k < n; ++k) e->idx->ensure_boundary(pd.ids, k);
@@ -479,6 +535,7 @@ int ref_engine_commit(void* ev) {
         e->idx->set_label(nd, SensitivityLabel::Private, true);
     }
   }
+  for (NodeRef n : pins) e->idx->unpin(n);
   e->pending.clear();
   return 0;
 }

@@ -291,6 +291,23 @@ struct skv_ctx {
   };
   HostSlot hslot[2];
   cudaStream_t copy = nullptr;
+
+  // A.9 tier budgets (skv_set_tier_budget): capacities and used blocks per tier; the commit then
+  // makes room for each insert (kernels.cu "A.9")
+  bool budget_on = false;
+  uint64_t bud_cap[3] = {0, 0, 0}, bud_used[3] = {0, 0, 0};
+  uint32_t* vstamp = nullptr;  // per slot: 0 pinned, p + 1 first walking prompt, ~0 none
+  uint32_t* mark_list = nullptr;
+  uint32_t* n_mark = nullptr;
+  uint32_t mark_cap = 0;
+  ulonglong2* dry_tab = nullptr;
+  uint32_t* dry_minp = nullptr;
+  uint64_t dry_cap = 0;
+  uint32_t* dry_slot = nullptr;
+  uint32_t* needed = nullptr;
+  skv::BudgetSim* sim = nullptr;
+  unsigned long long* nb_dev = nullptr;
+  std::vector<uint32_t> dropped;  // prompts of the last commit whose insert could not make room
   int pf_slot = -1;   // slot of the prefetched batch
   int use_slot = -1;  // slot of the pending (admitted) batch
 };
@@ -1409,6 +1426,116 @@ int commit_sms(const skv_ctx* c) {
   return env > 0 ? std::min(env, c->n_sm) : c->n_sm;
 }
 
+// ------------------------------------------------------------------ A.9 budgeted commit
+// Commit of prompts [lo, end) of the pending batch (its monitor records already applied):
+// claims + fix-ups, exact node ids, insert-walk epochs.  Returns the entries created.
+uint64_t commit_range(skv_ctx* c, uint32_t lo, uint32_t end) {
+  if (end <= lo) return 0;
+  cudaStream_t s = c->stream;
+  const uint32_t n = end - lo;
+  const uint32_t ep32 = static_cast<uint32_t>(c->epoch);
+  CK(cudaMemsetAsync(c->n_new, 0, 8, s));
+  CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));
+  CK(cudaMemsetAsync(c->counters + 11, 0, 8, s));
+  skv::Index ixc = c->ix;
+  skv::launch_node_bases(c->blk_off + lo, c->exist + lo, n, c->ev_counts, c->ev_incl, c->ev_temp, c->ev_temp_bytes, s);
+  ixc.em_base = c->ev_incl;
+  ixc.em_next = static_cast<uint32_t>(c->node_next);
+  ixc.em_epoch = ep32;
+  skv::launch_commit(ixc, c->bh, c->bd, c->blk_off + lo, c->exist + lo, c->blabel, c->uidx + lo,
+                     c->p_owners ? c->p_owners + lo : nullptr, n, c->bslot, c->n_new, c->fix_list, c->counters + 7,
+                     static_cast<uint32_t>(c->max_blocks), c->counters + 5, static_cast<int>(c->rec_grid),
+                     c->matched + lo, c->rec_users + lo, nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
+                     commit_sms(c), c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
+  CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
+  sync_check(s);
+  unsigned long long nn = 0;
+  std::memcpy(&nn, c->host_small, 8);
+  const uint32_t err = c->host_small[4], revived = c->host_small[6];
+  c->entries += nn + revived;
+  c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
+  if (err) {
+    c->node_next += nn + revived;
+    const char* why = (err & 2u) ? "index probe sequence exhausted" : "commit fix-up list overflow";
+    c->poisoned = why;
+    throw CapacityError(why);
+  }
+  skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off + lo, c->exist + lo, n, c->ev_counts, c->ev_incl, c->node_next,
+                           c->ev_temp, c->ev_temp_bytes, s);
+  skv::launch_path_epochs(c->ix, c->bslot, c->blk_off + lo, c->exist + lo, n, ep32, s);
+  c->node_next += nn + revived;
+  return nn + revived;
+}
+
+// The pending batch's commit under a bounded HBM budget (A.9): rounds over prompt ranges, each
+// inserting its prompts with the victims their make_room takes (kernels.cu "A.9").
+void commit_budgeted(skv_ctx* c) {
+  cudaStream_t s = c->stream;
+  const uint32_t N = c->p_n;
+  const uint32_t E = static_cast<uint32_t>(c->epoch);
+  ensure_admit_resolved(c);
+  flush_record(c);  // the batch's accesses (prompt order) before its inserts
+  c->dropped.clear();
+  uint32_t lo = 0;
+  while (lo < N) {
+    if (lo > 0) skv::launch_reprobe(c->ix, c->bh, c->bd, c->blk_off, lo, N, c->exist, c->bslot, s);
+    skv::launch_new_bound(c->blk_off, c->exist, lo, N, c->nb_dev, s);
+    CK(cudaMemcpyAsync(c->host_small, c->nb_dev, 8, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    uint64_t bound = 0;
+    std::memcpy(&bound, c->host_small, 8);
+    uint32_t end = N, next = N, dropped = skv::kNone, nvict = 0;
+    if (c->bud_used[0] + bound > c->bud_cap[0]) {
+      CK(cudaMemsetAsync(c->n_mark, 0, 4, s));
+      skv::launch_mark_paths(c->bslot, c->blk_off, c->exist, c->matched, lo, N, c->vstamp, c->mark_list, c->n_mark,
+                             c->mark_cap, s);
+      skv::launch_dry_needed(c->bh, c->bd, c->blk_off, c->exist, lo, N, c->dry_tab, c->dry_minp, c->dry_cap,
+                             c->dry_slot, c->needed, s);
+      std::vector<void*> tmp;
+      try {
+        const uint64_t L = std::max<uint64_t>(c->entries, 1);
+        auto* keys_a = dalloc<unsigned long long>(L, tmp);
+        auto* keys_b = dalloc<unsigned long long>(L, tmp);
+        auto* vals_a = dalloc<uint32_t>(L, tmp);
+        auto* vals_b = dalloc<uint32_t>(L, tmp);
+        auto* victims = dalloc<uint32_t>(L, tmp);
+        const uint32_t nv = skv::launch_evict_order(c->ix, c->vstamp, c->ev_eff, keys_a, keys_b, vals_a, vals_b,
+                                                    c->ev_n, c->ev_temp, c->ev_temp_bytes, c->host_small, s);
+        skv::launch_budget_sim(c->needed, lo, N, c->bud_used[0], c->bud_cap[0], vals_a, nv, c->ev_eff, c->vstamp, E,
+                               victims, c->sim, s);
+        CK(cudaMemcpyAsync(c->host_small, c->sim, sizeof(skv::BudgetSim), cudaMemcpyDeviceToHost, s));
+        sync_check(s);
+        skv::BudgetSim r;
+        std::memcpy(&r, c->host_small, sizeof(r));
+        nvict = r.n_victims;
+        next = r.next_lo;
+        dropped = r.dropped;
+        end = dropped != skv::kNone ? dropped : next;
+        skv::launch_clear_marks(c->vstamp, c->mark_list, c->n_mark, c->mark_cap, s);
+        skv::launch_evict_mark_list(c->ix, victims, nvict, s);
+        sync_check(s);
+      } catch (...) {
+        for (void* p : tmp) cudaFree(p);
+        throw;
+      }
+      for (void* p : tmp) cudaFree(p);
+      c->entries -= nvict;
+      c->tombstones += nvict;
+      c->bud_used[0] -= nvict;
+    }
+    const uint64_t made = commit_range(c, lo, end);
+    c->bud_used[0] += made;
+    if (dropped != skv::kNone) {  // its walk ran before make_room raised (cache_index.hpp:156-176)
+      skv::launch_path_epochs(c->ix, c->bslot, c->blk_off + dropped, c->exist + dropped, 1, E, s);
+      c->dropped.push_back(dropped);
+    }
+    if (next <= lo) throw StateError("budgeted commit made no progress");  // cannot happen (kernels.cu A.9)
+    lo = next;
+  }
+}
+
 int skv_commit(skv_ctx* c, uint64_t* new_entries) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
@@ -1427,6 +1554,22 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     }
     if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
       throw CapacityError("index capacity exhausted (eviction is not part of this path)");
+    if (c->budget_on) {
+      CK(cudaEventRecord(c->ev[5], s));
+      const uint64_t before = c->entries + c->tombstones;
+      const uint64_t made0 = c->node_next;
+      ++c->batch_id;
+      commit_budgeted(c);
+      CK(cudaEventRecord(c->ev[6], s));
+      sync_check(s);
+      c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
+      c->times.new_blocks = c->node_next - made0;
+      (void)before;
+      release_slot(c);
+      c->pending = false;
+      if (new_entries) *new_entries = c->times.new_blocks;
+      return SKV_OK;
+    }
     CK(cudaEventRecord(c->ev[5], s));
     CK(cudaMemsetAsync(c->n_new, 0, 8, s));
     CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
@@ -1510,6 +1653,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
     c->entries += nn + revived;
     c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
     nn += revived;
+    c->bud_used[0] += nn;
     c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
     c->times.kernels_launched += launched;
     c->times.new_blocks = nn;
@@ -1654,6 +1798,13 @@ int skv_set_tiers(skv_ctx* c, const uint64_t* h, const uint64_t* d, const uint32
     CK(cudaMemcpyAsync(dt, tiers, n, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(db, block_offsets, (n_prompts + 1ull) * 4, cudaMemcpyHostToDevice, s));
     skv::launch_set_tiers(c->ix, dh, dd, db, n_prompts, dt, static_cast<uint32_t>(n), s);
+    if (c->budget_on) {  // tier moves are accounted (not capacity-checked): recount the live entries
+      auto* cnt = dalloc<unsigned long long>(3, tmp);
+      skv::launch_count_tiers(c->ix, cnt, s);
+      CK(cudaMemcpyAsync(c->host_small, cnt, 24, cudaMemcpyDeviceToHost, s));
+      sync_check(s);
+      std::memcpy(c->bud_used, c->host_small, 24);
+    }
     sync_check(s);
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;
@@ -1712,6 +1863,60 @@ int skv_enable_eviction(skv_ctx* c, int tiered_demotion) {
   });
 }
 
+int skv_set_tier_budget(skv_ctx* c, uint64_t hbm_blocks, uint64_t dram_blocks, uint64_t ssd_blocks) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    if (!c->evict_on) throw StateError("skv_set_tier_budget needs eviction (skv_enable_eviction first)");
+    if (c->evict_tiered)
+      throw skv::ConfigError("tier budgets with tiered demotion (bounded DRAM/SSD cascade) are not supported");
+    if (c->entries || c->batch_id || c->pending) throw StateError("skv_set_tier_budget must precede the first admit");
+    if (!c->budget_on) {
+      c->vstamp = dalloc<uint32_t>(c->ix.cap, c->owned);
+      CK(cudaMemsetAsync(c->vstamp, 0xff, c->ix.cap * 4, c->stream));
+      c->mark_cap = static_cast<uint32_t>(std::min<uint64_t>(c->max_blocks + 1, 0xffffffffull));
+      c->mark_list = dalloc<uint32_t>(c->mark_cap, c->owned);
+      c->n_mark = dalloc<uint32_t>(1, c->owned);
+      uint64_t dc = 1024;
+      while (dc < 2 * c->max_blocks) dc <<= 1;
+      c->dry_cap = dc;
+      c->dry_tab = dalloc<ulonglong2>(dc, c->owned);
+      c->dry_minp = dalloc<uint32_t>(dc, c->owned);
+      c->dry_slot = dalloc<uint32_t>(c->max_blocks + 1, c->owned);
+      c->needed = dalloc<uint32_t>(c->max_prompts + 1, c->owned);
+      c->sim = dalloc<skv::BudgetSim>(1, c->owned);
+      c->nb_dev = dalloc<unsigned long long>(1, c->owned);
+      if (!c->ev_eff) {
+        c->ev_eff = dalloc<unsigned long long>(c->ix.cap, c->owned);
+        c->ev_n = dalloc<uint32_t>(1, c->owned);
+      }
+      sync_check(c->stream);
+    }
+    c->bud_cap[0] = hbm_blocks;
+    c->bud_cap[1] = dram_blocks;
+    c->bud_cap[2] = ssd_blocks;
+    c->budget_on = true;
+    return SKV_OK;
+  });
+}
+
+int skv_tier_usage(skv_ctx* c, uint64_t* used3, uint64_t* cap3) {
+  if (!c) return SKV_ERR_ARG;
+  for (int t = 0; t < 3; ++t) {
+    if (used3) used3[t] = c->bud_used[t];
+    if (cap3) cap3[t] = c->bud_cap[t];
+  }
+  return SKV_OK;
+}
+
+int skv_last_drops(skv_ctx* c, uint32_t* prompts, size_t cap, size_t* n) {
+  if (!c || !n) return SKV_ERR_ARG;
+  *n = c->dropped.size();
+  if (prompts)
+    for (size_t i = 0; i < c->dropped.size() && i < cap; ++i) prompts[i] = c->dropped[i];
+  return SKV_OK;
+}
+
 int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap) {
   (void)epoch;  // the victim order only compares access epochs (epoch - access_epoch, cache_index.hpp:709)
@@ -1756,6 +1961,7 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     if (!c->evict_tiered) {
       c->entries -= v;
       c->tombstones += v;
+      c->bud_used[0] -= std::min<uint64_t>(c->bud_used[0], v);
     }
     *n_evicted = v;
     if (v < needed_blocks) throw CapacityError("evict: no unpinned candidate leaf");

@@ -251,6 +251,30 @@ void launch_assign_nodes(const Index& ix, const uint32_t* slot, const uint32_t* 
                          uint32_t n, uint32_t* counts, uint32_t* incl, uint64_t next_id, void* temp,
                          size_t temp_bytes, cudaStream_t s);
 size_t evict_temp_bytes(uint32_t n_prompts, uint64_t cap);
+// A.9 budgeted commit (kernels.cu)
+struct BudgetSim {
+  unsigned long long used;  // HBM blocks after the round
+  uint32_t n_victims, next_lo, dropped, pad;
+};
+void launch_new_bound(const uint32_t* blk_off, const uint32_t* exist, uint32_t lo, uint32_t hi,
+                      unsigned long long* out, cudaStream_t s);
+void launch_mark_paths(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist, const uint32_t* matched,
+                       uint32_t lo, uint32_t hi, uint32_t* vstamp, uint32_t* list, uint32_t* n_list, uint32_t cap,
+                       cudaStream_t s);
+void launch_clear_marks(uint32_t* vstamp, const uint32_t* list, const uint32_t* n_list, uint32_t cap, cudaStream_t s);
+void launch_reprobe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off, uint32_t lo,
+                    uint32_t hi, uint32_t* exist, uint32_t* slot_out, cudaStream_t s);
+void launch_dry_needed(const uint64_t* h, const uint64_t* d, const uint32_t* blk_off, const uint32_t* exist,
+                       uint32_t lo, uint32_t hi, ulonglong2* tab, uint32_t* minp, uint64_t tcap, uint32_t* dslot,
+                       uint32_t* needed, cudaStream_t s);
+uint32_t launch_evict_order(const Index& ix, const uint32_t* vstamp, unsigned long long* eff,
+                            unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                            uint32_t* n_live, void* temp, size_t temp_bytes, uint32_t* host_n, cudaStream_t s);
+void launch_budget_sim(const uint32_t* needed, uint32_t lo, uint32_t hi, uint64_t used, uint64_t cap,
+                       const uint32_t* vals, uint32_t nv, const unsigned long long* eff, const uint32_t* vstamp,
+                       uint32_t epoch, uint32_t* victims, BudgetSim* out, cudaStream_t s);
+void launch_evict_mark_list(const Index& ix, const uint32_t* vals, uint32_t v, cudaStream_t s);
+void launch_count_tiers(const Index& ix, unsigned long long* out3, cudaStream_t s);
 uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
                       unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
                       size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, int tiered,

@@ -3235,3 +3235,279 @@ void launch_widen(const uint8_t* in, uint32_t* out, uint64_t n, cudaStream_t s) 
   if (n) k_widen<<<static_cast<uint32_t>((n + 16 * 256 - 1) / (16 * 256)), 256, 0, s>>>(in, out, n);
 }
 }  // namespace skv
+
+// =================================================================================
+// A.9: insert-time make_room under a bounded HBM budget (cache_index.hpp:183-190,
+// 801-806; serving pins, serving_sim.hpp:195-215).  The batch commits in rounds over
+// prompt ranges [lo, next): per round a dry claim pass gives every prompt the blocks it
+// would create (lowest prompt wins a key), the victim order V is the untiered eviction
+// order of the entries no prompt of the batch has matched (pinned), and one thread walks
+// the prompts in order, taking victims from V for each prompt's make_room.  A round ends
+// early where V stops being the reference's order: an eviction cutting a later prompt's
+// insert walk (it re-walks next round), or a victim of the current epoch (this batch's own
+// nodes compete with it) after the round's first prompt.  Every round commits >= 1 prompt.
+// =================================================================================
+namespace skv {
+namespace {
+constexpr uint32_t kStampNone = 0xffffffffu;
+
+__global__ void k_new_bound(const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist, uint32_t lo,
+                            uint32_t hi, unsigned long long* out) {
+  const uint32_t p = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = 0;
+  if (p < hi) {
+    const uint32_t n = blk_off[p + 1] - blk_off[p];
+    v = n - min(exist[p], n);
+  }
+  v = __reduce_add_sync(kFull, v);
+  if (lane_id() == 0 && v) atomicAdd(out, static_cast<unsigned long long>(v));
+}
+
+// pinned (matched by any prompt of the batch) = 0; walked by prompt p in [lo, hi) = p + 1 (the
+// first such p); every newly marked slot is listed for clearing
+__device__ __forceinline__ void mark_slot(uint32_t* vstamp, uint32_t s, uint32_t v, uint32_t* list, uint32_t* n_list,
+                                          uint32_t cap) {
+  const uint32_t old = atomicMin(&vstamp[s], v);
+  if (old == kStampNone) {
+    const uint32_t i = atomicAdd(n_list, 1u);
+    if (i < cap) list[i] = s;
+  }
+}
+
+__global__ void k_mark_paths(const uint32_t* __restrict__ slot, const uint32_t* __restrict__ blk_off,
+                             const uint32_t* __restrict__ exist, const uint32_t* __restrict__ matched, uint32_t lo,
+                             uint32_t hi, uint32_t* vstamp, uint32_t* list, uint32_t* n_list, uint32_t cap) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= hi) return;
+  const uint32_t bo = blk_off[p], m = matched[p], k = p >= lo ? exist[p] : m;
+  for (uint32_t b = lane_id(); b < k; b += 32) mark_slot(vstamp, slot[bo + b], b < m ? 0u : p + 1, list, n_list, cap);
+}
+
+__global__ void k_clear_marks(uint32_t* vstamp, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
+                              uint32_t cap) {
+  const uint32_t n = min(*n_list, cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    vstamp[list[i]] = kStampNone;
+}
+
+// the structural walk of prompts [lo, hi) after the previous rounds (their inserts and victims)
+__global__ void k_reprobe(Index ix, const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
+                          const uint32_t* __restrict__ blk_off, uint32_t lo, uint32_t hi, uint32_t* exist,
+                          uint32_t* slot_out) {
+  const uint32_t p = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (p >= hi) return;
+  const uint32_t lane = lane_id(), bo = blk_off[p], n = blk_off[p + 1] - bo;
+  uint32_t k = n;
+  for (uint32_t base = 0; base < n && base < k; base += 32) {
+    const uint32_t b = base + lane;
+    uint64_t h = 0, d = 0;
+    if (b < n) h = hk[bo + b], d = dk[bo + b];
+    const uint64_t hL = __shfl_sync(kFull, h, lane & ~(kGroup - 1)), dL = __shfl_sync(kFull, d, lane & ~(kGroup - 1));
+    uint32_t s = kNone;
+    if (b < n) {
+      Rec r;
+      s = find_slot(ix, h, d, hL, dL, b, &r);
+      if (s != kNone) slot_out[bo + b] = s;
+    }
+    const uint32_t miss = __ballot_sync(kFull, b < n && s == kNone);
+    if (miss) k = min(k, base + __ffs(miss) - 1);
+  }
+  if (lane == 0) exist[p] = k;
+}
+
+// dry claims: the blocks every prompt of [lo, hi) would create, duplicates won by the lowest prompt
+__global__ void k_dry_claims(const uint64_t* __restrict__ hk, const uint64_t* __restrict__ dk,
+                             const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist, uint32_t lo,
+                             uint32_t hi, ulonglong2* tab, uint32_t* minp, uint64_t tmask, uint32_t* dslot) {
+  const uint32_t p = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (p >= hi) return;
+  const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) {
+    const uint64_t h = hk[bo + b], d = dk[bo + b];
+    uint64_t s = slot_hash(h, d) & tmask;
+    for (uint64_t i = 0; i <= tmask; ++i, s = (s + 1) & tmask) {
+      unsigned long long ol, oh;
+      const bool won = cas128(reinterpret_cast<unsigned long long*>(&tab[s]), 0ull, 0ull, h, d, &ol, &oh);
+      if (won || (ol == h && oh == d)) {
+        atomicMin(&minp[s], p);
+        dslot[bo + b] = static_cast<uint32_t>(s);
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_dry_count(const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ exist, uint32_t lo,
+                            uint32_t hi, const uint32_t* __restrict__ minp, const uint32_t* __restrict__ dslot,
+                            uint32_t* needed) {
+  const uint32_t p = lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (p >= hi) return;
+  const uint32_t bo = blk_off[p], n = blk_off[p + 1] - bo;
+  uint32_t f = 0;
+  for (uint32_t b = exist[p] + lane_id(); b < n; b += 32) f += minp[dslot[bo + b]] == p ? 1u : 0u;
+  f = __reduce_add_sync(kFull, f);
+  if (lane_id() == 0) needed[p - lo] = f;
+}
+
+// the order key of an entry, with the batch's pinned entries blocking (k_evict_init)
+__global__ void k_evict_init_pinned(Index ix, const uint32_t* __restrict__ vstamp, unsigned long long* eff) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta))
+    eff[s] = 0ull;
+  else
+    eff[s] = vstamp[s] == 0u ? ~0ull : evict_key(ix, s);
+}
+
+// one thread: the prompts of the round in order, each insert's make_room taking victims from V
+__global__ void k_budget_sim(const uint32_t* __restrict__ needed, uint32_t lo, uint32_t hi, unsigned long long used,
+                             unsigned long long cap, const uint32_t* __restrict__ vals, uint32_t nv,
+                             const unsigned long long* __restrict__ eff, const uint32_t* __restrict__ vstamp,
+                             uint32_t epoch, uint32_t* victims, BudgetSim* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  uint32_t i = 0, nvict = 0, cut = kNone, p = lo, dropped = kNone;
+  for (; p < hi; ++p) {
+    if (p == cut) break;  // an eviction cut this prompt's insert walk: it walks again next round
+    const uint32_t need = needed[p - lo];
+    const uint32_t nvict0 = nvict, i0 = i;
+    const unsigned long long used0 = used;
+    bool stop = false, fail = false;
+    while (used + need > cap) {
+      // stamped by an insert walk of this round at or before p: the walk refreshed its epoch
+      // (young now, and no longer a leaf unless it ends the walk)
+      while (i < nv) {
+        const uint32_t st = vstamp[vals[i]];
+        if (st != kStampNone && st - 1 >= lo && st - 1 <= p)
+          ++i;
+        else
+          break;
+      }
+      if (i == nv) {
+        fail = true;
+        break;
+      }
+      if (p > lo && (eff[vals[i]] >> 32) == epoch) {
+        stop = true;
+        break;
+      }
+      const uint32_t st = vstamp[vals[i]];
+      if (st != kStampNone && st - 1 > p) cut = min(cut, st - 1);
+      victims[nvict++] = vals[i++];
+      --used;
+    }
+    if (fail && p > lo) stop = true;  // the round's own new nodes may still be candidates
+    if (stop) {                       // p's make_room is redone next round
+      nvict = nvict0;
+      i = i0;
+      used = used0;
+      break;
+    }
+    if (fail) {  // CapacityExhausted: its victims stay evicted, the prompt is dropped
+      dropped = p;
+      ++p;
+      break;
+    }
+    used += need;
+  }
+  out->used = used;
+  out->n_victims = nvict;
+  out->next_lo = p;
+  out->dropped = dropped;
+  out->pad = 0;
+}
+
+__global__ void k_evict_mark_list(Index ix, const uint32_t* __restrict__ vals, uint32_t v) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v) return;
+  const uint32_t s = vals[i];
+  Rec& r = ix.e[s].rec;
+  r.meta = (r.meta & 0x1fu) | 0xffffff00u;
+  ix.em[s].dead = 1;
+}
+}  // namespace
+
+void launch_new_bound(const uint32_t* blk_off, const uint32_t* exist, uint32_t lo, uint32_t hi,
+                      unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, 8, s);
+  if (hi > lo) k_new_bound<<<cdiv(hi - lo, 256), 256, 0, s>>>(blk_off, exist, lo, hi, out);
+}
+
+void launch_mark_paths(const uint32_t* slot, const uint32_t* blk_off, const uint32_t* exist, const uint32_t* matched,
+                       uint32_t lo, uint32_t hi, uint32_t* vstamp, uint32_t* list, uint32_t* n_list, uint32_t cap,
+                       cudaStream_t s) {
+  if (hi) k_mark_paths<<<cdiv(static_cast<uint64_t>(hi) * 32, 256), 256, 0, s>>>(slot, blk_off, exist, matched, lo, hi,
+                                                                                 vstamp, list, n_list, cap);
+}
+
+void launch_clear_marks(uint32_t* vstamp, const uint32_t* list, const uint32_t* n_list, uint32_t cap, cudaStream_t s) {
+  k_clear_marks<<<256, 256, 0, s>>>(vstamp, list, n_list, cap);
+}
+
+void launch_reprobe(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* blk_off, uint32_t lo,
+                    uint32_t hi, uint32_t* exist, uint32_t* slot_out, cudaStream_t s) {
+  if (hi > lo)
+    k_reprobe<<<cdiv(static_cast<uint64_t>(hi - lo) * 32, 256), 256, 0, s>>>(ix, h, d, blk_off, lo, hi, exist, slot_out);
+}
+
+void launch_dry_needed(const uint64_t* h, const uint64_t* d, const uint32_t* blk_off, const uint32_t* exist,
+                       uint32_t lo, uint32_t hi, ulonglong2* tab, uint32_t* minp, uint64_t tcap, uint32_t* dslot,
+                       uint32_t* needed, cudaStream_t s) {
+  if (hi <= lo) return;
+  cudaMemsetAsync(tab, 0, tcap * sizeof(ulonglong2), s);
+  cudaMemsetAsync(minp, 0xff, tcap * sizeof(uint32_t), s);
+  const unsigned g = static_cast<unsigned>(cdiv(static_cast<uint64_t>(hi - lo) * 32, 256));
+  k_dry_claims<<<g, 256, 0, s>>>(h, d, blk_off, exist, lo, hi, tab, minp, tcap - 1, dslot);
+  k_dry_count<<<g, 256, 0, s>>>(blk_off, exist, lo, hi, minp, dslot, needed);
+}
+
+uint32_t launch_evict_order(const Index& ix, const uint32_t* vstamp, unsigned long long* eff,
+                            unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                            uint32_t* n_live, void* temp, size_t temp_bytes, uint32_t* host_n, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(cdiv(ix.cap, 256));
+  cudaMemsetAsync(n_live, 0, 4, s);
+  k_evict_init_pinned<<<g, 256, 0, s>>>(ix, vstamp, eff);
+  k_evict_propagate<<<g, 256, 0, s>>>(ix, eff);
+  k_evict_compact<<<g, 256, 0, s>>>(ix, eff, keys_a, vals_a, n_live);
+  cudaMemcpyAsync(host_n, n_live, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const uint32_t n = *host_n;
+  if (n) {  // deeper first, then by effective key (stable): V in vals_a
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b, vals_a, vals_b, static_cast<int>(n), 0, 32, s);
+    k_evict_gather<<<cdiv(n, 256), 256, 0, s>>>(eff, vals_b, keys_a, n_live);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b, vals_b, vals_a, static_cast<int>(n), 0, 64, s);
+  }
+  return n;
+}
+
+void launch_budget_sim(const uint32_t* needed, uint32_t lo, uint32_t hi, uint64_t used, uint64_t cap,
+                       const uint32_t* vals, uint32_t nv, const unsigned long long* eff, const uint32_t* vstamp,
+                       uint32_t epoch, uint32_t* victims, BudgetSim* out, cudaStream_t s) {
+  k_budget_sim<<<1, 32, 0, s>>>(needed, lo, hi, used, cap, vals, nv, eff, vstamp, epoch, victims, out);
+}
+
+namespace {
+__global__ void k_count_tiers(Index ix, unsigned long long* out3) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t t = 3;
+  if (s <= ix.mask) {
+    const Rec& r = ix.e[s].rec;
+    if (!(r.h == 0 && r.d == 0) && meta_live(r.meta)) t = meta_tier(r.meta);
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < 3; ++k) {
+    const uint32_t c = __popc(__ballot_sync(kFull, t == k));
+    if (lane_id() == 0 && c) atomicAdd(&out3[k], static_cast<unsigned long long>(c));
+  }
+}
+}  // namespace
+
+void launch_count_tiers(const Index& ix, unsigned long long* out3, cudaStream_t s) {
+  cudaMemsetAsync(out3, 0, 24, s);
+  k_count_tiers<<<cdiv(ix.cap, 256), 256, 0, s>>>(ix, out3);
+}
+
+void launch_evict_mark_list(const Index& ix, const uint32_t* vals, uint32_t v, cudaStream_t s) {
+  if (v) k_evict_mark_list<<<cdiv(v, 256), 256, 0, s>>>(ix, vals, v);
+}
+}  // namespace skv

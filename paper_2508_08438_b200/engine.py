@@ -360,6 +360,27 @@ class AdmissionEngine:
         with ``tiered_demotion`` victims move HBM -> DRAM instead of leaving."""
         self._check(self._lib.skv_enable_eviction(self._h, 1 if tiered_demotion else 0))
 
+    def set_tier_budget(self, hbm_blocks: int, dram_blocks: int = 0, ssd_blocks: int = 0) -> None:
+        """TierBudget (cache_index.hpp:26-55) in blocks with insert-time make_room:
+        every commit inserts its prompts in order, each first evicting unpinned leaves until its
+        new blocks fit (needs ``enable_eviction()``, before the first admit)."""
+        self._check(self._lib.skv_set_tier_budget(self._h, hbm_blocks, dram_blocks, ssd_blocks))
+
+    def tier_usage(self):
+        """(used, capacity) blocks per tier (HBM, DRAM, SSD)."""
+        u = np.zeros(3, np.uint64)
+        c = np.zeros(3, np.uint64)
+        self._check(self._lib.skv_tier_usage(self._h, _ptr(u), _ptr(c)))
+        return u, c
+
+    def last_drops(self) -> np.ndarray:
+        """Prompts of the last commit whose insert could not make room (CapacityExhausted)."""
+        n = C.c_size_t()
+        self._check(self._lib.skv_last_drops(self._h, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint32)
+        self._check(self._lib.skv_last_drops(self._h, _ptr(out), n.value, C.byref(n)))
+        return out[:n.value]
+
     def evict(self, needed_blocks: int, epoch: int = 0):
         """RadixCacheIndex::evict (cache_index.hpp:281-292): frees ``needed_blocks`` entries
         in the reference's victim order; returns (n_evicted, victim h, victim d).  Raises

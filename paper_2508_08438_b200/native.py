@@ -188,6 +188,9 @@ SIGNATURES = {
                                  C.POINTER(C.c_uint64)]),
     "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
     "skv_stage": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "skv_set_tier_budget": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "skv_tier_usage": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "skv_last_drops": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "skv_tier1_scan_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_void_p]),
     "skv_token_seq_digest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "skv_set_replicated_depth": (C.c_int, [C.c_void_p, C.c_uint32]),

@@ -68,6 +68,9 @@ def load_ref():
         "ref_engine_evict": (C.c_int, [vp, C.c_uint64, C.c_uint64, u64p]),
         "ref_engine_current_epoch": (C.c_uint64, [vp]),
         "ref_engine_set_tiered": (C.c_int, [vp, C.c_int]),
+        "ref_engine_set_budget": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]),
+        "ref_engine_dropped": (sz, [vp, vp, sz]),
+        "ref_engine_budget_used": (None, [vp, vp]),
     }
     for n, (r, a) in sig.items():
         f = getattr(L, n)
@@ -165,6 +168,21 @@ class RefEngine:
 
     def set_tiered(self, tiered=True):
         assert self.L.ref_engine_set_tiered(self.h, 1 if tiered else 0) == 0
+
+    def set_budget(self, hbm, dram=0, ssd=0, tiered=False):
+        """A.9: TierBudget::from_tokens(hbm, dram, ssd) in blocks, before any insert."""
+        assert self.L.ref_engine_set_budget(self.h, hbm, dram, ssd, 1 if tiered else 0) == 0
+
+    def dropped(self):
+        n = self.L.ref_engine_dropped(self.h, None, 0)
+        out = np.zeros(max(n, 1), np.uint32)
+        self.L.ref_engine_dropped(self.h, _p(out), n)
+        return out[:n]
+
+    def budget_used(self):
+        out = np.zeros(3, np.uint64)
+        self.L.ref_engine_budget_used(self.h, _p(out))
+        return out
 
     def evict(self, needed):
         """RadixCacheIndex::evict(needed, current epoch); (rc, nodes freed)."""
