@@ -252,8 +252,11 @@ int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
  * serving_sim.hpp:195-215); the commit inserts the prompts in order, each first evicting unpinned
  * leaves in the reference's victim order until its new blocks fit the HBM budget; a prompt that
  * cannot make room is dropped (nothing inserted, CapacityExhausted in the reference -- listed by
- * skv_last_drops) and the commit continues.  Needs skv_enable_eviction (untiered); call before
- * the first admit.  skv_tier_usage: used / capacity blocks per tier (HBM, DRAM, SSD). */
+ * skv_last_drops) and the commit continues.  With tiered demotion (skv_enable_eviction(ctx, 1))
+ * a victim moves one tier down (HBM -> DRAM -> SSD) and a full lower tier first makes room the
+ * same way, freeing from SSD (evict_or_demote, cache_index.hpp:732-766); skv_evict then cascades
+ * too.  Needs skv_enable_eviction; call before the first admit.  skv_tier_usage: used / capacity
+ * blocks per tier (HBM, DRAM, SSD). */
 int skv_set_tier_budget(skv_ctx* ctx, uint64_t hbm_blocks, uint64_t dram_blocks, uint64_t ssd_blocks);
 int skv_tier_usage(skv_ctx* ctx, uint64_t* used3, uint64_t* cap3);
 /* Prompts (indices into the last committed batch, ascending) whose insert could not make room. */

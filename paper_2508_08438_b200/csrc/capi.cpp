@@ -1469,6 +1469,63 @@ uint64_t commit_range(skv_ctx* c, uint32_t lo, uint32_t end) {
   return nn + revived;
 }
 
+// cap-sized work arrays of one tiered round / tiered evict call (freed by the caller)
+skv::TieredWork tiered_work(skv_ctx* c, uint64_t n, std::vector<void*>& tmp) {
+  skv::TieredWork w;
+  w.cap_each = std::max<uint64_t>(n, 1);
+  w.cc = dalloc<uint32_t>(c->ix.cap, tmp);
+  w.cc_work = dalloc<uint32_t>(c->ix.cap, tmp);
+  w.tier = dalloc<uint8_t>(c->ix.cap, tmp);
+  w.keys_a = dalloc<unsigned long long>(3 * w.cap_each, tmp);
+  w.keys_b = dalloc<unsigned long long>(3 * w.cap_each, tmp);
+  w.hk = dalloc<unsigned long long>(3 * w.cap_each, tmp);
+  w.vals_a = dalloc<uint32_t>(3 * w.cap_each, tmp);
+  w.vals_b = dalloc<uint32_t>(3 * w.cap_each, tmp);
+  w.hv = dalloc<uint32_t>(3 * w.cap_each, tmp);
+  w.n3 = dalloc<uint32_t>(3, tmp);
+  w.act_cap = 3 * w.cap_each + 16;
+  w.act = dalloc<uint32_t>(w.act_cap, tmp);
+  w.n_act = dalloc<uint32_t>(1, tmp);
+  w.used3 = dalloc<unsigned long long>(4, tmp);
+  w.res = dalloc<skv::BudgetSim>(1, tmp);
+  w.temp = c->ev_temp;
+  w.temp_bytes = c->ev_temp_bytes;
+  return w;
+}
+
+// host view of a tiered round's result: tier usage, HBM departures, freed entries
+struct TieredOutcome {
+  skv::BudgetSim r;
+  uint64_t used[3], hbm_out, freed;
+};
+
+TieredOutcome run_tiered(skv_ctx* c, const uint32_t* vstamp, const uint32_t* needed, uint32_t lo, uint32_t hi,
+                         uint64_t need_evict, uint64_t extra) {
+  cudaStream_t s = c->stream;
+  std::vector<void*> tmp;
+  TieredOutcome o{};
+  try {
+    skv::TieredWork w = tiered_work(c, c->entries + extra + 1, tmp);
+    o.r = skv::launch_budget_tiered(c->ix, w, vstamp, needed, lo, hi, need_evict, c->bud_used, c->bud_cap,
+                                    static_cast<uint32_t>(c->epoch), c->host_small, s);
+    if (o.r.pad) throw CapacityError("tiered budget: action list overflow");
+    unsigned long long u[4];
+    std::memcpy(u, c->host_small + 8, 32);
+    for (int t = 0; t < 3; ++t) o.used[t] = u[t];
+    o.hbm_out = u[3];
+    // freed entries = live entries that disappeared (count the free actions)
+    std::vector<uint32_t> act(o.r.n_victims);
+    if (!act.empty()) CK(cudaMemcpyAsync(act.data(), w.act, act.size() * 4, cudaMemcpyDeviceToHost, s));
+    sync_check(s);
+    for (uint32_t a : act) o.freed += (a >> 30) == 0 ? 1 : 0;
+  } catch (...) {
+    for (void* p : tmp) cudaFree(p);
+    throw;
+  }
+  for (void* p : tmp) cudaFree(p);
+  return o;
+}
+
 // The pending batch's commit under a bounded HBM budget (A.9): rounds over prompt ranges, each
 // inserting its prompts with the victims their make_room takes (kernels.cu "A.9").
 void commit_budgeted(skv_ctx* c) {
@@ -1487,7 +1544,23 @@ void commit_budgeted(skv_ctx* c) {
     uint64_t bound = 0;
     std::memcpy(&bound, c->host_small, 8);
     uint32_t end = N, next = N, dropped = skv::kNone, nvict = 0;
-    if (c->bud_used[0] + bound > c->bud_cap[0]) {
+    if (c->evict_tiered && c->bud_used[0] + bound > c->bud_cap[0]) {  // bounded cascade (kernels.cu)
+      CK(cudaMemsetAsync(c->n_mark, 0, 4, s));
+      skv::launch_mark_paths(c->bslot, c->blk_off, c->exist, c->matched, lo, N, c->vstamp, c->mark_list, c->n_mark,
+                             c->mark_cap, s);
+      skv::launch_dry_needed(c->bh, c->bd, c->blk_off, c->exist, lo, N, c->dry_tab, c->dry_minp, c->dry_cap,
+                             c->dry_slot, c->needed, s);
+      const TieredOutcome o = run_tiered(c, c->vstamp, c->needed, lo, N, 0, c->p_blocks);
+      skv::launch_clear_marks(c->vstamp, c->mark_list, c->n_mark, c->mark_cap, s);
+      next = o.r.next_lo;
+      dropped = o.r.dropped;
+      end = dropped != skv::kNone ? dropped : next;
+      c->entries -= o.freed;
+      c->tombstones += o.freed;
+      c->bud_used[0] -= o.hbm_out;
+      c->bud_used[1] = o.used[1];
+      c->bud_used[2] = o.used[2];
+    } else if (c->bud_used[0] + bound > c->bud_cap[0]) {
       CK(cudaMemsetAsync(c->n_mark, 0, 4, s));
       skv::launch_mark_paths(c->bslot, c->blk_off, c->exist, c->matched, lo, N, c->vstamp, c->mark_list, c->n_mark,
                              c->mark_cap, s);
@@ -1868,8 +1941,6 @@ int skv_set_tier_budget(skv_ctx* c, uint64_t hbm_blocks, uint64_t dram_blocks, u
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     if (!c->evict_on) throw StateError("skv_set_tier_budget needs eviction (skv_enable_eviction first)");
-    if (c->evict_tiered)
-      throw skv::ConfigError("tier budgets with tiered demotion (bounded DRAM/SSD cascade) are not supported");
     if (c->entries || c->batch_id || c->pending) throw StateError("skv_set_tier_budget must precede the first admit");
     if (!c->budget_on) {
       c->vstamp = dalloc<uint32_t>(c->ix.cap, c->owned);
@@ -1950,6 +2021,17 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
     auto* vals_b = dalloc<uint32_t>(L, tmp);
     auto* vh = dalloc<uint64_t>(L, tmp);
     auto* vd = dalloc<uint64_t>(L, tmp);
+    if (c->budget_on && c->evict_tiered) {  // evict_or_demote with bounded DRAM / SSD (cascade)
+      for (void* p : tmp) cudaFree(p);
+      tmp.clear();
+      const TieredOutcome o = run_tiered(c, nullptr, nullptr, 0, 0, needed_blocks, 0);
+      c->entries -= o.freed;
+      c->tombstones += o.freed;
+      for (int t = 0; t < 3; ++t) c->bud_used[t] = o.used[t];
+      *n_evicted = o.hbm_out;
+      if (o.r.dropped == 0) throw CapacityError("evict: no unpinned candidate leaf");
+      return SKV_OK;
+    }
     const uint32_t v = skv::launch_evict(c->ix, needed_blocks, c->ev_eff, keys_a, keys_b, vals_a, vals_b, c->ev_n,
                                          c->ev_temp, c->ev_temp_bytes, vh, vd, c->host_small,
                                          c->evict_tiered ? 1 : 0, s);
@@ -1962,6 +2044,9 @@ int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_ev
       c->entries -= v;
       c->tombstones += v;
       c->bud_used[0] -= std::min<uint64_t>(c->bud_used[0], v);
+    } else {  // unbounded lower tiers: victims move HBM -> DRAM
+      c->bud_used[0] -= std::min<uint64_t>(c->bud_used[0], v);
+      c->bud_used[1] += v;
     }
     *n_evicted = v;
     if (v < needed_blocks) throw CapacityError("evict: no unpinned candidate leaf");

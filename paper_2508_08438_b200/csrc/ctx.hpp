@@ -275,6 +275,26 @@ void launch_budget_sim(const uint32_t* needed, uint32_t lo, uint32_t hi, uint64_
                        uint32_t epoch, uint32_t* victims, BudgetSim* out, cudaStream_t s);
 void launch_evict_mark_list(const Index& ix, const uint32_t* vals, uint32_t v, cudaStream_t s);
 void launch_count_tiers(const Index& ix, unsigned long long* out3, cudaStream_t s);
+// tiered rounds (bounded DRAM / SSD): cap-sized work arrays, 3 tiers x cap_each candidates
+struct TieredWork {
+  uint32_t* cc = nullptr;       // live children per slot (round start)
+  uint32_t* cc_work = nullptr;  // the simulation's copy
+  uint8_t* tier = nullptr;      // current tier per slot during the simulation
+  unsigned long long *keys_a = nullptr, *keys_b = nullptr, *hk = nullptr;
+  uint32_t *vals_a = nullptr, *vals_b = nullptr, *hv = nullptr;
+  uint64_t cap_each = 0;
+  uint32_t* n3 = nullptr;
+  uint32_t* act = nullptr;  // actions (slot | kind << 30)
+  uint64_t act_cap = 0;
+  uint32_t* n_act = nullptr;
+  unsigned long long* used3 = nullptr;
+  BudgetSim* res = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+};
+BudgetSim launch_budget_tiered(const Index& ix, const TieredWork& w, const uint32_t* vstamp, const uint32_t* needed,
+                               uint32_t lo, uint32_t hi, uint64_t need_evict, const uint64_t* used3,
+                               const uint64_t* cap3, uint32_t epoch, uint32_t* host, cudaStream_t s);
 uint32_t launch_evict(const Index& ix, uint64_t needed, unsigned long long* eff, unsigned long long* keys_a,
                       unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint32_t* n_live, void* temp,
                       size_t temp_bytes, uint64_t* victims_h, uint64_t* victims_d, uint32_t* host_n, int tiered,

@@ -3486,7 +3486,234 @@ void launch_budget_sim(const uint32_t* needed, uint32_t lo, uint32_t hi, uint64_
   k_budget_sim<<<1, 32, 0, s>>>(needed, lo, hi, used, cap, vals, nv, eff, vstamp, epoch, victims, out);
 }
 
+// ---- A.9 with tiered demotion (evict_or_demote, cache_index.hpp:732-766): bounded DRAM / SSD.
+// A victim moves one tier down and stays a leaf; a full lower tier first demotes (or, from SSD,
+// frees) its own smallest-key leaf; with no such leaf the victim is freed outright.  Frees
+// expose parents, so the per-tier candidate pools are the round's sorted leaves plus a heap of
+// nodes that became candidates during the round (demoted victims, exposed parents).
 namespace {
+__device__ __forceinline__ unsigned long long tier_key(const Index& ix, uint32_t s) {
+  const EvictMeta em = ix.em[s];
+  return (static_cast<unsigned long long>(em.access_epoch) << 32) |
+         (static_cast<unsigned long long>(meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) << 31) |
+         (em.node_id & 0x7fffffffu);
+}
+
+__global__ void k_child_counts(Index ix, uint32_t* cc) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta) || r.parent == kNone) return;
+  atomicAdd(&cc[r.parent], 1u);
+}
+
+__global__ void k_tier_leaves(Index ix, const uint32_t* __restrict__ cc, const uint32_t* __restrict__ vstamp,
+                              unsigned long long* keys, uint32_t* vals, uint32_t* n3, uint64_t cap_each) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  if ((r.h == 0 && r.d == 0) || !meta_live(r.meta) || cc[s] || (vstamp && vstamp[s] == 0u)) return;
+  const uint32_t t = meta_tier(r.meta);
+  const uint32_t i = atomicAdd(&n3[t], 1u);
+  keys[t * cap_each + i] = tier_key(ix, static_cast<uint32_t>(s));
+  vals[t * cap_each + i] = static_cast<uint32_t>(s);
+}
+
+struct TPool {  // one tier's candidates: the round's sorted leaves, then a min-heap of arrivals
+  const unsigned long long* lk;
+  const uint32_t* lv;
+  uint32_t ln, li;
+  unsigned long long* hk;
+  uint32_t* hv;
+  uint32_t hn;
+};
+
+__device__ void heap_push(TPool& P, unsigned long long k, uint32_t v) {
+  uint32_t i = P.hn++;
+  while (i) {
+    const uint32_t par = (i - 1) >> 1;
+    if (P.hk[par] <= k) break;
+    P.hk[i] = P.hk[par];
+    P.hv[i] = P.hv[par];
+    i = par;
+  }
+  P.hk[i] = k;
+  P.hv[i] = v;
+}
+
+__device__ void heap_pop(TPool& P) {
+  const unsigned long long k = P.hk[--P.hn];
+  const uint32_t v = P.hv[P.hn];
+  uint32_t i = 0;
+  for (;;) {
+    uint32_t c = 2 * i + 1;
+    if (c >= P.hn) break;
+    if (c + 1 < P.hn && P.hk[c + 1] < P.hk[c]) ++c;
+    if (P.hk[c] >= k) break;
+    P.hk[i] = P.hk[c];
+    P.hv[i] = P.hv[c];
+    i = c;
+  }
+  if (P.hn) {
+    P.hk[i] = k;
+    P.hv[i] = v;
+  }
+}
+
+struct TSim {
+  Index ix;
+  TPool pool[3];
+  uint32_t* cc;
+  const uint32_t* vstamp;
+  uint8_t* tier;  // current tier of every slot this round touched (255 = freed); init = table tier
+  uint32_t* act;  // actions in order: slot | kind << 30 (0 free, 1 -> DRAM, 2 -> SSD)
+  uint32_t n_act, act_cap;
+  unsigned long long used[3], cap[3];
+  uint32_t lo, p, cut, epoch;
+  unsigned long long hbm_out;  // blocks that left HBM (freed or demoted)
+  bool stop;
+};
+
+// the smallest-key current candidate of tier t (kNone: none).  Skipped for good: entries that
+// left the tier, and entries an insert walk of this round at or before prompt p refreshed (young,
+// and attach points: the current-epoch region ends the round, below)
+__device__ uint32_t pool_pop(TSim& S, uint32_t t) {
+  TPool& P = S.pool[t];
+  for (;;) {
+    uint32_t v = kNone;
+    unsigned long long k = 0;
+    const bool from_heap = P.hn && (P.li >= P.ln || P.hk[0] < P.lk[P.li]);
+    if (from_heap) {
+      v = P.hv[0], k = P.hk[0];
+      heap_pop(P);
+    } else if (P.li < P.ln) {
+      v = P.lv[P.li], k = P.lk[P.li];
+      ++P.li;
+    } else {
+      return kNone;
+    }
+    if (S.tier[v] != t) continue;
+    const uint32_t st = S.vstamp ? S.vstamp[v] : kStampNone;
+    if (st != kStampNone && st - 1 >= S.lo && st - 1 <= S.p) continue;
+    if (S.p > S.lo && (k >> 32) == S.epoch) {  // the batch's own nodes may precede it: end the round
+      S.stop = true;
+      return kNone;
+    }
+    return v;
+  }
+}
+
+__device__ bool sim_free(TSim& S, uint32_t v) {
+  const uint32_t t = S.tier[v];
+  S.used[t]--;
+  if (t == 0) ++S.hbm_out;
+  S.tier[v] = 255;
+  if (S.n_act < S.act_cap) S.act[S.n_act++] = v;
+  const uint32_t st = S.vstamp ? S.vstamp[v] : kStampNone;
+  if (st != kStampNone && st - 1 > S.p) S.cut = min(S.cut, st - 1);  // a later insert walks it
+  const uint32_t par = S.ix.e[v].rec.parent;
+  if (par != kNone && --S.cc[par] == 0 && S.tier[par] < 3 && !(S.vstamp && S.vstamp[par] == 0u))
+    heap_push(S.pool[S.tier[par]], tier_key(S.ix, par), par);  // the parent became a leaf
+  return true;
+}
+
+// evict_or_demote(v, t): false when a pool query ended the round
+__device__ bool sim_evict_or_demote(TSim& S, uint32_t v, uint32_t t) {
+  if (t == 2) return sim_free(S, v);
+  const uint32_t target = t + 1;
+  while (S.used[target] + 1 > S.cap[target]) {
+    const uint32_t lv = pool_pop(S, target);
+    if (S.stop) return false;
+    if (lv == kNone) return sim_free(S, v);  // lower tiers full and unfreeable: drop outright
+    if (!sim_evict_or_demote(S, lv, target)) return false;
+  }
+  S.used[t]--;
+  if (t == 0) ++S.hbm_out;
+  S.used[target]++;
+  S.tier[v] = static_cast<uint8_t>(target);
+  if (S.n_act < S.act_cap) S.act[S.n_act++] = v | (target << 30);
+  heap_push(S.pool[target], tier_key(S.ix, v), v);  // still a leaf, now in the lower tier
+  return true;
+}
+
+// needed == nullptr: RadixCacheIndex::evict(need_evict) instead of a commit round
+__global__ void k_budget_sim_tiered(TSim S, const uint32_t* __restrict__ needed, uint32_t hi, uint64_t need_evict,
+                                    BudgetSim* out, unsigned long long* used_out, uint32_t* n_act_out) {
+  if (threadIdx.x || blockIdx.x) return;
+  S.cut = kNone;
+  S.stop = false;
+  S.hbm_out = 0;
+  uint32_t p = S.lo, dropped = kNone;
+  if (!needed) {
+    S.p = S.lo;
+    uint64_t freed = 0;
+    while (freed < need_evict) {
+      const uint32_t v = pool_pop(S, 0);
+      if (v == kNone) {
+        dropped = 0;  // CapacityExhausted after freeing what it could
+        break;
+      }
+      sim_evict_or_demote(S, v, 0);
+      ++freed;
+    }
+    p = hi;
+  } else {
+    for (; p < hi; ++p) {
+      if (p == S.cut) break;
+      S.p = p;
+      const uint32_t need = needed[p - S.lo];
+      bool fail = false;
+      while (S.used[0] + need > S.cap[0]) {
+        const uint32_t v = pool_pop(S, 0);
+        if (S.stop) break;
+        if (v == kNone) {
+          fail = true;
+          break;
+        }
+        if (!sim_evict_or_demote(S, v, 0)) break;
+      }
+      if (fail && p > S.lo) S.stop = true;
+      if (S.stop) break;  // the caller re-runs the round up to p (its make_room is redone next round)
+      if (fail) {
+        dropped = p;
+        ++p;
+        break;
+      }
+      S.used[0] += need;
+    }
+  }
+  out->used = S.used[0];
+  out->n_victims = S.n_act;
+  out->next_lo = p;
+  out->dropped = S.stop ? kNone - 1 : dropped;
+  out->pad = S.n_act >= S.act_cap ? 1u : 0u;
+  for (int t = 0; t < 3; ++t) used_out[t] = S.used[t];
+  used_out[3] = S.hbm_out;
+  *n_act_out = S.n_act;
+}
+
+// apply the actions in order (a slot can move down twice, then be freed)
+__global__ void k_apply_actions(Index ix, const uint32_t* __restrict__ act, uint32_t n) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t s = act[i] & 0x3fffffffu, kind = act[i] >> 30;
+    Rec& r = ix.e[s].rec;
+    if (kind == 0) {
+      r.meta = (r.meta & 0x1fu) | 0xffffff00u;
+      ix.em[s].dead = 1;
+    } else {
+      r.meta = (r.meta & ~(3u << 3)) | (kind << 3);
+    }
+  }
+}
+
+__global__ void k_tier_init(Index ix, uint8_t* tier) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > ix.mask) return;
+  const Rec& r = ix.e[s].rec;
+  tier[s] = ((r.h == 0 && r.d == 0) || !meta_live(r.meta)) ? 255 : static_cast<uint8_t>(meta_tier(r.meta));
+}
+
 __global__ void k_count_tiers(Index ix, unsigned long long* out3) {
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t t = 3;
@@ -3501,6 +3728,59 @@ __global__ void k_count_tiers(Index ix, unsigned long long* out3) {
   }
 }
 }  // namespace
+
+// One tiered round (or one tiered evict call): candidate pools, then the sequential simulation.
+// Work buffers (TieredWork) hold cap-sized arrays; returns the round's BudgetSim in host memory.
+BudgetSim launch_budget_tiered(const Index& ix, const TieredWork& w, const uint32_t* vstamp, const uint32_t* needed,
+                               uint32_t lo, uint32_t hi, uint64_t need_evict, const uint64_t* used3,
+                               const uint64_t* cap3, uint32_t epoch, uint32_t* host, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(cdiv(ix.cap, 256));
+  cudaMemsetAsync(w.cc, 0, ix.cap * 4, s);
+  k_child_counts<<<g, 256, 0, s>>>(ix, w.cc);
+  cudaMemsetAsync(w.n3, 0, 12, s);
+  k_tier_leaves<<<g, 256, 0, s>>>(ix, w.cc, vstamp, w.keys_a, w.vals_a, w.n3, w.cap_each);
+  cudaMemcpyAsync(host, w.n3, 12, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  uint32_t n3[3] = {host[0], host[1], host[2]};
+  size_t tb = w.temp_bytes;
+  for (int t = 0; t < 3; ++t)
+    if (n3[t])
+      cub::DeviceRadixSort::SortPairs(w.temp, tb, w.keys_a + t * w.cap_each, w.keys_b + t * w.cap_each,
+                                      w.vals_a + t * w.cap_each, w.vals_b + t * w.cap_each, static_cast<int>(n3[t]),
+                                      0, 64, s);
+  // a stopped round is re-run up to its stop prompt from the same start state
+  uint32_t hi_run = hi;
+  BudgetSim r{};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cudaMemcpyAsync(w.cc_work, w.cc, ix.cap * 4, cudaMemcpyDeviceToDevice, s);
+    k_tier_init<<<g, 256, 0, s>>>(ix, w.tier);
+    TSim S{};
+    S.ix = ix;
+    for (int t = 0; t < 3; ++t) {
+      S.pool[t] = TPool{w.keys_b + t * w.cap_each, w.vals_b + t * w.cap_each, n3[t], 0u,
+                        w.hk + t * w.cap_each, w.hv + t * w.cap_each, 0u};
+      S.used[t] = used3[t];
+      S.cap[t] = cap3[t];
+    }
+    S.cc = w.cc_work;
+    S.vstamp = vstamp;
+    S.tier = w.tier;
+    S.act = w.act;
+    S.act_cap = static_cast<uint32_t>(std::min<uint64_t>(w.act_cap, 0x3fffffffull));
+    S.n_act = 0;
+    S.lo = lo;
+    S.epoch = epoch;
+    k_budget_sim_tiered<<<1, 32, 0, s>>>(S, needed, hi_run, need_evict, w.res, w.used3, w.n_act);
+    cudaMemcpyAsync(host, w.res, sizeof(BudgetSim), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(host + 8, w.used3, 32, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::memcpy(&r, host, sizeof(r));
+    if (r.dropped != kNone - 1) break;  // not stopped
+    hi_run = r.next_lo;                 // stopped at prompt next_lo > lo: redo the round up to it
+  }
+  if (r.n_victims) k_apply_actions<<<1, 32, 0, s>>>(ix, w.act, r.n_victims);
+  return r;
+}
 
 void launch_count_tiers(const Index& ix, unsigned long long* out3, cudaStream_t s) {
   cudaMemsetAsync(out3, 0, 24, s);
