@@ -571,13 +571,24 @@ def run_ours(args):
     alg_bytes = 4 * timed_tokens + 12 * timed_blocks
     achieved = alg_bytes / (hs_avg / 1e3) / 1e9
     peak, kind = peaks()
+    # ncu DRAM bytes of one k_hash_scan launch of THIS workload (profiles/hash_scan_traffic.json,
+    # one capture per workload; null when this workload has none)
     traffic = None
     tp = ROOT / "profiles" / "hash_scan_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("workloads", {}).get(str(args.workload), {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # SURVEY 8(d) algorithmic bytes of a whole step (hash+scan fused: 4 B/token once + 16 B keys +
+    # 3 B label/category per block; lookup: one 32-B sector per probed record, m+1 per prompt +
+    # 8 B; monitor: 64 B per matched block; commit: 32 B per new block) over the device step time
+    m_tot = float(np.mean([t["matched_total"] for t in per_dev]))
+    u_tot = float(np.mean([t["new_blocks"] for t in per_dev]))
+    step_bytes = (4 * timed_tokens + 19 * timed_blocks + 32 * (m_tot + n_local) + 8 * n_local + 64 * m_tot
+                  + 32 * u_tot)
+    step_roof = step_bytes / (ms_dev / steps / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # a bounded sample (~10-30 s of CPU work): CPU_STEPS timed steps of the first
@@ -643,7 +654,11 @@ def run_ours(args):
                      "traffic": traffic, "kernel": "k_hash_scan", "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": hs_avg,
                      "timing": "CUDA events around each k_hash_scan launch on its stream, un-pipelined pass",
-                     "avg_launch_ms_overlapped": hs_overlapped},
+                     "avg_launch_ms_overlapped": hs_overlapped,
+                     "frac_strict_scan_bytes": (4 * timed_tokens + 3 * timed_blocks) / (hs_avg / 1e3) / 1e9 / peak,
+                     "step": {"alg_bytes": step_bytes, "achieved": step_roof, "frac": step_roof / peak,
+                              "definition": "SURVEY 8(d) bytes of hash+scan, lookup, monitor records and commit "
+                                            "per step over the device step time"}},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "inputs": ("byte tokens (ByteVocabulary) + offsets, users, owners from pinned host memory, widened "

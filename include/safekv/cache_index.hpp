@@ -14,8 +14,10 @@
 //  * node identities follow inserts, not the reference's later edge splits (an insert of a
 //    prefix of an existing node returns a one-token node at the prefix end);
 //  * node_count() counts device entries (tokens), not radix nodes;
-//  * compression, pinning and the budget-driven eviction of this header are not provided (the
-//    device path's eviction is skv_evict); TierBudget is kept for the constructor's Config.
+//  * compression and per-node pinning are not provided, and eviction is per block rather than per
+//    multi-token radix node, so the facade's TierBudget is bookkeeping only: budgets with
+//    insert-time make_room and the evict_or_demote cascade run on the batch path
+//    (skv_set_tier_budget).
 #pragma once
 
 #include <array>

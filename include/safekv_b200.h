@@ -247,7 +247,7 @@ uint64_t skv_entry_count(skv_ctx* ctx);
  * be freed. */
 int skv_enable_eviction(skv_ctx* ctx, int tiered_demotion);
 /* TierBudget (cache_index.hpp:26-55) in blocks, with the reference's insert-time make_room
- * (cache_index.hpp:183-190, 801-806) -- SURVEY Appendix A.9: every prompt's matched path stays
+ * (cache_index.hpp:183-190, 801-806) -- contract A.9: every prompt's matched path stays
  * pinned from its lookup until the batch's commit ends (ServingSimulator::submit pins,
  * serving_sim.hpp:195-215); the commit inserts the prompts in order, each first evicting unpinned
  * leaves in the reference's victim order until its new blocks fit the HBM budget; a prompt that

@@ -361,7 +361,7 @@ class AdmissionEngine:
         self._check(self._lib.skv_enable_eviction(self._h, 1 if tiered_demotion else 0))
 
     def set_tier_budget(self, hbm_blocks: int, dram_blocks: int = 0, ssd_blocks: int = 0) -> None:
-        """TierBudget (cache_index.hpp:26-55) in blocks with insert-time make_room:
+        """TierBudget (cache_index.hpp:26-55) in blocks with insert-time make_room (A.9):
         every commit inserts its prompts in order, each first evicting unpinned leaves until its
         new blocks fit (needs ``enable_eviction()``, before the first admit)."""
         self._check(self._lib.skv_set_tier_budget(self._h, hbm_blocks, dram_blocks, ssd_blocks))

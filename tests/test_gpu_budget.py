@@ -1,5 +1,5 @@
 """TierBudget-bounded HBM with insert-time make_room (reference cache_index.hpp:26-55, 152-205,
-697-728, 801-806) under the batched serving contract of SURVEY Appendix A.9: each prompt's
+697-728, 801-806) under the batched serving contract A.9 (extending SURVEY Appendix A): each prompt's
 matched path stays pinned from its lookup to the end of the batch's commit
 (ServingSimulator::submit, serving_sim.hpp:195-215), the commit inserts the prompts in order and
 every insert first evicts unpinned leaves in the reference's victim order until its new blocks
