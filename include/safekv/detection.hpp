@@ -87,13 +87,13 @@ class CompiledRuleSet {
   // detection.hpp:148-170, on the device: sensitive iff some enabled rule matches; categories of
   // the hit rules in rule order, de-duplicated
   DetectionVerdict scan(std::string_view text) const {
-    uint32_t mask = 0;
+    std::vector<uint32_t> mask(words(), 0);
     {
       std::lock_guard lk(mu_);
       ensure_ctx();
-      b200::check(skv_tier1_scan(ctx_, text.data(), text.size(), &mask), ctx_);
+      b200::check(skv_tier1_scan(ctx_, text.data(), text.size(), mask.data()), ctx_);
     }
-    return verdict_of(mask);
+    return verdict_of(mask.data(), 1);
   }
 
   // scan() of many independent texts in one device launch (a pipeline drain)
@@ -103,7 +103,7 @@ class CompiledRuleSet {
     std::string flat;
     flat.reserve(off.back());
     for (const auto& t : texts) flat.append(t.data(), t.size());
-    std::vector<uint32_t> masks(texts.size(), 0);
+    std::vector<uint32_t> masks(texts.size() * words(), 0);  // word-major
     {
       std::lock_guard lk(mu_);
       ensure_ctx();
@@ -113,7 +113,7 @@ class CompiledRuleSet {
     }
     std::vector<DetectionVerdict> out;
     out.reserve(texts.size());
-    for (uint32_t m : masks) out.push_back(verdict_of(m));
+    for (size_t i = 0; i < texts.size(); ++i) out.push_back(verdict_of(masks.data() + i, texts.size()));
     return out;
   }
 
@@ -140,12 +140,16 @@ class CompiledRuleSet {
   }
 
   // detection.hpp:160-169: categories of the hit rules in rule order, de-duplicated
-  DetectionVerdict verdict_of(uint32_t mask) const {
+  uint32_t words() const { return skv_rules_mask_words(r_); }
+
+  // mask word w of this verdict at mask[w * stride]
+  DetectionVerdict verdict_of(const uint32_t* mask, size_t stride) const {
     DetectionVerdict v;
     v.tier = 1;
     std::vector<bool> hit(size(), false);
+    bool any = false;
     for (uint32_t j = 0; j < skv_rules_enabled_count(r_); ++j)
-      if (mask >> j & 1u) hit[skv_rules_enabled_rule(r_, j)] = true;
+      if (mask[(j / 32) * stride] >> (j % 32) & 1u) hit[skv_rules_enabled_rule(r_, j)] = any = true;
     for (uint32_t i = 0; i < size(); ++i) {
       if (!hit[i]) continue;
       const char* cat = nullptr;
@@ -154,7 +158,7 @@ class CompiledRuleSet {
       for (const auto& c : v.categories) dup |= c == cat;
       if (!dup) v.categories.emplace_back(cat);
     }
-    v.sensitive = mask != 0;
+    v.sensitive = any;
     v.score = v.sensitive ? 1.0 : 0.0;
     v.escalate = !v.sensitive;
     return v;

@@ -70,14 +70,21 @@ int skv_rules_info(const skv_rules* r, uint32_t i, const char** rule_id, const c
 size_t skv_rules_warning_count(const skv_rules* r);
 const char* skv_rules_warning(const skv_rules* r, size_t i);
 /* The device runs a rule set as consecutive groups of <= 16 enabled rules whose automata fit its
- * tables (one scan pass per group; window masks keep bit j = j-th enabled rule across groups),
- * so rule sets of up to 32 enabled rules load whatever their automaton size. */
+ * tables (one scan pass per group; no group straddles a 32-rule mask word), so rule libraries of
+ * up to 32 * SKV_MAX_MASK_WORDS enabled rules load whatever their automaton size (the reference
+ * accepts any size, detection.hpp:222-242; beyond the maximum: SKV_ERR_COMPILE at load). */
+#define SKV_MAX_MASK_WORDS 32
 uint32_t skv_rules_group_count(const skv_rules* r);
 /* Device rule masks use bit j = j-th ENABLED rule; this maps j -> rule list index. */
 uint32_t skv_rules_enabled_count(const skv_rules* r);
 uint32_t skv_rules_enabled_rule(const skv_rules* r, uint32_t j);
+/* u32 words of a window's rule mask: ceil(enabled / 32), at least 1.  Word w holds bits
+ * 32w .. 32w+31; every per-window mask output below with more than one word is word-major
+ * (word w of all windows, then word w + 1). */
+uint32_t skv_rules_mask_words(const skv_rules* r);
 
-/* Read-only view of the compiled automaton (tests / tooling). */
+/* Read-only view of the compiled automaton (tests / tooling); SKV_ERR_COMPILE for a set of more
+ * than 32 enabled rules (it exists only as its groups' automata). */
 typedef struct {
   uint32_t n_states, n_classes, start;
   const uint8_t* class_map; /* [256] byte -> class                     */
@@ -145,7 +152,8 @@ typedef struct {
   uint64_t* block_h;     /* chained prefix key h_b                          */
   uint64_t* block_d;     /* token_seq_digest of the block d_b               */
   uint8_t* label;        /* SKV_LABEL_PRIVATE / SKV_LABEL_PUBLIC (A.4)      */
-  uint32_t* rule_mask;   /* window verdict, bit j = j-th enabled rule (A.3) */
+  uint32_t* rule_mask;   /* window verdict, bit j = j-th enabled rule (A.3); word 0 of
+                          * the mask (more words: skv_last_rule_masks)              */
   uint8_t* decision;     /* SKV_MISS / SKV_PUBLIC_HIT / SKV_OWNER_HIT (A.5) */
   /* per prompt */
   uint32_t* matched_blocks; /* longest visible prefix, in blocks            */
@@ -158,6 +166,11 @@ typedef struct {
 } skv_admit_out;
 
 int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
+/* The last admitted batch's full window rule masks: skv_mask_words(ctx) words per block,
+ * word-major (out[w * n_blocks + b]); valid until the next skv_admit or skv_set_rules. */
+int skv_last_rule_masks(skv_ctx* ctx, uint32_t* out, int on_device);
+/* mask words of the context's active rule set (skv_rules_mask_words of it) */
+uint32_t skv_mask_words(const skv_ctx* ctx);
 /* Cross-batch pipelining: stage the NEXT device-resident batch's digests and window
  * rule masks (stages 1-2, which read no index state) on a side stream, so they overlap
  * the pending batch's commit/epoch.  The next skv_admit with the same tokens/offsets
@@ -335,10 +348,11 @@ int skv_check_anomaly(skv_ctx* ctx, uint64_t h, uint64_t d, uint64_t epoch, skv_
 
 /* Per-call wrappers (batch of one, still on the device) for the facade:
  * RuleEngine::tier1_scan (detection.hpp:217) and token_seq_digest (core.hpp:68). */
+/* rule_mask receives skv_mask_words(ctx) words (one for up to 32 enabled rules). */
 int skv_tier1_scan(skv_ctx* ctx, const char* text, size_t len, uint32_t* rule_mask);
 /* Tier-1 scan of n independent texts text[offsets[i] : offsets[i+1]] in one launch (the
  * DetectionPipeline drain's RuleEngine::tier1_scan per pending block, detection.hpp:547-552);
- * rule_masks[i] = enabled-rule mask of text i, as skv_tier1_scan. */
+ * rule_masks[w * n + i] = word w of the enabled-rule mask of text i, as skv_tier1_scan. */
 int skv_tier1_scan_batch(skv_ctx* ctx, const char* text, const uint64_t* offsets, uint32_t n, uint32_t* rule_masks);
 int skv_token_seq_digest(skv_ctx* ctx, const uint32_t* tokens, size_t n, uint64_t* digest);
 

@@ -123,10 +123,14 @@ void* ref_rules_masker(void* r) {
   return box;  // masks are computed on the fly in ref_rules_mask
 }
 
-uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
+// Per-rule hit bits of every rule (bit i of word i / 64 = rule i of the list), any library size.
+void ref_rules_mask_wide(void* r, const char* text, size_t len, uint64_t* out, size_t words) {
   const auto& set = *static_cast<RulesBox*>(r)->set;
   const auto& rules = set.rules();
-  uint64_t mask = 0;
+  for (size_t w = 0; w < words; ++w) out[w] = 0;
+  auto set_bit = [&](size_t i) {
+    if (i / 64 < words) out[i / 64] |= 1ull << (i % 64);
+  };
   // regex rules: one snapshot per rule (compiled lazily, cached per call site)
   // cache value keeps the owning snapshot alive so its address cannot be reused
   struct Entry {
@@ -134,7 +138,7 @@ uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
   };
   static thread_local std::map<std::pair<const void*, size_t>, Entry> cache;
   auto owner = static_cast<RulesBox*>(r)->set;
-  for (size_t i = 0; i < rules.size() && i < 64; ++i) {
+  for (size_t i = 0; i < rules.size(); ++i) {
     if (rules[i].kind == PatternRule::Kind::ExactBlacklist) continue;
     if (!rules[i].enabled) continue;
     auto key = std::make_pair(static_cast<const void*>(&set), i);
@@ -143,7 +147,7 @@ uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
       PatternRule one = rules[i];
       it = cache.emplace(key, Entry{owner, CompiledRuleSet::compile({one}, 0)}).first;
     }
-    if (it->second.compiled->scan(std::string_view(text, len)).sensitive) mask |= (1ull << i);
+    if (it->second.compiled->scan(std::string_view(text, len)).sensitive) set_bit(i);
   }
   // blacklist rules: compile the reference trie with every blacklist rule in order,
   // each tagged by a unique category, so the verdict names the winning rule.
@@ -152,7 +156,7 @@ uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
     auto it = cache.find(key);
     if (it == cache.end()) {
       std::vector<PatternRule> only;
-      for (size_t i = 0; i < rules.size() && i < 64; ++i) {
+      for (size_t i = 0; i < rules.size(); ++i) {
         if (rules[i].kind != PatternRule::Kind::ExactBlacklist) continue;
         PatternRule one = rules[i];
         one.rule_id = "r" + std::to_string(i);
@@ -162,9 +166,15 @@ uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
       it = cache.emplace(key, Entry{owner, CompiledRuleSet::compile(only, 0)}).first;
     }
     auto v = it->second.compiled->scan(std::string_view(text, len));
-    for (const auto& c : v.categories) mask |= (1ull << std::stoul(c));
+    for (const auto& c : v.categories) set_bit(std::stoul(c));
   }
-  return mask;
+}
+
+// rules 0..63 (the per-rule masks of the parity tests; wider sets: ref_rules_mask_wide)
+uint64_t ref_rules_mask(void* r, const char* text, size_t len) {
+  uint64_t m = 0;
+  ref_rules_mask_wide(r, text, len, &m, 1);
+  return m;
 }
 
 // Window verdict masks for every full block of every prompt (Appendix A.3).

@@ -22,6 +22,8 @@ struct skv_rules {
   skv::RuleSetSpec spec;
   skv::DfaTables dfa;       // the whole rule set's automaton (skv_rules_dfa; the rule order)
   skv::RuleGroups groups;   // the device's automata: consecutive groups of <= 16 enabled rules
+  std::vector<uint32_t> enabled;  // rule-list position of the j-th enabled rule (mask bit j)
+  bool whole = false;             // dfa holds the whole set (<= 32 enabled rules: one u32 mask)
 };
 
 #ifndef SKV_COMMIT_FLAT_HOST
@@ -31,6 +33,7 @@ struct skv_rules {
 #define SKV_REC_BESIDE 0  // measured: 0.82 ms beside vs 0.72 fused (DESIGN 5.3)
 #endif
 constexpr bool kRecordBeside = SKV_REC_BESIDE != 0;
+constexpr size_t kEpochEvPre = 128;  // events read back with an epoch's count
 #ifndef SKV_STREAM_PRIO
 #define SKV_STREAM_PRIO 0
 #endif
@@ -115,10 +118,12 @@ struct skv_ctx {
     void* buf = nullptr;
     skv::DevRules16 r16{};
     skv::HSLayout layout{};
-    uint32_t smem = 0, shift = 0;
+    uint32_t smem = 0, shift = 0, word = 0;  // mask bits: word `word`, from bit `shift`
     int grid = 0;
   };
   std::vector<DevGroup> groups;
+  uint32_t mask_words = 1;      // words of the active rule set's window masks
+  uint32_t mask_words_cap = 1;  // words bmask / alt_bmask hold per block (max_blocks stride)
   bool rules_loaded = false;
 
   // index
@@ -192,6 +197,7 @@ struct skv_ctx {
   void* temp = nullptr;
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
+  skv_event* host_events = nullptr;  // pinned: the first kEpochEvPre events of an epoch, read with its count
   int n_sm = 148;
   uint32_t rec_grid = 0;
 
@@ -346,6 +352,10 @@ int guard(skv_ctx* c, F&& f) {
 
 // Whether a group automaton fits the general kernel's device tables (u16 row offsets below the
 // 32 KB copy region, <= 63 byte classes, u16 copy-row rule masks: <= 16 rules per group).
+uint32_t mask_words_of(const skv_rules& r) {
+  return std::max<uint32_t>(1, static_cast<uint32_t>((r.enabled.size() + 31) / 32));
+}
+
 bool fits_device(const skv::DfaTables& d) {
   const uint32_t C = d.n_classes, S = d.n_states, row = (C + 1) * 2;
   if (C + 1 > 64 || d.rule_index.size() > 16) return false;
@@ -495,9 +505,31 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
     for (size_t i = 0; i < gs.size(); ++i) {
       build_group(c, r.groups.groups[i], gs[i]);
       build_group16(c, r.groups.groups[i], gs[i]);
-      gs[i].shift = r.groups.first_bit[i];
+      gs[i].shift = r.groups.first_bit[i] % 32;
+      gs[i].word = r.groups.first_bit[i] / 32;
     }
     sync_check(c->stream);
+    const uint32_t words = mask_words_of(r);
+    if (words > c->mask_words_cap) {  // a wider rule library: window masks of `words` words per block
+      if (c->side) CK(cudaStreamSynchronize(c->side));
+      const uint64_t NB = std::max<uint64_t>(c->max_blocks, 1);
+      uint32_t* nb = nullptr;
+      uint32_t* na = nullptr;
+      CK(cudaMalloc(&nb, NB * words * 4));
+      if (cudaMalloc(&na, NB * words * 4) != cudaSuccess) {
+        cudaFree(nb);
+        throw CudaError("cudaMalloc: rule mask words");
+      }
+      for (auto& p : c->owned)
+        if (p == c->bmask || p == c->alt_bmask) {
+          cudaFree(p);
+          p = p == c->bmask ? static_cast<void*>(nb) : static_cast<void*>(na);
+        }
+      c->bmask = nb;
+      c->alt_bmask = na;
+      c->mask_words_cap = words;
+    }
+    c->mask_words = words;
   } catch (...) {
     for (auto& g : gs) free_group(g);
     throw;
@@ -535,6 +567,11 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
   // SMs: the one-CTA-per-SM kernel would otherwise hold every SM until it ends and serialise the
   // commit behind it (measured: 1.13 ms per config-2 step at full grid, 0.97 at a quarter)
   static const int pf_frac = getenv("SKV_H16_PF_FRAC") ? atoi(getenv("SKV_H16_PF_FRAC")) : 4;
+  const uint64_t NB = std::max<uint64_t>(c->max_blocks, 1);
+  if (c->mask_words > 1) {  // words >= 1 are only OR-ed into by their groups
+    const uint64_t nb = std::min<uint64_t>(NB, std::max<uint64_t>(nb_hint, n_tokens / c->cfg.block_tokens));
+    for (uint32_t w = 1; w < c->mask_words; ++w) CK(cudaMemsetAsync(bmask + w * NB, 0, nb * 4, st));
+  }
   // one pass per rule group: the first stores the digests and the window masks, the others OR
   // their masks in at their rules' bits (a rule set larger than one device automaton)
   for (size_t gi = 0; gi < c->groups.size(); ++gi) {
@@ -559,7 +596,7 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
       h.mask_shift = g.shift;
       h.first = gi == 0;
       h.d_out = bd;
-      h.mask_out = bmask;
+      h.mask_out = bmask + g.word * NB;
       h.first_sens = first_sens;
       // a small batch needs fewer CTAs (one 32-warp CTA per SM otherwise)
       const uint64_t want = nb_hint ? (nb_hint + 32 * 32 - 1) / (32 * 32) : static_cast<uint64_t>(R.grid);
@@ -582,7 +619,7 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
     a.mask_shift = g.shift;
     a.first = gi == 0;
     a.d_out = bd;
-    a.mask_out = bmask;
+    a.mask_out = bmask + g.word * NB;
     a.first_sens = first_sens;
     a.off_list = g.layout.off_list;
     a.stage = g.layout.stage;
@@ -625,14 +662,28 @@ void check_usable(const skv_ctx* c) {
 extern "C" {
 
 // ------------------------------------------------------------------ rules
+// A rule set's device automata (consecutive groups, none straddling a 32-rule mask word) and,
+// up to 32 enabled rules, the whole set's automaton (skv_rules_dfa).  Larger libraries keep
+// bit j = j-th enabled rule across skv_rules_mask_words() u32 words per window.
+void compile_set(skv_rules& r) {
+  r.enabled.clear();
+  for (size_t i = 0; i < r.spec.rules.size(); ++i)
+    if (r.spec.rules[i].enabled) r.enabled.push_back(static_cast<uint32_t>(i));
+  if (r.enabled.size() > 32ull * SKV_MAX_MASK_WORDS)
+    throw skv::CompileError("rule set has " + std::to_string(r.enabled.size()) + " enabled rules (device maximum " +
+                            std::to_string(32 * SKV_MAX_MASK_WORDS) + ")");
+  r.groups = skv::compile_rule_groups(r.spec.rules, fits_device);
+  r.whole = r.enabled.size() <= 32;
+  r.dfa = r.whole ? skv::compile_rules(r.spec.rules) : skv::DfaTables{};
+}
+
 int skv_rules_default(skv_rules** out) {
   if (!out) return SKV_ERR_ARG;
   return guard(nullptr, [&] {
     auto r = std::make_unique<skv_rules>();
     r->spec.version = 1;  // RuleEngine() default snapshot version (detection.hpp:210)
     r->spec.rules = skv::default_pattern_rules();
-    r->dfa = skv::compile_rules(r->spec.rules);
-    r->groups = skv::compile_rule_groups(r->spec.rules, fits_device);
+    compile_set(*r);
     *out = r.release();
     return SKV_OK;
   });
@@ -644,8 +695,7 @@ int skv_rules_from_json(const char* json, size_t len, skv_rules** out, char* err
   int rc = guard(&scratch, [&] {
     auto r = std::make_unique<skv_rules>();
     r->spec = skv::parse_rules_json(std::string(json, len));
-    r->dfa = skv::compile_rules(r->spec.rules);
-    r->groups = skv::compile_rule_groups(r->spec.rules, fits_device);
+    compile_set(*r);
     *out = r.release();
     return SKV_OK;
   });
@@ -680,15 +730,15 @@ uint32_t skv_rules_group_count(const skv_rules* r) {
   return r ? static_cast<uint32_t>(r->groups.groups.size()) : 0;
 }
 
-uint32_t skv_rules_enabled_count(const skv_rules* r) {
-  return r ? static_cast<uint32_t>(r->dfa.rule_index.size()) : 0;
-}
+uint32_t skv_rules_enabled_count(const skv_rules* r) { return r ? static_cast<uint32_t>(r->enabled.size()) : 0; }
 uint32_t skv_rules_enabled_rule(const skv_rules* r, uint32_t j) {
-  return (r && j < r->dfa.rule_index.size()) ? r->dfa.rule_index[j] : UINT32_MAX;
+  return (r && j < r->enabled.size()) ? r->enabled[j] : UINT32_MAX;
 }
+uint32_t skv_rules_mask_words(const skv_rules* r) { return r ? mask_words_of(*r) : 0; }
 
 int skv_rules_dfa(const skv_rules* r, skv_dfa_view* v) {
   if (!r || !v) return SKV_ERR_ARG;
+  if (!r->whole) return SKV_ERR_COMPILE;  // more than 32 enabled rules: no single automaton
   v->n_states = r->dfa.n_states;
   v->n_classes = r->dfa.n_classes;
   v->start = r->dfa.start;
@@ -779,6 +829,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->cands = dalloc<uint32_t>(2ull * c->pool_cap, c->owned);
     c->fired = dalloc<uint32_t>(2ull * c->pool_cap, c->owned);
     c->events = dalloc<skv_event>(2ull * c->pool_cap, c->owned);
+    // the epoch reads back its first kEpochEvPre slots with the count (defined contents)
+    CK(cudaMemset(c->events, 0, std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap) * sizeof(skv_event)));
     // batch buffers
     c->max_prompts = cfg->max_prompts;
     c->max_tokens = cfg->max_tokens;
@@ -842,6 +894,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->side_temp = dalloc<uint8_t>(c->side_temp_bytes, c->owned);
     c->temp = dalloc<uint8_t>(tb, c->owned);
     CK(cudaMallocHost(&c->host_small, 64 * sizeof(uint32_t)));
+    CK(cudaMallocHost(&c->host_events, kEpochEvPre * sizeof(skv_event)));
     c->rec_grid = skv::record_grid(c->device);
     // default rules
     skv_rules* r = nullptr;
@@ -925,6 +978,7 @@ int skv_destroy(skv_ctx* c) {
   for (void* p : {c->rep_in, static_cast<void*>(c->rep_slots), static_cast<void*>(c->rep_uidx)})
     if (p) cudaFree(p);
   if (c->host_small) cudaFreeHost(c->host_small);
+  if (c->host_events) cudaFreeHost(c->host_events);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->side) {
@@ -1319,6 +1373,22 @@ int skv_admit_ttft(skv_ctx* c, const uint64_t* request_ids, double* ttft_ms, uin
     if (intra_tokens) CK(cudaMemcpyAsync(intra_tokens, c->d_intra, N * 4ull, outk, s));
     if (inter_tokens) CK(cudaMemcpyAsync(inter_tokens, c->d_inter, N * 4ull, outk, s));
     sync_check(s);
+    return SKV_OK;
+  });
+}
+
+uint32_t skv_mask_words(const skv_ctx* c) { return c ? c->mask_words : 0; }
+
+int skv_last_rule_masks(skv_ctx* c, uint32_t* out, int on_device) {
+  if (!c || !out) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    const uint64_t nb = c->last_n ? c->p_blocks : 0, NB = std::max<uint64_t>(c->max_blocks, 1);
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (nb)
+      CK(cudaMemcpy2DAsync(out, nb * 4, c->bmask, NB * 4, nb * 4, c->mask_words, k, c->stream));
+    sync_check(c->stream);
     return SKV_OK;
   });
 }
@@ -1754,33 +1824,47 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
     const int cur = c->cur, prev = 1 - c->cur;
     const uint32_t bound = 2 * c->pool_cap;
     CK(cudaMemsetAsync(c->counters + 3, 0, 8, s));  // n_cands, n_events
-    skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, stamp,
-                                 c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
-    skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, stamp,
-                                 c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
-    skv::launch_epoch_fire(c->ix, c->cands, c->counters + 3, bound, stamp, epoch, c->events, c->counters + 4, c->fired,
-                           s);
-    skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
-    skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s);
-    skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s);
+    static const bool split = getenv_flag("SKV_EPOCH_SPLIT");  // diagnostic: the six-kernel pass
+    if (!split) {
+      CK(skv::launch_epoch_fused(c->ix, c->touched[cur], c->counters + 1 + cur, c->touched[prev],
+                                 c->counters + 1 + prev, stamp, c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands,
+                                 c->counters + 3, epoch, c->events, c->counters + 4, c->fired, c->counters,
+                                 c->counters + 1 + prev, c->device, s));
+    } else {
+      skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, stamp,
+                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+      skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, stamp,
+                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+      skv::launch_epoch_fire(c->ix, c->cands, c->counters + 3, bound, stamp, epoch, c->events, c->counters + 4,
+                             c->fired, s);
+      skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
+      skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s);
+      skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s);
+    }
     CK(cudaMemcpyAsync(c->host_small, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
+    // the first events ride along with their count (events are rare: one synchronisation)
+    const size_t pre = std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap);
+    CK(cudaMemcpyAsync(c->host_events, c->events, pre * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
     // swap windows: the current list becomes the previous one (its count stays where it
-    // is); the pool and the new current list start empty
-    CK(cudaMemsetAsync(c->counters, 0, 4, s));
-    CK(cudaMemsetAsync(c->counters + 1 + prev, 0, 4, s));
+    // is); the pool and the new current list start empty (the fused pass resets them itself)
+    if (split) {
+      CK(cudaMemsetAsync(c->counters, 0, 4, s));
+      CK(cudaMemsetAsync(c->counters + 1 + prev, 0, 4, s));
+    }
+    CK(cudaEventRecord(c->ev[6], s));
     sync_check(s);
     const uint32_t ne = c->host_small[0];
     std::vector<skv_event> ev(ne);
-    if (ne) {
+    if (ne <= pre) {
+      std::copy(c->host_events, c->host_events + ne, ev.begin());
+    } else {
       CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
       sync_check(s);
     }
     c->cur = prev;
     c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
-    CK(cudaEventRecord(c->ev[6], s));
-    CK(cudaEventSynchronize(c->ev[6]));
     c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += 6;
+    c->times.kernels_launched += split ? 6 : 1;
     std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
       return x.h != y.h ? x.h < y.h : x.d < y.d;
     });
@@ -1898,6 +1982,7 @@ int skv_export(skv_ctx* c, skv_entry* out, size_t cap, size_t* n) {
     uint32_t cnt = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {  // the device count is exact even past the buffer
       dout = dalloc<skv_entry>(room, tmp);
+      CK(cudaMemsetAsync(dout, 0, room * sizeof(skv_entry), s));  // defined struct padding
       CK(cudaMemsetAsync(dn, 0, 4, s));
       skv::launch_export(c->ix, c->users_tab.rev, dout, dn, static_cast<uint32_t>(room), s);
       CK(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, s));
@@ -2436,14 +2521,15 @@ int skv_tier1_scan(skv_ctx* c, const char* text, size_t len, uint32_t* mask) {
     CK(cudaSetDevice(c->device));
     std::vector<void*> tmp;
     uint8_t* dt = dalloc<uint8_t>(len + 1, tmp);
-    uint32_t* dm = dalloc<uint32_t>(1, tmp);
+    const uint32_t words = c->mask_words;
+    uint32_t* dm = dalloc<uint32_t>(words, tmp);
     cudaStream_t s = c->stream;
     if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(dm, 0, 4, s));
-    for (const auto& g : c->groups) skv::launch_scan_text(dt, static_cast<uint32_t>(len), g.dev, dm, g.shift, s);
-    CK(cudaMemcpyAsync(c->host_small, dm, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemsetAsync(dm, 0, 4ull * words, s));
+    for (const auto& g : c->groups)
+      skv::launch_scan_text(dt, static_cast<uint32_t>(len), g.dev, dm + g.word, g.shift, s);
+    CK(cudaMemcpyAsync(mask, dm, 4ull * words, cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    *mask = c->host_small[0];
     for (void* p : tmp) cudaFree(p);
     return SKV_OK;
   });
@@ -2462,14 +2548,15 @@ int skv_tier1_scan_batch(skv_ctx* c, const char* text, const uint64_t* offsets, 
     std::vector<void*> tmp;
     uint8_t* dt = dalloc<uint8_t>(len + 1, tmp);
     uint64_t* doff = dalloc<uint64_t>(n + 1ull, tmp);
-    uint32_t* dm = dalloc<uint32_t>(n, tmp);
+    const uint64_t words = c->mask_words;
+    uint32_t* dm = dalloc<uint32_t>(n * words, tmp);
     cudaStream_t s = c->stream;
     try {
       if (len) CK(cudaMemcpyAsync(dt, text, len, cudaMemcpyHostToDevice, s));
       CK(cudaMemcpyAsync(doff, offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
-      CK(cudaMemsetAsync(dm, 0, n * 4ull, s));
-      for (const auto& g : c->groups) skv::launch_scan_texts(dt, doff, n, g.dev, dm, g.shift, s);
-      CK(cudaMemcpyAsync(rule_masks, dm, n * 4ull, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemsetAsync(dm, 0, n * words * 4, s));
+      for (const auto& g : c->groups) skv::launch_scan_texts(dt, doff, n, g.dev, dm + g.word * n, g.shift, s);
+      CK(cudaMemcpyAsync(rule_masks, dm, n * words * 4, cudaMemcpyDeviceToHost, s));
       sync_check(s);
     } catch (...) {
       for (void* p : tmp) cudaFree(p);

@@ -355,6 +355,13 @@ void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n
                        cudaStream_t s);
 void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
                             cudaStream_t s);
+// the whole epoch pass (candidates, fire, propagate, rolls, window-swap resets) in one
+// cooperative launch
+cudaError_t launch_epoch_fused(const Index& ix, const uint32_t* cur_list, uint32_t* n_cur, const uint32_t* prev_list,
+                               const uint32_t* n_prev, uint32_t stamp, double jump, uint64_t u_pre_max,
+                               uint32_t* cands, uint32_t* n_cands, uint64_t epoch, void* events, uint32_t* n_events,
+                               uint32_t* fired, uint32_t* pool_count, uint32_t* prev_count, int device,
+                               cudaStream_t s);
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
                        cudaStream_t s);
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,

@@ -60,15 +60,27 @@ __device__ __forceinline__ uint32_t h16_step_any(const uint8_t* __restrict__ tab
 }
 
 // exact run over tokens[tok, tok+len) from base state v: OR of the enabled-rule masks of
-// every accepting transition (the global transition table)
-__device__ __forceinline__ uint32_t h16_exact(const uint32_t* __restrict__ full, uint32_t S,
+// every accepting transition.  The walk steps through the SMEM image (an accepting
+// transition lands in a shadow state: the walk notes it and continues from the state's base
+// copy) and reads the global [256][S] table only at accepting transitions, so its
+// dependent chain is SMEM latency, not L2 latency (a small batch's flagged windows are its
+// tail: config 1 spends most of the kernel here otherwise)
+__device__ __forceinline__ uint32_t h16_exact(const uint8_t* __restrict__ tab, const uint16_t* __restrict__ hi,
+                                              uint32_t colbytes, uint32_t s2, const uint32_t* __restrict__ full,
                                               const uint32_t* __restrict__ tokens, uint64_t tok, uint32_t len,
                                               uint32_t v) {
+  const uint32_t S = s2 >> 1;
   uint32_t m = 0;
+#pragma unroll 4
   for (uint32_t j = 0; j < len; ++j) {
-    const uint32_t e = __ldg(full + (tokens[tok + j] & 0xffu) * S + (v >> 1));
-    m |= e >> 16;
-    v = e & 0xffffu;
+    const uint32_t b = tokens[tok + j] & 0xffu;
+    const uint32_t nv = h16_step_any(tab, hi, colbytes, v, b);
+    if (nv >= s2) {  // accepting transition out of base state v
+      m |= __ldg(full + b * S + (v >> 1)) >> 16;
+      v = nv - s2;
+    } else {
+      v = nv;
+    }
   }
   return m;
 }
@@ -123,13 +135,13 @@ struct H16Task {
   uint32_t gb, p;
 };
 
-__device__ __forceinline__ void h16_flush(H16Task* q, uint32_t qn, uint32_t lane, const HS16Args& a) {
+__device__ __forceinline__ void h16_flush(H16Task* q, uint32_t qn, uint32_t lane, const HS16Args& a,
+                                          const uint8_t* __restrict__ tab) {
   __syncwarp();
-  const uint32_t S = a.s2 >> 1;
   for (uint32_t k = lane; k < qn; k += 32) {
     const H16Task t = q[k];
-    const uint32_t m = h16_exact(a.full, S, a.tokens, t.tokv & 0xffffffffffull, (t.tokv >> 40) & 63u,
-                                 static_cast<uint32_t>(t.tokv >> 46));
+    const uint32_t m = h16_exact(tab, a.hi, a.colbytes, a.s2, a.full, a.tokens, t.tokv & 0xffffffffffull,
+                                 (t.tokv >> 40) & 63u, static_cast<uint32_t>(t.tokv >> 46));
     if (m) {
       atomicOr(&a.mask_out[t.gb], m << a.mask_shift);
       atomicMin(&a.first_sens[t.p], t.gb - a.blk_off[t.p]);
@@ -170,6 +182,7 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
     prev_s = cur_s > 0 ? a.blk_off[pp] : cur_s;
     next_p = h16_nonempty(a.blk_off, N, cur_p + 1);
     next_e = next_p < N ? a.blk_off[next_p + 1] : cur_e;
+    __syncwarp();  // every lane's reads of the previous slots precede their rewrite
     if (lane < 3) {
       const uint32_t sp = lane == 0 ? pp : (lane == 1 ? cur_p : next_p);
       slots[lane] = h16_slot(a, sp);
@@ -184,10 +197,11 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
     // advance the slots to the prompt of block g (at most one step for prompts >= 32 blocks)
     if (g >= cur_e && g < nb) {
       if (g < next_e) {
-        if (lane < 2) {
-          slots[lane] = slots[lane + 1];
-          slot_p[lane] = slot_p[lane + 1];
-        }
+        Slot16 nx{};
+        uint32_t nxp = 0;
+        if (lane < 2) nx = slots[lane + 1], nxp = slot_p[lane + 1];
+        __syncwarp();  // reads (this shift's and the previous chunk's) before the writes
+        if (lane < 2) slots[lane] = nx, slot_p[lane] = nxp;
         __syncwarp();
         prev_s = cur_s;
         cur_s = cur_e;
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
       const uint32_t c0 = __ballot_sync(kFull, cnt & 1u), c1 = __ballot_sync(kFull, cnt >> 1);
       const uint32_t tot = __popc(c0) + 2 * __popc(c1);
       if (qn + tot > a.q_cap) {  // q_cap >= 96 = 3 segments x 32 lanes
-        h16_flush(q, qn, lane, a);
+        h16_flush(q, qn, lane, a, tab);
         qn = 0;
       }
       const uint32_t lt = (1u << lane) - 1u;
@@ -406,5 +420,5 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
       qn += tot;
     }
   }
-  h16_flush(q, qn, lane, a);
+  h16_flush(q, qn, lane, a, tab);
 }

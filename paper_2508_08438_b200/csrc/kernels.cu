@@ -12,6 +12,7 @@
 //                 set_label propagation (cache_index.hpp:654-685), AccessStats::roll
 // No tensor cores: nothing here is a contraction.  Everything is integer/byte work
 // bounded by HBM, shared-memory lookups or memory latency.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "../../include/safekv_b200.h"
@@ -1277,6 +1278,10 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
   const uint32_t nmax = __reduce_max_sync(kFull, n);
   for (uint32_t t0 = 0; t0 < nmax; t0 += 32) {
     const uint32_t b = t0 + lane;
+    // keys precomputed: tiles past every prompt's first miss are not read at all (config 2:
+    // half of the key and digest rows)
+    if constexpr (kPre)
+      if (!__ballot_sync(kFull, has && k == n && n > t0)) break;
     // all the warp's prompts' digest rows in flight at once (cp.async: global -> SMEM)
     for (uint32_t j = 0; j < kCPPrompts; ++j) {
       const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
@@ -2043,6 +2048,100 @@ __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const 
   }
 }
 
+// The whole epoch pass in ONE cooperative launch (grid syncs between the phases instead of
+// six kernel boundaries): a small batch's epoch is otherwise launch-bound (config 1 / 5:
+// ~50 us of mostly empty grids sized for the window lists' capacity).  Same phases, same
+// order, each a grid-stride loop over the device-side list lengths:
+//   candidates (current list, then the untouched previous-window entries) | fire (an
+//   ancestor marked this epoch suppresses, monitor.hpp:88-95) | propagate | roll previous |
+//   roll current; then the window swap's counter resets.
+__device__ __forceinline__ void epoch_candidate(Index& ix, uint32_t s, bool only_untouched, uint32_t stamp,
+                                                double jump, uint64_t u_pre_max, uint32_t* cands,
+                                                uint32_t* n_cands) {
+  if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
+  if (!meta_live(ix.e[s].rec.meta) || meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
+  Stats st = ix.e[s].stats;
+  if (st.hit_pre == 0) return;
+  double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
+  double prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
+  if ((now - prev) >= jump && static_cast<uint64_t>(st.u_pre) <= u_pre_max) {
+    ix.e[s].aux.mark = stamp;
+    cands[atomicAdd(n_cands, 1u)] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_epoch_fused(Index ix, const uint32_t* __restrict__ cur_list,
+                                                     uint32_t* n_cur, const uint32_t* __restrict__ prev_list,
+                                                     const uint32_t* __restrict__ n_prev, uint32_t stamp, double jump,
+                                                     uint64_t u_pre_max, uint32_t* cands, uint32_t* n_cands,
+                                                     uint64_t epoch, DevEvent* events, uint32_t* n_events,
+                                                     uint32_t* fired, uint32_t* pool_count, uint32_t* prev_count) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  const uint32_t nc = *n_cur, np = *n_prev;
+  for (uint32_t i = t0; i < nc + np; i += T)
+    epoch_candidate(ix, i < nc ? cur_list[i] : prev_list[i - nc], i >= nc, stamp, jump, u_pre_max, cands, n_cands);
+  grid.sync();
+  const uint32_t nk = *n_cands;
+  for (uint32_t i = t0; i < nk; i += T) {
+    const uint32_t s = cands[i];
+    bool sup = false;
+    for (uint32_t a = ix.e[s].rec.parent; a != kNone && !sup; a = ix.e[a].rec.parent) sup = ix.e[a].aux.mark == stamp;
+    if (sup) continue;
+    Stats st = ix.e[s].stats;
+    const Rec& r = ix.e[s].rec;
+    const uint32_t e = atomicAdd(n_events, 1u);
+    DevEvent ev;
+    ev.h = r.h;
+    ev.d = r.d;
+    ev.owner = static_cast<uint8_t>(meta_owner(r.meta));
+    ev.action = ev.owner == 0 ? SKV_ACTION_DOWNGRADE : SKV_ACTION_RESTRICT;
+    for (int k = 0; k < 6; ++k) ev.pad[k] = 0;
+    ev.now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
+    ev.prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
+    ev.u_pre = st.u_pre;
+    ev.epoch = epoch;
+    events[e] = ev;
+    fired[e] = s;
+  }
+  grid.sync();
+  const uint32_t nf = *n_events;
+  for (uint32_t i = t0; i < nf; i += T) {
+    const uint32_t root = fired[i];
+    const uint32_t lab = meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+    ix.e[root].rec.meta = (ix.e[root].rec.meta & ~3u) | lab;
+    uint32_t cur = ix.e[root].rec.first_child;
+    while (cur != kNone) {
+      ix.e[cur].rec.meta = (ix.e[cur].rec.meta & ~3u) | lab;
+      const uint32_t c = ix.e[cur].rec.first_child;
+      if (c != kNone) {
+        cur = c;
+        continue;
+      }
+      while (cur != root && ix.e[cur].aux.next_sibling == kNone) cur = ix.e[cur].rec.parent;
+      if (cur == root) break;
+      cur = ix.e[cur].aux.next_sibling;
+    }
+  }
+  for (uint32_t i = t0; i < np; i += T) {  // the previous window's untouched entries roll to zero
+    const uint32_t s = prev_list[i];
+    if (ix.e[s].aux.set_idx != kNone) continue;  // rolled below with the current window
+    ix.e[s].stats = Stats{0, 0, 0, 0};
+  }
+  grid.sync();
+  for (uint32_t i = t0; i < nc; i += T) {
+    const uint32_t s = cur_list[i];
+    const Stats st = ix.e[s].stats;
+    ix.e[s].stats = Stats{0, 0, st.hit_cur, st.u_cnt};
+    ix.e[s].aux.set_idx = kNone;
+  }
+  if (t0 == 0) {  // the window swap: the pool and the list that becomes current start empty
+    *pool_count = 0;
+    *prev_count = 0;
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // misc: tiers, export, per-call wrappers
 // ---------------------------------------------------------------------------------
@@ -2662,6 +2761,32 @@ void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n
 void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
                             cudaStream_t s) {
   if (grid_n) k_epoch_propagate<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, fired, n_events);
+}
+
+int epoch_fused_grid(int device) {
+  static int grid[16] = {};
+  if (device < 0 || device >= 16) return 0;
+  if (!grid[device]) {
+    int per_sm = 0, n_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_epoch_fused, 256, 0) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+      return 0;
+    grid[device] = std::max(1, std::min(per_sm, 2) * n_sm);
+  }
+  return grid[device];
+}
+
+cudaError_t launch_epoch_fused(const Index& ix, const uint32_t* cur_list, uint32_t* n_cur, const uint32_t* prev_list,
+                        const uint32_t* n_prev, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
+                        uint32_t* n_cands, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
+                        uint32_t* pool_count, uint32_t* prev_count, int device, cudaStream_t s) {
+  Index ixv = ix;
+  DevEvent* ev = static_cast<DevEvent*>(events);
+  void* args[] = {&ixv, &cur_list, &n_cur, &prev_list, &n_prev, &stamp, &jump, &u_pre_max, &cands, &n_cands,
+                  &epoch, &ev, &n_events, &fired, &pool_count, &prev_count};
+  const int grid = epoch_fused_grid(device);
+  if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epoch_fused), dim3(grid), dim3(256), args, 0, s);
 }
 
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,

@@ -1086,7 +1086,9 @@ RuleGroups compile_rule_groups(const std::vector<PatternRule>& rules,
     return out;
   }
   for (size_t a = 0; a < enabled.size();) {
-    size_t b = std::min(enabled.size(), a + max_group);
+    // a group never straddles a 32-bit mask word (its bits are one word's shifted rule mask)
+    const size_t word_end = (a / 32 + 1) * 32;
+    size_t b = std::min({enabled.size(), a + max_group, word_end});
     DfaTables t = compile_range(a, b);
     while (!fits(t)) {  // shrink until the group's automaton fits the device tables
       if (b - a == 1)
@@ -1095,7 +1097,7 @@ RuleGroups compile_rule_groups(const std::vector<PatternRule>& rules,
       t = compile_range(a, b);
     }
     // grow back one rule at a time while it still fits (halving may have overshot)
-    while (b < enabled.size() && b - a < max_group) {
+    while (b < enabled.size() && b - a < max_group && b < word_end) {
       DfaTables t2 = compile_range(a, b + 1);
       if (!fits(t2)) break;
       t = std::move(t2);

@@ -88,6 +88,11 @@ class RuleSet:
         n = self._lib.skv_rules_enabled_count(self._h)
         return [int(self._lib.skv_rules_enabled_rule(self._h, j)) for j in range(n)]
 
+    def mask_words(self) -> int:
+        """u32 words of a window's device mask (bit j = j-th enabled rule; > 32 enabled rules
+        take more than one word)."""
+        return int(self._lib.skv_rules_mask_words(self._h))
+
     def to_rule_mask(self, device_mask: int) -> int:
         """Device mask (bit j = j-th enabled rule) -> mask over rule-list positions."""
         m = 0
@@ -133,12 +138,13 @@ class AdmitResult:
     block_h: np.ndarray         # uint64 per block
     block_d: np.ndarray
     label: np.ndarray           # uint8 per block (0 Private, 1 Public)
-    rule_mask: np.ndarray       # uint32 per block (bit j = j-th enabled rule)
+    rule_mask: np.ndarray       # uint32 per block (bit j = j-th enabled rule; word 0 of the mask)
     decision: np.ndarray        # uint8 per block (0 miss, 1 public hit, 2 owner hit)
     matched_blocks: np.ndarray  # uint32 per prompt
     lowest_tier: np.ndarray     # uint8 per prompt
     n_blocks: int = 0
     matched_total: int = 0
+    rule_mask_words: Optional[np.ndarray] = None  # [words, n_blocks] when > 32 rules are enabled
 
 
 @dataclass
@@ -243,6 +249,8 @@ class AdmissionEngine:
         self._check(self._lib.skv_admit(self._h, C.byref(b), C.byref(o)))
         res.n_blocks, res.matched_total = int(o.n_blocks), int(o.matched_total)
         self._last_blocks = res.n_blocks
+        if int(self._lib.skv_mask_words(self._h)) > 1:  # a rule library of more than 32 enabled rules
+            res.rule_mask_words = self.last_rule_masks()
         return res
 
     def admit_raw(self, batch: N.Batch, out: Optional[N.AdmitOut] = None) -> None:
@@ -464,9 +472,17 @@ class AdmissionEngine:
         Returns the device rule mask; ``self.rules.categories(mask)`` gives the verdict's
         category list and ``mask != 0`` its ``sensitive`` flag."""
         raw = text.encode("latin-1") if isinstance(text, str) else bytes(text)
-        m = C.c_uint32()
-        self._check(self._lib.skv_tier1_scan(self._h, raw, len(raw), C.byref(m)))
-        return int(m.value)
+        m = np.zeros(max(1, int(self._lib.skv_mask_words(self._h))), np.uint32)
+        self._check(self._lib.skv_tier1_scan(self._h, raw, len(raw), _ptr(m)))
+        return combine_mask_words(m[:, None])[0]
+
+    def last_rule_masks(self) -> np.ndarray:
+        """The last admitted batch's full window masks, ``[mask words, n_blocks]`` uint32
+        (word 0 is ``AdmitResult.rule_mask``); ``combine_mask_words`` gives one int per block."""
+        w = int(self._lib.skv_mask_words(self._h))
+        out = np.zeros((w, getattr(self, "_last_blocks", 0)), np.uint32)
+        self._check(self._lib.skv_last_rule_masks(self._h, _ptr(out), 0))
+        return out
 
     def token_seq_digest(self, tokens: Sequence[int]) -> int:
         """``safekv::token_seq_digest`` (core.hpp:68-73) on the device."""
@@ -474,6 +490,18 @@ class AdmissionEngine:
         d = C.c_uint64()
         self._check(self._lib.skv_token_seq_digest(self._h, _ptr(t), len(t), C.byref(d)))
         return int(d.value)
+
+
+def combine_mask_words(words: np.ndarray) -> list[int]:
+    """``[mask words, n]`` uint32 device masks -> one Python int per window (bit j = j-th
+    enabled rule, any number of words)."""
+    words = np.asarray(words, np.uint32)
+    out = [0] * words.shape[1]
+    for w in range(words.shape[0]):
+        nz = np.nonzero(words[w])[0]
+        for i in nz:
+            out[i] |= int(words[w, i]) << (32 * w)
+    return out
 
 
 # skv_rep_entry / skv_rep_access (include/safekv_b200.h)

@@ -148,6 +148,9 @@ SIGNATURES = {
     "skv_rules_group_count": (C.c_uint32, [C.c_void_p]),
     "skv_rules_enabled_count": (C.c_uint32, [C.c_void_p]),
     "skv_rules_enabled_rule": (C.c_uint32, [C.c_void_p, C.c_uint32]),
+    "skv_rules_mask_words": (C.c_uint32, [C.c_void_p]),
+    "skv_mask_words": (C.c_uint32, [C.c_void_p]),
+    "skv_last_rule_masks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "skv_rules_dfa": (C.c_int, [C.c_void_p, C.POINTER(DfaView)]),
     "skv_config_default": (None, [C.POINTER(Config)]),
     "skv_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
@@ -186,7 +189,7 @@ SIGNATURES = {
                                     C.POINTER(C.c_int)]),
     "skv_leak_flags": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.POINTER(C.c_uint64)]),
-    "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint32)]),
+    "skv_tier1_scan": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.c_void_p]),
     "skv_stage": (C.c_int, [C.c_void_p, C.c_void_p]),
     "skv_set_tier_budget": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64]),
     "skv_tier_usage": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

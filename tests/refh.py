@@ -37,6 +37,8 @@ def load_ref():
         "ref_rules_count": (C.c_uint32, [vp]),
         "ref_rules_verdict": (C.c_int, [vp, C.c_char_p, sz, C.c_char_p, sz]),
         "ref_rules_mask": (C.c_uint64, [vp, C.c_char_p, sz]),
+        "ref_rules_mask_wide": (None, [vp, C.c_char_p, sz, vp, sz]),
+        "ref_engine_set_stock_scan": (None, [vp, C.c_int]),
         "ref_scan_windows": (C.c_uint64, [vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_int]),
         "ref_token_seq_digest": (C.c_uint64, [vp, sz]),
         "ref_fnv1a64_bytes": (C.c_uint64, [vp, sz]),
@@ -93,6 +95,12 @@ class RefRules:
     def mask(self, text: bytes) -> int:
         return int(self.L.ref_rules_mask(self.h, text, len(text)))
 
+    def mask_wide(self, text: bytes, n_rules: int) -> int:
+        """Per-rule hit bits of every rule of the list (bit i = rule i), any library size."""
+        w = np.zeros((n_rules + 63) // 64, np.uint64)
+        self.L.ref_rules_mask_wide(self.h, text, len(text), w.ctypes.data, len(w))
+        return sum(int(x) << (64 * i) for i, x in enumerate(w))
+
     def verdict(self, text: bytes) -> tuple[bool, list[str]]:
         buf = C.create_string_buffer(4096)
         s = self.L.ref_rules_verdict(self.h, text, len(text), buf, len(buf))
@@ -113,6 +121,10 @@ class RefEngine:
         if self.h:
             self.L.ref_engine_free(self.h)
             self.h = None
+
+    def set_stock_scan(self, on: bool = True):
+        """One stock CompiledRuleSet::scan per window: mask = the window's sensitive flag."""
+        self.L.ref_engine_set_stock_scan(self.h, 1 if on else 0)
 
     def set_rules(self, rules: "RefRules"):
         """Reload between batches (RuleEngine::load_rules swap, detection.hpp:238-241)."""

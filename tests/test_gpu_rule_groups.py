@@ -116,3 +116,69 @@ def test_hot_reload_parity(ref, gpu):
                     check_index(eng, re_)
         finally:
             re_.close()
+
+
+def windows_of(tokens, offsets, B, W):
+    """A.3 window texts: tokens[bB : min(L, (b+1)B + W)] of every full block, prompt-major."""
+    out = []
+    for p in range(len(offsets) - 1):
+        t = tokens[int(offsets[p]):int(offsets[p + 1])].astype(np.uint8).tobytes()
+        for b in range(len(t) // B):
+            out.append(t[b * B:min(len(t), (b + 1) * B + W)])
+    return out
+
+
+@pytest.mark.parametrize("B,W", [(16, 32), (8, 16)])
+def test_wide_rule_library_parity(ref, gpu, B, W):
+    """A library of more than 32 enabled rules (three mask words) on both scan kernels: every
+    window's full per-rule mask equals the reference's per-rule verdicts, the category list of a
+    sample of windows equals the stock CompiledRuleSet::scan's (rule order, de-duplicated), and
+    labels, matches, decisions, events and the index equal the reference engine's (one stock scan
+    per window)."""
+    from paper_2508_08438_b200 import combine_mask_words
+    from test_rules_compiler import wide_library
+    text, words = wide_library()
+    rs = RuleSet.from_json(text)
+    assert rs.mask_words() >= 3
+    n_rules = rs.size()
+    rr = RefRules(ref, text)
+    vocab = [f"{w}{i}" for i, w in enumerate(words * 8)] + [f"{w.upper()}-{i}" for i, w in enumerate(words * 8)] + words
+    rng = np.random.default_rng(B)
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 16, max_prompts=512, max_tokens=1 << 18,
+                       max_window_entries=1 << 14)
+    with AdmissionEngine(cfg) as eng:
+        eng.set_rules(rs)
+        re_ = RefEngine(ref, rr, B=B, W=W)
+        re_.set_stock_scan(True)
+        try:
+            hits_hi = 0
+            for _ in range(3):
+                batch = make_batch(rng, vocab, 120, 5)
+                got = eng.admit(*batch)
+                exp = re_.admit(*batch)
+                assert got.rule_mask_words is not None and got.rule_mask_words.shape[0] == rs.mask_words()
+                np.testing.assert_array_equal(got.rule_mask_words[0], got.rule_mask)
+                dev = combine_mask_words(got.rule_mask_words)
+                wins = windows_of(batch[0], batch[1], B, W)
+                assert len(wins) == got.n_blocks
+                for i, t in enumerate(wins):
+                    assert rs.to_rule_mask(dev[i]) == rr.mask_wide(t, n_rules), (i, t)
+                for i in range(0, len(wins), 7):
+                    assert (dev[i] != 0, rs.categories(dev[i])) == rr.verdict(wins[i]), (i, wins[i])
+                hits_hi += sum(1 for m in dev if m >> 32)
+                np.testing.assert_array_equal(got.block_h, exp["block_h"])
+                np.testing.assert_array_equal(np.array([m != 0 for m in dev], np.uint64), exp["mask"])
+                for k in ("label", "decision", "matched_blocks", "lowest_tier"):
+                    np.testing.assert_array_equal(getattr(got, k), exp[k], k)
+                eng.commit()
+                re_.commit()
+                _, ev_g = eng.epoch_pass()
+                check_events(ev_g, re_.epoch()[1])
+                check_index(eng, re_)
+            assert hits_hi > 0  # rules beyond the first mask word fired
+            # per-call tier1_scan and the facade's batch scan across the words
+            for t in wins[:64:5] + [b"acct13 Q7 q41abz", f"{words[1].upper()}-85 x".encode()]:
+                m = eng.tier1_scan(t)
+                assert rs.to_rule_mask(m) == rr.mask_wide(t, n_rules)
+        finally:
+            re_.close()

@@ -160,3 +160,41 @@ def test_disabled_and_blacklist_semantics():
     texts = [b"danger zone", b"TERM", b"(x)", b"x", b"a b", b"(Q.Q).", b"Q.Q\x0bz", b"Q.Q\tz"]
     m = [rs.to_rule_mask(int(x)) for x in run_dfa(rs.dfa(), texts)]
     assert m == [0, 0, 0, 0, 0, 1 << 5, 0, 1 << 5]
+
+
+def wide_library(n_rules=90, seed=5):
+    """A rule library of more than 32 enabled rules (several mask words): regexes and blacklist
+    terms over a small vocabulary, a handful disabled, categories shared across rules."""
+    rng = np.random.default_rng(seed)
+    words = ["acct", "iban", "pin", "token", "secret", "badge", "vin", "mrn", "npi", "dea", "swift", "sort"]
+    rules = []
+    for i in range(n_rules):
+        w = words[i % len(words)]
+        if i % 5 == 0:
+            rules.append({"rule_id": f"bl{i}", "category": f"Cat{i % 7}", "kind": "blacklist",
+                          "pattern": f"{w.upper()}-{i}"})
+        else:
+            rules.append({"rule_id": f"rx{i}", "category": f"Cat{(i * 3) % 11}", "kind": "regex",
+                          "pattern": f"\\b{w}{i}[0-9]{{{1 + i % 3}}}\\b|q{i}[a-c]+z",
+                          "enabled": i % 17 != 3})
+    return json.dumps({"version": 21, "rules": rules}), words
+
+
+def test_wide_rule_library_loads():
+    """More than 32 enabled rules load as several mask words (the reference
+    loads a library of any size, detection.hpp:222-242); the single-automaton view is refused."""
+    text, _ = wide_library()
+    rs = RuleSet.from_json(text)
+    en = rs.enabled_rules()
+    assert len(en) == sum(1 for r in json.loads(text)["rules"] if r.get("enabled", True))
+    assert rs.mask_words() == (len(en) + 31) // 32 >= 3
+    assert rs.group_count() >= rs.mask_words()
+    with pytest.raises(CompileError):
+        rs.dfa()
+    assert RuleSet.default().mask_words() == 1
+
+
+def test_rule_library_maximum():
+    rules = [{"rule_id": f"t{i}", "category": "C", "kind": "blacklist", "pattern": f"TERM{i}"} for i in range(1025)]
+    with pytest.raises(CompileError):
+        RuleSet.from_json(json.dumps({"version": 1, "rules": rules}))

@@ -19,8 +19,10 @@ own = torch.from_numpy(w["owners"].astype(np.uint8)).to(dev)
 n = len(w["offsets"]) - 1
 cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 18, max_prompts=4096, max_tokens=1 << 20,
                    max_window_entries=1 << 15)
+REPS = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 25
+SKIP = 5 if REPS > 5 else 0
 cold, warm = [], []
-for rep in range(25):
+for rep in range(REPS):
     with AdmissionEngine(cfg) as eng:
         s = torch.cuda.ExternalStream(eng.stream)
         b = N.Batch(tok.data_ptr(), off.data_ptr(), usr.data_ptr(), own.data_ptr(), n, int(w["offsets"][-1]), 1)
@@ -33,7 +35,7 @@ for rep in range(25):
             eng.epoch_pass()
             e1.record(s)
             torch.cuda.synchronize()
-            if rep >= 5:
+            if rep >= SKIP:
                 out.append(e0.elapsed_time(e1) * 1e3)
 print(json.dumps({"workload": "config 1: 1000 x 112-token prompts (golden), B=16, W=32", "blocks": 7000,
                   "us_per_batch_cold_index": float(np.median(cold)), "us_per_batch_warm_index": float(np.median(warm))}))
