@@ -820,6 +820,10 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->pool_cap = static_cast<uint32_t>(cfg->max_window_entries);
     c->set_hdr = dalloc<skv::SetHdr>(c->pool_cap, c->owned);
     c->set_tab = dalloc<ulonglong2>(static_cast<size_t>(c->pool_cap) * skv::kSetSlots, c->owned);
+    // slots are live by their window stamp: a fresh pool must hold none (memory reused from an
+    // earlier context would otherwise carry its stamps)
+    CK(cudaMemsetAsync(c->set_tab, 0, static_cast<size_t>(c->pool_cap) * skv::kSetSlots * sizeof(ulonglong2), c->stream));
+    CK(cudaMemsetAsync(c->set_hdr, 0, static_cast<size_t>(c->pool_cap) * sizeof(skv::SetHdr), c->stream));
     c->replay = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[0] = dalloc<uint32_t>(c->pool_cap, c->owned);
     c->touched[1] = dalloc<uint32_t>(c->pool_cap, c->owned);

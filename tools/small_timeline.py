@@ -17,7 +17,7 @@ dev = torch.device("cuda", 0)
 def run(name, tok, off, usr, own, steps=30, fresh=False, batches=None):
     n = len(off) - 1
     cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 24, max_prompts=max(n, 4096),
-                       max_tokens=max(int(off[-1]), 1 << 20), max_window_entries=1 << 18)
+                       max_tokens=max(int(off[-1]), 1 << 20), max_window_entries=1 << 20)
     tk = [torch.from_numpy(t.astype(np.uint32).view(np.int32)).to(dev) for t in (batches or [tok])]
     of = torch.from_numpy(off.astype(np.uint64).view(np.int64)).to(dev)
     us = torch.from_numpy(usr.astype(np.uint64).view(np.int64)).to(dev)
