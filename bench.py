@@ -406,7 +406,12 @@ def run_ours(args):
         from paper_2508_08438_b200 import split_batch
         pool = split_batch(pt, po, pu, pw, pr, rank)
         pool_gids = np.flatnonzero(pr == rank).astype(np.uint64)
-    pipeline = not args.no_pipeline
+    # small batches (configs 1 and 5) are bound by host round trips, not by their kernels: one
+    # skv_step call per step (CUDA-graph replayed admit / commit / epoch, one synchronisation)
+    # instead of the stages-1-2 prefetch pipeline of the large batches
+    fused_step = bool(args.fused_step)
+    fused_step = fused_step and not rep_depth
+    pipeline = not args.no_pipeline and not fused_step
     replica = {}
 
     def fresh_engine():
@@ -458,6 +463,9 @@ def run_ours(args):
     # one step = admit(k) [+ stage batch k+1's stages 1-2 (and, e2e, its H2D) on the side
     # stream, overlapping] + commit(k) + epoch; nxt is None at the edge of a timed region
     def step_device(eng, k, nxt):
+        if fused_step:  # skv_step: admit + commit + epoch in one call (small batches)
+            eng.step_raw(dev_batch(k))
+            return
         eng.admit_raw(dev_batch(k))
         if nxt is not None:
             eng.prefetch_raw(dev_batch(nxt))
@@ -552,7 +560,7 @@ def run_ours(args):
     ms_dev, hs, launches, last, pf_dev = timed(step_device, clocks)
     clk = clocks.stop()
     per_dev = timed.per_step
-    ms_e2e, _, _, _, pf_e2e = timed(step_host)
+    ms_e2e, _, _, _, pf_e2e = timed(step_host, pipe=not args.no_pipeline)
     hs_overlapped = float(np.mean(hs))
     if pipeline:
         # roofline pass: the same device steps without skv_prefetch, so every k_hash_scan
@@ -647,7 +655,10 @@ def run_ours(args):
                                    if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
                                 f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
-                                if pipeline else "off")},
+                                if pipeline else
+                                ("device arm: one skv_step per step (CUDA-graph replayed admit/commit/epoch, one "
+                                 f"synchronisation); e2e arm: skv_stage/skv_prefetch ({pf_e2e}/{steps} prefetched)"
+                                 if fused_step else "off"))},
         "stage_ms_last": {k: round(float(last[k]), 4) for k in ("hash_scan_ms", "chain_probe_ms", "record_ms",
                                                                   "admit_total_ms", "commit_ms", "epoch_ms")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -694,6 +705,8 @@ def main():
                          "6 = one shared 8,192-token system prompt)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
+    ap.add_argument("--fused-step", type=int, default=None, choices=[0, 1],
+                    help="device arm: one skv_step call per step instead of the prefetch pipeline (default 0)")
     ap.add_argument("--e2e-u32", action="store_true", help="e2e arm: send uint32 TokenIds instead of byte tokens")
     ap.add_argument("--rep-depth", type=int, default=-1,
                     help="N > 1: replicated-layer depth (-1 = the workload's default: 512 for 6, else 0)")

@@ -169,6 +169,12 @@ int skv_admit(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out);
 /* The last admitted batch's full window rule masks: skv_mask_words(ctx) words per block,
  * word-major (out[w * n_blocks + b]); valid until the next skv_admit or skv_set_rules. */
 int skv_last_rule_masks(skv_ctx* ctx, uint32_t* out, int on_device);
+/* CUDA graphs for small batches (default on; SKV_GRAPHS=0 in the environment turns the default
+ * off): a device-resident batch admitted without per-block outputs (no eviction, budgets,
+ * replicated layer or prefetch) replays its admit, commit and epoch launches from graphs captured
+ * once per buffer set; the per-step stamps come from a device-side step state.  Results are
+ * identical either way; only the host issue cost differs. */
+int skv_set_graphs(skv_ctx* ctx, int on);
 /* mask words of the context's active rule set (skv_rules_mask_words of it) */
 uint32_t skv_mask_words(const skv_ctx* ctx);
 /* Cross-batch pipelining: stage the NEXT device-resident batch's digests and window
@@ -216,6 +222,13 @@ int skv_set_monitor_config(skv_ctx* ctx, double entropy_jump, uint64_t u_pre_max
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
 /* The events of the last skv_epoch (sorted by (h, d)); *n_events = their total count. */
 int skv_last_events(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events);
+/* skv_admit (no per-block outputs) + skv_commit + skv_epoch of one batch in one call, with one
+ * host synchronisation in the common case: the epoch pass is queued right behind the commit and
+ * aborts itself on the device when the commit failed or needs its ordered replay (it then runs
+ * after the replay).  Same results and errors as the three calls (A.1 with K = 1); the path for
+ * small batches, whose step is otherwise bound by host round trips. */
+int skv_step(skv_ctx* ctx, const skv_batch* batch, uint64_t* new_entries, skv_event* events, size_t cap,
+             size_t* n_events, uint64_t* epoch_out);
 
 /* Label landing.  With pending != 0, skv_commit stores new entries
  * as PendingPrivate (visible to their creator only, like the reference's freshly inserted

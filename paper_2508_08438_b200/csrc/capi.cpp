@@ -34,6 +34,7 @@ struct skv_rules {
 #endif
 constexpr bool kRecordBeside = SKV_REC_BESIDE != 0;
 constexpr size_t kEpochEvPre = 128;  // events read back with an epoch's count
+constexpr int kEpochCountSlot = 56;  // host_small word of the epoch's event count
 #ifndef SKV_STREAM_PRIO
 #define SKV_STREAM_PRIO 0
 #endif
@@ -315,6 +316,25 @@ struct skv_ctx {
   unsigned long long* nb_dev = nullptr;
   std::vector<uint32_t> dropped;  // prompts of the last commit whose insert could not make room
   int pf_slot = -1;   // slot of the prefetched batch
+
+  // CUDA graphs for small batches (a device-resident batch admitted without per-block outputs,
+  // no eviction / budgets / replicated layer / pending prefetch): each phase's launches are
+  // captured once per buffer set and replayed with one cudaGraphLaunch; the per-step scalars the
+  // kernels need (batch and window stamps, current window list, epoch) come from the device step
+  // state dstate = {batch, wstart, cur, stamp, epoch lo, epoch hi}, copied from pinned host
+  // memory before each launch (one slot per phase).  A small batch's step is otherwise bound by
+  // host issue: ~40 API calls for ~80 us of kernels (config 1).
+  struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uintptr_t> key;
+  };
+  GraphCache g_admit, g_commit, g_epoch;
+  bool graphs = true;
+  bool capturing = false;
+  bool adm_graph = false;    // the pending batch was admitted through its graph
+  uint32_t* dstate = nullptr;
+  uint32_t* hstate = nullptr;  // pinned, 3 x 8 words (admit, commit, epoch)
+  uint64_t rules_gen = 0;      // bumped by upload_rules (the admit graph bakes the rule tables in)
   int use_slot = -1;  // slot of the pending (admitted) batch
 };
 
@@ -538,6 +558,7 @@ void upload_rules(skv_ctx* c, const skv_rules& r) {
   c->groups = std::move(gs);
   c->rules_host = r;
   c->rules_loaded = true;
+  ++c->rules_gen;
 }
 
 skv::MonCtx monitor_ctx(skv_ctx* c) {
@@ -653,15 +674,69 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// an event record inside a captured phase is an external event node (its timestamps stay
+// readable after the graph ran)
+void rec_ev(skv_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  CK(c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s));
+}
+
+// the device step state of phase `slot` (0 admit, 1 commit, 2 epoch) from the host mirrors
+void put_state(skv_ctx* c, int slot, uint32_t batch, uint64_t epoch, bool armed = false) {
+  uint32_t* h = c->hstate + 8 * slot;
+  h[0] = batch;
+  h[1] = c->wstart;
+  h[2] = static_cast<uint32_t>(c->cur);
+  h[3] = static_cast<uint32_t>(epoch);
+  h[4] = static_cast<uint32_t>(epoch);
+  h[5] = static_cast<uint32_t>(epoch >> 32);
+  h[6] = armed ? 1u : 0u;  // a speculative epoch pass (skv_step)
+  CK(cudaMemcpyAsync(c->dstate, h, 7 * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+}
+
+// Replay `issue` (the phase's launches) from its graph, capturing it first when the key (the
+// buffers and shapes the launches bake in) changed.
+template <typename F>
+void run_graph(skv_ctx* c, skv_ctx::GraphCache& g, const std::vector<uintptr_t>& key, F&& issue) {
+  cudaStream_t s = c->stream;
+  if (!g.exec || g.key != key) {
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    c->capturing = true;
+    try {
+      issue();
+    } catch (...) {
+      c->capturing = false;
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      throw;
+    }
+    c->capturing = false;
+    CK(cudaStreamEndCapture(s, &graph));
+    if (g.exec) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(g.exec, graph, &info) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+      }
+    }
+    if (!g.exec) {
+      const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(e);
+    } else {
+      cudaGraphDestroy(graph);
+    }
+    g.key = key;
+  }
+  CK(cudaGraphLaunch(g.exec, s));
+}
+
 void check_usable(const skv_ctx* c) {
   if (!c->poisoned.empty()) throw StateError("context unusable after an earlier failure: " + c->poisoned);
 }
 
-}  // namespace
-
-extern "C" {
-
-// ------------------------------------------------------------------ rules
 // A rule set's device automata (consecutive groups, none straddling a 32-rule mask word) and,
 // up to 32 enabled rules, the whole set's automaton (skv_rules_dfa).  Larger libraries keep
 // bit j = j-th enabled rule across skv_rules_mask_words() u32 words per window.
@@ -677,6 +752,11 @@ void compile_set(skv_rules& r) {
   r.dfa = r.whole ? skv::compile_rules(r.spec.rules) : skv::DfaTables{};
 }
 
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------------ rules
 int skv_rules_default(skv_rules** out) {
   if (!out) return SKV_ERR_ARG;
   return guard(nullptr, [&] {
@@ -899,6 +979,10 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     c->temp = dalloc<uint8_t>(tb, c->owned);
     CK(cudaMallocHost(&c->host_small, 64 * sizeof(uint32_t)));
     CK(cudaMallocHost(&c->host_events, kEpochEvPre * sizeof(skv_event)));
+    CK(cudaMallocHost(&c->hstate, 24 * sizeof(uint32_t)));
+    c->dstate = dalloc<uint32_t>(8, c->owned);
+    CK(cudaMemsetAsync(c->dstate, 0, 8 * sizeof(uint32_t), c->stream));
+    c->graphs = !(std::getenv("SKV_GRAPHS") && std::atoi(std::getenv("SKV_GRAPHS")) == 0);
     c->rec_grid = skv::record_grid(c->device);
     // default rules
     skv_rules* r = nullptr;
@@ -983,6 +1067,9 @@ int skv_destroy(skv_ctx* c) {
     if (p) cudaFree(p);
   if (c->host_small) cudaFreeHost(c->host_small);
   if (c->host_events) cudaFreeHost(c->host_events);
+  if (c->hstate) cudaFreeHost(c->hstate);
+  for (auto* g : {&c->g_admit, &c->g_commit, &c->g_epoch})
+    if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->side) {
@@ -1058,6 +1145,8 @@ void flush_record(skv_ctx* c) {
   // a replicated layer aggregates the batch's accesses for the cross-rank merge, which follows
   // the batch's commit: an uncommitted batch cannot be merged
   if (c->ix.rep.depth) throw StateError("replicated layer: commit the admitted batch first");
+  c->rec_mon.st = nullptr;  // outside a graph: the host's stamps
+  c->adm_graph = false;
   cudaStream_t s = c->stream;
   skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, s);
   finish_record(c, s);
@@ -1144,6 +1233,71 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       unprefetch_slot(c);
     }
     c->pf_valid = false;
+    c->adm_graph = false;
+    // a small device batch without per-block outputs: the admit's launches replay from a graph
+    if (c->graphs && b->on_device && !use_pf && !out && !c->evict_on && !c->budget_on && !c->ix.rep.depth) {
+      c->pf_slot = -1;
+      const bool bytes = b->token_bytes != nullptr;
+      const bool unaligned = !bytes && reinterpret_cast<uintptr_t>(b->tokens) % 16 != 0;
+      const uint32_t* tokens = (bytes || unaligned) ? c->d_tokens : b->tokens;
+      const uint64_t nb_bound = b->n_tokens / B;
+      skv::MonCtx mon = monitor_ctx(c);
+      mon.st = c->dstate;
+      mon.tl[0] = c->touched[0];
+      mon.tl[1] = c->touched[1];
+      mon.ntb = c->counters + 1;
+      const std::vector<uintptr_t> key = {
+          reinterpret_cast<uintptr_t>(bytes ? static_cast<const void*>(b->token_bytes) : b->tokens),
+          reinterpret_cast<uintptr_t>(b->offsets), reinterpret_cast<uintptr_t>(b->users),
+          reinterpret_cast<uintptr_t>(b->owners), N, b->n_tokens, reinterpret_cast<uintptr_t>(c->bd),
+          reinterpret_cast<uintptr_t>(c->bh), reinterpret_cast<uintptr_t>(c->bmask),
+          reinterpret_cast<uintptr_t>(c->blk_off), reinterpret_cast<uintptr_t>(c->first_sens),
+          reinterpret_cast<uintptr_t>(c->bslot), reinterpret_cast<uintptr_t>(c->blabel),
+          reinterpret_cast<uintptr_t>(c->counts), reinterpret_cast<uintptr_t>(c->plen), c->rules_gen, c->mask_words,
+          static_cast<uintptr_t>(bytes), static_cast<uintptr_t>(unaligned)};
+      put_state(c, 0, mon.batch, c->epoch);
+      run_graph(c, c->g_admit, key, [&] {
+        rec_ev(c, c->ev[0], s);
+        if (bytes)
+          skv::launch_widen(b->token_bytes, c->d_tokens, b->n_tokens, s);
+        else if (unaligned)
+          CK(cudaMemcpyAsync(c->d_tokens, b->tokens, b->n_tokens * 4, cudaMemcpyDeviceToDevice, s));
+        skv::launch_block_counts(b->offsets, N, B, c->counts, c->plen, s);
+        skv::launch_exclusive_scan(c->temp, c->temp_bytes, c->counts, c->blk_off, N + 1, s);
+        CK(cudaMemsetAsync(c->first_sens, 0xff, N * 4ull, s));
+        CK(cudaMemsetAsync(c->bdecision, 0, std::max<uint64_t>(nb_bound, 1), s));
+        CK(cudaMemsetAsync(c->matched + N, 0, 4, s));
+        rec_ev(c, c->ev[1], s);
+        stage12(c, s, tokens, b->offsets, N, b->n_tokens, nb_bound, c->blk_off, c->first_sens, c->bd, c->bmask);
+        rec_ev(c, c->ev[2], s);
+        CK(cudaMemsetAsync(c->counters + 8, 0, 12, s));  // n_replay, n_keys, matched_total
+        skv::launch_intern_users(c->users_tab, b->users, N, c->uidx, c->counters + 5, s);
+        skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel,
+                                c->bdecision, c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt, 0,
+                                s);
+        rec_ev(c, c->ev[3], s);
+        rec_ev(c, c->ev[4], s);
+        CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 11 * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->host_small + 20, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
+      });
+      c->rec_pending = !c->no_record;
+      c->rec_mon = mon;
+      c->rec_users = b->users;
+      c->rec_n = N;
+      c->adm_lazy = true;
+      c->adm_use_pf = false;
+      c->adm_pf_pair = c->pf_pair;
+      c->adm_launched = 6;
+      c->adm_graph = true;
+      c->pending = true;
+      c->p_n = N;
+      c->p_blocks = nb_bound;  // exact after resolve_admit
+      c->p_users = b->users;
+      c->p_owners = b->owners;
+      c->last_n = N;
+      c->admitted_prompts += N;
+      return SKV_OK;
+    }
     CK(cudaEventRecord(c->ev[0], s));
     // the host batch's H2D already queued by skv_stage (and its stages 1-2 by skv_prefetch)?
     int si = -1;
@@ -1382,6 +1536,12 @@ int skv_admit_ttft(skv_ctx* c, const uint64_t* request_ids, double* ttft_ms, uin
 }
 
 uint32_t skv_mask_words(const skv_ctx* c) { return c ? c->mask_words : 0; }
+
+int skv_set_graphs(skv_ctx* c, int on) {
+  if (!c) return SKV_ERR_ARG;
+  c->graphs = on != 0;
+  return SKV_OK;
+}
 
 int skv_last_rule_masks(skv_ctx* c, uint32_t* out, int on_device) {
   if (!c || !out) return SKV_ERR_ARG;
@@ -1683,6 +1843,145 @@ void commit_budgeted(skv_ctx* c) {
   }
 }
 
+}  // extern "C"
+
+namespace {
+
+// The non-budgeted commit of the pending batch, enqueued (graph or launches); its readbacks land
+// in host_small with the next synchronisation of the stream.
+struct CommitRun {
+  bool rec;
+  uint32_t ep32, launched;
+};
+
+CommitRun commit_enqueue(skv_ctx* c) {
+  cudaStream_t s = c->stream;
+  ++c->batch_id;
+  const bool rec = c->rec_pending;  // the batch's monitor records (see skv_admit)
+  const uint32_t ep32 = static_cast<uint32_t>(c->epoch);
+  // node ids are u32 on the device (the victim order's tie-break); refuse before they wrap
+  if (c->evict_on && c->node_next + c->p_blocks >= (1ull << 31))
+    throw CapacityError("eviction node-id space exhausted (2^31 nodes created)");
+  // a batch admitted through its graph commits through one too (records ride in k_commit)
+  const bool graphed = c->graphs && c->adm_graph && !c->evict_on && !c->ix.rep.depth && rec && !kRecordBeside;
+  if (!graphed) c->rec_mon.st = nullptr;  // the host's stamps (equal to the device state's)
+  uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
+  if (c->evict_on) launched += 2;
+  auto issue = [&] {
+    rec_ev(c, c->ev[5], s);
+    CK(cudaMemsetAsync(c->n_new, 0, 8, s));
+    CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
+    CK(cudaMemsetAsync(c->counters + 11, 0, 8, s));  // late child links, re-inserted tombstones
+    if (c->ix.rep.depth) CK(cudaMemsetAsync(c->ix.rep.new_n, 0, 4, s));
+    // The records (sector 1 of the matched entries, the window user sets) and the inserts
+    // (sector 0 of new entries, first-child links) touch disjoint words, so the record
+    // kernel runs on its own stream beside the commit kernels; without it the commit
+    // kernel needs fewer registers and keeps more claims in flight.
+    if (rec && kRecordBeside) {
+      CK(cudaEventRecord(c->rec_start, s));
+      CK(cudaStreamWaitEvent(c->rec_stream, c->rec_start, 0));
+      skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n,
+                         c->rec_stream);
+      CK(cudaEventRecord(c->rec_done, c->rec_stream));
+    }
+    skv::Index ixc = c->ix;
+    if (c->evict_on) {  // speculative node ids: prefix over prompts of the blocks each would create
+      skv::launch_node_bases(c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl, c->ev_temp, c->ev_temp_bytes,
+                             s);
+      ixc.em_base = c->ev_incl;
+      ixc.em_next = static_cast<uint32_t>(c->node_next);
+      ixc.em_epoch = static_cast<uint32_t>(c->epoch);
+    }
+    skv::launch_commit(ixc, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
+                       c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks),
+                       c->counters + 5, static_cast<int>(c->rec_grid), c->matched, c->rec_users,
+                       rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
+                       commit_sms(c), c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
+    if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
+    if (rec) finish_record(c, s);
+    rec_ev(c, c->ev[6], s);
+    CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 7, c->counters + 7, 4, cudaMemcpyDeviceToHost, s));
+  };
+  if (graphed) {
+    const std::vector<uintptr_t> key = {
+        c->p_n, c->p_blocks, reinterpret_cast<uintptr_t>(c->rec_users), reinterpret_cast<uintptr_t>(c->p_owners),
+        static_cast<uintptr_t>(c->pending_labels), reinterpret_cast<uintptr_t>(c->bh),
+        reinterpret_cast<uintptr_t>(c->bd), reinterpret_cast<uintptr_t>(c->blk_off),
+        reinterpret_cast<uintptr_t>(c->blabel), reinterpret_cast<uintptr_t>(c->bslot),
+        static_cast<uintptr_t>(commit_sms(c)), static_cast<uintptr_t>(c->rec_grid)};
+    put_state(c, 1, c->rec_mon.batch, c->epoch);
+    run_graph(c, c->g_commit, key, issue);
+  } else {
+    issue();
+  }
+  c->adm_graph = false;
+  return CommitRun{rec, ep32, launched};
+}
+
+// After the synchronisation: errors, the admit's readbacks, the rare ordered replay, counters.
+void commit_finish(skv_ctx* c, const CommitRun& run, uint64_t* new_entries) {
+  cudaStream_t s = c->stream;
+  const bool rec = run.rec;
+  const uint32_t ep32 = run.ep32;
+  uint32_t launched = run.launched;
+  unsigned long long nn = 0;
+  std::memcpy(&nn, c->host_small, 8);
+  const uint32_t err = c->host_small[4];
+  const uint32_t revived = c->host_small[6];
+  if (err) {
+    // the kernels have run: the host counters follow the device state before anything is
+    // raised (skv_export sizes its buffer by them), and the context refuses further batches
+    // (its index or monitor state no longer equals the reference's)
+    c->entries += nn + revived;
+    c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
+    c->node_next += nn + revived;
+    release_slot(c);
+    c->pending = false;
+    c->rec_pending = false;
+    if (c->adm_lazy) c->adm_lazy = false, c->p_blocks = c->host_small[20];
+    const char* why = (err & 8u)   ? "user table exhausted (raise max_users); the batch was not inserted"
+                      : (err & 2u) ? "index probe sequence exhausted"
+                      : (err & 1u) ? "monitor window user-set pool exhausted (raise max_window_entries)"
+                                   : "commit fix-up list overflow";
+    if (!(err & 8u)) c->poisoned = why;  // a user-table overflow inserts nothing: still consistent
+    else CK(cudaMemsetAsync(c->counters + 5, 0, 4, s));  // ... and the next batch may go ahead
+    throw CapacityError(why);
+  }
+  if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
+  if (rec) launched += replay_record(c, s, c->host_small[5], err);
+  if (c->evict_on) {
+    // the insert walk refreshes every pre-existing block's access epoch; node ids are exact
+    // already unless the batch had duplicate claims
+    skv::launch_path_epochs(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, ep32, s);
+    launched += 1;
+    if (c->host_small[7] || !skv::node_ids_speculative()) {
+      skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl,
+                               c->node_next, c->ev_temp, c->ev_temp_bytes, s);
+      launched += 3;
+    }
+    c->node_next += nn + revived;
+  }
+  c->entries += nn + revived;
+  c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
+  nn += revived;
+  c->bud_used[0] += nn;
+  c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
+  c->times.kernels_launched += launched;
+  c->times.new_blocks = nn;
+  release_slot(c);
+  c->pending = false;
+  c->rep_sync_due = c->ix.rep.depth != 0;
+  if (new_entries) *new_entries = nn;
+}
+
+}  // namespace
+
+extern "C" {
+
 int skv_commit(skv_ctx* c, uint64_t* new_entries) {
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
@@ -1717,123 +2016,48 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       if (new_entries) *new_entries = c->times.new_blocks;
       return SKV_OK;
     }
-    CK(cudaEventRecord(c->ev[5], s));
-    CK(cudaMemsetAsync(c->n_new, 0, 8, s));
-    CK(cudaMemsetAsync(c->counters + 7, 0, 4, s));   // intra-batch duplicate fix-up count
-    CK(cudaMemsetAsync(c->counters + 11, 0, 8, s));  // late child links, re-inserted tombstones
-    if (c->ix.rep.depth) CK(cudaMemsetAsync(c->ix.rep.new_n, 0, 4, s));
-    ++c->batch_id;
-    const bool rec = c->rec_pending;  // the batch's monitor records (see skv_admit)
-    // The records (sector 1 of the matched entries, the window user sets) and the inserts
-    // (sector 0 of new entries, first-child links) touch disjoint words, so the record
-    // kernel runs on its own stream beside the commit kernels; without it the commit
-    // kernel needs fewer registers and keeps more claims in flight.
-    if (rec && kRecordBeside) {
-      CK(cudaEventRecord(c->rec_start, s));
-      CK(cudaStreamWaitEvent(c->rec_stream, c->rec_start, 0));
-      skv::launch_record(c->ix, c->rec_mon, c->bslot, c->blk_off, c->matched, c->rec_users, c->rec_n, c->rec_stream);
-      CK(cudaEventRecord(c->rec_done, c->rec_stream));
-    }
-    skv::Index ixc = c->ix;
-    const uint32_t ep32 = static_cast<uint32_t>(c->epoch);
-    // node ids are u32 on the device (the victim order's tie-break); refuse before they wrap
-    if (c->evict_on && c->node_next + c->p_blocks >= (1ull << 31))
-      throw CapacityError("eviction node-id space exhausted (2^31 nodes created)");
-    if (c->evict_on) {  // speculative node ids: prefix over prompts of the blocks each would create
-      skv::launch_node_bases(c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl, c->ev_temp, c->ev_temp_bytes, s);
-      ixc.em_base = c->ev_incl;
-      ixc.em_next = static_cast<uint32_t>(c->node_next);
-      ixc.em_epoch = ep32;
-    }
-    skv::launch_commit(ixc, c->bh, c->bd, c->blk_off, c->exist, c->blabel, c->uidx, c->p_owners, c->p_n, c->bslot,
-                       c->n_new, c->fix_list, c->counters + 7, static_cast<uint32_t>(c->max_blocks), c->counters + 5,
-                       static_cast<int>(c->rec_grid), c->matched, c->rec_users,
-                       rec && !kRecordBeside ? &c->rec_mon : nullptr, c->pending_labels ? 1 : 0, c->p_blocks,
-                       commit_sms(c), c->bprompt, c->late, c->counters + 11, c->counters + 12, c->rec_mon, s);
-    if (rec && kRecordBeside) CK(cudaStreamWaitEvent(s, c->rec_done, 0));
-    uint32_t launched = 4 + (rec && kRecordBeside ? 1 : 0);  // commit, fix-up x2, links
-    if (c->evict_on) launched += 2;
-    if (rec) finish_record(c, s);
-    CK(cudaEventRecord(c->ev[6], s));
-    unsigned long long nn = 0;
-    CK(cudaMemcpyAsync(c->host_small, c->n_new, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->host_small + 4, c->counters + 5, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->host_small + 7, c->counters + 7, 4, cudaMemcpyDeviceToHost, s));
+    const CommitRun run = commit_enqueue(c);
     sync_check(s);  // the commit's one synchronisation (plus the rare ordered replay)
-    std::memcpy(&nn, c->host_small, 8);
-    const uint32_t err = c->host_small[4];
-    const uint32_t revived = c->host_small[6];
-    if (err) {
-      // the kernels have run: the host counters follow the device state before anything is
-      // raised (skv_export sizes its buffer by them), and the context refuses further batches
-      // (its index or monitor state no longer equals the reference's)
-      c->entries += nn + revived;
-      c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
-      c->node_next += nn + revived;
-      release_slot(c);
-      c->pending = false;
-      c->rec_pending = false;
-      if (c->adm_lazy) c->adm_lazy = false, c->p_blocks = c->host_small[20];
-      const char* why = (err & 8u)   ? "user table exhausted (raise max_users); the batch was not inserted"
-                        : (err & 2u) ? "index probe sequence exhausted"
-                        : (err & 1u) ? "monitor window user-set pool exhausted (raise max_window_entries)"
-                                     : "commit fix-up list overflow";
-      if (!(err & 8u)) c->poisoned = why;  // a user-table overflow inserts nothing: still consistent
-      throw CapacityError(why);
-    }
-    if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
-    if (rec) launched += replay_record(c, s, c->host_small[5], err);
-    if (c->evict_on) {
-      // the insert walk refreshes every pre-existing block's access epoch; node ids are exact
-      // already unless the batch had duplicate claims
-      skv::launch_path_epochs(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, ep32, s);
-      launched += 1;
-      if (c->host_small[7] || !skv::node_ids_speculative()) {
-        skv::launch_assign_nodes(c->ix, c->bslot, c->blk_off, c->exist, c->p_n, c->ev_counts, c->ev_incl,
-                                 c->node_next, c->ev_temp, c->ev_temp_bytes, s);
-        launched += 3;
-      }
-      c->node_next += nn + revived;
-    }
-    c->entries += nn + revived;
-    c->tombstones -= std::min<uint64_t>(c->tombstones, revived);
-    nn += revived;
-    c->bud_used[0] += nn;
-    c->times.commit_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += launched;
-    c->times.new_blocks = nn;
-    release_slot(c);
-    c->pending = false;
-    c->rep_sync_due = c->ix.rep.depth != 0;
-    if (new_entries) *new_entries = nn;
+    commit_finish(c, run, new_entries);
     return SKV_OK;
   });
 }
 
-int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch_out) {
-  if (!c) return SKV_ERR_ARG;
-  return guard(c, [&] {
-    check_usable(c);
-    CK(cudaSetDevice(c->device));
-    ensure_admit_resolved(c);
-    flush_record(c);
-    cudaStream_t s = c->stream;
-    CK(cudaEventRecord(c->ev[5], s));
-    const uint64_t epoch = ++c->epoch;  // advance_epoch (cache_index.hpp:296-299)
-    const uint32_t stamp = static_cast<uint32_t>(epoch);
-    // grids cover the window lists' capacity; the kernels read the list lengths on the
-    // device, so the epoch needs no host round trip before its kernels
-    const int cur = c->cur, prev = 1 - c->cur;
-    const uint32_t bound = 2 * c->pool_cap;
+}  // extern "C"
+
+namespace {
+
+// advance_epoch + epoch_pass + roll (monitor.hpp:85-99, cache_index.hpp:296-299), enqueued: the
+// host state (epoch, current window) advances in epoch_finish.  speculative: the pass aborts on
+// the device, before touching anything, when the commit queued ahead of it raised an error or
+// needs the ordered replay (counters[5] | counters[8]) -- the caller then runs it again.
+struct EpochRun {
+  uint64_t epoch;
+  size_t pre;
+  bool split;
+};
+
+EpochRun epoch_enqueue(skv_ctx* c, bool speculative) {
+  cudaStream_t s = c->stream;
+  const uint64_t epoch = c->epoch + 1;
+  const uint32_t stamp = static_cast<uint32_t>(epoch);
+  // grids cover the window lists' capacity; the kernels read the list lengths on the
+  // device, so the epoch needs no host round trip before its kernels
+  const int cur = c->cur, prev = 1 - c->cur;
+  const uint32_t bound = 2 * c->pool_cap;
+  static const bool split_env = getenv_flag("SKV_EPOCH_SPLIT");  // diagnostic: the six-kernel pass
+  const bool split = split_env && !speculative;
+  const size_t pre = std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap);
+  const bool graphed = c->graphs && !split;
+  auto issue = [&] {
+    rec_ev(c, c->ev[5], s);
     CK(cudaMemsetAsync(c->counters + 3, 0, 8, s));  // n_cands, n_events
-    static const bool split = getenv_flag("SKV_EPOCH_SPLIT");  // diagnostic: the six-kernel pass
     if (!split) {
-      CK(skv::launch_epoch_fused(c->ix, c->touched[cur], c->counters + 1 + cur, c->touched[prev],
-                                 c->counters + 1 + prev, stamp, c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands,
-                                 c->counters + 3, epoch, c->events, c->counters + 4, c->fired, c->counters,
-                                 c->counters + 1 + prev, c->device, s));
+      // a graph's pass takes its stamps and arming from the device step state
+      CK(skv::launch_epoch_fused(c->ix, c->touched, c->counters + 1, cur, stamp, c->cfg.entropy_jump,
+                                 c->cfg.u_pre_max, c->cands, c->counters + 3, epoch, c->events, c->counters + 4,
+                                 c->fired, c->counters, graphed ? c->dstate : nullptr,
+                                 (graphed || speculative) ? c->counters : nullptr, c->device, s));
     } else {
       skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, stamp,
                                    c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
@@ -1844,39 +2068,99 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
       skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
       skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s);
       skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s);
-    }
-    CK(cudaMemcpyAsync(c->host_small, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
-    // the first events ride along with their count (events are rare: one synchronisation)
-    const size_t pre = std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap);
-    CK(cudaMemcpyAsync(c->host_events, c->events, pre * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
-    // swap windows: the current list becomes the previous one (its count stays where it
-    // is); the pool and the new current list start empty (the fused pass resets them itself)
-    if (split) {
+      // swap windows: the current list becomes the previous one (its count stays where it
+      // is); the pool and the new current list start empty (the fused pass resets them itself)
       CK(cudaMemsetAsync(c->counters, 0, 4, s));
       CK(cudaMemsetAsync(c->counters + 1 + prev, 0, 4, s));
     }
-    CK(cudaEventRecord(c->ev[6], s));
+    CK(cudaMemcpyAsync(c->host_small + kEpochCountSlot, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
+    // the first events ride along with their count (events are rare: one synchronisation)
+    CK(cudaMemcpyAsync(c->host_events, c->events, pre * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
+    rec_ev(c, c->ev[6], s);
+  };
+  if (graphed) {
+    put_state(c, 2, c->rec_batch, epoch, speculative);
+    run_graph(c, c->g_epoch, {reinterpret_cast<uintptr_t>(c->events), c->pool_cap}, issue);
+  } else {
+    issue();
+  }
+  return EpochRun{epoch, pre, split};
+}
+
+// After the synchronisation of a pass that ran: its events, and the host state advances.
+void epoch_finish(skv_ctx* c, const EpochRun& run, skv_event* events, size_t cap, size_t* n_events,
+                  uint64_t* epoch_out) {
+  cudaStream_t s = c->stream;
+  const uint32_t ne = c->host_small[kEpochCountSlot];
+  std::vector<skv_event> ev(ne);
+  if (ne <= run.pre) {
+    std::copy(c->host_events, c->host_events + ne, ev.begin());
+  } else {
+    CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
     sync_check(s);
-    const uint32_t ne = c->host_small[0];
-    std::vector<skv_event> ev(ne);
-    if (ne <= pre) {
-      std::copy(c->host_events, c->host_events + ne, ev.begin());
+  }
+  c->epoch = run.epoch;  // advance_epoch
+  c->cur = 1 - c->cur;
+  c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
+  c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
+  c->times.kernels_launched += run.split ? 6 : 1;
+  std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
+    return x.h != y.h ? x.h < y.h : x.d < y.d;
+  });
+  if (events)
+    for (size_t i = 0; i < ev.size() && i < cap; ++i) events[i] = ev[i];
+  if (n_events) *n_events = ev.size();
+  c->last_events = std::move(ev);  // the whole list stays retrievable (skv_last_events)
+  if (epoch_out) *epoch_out = run.epoch;
+}
+
+}  // namespace
+
+extern "C" {
+
+int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch_out) {
+  if (!c) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    check_usable(c);
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    flush_record(c);
+    const EpochRun run = epoch_enqueue(c, false);
+    sync_check(c->stream);
+    epoch_finish(c, run, events, cap, n_events, epoch_out);
+    return SKV_OK;
+  });
+}
+
+// admit + commit + epoch of one batch with one synchronisation in the common case: the epoch is
+// queued behind the commit speculatively (it aborts itself on the device if the commit failed or
+// needs the ordered replay; the epoch then runs again after the replay).  A small batch's step is
+// bound by host round trips otherwise.
+int skv_step(skv_ctx* c, const skv_batch* b, uint64_t* new_entries, skv_event* events, size_t cap,
+             size_t* n_events, uint64_t* epoch_out) {
+  if (!c || !b) return SKV_ERR_ARG;
+  int rc = skv_admit(c, b, nullptr);
+  if (rc != SKV_OK) return rc;
+  const bool fused = c->p_n > 0 && !c->budget_on && !c->evict_on && !c->ix.rep.depth;
+  if (!fused) {
+    if ((rc = skv_commit(c, new_entries)) != SKV_OK) return rc;
+    return skv_epoch(c, events, cap, n_events, epoch_out);
+  }
+  return guard(c, [&] {
+    if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
+      throw CapacityError("index capacity exhausted (eviction is not part of this path)");
+    const CommitRun crun = commit_enqueue(c);
+    const EpochRun erun = epoch_enqueue(c, true);
+    sync_check(c->stream);
+    const bool epoch_ran = c->host_small[4] == 0 && c->host_small[5] == 0;  // the pass's own abort test
+    commit_finish(c, crun, new_entries);  // raises the commit's errors; runs the ordered replay
+    if (epoch_ran) {
+      epoch_finish(c, erun, events, cap, n_events, epoch_out);
     } else {
-      CK(cudaMemcpyAsync(ev.data(), c->events, ne * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
-      sync_check(s);
+      const EpochRun again = epoch_enqueue(c, false);
+      sync_check(c->stream);
+      epoch_finish(c, again, events, cap, n_events, epoch_out);
     }
-    c->cur = prev;
-    c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
-    c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
-    c->times.kernels_launched += split ? 6 : 1;
-    std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
-      return x.h != y.h ? x.h < y.h : x.d < y.d;
-    });
-    if (events)
-      for (size_t i = 0; i < ev.size() && i < cap; ++i) events[i] = ev[i];
-    if (n_events) *n_events = ev.size();
-    c->last_events = std::move(ev);  // the whole list stays retrievable (skv_last_events)
-    if (epoch_out) *epoch_out = epoch;
     return SKV_OK;
   });
 }

@@ -226,6 +226,12 @@ struct MonCtx {
   uint32_t wstart;  // first batch id of the current window
   uint32_t* err;
   uint32_t* matched_total;
+  // graph-replayed steps (capi.cpp "CUDA graphs"): the window and batch stamps live on the device
+  // ({batch, wstart, cur} at st[0..2], written before each graph launch); kernels then take the
+  // current window list from tl[cur] and its count from ntb[cur].  st == nullptr: the fields above.
+  const uint32_t* st = nullptr;
+  uint32_t* tl[2] = {nullptr, nullptr};
+  uint32_t* ntb = nullptr;
 };
 
 // CostModel (serving_sim.hpp:25-57) in device form
@@ -357,11 +363,14 @@ void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32
                             cudaStream_t s);
 // the whole epoch pass (candidates, fire, propagate, rolls, window-swap resets) in one
 // cooperative launch
-cudaError_t launch_epoch_fused(const Index& ix, const uint32_t* cur_list, uint32_t* n_cur, const uint32_t* prev_list,
-                               const uint32_t* n_prev, uint32_t stamp, double jump, uint64_t u_pre_max,
-                               uint32_t* cands, uint32_t* n_cands, uint64_t epoch, void* events, uint32_t* n_events,
-                               uint32_t* fired, uint32_t* pool_count, uint32_t* prev_count, int device,
-                               cudaStream_t s);
+// (st != nullptr: cur, stamp and epoch from the device step state st[2], st[3], st[4..5]; the lists
+// are lists[cur] / lists[1 - cur] with counts ntb[cur] / ntb[1 - cur].  guard != nullptr -- and,
+// with st, st[6] != 0 -- arms a speculative pass: it returns untouched when guard[5] (commit
+// errors) or guard[8] (ordered replay pending) is set.)
+cudaError_t launch_epoch_fused(const Index& ix, uint32_t* const lists[2], uint32_t* ntb, int cur, uint32_t stamp,
+                               double jump, uint64_t u_pre_max, uint32_t* cands, uint32_t* n_cands, uint64_t epoch,
+                               void* events, uint32_t* n_events, uint32_t* fired, uint32_t* pool_count,
+                               const uint32_t* st, const uint32_t* guard, int device, cudaStream_t s);
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
                        cudaStream_t s);
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,

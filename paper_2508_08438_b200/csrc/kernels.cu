@@ -814,6 +814,18 @@ __device__ __forceinline__ bool cas128(unsigned long long* addr, unsigned long l
 // set did not cross 64 in this batch; the rare crossing entries are replayed in prompt
 // order by k_record_replay.
 // ---------------------------------------------------------------------------------
+// the batch / window stamps of a graph-replayed step from the device step state (MonCtx::st)
+__device__ __forceinline__ MonCtx mon_live(MonCtx M) {
+  if (M.st) {
+    const uint32_t cur = M.st[2];
+    M.batch = M.st[0];
+    M.wstart = M.st[1];
+    M.touched = M.tl[cur];
+    M.n_touched = M.ntb + cur;
+  }
+  return M;
+}
+
 __device__ __forceinline__ uint32_t mix32(uint64_t u) {
   u ^= u >> 33;
   u *= 0xff51afd7ed558ccdULL;
@@ -932,6 +944,7 @@ __device__ void record_user(const Index& ix, const MonCtx& M, uint32_t slot, uin
 
 // one thread per entry touched in the current monitor window
 __global__ void k_record_finish(Index ix, MonCtx M, uint32_t* replay, uint32_t* n_replay) {
+  M = mon_live(M);
   const uint32_t n = *M.n_touched;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t slot = M.touched[i];
@@ -1468,6 +1481,7 @@ __global__ void __launch_bounds__(256, kRec ? SKV_COMMIT_MINB : SKV_COMMIT_MINB_
   constexpr int R = kCommitRounds;  // rounds of 32 blocks whose claims are in flight together
   const uint32_t lane = lane_id();
   uint32_t inserted = 0;
+  if constexpr (kRec) M = mon_live(M);
   // the admit of this batch overflowed the user table (k_intern_users, err bit 8): its creator
   // indices are invalid, so nothing is inserted or recorded (the host raises CapacityExhausted)
   if (*reinterpret_cast<volatile uint32_t*>(err_flag) & 8u) return;
@@ -1915,6 +1929,7 @@ __global__ void k_commit_fixup(Index ix, const uint32_t* __restrict__ blk_off, c
                                const uint32_t* __restrict__ uidx, const uint8_t* __restrict__ owners,
                                const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ n_fix,
                                uint32_t fix_cap, int pending_labels, uint32_t* n_revived, MonCtx P) {
+  P = mon_live(P);
   const uint32_t nf = min(*n_fix, fix_cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const uint32_t s = fix_list[i], b = fix_list[fix_cap + i];
@@ -2070,16 +2085,27 @@ __device__ __forceinline__ void epoch_candidate(Index& ix, uint32_t s, bool only
   }
 }
 
-__global__ void __launch_bounds__(256) k_epoch_fused(Index ix, const uint32_t* __restrict__ cur_list,
-                                                     uint32_t* n_cur, const uint32_t* __restrict__ prev_list,
-                                                     const uint32_t* __restrict__ n_prev, uint32_t stamp, double jump,
-                                                     uint64_t u_pre_max, uint32_t* cands, uint32_t* n_cands,
-                                                     uint64_t epoch, DevEvent* events, uint32_t* n_events,
-                                                     uint32_t* fired, uint32_t* pool_count, uint32_t* prev_count) {
+__global__ void __launch_bounds__(256) k_epoch_fused(Index ix, uint32_t* l0, uint32_t* l1, uint32_t* ntb, int cur_in,
+                                                     uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
+                                                     uint32_t* n_cands, uint64_t epoch, DevEvent* events,
+                                                     uint32_t* n_events, uint32_t* fired, uint32_t* pool_count,
+                                                     const uint32_t* st, const uint32_t* guard) {
   namespace cg = cooperative_groups;
+  // a speculative pass behind a commit that failed or needs the ordered replay: nothing happens
+  // (every thread leaves before the first grid sync)
+  if (guard && (!st || st[6]) && (guard[5] | guard[8])) return;
   cg::grid_group grid = cg::this_grid();
   const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
-  const uint32_t nc = *n_cur, np = *n_prev;
+  uint32_t cur = static_cast<uint32_t>(cur_in);
+  if (st) {  // a graph-replayed epoch: window and stamps from the device step state
+    cur = st[2];
+    stamp = st[3];
+    epoch = static_cast<uint64_t>(st[4]) | (static_cast<uint64_t>(st[5]) << 32);
+  }
+  const uint32_t* cur_list = cur ? l1 : l0;
+  const uint32_t* prev_list = cur ? l0 : l1;
+  uint32_t* prev_count = ntb + (1 - cur);
+  const uint32_t nc = ntb[cur], np = *prev_count;
   for (uint32_t i = t0; i < nc + np; i += T)
     epoch_candidate(ix, i < nc ? cur_list[i] : prev_list[i - nc], i >= nc, stamp, jump, u_pre_max, cands, n_cands);
   grid.sync();
@@ -2776,14 +2802,16 @@ int epoch_fused_grid(int device) {
   return grid[device];
 }
 
-cudaError_t launch_epoch_fused(const Index& ix, const uint32_t* cur_list, uint32_t* n_cur, const uint32_t* prev_list,
-                        const uint32_t* n_prev, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
-                        uint32_t* n_cands, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
-                        uint32_t* pool_count, uint32_t* prev_count, int device, cudaStream_t s) {
+cudaError_t launch_epoch_fused(const Index& ix, uint32_t* const lists[2], uint32_t* ntb, int cur, uint32_t stamp,
+                               double jump, uint64_t u_pre_max, uint32_t* cands, uint32_t* n_cands, uint64_t epoch,
+                               void* events, uint32_t* n_events, uint32_t* fired, uint32_t* pool_count,
+                               const uint32_t* st, const uint32_t* guard, int device, cudaStream_t s) {
   Index ixv = ix;
   DevEvent* ev = static_cast<DevEvent*>(events);
-  void* args[] = {&ixv, &cur_list, &n_cur, &prev_list, &n_prev, &stamp, &jump, &u_pre_max, &cands, &n_cands,
-                  &epoch, &ev, &n_events, &fired, &pool_count, &prev_count};
+  uint32_t* l0 = lists[0];
+  uint32_t* l1 = lists[1];
+  void* args[] = {&ixv, &l0, &l1, &ntb, &cur, &stamp, &jump, &u_pre_max, &cands, &n_cands,
+                  &epoch, &ev, &n_events, &fired, &pool_count, &st, &guard};
   const int grid = epoch_fused_grid(device);
   if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epoch_fused), dim3(grid), dim3(256), args, 0, s);

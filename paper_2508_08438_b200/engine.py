@@ -253,6 +253,10 @@ class AdmissionEngine:
             res.rule_mask_words = self.last_rule_masks()
         return res
 
+    def set_graphs(self, on: bool) -> None:
+        """CUDA-graph replay of small device-batch steps (``skv_set_graphs``; default on)."""
+        self._check(self._lib.skv_set_graphs(self._h, 1 if on else 0))
+
     def admit_raw(self, batch: N.Batch, out: Optional[N.AdmitOut] = None) -> None:
         """Zero-copy entry point: device (or host) pointers supplied by the caller."""
         self._check(self._lib.skv_admit(self._h, C.byref(batch), C.byref(out) if out is not None else None))
@@ -302,6 +306,21 @@ class AdmissionEngine:
         evs = [AnomalyEvent(e.h, e.d, e.action, e.owner, e.entropy_now, e.entropy_prev, e.u_pre, e.epoch)
                for e in buf[:n.value]]
         return int(ep.value), evs
+
+    def step_raw(self, batch: N.Batch, cap: int = 1 << 16) -> tuple[int, int, list[AnomalyEvent]]:
+        """``skv_step``: admit (no per-block outputs) + commit + epoch of one batch, one host
+        synchronisation in the common case.  Returns (new entries, epoch, events)."""
+        buf = getattr(self, "_evbuf", None)
+        if buf is None or len(buf) < cap:
+            buf = self._evbuf = (N.Event * cap)()
+        n, ep, nn = C.c_size_t(), C.c_uint64(), C.c_uint64()
+        self._check(self._lib.skv_step(self._h, C.byref(batch), C.byref(nn), buf, cap, C.byref(n), C.byref(ep)))
+        if n.value > cap:
+            buf = self._evbuf = (N.Event * n.value)()
+            self._check(self._lib.skv_last_events(self._h, buf, n.value, C.byref(n)))
+        evs = [AnomalyEvent(e.h, e.d, e.action, e.owner, e.entropy_now, e.entropy_prev, e.u_pre, e.epoch)
+               for e in buf[:n.value]]
+        return int(nn.value), int(ep.value), evs
 
     # --------------------------------------------------------------- misc
     # --------------------------------------------------------------- serving observables
@@ -476,11 +495,13 @@ class AdmissionEngine:
         self._check(self._lib.skv_tier1_scan(self._h, raw, len(raw), _ptr(m)))
         return combine_mask_words(m[:, None])[0]
 
-    def last_rule_masks(self) -> np.ndarray:
+    def last_rule_masks(self, n_blocks: Optional[int] = None) -> np.ndarray:
         """The last admitted batch's full window masks, ``[mask words, n_blocks]`` uint32
-        (word 0 is ``AdmitResult.rule_mask``); ``combine_mask_words`` gives one int per block."""
+        (word 0 is ``AdmitResult.rule_mask``); ``combine_mask_words`` gives one int per block.
+        ``n_blocks``: the batch's block count (default: that of the last ``admit``)."""
         w = int(self._lib.skv_mask_words(self._h))
-        out = np.zeros((w, getattr(self, "_last_blocks", 0)), np.uint32)
+        nb = getattr(self, "_last_blocks", 0) if n_blocks is None else int(n_blocks)
+        out = np.zeros((w, nb), np.uint32)
         self._check(self._lib.skv_last_rule_masks(self._h, _ptr(out), 0))
         return out
 
