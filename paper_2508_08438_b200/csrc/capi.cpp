@@ -4,6 +4,8 @@
 // computation runs on the device (kernels.cu).  There is no CPU fallback path.
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
@@ -199,6 +201,8 @@ struct skv_ctx {
   size_t temp_bytes = 0;
   uint32_t* host_small = nullptr;  // pinned scratch for small readbacks
   skv_event* host_events = nullptr;  // pinned: the first kEpochEvPre events of an epoch, read with its count
+  uint32_t* hs_map = nullptr;      // block -> prompt of a short-prompt batch (stages 1-2 on the context stream)
+  uint32_t* alt_hs_map = nullptr;  // ... of a prefetched batch (side stream)
   int n_sm = 148;
   uint32_t rec_grid = 0;
 
@@ -481,8 +485,9 @@ void build_group16(skv_ctx* c, const skv::DfaTables& d, skv_ctx::DevGroup& g) {
   const uint32_t S2 = 2 * S, colbytes = 4 * S;
   const uint32_t img_bytes = 129 * colbytes;
   uint32_t q_cap = 256;  // deferred tasks per warp: shrink to fit, at least 3 segments x 32 lanes
-  while (q_cap > 96 && skv::hash_scan16_smem(img_bytes, q_cap) > 227 * 1024) q_cap -= 32;
-  if (skv::hash_scan16_smem(img_bytes, q_cap) > 227 * 1024) return;
+  constexpr uint32_t kSmemMax = 227 * 1024 - 1024;  // the kernel's static shared (image mbarrier) beside it
+  while (q_cap > 96 && skv::hash_scan16_smem(img_bytes, q_cap) > kSmemMax) q_cap -= 32;
+  if (skv::hash_scan16_smem(img_bytes, q_cap) > kSmemMax) return;
   std::vector<uint16_t> img(129ull * S2 + 8, 0), hi(128ull * S2, 0);
   std::vector<uint32_t> full(256ull * S, 0);
   for (uint32_t b = 0; b < 256; ++b) {
@@ -619,11 +624,27 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
       h.d_out = bd;
       h.mask_out = bmask + g.word * NB;
       h.first_sens = first_sens;
-      // a small batch needs fewer CTAs (one 32-warp CTA per SM otherwise)
-      const uint64_t want = nb_hint ? (nb_hint + 32 * 32 - 1) / (32 * 32) : static_cast<uint64_t>(R.grid);
-      uint64_t grid = std::min<uint64_t>(R.grid, std::max<uint64_t>(want, 1));
-      if (overlapped && pf_frac > 1) grid = std::max<uint64_t>(1, grid / pf_frac);
-      skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st);
+      // a large batch: one 32-warp CTA per SM, a warp per 32-block chunk in turn.  A small batch
+      // (fewer chunks than 32 warps x SMs): its chunks spread over the SMs with fewer warps per CTA
+      // (the per-SM issue of 32 warps would otherwise bound it on a handful of SMs)
+      const uint64_t nb_est = nb_hint ? nb_hint : n_tokens / 16;
+      const uint64_t chunks = std::max<uint64_t>(1, (nb_est + 31) / 32);
+      uint64_t grid = R.grid;
+      int warps = 32;
+      if (chunks < 32ull * R.grid) {
+        warps = static_cast<int>(std::clamp<uint64_t>((chunks + R.grid - 1) / R.grid, 4, 32));
+        grid = std::min<uint64_t>(R.grid, (chunks + warps - 1) / warps);
+      }
+      // a prefetch (beside the previous batch's commit) keeps to a quarter of the SMs
+      if (overlapped && pf_frac > 1) grid = std::min<uint64_t>(grid, std::max<uint64_t>(1, R.grid / pf_frac));
+      // short prompts (< ~34 blocks): the chunk geometry comes from a block -> prompt map
+      if (N && nb_est / N < 34) {
+        uint32_t*& map = overlapped ? c->alt_hs_map : c->hs_map;
+        if (!map) map = dalloc<uint32_t>(std::max<uint64_t>(c->max_blocks, 1), c->owned);
+        skv::launch_block_prompts(blk_off, N, map, st);
+        h.bmap = map;
+      }
+      skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st, warps);
       continue;
     }
     skv::HashScanArgs a;
@@ -673,6 +694,14 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   }
   return ms;
 }
+
+// NVTX range of a C-ABI call (visible in nsys / ncu timelines; a no-op without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // an event record inside a captured phase is an external event node (its timestamps stay
 // readable after the graph ran)
@@ -1009,6 +1038,7 @@ int find_staged(skv_ctx* c, const skv_batch* b);
 void unprefetch_slot(skv_ctx* c);
 
 int skv_stage(skv_ctx* c, const skv_batch* b) {
+  NvtxRange nvtx_range("skv_stage");
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
@@ -1195,6 +1225,7 @@ void unprefetch_slot(skv_ctx* c) {
 }
 
 int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
+  NvtxRange nvtx_range("skv_admit");
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
     check_usable(c);
@@ -1558,6 +1589,7 @@ int skv_last_rule_masks(skv_ctx* c, uint32_t* out, int on_device) {
 }
 
 int skv_prefetch(skv_ctx* c, const skv_batch* b) {
+  NvtxRange nvtx_range("skv_prefetch");
   if (!c || !b) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
@@ -1983,6 +2015,7 @@ void commit_finish(skv_ctx* c, const CommitRun& run, uint64_t* new_entries) {
 extern "C" {
 
 int skv_commit(skv_ctx* c, uint64_t* new_entries) {
+  NvtxRange nvtx_range("skv_commit");
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     check_usable(c);
@@ -2119,6 +2152,7 @@ void epoch_finish(skv_ctx* c, const EpochRun& run, skv_event* events, size_t cap
 extern "C" {
 
 int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch_out) {
+  NvtxRange nvtx_range("skv_epoch");
   if (!c) return SKV_ERR_ARG;
   return guard(c, [&] {
     check_usable(c);
@@ -2138,6 +2172,7 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
 // bound by host round trips otherwise.
 int skv_step(skv_ctx* c, const skv_batch* b, uint64_t* new_entries, skv_event* events, size_t cap,
              size_t* n_events, uint64_t* epoch_out) {
+  NvtxRange nvtx_range("skv_step");
   if (!c || !b) return SKV_ERR_ARG;
   int rc = skv_admit(c, b, nullptr);
   if (rc != SKV_OK) return rc;
@@ -2363,6 +2398,7 @@ int skv_last_drops(skv_ctx* c, uint32_t* prompts, size_t cap, size_t* n) {
 
 int skv_evict(skv_ctx* c, uint64_t needed_blocks, uint64_t epoch, uint64_t* n_evicted, uint64_t* victims_h,
               uint64_t* victims_d, size_t cap) {
+  NvtxRange nvtx_range("skv_evict");
   (void)epoch;  // the victim order only compares access epochs (epoch - access_epoch, cache_index.hpp:709)
   if (!c || !n_evicted) return SKV_ERR_ARG;
   *n_evicted = 0;
@@ -2475,6 +2511,7 @@ int skv_set_replicated_depth(skv_ctx* c, uint32_t depth) {
 
 int skv_replica_export(skv_ctx* c, const uint64_t* gids, skv_rep_entry* ents, size_t ecap, size_t* n_ents,
                        skv_rep_access* accs, size_t acap, size_t* n_accs, int accs_on_device) {
+  NvtxRange nvtx_range("skv_replica_export");
   if (!c || !n_ents || !n_accs) return SKV_ERR_ARG;
   *n_ents = *n_accs = 0;
   return guard(c, [&] {
@@ -2510,6 +2547,7 @@ int skv_replica_export(skv_ctx* c, const uint64_t* gids, skv_rep_entry* ents, si
 
 int skv_replica_apply(skv_ctx* c, const skv_rep_entry* ents, size_t n_ents, const skv_rep_access* accs,
                       size_t n_accs, int accs_on_device) {
+  NvtxRange nvtx_range("skv_replica_apply");
   if (!c || (n_ents && !ents) || (n_accs && !accs)) return SKV_ERR_ARG;
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));

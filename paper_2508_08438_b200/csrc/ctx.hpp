@@ -145,6 +145,7 @@ struct HS16Args {
   uint64_t* d_out;
   uint32_t* mask_out;
   uint32_t* first_sens;
+  const uint32_t* bmap = nullptr;  // block -> prompt (short-prompt batches), else binary searches
 };
 
 struct HashScanArgs {
@@ -324,7 +325,9 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 // queue capacity, and the persistent grid (-1 on failure)
 uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap);
 int hash_scan16_grid(int device, uint32_t smem);
-void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s);
+void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s, int warps = 0);
+// block -> prompt map of a batch (warp per prompt), for short-prompt batches
+void launch_block_prompts(const uint32_t* blk_off, uint32_t n_prompts, uint32_t* map, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,

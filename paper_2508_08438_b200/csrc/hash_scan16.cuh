@@ -150,22 +150,47 @@ __device__ __forceinline__ void h16_flush(H16Task* q, uint32_t qn, uint32_t lane
   __syncwarp();
 }
 
+// The automaton image -> SMEM by bulk (TMA) copies issued by one thread, completion counted on an
+// mbarrier (transaction bytes): the image arrives at the copy engine's rate instead of one L2
+// round trip per 16-B load and thread (which bounds a CTA of few warps -- a small batch's launch
+// shape -- at ~70 dependent round trips)
+__device__ __forceinline__ void h16_load_image(uint8_t* sm, const void* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      const uint32_t n = min(32768u, bytes - off);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + off),
+                   "l"(static_cast<const uint8_t*>(src) + off), "r"(n), "r"(bar)
+                   : "memory");
+    }
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tH16_WAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra H16_WAIT_%=;\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+// blockDim.x = 32 x WPC warps (kH16Warps for large batches; a small batch spreads its chunks over
+// more SMs with fewer warps each, capi.cpp stage12)
 __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_hash_scan16(HS16Args a) {
   extern __shared__ __align__(16) uint8_t sm[];
   const uint8_t* tab = sm;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, WPC = blockDim.x >> 5;
   const uint32_t img_al = (a.img_bytes + 15) & ~15u;
   Slot16* slots = reinterpret_cast<Slot16*>(sm + img_al) + 4 * wid;  // prev, cur, next; [3].start..: prompt ids
   uint32_t* slot_p = reinterpret_cast<uint32_t*>(slots + 3);
-  H16Task* q = reinterpret_cast<H16Task*>(sm + img_al + 4 * kH16Warps * sizeof(Slot16)) + wid * a.q_cap;
-  {  // the automaton image -> SMEM
-    const uint4* src = reinterpret_cast<const uint4*>(a.img);
-    uint4* dst = reinterpret_cast<uint4*>(sm);
-    for (uint32_t i = tid; i < img_al / 16; i += blockDim.x) dst[i] = src[i];
-  }
+  H16Task* q = reinterpret_cast<H16Task*>(sm + img_al + 4 * WPC * sizeof(Slot16)) + wid * a.q_cap;
+  __shared__ uint64_t img_bar;
+  h16_load_image(sm, a.img, img_al, &img_bar);
   const uint32_t N = a.n_prompts;
   const uint32_t nb = a.blk_off[N];
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kH16Warps + wid, TW = static_cast<uint64_t>(gridDim.x) * kH16Warps;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WPC + wid, TW = static_cast<uint64_t>(gridDim.x) * WPC;
   const uint32_t G0 = static_cast<uint32_t>(gw * nb / TW), G1 = static_cast<uint32_t>((gw + 1) * nb / TW);
   __syncthreads();
   if (G0 >= G1) return;
@@ -175,10 +200,10 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
   // ---- prompt slots (warp-uniform): prev / cur / next non-empty prompts around block g
   uint32_t prev_s = 0, cur_s = 0, cur_e = 0, next_e = 0, cur_p = 0, next_p = 0;
   auto load_slots = [&](uint32_t g) {
-    cur_p = h16_prompt_of(a.blk_off, N, min(g, nb - 1));
+    cur_p = a.bmap ? __ldg(a.bmap + min(g, nb - 1)) : h16_prompt_of(a.blk_off, N, min(g, nb - 1));
     cur_s = a.blk_off[cur_p];
     cur_e = a.blk_off[cur_p + 1];
-    const uint32_t pp = cur_s > 0 ? h16_prompt_of(a.blk_off, N, cur_s - 1) : cur_p;
+    const uint32_t pp = cur_s > 0 ? (a.bmap ? __ldg(a.bmap + cur_s - 1) : h16_prompt_of(a.blk_off, N, cur_s - 1)) : cur_p;
     prev_s = cur_s > 0 ? a.blk_off[pp] : cur_s;
     next_p = h16_nonempty(a.blk_off, N, cur_p + 1);
     next_e = next_p < N ? a.blk_off[next_p + 1] : cur_e;
@@ -234,12 +259,12 @@ __global__ void __launch_bounds__(kH16Warps * 32, kH16Warps <= 16 ? 2 : 1) k_has
       bw = w - sw.start;
       pw = iw;  // slot index for now: the prompt id is read only when needed (below)
     } else {  // short prompts: per-lane lookups
-      if (k0 < nb) {
-        const uint32_t p0 = h16_prompt_of(a.blk_off, N, k0);
+      if (k0 < nb) {  // the batch's block -> prompt map when the host built one (short prompts)
+        const uint32_t p0 = a.bmap ? __ldg(a.bmap + k0) : h16_prompt_of(a.blk_off, N, k0);
         tok0 = a.tok_off[p0] + 16ull * (k0 - a.blk_off[p0]);
       }
       if (w >= G0 && w < G1) {
-        pw = h16_prompt_of(a.blk_off, N, w);
+        pw = a.bmap ? __ldg(a.bmap + w) : h16_prompt_of(a.blk_off, N, w);
         bw = w - a.blk_off[pw];
         tokw = a.tok_off[pw] + 16ull * bw;
         ew = static_cast<uint32_t>(a.tok_off[pw + 1] - tokw);

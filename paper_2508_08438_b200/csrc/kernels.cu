@@ -2427,9 +2427,21 @@ int hash_scan16_grid(int device, uint32_t smem) {
   return per_sm * sms;
 }
 
-void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s) {
+void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s, int warps) {
   if (a.n_prompts == 0 || grid <= 0) return;
-  k_hash_scan16<<<grid, kH16Warps * 32, smem, s>>>(a);
+  const int w = warps > 0 && warps < static_cast<int>(kH16Warps) ? warps : static_cast<int>(kH16Warps);
+  k_hash_scan16<<<grid, w * 32, smem, s>>>(a);
+}
+
+__global__ void k_block_prompts(const uint32_t* __restrict__ blk_off, uint32_t n, uint32_t* __restrict__ map) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t b = blk_off[p] + lane; b < blk_off[p + 1]; b += 32) map[b] = p;
+}
+
+void launch_block_prompts(const uint32_t* blk_off, uint32_t n, uint32_t* map, cudaStream_t s) {
+  if (n) k_block_prompts<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(static_cast<uint64_t>(n) * 32, 256), 4096)),
+                           256, 0, s>>>(blk_off, n, map);
 }
 
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
