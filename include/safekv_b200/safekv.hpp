@@ -6,6 +6,7 @@
 // the reference's exception classes (core.hpp:19-59).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -108,12 +109,17 @@ class CompiledRuleSet {
   uint64_t version() const { return skv_rules_version(r_); }
   const skv_rules* handle() const { return r_; }
 
+  // u32 words of a window's device mask (more than 32 enabled rules: several)
+  uint32_t mask_words() const { return skv_rules_mask_words(r_); }
+
   // verdict of a device rule mask, in the reference's category order (detection.hpp:160-169)
-  DetectionVerdict verdict(uint32_t device_mask) const {
+  DetectionVerdict verdict(uint32_t device_mask) const { return verdict(&device_mask, 1); }
+  // ... of a mask of mask_words() words, word w at words[w * stride]
+  DetectionVerdict verdict(const uint32_t* words, size_t stride) const {
     DetectionVerdict v;
     std::vector<bool> hit(size(), false);
     for (uint32_t j = 0; j < skv_rules_enabled_count(r_); ++j)
-      if (device_mask >> j & 1u) hit[skv_rules_enabled_rule(r_, j)] = true;
+      if (words[(j / 32) * stride] >> (j % 32) & 1u) hit[skv_rules_enabled_rule(r_, j)] = true;
     for (uint32_t i = 0; i < size(); ++i) {
       if (!hit[i]) continue;
       const char* cat = nullptr;
@@ -146,7 +152,7 @@ class AdmissionIndex {
     std::vector<uint64_t> block_offsets;  // n + 1
     std::vector<uint64_t> key_h, key_d;   // per block
     std::vector<uint8_t> labels;          // SensitivityLabel per block
-    std::vector<uint32_t> rule_masks;     // device rule mask per block
+    std::vector<uint32_t> rule_masks;     // device rule mask per block (word 0; skv_last_rule_masks: all)
     std::vector<uint8_t> decisions;       // 0 miss, 1 public hit, 2 owner hit
     std::vector<uint32_t> matched_blocks; // per request
     std::vector<MemTier> lowest_tier;     // per request
@@ -187,9 +193,9 @@ class AdmissionIndex {
 
   // RuleEngine::tier1_scan (detection.hpp:217)
   DetectionVerdict tier1_scan(std::string_view text) {
-    uint32_t mask = 0;
-    ok(skv_tier1_scan(ctx_, text.data(), text.size(), &mask));
-    return rules_->verdict(mask);
+    std::vector<uint32_t> mask(std::max<uint32_t>(1, skv_mask_words(ctx_)), 0);
+    ok(skv_tier1_scan(ctx_, text.data(), text.size(), mask.data()));
+    return rules_->verdict(mask.data(), 1);
   }
 
   // token_seq_digest (core.hpp:68-73)

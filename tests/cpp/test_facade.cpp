@@ -115,6 +115,21 @@ int main() {
     idx.load_rules_json(
         R"({"version":1,"rules":[{"rule_id":"off","category":"X","kind":"regex","pattern":"danger","enabled":false}]})");
     CHECK(!idx.tier1_scan("danger zone").sensitive);
+    // a library of more than 32 enabled rules (several mask words): a verdict from any word, the
+    // categories in rule order (detection.hpp:160-169)
+    std::string wide = R"({"version":9,"rules":[)";
+    for (int i = 0; i < 70; ++i)
+      wide += std::string(i ? "," : "") + R"({"rule_id":"w)" + std::to_string(i) + R"(","category":"C)" +
+              std::to_string(i % 7) + R"(","kind":"regex","pattern":"tok)" + std::to_string(i) + R"(x"})";
+    wide += "]}";
+    auto ws = idx.load_rules_json(wide);
+    CHECK(ws->mask_words() == 3);
+    DetectionVerdict v65 = idx.tier1_scan("a tok65x b");
+    CHECK(v65.sensitive && v65.categories.size() == 1 && v65.categories[0] == "C2");
+    DetectionVerdict v2 = idx.tier1_scan("tok69x tok3x tok40x");  // rules 3 (C3), 40 (C5), 69 (C6)
+    CHECK(v2.sensitive && v2.categories.size() == 3 && v2.categories[0] == "C3" && v2.categories[1] == "C5" &&
+          v2.categories[2] == "C6");
+    CHECK(!idx.tier1_scan("tok70x").sensitive);
   }
   // test_core.cpp:31-45 digests are structural
   {

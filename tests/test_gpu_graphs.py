@@ -114,3 +114,35 @@ def test_step_equals_three_calls(gpu, graphs):
                    [(x.h, x.d, x.action, x.entropy_now, x.entropy_prev, x.u_pre) for x in ev_b]
             same_index(a, b)
         assert replays > 0  # the abort-and-rerun path ran
+
+
+def test_step_error_leaves_state_consistent(gpu):
+    """A commit error inside skv_step (the user table overflows: nothing of the batch is inserted)
+    aborts the speculative epoch on the device; the context stays usable and equals one driven by
+    skv_admit / skv_commit / skv_epoch through the same sequence (the failed batch's epoch is not
+    applied by either)."""
+    from paper_2508_08438_b200 import CapacityExhausted
+    rng = np.random.default_rng(5)
+    trunks = make_trunks(rng, 4)
+    cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 16, max_prompts=512,
+                       max_tokens=1 << 18, max_window_entries=1 << 13, max_users=16)
+    with AdmissionEngine(cfg) as a, AdmissionEngine(cfg) as b:
+        for step, n_users in enumerate([4, 4, 40, 4, 4]):
+            tok, off, usr, own = make_batch(rng, trunks, 100, n_users)
+            t = dev(tok.astype(np.uint32), np.int32)
+            o, u, w = dev(off, np.int64), dev(usr, np.int64), dev(own, np.uint8)
+            bt = N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), 100, len(tok), 1)
+            if n_users > 16:
+                with pytest.raises(CapacityExhausted):
+                    a.step_raw(bt)
+                b.admit_raw(bt)
+                with pytest.raises(CapacityExhausted):
+                    b.commit()
+                continue
+            _, ep_a, ev_a = a.step_raw(bt)
+            b.admit_raw(bt)
+            b.commit()
+            ep_b, ev_b = b.epoch_pass()
+            assert ep_a == ep_b
+            assert [(x.h, x.d, x.action) for x in ev_a] == [(x.h, x.d, x.action) for x in ev_b]
+            same_index(a, b)
