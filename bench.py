@@ -406,12 +406,11 @@ def run_ours(args):
         from paper_2508_08438_b200 import split_batch
         pool = split_batch(pt, po, pu, pw, pr, rank)
         pool_gids = np.flatnonzero(pr == rank).astype(np.uint64)
-    # small batches (configs 1 and 5) are bound by host round trips, not by their kernels: one
-    # skv_step call per step (CUDA-graph replayed admit / commit / epoch, one synchronisation)
-    # instead of the stages-1-2 prefetch pipeline of the large batches
-    fused_step = bool(args.fused_step)
-    fused_step = fused_step and not rep_depth
-    pipeline = not args.no_pipeline and not fused_step
+    # one skv_step call per step (admit + prefetch of the next batch + commit + stage + epoch, one
+    # host synchronisation) unless --fused-step 0; the replicated layer's merge sits between the
+    # commit and the epoch, so it keeps the separate calls
+    fused_step = bool(args.fused_step) and not rep_depth
+    pipeline = not args.no_pipeline
     replica = {}
 
     def fresh_engine():
@@ -463,8 +462,8 @@ def run_ours(args):
     # one step = admit(k) [+ stage batch k+1's stages 1-2 (and, e2e, its H2D) on the side
     # stream, overlapping] + commit(k) + epoch; nxt is None at the edge of a timed region
     def step_device(eng, k, nxt):
-        if fused_step:  # skv_step: admit + commit + epoch in one call (small batches)
-            eng.step_raw(dev_batch(k))
+        if fused_step:  # skv_step: admit + prefetch(k+1) + commit + epoch in one call
+            eng.step_raw(dev_batch(k), next_batch=dev_batch(nxt) if nxt is not None else None)
             return
         eng.admit_raw(dev_batch(k))
         if nxt is not None:
@@ -489,6 +488,10 @@ def run_ours(args):
     def step_host(eng, k, nxt):
         o = N.AdmitOut(None, None, out_label.data_ptr(), None, out_dec.data_ptr(), out_match.data_ptr(),
                        out_tier.data_ptr(), None, 0, 0, 0)
+        if fused_step:  # skv_step: admit(k) + prefetch(k+1) + commit + stage(k+2) + epoch in one call
+            stg = host_batch(nxt + 1) if nxt is not None and nxt + 1 < step_host.limit else None
+            eng.step_raw(host_batch(k), out=o, next_batch=host_batch(nxt) if nxt is not None else None, stage=stg)
+            return
         eng.admit_raw(host_batch(k), o)
         if nxt is not None:
             eng.prefetch_raw(host_batch(nxt))
@@ -655,10 +658,8 @@ def run_ours(args):
                                    if world > 1 else "single GPU"),
                    "pipeline": (f"skv_prefetch: stages 1-2 of batch k+1 overlap commit/epoch of batch k "
                                 f"({pf_dev}/{steps} device steps, {pf_e2e}/{steps} e2e steps prefetched)"
-                                if pipeline else
-                                ("device arm: one skv_step per step (CUDA-graph replayed admit/commit/epoch, one "
-                                 f"synchronisation); e2e arm: skv_stage/skv_prefetch ({pf_e2e}/{steps} prefetched)"
-                                 if fused_step else "off"))},
+                                + ("; one skv_step call per step (one host synchronisation)" if fused_step else "")
+                                if pipeline else "off")},
         "stage_ms_last": {k: round(float(last[k]), 4) for k in ("hash_scan_ms", "chain_probe_ms", "record_ms",
                                                                   "admit_total_ms", "commit_ms", "epoch_ms")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -705,8 +706,8 @@ def main():
                          "6 = one shared 8,192-token system prompt)")
     ap.add_argument("--index-log2", type=int, default=0, help="override the index capacity (debug)")
     ap.add_argument("--no-pipeline", action="store_true", help="admit each batch without skv_prefetch")
-    ap.add_argument("--fused-step", type=int, default=None, choices=[0, 1],
-                    help="device arm: one skv_step call per step instead of the prefetch pipeline (default 0)")
+    ap.add_argument("--fused-step", type=int, default=1, choices=[0, 1],
+                    help="1 (default): one skv_step call per step; 0: separate admit/prefetch/commit/stage/epoch calls")
     ap.add_argument("--e2e-u32", action="store_true", help="e2e arm: send uint32 TokenIds instead of byte tokens")
     ap.add_argument("--rep-depth", type=int, default=-1,
                     help="N > 1: replicated-layer depth (-1 = the workload's default: 512 for 6, else 0)")

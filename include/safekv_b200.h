@@ -222,12 +222,15 @@ int skv_set_monitor_config(skv_ctx* ctx, double entropy_jump, uint64_t u_pre_max
 int skv_epoch(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events, uint64_t* epoch);
 /* The events of the last skv_epoch (sorted by (h, d)); *n_events = their total count. */
 int skv_last_events(skv_ctx* ctx, skv_event* events, size_t cap, size_t* n_events);
-/* skv_admit (no per-block outputs) + skv_commit + skv_epoch of one batch in one call, with one
- * host synchronisation in the common case: the epoch pass is queued right behind the commit and
- * aborts itself on the device when the commit failed or needs its ordered replay (it then runs
- * after the replay).  Same results and errors as the three calls (A.1 with K = 1); the path for
- * small batches, whose step is otherwise bound by host round trips. */
-int skv_step(skv_ctx* ctx, const skv_batch* batch, uint64_t* new_entries, skv_event* events, size_t cap,
+/* One step of the batch pipeline in one call, with one host synchronisation in the common case:
+ * skv_admit(batch, out) -> skv_prefetch(prefetch_next) -> skv_commit -> skv_stage(stage_after) ->
+ * skv_epoch.  The admit's output copies complete with the step's synchronisation (out's summary is
+ * filled then); the epoch pass is queued right behind the commit and aborts itself on the device
+ * when the commit failed or needs its ordered replay (it then runs after the replay).  Same
+ * results and errors as the separate calls (A.1 with K = 1); prefetch_next / stage_after / out may
+ * be NULL.  Eviction, budgets and the replicated layer take the separate calls' path. */
+int skv_step(skv_ctx* ctx, const skv_batch* batch, skv_admit_out* out, const skv_batch* prefetch_next,
+             const skv_batch* stage_after, uint64_t* new_entries, skv_event* events, size_t cap,
              size_t* n_events, uint64_t* epoch_out);
 
 /* Label landing.  With pending != 0, skv_commit stores new entries

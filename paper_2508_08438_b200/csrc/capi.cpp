@@ -241,7 +241,7 @@ struct skv_ctx {
   const uint8_t* p_owners = nullptr;
   uint32_t batch_id = 0;
 
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};  // 0-4 admit, 5-6 commit, 8-9 epoch
   skv_stage_times times{};
 
   // cross-batch pipelining (skv_prefetch): stages 1-2 of the next batch on a side stream
@@ -336,6 +336,9 @@ struct skv_ctx {
   bool graphs = true;
   bool capturing = false;
   bool adm_graph = false;    // the pending batch was admitted through its graph
+  bool adm_nb_dev = false;   // the pending batch's block count arrives in host_small[20]
+  bool lazy_outputs = false; // skv_step: the admit's output copies complete with the step's synchronisation
+  skv_admit_out* adm_out = nullptr;  // ... whose summary resolve_admit fills
   uint32_t* dstate = nullptr;
   uint32_t* hstate = nullptr;  // pinned, 3 x 8 words (admit, commit, epoch)
   uint64_t rules_gen = 0;      // bumped by upload_rules (the admit graph bakes the rule tables in)
@@ -1316,6 +1319,8 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       c->rec_users = b->users;
       c->rec_n = N;
       c->adm_lazy = true;
+      c->adm_nb_dev = true;
+      c->adm_out = nullptr;
       c->adm_use_pf = false;
       c->adm_pf_pair = c->pf_pair;
       c->adm_launched = 6;
@@ -1463,7 +1468,9 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     // it) and these are read with the commit's synchronisation (resolve_admit)
     CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 11 * 4, cudaMemcpyDeviceToHost, s));
     if (!nb_known && !out) CK(cudaMemcpyAsync(c->host_small + 20, c->blk_off + N, 4, cudaMemcpyDeviceToHost, s));
-    c->adm_lazy = !out && b->on_device;
+    c->adm_lazy = (!out && b->on_device) || c->lazy_outputs;
+    c->adm_nb_dev = !out && b->on_device;
+    c->adm_out = c->adm_lazy ? out : nullptr;
     c->adm_use_pf = use_pf;
     c->adm_pf_pair = c->pf_pair;
     c->adm_launched = launched;
@@ -1489,8 +1496,13 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
 // Host-side bookkeeping of the last admit once its readbacks have landed.
 void resolve_admit(skv_ctx* c) {
   const uint32_t M = c->host_small[8 + 10];
-  if (c->adm_lazy) c->p_blocks = c->host_small[20];
+  if (c->adm_lazy && c->adm_nb_dev) c->p_blocks = c->host_small[20];
   c->adm_lazy = false;
+  if (c->adm_out) {  // a lazily admitted batch's output summary (skv_step)
+    c->adm_out->n_blocks = c->p_blocks;
+    c->adm_out->matched_total = M;
+    c->adm_out = nullptr;
+  }
   if (c->host_small[8 + 5] & 8u) throw CapacityError("user table exhausted (raise max_users)");
   const bool use_pf = c->adm_use_pf;
   const uint32_t launched = c->adm_launched;
@@ -1974,7 +1986,9 @@ void commit_finish(skv_ctx* c, const CommitRun& run, uint64_t* new_entries) {
     release_slot(c);
     c->pending = false;
     c->rec_pending = false;
-    if (c->adm_lazy) c->adm_lazy = false, c->p_blocks = c->host_small[20];
+    if (c->adm_lazy && c->adm_nb_dev) c->p_blocks = c->host_small[20];
+    c->adm_lazy = false;
+    c->adm_out = nullptr;
     const char* why = (err & 8u)   ? "user table exhausted (raise max_users); the batch was not inserted"
                       : (err & 2u) ? "index probe sequence exhausted"
                       : (err & 1u) ? "monitor window user-set pool exhausted (raise max_window_entries)"
@@ -2083,7 +2097,7 @@ EpochRun epoch_enqueue(skv_ctx* c, bool speculative) {
   const size_t pre = std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap);
   const bool graphed = c->graphs && !split;
   auto issue = [&] {
-    rec_ev(c, c->ev[5], s);
+    rec_ev(c, c->ev[8], s);
     CK(cudaMemsetAsync(c->counters + 3, 0, 8, s));  // n_cands, n_events
     if (!split) {
       // a graph's pass takes its stamps and arming from the device step state
@@ -2109,7 +2123,7 @@ EpochRun epoch_enqueue(skv_ctx* c, bool speculative) {
     CK(cudaMemcpyAsync(c->host_small + kEpochCountSlot, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
     // the first events ride along with their count (events are rare: one synchronisation)
     CK(cudaMemcpyAsync(c->host_events, c->events, pre * sizeof(skv_event), cudaMemcpyDeviceToHost, s));
-    rec_ev(c, c->ev[6], s);
+    rec_ev(c, c->ev[9], s);
   };
   if (graphed) {
     put_state(c, 2, c->rec_batch, epoch, speculative);
@@ -2135,7 +2149,7 @@ void epoch_finish(skv_ctx* c, const EpochRun& run, skv_event* events, size_t cap
   c->epoch = run.epoch;  // advance_epoch
   c->cur = 1 - c->cur;
   c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
-  c->times.epoch_ms = elapsed(c->ev[5], c->ev[6]);
+  c->times.epoch_ms = elapsed(c->ev[8], c->ev[9]);
   c->times.kernels_launched += run.split ? 6 : 1;
   std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
     return x.h != y.h ? x.h < y.h : x.d < y.d;
@@ -2170,18 +2184,23 @@ int skv_epoch(skv_ctx* c, skv_event* events, size_t cap, size_t* n_events, uint6
 // queued behind the commit speculatively (it aborts itself on the device if the commit failed or
 // needs the ordered replay; the epoch then runs again after the replay).  A small batch's step is
 // bound by host round trips otherwise.
-int skv_step(skv_ctx* c, const skv_batch* b, uint64_t* new_entries, skv_event* events, size_t cap,
-             size_t* n_events, uint64_t* epoch_out) {
+int skv_step(skv_ctx* c, const skv_batch* b, skv_admit_out* out, const skv_batch* prefetch_next,
+             const skv_batch* stage_after, uint64_t* new_entries, skv_event* events, size_t cap, size_t* n_events,
+             uint64_t* epoch_out) {
   NvtxRange nvtx_range("skv_step");
   if (!c || !b) return SKV_ERR_ARG;
-  int rc = skv_admit(c, b, nullptr);
+  const bool fused = !c->budget_on && !c->evict_on && !c->ix.rep.depth;
+  c->lazy_outputs = fused;  // the admit's output copies complete with the step's one synchronisation
+  int rc = skv_admit(c, b, out);
+  c->lazy_outputs = false;
   if (rc != SKV_OK) return rc;
-  const bool fused = c->p_n > 0 && !c->budget_on && !c->evict_on && !c->ix.rep.depth;
-  if (!fused) {
+  if (prefetch_next && (rc = skv_prefetch(c, prefetch_next)) != SKV_OK) return rc;
+  if (!fused || c->p_n == 0) {
     if ((rc = skv_commit(c, new_entries)) != SKV_OK) return rc;
+    if (stage_after && (rc = skv_stage(c, stage_after)) != SKV_OK) return rc;
     return skv_epoch(c, events, cap, n_events, epoch_out);
   }
-  return guard(c, [&] {
+  return guard(c, [&]() -> int {
     if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
       throw CapacityError("index capacity exhausted (eviction is not part of this path)");
     const CommitRun crun = commit_enqueue(c);
@@ -2189,6 +2208,10 @@ int skv_step(skv_ctx* c, const skv_batch* b, uint64_t* new_entries, skv_event* e
     sync_check(c->stream);
     const bool epoch_ran = c->host_small[4] == 0 && c->host_small[5] == 0;  // the pass's own abort test
     commit_finish(c, crun, new_entries);  // raises the commit's errors; runs the ordered replay
+    if (stage_after) {  // the committed batch's staging slot is free again: queue the H2D of a later batch
+      const int rs = skv_stage(c, stage_after);
+      if (rs != SKV_OK) return rs;
+    }
     if (epoch_ran) {
       epoch_finish(c, erun, events, cap, n_events, epoch_out);
     } else {

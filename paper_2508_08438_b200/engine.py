@@ -307,14 +307,17 @@ class AdmissionEngine:
                for e in buf[:n.value]]
         return int(ep.value), evs
 
-    def step_raw(self, batch: N.Batch, cap: int = 1 << 16) -> tuple[int, int, list[AnomalyEvent]]:
-        """``skv_step``: admit (no per-block outputs) + commit + epoch of one batch, one host
-        synchronisation in the common case.  Returns (new entries, epoch, events)."""
+    def step_raw(self, batch: N.Batch, out: Optional[N.AdmitOut] = None, next_batch: Optional[N.Batch] = None,
+                 stage: Optional[N.Batch] = None, cap: int = 1 << 16) -> tuple[int, int, list[AnomalyEvent]]:
+        """``skv_step``: admit (+ ``out``) -> prefetch ``next_batch`` -> commit -> stage ``stage`` ->
+        epoch, one host synchronisation in the common case.  Returns (new entries, epoch, events)."""
         buf = getattr(self, "_evbuf", None)
         if buf is None or len(buf) < cap:
             buf = self._evbuf = (N.Event * cap)()
         n, ep, nn = C.c_size_t(), C.c_uint64(), C.c_uint64()
-        self._check(self._lib.skv_step(self._h, C.byref(batch), C.byref(nn), buf, cap, C.byref(n), C.byref(ep)))
+        ref = lambda x: C.byref(x) if x is not None else None  # noqa: E731
+        self._check(self._lib.skv_step(self._h, C.byref(batch), ref(out), ref(next_batch), ref(stage), C.byref(nn), buf,
+                                       cap, C.byref(n), C.byref(ep)))
         if n.value > cap:
             buf = self._evbuf = (N.Event * n.value)()
             self._check(self._lib.skv_last_events(self._h, buf, n.value, C.byref(n)))

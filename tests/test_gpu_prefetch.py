@@ -233,3 +233,57 @@ def test_staged_host_pipeline_parity(ref, gpu, pattern, byte_tokens):
                 check_index(eng, re_)
         finally:
             re_.close()
+
+
+@pytest.mark.parametrize("byte_tokens", [False, True])
+def test_step_host_pipeline_parity(ref, gpu, byte_tokens):
+    """skv_step with the end-to-end call pattern folded into one call per batch -- admit(k) with
+    host outputs, prefetch(k+1), commit(k), stage(k+2), epoch, one synchronisation: the outputs
+    (filled by the step's synchronisation), events and the index equal the reference harness's
+    after every batch."""
+    B, W = 16, 32
+    rng = np.random.default_rng(404 + byte_tokens)
+    trunks = make_trunks(rng, 12)
+    batches = [make_batch(rng, trunks, 150, 4) for _ in range(7)]
+    keep = []
+    for tok, off, users, owners in batches:
+        t = np.ascontiguousarray(tok, dtype=np.uint8 if byte_tokens else np.uint32)
+        keep.append((t, off.astype(np.uint64), users.astype(np.uint64), owners.astype(np.uint8)))
+
+    def hb(k):
+        t, o, u, w = keep[k]
+        if byte_tokens:
+            return N.Batch(None, o.ctypes.data, u.ctypes.data, w.ctypes.data, len(o) - 1, len(t), 0, t.ctypes.data)
+        return N.Batch(t.ctypes.data, o.ctypes.data, u.ctypes.data, w.ctypes.data, len(o) - 1, len(t), 0)
+
+    cfg = EngineConfig(block_tokens=B, window_tokens=W, index_capacity=1 << 18, max_prompts=4096,
+                       max_tokens=1 << 20, max_window_entries=1 << 15, entropy_jump=0.3, u_pre_max=1)
+    with AdmissionEngine(cfg) as eng:
+        rs = eng.rules
+        re_ = RefEngine(ref, RefRules(ref, None), B=B, W=W, jump=0.3, u_pre_max=1)
+        try:
+            eng.stage_raw(hb(0))
+            eng.stage_raw(hb(1))
+            eng.prefetch_raw(hb(0))
+            for k, batch in enumerate(batches):
+                o, got = _admit_out(len(batch[2]), len(batch[0]) // B + 1)
+                nxt = hb(k + 1) if k + 1 < len(batches) else None
+                stg = hb(k + 2) if k + 2 < len(batches) else None
+                _, ep_g, ev_g = eng.step_raw(hb(k), out=o, next_batch=nxt, stage=stg)
+                exp = re_.admit(*batch)
+                n = o.n_blocks
+                assert n == len(exp["block_h"])
+                np.testing.assert_array_equal(got["block_h"][:n], exp["block_h"])
+                np.testing.assert_array_equal(device_to_rule_masks(rs, got["rule_mask"][:n]), exp["mask"])
+                np.testing.assert_array_equal(got["label"][:n], exp["label"])
+                np.testing.assert_array_equal(got["decision"][:n], exp["decision"])
+                np.testing.assert_array_equal(got["matched_blocks"], exp["matched_blocks"])
+                np.testing.assert_array_equal(got["lowest_tier"], exp["lowest_tier"])
+                re_.commit()
+                ep_r, ev_r = re_.epoch(cap=1 << 16)
+                assert ep_g == ep_r
+                check_events(ev_g, ev_r)
+                check_index(eng, re_)
+                assert eng.times()["prefetched"] == 1  # every batch was staged and prefetched
+        finally:
+            re_.close()
