@@ -485,8 +485,16 @@ class AdmissionEngine:
         return int(self._lib.skv_entry_count(self._h))
 
     def times(self) -> dict:
+        return self.times_dict(self.times_raw())
+
+    def times_raw(self) -> "N.StageTimes":
+        """``skv_last_times`` as the raw struct (one ctypes call; ``times_dict`` converts)."""
         t = N.StageTimes()
         self._check(self._lib.skv_last_times(self._h, C.byref(t)))
+        return t
+
+    @staticmethod
+    def times_dict(t: "N.StageTimes") -> dict:
         return {f: getattr(t, f) for f, _ in N.StageTimes._fields_}
 
     def tier1_scan(self, text: str | bytes) -> int:
