@@ -1185,6 +1185,9 @@ constexpr int kCPPrompts = SKV_KCPPROMPTS;  // prompts per warp: 4096 warps for 
 #define SKV_KCPINFLIGHT 8
 #endif
 constexpr int kCPInFlight = SKV_KCPINFLIGHT;  // prompts whose probe loads are in flight together
+#ifndef SKV_KCP_HALVES_MIN_PROMPTS
+#define SKV_KCP_HALVES_MIN_PROMPTS 16384  // two probe waves per tile from this batch size on (measured:
+#endif                                    // config 2 probe 0.137 -> 0.111 ms; config 5 0.035 -> 0.040)
 constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
 
 struct Probe {
@@ -1272,7 +1275,8 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
     const uint32_t* __restrict__ first_sens, const uint32_t* __restrict__ uidx, uint32_t n_prompts,
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
-    uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon, uint32_t* __restrict__ bprompt) {
+    uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon, uint32_t* __restrict__ bprompt,
+    uint32_t halves) {
   __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
   __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -1329,7 +1333,13 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
       }
     }
     }  // !kPre
-    uint32_t todo = __ballot_sync(kFull, has && k == n && n > t0);
+    // large batches probe in two waves of 16 blocks (halves = 2): the second half of a tile is probed only
+    // for prompts whose first half found no miss, so a tile holding a prompt's first miss wastes at
+    // most 15 random probes past it instead of 31 (config 2: ~23 -> ~7 per prompt)
+    for (uint32_t half = 0; half < halves; ++half) {
+    const uint32_t lo_b = t0 + half * (32 / halves);
+    const bool in_half = halves == 1 || (lane >> 4) == half;
+    uint32_t todo = __ballot_sync(kFull, has && k == n && n > lo_b);
     while (todo) {
       uint32_t js[kCPInFlight];
       int ng = 0;
@@ -1351,7 +1361,7 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
         kk[q] = make_ulonglong2(0, 0);
         mm[q] = make_ulonglong2(0, 0);
         ss[q] = 0;
-        if (q < ng && b < nj) {
+        if (q < ng && b < nj && in_half) {
           ss[q] = home_slot(ix, th[j][lane & ~(kGroup - 1)], td[j][lane & ~(kGroup - 1)], b);
           const ulonglong2* rp = reinterpret_cast<const ulonglong2*>(&ix.e[ss[q]].rec);
           kk[q] = rp[0];
@@ -1365,7 +1375,7 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
         const uint32_t bj = __shfl_sync(kFull, bo, j), nj = __shfl_sync(kFull, n, j);
         const uint32_t uj = __shfl_sync(kFull, user, j);
         const uint32_t mj = __shfl_sync(kFull, m, j);
-        const bool act = b < nj;
+        const bool act = b < nj && in_half;
         Probe pr{kNone, 0, 0};
         if (act) pr = probe_resolve(ix, th[j][lane], td[j][lane], ss[q], kk[q], mm[q]);
         const bool found = pr.slot != kNone && meta_live(pr.meta);  // a tombstone is missing
@@ -1393,6 +1403,7 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
         }
       }
     }
+    }  // halves
     __syncwarp();
   }
   if (has) {
@@ -2455,7 +2466,7 @@ void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_
                                                                                  : ~0ull)),
                     kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
                                                                    decision, slot, matched, exist, tier, bmeta, mon,
-                                                                   bprompt);
+                                                                   bprompt, n >= SKV_KCP_HALVES_MIN_PROMPTS ? 2u : 1u);
 }
 
 uint32_t record_grid(int device) {
