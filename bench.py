@@ -482,22 +482,22 @@ def run_ours(args):
     out_match = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
     out_tier = torch.empty(n_local, dtype=torch.uint8, pin_memory=True)
 
-    # e2e step: the PCIe copy of the inputs is the bottleneck, so batch k+2's copy is queued
+    # e2e step: the PCIe copy of the inputs is the bottleneck, so batch k+3's copy is queued
     # (skv_stage) as soon as batch k's commit frees its staging slot, and runs while batch k+1
     # is admitted; batch k+1's stages 1-2 are prefetched from its staged copy
     def step_host(eng, k, nxt):
         o = N.AdmitOut(None, None, out_label.data_ptr(), None, out_dec.data_ptr(), out_match.data_ptr(),
                        out_tier.data_ptr(), None, 0, 0, 0)
-        if fused_step:  # skv_step: admit(k) + prefetch(k+1) + commit + stage(k+2) + epoch in one call
-            stg = host_batch(nxt + 1) if nxt is not None and nxt + 1 < step_host.limit else None
+        if fused_step:  # skv_step: admit(k) + prefetch(k+1) + commit + stage(k+3) + epoch in one call
+            stg = host_batch(nxt + 2) if nxt is not None and nxt + 2 < step_host.limit else None
             eng.step_raw(host_batch(k), out=o, next_batch=host_batch(nxt) if nxt is not None else None, stage=stg)
             return
         eng.admit_raw(host_batch(k), o)
         if nxt is not None:
             eng.prefetch_raw(host_batch(nxt))
         eng.commit()
-        if nxt is not None and nxt + 1 < step_host.limit:
-            eng.stage_raw(host_batch(nxt + 1))
+        if nxt is not None and nxt + 2 < step_host.limit:
+            eng.stage_raw(host_batch(nxt + 2))
         if replica:
             replica["g"].sync(batch_gids[k])
         eng.epoch_pass()
@@ -518,9 +518,8 @@ def run_ours(args):
             if not pipe or first >= limit:
                 return
             if step_fn is step_host:
-                eng.stage_raw(host_batch(first))
-                if first + 1 < limit:
-                    eng.stage_raw(host_batch(first + 1))
+                for j in range(first, min(first + 3, limit)):  # three staging slots
+                    eng.stage_raw(host_batch(j))
                 eng.prefetch_raw(host_batch(first))
             else:
                 eng.prefetch_raw(dev_batch(first))

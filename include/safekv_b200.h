@@ -190,11 +190,11 @@ uint32_t skv_mask_words(const skv_ctx* ctx);
  * a time). */
 int skv_prefetch(skv_ctx* ctx, const skv_batch* next);
 /* Host-input staging (end-to-end pipelining): queue the host->device copy of a HOST batch
- * (tokens or token bytes, offsets, users, owners) on a copy stream into one of two device
- * slots, so the copy of batch k+1 or k+2 overlaps the admission of batch k.  A later
+ * (tokens or token bytes, offsets, users, owners) on a copy stream into one of three device
+ * slots, so the copies of batches k+1..k+3 overlap the admission of batch k.  A later
  * skv_prefetch / skv_admit of the same batch (same pointers and sizes) reads the staged copy;
  * the caller keeps the host buffers unchanged until that admit returns.  A slot is reused once
- * the batch admitted from it is committed (or dropped); with both slots busy the call stages
+ * the batch admitted from it is committed (or dropped); with every slot busy the call stages
  * nothing and the batch is copied inline later.  Pinned host memory makes the copy
  * asynchronous.  No reference counterpart (the reference has no device). */
 int skv_stage(skv_ctx* ctx, const skv_batch* batch);

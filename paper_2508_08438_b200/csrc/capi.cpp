@@ -300,7 +300,8 @@ struct skv_ctx {
     uint64_t ntok = 0;
     bool bytes = false;
   };
-  HostSlot hslot[2];
+  static constexpr int kHostSlots = 3;  // batch k in use, k+1 prefetched, k+2 copying: the copy engine never waits
+  HostSlot hslot[kHostSlots];
   cudaStream_t copy = nullptr;
 
   // A.9 tier budgets (skv_set_tier_budget): capacities and used blocks per tier; the commit then
@@ -1052,9 +1053,9 @@ int skv_stage(skv_ctx* c, const skv_batch* b) {
     if (N == 0 || (!b->tokens && !b->token_bytes) || !b->offsets || !b->users) return SKV_OK;
     if (find_staged(c, b) >= 0) return SKV_OK;
     int si = -1;
-    for (int i = 0; i < 2 && si < 0; ++i)
+    for (int i = 0; i < skv_ctx::kHostSlots && si < 0; ++i)
       if (c->hslot[i].state == skv_ctx::kSlotFree) si = i;
-    if (si < 0) return SKV_OK;  // both slots busy: the prefetch / admit copies it inline
+    if (si < 0) return SKV_OK;  // every slot busy: the prefetch / admit copies it inline
     auto& hs = c->hslot[si];
     if (!c->copy) CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     if (!hs.tok) {
@@ -1202,7 +1203,7 @@ void ensure_admit_resolved(skv_ctx* c) {
 // ------------------------------------------------------------------ host staging ring
 int find_staged(skv_ctx* c, const skv_batch* b) {
   const void* tok = b->token_bytes ? static_cast<const void*>(b->token_bytes) : b->tokens;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < skv_ctx::kHostSlots; ++i) {
     const auto& h = c->hslot[i];
     if (h.state == skv_ctx::kSlotStaged && h.id_tok == tok && h.id_off == b->offsets && h.id_users == b->users &&
         h.id_owners == b->owners && h.n == b->n_prompts && h.ntok == b->n_tokens && h.bytes == (b->token_bytes != nullptr))
