@@ -175,6 +175,13 @@ int skv_last_rule_masks(skv_ctx* ctx, uint32_t* out, int on_device);
  * once per buffer set; the per-step stamps come from a device-side step state.  Results are
  * identical either way; only the host issue cost differs. */
 int skv_set_graphs(skv_ctx* ctx, int on);
+/* Diagnostic (no reference counterpart; SURVEY D4 -- the monitor's flags use the reference's
+ * u / h predicate): for every entry the last admitted batch matched, that batch's accesses, its
+ * distinct users and the Shannon entropy in bits of its accesses over users, H = log2 T -
+ * sum_u c_u log2 c_u / T.  Entries in slot order; *n_entries = all of them (the first cap are
+ * written).  Valid until the next skv_admit. */
+int skv_access_entropy(skv_ctx* ctx, uint64_t* h, uint64_t* d, uint64_t* accesses, uint64_t* users, double* bits,
+                       size_t cap, size_t* n_entries);
 /* mask words of the context's active rule set (skv_rules_mask_words of it) */
 uint32_t skv_mask_words(const skv_ctx* ctx);
 /* Cross-batch pipelining: stage the NEXT device-resident batch's digests and window

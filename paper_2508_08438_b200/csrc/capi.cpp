@@ -1581,6 +1581,46 @@ int skv_admit_ttft(skv_ctx* c, const uint64_t* request_ids, double* ttft_ms, uin
 
 uint32_t skv_mask_words(const skv_ctx* c) { return c ? c->mask_words : 0; }
 
+int skv_access_entropy(skv_ctx* c, uint64_t* h, uint64_t* d, uint64_t* accesses, uint64_t* users, double* bits,
+                       size_t cap, size_t* n_entries) {
+  if (!c || (cap && (!h || !d || !accesses || !users || !bits))) return SKV_ERR_ARG;
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    ensure_admit_resolved(c);
+    const uint64_t M = c->times.matched_total;
+    if (!c->last_n || M == 0) {
+      if (n_entries) *n_entries = 0;
+      return SKV_OK;
+    }
+    if (M > 0xffffffffull) throw ArgError("access entropy: batch too large");
+    std::vector<void*> tmp;
+    const uint32_t w = static_cast<uint32_t>(std::min<size_t>(cap, M));
+    uint64_t* dh = dalloc<uint64_t>(std::max<uint32_t>(w, 1), tmp);
+    uint64_t* dd = dalloc<uint64_t>(std::max<uint32_t>(w, 1), tmp);
+    uint64_t* da = dalloc<uint64_t>(std::max<uint32_t>(w, 1), tmp);
+    uint64_t* du = dalloc<uint64_t>(std::max<uint32_t>(w, 1), tmp);
+    double* db = dalloc<double>(std::max<uint32_t>(w, 1), tmp);
+    uint32_t total = 0, wr = 0;
+    try {
+      wr = skv::launch_access_entropy(c->ix, c->blk_off, c->matched, c->bslot, c->uidx, c->last_n,
+                                      static_cast<uint32_t>(M), dh, dd, da, du, db, w, &total, c->stream);
+      if (wr) {
+        CK(cudaMemcpy(h, dh, wr * 8ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(d, dd, wr * 8ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(accesses, da, wr * 8ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(users, du, wr * 8ull, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(bits, db, wr * 8ull, cudaMemcpyDeviceToHost));
+      }
+    } catch (const std::runtime_error& e) {
+      for (void* p : tmp) cudaFree(p);
+      throw CudaError(e.what());
+    }
+    for (void* p : tmp) cudaFree(p);
+    if (n_entries) *n_entries = total;
+    return SKV_OK;
+  });
+}
+
 int skv_set_graphs(skv_ctx* c, int on) {
   if (!c) return SKV_ERR_ARG;
   c->graphs = on != 0;

@@ -326,6 +326,12 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
 uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap);
 int hash_scan16_grid(int device, uint32_t smem);
 void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s, int warps = 0);
+// diagnostic: per entry matched by the last admitted batch, its accesses, distinct users and the
+// Shannon entropy (bits) of the batch's accesses over users; returns the entries written
+uint32_t launch_access_entropy(const Index& ix, const uint32_t* blk_off, const uint32_t* matched,
+                               const uint32_t* slot, const uint32_t* uidx, uint32_t n_prompts, uint32_t n_access,
+                               uint64_t* out_h, uint64_t* out_d, uint64_t* out_acc, uint64_t* out_users,
+                               double* out_bits, uint32_t cap, uint32_t* total, cudaStream_t s);
 // block -> prompt map of a batch (warp per prompt), for short-prompt batches
 void launch_block_prompts(const uint32_t* blk_off, uint32_t n_prompts, uint32_t* map, cudaStream_t s);
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,

@@ -13,6 +13,10 @@
 // No tensor cores: nothing here is a contraction.  Everything is integer/byte work
 // bounded by HBM, shared-memory lookups or memory latency.
 #include <cooperative_groups.h>
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+#include <vector>
 #include <cub/cub.cuh>
 
 #include "../../include/safekv_b200.h"
@@ -2504,6 +2508,121 @@ size_t sort_keys_temp_bytes(uint32_t n, int end_bit) {
 void launch_sort_keys(void* temp, size_t temp_bytes, const unsigned long long* in, unsigned long long* out, uint32_t n,
                       int end_bit, cudaStream_t s) {
   cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, n, 0, end_bit, s);
+}
+
+// ---------------------------------------------------------------------------------
+// Diagnostic (no reference counterpart): per entry matched by the last admitted
+// batch, the histogram of that batch's accesses over users and its Shannon entropy in bits.
+// (entry slot, user) keys of every matched block -> radix sort -> run-length encode (per-user
+// counts) -> reduce by entry (accesses T, distinct users D, sum c log2 c) -> H = log2 T - S / T.
+// The monitor's flags stay on the reference predicate (u / h, monitor.hpp:68-70).
+// ---------------------------------------------------------------------------------
+struct EntHist {
+  unsigned long long accesses;
+  unsigned long long users;
+  double clogc;  // sum over users of c * log2(c)
+};
+struct EntHistSum {
+  __host__ __device__ EntHist operator()(const EntHist& a, const EntHist& b) const {
+    return EntHist{a.accesses + b.accesses, a.users + b.users, a.clogc + b.clogc};
+  }
+};
+
+__global__ void k_entropy_emit(const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ matched,
+                               const uint32_t* __restrict__ slot, const uint32_t* __restrict__ uidx, uint32_t n,
+                               unsigned long long* keys, uint32_t* n_keys, uint32_t cap) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t bo = blk_off[p], m = matched[p];
+    const unsigned long long u = uidx[p];
+    for (uint32_t b = lane; b < m; b += 32) {
+      const uint32_t k = atomicAdd(n_keys, 1u);
+      if (k < cap) keys[k] = (static_cast<unsigned long long>(slot[bo + b]) << 32) | u;
+    }
+  }
+}
+
+__global__ void k_entropy_runs(const unsigned long long* __restrict__ ukeys, const uint32_t* __restrict__ counts,
+                               const uint32_t* __restrict__ n_runs, uint32_t* __restrict__ eslot,
+                               EntHist* __restrict__ vals) {
+  const uint32_t n = *n_runs;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double c = counts[i];
+    eslot[i] = static_cast<uint32_t>(ukeys[i] >> 32);
+    vals[i] = EntHist{counts[i], 1ull, c * log2(c)};
+  }
+}
+
+__global__ void k_entropy_out(Index ix, const uint32_t* __restrict__ eslot, const EntHist* __restrict__ h,
+                              const uint32_t* __restrict__ n_seg, uint64_t* __restrict__ out_h,
+                              uint64_t* __restrict__ out_d, uint64_t* __restrict__ out_acc,
+                              uint64_t* __restrict__ out_users, double* __restrict__ out_bits) {
+  const uint32_t n = *n_seg;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const Rec& r = ix.e[eslot[i]].rec;
+    const double T = static_cast<double>(h[i].accesses);
+    out_h[i] = r.h;
+    out_d[i] = r.d;
+    out_acc[i] = h[i].accesses;
+    out_users[i] = h[i].users;
+    out_bits[i] = log2(T) - h[i].clogc / T;
+  }
+}
+
+// Returns the entries written (<= cap); *total = the batch's matched entries
+uint32_t launch_access_entropy(const Index& ix, const uint32_t* blk_off, const uint32_t* matched,
+                               const uint32_t* slot, const uint32_t* uidx, uint32_t n_prompts, uint32_t n_access,
+                               uint64_t* out_h, uint64_t* out_d, uint64_t* out_acc, uint64_t* out_users,
+                               double* out_bits, uint32_t cap, uint32_t* total, cudaStream_t s) {
+  std::vector<void*> tmp;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      for (void* q : tmp) cudaFree(q);
+      throw std::runtime_error("cudaMalloc: access entropy scratch");
+    }
+    tmp.push_back(p);
+    return p;
+  };
+  const uint32_t n = std::max<uint32_t>(n_access, 1);
+  auto* keys = static_cast<unsigned long long*>(alloc(8ull * n));
+  auto* sorted = static_cast<unsigned long long*>(alloc(8ull * n));
+  auto* ukeys = static_cast<unsigned long long*>(alloc(8ull * n));
+  auto* counts = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* eslot = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* seg = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* vals = static_cast<EntHist*>(alloc(sizeof(EntHist) * n));
+  auto* hist = static_cast<EntHist*>(alloc(sizeof(EntHist) * n));
+  auto* ctr = static_cast<uint32_t*>(alloc(16));
+  cudaMemsetAsync(ctr, 0, 16, s);
+  k_entropy_emit<<<std::max<uint32_t>(1, std::min<uint32_t>(cdiv(static_cast<uint64_t>(n_prompts) * 32, 256), 4096)),
+                   256, 0, s>>>(blk_off, matched, slot, uidx, n_prompts, keys, ctr, n);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, keys, sorted, n_access, 0, 64, s);
+  cub::DeviceRunLengthEncode::Encode(nullptr, b2, sorted, ukeys, counts, ctr + 1, n_access, s);
+  cub::DeviceReduce::ReduceByKey(nullptr, b3, eslot, seg, vals, hist, ctr + 2, EntHistSum{}, n_access, s);
+  void* t = alloc(std::max({b1, b2, b3}));
+  const size_t tb = std::max({b1, b2, b3});
+  cub::DeviceRadixSort::SortKeys(t, b1 = tb, keys, sorted, n_access, 0, 64, s);
+  cub::DeviceRunLengthEncode::Encode(t, b2 = tb, sorted, ukeys, counts, ctr + 1, n_access, s);
+  uint32_t h_runs = 0;
+  cudaMemcpyAsync(&h_runs, ctr + 1, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  k_entropy_runs<<<std::max<uint32_t>(1, cdiv(h_runs, 256)), 256, 0, s>>>(ukeys, counts, ctr + 1, eslot, vals);
+  cub::DeviceReduce::ReduceByKey(t, b3 = tb, eslot, seg, vals, hist, ctr + 2, EntHistSum{}, h_runs, s);
+  uint32_t h_seg = 0;
+  cudaMemcpyAsync(&h_seg, ctr + 2, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const uint32_t w = std::min(h_seg, cap);
+  if (w) {
+    cudaMemcpyAsync(ctr + 3, &w, 4, cudaMemcpyHostToDevice, s);
+    k_entropy_out<<<cdiv(w, 256), 256, 0, s>>>(ix, seg, hist, ctr + 3, out_h, out_d, out_acc, out_users, out_bits);
+  }
+  const cudaError_t e = cudaStreamSynchronize(s);
+  for (void* q : tmp) cudaFree(q);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("access entropy: ") + cudaGetErrorString(e));
+  *total = h_seg;
+  return w;
 }
 
 // ---------------------------------------------------------------------------------

@@ -253,6 +253,18 @@ class AdmissionEngine:
             res.rule_mask_words = self.last_rule_masks()
         return res
 
+    def access_entropy(self, cap: int = 1 << 22) -> dict:
+        """Diagnostic (``skv_access_entropy``; no reference counterpart): for every entry the last
+        admitted batch matched, its accesses, distinct users and the Shannon entropy (bits) of the
+        batch's accesses over users.  The monitor's leak flags use the reference predicate."""
+        out = {k: np.zeros(cap, t) for k, t in (("h", np.uint64), ("d", np.uint64), ("accesses", np.uint64),
+                                                ("users", np.uint64), ("bits", np.float64))}
+        n = C.c_size_t()
+        self._check(self._lib.skv_access_entropy(self._h, _ptr(out["h"]), _ptr(out["d"]), _ptr(out["accesses"]),
+                                                 _ptr(out["users"]), _ptr(out["bits"]), cap, C.byref(n)))
+        k = min(int(n.value), cap)
+        return {key: v[:k] for key, v in out.items()}
+
     def set_graphs(self, on: bool) -> None:
         """CUDA-graph replay of small device-batch steps (``skv_set_graphs``; default on)."""
         self._check(self._lib.skv_set_graphs(self._h, 1 if on else 0))

@@ -151,6 +151,8 @@ SIGNATURES = {
     "skv_rules_mask_words": (C.c_uint32, [C.c_void_p]),
     "skv_mask_words": (C.c_uint32, [C.c_void_p]),
     "skv_set_graphs": (C.c_int, [C.c_void_p, C.c_int]),
+    "skv_access_entropy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_size_t, C.c_void_p]),
     "skv_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                            C.c_size_t, C.c_void_p, C.c_void_p]),
     "skv_last_rule_masks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

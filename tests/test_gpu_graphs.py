@@ -146,3 +146,37 @@ def test_step_error_leaves_state_consistent(gpu):
             assert ep_a == ep_b
             assert [(x.h, x.d, x.action) for x in ev_a] == [(x.h, x.d, x.action) for x in ev_b]
             same_index(a, b)
+
+
+def test_access_entropy_diagnostic(gpu):
+    """skv_access_entropy (SURVEY D4's Shannon-entropy diagnostic; no reference oracle): per entry
+    the last batch matched, its accesses, distinct users and Shannon entropy over users -- against
+    a numpy restatement from the same batch's admit outputs (match lengths, keys, users)."""
+    import collections
+    import math
+    from paper_2508_08438_b200 import AdmissionEngine, EngineConfig
+    rng = np.random.default_rng(12)
+    trunks = make_trunks(rng, 5, pii_p=0.0)
+    cfg = EngineConfig(block_tokens=16, window_tokens=32, index_capacity=1 << 16, max_prompts=1024,
+                       max_tokens=1 << 19, max_window_entries=1 << 14)
+    with AdmissionEngine(cfg) as eng:
+        eng.admit(*make_batch(rng, trunks, 300, 7, pii_p=0.0))
+        eng.commit()
+        for _ in range(2):
+            tok, off, usr, own = make_batch(rng, trunks, 300, 9, pii_p=0.0)
+            res = eng.admit(tok, off, usr, own)
+            got = eng.access_entropy()
+            hist = collections.defaultdict(collections.Counter)
+            bo = res.block_offsets
+            for p in range(len(usr)):
+                for b in range(int(res.matched_blocks[p])):
+                    hist[(int(res.block_h[bo[p] + b]), int(res.block_d[bo[p] + b]))][int(usr[p])] += 1
+            assert len(got["h"]) == len(hist) > 0
+            for i in range(len(got["h"])):
+                cnt = hist[(int(got["h"][i]), int(got["d"][i]))]
+                T = sum(cnt.values())
+                H = math.log2(T) - sum(c * math.log2(c) for c in cnt.values()) / T
+                assert (int(got["accesses"][i]), int(got["users"][i])) == (T, len(cnt))
+                assert got["bits"][i] == pytest.approx(H, rel=1e-12, abs=1e-12)
+            eng.commit()
+            eng.epoch_pass()
