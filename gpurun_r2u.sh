@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+SKV_EPOCH_SPLIT=1 timeout 900 python -m pytest tests/test_gpu_graphs.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q -p no:cacheprovider > gpurun_out/u_pytest_split.log 2>&1; echo "split rc=$?"; tail -1 gpurun_out/u_pytest_split.log
+timeout 900 python -m pytest tests/test_gpu_graphs.py tests/test_gpu_parity.py "tests/test_gpu_scale.py::test_scale_config4_long_context_tiered" -x -q -p no:cacheprovider > gpurun_out/u_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/u_pytest.log
+for w in 4 2 5; do timeout 600 python bench.py --workload $w --no-cpu-baseline > gpurun_out/u_wl$w.json 2>/dev/null
+python - gpurun_out/u_wl$w.json <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+print(sys.argv[1], round(d["value"]/1e9,4), round(d["ms_per_step"],4), "e2e", round(d["e2e"]["value"]/1e9,4), "epoch", d["step_breakdown"]["epoch_ms"], d["stage_ms_last"]["epoch_ms"])
+PY
+done

@@ -37,6 +37,7 @@ struct skv_rules {
 constexpr bool kRecordBeside = SKV_REC_BESIDE != 0;
 constexpr size_t kEpochEvPre = 128;  // events read back with an epoch's count
 constexpr int kEpochCountSlot = 56;  // host_small word of the epoch's event count
+constexpr uint64_t kEpochSplitMin = 65536;  // touched entries from which the epoch runs as six kernels
 #ifndef SKV_STREAM_PRIO
 #define SKV_STREAM_PRIO 0
 #endif
@@ -338,6 +339,8 @@ struct skv_ctx {
   bool capturing = false;
   bool adm_graph = false;    // the pending batch was admitted through its graph
   bool adm_nb_dev = false;   // the pending batch's block count arrives in host_small[20]
+  double probe_est = -1.0;   // mean matched blocks per prompt of the last resolved admit (probe wave split)
+  uint64_t touched_est = 0;  // entries in the current window list after the last commit (epoch shape)
   bool lazy_outputs = false; // skv_step: the admit's output copies complete with the step's synchronisation
   skv_admit_out* adm_out = nullptr;  // ... whose summary resolve_admit fills
   uint32_t* dstate = nullptr;
@@ -706,6 +709,19 @@ struct NvtxRange {
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
+
+// First block (a multiple of 32) from which k_chain_probe probes a tile in two waves: the tile
+// expected to hold a large batch's first misses (the previous batch's mean match length), so the
+// probes past a miss shrink without adding rounds to the all-found tiles before it.  Performance
+// only: every choice gives the same results.
+uint32_t probe_split_from(const skv_ctx* c, uint32_t N) {
+  static const char* force = std::getenv("SKV_PROBE_SPLIT");  // diagnostic / tests: a fixed split block
+  if (force) return static_cast<uint32_t>(std::strtoul(force, nullptr, 10));
+  if (N < 16384 || c->probe_est < 0) return UINT32_MAX;
+  if (c->probe_est < 24) return 0;
+  if (c->probe_est < 64) return 32;
+  return UINT32_MAX;
+}
 
 // an event record inside a captured phase is an external event node (its timestamps stay
 // readable after the graph ran)
@@ -1276,6 +1292,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
       const bool unaligned = !bytes && reinterpret_cast<uintptr_t>(b->tokens) % 16 != 0;
       const uint32_t* tokens = (bytes || unaligned) ? c->d_tokens : b->tokens;
       const uint64_t nb_bound = b->n_tokens / B;
+      const uint32_t split = probe_split_from(c, N);
       skv::MonCtx mon = monitor_ctx(c);
       mon.st = c->dstate;
       mon.tl[0] = c->touched[0];
@@ -1289,7 +1306,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
           reinterpret_cast<uintptr_t>(c->blk_off), reinterpret_cast<uintptr_t>(c->first_sens),
           reinterpret_cast<uintptr_t>(c->bslot), reinterpret_cast<uintptr_t>(c->blabel),
           reinterpret_cast<uintptr_t>(c->counts), reinterpret_cast<uintptr_t>(c->plen), c->rules_gen, c->mask_words,
-          static_cast<uintptr_t>(bytes), static_cast<uintptr_t>(unaligned)};
+          static_cast<uintptr_t>(bytes), static_cast<uintptr_t>(unaligned), split};
       put_state(c, 0, mon.batch, c->epoch);
       run_graph(c, c->g_admit, key, [&] {
         rec_ev(c, c->ev[0], s);
@@ -1309,7 +1326,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
         skv::launch_intern_users(c->users_tab, b->users, N, c->uidx, c->counters + 5, s);
         skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel,
                                 c->bdecision, c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt, 0,
-                                s);
+                                split, s);
         rec_ev(c, c->ev[3], s);
         rec_ev(c, c->ev[4], s);
         CK(cudaMemcpyAsync(c->host_small + 8, c->counters, 11 * 4, cudaMemcpyDeviceToHost, s));
@@ -1438,7 +1455,7 @@ int skv_admit(skv_ctx* c, const skv_batch* b, skv_admit_out* out) {
     skv::launch_intern_users(c->users_tab, users, N, c->uidx, c->counters + 5, s);
     skv::launch_chain_probe(c->ix, c->bd, c->blk_off, c->first_sens, c->uidx, N, c->bh, c->blabel, c->bdecision,
                             c->bslot, c->matched, c->exist, c->tier, c->bmeta, mon, c->bprompt,
-                            use_pf && kPrefetchChain ? 1 : 0, s);
+                            use_pf && kPrefetchChain ? 1 : 0, probe_split_from(c, N), s);
     if (c->evict_on)  // match_prefix refreshes the access epoch of every visible matched node
       skv::launch_touch_matched(c->ix, c->bslot, c->blk_off, c->matched, N, static_cast<uint32_t>(c->epoch), s);
     CK(cudaEventRecord(c->ev[3], s));
@@ -1516,6 +1533,7 @@ void resolve_admit(skv_ctx* c) {
     c->times.admit_total_ms = elapsed(c->ev[0], c->ev[4]);
     c->times.matched_total = M;
     c->times.accesses = M;
+    if (c->last_n) c->probe_est = static_cast<double>(M) / c->last_n;
     c->times.replayed_entries = 0;
     c->times.touched_entries = c->host_small[8 + 1 + c->cur];
     c->times.kernels_launched = launched;
@@ -1990,6 +2008,7 @@ CommitRun commit_enqueue(skv_ctx* c) {
     CK(cudaMemcpyAsync(c->host_small + 5, c->counters + 8, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 6, c->counters + 12, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->host_small + 7, c->counters + 7, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->host_small + 44, c->counters + 1, 8, cudaMemcpyDeviceToHost, s));  // both window lists
   };
   if (graphed) {
     const std::vector<uintptr_t> key = {
@@ -2039,6 +2058,7 @@ void commit_finish(skv_ctx* c, const CommitRun& run, uint64_t* new_entries) {
     throw CapacityError(why);
   }
   if (c->adm_lazy) resolve_admit(c);  // the admit's readbacks landed with it
+  c->touched_est = c->host_small[44 + c->cur];
   if (rec) launched += replay_record(c, s, c->host_small[5], err);
   if (c->evict_on) {
     // the insert walk refreshes every pre-existing block's access epoch; node ids are exact
@@ -2133,8 +2153,13 @@ EpochRun epoch_enqueue(skv_ctx* c, bool speculative) {
   // device, so the epoch needs no host round trip before its kernels
   const int cur = c->cur, prev = 1 - c->cur;
   const uint32_t bound = 2 * c->pool_cap;
-  static const bool split_env = getenv_flag("SKV_EPOCH_SPLIT");  // diagnostic: the six-kernel pass
-  const bool split = split_env && !speculative;
+  // the pass as six kernels over the window lists' capacity (every entry its own thread) when the
+  // last admit's window was large: the fused pass's co-resident grid strides over such lists with
+  // less memory parallelism (config 4, ~0.5 M touched entries: 0.35 vs 0.29 ms); one cooperative
+  // launch otherwise (small windows are launch-bound).  SKV_EPOCH_SPLIT=1 / 0 forces either.
+  static const char* split_env = std::getenv("SKV_EPOCH_SPLIT");
+  const bool split = split_env ? std::atoi(split_env) != 0 : c->touched_est > kEpochSplitMin;
+  const uint32_t* guard = speculative ? c->counters : nullptr;
   const size_t pre = std::min<size_t>(kEpochEvPre, 2ull * c->pool_cap);
   const bool graphed = c->graphs && !split;
   auto issue = [&] {
@@ -2148,18 +2173,17 @@ EpochRun epoch_enqueue(skv_ctx* c, bool speculative) {
                                  (graphed || speculative) ? c->counters : nullptr, c->device, s));
     } else {
       skv::launch_epoch_candidates(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, stamp,
-                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s, guard);
       skv::launch_epoch_candidates(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, stamp,
-                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s);
+                                   c->cfg.entropy_jump, c->cfg.u_pre_max, c->cands, c->counters + 3, s, guard);
       skv::launch_epoch_fire(c->ix, c->cands, c->counters + 3, bound, stamp, epoch, c->events, c->counters + 4,
-                             c->fired, s);
-      skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s);
-      skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s);
-      skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s);
+                             c->fired, s, guard);
+      skv::launch_epoch_propagate(c->ix, c->fired, c->counters + 4, bound, s, guard);
+      skv::launch_epoch_roll(c->ix, c->touched[prev], c->counters + 1 + prev, c->pool_cap, 1, s, guard);
+      skv::launch_epoch_roll(c->ix, c->touched[cur], c->counters + 1 + cur, c->pool_cap, 0, s, guard);
       // swap windows: the current list becomes the previous one (its count stays where it
       // is); the pool and the new current list start empty (the fused pass resets them itself)
-      CK(cudaMemsetAsync(c->counters, 0, 4, s));
-      CK(cudaMemsetAsync(c->counters + 1 + prev, 0, 4, s));
+      skv::launch_epoch_reset(c->counters, c->counters + 1 + prev, guard, s);
     }
     CK(cudaMemcpyAsync(c->host_small + kEpochCountSlot, c->counters + 4, 4, cudaMemcpyDeviceToHost, s));
     // the first events ride along with their count (events are rare: one synchronisation)
@@ -2191,7 +2215,7 @@ void epoch_finish(skv_ctx* c, const EpochRun& run, skv_event* events, size_t cap
   c->cur = 1 - c->cur;
   c->wstart = c->rec_batch + 1;  // user-set stamps of the closed window become stale
   c->times.epoch_ms = elapsed(c->ev[8], c->ev[9]);
-  c->times.kernels_launched += run.split ? 6 : 1;
+  c->times.kernels_launched += run.split ? 7 : 1;
   std::sort(ev.begin(), ev.end(), [](const skv_event& x, const skv_event& y) {
     return x.h != y.h ? x.h < y.h : x.d < y.d;
   });

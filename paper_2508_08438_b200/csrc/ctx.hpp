@@ -337,7 +337,7 @@ void launch_block_prompts(const uint32_t* blk_off, uint32_t n_prompts, uint32_t*
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* uidx, uint32_t n_prompts, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, uint32_t* bprompt, int prechained, cudaStream_t s);
+                        const MonCtx& mon, uint32_t* bprompt, int prechained, uint32_t split_from, cudaStream_t s);
 void launch_chain(const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens, uint32_t n, uint64_t* h,
                   uint8_t* label, uint32_t* slot, cudaStream_t s);
 void launch_record(const Index& ix, const MonCtx& mon, const uint32_t* slot, const uint32_t* blk_off,
@@ -364,12 +364,12 @@ void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const
                     const uint32_t* first, const uint8_t* labels, uint32_t n, uint32_t* missing, cudaStream_t s);
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
                              int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
-                             uint32_t* n_cands, cudaStream_t s);
+                             uint32_t* n_cands, cudaStream_t s, const uint32_t* guard = nullptr);
 void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n_cands, uint32_t grid_n,
                        uint32_t stamp, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
-                       cudaStream_t s);
+                       cudaStream_t s, const uint32_t* guard = nullptr);
 void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
-                            cudaStream_t s);
+                            cudaStream_t s, const uint32_t* guard = nullptr);
 // the whole epoch pass (candidates, fire, propagate, rolls, window-swap resets) in one
 // cooperative launch
 // (st != nullptr: cur, stamp and epoch from the device step state st[2], st[3], st[4..5]; the lists
@@ -381,7 +381,8 @@ cudaError_t launch_epoch_fused(const Index& ix, uint32_t* const lists[2], uint32
                                void* events, uint32_t* n_events, uint32_t* fired, uint32_t* pool_count,
                                const uint32_t* st, const uint32_t* guard, int device, cudaStream_t s);
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
-                       cudaStream_t s);
+                       cudaStream_t s, const uint32_t* guard = nullptr);
+void launch_epoch_reset(uint32_t* pool_count, uint32_t* prev_count, const uint32_t* guard, cudaStream_t s);
 void launch_set_tiers(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
                       const uint8_t* tiers, uint32_t n,
                       cudaStream_t s);

@@ -1189,9 +1189,7 @@ constexpr int kCPPrompts = SKV_KCPPROMPTS;  // prompts per warp: 4096 warps for 
 #define SKV_KCPINFLIGHT 8
 #endif
 constexpr int kCPInFlight = SKV_KCPINFLIGHT;  // prompts whose probe loads are in flight together
-#ifndef SKV_KCP_HALVES_MIN_PROMPTS
-#define SKV_KCP_HALVES_MIN_PROMPTS 16384  // two probe waves per tile from this batch size on (measured:
-#endif                                    // config 2 probe 0.137 -> 0.111 ms; config 5 0.035 -> 0.040)
+
 constexpr int kPitch = 33;  // u64 per SMEM tile row (odd pitch: conflict-free transposes)
 
 struct Probe {
@@ -1280,7 +1278,7 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
     uint64_t* __restrict__ hk, uint8_t* __restrict__ label, uint8_t* __restrict__ decision,
     uint32_t* __restrict__ slot_out, uint32_t* __restrict__ matched, uint32_t* __restrict__ exist,
     uint8_t* __restrict__ tier, uint8_t* __restrict__ bmeta, MonCtx mon, uint32_t* __restrict__ bprompt,
-    uint32_t halves) {
+    uint32_t split_from) {
   __shared__ uint64_t s_d[kCPWarps][kCPPrompts][kPitch];
   __shared__ uint64_t s_h[kCPWarps][kCPPrompts][kPitch];
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -1337,12 +1335,14 @@ __global__ void __launch_bounds__(kCPWarps * 32, SKV_KCP_MINB) k_chain_probe(
       }
     }
     }  // !kPre
-    // large batches probe in two waves of 16 blocks (halves = 2): the second half of a tile is probed only
-    // for prompts whose first half found no miss, so a tile holding a prompt's first miss wastes at
-    // most 15 random probes past it instead of 31 (config 2: ~23 -> ~7 per prompt)
-    for (uint32_t half = 0; half < halves; ++half) {
-    const uint32_t lo_b = t0 + half * (32 / halves);
-    const bool in_half = halves == 1 || (lane >> 4) == half;
+    // tiles from split_from on are probed in two waves of 16 blocks: the second half only for prompts
+    // whose first half found no miss, so the tile holding a prompt's first miss wastes at most 15
+    // random probes past it instead of 31 (config 2: ~23 -> ~7 per prompt); the host picks split_from
+    // from the previous batch's match lengths (capi.cpp probe_split_from)
+    const uint32_t waves = t0 >= split_from ? 2u : 1u;
+    for (uint32_t half = 0; half < waves; ++half) {
+    const uint32_t lo_b = t0 + half * (32 / waves);
+    const bool in_half = waves == 1 || (lane >> 4) == half;
     uint32_t todo = __ballot_sync(kFull, has && k == n && n > lo_b);
     while (todo) {
       uint32_t js[kCPInFlight];
@@ -2000,7 +2000,9 @@ static_assert(sizeof(DevEvent) == sizeof(skv_event), "event layout");
 
 __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
                                    int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max,
-                                   uint32_t* __restrict__ cands, uint32_t* __restrict__ n_cands) {
+                                   uint32_t* __restrict__ cands, uint32_t* __restrict__ n_cands,
+                                   const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_list) return;
   uint32_t s = list[i];
@@ -2018,7 +2020,9 @@ __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, 
 
 __global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const uint32_t* __restrict__ n_cands,
                              uint32_t stamp, uint64_t epoch, DevEvent* __restrict__ events,
-                             uint32_t* __restrict__ n_events, uint32_t* __restrict__ fired) {
+                             uint32_t* __restrict__ n_events, uint32_t* __restrict__ fired,
+                             const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_cands) return;
   uint32_t s = cands[i];
@@ -2041,7 +2045,9 @@ __global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const
   fired[e] = s;
 }
 
-__global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, const uint32_t* __restrict__ n_fired) {
+__global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, const uint32_t* __restrict__ n_fired,
+                                  const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_fired) return;
   uint32_t root = fired[i];
@@ -2062,7 +2068,8 @@ __global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, 
 }
 
 __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
-                             int prev_list) {
+                             int prev_list, const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_list) return;
   uint32_t s = list[i];
@@ -2085,6 +2092,13 @@ __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const 
 //   candidates (current list, then the untouched previous-window entries) | fire (an
 //   ancestor marked this epoch suppresses, monitor.hpp:88-95) | propagate | roll previous |
 //   roll current; then the window swap's counter resets.
+// the split pass's window swap (its counter resets), skipped with the pass
+__global__ void k_epoch_reset(uint32_t* pool_count, uint32_t* prev_count, const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;
+  *pool_count = 0;
+  *prev_count = 0;
+}
+
 __device__ __forceinline__ void epoch_candidate(Index& ix, uint32_t s, bool only_untouched, uint32_t stamp,
                                                 double jump, uint64_t u_pre_max, uint32_t* cands,
                                                 uint32_t* n_cands) {
@@ -2462,7 +2476,8 @@ void launch_block_prompts(const uint32_t* blk_off, uint32_t n, uint32_t* map, cu
 void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_off, const uint32_t* first_sens,
                         const uint32_t* users, uint32_t n, uint64_t* h, uint8_t* label, uint8_t* decision,
                         uint32_t* slot, uint32_t* matched, uint32_t* exist, uint8_t* tier, uint8_t* bmeta,
-                        const MonCtx& mon, uint32_t* bprompt, int prechained, cudaStream_t s) {
+                        const MonCtx& mon, uint32_t* bprompt, int prechained, uint32_t split_from,
+                        cudaStream_t s) {
   auto* kern = prechained ? k_chain_probe<true> : k_chain_probe<false>;
   if (n)
     kern<<<static_cast<unsigned>(std::min<uint64_t>(cdiv(n, kCPPrompts * kCPWarps),
@@ -2470,7 +2485,7 @@ void launch_chain_probe(const Index& ix, const uint64_t* d, const uint32_t* blk_
                                                                                  : ~0ull)),
                     kCPWarps * 32, 0, s>>>(ix, d, blk_off, first_sens, users, n, h, label,
                                                                    decision, slot, matched, exist, tier, bmeta, mon,
-                                                                   bprompt, n >= SKV_KCP_HALVES_MIN_PROMPTS ? 2u : 1u);
+                                                                   bprompt, split_from);
 }
 
 uint32_t record_grid(int device) {
@@ -2912,23 +2927,23 @@ ix, h, d, blk_off, exist, label, users, owners, n,
 
 void launch_epoch_candidates(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n,
                              int only_untouched, uint32_t stamp, double jump, uint64_t u_pre_max, uint32_t* cands,
-                             uint32_t* n_cands, cudaStream_t s) {
+                             uint32_t* n_cands, cudaStream_t s, const uint32_t* guard) {
   if (grid_n)
     k_epoch_candidates<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, only_untouched, stamp, jump, u_pre_max,
-                                                          cands, n_cands);
+                                                          cands, n_cands, guard);
 }
 
 void launch_epoch_fire(const Index& ix, const uint32_t* cands, const uint32_t* n_cands, uint32_t grid_n,
                        uint32_t stamp, uint64_t epoch, void* events, uint32_t* n_events, uint32_t* fired,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint32_t* guard) {
   if (grid_n)
     k_epoch_fire<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, cands, n_cands, stamp, epoch, static_cast<DevEvent*>(events),
-                                                    n_events, fired);
+                                                    n_events, fired, guard);
 }
 
 void launch_epoch_propagate(const Index& ix, const uint32_t* fired, const uint32_t* n_events, uint32_t grid_n,
-                            cudaStream_t s) {
-  if (grid_n) k_epoch_propagate<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, fired, n_events);
+                            cudaStream_t s, const uint32_t* guard) {
+  if (grid_n) k_epoch_propagate<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, fired, n_events, guard);
 }
 
 int epoch_fused_grid(int device) {
@@ -2939,7 +2954,7 @@ int epoch_fused_grid(int device) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_epoch_fused, 256, 0) != cudaSuccess ||
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
       return 0;
-    grid[device] = std::max(1, std::min(per_sm, 2) * n_sm);
+    grid[device] = std::max(1, per_sm * n_sm);  // every co-resident CTA: the phases are latency-bound
   }
   return grid[device];
 }
@@ -2960,8 +2975,12 @@ cudaError_t launch_epoch_fused(const Index& ix, uint32_t* const lists[2], uint32
 }
 
 void launch_epoch_roll(const Index& ix, const uint32_t* list, const uint32_t* n_list, uint32_t grid_n, int prev_list,
-                       cudaStream_t s) {
-  if (grid_n) k_epoch_roll<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, prev_list);
+                       cudaStream_t s, const uint32_t* guard) {
+  if (grid_n) k_epoch_roll<<<cdiv(grid_n, 256), 256, 0, s>>>(ix, list, n_list, prev_list, guard);
+}
+
+void launch_epoch_reset(uint32_t* pool_count, uint32_t* prev_count, const uint32_t* guard, cudaStream_t s) {
+  k_epoch_reset<<<1, 1, 0, s>>>(pool_count, prev_count, guard);
 }
 
 void launch_resolve(const Index& ix, const uint64_t* h, const uint64_t* d, const uint32_t* boff, uint32_t n_prompts,
