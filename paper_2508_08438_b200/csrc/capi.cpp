@@ -600,6 +600,7 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
   // SMs: the one-CTA-per-SM kernel would otherwise hold every SM until it ends and serialise the
   // commit behind it (measured: 1.13 ms per config-2 step at full grid, 0.97 at a quarter)
   static const int pf_frac = getenv("SKV_H16_PF_FRAC") ? atoi(getenv("SKV_H16_PF_FRAC")) : 4;
+  static const int pf_warps = getenv("SKV_H16_PF_WARPS") ? atoi(getenv("SKV_H16_PF_WARPS")) : 8;
   const uint64_t NB = std::max<uint64_t>(c->max_blocks, 1);
   if (c->mask_words > 1) {  // words >= 1 are only OR-ed into by their groups
     const uint64_t nb = std::min<uint64_t>(NB, std::max<uint64_t>(nb_hint, n_tokens / c->cfg.block_tokens));
@@ -642,8 +643,16 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
         warps = static_cast<int>(std::clamp<uint64_t>((chunks + R.grid - 1) / R.grid, 4, 32));
         grid = std::min<uint64_t>(R.grid, (chunks + warps - 1) / warps);
       }
-      // a prefetch (beside the previous batch's commit) keeps to a quarter of the SMs
-      if (overlapped && pf_frac > 1) grid = std::min<uint64_t>(grid, std::max<uint64_t>(1, R.grid / pf_frac));
+      uint32_t smem = R.smem;
+      if (overlapped && pf_warps > 0 && warps == 32) {
+        // a prefetch beside the previous batch's commit: one small CTA on every SM, which fits next
+        // to the commit's CTAs (registers / SMEM) and uses the issue slots its memory stalls leave
+        warps = pf_warps;
+        smem = skv::hash_scan16_smem(R.img_bytes, R.q_cap, static_cast<uint32_t>(pf_warps));
+      } else if (overlapped && pf_frac > 1) {
+        // ... or (SKV_H16_PF_WARPS=0) a quarter of the SMs with full CTAs
+        grid = std::min<uint64_t>(grid, std::max<uint64_t>(1, R.grid / pf_frac));
+      }
       // short prompts (< ~34 blocks): the chunk geometry comes from a block -> prompt map
       if (N && nb_est / N < 34) {
         uint32_t*& map = overlapped ? c->alt_hs_map : c->hs_map;
@@ -651,7 +660,7 @@ void stage12(skv_ctx* c, cudaStream_t st, const uint32_t* tokens, const uint64_t
         skv::launch_block_prompts(blk_off, N, map, st);
         h.bmap = map;
       }
-      skv::launch_hash_scan16(h, static_cast<int>(grid), R.smem, st, warps);
+      skv::launch_hash_scan16(h, static_cast<int>(grid), smem, st, warps);
       continue;
     }
     skv::HashScanArgs a;

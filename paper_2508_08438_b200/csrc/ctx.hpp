@@ -323,7 +323,7 @@ HSLayout hash_scan_layout(const DevRules& r, uint32_t B, uint32_t W);
 void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t threads, cudaStream_t s);
 // k_hash_scan16: fixed task-queue / slot layout; returns the dynamic SMEM bytes for an image and
 // queue capacity, and the persistent grid (-1 on failure)
-uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap);
+uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap, uint32_t warps = 0);
 int hash_scan16_grid(int device, uint32_t smem);
 void launch_hash_scan16(const HS16Args& a, int grid, uint32_t smem, cudaStream_t s, int warps = 0);
 // diagnostic: per entry matched by the last admitted batch, its accesses, distinct users and the

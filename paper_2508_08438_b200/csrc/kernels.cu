@@ -2440,9 +2440,10 @@ void launch_hash_scan(const HashScanArgs& a, int grid, uint32_t smem, uint32_t t
   k_hash_scan<<<g, threads, smem, s>>>(a);
 }
 
-uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap) {
-  return round16(img_bytes) + 4 * kH16Warps * static_cast<uint32_t>(sizeof(Slot16)) +
-         kH16Warps * q_cap * static_cast<uint32_t>(sizeof(H16Task));
+uint32_t hash_scan16_smem(uint32_t img_bytes, uint32_t q_cap, uint32_t warps) {
+  const uint32_t w = warps ? warps : kH16Warps;
+  return round16(img_bytes) + 4 * w * static_cast<uint32_t>(sizeof(Slot16)) +
+         w * q_cap * static_cast<uint32_t>(sizeof(H16Task));
 }
 
 int hash_scan16_grid(int device, uint32_t smem) {
