@@ -330,9 +330,12 @@ struct skv_ctx {
   // state dstate = {batch, wstart, cur, stamp, epoch lo, epoch hi}, copied from pinned host
   // memory before each launch (one slot per phase).  A small batch's step is otherwise bound by
   // host issue: ~40 API calls for ~80 us of kernels (config 1).
-  struct GraphCache {
-    cudaGraphExec_t exec = nullptr;
-    std::vector<uintptr_t> key;
+  struct GraphCache {  // the last few instantiated graphs of a phase, by key (most recent first)
+    struct Item {
+      cudaGraphExec_t exec = nullptr;
+      std::vector<uintptr_t> key;
+    };
+    std::vector<Item> items;
   };
   GraphCache g_admit, g_commit, g_epoch;
   bool graphs = true;
@@ -755,8 +758,10 @@ void put_state(skv_ctx* c, int slot, uint32_t batch, uint64_t epoch, bool armed 
 // buffers and shapes the launches bake in) changed.
 template <typename F>
 void run_graph(skv_ctx* c, skv_ctx::GraphCache& g, const std::vector<uintptr_t>& key, F&& issue) {
+  constexpr size_t kKeep = 4;  // e.g. alternating batch shapes / buffers replay without re-capture
   cudaStream_t s = c->stream;
-  if (!g.exec || g.key != key) {
+  auto hit = std::find_if(g.items.begin(), g.items.end(), [&](const auto& it) { return it.key == key; });
+  if (hit == g.items.end()) {
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     c->capturing = true;
@@ -771,24 +776,21 @@ void run_graph(skv_ctx* c, skv_ctx::GraphCache& g, const std::vector<uintptr_t>&
     }
     c->capturing = false;
     CK(cudaStreamEndCapture(s, &graph));
-    if (g.exec) {
-      cudaGraphExecUpdateResultInfo info;
-      if (cudaGraphExecUpdate(g.exec, graph, &info) != cudaSuccess) {
-        cudaGetLastError();
-        cudaGraphExecDestroy(g.exec);
-        g.exec = nullptr;
-      }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    if (g.items.size() == kKeep) {
+      cudaGraphExecDestroy(g.items.back().exec);
+      g.items.pop_back();
     }
-    if (!g.exec) {
-      const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
-      cudaGraphDestroy(graph);
-      CK(e);
-    } else {
-      cudaGraphDestroy(graph);
-    }
-    g.key = key;
+    g.items.insert(g.items.begin(), skv_ctx::GraphCache::Item{exec, key});
+    hit = g.items.begin();
+  } else if (hit != g.items.begin()) {
+    std::rotate(g.items.begin(), hit, hit + 1);
+    hit = g.items.begin();
   }
-  CK(cudaGraphLaunch(g.exec, s));
+  CK(cudaGraphLaunch(hit->exec, s));
 }
 
 void check_usable(const skv_ctx* c) {
@@ -1128,7 +1130,8 @@ int skv_destroy(skv_ctx* c) {
   if (c->host_events) cudaFreeHost(c->host_events);
   if (c->hstate) cudaFreeHost(c->hstate);
   for (auto* g : {&c->g_admit, &c->g_commit, &c->g_epoch})
-    if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (auto& it : g->items)
+      if (it.exec) cudaGraphExecDestroy(it.exec);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->side) {
