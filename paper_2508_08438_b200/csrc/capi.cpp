@@ -2271,7 +2271,15 @@ int skv_step(skv_ctx* c, const skv_batch* b, skv_admit_out* out, const skv_batch
   int rc = skv_admit(c, b, out);
   c->lazy_outputs = false;
   if (rc != SKV_OK) return rc;
-  if (prefetch_next && (rc = skv_prefetch(c, prefetch_next)) != SKV_OK) return rc;
+  if (prefetch_next && (rc = skv_prefetch(c, prefetch_next)) != SKV_OK) {
+    // the admitted batch stays pending: its outputs land now, not at a later commit (the caller
+    // may drop `out` after this error)
+    guard(c, [&] {
+      ensure_admit_resolved(c);
+      return SKV_OK;
+    });
+    return rc;
+  }
   if (!fused || c->p_n == 0) {
     if ((rc = skv_commit(c, new_entries)) != SKV_OK) return rc;
     if (stage_after && (rc = skv_stage(c, stage_after)) != SKV_OK) return rc;
