@@ -824,8 +824,8 @@ __device__ __forceinline__ MonCtx mon_live(MonCtx M) {
     const uint32_t cur = M.st[2];
     M.batch = M.st[0];
     M.wstart = M.st[1];
-    M.touched = M.tl[cur];
-    M.n_touched = M.ntb + cur;
+    M.touched = cur ? M.tl[1] : M.tl[0];  // a select, not a dynamic index (that would put M in local memory)
+    M.n_touched = M.ntb + (cur ? 1 : 0);
   }
   return M;
 }
@@ -1474,7 +1474,8 @@ __device__ __forceinline__ void cas128_empty_x4(const uint64_t* sl, const bool* 
 constexpr int kCommitRounds = SKV_COMMIT_ROUNDS;
 
 #ifndef SKV_COMMIT_MINB
-#define SKV_COMMIT_MINB 1
+#define SKV_COMMIT_MINB 3  // 74 registers (profiles/r02_z_*: config 2 0.963 -> 0.946 ms per step; 4 / 64 registers 0.939 but
+                           // the system-prompt workload 1.27 -> 1.59 ms, its prefetch no longer fits beside the commit)
 #endif
 #ifndef SKV_COMMIT_PERSIST
 #define SKV_COMMIT_PERSIST 8  // CTAs per SM; each warp then strides over ~7 prompts (0.72 -> 0.60 ms, run 103)
