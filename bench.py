@@ -436,9 +436,16 @@ def run_ours(args):
         eng.epoch_pass()
         return eng
 
+    # batch descriptors (the pointers of each pre-generated batch) built once, as a serving loop
+    # builds one per staging buffer
+    desc = {}
+
     def dev_batch(k):
-        t, o, u, w = devb[k]
-        return N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, ntok[k], 1)
+        key = ("dev", k)
+        if key not in desc:
+            t, o, u, w = devb[k]
+            desc[key] = N.Batch(t.data_ptr(), o.data_ptr(), u.data_ptr(), w.data_ptr(), n_local, ntok[k], 1)
+        return desc[key]
 
     # e2e inputs: the prompts' byte tokens (the reference's ByteVocabulary, core.hpp:92-101 -- every
     # workload token is a byte) in pinned host memory, a quarter of the TokenId copy; widened on
@@ -452,12 +459,16 @@ def run_ours(args):
             host8.append(t8)
 
     def host_batch(k):
-        _, tok, off, users, owners, _ = host[k]
-        if byte_tokens:
-            return N.Batch(None, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local, ntok[k], 0,
-                           host8[k].data_ptr())
-        return N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local,
-                       ntok[k], 0)
+        key = ("host", k)
+        if key not in desc:
+            _, tok, off, users, owners, _ = host[k]
+            if byte_tokens:
+                desc[key] = N.Batch(None, off.ctypes.data, users.ctypes.data, owners.ctypes.data, n_local, ntok[k], 0,
+                                    host8[k].data_ptr())
+            else:
+                desc[key] = N.Batch(tok.ctypes.data, off.ctypes.data, users.ctypes.data, owners.ctypes.data,
+                                    n_local, ntok[k], 0)
+        return desc[key]
 
     # one step = admit(k) [+ stage batch k+1's stages 1-2 (and, e2e, its H2D) on the side
     # stream, overlapping] + commit(k) + epoch; nxt is None at the edge of a timed region
@@ -485,9 +496,8 @@ def run_ours(args):
     # e2e step: the PCIe copy of the inputs is the bottleneck, so batch k+3's copy is queued
     # (skv_stage) as soon as batch k's commit frees its staging slot, and runs while batch k+1
     # is admitted; batch k+1's stages 1-2 are prefetched from its staged copy
-    def step_host(eng, k, nxt):
-        o = N.AdmitOut(None, None, out_label.data_ptr(), None, out_dec.data_ptr(), out_match.data_ptr(),
-                       out_tier.data_ptr(), None, 0, 0, 0)
+    def step_host(eng, k, nxt):  # (step_host.out: the fixed output descriptor, built below)
+        o = step_host.out
         if fused_step:  # skv_step: admit(k) + prefetch(k+1) + commit + stage(k+3) + epoch in one call
             stg = host_batch(nxt + 2) if nxt is not None and nxt + 2 < step_host.limit else None
             eng.step_raw(host_batch(k), out=o, next_batch=host_batch(nxt) if nxt is not None else None, stage=stg)
@@ -501,6 +511,9 @@ def run_ours(args):
         if replica:
             replica["g"].sync(batch_gids[k])
         eng.epoch_pass()
+
+    step_host.out = N.AdmitOut(None, None, out_label.data_ptr(), None, out_dec.data_ptr(), out_match.data_ptr(),
+                               out_tier.data_ptr(), None, 0, 0, 0)
 
     def barrier():
         if world > 1:

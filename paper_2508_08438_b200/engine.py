@@ -326,10 +326,14 @@ class AdmissionEngine:
         buf = getattr(self, "_evbuf", None)
         if buf is None or len(buf) < cap:
             buf = self._evbuf = (N.Event * cap)()
-        n, ep, nn = C.c_size_t(), C.c_uint64(), C.c_uint64()
-        ref = lambda x: C.byref(x) if x is not None else None  # noqa: E731
-        self._check(self._lib.skv_step(self._h, C.byref(batch), ref(out), ref(next_batch), ref(stage), C.byref(nn), buf,
-                                       cap, C.byref(n), C.byref(ep)))
+        sc = getattr(self, "_step_scalars", None)
+        if sc is None:  # per-engine result scalars (a serving loop calls this once per batch)
+            sc = self._step_scalars = (C.c_size_t(), C.c_uint64(), C.c_uint64())
+        n, ep, nn = sc
+        self._check(self._lib.skv_step(self._h, C.byref(batch), None if out is None else C.byref(out),
+                                       None if next_batch is None else C.byref(next_batch),
+                                       None if stage is None else C.byref(stage), C.byref(nn), buf, cap, C.byref(n),
+                                       C.byref(ep)))
         if n.value > cap:
             buf = self._evbuf = (N.Event * n.value)()
             self._check(self._lib.skv_last_events(self._h, buf, n.value, C.byref(n)))
