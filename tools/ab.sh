@@ -4,6 +4,7 @@
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
+# variants/ is gpurun-ignored: run A/B variants by removing that line from .gpurunignore for the call
 cp paper_2508_08438_b200/libsafekv_b200.so /tmp/libsafekv_b200.so.orig
 for spec in "$@"; do
   v="${spec%%:*}"; flags=""; [ "$spec" != "$v" ] && flags="${spec#*:}"
