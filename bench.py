@@ -411,6 +411,10 @@ def run_ours(args):
     # commit and the epoch, so it keeps the separate calls
     fused_step = bool(args.fused_step) and not rep_depth
     pipeline = not args.no_pipeline
+    comm_backend = "single process"
+    if world > 1:
+        import torch.distributed as dist
+        comm_backend = dist.get_backend().upper()  # NCCL with a GPU per rank; gloo when ranks share one
     replica = {}
 
     def fresh_engine():
@@ -667,7 +671,7 @@ def run_ours(args):
                    "step": "admit + commit + epoch",
                    "index": f"{cap} slots x 64 B ({cap * 64 / 2**30:.0f} GiB), load {need / cap:.2f} at run end",
                    "parallelism": ((f"x{world} ranks: depth < {rep_depth} replicated on every rank (new entries + "
-                                    f"window statistics merged per step over {'NCCL' if world > 1 else ''} all-gather), "
+                                    f"window statistics merged per step over {comm_backend} all-gather), "
                                     f"prompts routed by block {rep_depth}" if rep_depth else
                                     f"prefix-forest partitioned x{world} (skv_route; no data-path collective)")
                                    if world > 1 else "single GPU"),
