@@ -2007,9 +2007,12 @@ __global__ void k_epoch_candidates(Index ix, const uint32_t* __restrict__ list, 
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_list) return;
   uint32_t s = list[i];
-  if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
-  if (!meta_live(ix.e[s].rec.meta) || meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
-  Stats st = ix.e[s].stats;
+  // the entry's label and its monitor sector in ONE round trip (independent loads before any test)
+  const uint32_t meta = ix.e[s].rec.meta;
+  const Stats st = ix.e[s].stats;
+  const uint32_t set_idx = ix.e[s].aux.set_idx;
+  if (only_untouched && set_idx != kNone) return;
+  if (!meta_live(meta) || meta_label(meta) != SKV_LABEL_PUBLIC) return;
   if (st.hit_pre == 0) return;
   double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
   double prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
@@ -2103,9 +2106,11 @@ __global__ void k_epoch_reset(uint32_t* pool_count, uint32_t* prev_count, const 
 __device__ __forceinline__ void epoch_candidate(Index& ix, uint32_t s, bool only_untouched, uint32_t stamp,
                                                 double jump, uint64_t u_pre_max, uint32_t* cands,
                                                 uint32_t* n_cands) {
-  if (only_untouched && ix.e[s].aux.set_idx != kNone) return;
-  if (!meta_live(ix.e[s].rec.meta) || meta_label(ix.e[s].rec.meta) != SKV_LABEL_PUBLIC) return;
-  Stats st = ix.e[s].stats;
+  const uint32_t meta = ix.e[s].rec.meta;  // one round trip: every load before any test
+  const Stats st = ix.e[s].stats;
+  const uint32_t set_idx = ix.e[s].aux.set_idx;
+  if (only_untouched && set_idx != kNone) return;
+  if (!meta_live(meta) || meta_label(meta) != SKV_LABEL_PUBLIC) return;
   if (st.hit_pre == 0) return;
   double now = st.hit_cur ? static_cast<double>(st.u_cnt) / static_cast<double>(st.hit_cur) : 0.0;
   double prev = static_cast<double>(st.u_pre) / static_cast<double>(st.hit_pre);
