@@ -12,9 +12,10 @@ L2 flush is needed between steps).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  For N > 1 (torchrun) every rank admits its own shard
-of the prompt stream against its own index replica (weak scaling; see DESIGN.md
-"Multi-GPU" -- the replica merge is not part of this round's timed step).
+Prints ONE JSON line (rank 0).  For N > 1 (torchrun) every rank admits a full batch of the
+prompts routed to it (weak scaling): prefix-forest partitioning for
+configs 2-5 (no data-path collective), and for --workload 6 the replicated layer, whose
+per-step NCCL merge is inside the timed step.
 """
 from __future__ import annotations
 

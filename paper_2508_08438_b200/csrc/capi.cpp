@@ -2119,7 +2119,7 @@ int skv_commit(skv_ctx* c, uint64_t* new_entries) {
       return SKV_OK;
     }
     if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
-      throw CapacityError("index capacity exhausted (eviction is not part of this path)");
+      throw CapacityError("index capacity exhausted (enable eviction: skv_enable_eviction / skv_set_tier_budget)");
     if (c->budget_on) {
       CK(cudaEventRecord(c->ev[5], s));
       const uint64_t before = c->entries + c->tombstones;
@@ -2287,7 +2287,7 @@ int skv_step(skv_ctx* c, const skv_batch* b, skv_admit_out* out, const skv_batch
   }
   return guard(c, [&]() -> int {
     if (c->entries + c->tombstones + c->p_blocks > c->ix.cap - c->ix.cap / 8)
-      throw CapacityError("index capacity exhausted (eviction is not part of this path)");
+      throw CapacityError("index capacity exhausted (enable eviction: skv_enable_eviction / skv_set_tier_budget)");
     const CommitRun crun = commit_enqueue(c);
     const EpochRun erun = epoch_enqueue(c, true);
     sync_check(c->stream);
