@@ -2049,18 +2049,45 @@ __global__ void k_epoch_fire(Index ix, const uint32_t* __restrict__ cands, const
   fired[e] = s;
 }
 
-__global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, const uint32_t* __restrict__ n_fired,
-                                  const uint32_t* __restrict__ guard) {
-  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= *n_fired) return;
-  uint32_t root = fired[i];
-  const uint32_t lab = meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
+// Relabel a fired entry's whole subtree (monitor.hpp:88-95 -> apply_label_subtree): a DFS whose
+// per-node loads (label, first child, next sibling) are issued together -- one dependent round trip
+// per node -- with the pending siblings on a per-thread stack instead of climbing parent links back
+// up (a 256-deep chain of config 4 cost ~3 round trips per node).  A stack overflow (deeper branching
+// than kRelabelStack levels) falls back to the parent-climbing walk, which relabels everything again
+// (idempotent).
+#ifndef SKV_RELABEL_STACK
+#define SKV_RELABEL_STACK 64
+#endif
+constexpr int kRelabelStack = SKV_RELABEL_STACK;
+__device__ void relabel_subtree(const Index& ix, uint32_t root, uint32_t lab) {
   ix.e[root].rec.meta = (ix.e[root].rec.meta & ~3u) | lab;
+  uint32_t stack[kRelabelStack];
+  int sp = 0;
+  bool overflow = false;
   uint32_t cur = ix.e[root].rec.first_child;
+  for (;;) {
+    if (cur == kNone) {
+      if (sp == 0) break;
+      cur = stack[--sp];
+      continue;
+    }
+    const uint32_t m = ix.e[cur].rec.meta, fc = ix.e[cur].rec.first_child, ns = ix.e[cur].aux.next_sibling;
+    ix.e[cur].rec.meta = (m & ~3u) | lab;
+    if (ns != kNone) {
+      if (sp < kRelabelStack) {
+        stack[sp++] = ns;
+      } else {
+        overflow = true;
+        break;
+      }
+    }
+    cur = fc;
+  }
+  if (!overflow) return;
+  cur = ix.e[root].rec.first_child;
   while (cur != kNone) {
     ix.e[cur].rec.meta = (ix.e[cur].rec.meta & ~3u) | lab;
-    uint32_t c = ix.e[cur].rec.first_child;
+    const uint32_t c = ix.e[cur].rec.first_child;
     if (c != kNone) {
       cur = c;
       continue;
@@ -2069,6 +2096,15 @@ __global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, 
     if (cur == root) break;
     cur = ix.e[cur].aux.next_sibling;
   }
+}
+
+__global__ void k_epoch_propagate(Index ix, const uint32_t* __restrict__ fired, const uint32_t* __restrict__ n_fired,
+                                  const uint32_t* __restrict__ guard) {
+  if (guard && (guard[5] | guard[8])) return;  // a speculative pass behind a failed / replaying commit
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_fired) return;
+  const uint32_t root = fired[i];
+  relabel_subtree(ix, root, meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED);
 }
 
 __global__ void k_epoch_roll(Index ix, const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
@@ -2170,20 +2206,7 @@ __global__ void __launch_bounds__(256) k_epoch_fused(Index ix, uint32_t* l0, uin
   const uint32_t nf = *n_events;
   for (uint32_t i = t0; i < nf; i += T) {
     const uint32_t root = fired[i];
-    const uint32_t lab = meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED;
-    ix.e[root].rec.meta = (ix.e[root].rec.meta & ~3u) | lab;
-    uint32_t cur = ix.e[root].rec.first_child;
-    while (cur != kNone) {
-      ix.e[cur].rec.meta = (ix.e[cur].rec.meta & ~3u) | lab;
-      const uint32_t c = ix.e[cur].rec.first_child;
-      if (c != kNone) {
-        cur = c;
-        continue;
-      }
-      while (cur != root && ix.e[cur].aux.next_sibling == kNone) cur = ix.e[cur].rec.parent;
-      if (cur == root) break;
-      cur = ix.e[cur].aux.next_sibling;
-    }
+    relabel_subtree(ix, root, meta_owner(ix.e[root].rec.meta) == 0 ? SKV_LABEL_PRIVATE : SKV_LABEL_RESTRICTED);
   }
   for (uint32_t i = t0; i < np; i += T) {  // the previous window's untouched entries roll to zero
     const uint32_t s = prev_list[i];
