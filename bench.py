@@ -362,6 +362,13 @@ def run_ours(args):
                    int(np.ceil(np.log2(need * 1.7))))
     if args.index_log2:
         cap = 1 << args.index_log2
+    # every step admits a distinct pre-generated batch held in HBM: refuse a run whose batches and
+    # index (at load <= 0.6) cannot share the device, instead of failing in an allocation
+    total = torch.cuda.get_device_properties(gpu).total_memory // ranks_per_dev
+    batch_bytes = n_batches * n_local * L * 4
+    if 64 * cap + batch_bytes > 0.9 * total:
+        raise SystemExit(f"bench: {n_batches} distinct batches ({batch_bytes / 2**30:.0f} GiB) and a {cap}-slot index "
+                         f"({64 * cap / 2**30:.0f} GiB) exceed this device's memory; use fewer --steps / --warmup")
     ecfg = EngineConfig(block_tokens=B, window_tokens=c["window_tokens"], index_capacity=cap,
                         max_prompts=n_local, max_tokens=n_local * L,
                         max_window_entries=1 << (20 if args.workload == 4 else 18),  # entries touched per window
